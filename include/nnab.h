@@ -1,0 +1,120 @@
+/*
+ * nnab -- B200 (sm_100a) spectrogram kernels behind a plain C ABI.
+ *
+ * This is the drop-in boundary for the `spectro` reference's hot path
+ * (/root/reference/pkg/src/spectro).  The reference is pure Python/NumPy, so
+ * its "FFI" is the call a Python caller makes; every entry point below names
+ * the reference function it replaces (file:line, relative to
+ * pkg/src/spectro/).  The Python host mirror in paper_1912_12055_b200/ binds
+ * these symbols with ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - All float pointers are DEVICE pointers (caller-allocated) unless a
+ *    function says otherwise; execution is stream-ordered on `stream`
+ *    (a cudaStream_t passed as void*).  No call allocates device memory:
+ *    scratch comes from a caller-supplied workspace sized by the matching
+ *    *_workspace_bytes() query.
+ *  - Calls are re-entrant and hold no global mutable state.
+ *  - Return value: NNAB_OK or an NNAB_E* code; nnab_strerror() names it.
+ *    NNAB_EINVAL mirrors the reference's ValueError cases (reflect pad >=
+ *    signal length signal.py:147-150, kernel longer than padded signal
+ *    signal.py:176-177, hop < 1 signal.py:178-179, CQT hop divisibility
+ *    transforms.py:253-257).
+ *  - Signals are float32 (B, L) row-major; spectrogram outputs are
+ *    (B, F, T) row-major float32 (complex outputs: interleaved (re, im)
+ *    float pairs, i.e. complex64), matching nnAudio's (batch, freq, time).
+ */
+#ifndef NNAB_H
+#define NNAB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NNAB_OK 0
+#define NNAB_EINVAL 1   /* bad argument (reference raises ValueError) */
+#define NNAB_ECUDA 2    /* CUDA runtime / driver error */
+#define NNAB_ENOTSUP 3  /* configuration not supported by the sm_100a kernels */
+#define NNAB_ENODEV 4   /* no sm_100 device */
+
+#define NNAB_PAD_REFLECT 0 /* np.pad(..., "reflect"): mirror without the edge sample */
+#define NNAB_PAD_ZERO 1    /* "constant_zero" */
+
+#define NNAB_OUT_MAGNITUDE 0 /* hypot(re, im)            transforms.py:86-93 */
+#define NNAB_OUT_POWER 1     /* re^2 + im^2                                 */
+#define NNAB_OUT_COMPLEX 2   /* re - i*im (interleaved complex64)            */
+#define NNAB_OUT_MEL 3       /* W @ |X|^power            transforms.py:164-172 */
+#define NNAB_OUT_SMOOTH_MAG 4 /* sqrt(re^2+im^2+eps)      gradients.py:61-67 */
+
+#define NNAB_PREC_TF32 0  /* one TF32 tcgen05 pass (peak-normalised error <= 1e-3) */
+#define NNAB_PREC_3XTF32 1 /* hi/lo split, 3 passes (<= 1e-5, FP32-equivalent) */
+
+/* A strided-correlation ("conv1d with a kernel bank") problem:
+ * out[r, t] = sum_m padded[t*hop + m] * bank[r, m]   (signal.py:159-183)  */
+typedef struct nnab_frames {
+  int64_t batch;    /* B clips */
+  int64_t length;   /* L samples per clip */
+  int32_t width;    /* kernel width M (n_fft, or the CQT bank width) */
+  int32_t hop;      /* stride between frames */
+  int32_t pad;      /* samples padded on each side (n_fft//2 when centred) */
+  int32_t pad_mode; /* NNAB_PAD_* */
+} nnab_frames;
+
+/* ---------------------------------------------------------------- misc */
+int nnab_version(void);
+const char* nnab_strerror(int code);
+/* last CUDA error string recorded by a failing call on this thread */
+const char* nnab_last_error(void);
+/* number of frames T and the staging layout for a problem; NNAB_EINVAL for
+ * the reference's ValueError cases. */
+int nnab_frames_geometry(const nnab_frames* f, int32_t* n_frames, int32_t* row_len, int32_t* rows_per_clip);
+
+/* --------------------------------------------------- bank preparation
+ * Pack a DFT bank (h_re, h_im: (n_bins, n_fft) float32 device rows,
+ * kernels.py:137-146) into the GEMM operand layout: tiles of 256 rows
+ * (128 cos rows, 128 sin rows), K padded to a multiple of 32, TF32-rounded.
+ * With 3xTF32 a second (lo) array receives the rounding residual.
+ * fold_nyquist: bins 0 and n_bins-1 have all-zero sine rows (the default
+ * integer-bin bank), so bin n_bins-1's cosine row takes the sine slot of bin 0
+ * and the bank tiles exactly (1025 bins -> 8 tiles).                    */
+int nnab_dft_bank_tiles(int32_t n_bins, int32_t fold_nyquist);
+size_t nnab_dft_bank_bytes(int32_t n_bins, int32_t n_fft, int32_t fold_nyquist);
+int nnab_pack_dft_bank(const float* h_re, const float* h_im, int32_t n_bins, int32_t n_fft,
+                       int32_t fold_nyquist, int32_t precision, float* packed_hi, float* packed_lo,
+                       void* stream);
+
+/* ------------------------------------------------------- STFT / Mel
+ * Stft.__call__ (transforms.py:130-144), MelSpec.__call__ (transforms.py:164-172),
+ * TrainableLayer.spectrogram for DFT banks (gradients.py:61-67, out_kind
+ * NNAB_OUT_SMOOTH_MAG with eps).
+ *  x          (B, L) float32
+ *  packed_*   from nnab_pack_dft_bank (lo only for 3xTF32, else may be NULL)
+ *  mel_w      (n_mels, mel_ld) float32, zero-padded rows (NNAB_OUT_MEL only)
+ *  mel_band   optional int32 pairs [lo, hi) of mel rows touching each 32-bin
+ *             chunk (NULL = dense W)
+ *  out        (B, n_bins, T) float32 | (B, n_bins, T, 2) | (B, n_mels, T)   */
+size_t nnab_stft_workspace_bytes(const nnab_frames* f, int32_t precision);
+int nnab_stft_forward(const nnab_frames* f, const float* x, const float* packed_hi, const float* packed_lo,
+                      int32_t n_bins, int32_t fold_nyquist, int32_t precision, int32_t out_kind, float power,
+                      float eps, const float* mel_w, int32_t n_mels, int32_t mel_ld, const int32_t* mel_band,
+                      float* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Host-buffer end-to-end variant (the call a CPU caller of the reference
+ * makes): x_host and out_host are pinned host buffers; the batch is streamed
+ * through the device in chunks so H2D, compute and D2H overlap.  All device
+ * buffers (x chunk, workspace, out chunk) come from `device_scratch`. */
+size_t nnab_stft_host_scratch_bytes(const nnab_frames* f, int32_t precision, int32_t out_rows,
+                                    int64_t chunk_clips);
+int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const float* packed_hi,
+                           const float* packed_lo, int32_t n_bins, int32_t fold_nyquist, int32_t precision,
+                           int32_t out_kind, float power, float eps, const float* mel_w, int32_t n_mels,
+                           int32_t mel_ld, const int32_t* mel_band, float* out_host, int64_t chunk_clips,
+                           void* device_scratch, size_t scratch_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNAB_H */

@@ -1,0 +1,255 @@
+// extern "C" boundary of libnnab plus host-side helpers (tensor maps, errors).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+
+namespace nnab {
+
+static thread_local char g_last_error[256] = "";
+
+int cuda_fail(cudaError_t e, const char* where) {
+  std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
+  return NNAB_ECUDA;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                 uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+  auto enc = get_encode();
+  if (!enc) {
+    std::snprintf(g_last_error, sizeof(g_last_error), "cuTensorMapEncodeTiled unavailable");
+    return NNAB_ECUDA;
+  }
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0 || row_bytes % 16 != 0) return NNAB_EINVAL;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    std::snprintf(g_last_error, sizeof(g_last_error), "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return NNAB_ECUDA;
+  }
+  return NNAB_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static size_t stage_bytes(const FrameGeom& g) { return align256((size_t)g.B * g.R * g.row_len * sizeof(float)); }
+
+static int check_device() {
+  static int ok = -1;
+  if (ok < 0) {
+    int dev = 0, major = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+      ok = 0;
+    else
+      ok = major == 10;
+  }
+  return ok ? NNAB_OK : NNAB_ENODEV;
+}
+
+}  // namespace nnab
+
+using namespace nnab;
+
+extern "C" int nnab_version(void) { return 1; }
+
+extern "C" const char* nnab_strerror(int code) {
+  switch (code) {
+    case NNAB_OK: return "ok";
+    case NNAB_EINVAL: return "invalid argument";
+    case NNAB_ECUDA: return "CUDA error";
+    case NNAB_ENOTSUP: return "configuration not supported by the sm_100a kernels";
+    case NNAB_ENODEV: return "no sm_100 (B200) device";
+    default: return "unknown nnab status";
+  }
+}
+
+extern "C" const char* nnab_last_error(void) { return g_last_error; }
+
+extern "C" size_t nnab_stft_workspace_bytes(const nnab_frames* f, int32_t precision) {
+  FrameGeom g;
+  if (frame_geometry(f, &g)) return 0;
+  return stage_bytes(g) * (precision == NNAB_PREC_3XTF32 ? 2 : 1);
+}
+
+static int validate_kind(int32_t out_kind, int32_t n_bins, const float* mel_w, int32_t n_mels, int32_t mel_ld,
+                         int32_t n_tiles) {
+  if (out_kind < NNAB_OUT_MAGNITUDE || out_kind > NNAB_OUT_SMOOTH_MAG) return NNAB_EINVAL;
+  if (out_kind == NNAB_OUT_MEL) {
+    if (!mel_w || n_mels < 1) return NNAB_EINVAL;
+    if (mel_ld < std::max(n_tiles * 128, n_bins)) return NNAB_EINVAL;
+  }
+  return NNAB_OK;
+}
+
+extern "C" int nnab_stft_forward(const nnab_frames* f, const float* x, const float* packed_hi,
+                                 const float* packed_lo, int32_t n_bins, int32_t fold_nyquist, int32_t precision,
+                                 int32_t out_kind, float power, float eps, const float* mel_w, int32_t n_mels,
+                                 int32_t mel_ld, const int32_t* mel_band, float* out, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  FrameGeom g;
+  if ((rc = frame_geometry(f, &g))) return rc;
+  if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
+  const int split = precision == NNAB_PREC_3XTF32;
+  if (!x || !packed_hi || (split && !packed_lo) || !out || n_bins < 1) return NNAB_EINVAL;
+  if (fold_nyquist && n_bins < 2) return NNAB_EINVAL;
+  const int32_t tiles = nnab_dft_bank_tiles(n_bins, fold_nyquist);
+  if ((rc = validate_kind(out_kind, n_bins, mel_w, n_mels, mel_ld, tiles))) return rc;
+  if (g.B == 0) return NNAB_OK;
+  const size_t need = nnab_stft_workspace_bytes(f, precision);
+  if (!workspace || workspace_bytes < need) return NNAB_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  float* rows_hi = reinterpret_cast<float*>(workspace);
+  float* rows_lo = split ? reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + stage_bytes(g)) : nullptr;
+  if ((rc = stage_frames(g, x, rows_hi, rows_lo, split, s))) return rc;
+  StftGemmArgs a{};
+  a.a_hi = rows_hi;
+  a.a_lo = rows_lo;
+  a.b_hi = packed_hi;
+  a.b_lo = packed_lo;
+  a.n_tiles = tiles;
+  a.n_bins = n_bins;
+  a.fold = fold_nyquist ? 1 : 0;
+  a.out_kind = out_kind;
+  a.power = power;
+  a.eps = eps;
+  a.mel_w = mel_w;
+  a.n_mels = n_mels;
+  a.mel_ld = mel_ld;
+  a.mel_band = mel_band;
+  a.out = out;
+  return launch_stft_gemm(g, a, precision, s);
+}
+
+// ------------------------------------------------------------ host variant
+static int64_t out_elems_per_clip(int32_t out_kind, int32_t n_bins, int32_t n_mels, int32_t T) {
+  if (out_kind == NNAB_OUT_MEL) return (int64_t)n_mels * T;
+  if (out_kind == NNAB_OUT_COMPLEX) return 2ll * n_bins * T;
+  return (int64_t)n_bins * T;
+}
+
+extern "C" size_t nnab_stft_host_scratch_bytes(const nnab_frames* f, int32_t precision, int32_t out_rows,
+                                               int64_t chunk_clips) {
+  FrameGeom g;
+  if (frame_geometry(f, &g) || chunk_clips < 1) return 0;
+  nnab_frames fc = *f;
+  fc.batch = std::min<int64_t>(chunk_clips, f->batch);
+  const size_t ws = nnab_stft_workspace_bytes(&fc, precision);
+  const size_t xin = align256((size_t)fc.batch * g.L * 4);
+  const size_t o = align256((size_t)fc.batch * out_rows * g.T * 4);
+  return 2 * (xin + o) + ws;
+}
+
+extern "C" int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const float* packed_hi,
+                                      const float* packed_lo, int32_t n_bins, int32_t fold_nyquist,
+                                      int32_t precision, int32_t out_kind, float power, float eps,
+                                      const float* mel_w, int32_t n_mels, int32_t mel_ld, const int32_t* mel_band,
+                                      float* out_host, int64_t chunk_clips, void* device_scratch,
+                                      size_t scratch_bytes, void* stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  FrameGeom g;
+  if ((rc = frame_geometry(f, &g))) return rc;
+  if (!x_host || !out_host || chunk_clips < 1) return NNAB_EINVAL;
+  if (g.B == 0) return NNAB_OK;
+  const int64_t per_clip_out = out_elems_per_clip(out_kind, n_bins, n_mels, g.T);
+  const int32_t out_rows = (int32_t)(per_clip_out / g.T);
+  const int64_t chunk = std::min<int64_t>(chunk_clips, g.B);
+  if (scratch_bytes < nnab_stft_host_scratch_bytes(f, precision, out_rows, chunk)) return NNAB_EINVAL;
+  nnab_frames fc = *f;
+  fc.batch = chunk;
+  const size_t xin = align256((size_t)chunk * g.L * 4);
+  const size_t ob = align256((size_t)chunk * per_clip_out * 4);
+  char* base = reinterpret_cast<char*>(device_scratch);
+  float* xd[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + xin)};
+  float* od[2] = {reinterpret_cast<float*>(base + 2 * xin), reinterpret_cast<float*>(base + 2 * xin + ob)};
+  void* ws = base + 2 * xin + 2 * ob;
+  const size_t ws_bytes = nnab_stft_workspace_bytes(&fc, precision);
+
+  // Three-stage software pipeline over clip chunks: copy-in on `cin`, compute
+  // on the caller's stream, copy-out on `cout`; events order the hand-offs.
+  cudaStream_t s = (cudaStream_t)stream, cin = nullptr, cout = nullptr;
+  NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+  NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+  cudaEvent_t start, in_done[2], comp_done[2], out_done[2];
+  NNAB_CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming));
+    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming));
+    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
+  }
+  NNAB_CUDA_TRY(cudaEventRecord(start, s));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(cin, start, 0));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(cout, start, 0));
+  const int64_t n_chunks = (g.B + chunk - 1) / chunk;
+  for (int64_t i = 0; i < n_chunks && rc == NNAB_OK; ++i) {
+    const int slot = (int)(i & 1);
+    const int64_t c0 = i * chunk;
+    const int64_t nb = std::min<int64_t>(chunk, g.B - c0);
+    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(cin, comp_done[slot], 0));  // x slot free
+    NNAB_CUDA_TRY(cudaMemcpyAsync(xd[slot], x_host + c0 * g.L, (size_t)nb * g.L * 4, cudaMemcpyHostToDevice, cin));
+    NNAB_CUDA_TRY(cudaEventRecord(in_done[slot], cin));
+    NNAB_CUDA_TRY(cudaStreamWaitEvent(s, in_done[slot], 0));
+    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(s, out_done[slot], 0));  // out slot drained
+    fc.batch = nb;
+    rc = nnab_stft_forward(&fc, xd[slot], packed_hi, packed_lo, n_bins, fold_nyquist, precision, out_kind, power,
+                           eps, mel_w, n_mels, mel_ld, mel_band, od[slot], ws, ws_bytes, s);
+    NNAB_CUDA_TRY(cudaEventRecord(comp_done[slot], s));
+    NNAB_CUDA_TRY(cudaStreamWaitEvent(cout, comp_done[slot], 0));
+    NNAB_CUDA_TRY(cudaMemcpyAsync(out_host + c0 * per_clip_out, od[slot], (size_t)nb * per_clip_out * 4,
+                                  cudaMemcpyDeviceToHost, cout));
+    NNAB_CUDA_TRY(cudaEventRecord(out_done[slot], cout));
+  }
+  // join: the caller's stream waits for the last copy-out
+  NNAB_CUDA_TRY(cudaEventRecord(out_done[0], cout));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(s, out_done[0], 0));
+  cudaStreamDestroy(cin);
+  cudaStreamDestroy(cout);
+  cudaEventDestroy(start);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(in_done[i]);
+    cudaEventDestroy(comp_done[i]);
+    cudaEventDestroy(out_done[i]);
+  }
+  return rc;
+}

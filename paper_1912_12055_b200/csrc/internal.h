@@ -1,0 +1,59 @@
+// Host-side internals shared by the libnnab translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/nnab.h"
+
+namespace nnab {
+
+// Record a CUDA error for nnab_last_error() and map it to NNAB_ECUDA.
+int cuda_fail(cudaError_t e, const char* where);
+#define NNAB_CUDA_TRY(expr)                              \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
+  } while (0)
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                 uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+
+int num_sms();
+
+// Staging layout for frames: see frames.cu.
+struct FrameGeom {
+  int64_t B, L;
+  int32_t width, hop, pad, pad_mode;
+  int32_t T;         // frames per clip
+  int32_t k_pad;     // width rounded up to 32
+  int32_t row_len;   // TMA row (hop in hop-row mode, k_pad in framed mode)
+  int32_t R;         // staged rows per clip
+  int64_t padded_len;
+};
+int frame_geometry(const nnab_frames* f, FrameGeom* g);
+
+int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows_lo, int split,
+                 cudaStream_t s);
+
+struct StftGemmArgs {
+  const float* a_hi;  // staged rows (B*R, row_len)
+  const float* a_lo;
+  const float* b_hi;  // packed bank (n_tiles*256, k_pad)
+  const float* b_lo;
+  int32_t n_tiles;
+  int32_t n_bins;
+  int32_t fold;
+  int32_t out_kind;
+  float power;
+  float eps;
+  const float* mel_w;
+  int32_t n_mels, mel_ld;
+  const int32_t* mel_band;
+  float* out;
+};
+int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, cudaStream_t s);
+
+}  // namespace nnab

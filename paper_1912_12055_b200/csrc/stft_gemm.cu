@@ -1,0 +1,363 @@
+// STFT / Mel forward: one persistent warp-specialised tcgen05 GEMM per call.
+//
+// Replaces the reference's per-clip DGEMM `frames @ kernels.T`
+// (signal.py:181-182 via transforms.py:130-144) and the follow-on
+// magnitude / power / complex finish (transforms.py:86-93) and Mel projection
+// `weights @ |X|^power` (transforms.py:164-172), fused into the epilogue.
+//
+//   D[slot, col] = sum_k rows[slot + k/row_len, k%row_len] * bank[col, k]
+//
+// M = frame slots (128 per tile, spanning clips), N = 256 bank rows per tile
+// (128 cosine + 128 sine rows of the same 128 bins, so magnitude needs no
+// cross-CTA exchange), K = kernel width.  Operands arrive by TMA (128-byte
+// swizzle, 32-sample K blocks; 64-byte swizzle + 16-sample blocks in 3xTF32
+// mode where each stage carries hi and lo halves), accumulate in TMEM (two
+// 256-column accumulators so the epilogue of tile n overlaps the MMAs of n+1),
+// and the epilogue warps read TMEM with tcgen05.ld.
+//
+// Warp roles (256 threads, one CTA per SM):
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      MMA issuer (one elected lane)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: thread = accumulator row = one frame slot
+#include <algorithm>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace nnab {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBN = 256;  // 128 bins x {cos, sin}
+constexpr int kThreads = 256;
+constexpr int kMelRows = 128;  // mel accumulator rows resident in smem
+
+template <bool kSplit>
+struct Cfg {
+  static constexpr int BK = kSplit ? 16 : 32;            // fp32 elements per K block
+  static constexpr int SWZ = BK * 4;                     // swizzle span in bytes (64 or 128)
+  static constexpr int A_BYTES = kBM * BK * 4;           // 16 KB | 8 KB
+  static constexpr int B_BYTES = kBN * BK * 4;           // 32 KB | 16 KB
+  static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);  // 48 KB either way
+  // TF32: two 256-column accumulators (double buffer).  3xTF32: one buffer of
+  // main (hi*hi) + correction (hi*lo + lo*hi) accumulators.  Keeping the large
+  // hi*hi chain apart from the small cross terms cuts the number of
+  // accumulate steps the big partial sums go through by 3x, which is what
+  // bounds 3xTF32 accuracy (the tensor-core FP32 accumulate is not RNE).
+  static constexpr int NUM_ACC = kSplit ? 1 : 2;
+  static constexpr int ACC_STRIDE = kSplit ? 512 : 256;
+};
+
+struct Params {
+  int64_t B;
+  int32_t T, R, row_len, kblocks, n_mtiles, n_tiles, n_bins, fold, out_kind;
+  float power, eps;
+  const float* mel_w;
+  int32_t n_mels, mel_ld;
+  const int32_t* mel_band;
+  float* out;
+};
+
+NNAB_DEV uint64_t make_sdesc(const void* p, int swz_bytes) {
+  // K-major, rows of swz_bytes, 8-row atoms of 8*swz_bytes
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * swz_bytes) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(swz_bytes == 128 ? 2 : 4) << 61;
+  return d;
+}
+
+NNAB_DEV float finish(float re, float im, int kind, float power, float eps) {
+  const float p = fmaf(re, re, im * im);
+  if (kind == NNAB_OUT_POWER) return p;
+  if (kind == NNAB_OUT_SMOOTH_MAG) return sqrtf(p + eps);
+  const float m = sqrtf(p);
+  if (kind == NNAB_OUT_MEL) {
+    if (power == 1.f) return m;
+    if (power == 2.f) return p;
+    return powf(m, power);
+  }
+  return m;
+}
+
+template <bool kSplit>
+__global__ void __launch_bounds__(kThreads, 1)
+    stft_gemm_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
+                     const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
+                     const Params p) {
+  using C = Cfg<kSplit>;
+  const bool mel = p.out_kind == NNAB_OUT_MEL;
+  const int stages = mel ? 3 : 4;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* mel_acc = reinterpret_cast<float*>(smem + stages * C::STAGE_BYTES);  // [kMelRows][kBM]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * C::STAGE_BYTES + (mel ? kMelRows * kBM * 4 : 0));
+  uint64_t* full = bars;            // [stages]
+  uint64_t* empty = bars + 4;       // [stages]
+  uint64_t* tmem_full = bars + 8;   // [2]
+  uint64_t* tmem_empty = bars + 10; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_a_hi);
+    tma_prefetch(&tm_b_hi);
+    if (kSplit) {
+      tma_prefetch(&tm_a_lo);
+      tma_prefetch(&tm_b_lo);
+    }
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], kBM);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (mel) {
+    for (int i = threadIdx.x; i < kMelRows * kBM; i += kThreads) mel_acc[i] = 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nt = p.n_tiles, kb_n = p.kblocks;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      const uint64_t keep = policy_evict_last();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int mt = blockIdx.x; mt < p.n_mtiles; mt += gridDim.x) {
+        for (int n = 0; n < nt; ++n) {
+          for (int kb = 0; kb < kb_n; ++kb) {
+            mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* st = smem + s * C::STAGE_BYTES;
+            mbar_expect_tx(&full[s], C::STAGE_BYTES);
+            const int k = kb * C::BK;
+            const int a_col = k % p.row_len;
+            const int a_row = mt * kBM + k / p.row_len;
+            tma_load_2d_hint(st, &tm_a_hi, &full[s], a_col, a_row, keep);
+            tma_load_2d_hint(st + C::A_BYTES, &tm_b_hi, &full[s], k, n * kBN, keep);
+            if (kSplit) {
+              tma_load_2d_hint(st + C::A_BYTES + C::B_BYTES, &tm_a_lo, &full[s], a_col, a_row, keep);
+              tma_load_2d_hint(st + 2 * C::A_BYTES + C::B_BYTES, &tm_b_lo, &full[s], k, n * kBN, keep);
+            }
+            if (++s == stages) { s = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int mt = blockIdx.x; mt < p.n_mtiles; mt += gridDim.x) {
+        for (int n = 0; n < nt; ++n) {
+          mbar_wait(&tmem_empty[acc], aph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem_base + acc * C::ACC_STRIDE;
+          for (int kb = 0; kb < kb_n; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            uint8_t* st = smem + s * C::STAGE_BYTES;
+            const uint64_t a_hi = make_sdesc(st, C::SWZ);
+            const uint64_t b_hi = make_sdesc(st + C::A_BYTES, C::SWZ);
+#pragma unroll
+            for (int k = 0; k < C::BK / 8; ++k) {
+              const uint64_t off = (uint64_t)((k * 32) >> 4);  // 8 tf32 = 32 bytes along K
+              mma_tf32(d, a_hi + off, b_hi + off, idesc, (kb | k) != 0);
+              if (kSplit) {
+                const uint64_t a_lo = make_sdesc(st + C::A_BYTES + C::B_BYTES, C::SWZ);
+                const uint64_t b_lo = make_sdesc(st + 2 * C::A_BYTES + C::B_BYTES, C::SWZ);
+                mma_tf32(d + kBN, a_hi + off, b_lo + off, idesc, (kb | k) != 0);
+                mma_tf32(d + kBN, a_lo + off, b_hi + off, idesc, 1);
+              }
+            }
+            mma_commit(&empty[s]);
+            if (++s == stages) { s = 0; ph ^= 1; }
+          }
+          mma_commit(&tmem_full[acc]);
+          if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t q = warp - 4;  // TMEM lane quarter
+    const uint32_t row = q * 32 + lane;
+    const int kind = p.out_kind;
+    const int F = p.n_bins;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int mt = blockIdx.x; mt < p.n_mtiles; mt += gridDim.x) {
+      const int64_t g = (int64_t)mt * kBM + row;
+      const int64_t b = g / p.R;
+      const int t = (int)(g - b * p.R);
+      const bool valid = b < p.B && t < p.T;
+      float nyq_val = 0.f;
+      for (int n = 0; n < nt; ++n) {
+        mbar_wait(&tmem_full[acc], aph);
+        tc_fence_after();
+        const uint32_t tb = tmem_base + ((q * 32) << 16) + acc * C::ACC_STRIDE;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float re[32], im[32];
+          tmem_ld32(tb + c * 32, re);
+          tmem_ld32(tb + 128 + c * 32, im);
+          if (kSplit) {
+            float cre[32], cim[32];
+            tmem_ld32(tb + kBN + c * 32, cre);
+            tmem_ld32(tb + kBN + 128 + c * 32, cim);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              re[j] += cre[j];
+              im[j] += cim[j];
+            }
+          } else {
+            tmem_ld_wait();
+          }
+          const int bin0 = n * 128 + c * 32;
+          float nyq_re = 0.f;
+          if (p.fold && n == 0 && c == 0) {
+            nyq_re = im[0];  // cosine row of bin F-1 sits in bin 0's sine slot
+            im[0] = 0.f;
+          }
+          if (kind == NNAB_OUT_MEL) {
+            float m32[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) m32[j] = finish(re[j], im[j], kind, p.power, p.eps);
+            const int ch = bin0 >> 5;
+            const int lo = p.mel_band ? p.mel_band[2 * ch] : 0;
+            const int hi = p.mel_band ? p.mel_band[2 * ch + 1] : p.n_mels;
+            for (int m = lo; m < hi; ++m) {
+              const float4* w = reinterpret_cast<const float4*>(p.mel_w + (int64_t)m * p.mel_ld + bin0);
+              float a = mel_acc[m * kBM + row];
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 wv = __ldg(w + j4);
+                a = fmaf(wv.x, m32[4 * j4 + 0], a);
+                a = fmaf(wv.y, m32[4 * j4 + 1], a);
+                a = fmaf(wv.z, m32[4 * j4 + 2], a);
+                a = fmaf(wv.w, m32[4 * j4 + 3], a);
+              }
+              mel_acc[m * kBM + row] = a;
+            }
+            if (p.fold && n == 0 && c == 0) nyq_val = finish(nyq_re, 0.f, kind, p.power, p.eps);
+          } else if (valid) {
+            const int64_t ob = b * (int64_t)F;
+            if (kind == NNAB_OUT_COMPLEX) {
+              float2* o = reinterpret_cast<float2*>(p.out);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (bin0 + j < F - p.fold) o[(ob + bin0 + j) * p.T + t] = make_float2(re[j], -im[j]);
+              if (p.fold && n == 0 && c == 0) o[(ob + F - 1) * p.T + t] = make_float2(nyq_re, 0.f);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (bin0 + j < F - p.fold) p.out[(ob + bin0 + j) * p.T + t] = finish(re[j], im[j], kind, p.power, p.eps);
+              if (p.fold && n == 0 && c == 0) p.out[(ob + F - 1) * p.T + t] = finish(nyq_re, 0.f, kind, p.power, p.eps);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[acc]);
+        if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
+      }
+      if (kind == NNAB_OUT_MEL) {
+        if (p.fold) {  // Nyquist bin's mel contribution
+          const int ch = (F - 1) >> 5;
+          const int lo = p.mel_band ? p.mel_band[2 * ch] : 0;
+          const int hi = p.mel_band ? p.mel_band[2 * ch + 1] : p.n_mels;
+          for (int m = lo; m < hi; ++m)
+            mel_acc[m * kBM + row] = fmaf(__ldg(p.mel_w + (int64_t)m * p.mel_ld + F - 1), nyq_val, mel_acc[m * kBM + row]);
+        }
+        for (int m = 0; m < p.n_mels; ++m) {
+          if (valid) p.out[(b * p.n_mels + m) * (int64_t)p.T + t] = mel_acc[m * kBM + row];
+          mel_acc[m * kBM + row] = 0.f;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem_base);
+}
+
+template <bool kSplit>
+int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
+  using C = Cfg<kSplit>;
+  const bool mel = a.out_kind == NNAB_OUT_MEL;
+  if (mel && (a.n_mels < 1 || a.n_mels > kMelRows || !a.mel_w || a.mel_ld % 4 != 0)) return NNAB_ENOTSUP;
+  if (g.row_len % C::BK != 0) return NNAB_ENOTSUP;
+  CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
+  const uint64_t rows_total = (uint64_t)g.B * g.R;
+  const uint64_t bank_rows = (uint64_t)a.n_tiles * kBN;
+  int rc = make_tmap_2d(&ta_hi, a.a_hi, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
+  if (!rc) rc = make_tmap_2d(&tb_hi, a.b_hi, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, kBN, C::SWZ);
+  if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, a.a_lo, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
+  if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, a.b_lo, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, kBN, C::SWZ);
+  if (rc) return rc;
+  if (!kSplit) {
+    ta_lo = ta_hi;
+    tb_lo = tb_hi;
+  }
+  Params p{};
+  p.B = g.B;
+  p.T = g.T;
+  p.R = g.R;
+  p.row_len = g.row_len;
+  p.kblocks = g.k_pad / C::BK;
+  p.n_mtiles = (int32_t)((rows_total + kBM - 1) / kBM);
+  p.n_tiles = a.n_tiles;
+  p.n_bins = a.n_bins;
+  p.fold = a.fold;
+  p.out_kind = a.out_kind;
+  p.power = a.power;
+  p.eps = a.eps;
+  p.mel_w = a.mel_w;
+  p.n_mels = a.n_mels;
+  p.mel_ld = a.mel_ld;
+  p.mel_band = a.mel_band;
+  p.out = a.out;
+  if (p.n_mtiles == 0) return NNAB_OK;
+  const int stages = mel ? 3 : 4;
+  const size_t smem = 1024 + (size_t)stages * C::STAGE_BYTES + (mel ? kMelRows * kBM * 4 : 0) + 128;
+  auto kern = stft_gemm_kernel<kSplit>;
+  NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = std::min(p.n_mtiles, num_sms());
+  kern<<<grid, kThreads, smem, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+  NNAB_CUDA_TRY(cudaGetLastError());
+  return NNAB_OK;
+}
+
+}  // namespace
+
+int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, cudaStream_t s) {
+  if (precision == NNAB_PREC_3XTF32) return launch_impl<true>(g, a, s);
+  if (precision == NNAB_PREC_TF32) return launch_impl<false>(g, a, s);
+  return NNAB_EINVAL;
+}
+
+}  // namespace nnab

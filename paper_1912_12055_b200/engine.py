@@ -1,0 +1,207 @@
+"""Device-side engines: own the packed kernel banks on the GPU and run the
+sm_100a kernels through the C ABI.  Everything above this module (the
+`spectro`-compatible transforms and the nnAudio-style nn.Modules) funnels
+through here, mirroring how every reference transform funnels through
+`conv1d_strided` (signal.py:159-183)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _require_cuda(device) -> torch.device:
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise L.NnabError("paper_1912_12055_b200 runs only on CUDA (sm_100a); got device " + str(device))
+    if not torch.cuda.is_available():
+        raise L.NnabError("no CUDA device: the sm_100a kernels have no CPU fallback")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    major, _ = torch.cuda.get_device_capability(device)
+    if major != 10:
+        raise L.NnabError(f"sm_100 (B200) required, found compute capability {major}.x")
+    return device
+
+
+def frames_struct(B: int, length: int, width: int, hop: int, pad: int, pad_mode: str) -> L.nnab_frames:
+    if pad_mode not in L.PAD_MODES:
+        raise ValueError(f"unknown pad mode {pad_mode!r}")
+    return L.nnab_frames(int(B), int(length), int(width), int(hop), int(pad), L.PAD_MODES[pad_mode])
+
+
+def geometry(length: int, width: int, hop: int, pad: int, pad_mode: str):
+    """(n_frames, row_len, rows_per_clip) with the reference's ValueErrors."""
+    if hop < 1:
+        raise ValueError(f"stride must be >= 1, got {hop}")
+    if pad_mode == "reflect" and pad > 0 and pad >= length:
+        raise ValueError(f"reflect padding ({pad}, {pad}) must be shorter than the signal (len {length})")
+    if width > length + 2 * pad:
+        raise ValueError(f"kernel length {width} exceeds signal length {length + 2 * pad}; pad the signal first")
+    f = frames_struct(1, length, width, hop, pad, pad_mode)
+    t, rl, r = C.c_int32(), C.c_int32(), C.c_int32()
+    L.check(L.load().nnab_frames_geometry(C.byref(f), C.byref(t), C.byref(rl), C.byref(r)), "frames_geometry")
+    return t.value, rl.value, r.value
+
+
+class _Workspace:
+    """Grow-only device scratch, one per engine and device."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+class DftEngine:
+    """A DFT-type bank (h_re, h_im rows of width n_fft) applied at a hop,
+    optionally followed by a fused Mel projection.
+
+    fold_nyquist packs the default integer-bin bank into whole 256-row tiles
+    (its bin-0 and Nyquist sine rows are zero); trainable banks never fold
+    because their sine rows may become non-zero.
+    """
+
+    def __init__(self, h_re, h_im, hop: int, center: bool = True, pad_mode: str = "reflect",
+                 precision: str = "tf32", device="cuda", allow_fold: bool = True):
+        self.device = _require_cuda(device)
+        if precision not in L.PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
+        self.precision = L.PRECISIONS[precision]
+        h_re = torch.as_tensor(h_re)
+        h_im = torch.as_tensor(h_im)
+        if h_re.shape != h_im.shape or h_re.dim() != 2:
+            raise ValueError("h_re and h_im must be equal-shape 2-D banks")
+        self.n_bins, self.n_fft = int(h_re.shape[0]), int(h_re.shape[1])
+        self.hop, self.center, self.pad_mode = int(hop), bool(center), pad_mode
+        if self.hop < 1:
+            raise ValueError(f"stride must be >= 1, got {hop}")
+        self.fold = 0
+        if allow_fold and self.n_bins >= 2:
+            scale = float(h_re.abs().max()) or 1.0
+            z0 = float(h_im[0].abs().max()) <= 1e-9 * scale
+            zn = float(h_im[-1].abs().max()) <= 1e-9 * scale
+            self.fold = int(z0 and zn and (self.n_bins - 1) % 128 == 0)
+        self._ws = _Workspace()
+        self.mel_w = None
+        self.set_bank(h_re, h_im)
+
+    # ------------------------------------------------------------ banks
+    def set_bank(self, h_re, h_im) -> None:
+        """(Re)pack the bank on the device (used every step by trainable layers)."""
+        lib = L.load()
+        h_re = torch.as_tensor(h_re).to(self.device, torch.float32).contiguous()
+        h_im = torch.as_tensor(h_im).to(self.device, torch.float32).contiguous()
+        nbytes = lib.nnab_dft_bank_bytes(self.n_bins, self.n_fft, self.fold)
+        n = nbytes // 4
+        if getattr(self, "packed_hi", None) is None or self.packed_hi.numel() != n:
+            self.packed_hi = torch.empty(n, dtype=torch.float32, device=self.device)
+            self.packed_lo = (torch.empty(n, dtype=torch.float32, device=self.device)
+                              if self.precision == L.PREC_3XTF32 else None)
+        L.check(lib.nnab_pack_dft_bank(h_re.data_ptr(), h_im.data_ptr(), self.n_bins, self.n_fft, self.fold,
+                                       self.precision, self.packed_hi.data_ptr(), L.ptr(self.packed_lo),
+                                       L.stream_handle(self.device)), "pack_dft_bank")
+        self.n_tiles = lib.nnab_dft_bank_tiles(self.n_bins, self.fold)
+
+    def set_mel(self, weights, power: float = 1.0, banded: bool = True) -> None:
+        """Mel weights (n_mels, n_bins) for the fused epilogue; rows padded to
+        a multiple of 4 floats so the epilogue reads them with 16-byte loads."""
+        w = torch.as_tensor(weights, dtype=torch.float64)
+        if w.dim() != 2 or w.shape[1] != self.n_bins:
+            raise ValueError(f"mel weights must be (n_mels, {self.n_bins})")
+        self.n_mels = int(w.shape[0])
+        if self.n_mels > 128:
+            raise L.NnabError("fused Mel epilogue supports n_mels <= 128")
+        self.mel_ld = ((max(self.n_tiles * 128, self.n_bins) + 3) // 4) * 4 + 32
+        wp = torch.zeros(self.n_mels, self.mel_ld, dtype=torch.float32)
+        wp[:, : self.n_bins] = w.to(torch.float32)
+        self.mel_w = wp.to(self.device)
+        n_chunks = self.mel_ld // 32 + 1
+        if banded:
+            from .banks import mel_bands
+            band = mel_bands(wp.numpy(), n_chunks)
+            self.mel_band = torch.from_numpy(band.reshape(-1)).to(self.device)
+        else:
+            self.mel_band = None
+        self.power = float(power)
+
+    # ------------------------------------------------------------ forward
+    def frames(self, B: int, length: int) -> L.nnab_frames:
+        pad = self.n_fft // 2 if self.center else 0
+        return frames_struct(B, length, self.n_fft, self.hop, pad, self.pad_mode)
+
+    def n_frames(self, length: int) -> int:
+        pad = self.n_fft // 2 if self.center else 0
+        return geometry(length, self.n_fft, self.hop, pad, self.pad_mode)[0]
+
+    def forward(self, x: torch.Tensor, kind: str = "magnitude", eps: float = 1e-12,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+        """x (B, L) float32 on the engine's device -> (B, F, T) [complex64 for 'complex',
+        (B, n_mels, T) for 'mel']."""
+        lib = L.load()
+        if x.dim() == 1:
+            x = x[None]
+        if x.device != self.device:
+            raise ValueError(f"input on {x.device}, engine on {self.device}")
+        x = x.to(torch.float32).contiguous()
+        B, length = int(x.shape[0]), int(x.shape[1])
+        if length < 1:
+            raise ValueError("signal must be non-empty")
+        T = self.n_frames(length)
+        kinds = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX,
+                 "mel": L.OUT_MEL, "smooth": L.OUT_SMOOTH_MAG}
+        if kind not in kinds:
+            raise ValueError(f"output must be one of {sorted(kinds)}, got {kind!r}")
+        k = kinds[kind]
+        if k == L.OUT_MEL and self.mel_w is None:
+            raise ValueError("set_mel() first")
+        if out is None:
+            if k == L.OUT_COMPLEX:
+                out = torch.empty(B, self.n_bins, T, dtype=torch.complex64, device=self.device)
+            elif k == L.OUT_MEL:
+                out = torch.empty(B, self.n_mels, T, dtype=torch.float32, device=self.device)
+            else:
+                out = torch.empty(B, self.n_bins, T, dtype=torch.float32, device=self.device)
+        if B == 0:
+            return out
+        f = self.frames(B, length)
+        need = lib.nnab_stft_workspace_bytes(C.byref(f), self.precision)
+        ws = self._ws.get(need, self.device)
+        mel = k == L.OUT_MEL
+        L.check(lib.nnab_stft_forward(
+            C.byref(f), x.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins, self.fold,
+            self.precision, k, float(getattr(self, "power", 1.0)), float(eps),
+            self.mel_w.data_ptr() if mel else None, self.n_mels if mel else 0, self.mel_ld if mel else 0,
+            L.ptr(self.mel_band) if mel else None, out.data_ptr(), ws.data_ptr(), ws.numel(),
+            L.stream_handle(self.device)), "stft_forward")
+        return out
+
+    def forward_host(self, x_host: torch.Tensor, kind: str = "magnitude", chunk_clips: int = 128,
+                     out_host: torch.Tensor | None = None) -> torch.Tensor:
+        """Pinned host (B, L) -> pinned host result, streamed through the GPU
+        in chunks with copy/compute overlap (nnab_stft_forward_host)."""
+        lib = L.load()
+        B, length = int(x_host.shape[0]), int(x_host.shape[1])
+        T = self.n_frames(length)
+        k = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "mel": L.OUT_MEL}[kind]
+        rows = self.n_mels if k == L.OUT_MEL else self.n_bins
+        if out_host is None:
+            out_host = torch.empty(B, rows, T, dtype=torch.float32, pin_memory=True)
+        f = self.frames(B, length)
+        need = lib.nnab_stft_host_scratch_bytes(C.byref(f), self.precision, rows, chunk_clips)
+        ws = self._ws.get(need, self.device)
+        mel = k == L.OUT_MEL
+        L.check(lib.nnab_stft_forward_host(
+            C.byref(f), x_host.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins, self.fold,
+            self.precision, k, float(getattr(self, "power", 1.0)), 1e-12,
+            self.mel_w.data_ptr() if mel else None, self.n_mels if mel else 0, self.mel_ld if mel else 0,
+            L.ptr(self.mel_band) if mel else None, out_host.data_ptr(), int(chunk_clips), ws.data_ptr(),
+            ws.numel(), L.stream_handle(self.device)), "stft_forward_host")
+        return out_host

@@ -1,0 +1,116 @@
+"""GPU parity: STFT / Mel through the sm_100a tcgen05 kernels vs the oracle.
+
+Tolerances are peak-normalised max error (SURVEY.md section 0 finding 2):
+TF32 mode <= 1e-3, 3xTF32 ("fp32") mode <= 1e-5.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import spectro_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"tf32": 1e-3, "fp32": 1e-5}
+# power = |X|^2 doubles the relative error of the magnitude it squares, so the
+# magnitude gate of 1e-5 (fp32 mode) is 2e-5 on power outputs.
+TOL_POWER = {"tf32": 2e-3, "fp32": 2e-5}
+SR = 44100.0
+
+
+def engine(h_re, h_im, hop, precision, **kw):
+    from paper_1912_12055_b200.engine import DftEngine
+    return DftEngine(h_re, h_im, hop, precision=precision, device="cuda", **kw)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_stft_full_config_golden(golden, cuda_dev, precision):
+    h_re, h_im = O.stft_bank()
+    eng = engine(h_re, h_im, 512, precision)
+    assert eng.fold == 1 and eng.n_tiles == 8
+    x = torch.from_numpy(golden["clips"]).to(cuda_dev)
+    got = eng.forward(x, "magnitude").cpu().numpy()
+    assert got.shape == (2, 1025, 157)
+    for i in range(2):
+        err = O.peak_err(got[i], golden["stft_mag_full"][i])
+        assert err <= TOL[precision], (precision, i, err)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("power,key", [(1.0, "mel_full"), (2.0, "mel_full_p2")])
+def test_mel_full_config_golden(golden, cuda_dev, precision, power, key):
+    h_re, h_im = O.stft_bank()
+    eng = engine(h_re, h_im, 512, precision)
+    eng.set_mel(O.mel_bank(SR, 2048, 128, formula="slaney"), power=power)
+    x = torch.from_numpy(golden["clips"]).to(cuda_dev)
+    got = eng.forward(x, "mel").cpu().numpy()
+    assert got.shape == (2, 128, 157)
+    for i in range(2):
+        err = O.peak_err(got[i], golden[key][i])
+        tol = (TOL_POWER if power == 2.0 else TOL)[precision]
+        assert err <= tol, (precision, key, i, err)
+
+
+def test_mel_dense_weights_match_banded(golden, cuda_dev):
+    h_re, h_im = O.stft_bank()
+    W = O.mel_bank(SR, 2048, 128, formula="htk", norm="area")
+    a = engine(h_re, h_im, 512, "fp32")
+    a.set_mel(W, banded=True)
+    b = engine(h_re, h_im, 512, "fp32")
+    b.set_mel(W, banded=False)
+    x = torch.from_numpy(golden["clips"]).to(cuda_dev)
+    ra, rb = a.forward(x, "mel").cpu().numpy(), b.forward(x, "mel").cpu().numpy()
+    assert O.peak_err(ra, rb) < 1e-6
+    ref = np.stack([O.mel_clip(c.astype(np.float64), h_re, h_im, W, 512) for c in golden["clips"]])
+    assert O.peak_err(ra, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_stft_small_configs_golden(golden, cuda_dev, precision):
+    xs = torch.from_numpy(golden["small_x"].astype(np.float32)).to(cuda_dev)
+    cases = [
+        ("stft_small_complex", O.stft_bank(128, 8000.0), 64, dict(), "complex"),
+        ("stft_small_power_zero", O.stft_bank(128, 8000.0), 32, dict(pad_mode="constant_zero"), "power"),
+        ("stft_small_nocenter", O.stft_bank(128, 8000.0, window_kind="hamming"), 48, dict(center=False), "magnitude"),
+        ("stft_small_log", O.stft_bank(256, 8000.0, freq_scale="log", fmin=80.0, fmax=3500.0, freq_bins=100), 64,
+         dict(), "magnitude"),
+        ("stft_small_linear", O.stft_bank(256, 8000.0, freq_scale="linear", fmin=50.0, fmax=3000.0, freq_bins=90),
+         64, dict(), "magnitude"),
+    ]
+    for key, (h_re, h_im), hop, kw, kind in cases:
+        eng = engine(h_re, h_im, hop, precision, **kw)
+        got = eng.forward(xs[None], kind)[0].cpu().numpy()
+        ref = golden[key]
+        assert got.shape == ref.shape, key
+        err = O.peak_err(got, ref)
+        assert err <= TOL[precision], (key, precision, err)
+
+
+def test_batch_spanning_tiles_matches_oracle(cuda_dev):
+    # 37 clips of 5000 samples: M tiles straddle clip boundaries and the last tile is ragged
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal((37, 5000)) * 0.5).astype(np.float32)
+    h_re, h_im = O.stft_bank(512, 16000.0)
+    eng = engine(h_re, h_im, 128, "fp32")
+    got = eng.forward(torch.from_numpy(x).to(cuda_dev), "magnitude").cpu().numpy()
+    ref = O.map_clips(lambda c: O.stft_clip(c.astype(np.float64), h_re, h_im, 128), x, threads=4)
+    assert got.shape == ref.shape
+    assert O.peak_err(got, ref) <= 1e-5
+    # batch == sequential, bit-exact (tests/test_transforms.py:325-342)
+    one = np.stack([eng.forward(torch.from_numpy(c).to(cuda_dev)[None], "magnitude")[0].cpu().numpy() for c in x[:3]])
+    assert np.array_equal(one, got[:3])
+
+
+def test_zero_signal_and_bin_exact_tone(cuda_dev):
+    # tests/test_transforms.py:29-47
+    h_re, h_im = O.stft_bank(64, 6400.0, window_kind="rectangular")
+    eng = engine(h_re, h_im, 64, "fp32", center=False)
+    sr, n = 6400.0, 64
+    x = np.cos(2 * np.pi * (8 * sr / n) * np.arange(640) / sr).astype(np.float32)
+    got = eng.forward(torch.from_numpy(x).to(cuda_dev)[None], "magnitude")[0].cpu().numpy()
+    assert got.shape == (33, 10)
+    assert np.allclose(got[8], 32.0, atol=1e-4)
+    assert np.max(np.delete(got, 8, axis=0)) <= 1e-4
+    z = eng.forward(torch.zeros(2, 4000, device=cuda_dev), "magnitude")
+    assert not z.any()
