@@ -114,6 +114,41 @@ int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const floa
                            int32_t mel_ld, const int32_t* mel_band, float* out_host, int64_t chunk_clips,
                            void* device_scratch, size_t scratch_bytes, void* stream);
 
+/* ------------------------------------------------------- CQT1992v2
+ * Cqt1992v2.__call__ (transforms.py:201-208 via _complex_conv 175-186) and
+ * TrainableLayer.spectrogram for CQT banks (gradients.py:61-67).
+ * Bank: k_re/k_im (n_bins, width) float32 device rows (kernels.py:361-402),
+ * packed with re/im rows of each bin interleaved.  `schedule` (device, from
+ * nnab_cqt_schedule over each row's non-zero support) lists the K blocks in
+ * longest-first order with the MMA width each needs.
+ * out: (B, n_bins, T) float32, or complex64 re + i*im for NNAB_OUT_COMPLEX. */
+int nnab_cqt_bank_tiles(int32_t n_bins);
+size_t nnab_cqt_bank_bytes(int32_t n_bins, int32_t width);
+int nnab_pack_cqt_bank(const float* k_re, const float* k_im, int32_t n_bins, int32_t width, int32_t precision,
+                       float* packed_hi, float* packed_lo, void* stream);
+/* host-only: support[2*bin], support[2*bin+1] = non-zero column range [begin, end)
+ * of each row; table_host capacity n_tiles * width/16 + 16 entries. */
+int nnab_cqt_schedule(const int32_t* support, int32_t n_bins, int32_t width, int32_t precision,
+                      uint32_t* table_host, int32_t* n_entries);
+int nnab_cqt1992v2_forward(const nnab_frames* f, const float* x, const float* packed_hi, const float* packed_lo,
+                           int32_t n_bins, const uint32_t* schedule, int32_t n_entries, int32_t precision,
+                           int32_t out_kind, float eps, float* out, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
+/* ------------------------------------------------------- CQT2010v2
+ * Cqt2010v2.__call__ (transforms.py:290-313, 319-323): early_stages x
+ * downsample2 (signal.py:232-247), then per octave alpha: downsample2 (alpha>0)
+ * and the centred complex conv with the top-octave bank (n_filters, width) at
+ * hop kernel_hop >> alpha; rows scattered to first_bin + j - alpha*bins_per_octave.
+ * taps: the (odd, symmetric) anti-alias FIR, HOST float32 (n_taps values).
+ * out (B, n_bins, T) with T = the shortest octave's frame count (returned). */
+size_t nnab_cqt2010v2_workspace_bytes(int64_t B, int64_t L, int32_t early_stages);
+int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, const float* taps, int32_t n_taps,
+                           const float* k_re, const float* k_im, int32_t n_filters, int32_t width,
+                           int32_t early_stages, int32_t n_octaves, int32_t kernel_hop, int32_t first_bin,
+                           int32_t bins_per_octave, int32_t n_bins, int32_t pad_mode, int32_t out_kind, float* out,
+                           int32_t* n_frames_out, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,10 @@ struct StftGemmArgs {
   int32_t n_mels, mel_ld;
   const int32_t* mel_band;
   float* out;
+  const uint32_t* kb_tab = nullptr;  // CQT long-bank schedule (device), see stft_gemm.cu
+  int32_t n_tab = 0;
+  int32_t b_box = 256;
+  int32_t pairs = 0;
 };
 int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, cudaStream_t s);
 

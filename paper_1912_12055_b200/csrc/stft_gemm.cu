@@ -58,6 +58,10 @@ struct Params {
   int32_t n_mels, mel_ld;
   const int32_t* mel_band;
   float* out;
+  // CQT1992v2 long-bank schedule: per N tile, n_tab entries (kblock << 16 | N),
+  // longest-first so the first MMA (N = max) initialises every used column.
+  const uint32_t* kb_tab;
+  int32_t n_tab, b_box, pairs;
 };
 
 NNAB_DEV uint64_t make_sdesc(const void* p, int swz_bytes) {
@@ -132,7 +136,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int nt = p.n_tiles, kb_n = p.kblocks;
+  const int nt = p.n_tiles;
+  const int n_iter = p.kb_tab ? p.n_tab : p.kblocks;
+  const uint32_t stage_tx = (uint32_t)(C::A_BYTES + p.b_box * C::BK * 4) * (kSplit ? 2 : 1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -142,10 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       for (int mt = blockIdx.x; mt < p.n_mtiles; mt += gridDim.x) {
         for (int n = 0; n < nt; ++n) {
-          for (int kb = 0; kb < kb_n; ++kb) {
+          for (int it = 0; it < n_iter; ++it) {
+            const int kb = p.kb_tab ? (int)(__ldg(p.kb_tab + n * p.n_tab + it) >> 16) : it;
             mbar_wait(&empty[s], ph ^ 1);
             uint8_t* st = smem + s * C::STAGE_BYTES;
-            mbar_expect_tx(&full[s], C::STAGE_BYTES);
+            mbar_expect_tx(&full[s], stage_tx);
             const int k = kb * C::BK;
             const int a_col = k % p.row_len;
             const int a_row = mt * kBM + k / p.row_len;
@@ -164,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
-      constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
+      constexpr uint32_t idesc_full = idesc_tf32(kBM, kBN);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -174,7 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&tmem_empty[acc], aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem_base + acc * C::ACC_STRIDE;
-          for (int kb = 0; kb < kb_n; ++kb) {
+          for (int kb = 0; kb < n_iter; ++kb) {
+            uint32_t idesc = idesc_full;
+            if (p.kb_tab) idesc = idesc_tf32(kBM, __ldg(p.kb_tab + n * p.n_tab + kb) & 0xffffu);
             mbar_wait(&full[s], ph);
             tc_fence_after();
             uint8_t* st = smem + s * C::STAGE_BYTES;
@@ -218,6 +227,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tmem_full[acc], aph);
         tc_fence_after();
         const uint32_t tb = tmem_base + ((q * 32) << 16) + acc * C::ACC_STRIDE;
+        if (p.pairs) {
+          // columns (2j, 2j+1) = (re, im) of bin 128n + j; complex value re + i*im
+          const int bins_here = min(128, F - n * 128);
+          const int nc = (2 * bins_here + 31) / 32;
+#pragma unroll 1
+          for (int c = 0; c < nc; ++c) {
+            float v[32];
+            tmem_ld32(tb + c * 32, v);
+            if (kSplit) {
+              float cv[32];
+              tmem_ld32(tb + kBN + c * 32, cv);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += cv[j];
+            } else {
+              tmem_ld_wait();
+            }
+            if (valid) {
+              const int bin0 = n * 128 + c * 16;
+              const int64_t ob = b * (int64_t)F;
+              if (kind == NNAB_OUT_COMPLEX) {
+                float2* o = reinterpret_cast<float2*>(p.out);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (bin0 + j < F) o[(ob + bin0 + j) * p.T + t] = make_float2(v[2 * j], v[2 * j + 1]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (bin0 + j < F) p.out[(ob + bin0 + j) * p.T + t] = finish(v[2 * j], v[2 * j + 1], kind, p.power, p.eps);
+              }
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&tmem_empty[acc]);
+          if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
+          continue;
+        }
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           float re[32], im[32];
@@ -315,9 +361,11 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   const uint64_t rows_total = (uint64_t)g.B * g.R;
   const uint64_t bank_rows = (uint64_t)a.n_tiles * kBN;
   int rc = make_tmap_2d(&ta_hi, a.a_hi, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
-  if (!rc) rc = make_tmap_2d(&tb_hi, a.b_hi, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, kBN, C::SWZ);
+  const int b_box = a.b_box > 0 ? a.b_box : kBN;
+  if (b_box % 16 != 0 || b_box > kBN) return NNAB_EINVAL;
+  if (!rc) rc = make_tmap_2d(&tb_hi, a.b_hi, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, b_box, C::SWZ);
   if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, a.a_lo, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
-  if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, a.b_lo, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, kBN, C::SWZ);
+  if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, a.b_lo, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, b_box, C::SWZ);
   if (rc) return rc;
   if (!kSplit) {
     ta_lo = ta_hi;
@@ -341,6 +389,11 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.mel_ld = a.mel_ld;
   p.mel_band = a.mel_band;
   p.out = a.out;
+  p.kb_tab = a.kb_tab;
+  p.n_tab = a.n_tab;
+  p.b_box = b_box;
+  p.pairs = a.pairs;
+  if (a.kb_tab && (a.n_tab < 1 || mel)) return NNAB_EINVAL;
   if (p.n_mtiles == 0) return NNAB_OK;
   const int stages = mel ? 3 : 4;
   const size_t smem = 1024 + (size_t)stages * C::STAGE_BYTES + (mel ? kMelRows * kBM * 4 : 0) + 128;

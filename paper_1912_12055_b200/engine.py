@@ -205,3 +205,158 @@ class DftEngine:
             L.ptr(self.mel_band) if mel else None, out_host.data_ptr(), int(chunk_clips), ws.data_ptr(),
             ws.numel(), L.stream_handle(self.device)), "stft_forward_host")
         return out_host
+
+
+def _row_support(k_re: np.ndarray, k_im: np.ndarray) -> np.ndarray:
+    """[begin, end) of the non-zero columns of each complex row (int32 pairs)."""
+    nz = (k_re != 0) | (k_im != 0)
+    sup = np.zeros((k_re.shape[0], 2), dtype=np.int32)
+    for r in range(k_re.shape[0]):
+        idx = np.flatnonzero(nz[r])
+        if idx.size:
+            sup[r] = (idx[0], idx[-1] + 1)
+    return sup
+
+
+class CqtLongEngine:
+    """CQT1992v2's long complex bank (kernels.py:361-402) on the tcgen05 GEMM
+    with the longest-first per-K-block schedule (csrc/cqt1992.cu)."""
+
+    def __init__(self, kernels, hop: int, pad_mode: str = "reflect", precision: str = "tf32", device="cuda",
+                 dense: bool = False):
+        self.device = _require_cuda(device)
+        if precision not in L.PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
+        self.precision = L.PRECISIONS[precision]
+        k = np.asarray(kernels)
+        self.n_bins, self.width = int(k.shape[0]), int(k.shape[1])
+        self.hop, self.pad_mode = int(hop), pad_mode
+        if self.hop < 1:
+            raise ValueError(f"stride must be >= 1, got {hop}")
+        self._ws = _Workspace()
+        self.set_bank(k.real, k.imag, dense=dense)
+
+    def set_bank(self, k_re, k_im, dense: bool = False) -> None:
+        lib = L.load()
+        kr = np.ascontiguousarray(np.asarray(k_re, dtype=np.float32)) if not torch.is_tensor(k_re) else None
+        ki = np.ascontiguousarray(np.asarray(k_im, dtype=np.float32)) if not torch.is_tensor(k_im) else None
+        if dense or kr is None:
+            sup = np.tile(np.array([0, self.width], dtype=np.int32), (self.n_bins, 1))
+        else:
+            sup = _row_support(kr, ki)
+        cap = lib.nnab_cqt_bank_tiles(self.n_bins) * (((self.width + 31) // 32 * 32) // 16) + 16
+        tab = np.zeros(cap, dtype=np.uint32)
+        n_ent = C.c_int32()
+        L.check(lib.nnab_cqt_schedule(sup.ctypes.data, self.n_bins, self.width, self.precision, tab.ctypes.data,
+                                      C.byref(n_ent)), "cqt_schedule")
+        self.n_entries = n_ent.value
+        tiles = lib.nnab_cqt_bank_tiles(self.n_bins)
+        self.schedule = torch.from_numpy(tab[: tiles * self.n_entries].astype(np.int32)).to(self.device)
+        dr = torch.as_tensor(k_re).to(self.device, torch.float32).contiguous()
+        di = torch.as_tensor(k_im).to(self.device, torch.float32).contiguous()
+        n = lib.nnab_cqt_bank_bytes(self.n_bins, self.width) // 4
+        self.packed_hi = torch.empty(n, dtype=torch.float32, device=self.device)
+        self.packed_lo = (torch.empty(n, dtype=torch.float32, device=self.device)
+                          if self.precision == L.PREC_3XTF32 else None)
+        L.check(lib.nnab_pack_cqt_bank(dr.data_ptr(), di.data_ptr(), self.n_bins, self.width, self.precision,
+                                       self.packed_hi.data_ptr(), L.ptr(self.packed_lo),
+                                       L.stream_handle(self.device)), "pack_cqt_bank")
+
+    def frames(self, B: int, length: int) -> L.nnab_frames:
+        return frames_struct(B, length, self.width, self.hop, self.width // 2, self.pad_mode)
+
+    def n_frames(self, length: int) -> int:
+        return geometry(length, self.width, self.hop, self.width // 2, self.pad_mode)[0]
+
+    def forward(self, x: torch.Tensor, kind: str = "magnitude", eps: float = 1e-12) -> torch.Tensor:
+        lib = L.load()
+        if x.dim() == 1:
+            x = x[None]
+        if x.device != self.device:
+            raise ValueError(f"input on {x.device}, engine on {self.device}")
+        x = x.to(torch.float32).contiguous()
+        B, length = int(x.shape[0]), int(x.shape[1])
+        T = self.n_frames(length)
+        kinds = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX,
+                 "smooth": L.OUT_SMOOTH_MAG}
+        if kind not in kinds:
+            raise ValueError(f"output must be one of {sorted(kinds)}, got {kind!r}")
+        dt = torch.complex64 if kind == "complex" else torch.float32
+        out = torch.empty(B, self.n_bins, T, dtype=dt, device=self.device)
+        if B == 0:
+            return out
+        f = self.frames(B, length)
+        need = lib.nnab_stft_workspace_bytes(C.byref(f), self.precision)
+        ws = self._ws.get(need, self.device)
+        L.check(lib.nnab_cqt1992v2_forward(C.byref(f), x.data_ptr(), self.packed_hi.data_ptr(),
+                                           L.ptr(self.packed_lo), self.n_bins, self.schedule.data_ptr(),
+                                           self.n_entries, self.precision, kinds[kind], float(eps), out.data_ptr(),
+                                           ws.data_ptr(), ws.numel(), L.stream_handle(self.device)),
+                "cqt1992v2_forward")
+        return out
+
+
+class Cqt2010Engine:
+    """CQT2010v2's octave recursion (transforms.py:241-323): FIR halvings and
+    per-octave short complex convs, all on the device (csrc/cqt2010.cu)."""
+
+    def __init__(self, taps: np.ndarray, top_kernels: np.ndarray, early_stages: int, n_octaves: int,
+                 kernel_hop: int, first_bin: int, bins_per_octave: int, n_bins: int, pad_mode: str = "reflect",
+                 device="cuda"):
+        self.device = _require_cuda(device)
+        self.taps = np.ascontiguousarray(np.asarray(taps, dtype=np.float32))
+        k = np.asarray(top_kernels)
+        self.k_re = torch.from_numpy(np.ascontiguousarray(k.real, dtype=np.float32)).to(self.device)
+        self.k_im = torch.from_numpy(np.ascontiguousarray(k.imag, dtype=np.float32)).to(self.device)
+        self.n_filters, self.width = int(k.shape[0]), int(k.shape[1])
+        self.early_stages, self.n_octaves = int(early_stages), int(n_octaves)
+        self.kernel_hop, self.first_bin = int(kernel_hop), int(first_bin)
+        self.bins_per_octave, self.n_bins = int(bins_per_octave), int(n_bins)
+        if pad_mode not in L.PAD_MODES:
+            raise ValueError(f"unknown pad mode {pad_mode!r}")
+        self.pad_mode = L.PAD_MODES[pad_mode]
+        self._ws = _Workspace()
+
+    def _call(self, x, B, length, kind, out):
+        lib = L.load()
+        kinds = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX}
+        if kind not in kinds:
+            raise ValueError(f"output must be one of {sorted(kinds)}, got {kind!r}")
+        need = lib.nnab_cqt2010v2_workspace_bytes(B, length, self.early_stages)
+        ws = self._ws.get(need, self.device) if B else None
+        T = C.c_int32()
+        rc = lib.nnab_cqt2010v2_forward(
+            None if x is None else x.data_ptr(), B, length, self.taps.ctypes.data, self.taps.size,
+            self.k_re.data_ptr(), self.k_im.data_ptr(), self.n_filters, self.width, self.early_stages,
+            self.n_octaves, self.kernel_hop, self.first_bin, self.bins_per_octave, self.n_bins, self.pad_mode,
+            kinds[kind], None if out is None else out.data_ptr(), C.byref(T), None if ws is None else ws.data_ptr(),
+            0 if ws is None else ws.numel(), L.stream_handle(self.device))
+        return rc, T.value
+
+    def n_frames(self, length: int) -> int:
+        lib = L.load()
+        T = C.c_int32()
+        dummy = torch.empty(1, device=self.device)
+        rc = lib.nnab_cqt2010v2_forward(dummy.data_ptr(), 0, length, self.taps.ctypes.data, self.taps.size,
+                                        self.k_re.data_ptr(), self.k_im.data_ptr(), self.n_filters, self.width,
+                                        self.early_stages, self.n_octaves, self.kernel_hop, self.first_bin,
+                                        self.bins_per_octave, self.n_bins, self.pad_mode, L.OUT_MAGNITUDE,
+                                        dummy.data_ptr(), C.byref(T), None, 0, L.stream_handle(self.device))
+        L.check(rc, "cqt2010v2_forward")
+        return T.value
+
+    def forward(self, x: torch.Tensor, kind: str = "magnitude") -> torch.Tensor:
+        if x.dim() == 1:
+            x = x[None]
+        if x.device != self.device:
+            raise ValueError(f"input on {x.device}, engine on {self.device}")
+        x = x.to(torch.float32).contiguous()
+        B, length = int(x.shape[0]), int(x.shape[1])
+        T = self.n_frames(length)
+        dt = torch.complex64 if kind == "complex" else torch.float32
+        out = torch.zeros(B, self.n_bins, T, dtype=dt, device=self.device)
+        if B == 0:
+            return out
+        rc, _ = self._call(x, B, length, kind, out)
+        L.check(rc, "cqt2010v2_forward")
+        return out

@@ -1,0 +1,89 @@
+"""GPU parity: CQT1992v2 (tcgen05 long-bank GEMM) and CQT2010v2 (device octave
+recursion) vs the reference's golden vectors and the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import spectro_oracle as O
+
+pytestmark = pytest.mark.gpu
+SR = 44100.0
+TOL = {"tf32": 1e-3, "fp32": 1e-5}
+
+
+def long_engine(cfg, precision, **kw):
+    from paper_1912_12055_b200.engine import CqtLongEngine
+    k, _ = O.cqt_time_bank(cfg)
+    return CqtLongEngine(k, cfg.hop_length, cfg.pad_mode, precision=precision, **kw)
+
+
+def rec_engine(cfg):
+    from paper_1912_12055_b200.engine import Cqt2010Engine
+    p = O.cqt2010_plan(cfg)
+    return Cqt2010Engine(p.taps, p.top_kernels, p.early_stages, p.n_octaves, p.kernel_hop, p.first_bin,
+                         cfg.bins_per_octave, cfg.n_bins, cfg.pad_mode)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_cqt1992v2_full_config_golden(golden, cuda_dev, precision):
+    eng = long_engine(O.CqtCfg(sr=SR), precision)
+    x = torch.from_numpy(golden["clips"]).to(cuda_dev)
+    got = eng.forward(x, "magnitude").cpu().numpy()
+    assert got.shape == (2, 84, 157)
+    for i in range(2):
+        err = O.peak_err(got[i], golden["cqt1992v2_full"][i])
+        assert err <= TOL[precision], (precision, i, err)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_cqt1992v2_small_complex_golden(golden, cuda_dev, precision):
+    cfg = O.CqtCfg(sr=22050.0, fmin=220.0, n_bins=24)
+    eng = long_engine(cfg, precision)
+    got = eng.forward(torch.from_numpy(golden["x22"].astype(np.float32)).to(cuda_dev), "complex")[0].cpu().numpy()
+    ref = golden["cqt1992v2_small_complex"]
+    assert got.shape == ref.shape
+    assert O.peak_err(got, ref) <= TOL[precision]
+
+
+def test_cqt1992v2_dense_schedule_matches_sparse(golden, cuda_dev):
+    cfg = O.CqtCfg(sr=SR)
+    a = long_engine(cfg, "fp32")
+    b = long_engine(cfg, "fp32", dense=True)
+    x = torch.from_numpy(golden["clips"]).to(cuda_dev)
+    assert O.peak_err(a.forward(x).cpu().numpy(), b.forward(x).cpu().numpy()) < 1e-5  # accumulation order only
+
+
+def test_cqt2010v2_full_config_golden(golden, cuda_dev):
+    eng = rec_engine(O.CqtCfg(sr=SR))
+    x = torch.from_numpy(golden["clips"]).to(cuda_dev)
+    got = eng.forward(x, "magnitude").cpu().numpy()
+    assert got.shape == (2, 84, 157)
+    for i in range(2):
+        err = O.peak_err(got[i], golden["cqt2010v2_full"][i])
+        assert err <= 1e-5, (i, err)
+
+
+@pytest.mark.parametrize("key,cfg", [
+    ("cqt2010v2_small", O.CqtCfg(sr=22050.0, fmin=55.0, n_bins=48, hop_length=256)),
+    ("cqt2010v2_ragged", O.CqtCfg(sr=22050.0, fmin=82.0, n_bins=50, hop_length=256)),
+    ("cqt2010v2_noearly", O.CqtCfg(sr=22050.0, fmin=55.0, n_bins=48, hop_length=256, early_downsample=False)),
+])
+def test_cqt2010v2_small_golden(golden, cuda_dev, key, cfg):
+    eng = rec_engine(cfg)
+    got = eng.forward(torch.from_numpy(golden["x22"].astype(np.float32)).to(cuda_dev))[0].cpu().numpy()
+    ref = golden[key]
+    assert got.shape == ref.shape
+    assert O.peak_err(got, ref) <= 1e-5
+
+
+def test_cqt2010v2_batch_matches_oracle(cuda_dev):
+    cfg = O.CqtCfg(sr=SR)
+    rng = np.random.default_rng(9)
+    x = (rng.standard_normal((5, 80000)) * 0.5).astype(np.float32)
+    plan = O.cqt2010_plan(cfg)
+    ref = O.map_clips(lambda c: O.cqt2010v2_clip(c.astype(np.float64), cfg, plan), x, threads=4)
+    got = rec_engine(cfg).forward(torch.from_numpy(x).to(cuda_dev)).cpu().numpy()
+    assert O.peak_err(got, ref) <= 1e-5
+    z = rec_engine(cfg).forward(torch.zeros(2, 80000, device=cuda_dev))
+    assert not z.any()
