@@ -102,6 +102,18 @@ int nnab_stft_forward(const nnab_frames* f, const float* x, const float* packed_
                       float eps, const float* mel_w, int32_t n_mels, int32_t mel_ld, const int32_t* mel_band,
                       float* out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The two phases of nnab_stft_forward, for callers that reuse staged frames
+ * (the backward pass re-reads them for the kernel gradient) or time the GEMM
+ * alone.  Stage: pad (np.pad index map, signal.py:151 / gradients.py:18-25)
+ * and lay the clips out as hop rows in `workspace`, TF32-rounded (3xTF32: hi
+ * and lo halves).  Staged forward: the tcgen05 GEMM + fused epilogue on them. */
+int nnab_stage_frames(const nnab_frames* f, const float* x, int32_t precision, void* workspace,
+                      size_t workspace_bytes, void* stream);
+int nnab_stft_forward_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo, int32_t n_bins,
+                             int32_t fold_nyquist, int32_t precision, int32_t out_kind, float power, float eps,
+                             const float* mel_w, int32_t n_mels, int32_t mel_ld, const int32_t* mel_band,
+                             float* out, const void* workspace, size_t workspace_bytes, void* stream);
+
 /* Host-buffer end-to-end variant (the call a CPU caller of the reference
  * makes): x_host and out_host are pinned host buffers; the batch is streamed
  * through the device in chunks so H2D, compute and D2H overlap.  All device
@@ -134,6 +146,11 @@ int nnab_cqt1992v2_forward(const nnab_frames* f, const float* x, const float* pa
                            int32_t n_bins, const uint32_t* schedule, int32_t n_entries, int32_t precision,
                            int32_t out_kind, float eps, float* out, void* workspace, size_t workspace_bytes,
                            void* stream);
+/* GEMM phase only, on frames already staged by nnab_stage_frames */
+int nnab_cqt1992v2_forward_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
+                                  int32_t n_bins, const uint32_t* schedule, int32_t n_entries, int32_t precision,
+                                  int32_t out_kind, float eps, float* out, const void* workspace,
+                                  size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------- CQT2010v2
  * Cqt2010v2.__call__ (transforms.py:290-313, 319-323): early_stages x

@@ -45,6 +45,11 @@ SIGNATURES = {
     "nnab_stft_workspace_bytes": (_sz, [_FR, _i32]),
     "nnab_stft_forward": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _i32, _i32, _i32, _f32, _f32, _fp, _i32, _i32, _ip,
                                     _fp, _vp, _sz, _vp]),
+    "nnab_stage_frames": (C.c_int, [_FR, _fp, _i32, _vp, _sz, _vp]),
+    "nnab_stft_forward_staged": (C.c_int, [_FR, _fp, _fp, _i32, _i32, _i32, _i32, _f32, _f32, _fp, _i32, _i32,
+                                           _ip, _fp, _vp, _sz, _vp]),
+    "nnab_cqt1992v2_forward_staged": (C.c_int, [_FR, _fp, _fp, _i32, _ip, _i32, _i32, _i32, _f32, _fp, _vp, _sz,
+                                                _vp]),
     "nnab_stft_host_scratch_bytes": (_sz, [_FR, _i32, _i32, _i64]),
     "nnab_stft_forward_host": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _i32, _i32, _i32, _f32, _f32, _fp, _i32, _i32,
                                          _ip, _fp, _i64, _vp, _sz, _vp]),

@@ -136,12 +136,47 @@ extern "C" int nnab_stft_forward(const nnab_frames* f, const float* x, const flo
   const int32_t tiles = nnab_dft_bank_tiles(n_bins, fold_nyquist);
   if ((rc = validate_kind(out_kind, n_bins, mel_w, n_mels, mel_ld, tiles))) return rc;
   if (g.B == 0) return NNAB_OK;
-  const size_t need = nnab_stft_workspace_bytes(f, precision);
-  if (!workspace || workspace_bytes < need) return NNAB_EINVAL;
-  cudaStream_t s = (cudaStream_t)stream;
+  if ((rc = nnab_stage_frames(f, x, precision, workspace, workspace_bytes, stream))) return rc;
+  return nnab_stft_forward_staged(f, packed_hi, packed_lo, n_bins, fold_nyquist, precision, out_kind, power, eps,
+                                  mel_w, n_mels, mel_ld, mel_band, out, workspace, workspace_bytes, stream);
+}
+
+extern "C" int nnab_stage_frames(const nnab_frames* f, const float* x, int32_t precision, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  FrameGeom g;
+  if ((rc = frame_geometry(f, &g))) return rc;
+  if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
+  if (g.B == 0) return NNAB_OK;
+  if (!x || !workspace || workspace_bytes < nnab_stft_workspace_bytes(f, precision)) return NNAB_EINVAL;
+  const int split = precision == NNAB_PREC_3XTF32;
   float* rows_hi = reinterpret_cast<float*>(workspace);
   float* rows_lo = split ? reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + stage_bytes(g)) : nullptr;
-  if ((rc = stage_frames(g, x, rows_hi, rows_lo, split, s))) return rc;
+  return stage_frames(g, x, rows_hi, rows_lo, split, (cudaStream_t)stream);
+}
+
+extern "C" int nnab_stft_forward_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
+                                        int32_t n_bins, int32_t fold_nyquist, int32_t precision, int32_t out_kind,
+                                        float power, float eps, const float* mel_w, int32_t n_mels, int32_t mel_ld,
+                                        const int32_t* mel_band, float* out, const void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  FrameGeom g;
+  if ((rc = frame_geometry(f, &g))) return rc;
+  if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
+  const int split = precision == NNAB_PREC_3XTF32;
+  if (!packed_hi || (split && !packed_lo) || !out || n_bins < 1) return NNAB_EINVAL;
+  if (fold_nyquist && n_bins < 2) return NNAB_EINVAL;
+  const int32_t tiles = nnab_dft_bank_tiles(n_bins, fold_nyquist);
+  if ((rc = validate_kind(out_kind, n_bins, mel_w, n_mels, mel_ld, tiles))) return rc;
+  if (g.B == 0) return NNAB_OK;
+  if (!workspace || workspace_bytes < nnab_stft_workspace_bytes(f, precision)) return NNAB_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const float* rows_hi = reinterpret_cast<const float*>(workspace);
+  const float* rows_lo =
+      split ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + stage_bytes(g)) : nullptr;
   StftGemmArgs a{};
   a.a_hi = rows_hi;
   a.a_lo = rows_lo;

@@ -110,12 +110,23 @@ extern "C" int nnab_cqt1992v2_forward(const nnab_frames* f, const float* x, cons
                                       const float* packed_lo, int32_t n_bins, const uint32_t* schedule,
                                       int32_t n_entries, int32_t precision, int32_t out_kind, float eps, float* out,
                                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (!x) return NNAB_EINVAL;
+  int rc = nnab_stage_frames(f, x, precision, workspace, workspace_bytes, stream);
+  if (rc) return rc;
+  return nnab_cqt1992v2_forward_staged(f, packed_hi, packed_lo, n_bins, schedule, n_entries, precision, out_kind,
+                                       eps, out, workspace, workspace_bytes, stream);
+}
+
+extern "C" int nnab_cqt1992v2_forward_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
+                                             int32_t n_bins, const uint32_t* schedule, int32_t n_entries,
+                                             int32_t precision, int32_t out_kind, float eps, float* out,
+                                             const void* workspace, size_t workspace_bytes, void* stream) {
   FrameGeom g;
   int rc = frame_geometry(f, &g);
   if (rc) return rc;
   if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
   const int split = precision == NNAB_PREC_3XTF32;
-  if (!x || !packed_hi || (split && !packed_lo) || !out || !schedule || n_entries < 1 || n_bins < 1)
+  if (!packed_hi || (split && !packed_lo) || !out || !schedule || n_entries < 1 || n_bins < 1)
     return NNAB_EINVAL;
   if (out_kind != NNAB_OUT_MAGNITUDE && out_kind != NNAB_OUT_POWER && out_kind != NNAB_OUT_COMPLEX &&
       out_kind != NNAB_OUT_SMOOTH_MAG)
@@ -124,9 +135,9 @@ extern "C" int nnab_cqt1992v2_forward(const nnab_frames* f, const float* x, cons
   const size_t need = nnab_stft_workspace_bytes(f, precision);
   if (!workspace || workspace_bytes < need) return NNAB_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  float* rows_hi = reinterpret_cast<float*>(workspace);
-  float* rows_lo = split ? reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + need / 2) : nullptr;
-  if ((rc = stage_frames(g, x, rows_hi, rows_lo, split, s))) return rc;
+  const float* rows_hi = reinterpret_cast<const float*>(workspace);
+  const float* rows_lo =
+      split ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + need / 2) : nullptr;
   StftGemmArgs a{};
   a.a_hi = rows_hi;
   a.a_lo = rows_lo;

@@ -145,6 +145,15 @@ class DftEngine:
                 out: torch.Tensor | None = None) -> torch.Tensor:
         """x (B, L) float32 on the engine's device -> (B, F, T) [complex64 for 'complex',
         (B, n_mels, T) for 'mel']."""
+        B, length = self.stage(x)
+        return self.run_staged(B, length, kind, eps, out)
+
+    _KINDS = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX,
+              "mel": L.OUT_MEL, "smooth": L.OUT_SMOOTH_MAG}
+
+    def stage(self, x: torch.Tensor):
+        """Pad + lay out x as hop rows in the engine workspace (nnab_stage_frames).
+        Returns (B, L); the staged frames stay valid until the next stage()."""
         lib = L.load()
         if x.dim() == 1:
             x = x[None]
@@ -154,33 +163,40 @@ class DftEngine:
         B, length = int(x.shape[0]), int(x.shape[1])
         if length < 1:
             raise ValueError("signal must be non-empty")
+        self.n_frames(length)  # reference ValueErrors before any launch
+        if B == 0:
+            return B, length
+        f = self.frames(B, length)
+        ws = self._ws.get(lib.nnab_stft_workspace_bytes(C.byref(f), self.precision), self.device)
+        L.check(lib.nnab_stage_frames(C.byref(f), x.data_ptr(), self.precision, ws.data_ptr(), ws.numel(),
+                                      L.stream_handle(self.device)), "stage_frames")
+        return B, length
+
+    def run_staged(self, B: int, length: int, kind: str = "magnitude", eps: float = 1e-12,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+        """The tcgen05 GEMM + fused epilogue on the frames staged by stage()."""
+        lib = L.load()
         T = self.n_frames(length)
-        kinds = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX,
-                 "mel": L.OUT_MEL, "smooth": L.OUT_SMOOTH_MAG}
-        if kind not in kinds:
-            raise ValueError(f"output must be one of {sorted(kinds)}, got {kind!r}")
-        k = kinds[kind]
+        if kind not in self._KINDS:
+            raise ValueError(f"output must be one of {sorted(self._KINDS)}, got {kind!r}")
+        k = self._KINDS[kind]
         if k == L.OUT_MEL and self.mel_w is None:
             raise ValueError("set_mel() first")
         if out is None:
-            if k == L.OUT_COMPLEX:
-                out = torch.empty(B, self.n_bins, T, dtype=torch.complex64, device=self.device)
-            elif k == L.OUT_MEL:
-                out = torch.empty(B, self.n_mels, T, dtype=torch.float32, device=self.device)
-            else:
-                out = torch.empty(B, self.n_bins, T, dtype=torch.float32, device=self.device)
+            rows = self.n_mels if k == L.OUT_MEL else self.n_bins
+            dt = torch.complex64 if k == L.OUT_COMPLEX else torch.float32
+            out = torch.empty(B, rows, T, dtype=dt, device=self.device)
         if B == 0:
             return out
         f = self.frames(B, length)
-        need = lib.nnab_stft_workspace_bytes(C.byref(f), self.precision)
-        ws = self._ws.get(need, self.device)
+        ws = self._ws.buf
         mel = k == L.OUT_MEL
-        L.check(lib.nnab_stft_forward(
-            C.byref(f), x.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins, self.fold,
+        L.check(lib.nnab_stft_forward_staged(
+            C.byref(f), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins, self.fold,
             self.precision, k, float(getattr(self, "power", 1.0)), float(eps),
             self.mel_w.data_ptr() if mel else None, self.n_mels if mel else 0, self.mel_ld if mel else 0,
             L.ptr(self.mel_band) if mel else None, out.data_ptr(), ws.data_ptr(), ws.numel(),
-            L.stream_handle(self.device)), "stft_forward")
+            L.stream_handle(self.device)), "stft_forward_staged")
         return out
 
     def forward_host(self, x_host: torch.Tensor, kind: str = "magnitude", chunk_clips: int = 128,
@@ -269,6 +285,10 @@ class CqtLongEngine:
         return geometry(length, self.width, self.hop, self.width // 2, self.pad_mode)[0]
 
     def forward(self, x: torch.Tensor, kind: str = "magnitude", eps: float = 1e-12) -> torch.Tensor:
+        B, length = self.stage(x)
+        return self.run_staged(B, length, kind, eps)
+
+    def stage(self, x: torch.Tensor):
         lib = L.load()
         if x.dim() == 1:
             x = x[None]
@@ -276,6 +296,16 @@ class CqtLongEngine:
             raise ValueError(f"input on {x.device}, engine on {self.device}")
         x = x.to(torch.float32).contiguous()
         B, length = int(x.shape[0]), int(x.shape[1])
+        self.n_frames(length)
+        if B:
+            f = self.frames(B, length)
+            ws = self._ws.get(lib.nnab_stft_workspace_bytes(C.byref(f), self.precision), self.device)
+            L.check(lib.nnab_stage_frames(C.byref(f), x.data_ptr(), self.precision, ws.data_ptr(), ws.numel(),
+                                          L.stream_handle(self.device)), "stage_frames")
+        return B, length
+
+    def run_staged(self, B: int, length: int, kind: str = "magnitude", eps: float = 1e-12) -> torch.Tensor:
+        lib = L.load()
         T = self.n_frames(length)
         kinds = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX,
                  "smooth": L.OUT_SMOOTH_MAG}
@@ -286,13 +316,12 @@ class CqtLongEngine:
         if B == 0:
             return out
         f = self.frames(B, length)
-        need = lib.nnab_stft_workspace_bytes(C.byref(f), self.precision)
-        ws = self._ws.get(need, self.device)
-        L.check(lib.nnab_cqt1992v2_forward(C.byref(f), x.data_ptr(), self.packed_hi.data_ptr(),
-                                           L.ptr(self.packed_lo), self.n_bins, self.schedule.data_ptr(),
-                                           self.n_entries, self.precision, kinds[kind], float(eps), out.data_ptr(),
-                                           ws.data_ptr(), ws.numel(), L.stream_handle(self.device)),
-                "cqt1992v2_forward")
+        ws = self._ws.buf
+        L.check(lib.nnab_cqt1992v2_forward_staged(C.byref(f), self.packed_hi.data_ptr(), L.ptr(self.packed_lo),
+                                                  self.n_bins, self.schedule.data_ptr(), self.n_entries,
+                                                  self.precision, kinds[kind], float(eps), out.data_ptr(),
+                                                  ws.data_ptr(), ws.numel(), L.stream_handle(self.device)),
+                "cqt1992v2_forward_staged")
         return out
 
 
