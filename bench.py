@@ -42,7 +42,36 @@ WORKLOADS = {
     "mel": "MelSpectrogram n_fft=2048 n_mels=128 hop=512 slaney norm=none power=1, fused (BASELINE config 2)",
     "cqt1992v2": "CQT1992v2 84 bins 12/oct fmin=32.70 hop=512, magnitude (BASELINE config 3)",
     "cqt2010v2": "CQT2010v2 84 bins 12/oct fmin=32.70 hop=512 early downsample, magnitude (BASELINE config 4)",
+    "train": "trainable STFT+Mel (trainable_mel + trainable_STFT, n_fft=2048 n_mels=128 hop=512) forward + "
+             "backward (dW, dS, dh) + NCCL kernel-grad all-reduce (BASELINE config 5)",
 }
+FLOP_TRAIN = FLOP_MEL + 2.0 * M_FRAMES * 2048 * 2050 + 2 * (2.0 * M_FRAMES * 1025 * 128)  # 4.886e12 (section 8d)
+
+
+class TrainStep:
+    """One optimisation step's compute for config 5: forward of the trainable
+    Mel layer, backward for the mel weights and both DFT banks, and (N > 1)
+    the single flattened gradient all-reduce."""
+
+    def __init__(self, device, precision, world):
+        import torch
+        from paper_1912_12055_b200.layers import MelSpectrogram
+        self.m = MelSpectrogram(sr=SR, n_fft=2048, n_mels=128, hop_length=512, trainable_mel=True,
+                                trainable_STFT=True, precision=precision, device=device)
+        self.world = world
+        gen = torch.Generator(device=device)
+        gen.manual_seed(77)
+        self.g = torch.randn(B_CLIPS, 128, T_FRAMES, device=device, generator=gen) * 1e-3
+
+    def forward(self, x, kind=None):
+        from paper_1912_12055_b200.dist import allreduce_grads
+        for p in self.m.parameters():
+            p.grad = None
+        out = self.m(x)
+        out.backward(self.g)
+        if self.world > 1:
+            allreduce_grads(list(self.m.parameters()))
+        return out
 
 
 def load_peaks():
@@ -137,6 +166,12 @@ def build_workload(name: str, device, precision: str):
         work = {"bound": "tensor", "per_batch": 4.0 * M_FRAMES * float(lens.sum()), "unit": "TFLOP/s",
                 "kernel": "stft_gemm_kernel"}
         return eng, "magnitude", work, 2
+    if name == "train":
+        import torch.distributed as dist
+        world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+        work = {"bound": "tensor", "per_batch": FLOP_TRAIN, "unit": "TFLOP/s",
+                "kernel": "train step (stft_gemm fwd + rgemm dW/dS/dK + glue)"}
+        return TrainStep(device, precision, world), None, work, 0
     if name == "cqt2010v2":
         cfg = CqtConfig(sr=SR)
         p = cqt2010_plan(cfg)
@@ -183,7 +218,15 @@ def cpu_reference(name: str, max_seconds: float, threads: int, min_clips: int | 
     W = O.mel_bank(SR, 2048, 128, formula="slaney")
     kern = O.cqt_time_bank(O.CqtCfg(sr=SR))[0] if name == "cqt1992v2" else None
     plan = O.cqt2010_plan(O.CqtCfg(sr=SR)) if name == "cqt2010v2" else None
+    def train_clip(c):  # joint trainable STFT + Mel layer: forward + vjp (gradients.py:61-129)
+        fr, re, im, S = O.smooth_mag_forward(c, h_re, h_im, 512)
+        g = np.ones((128, S.shape[1]))
+        dW = g @ S.T
+        dS = W.T @ g
+        return (dS * re / S) @ fr + (dS * im / S) @ fr + dW.sum()
+
     fn = {
+        "train": train_clip,
         "stft": lambda c: O.stft_clip(c, h_re, h_im, 512),
         "mel": lambda c: O.mel_clip(c, h_re, h_im, W, 512),
         "cqt1992v2": lambda c: O.cqt1992v2_clip(c, kern, 512),
@@ -275,8 +318,9 @@ def main():
                 "peak_source": (f"TF32 = bf16 burst / 2, bf16 {peak_src}" if work["bound"] == "tensor"
                                 else f"HBM copy {peak_src}")}
 
-    eng, kind, work, launches = build_workload(args.workload, device, args.precision)
-    staged = args.workload != "cqt2010v2"
+    from paper_1912_12055_b200 import _lib
+    eng, kind, work, _ = build_workload(args.workload, device, args.precision)
+    staged = args.workload not in ("cqt2010v2", "train")
 
     clocks = Clocks(local_rank)
     if world > 1:
@@ -284,7 +328,10 @@ def main():
     torch.cuda.synchronize()
     if rank == 0:
         clocks.start()
+    n0 = _lib.load().nnab_launch_count()
     ms, gemm_ms = run_timed(eng, kind, x, args.steps, args.warmup, torch, stream, time_gemm=staged)
+    launches_total = _lib.load().nnab_launch_count() - n0  # includes the W warm-up steps
+    launches = launches_total * args.steps // (args.steps + args.warmup)
     ck = clocks.stop() if rank == 0 else None
     if world > 1:
         t = torch.tensor([ms], device=device)
@@ -322,16 +369,51 @@ def main():
                "h2d_bytes_per_step": B_CLIPS * L_SAMPLES * 4, "d2h_bytes_per_step": B_CLIPS * out_rows * T_FRAMES * 4,
                "path": "nnab_stft_forward_host (C ABI, pinned host buffers, 15 chunks, 3-stream overlap)"}
         del xh, oh
+    elif args.workload == "train":
+        # pinned host batch -> device, fwd + bwd (+ all-reduce), kernel grads -> host, every step
+        xh = x.cpu().pin_memory()
+        params = list(eng.m.parameters())
+        gh = [torch.empty(p.shape, dtype=torch.float32, pin_memory=True) for p in params]
+        xd = torch.empty_like(x)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            eng.forward(xd)
+            for hbuf, p in zip(gh, params):
+                hbuf.copy_(p.grad, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        ks = max(3, min(5, args.steps))
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ks):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = e0.elapsed_time(e1) / ks
+        if world > 1:
+            t = torch.tensor([et], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        e2e = {"value": world * B_CLIPS / (et / 1e3), "unit": "spectrograms/s", "ms_per_step": et,
+               "h2d_bytes_per_step": B_CLIPS * L_SAMPLES * 4,
+               "d2h_bytes_per_step": int(sum(p.numel() for p in params) * 4),
+               "path": "layers.MelSpectrogram(trainable_mel, trainable_STFT) fwd+bwd, pinned H2D input, D2H grads"}
+        del xh, xd
 
     breakdown = {}
     if rank == 0 and world == 1 and not args.no_breakdown:
-        for name in ["stft", "mel", "cqt1992v2", "cqt2010v2"]:
+        for name in ["stft", "mel", "cqt1992v2", "cqt2010v2", "train"]:
             for prec in (["tf32", "fp32"] if name != "cqt2010v2" else ["fp32"]):
                 if name == args.workload and prec == args.precision:
                     continue
                 e, k, w, _ = build_workload(name, device, "tf32" if name == "cqt2010v2" else prec)
-                st = name != "cqt2010v2"
-                m, gm = run_timed(e, k, x, 20, 3, torch, stream, time_gemm=st)
+                st = name not in ("cqt2010v2", "train")
+                m, gm = run_timed(e, k, x, 20 if name != "train" else 5, 3, torch, stream, time_gemm=st)
                 r = roofline(w, m, gm if st else m)
                 breakdown[f"{name}_{prec}"] = {"ms_per_step": m, "value": B_CLIPS / (m / 1e3),
                                                "roofline_frac": r["frac"], "achieved": r["achieved"],
@@ -361,7 +443,7 @@ def main():
             "roofline": rf,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches * args.steps,
+            "gpu_launches": launches,
             "clocks": ck,
             "transforms": breakdown or None,
         }

@@ -68,6 +68,8 @@ int nnab_version(void);
 const char* nnab_strerror(int code);
 /* last CUDA error string recorded by a failing call on this thread */
 const char* nnab_last_error(void);
+/* kernels this library has launched in the process (all threads) */
+uint64_t nnab_launch_count(void);
 /* number of frames T and the staging layout for a problem; NNAB_EINVAL for
  * the reference's ValueError cases. */
 int nnab_frames_geometry(const nnab_frames* f, int32_t* n_frames, int32_t* row_len, int32_t* rows_per_clip);
@@ -125,6 +127,47 @@ int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const floa
                            int32_t out_kind, float power, float eps, const float* mel_w, int32_t n_mels,
                            int32_t mel_ld, const int32_t* mel_band, float* out_host, int64_t chunk_clips,
                            void* device_scratch, size_t scratch_bytes, void* stream);
+
+/* ------------------------------------------------------- trainable layers
+ * TrainableLayer / spectrogram_vjp (gradients.py:28-149) on the device.
+ * Frame slots: clip b, frame t -> slot b*R + t (R = rows per clip from
+ * nnab_frames_geometry); slot-major arrays are [rows][ld], ld = nnab_slots_ld. */
+int64_t nnab_slots_ld(const nnab_frames* f);
+/* Training forward on staged frames: out = smoothed magnitude sqrt(re^2+im^2+eps)
+ * (NNAB_OUT_SMOOTH_MAG, gradients.py:61-67) or W @ that (NNAB_OUT_MEL,
+ * gradients.py:69-80); also stores re, im and (if save_mag) S, slot-major. */
+int nnab_stft_forward_train_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
+                                   int32_t n_bins, int32_t fold_nyquist, int32_t precision, int32_t out_kind,
+                                   float power, float eps, const float* mel_w, int32_t n_mels, int32_t mel_ld,
+                                   const int32_t* mel_band, float* out, float* save_re, float* save_im,
+                                   float* save_mag, int64_t ld, const void* workspace, size_t workspace_bytes,
+                                   void* stream);
+/* (B, rows, T) -> slot-major [rows][ld], zero on non-frame slots */
+int nnab_grad_to_slots(const float* g_brt, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld, float* out,
+                       void* stream);
+/* coef = dS*re/S (rows 0..F-1) and dS*im/S (rows F..2F-1), gradients.py:127-128;
+ * dS from ds_slots ([F][ld]) or g_bft ((B, F, T)); TF32 hi (+ lo residual). */
+int nnab_dft_coef(const float* ds_slots, const float* g_bft, const float* re_s, const float* im_s, int32_t F,
+                  int64_t B, int32_t T, int32_t R, int64_t ld, float eps, int32_t precision, float* coef_hi,
+                  float* coef_lo, void* stream);
+/* dst[c][r] = src[r][c] zero-padded to ld rows, TF32 hi (+ lo) */
+int nnab_transpose_pad(const float* src, int32_t rows, int32_t cols, int32_t ld, int32_t precision, float* hi,
+                       float* lo, void* stream);
+int nnab_tf32_split(const float* src, int64_t n, int32_t precision, float* hi, float* lo, void* stream);
+/* C[M][N] = sum_k A[M][k] B(k, N) on tcgen05; B K-major (b_mn = 0: row n at
+ * b + n*ldb) or MN-major ((k, n) at rows[k + n/b_row_len][n % b_row_len]);
+ * split-K partials (deterministic fixed-order sum) in `partial`. */
+size_t nnab_rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits);
+int nnab_rgemm(int32_t M, int32_t N, int64_t K, const float* a_hi, const float* a_lo, int64_t lda, const float* b_hi,
+               const float* b_lo, int64_t ldb, int32_t b_mn, int32_t b_row_len, int64_t b_rows, float* c,
+               int64_t ldc, int32_t splits, float* partial, int32_t precision, void* stream);
+/* dK = coef @ frames (gradients.py:129) with the frames read from the staged rows */
+int nnab_kernel_grad(const nnab_frames* f, const float* coef_hi, const float* coef_lo, int32_t rows, int64_t ld,
+                     int32_t precision, float* dk, int64_t ldk, const void* workspace, size_t workspace_bytes,
+                     float* partial, int32_t splits, void* stream);
+/* dx: overlap-add of frame grads ([tap][ld] = h^T @ coef) folded through the
+ * pad index map (gradients.py:133-149); deterministic gather, (B, L) out. */
+int nnab_input_grad(const nnab_frames* f, const float* frame_grads_t, int64_t ld, float* gx, void* stream);
 
 /* ------------------------------------------------------- CQT1992v2
  * Cqt1992v2.__call__ (transforms.py:201-208 via _complex_conv 175-186) and

@@ -38,6 +38,7 @@ SIGNATURES = {
     "nnab_version": (C.c_int, []),
     "nnab_strerror": (C.c_char_p, [C.c_int]),
     "nnab_last_error": (C.c_char_p, []),
+    "nnab_launch_count": (C.c_uint64, []),
     "nnab_frames_geometry": (C.c_int, [_FR, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "nnab_dft_bank_tiles": (C.c_int, [_i32, _i32]),
     "nnab_dft_bank_bytes": (_sz, [_i32, _i32, _i32]),
@@ -53,6 +54,18 @@ SIGNATURES = {
     "nnab_stft_host_scratch_bytes": (_sz, [_FR, _i32, _i32, _i64]),
     "nnab_stft_forward_host": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _i32, _i32, _i32, _f32, _f32, _fp, _i32, _i32,
                                          _ip, _fp, _i64, _vp, _sz, _vp]),
+    "nnab_slots_ld": (_i64, [_FR]),
+    "nnab_stft_forward_train_staged": (C.c_int, [_FR, _fp, _fp, _i32, _i32, _i32, _i32, _f32, _f32, _fp, _i32, _i32,
+                                                 _ip, _fp, _fp, _fp, _fp, _i64, _vp, _sz, _vp]),
+    "nnab_grad_to_slots": (C.c_int, [_fp, _i64, _i32, _i32, _i32, _i64, _fp, _vp]),
+    "nnab_dft_coef": (C.c_int, [_fp, _fp, _fp, _fp, _i32, _i64, _i32, _i32, _i64, _f32, _i32, _fp, _fp, _vp]),
+    "nnab_transpose_pad": (C.c_int, [_fp, _i32, _i32, _i32, _i32, _fp, _fp, _vp]),
+    "nnab_tf32_split": (C.c_int, [_fp, _i64, _i32, _fp, _fp, _vp]),
+    "nnab_rgemm_partial_bytes": (_sz, [_i32, _i32, _i64, _i32]),
+    "nnab_rgemm": (C.c_int, [_i32, _i32, _i64, _fp, _fp, _i64, _fp, _fp, _i64, _i32, _i32, _i64, _fp, _i64, _i32,
+                             _fp, _i32, _vp]),
+    "nnab_kernel_grad": (C.c_int, [_FR, _fp, _fp, _i32, _i64, _i32, _fp, _i64, _vp, _sz, _fp, _i32, _vp]),
+    "nnab_input_grad": (C.c_int, [_FR, _fp, _i64, _fp, _vp]),
     "nnab_cqt_bank_tiles": (C.c_int, [_i32]),
     "nnab_cqt_bank_bytes": (_sz, [_i32, _i32]),
     "nnab_pack_cqt_bank": (C.c_int, [_fp, _fp, _i32, _i32, _i32, _fp, _fp, _vp]),

@@ -1,0 +1,194 @@
+"""Trainable spectrogram layers: forward/backward through the sm_100a kernels.
+
+`DftLayerOp` is the device counterpart of the reference's TrainableLayer +
+spectrogram_vjp (gradients.py:28-149) over a whole batch of clips:
+
+  forward   S = sqrt(re^2 + im^2 + eps)           (conv layer, gradients.py:61-67)
+            mel = W @ S                           (mel layer,  gradients.py:69-80)
+  backward  dW  = g @ S^T                         (gradients.py:118-121)
+            dS  = W^T g          (joint mel + trainable STFT, nnAudio trainable_STFT)
+            dh  = (dS*re/S, dS*im/S) @ frames     (gradients.py:125-129)
+            dx  = overlap-add(coef^T @ h) folded through the pad map (gradients.py:133-149)
+
+Every product is a tcgen05 GEMM (stft_gemm / rgemm); kernel gradients are
+summed over all clips of the batch in one reduction (the batch-mean is the
+caller's choice of upstream scaling).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib as L
+from .engine import DftEngine
+
+
+def _f32(n_rows: int, n_cols: int, device) -> torch.Tensor:
+    return torch.empty(n_rows, n_cols, dtype=torch.float32, device=device)
+
+
+class DftLayerOp:
+    """Batched forward/backward for a DFT-type bank (STFT or time-domain CQT
+    rows) with an optional Mel projection on top."""
+
+    def __init__(self, h_re, h_im, hop: int, center: bool = True, pad_mode: str = "reflect", eps: float = 1e-12,
+                 precision: str = "tf32", device="cuda"):
+        # trainable sine rows may leave zero -> never fold the Nyquist bin
+        self.engine = DftEngine(h_re, h_im, hop, center, pad_mode, precision=precision, device=device,
+                                allow_fold=False)
+        self.eps = float(eps)
+        self.device = self.engine.device
+        self.prec = self.engine.precision
+        self.split = self.prec == L.PREC_3XTF32
+
+    @property
+    def n_bins(self):
+        return self.engine.n_bins
+
+    def set_bank(self, h_re: torch.Tensor, h_im: torch.Tensor):
+        self.engine.set_bank(h_re.detach(), h_im.detach())
+
+    # ------------------------------------------------------------ forward
+    def forward(self, x: torch.Tensor, mel_w: torch.Tensor | None = None):
+        """x (B, L) -> (S (B, F, T) or mel (B, n_mels, T), saved state)."""
+        lib, eng = L.load(), self.engine
+        if x.dim() == 1:
+            x = x[None]
+        x = x.detach().to(self.device, torch.float32).contiguous()
+        B, length = int(x.shape[0]), int(x.shape[1])
+        T = eng.n_frames(length)
+        f = eng.frames(B, length)
+        ws = torch.empty(lib.nnab_stft_workspace_bytes(C.byref(f), self.prec), dtype=torch.uint8, device=self.device)
+        stream = L.stream_handle(self.device)
+        L.check(lib.nnab_stage_frames(C.byref(f), x.data_ptr(), self.prec, ws.data_ptr(), ws.numel(), stream),
+                "stage_frames")
+        ld = lib.nnab_slots_ld(C.byref(f))
+        F = self.n_bins
+        re_s, im_s = _f32(F, ld, self.device), _f32(F, ld, self.device)
+        mag_s = _f32(F, ld, self.device) if mel_w is not None else None
+        if mel_w is not None:
+            eng.set_mel(mel_w.detach(), power=1.0, banded=False)
+            out = torch.empty(B, eng.n_mels, T, device=self.device)
+            kind, mw, nm, mld = L.OUT_MEL, eng.mel_w.data_ptr(), eng.n_mels, eng.mel_ld
+        else:
+            out = torch.empty(B, F, T, device=self.device)
+            kind, mw, nm, mld = L.OUT_SMOOTH_MAG, None, 0, 0
+        L.check(lib.nnab_stft_forward_train_staged(
+            C.byref(f), eng.packed_hi.data_ptr(), L.ptr(eng.packed_lo), F, eng.fold, self.prec, kind, 1.0, self.eps,
+            mw, nm, mld, None, out.data_ptr(), re_s.data_ptr(), im_s.data_ptr(), L.ptr(mag_s), ld, ws.data_ptr(),
+            ws.numel(), stream), "stft_forward_train")
+        saved = {"ws": ws, "re": re_s, "im": im_s, "mag": mag_s, "B": B, "L": length, "T": T, "ld": ld,
+                 "R": self._rows_per_clip(length)}
+        return out, saved
+
+    def _rows_per_clip(self, length):
+        from .engine import geometry
+        pad = self.engine.n_fft // 2 if self.engine.center else 0
+        return geometry(length, self.engine.n_fft, self.engine.hop, pad, self.engine.pad_mode)[2]
+
+    # ------------------------------------------------------------ helpers
+    def _split(self, t: torch.Tensor):
+        lib = L.load()
+        hi = torch.empty_like(t)
+        lo = torch.empty_like(t) if self.split else None
+        L.check(lib.nnab_tf32_split(t.data_ptr(), t.numel(), self.prec, hi.data_ptr(), L.ptr(lo),
+                                    L.stream_handle(self.device)), "tf32_split")
+        return hi, lo
+
+    def _rgemm(self, M, N, K, a, lda, b, ldb, b_mn, b_row_len, b_rows, c, ldc, splits=0):
+        lib = L.load()
+        part_bytes = lib.nnab_rgemm_partial_bytes(M, N, K, splits)
+        part = torch.empty(max(part_bytes // 4, 1), dtype=torch.float32, device=self.device)
+        L.check(lib.nnab_rgemm(M, N, K, a[0].data_ptr(), L.ptr(a[1]), lda, b[0].data_ptr(), L.ptr(b[1]), ldb, b_mn,
+                               b_row_len, b_rows, c.data_ptr(), ldc, splits, part.data_ptr(), self.prec,
+                               L.stream_handle(self.device)), "rgemm")
+
+    # ------------------------------------------------------------ backward
+    def backward(self, saved: dict, g: torch.Tensor, h_re=None, h_im=None, mel_w: torch.Tensor | None = None,
+                 need_bank: bool = True, need_mel: bool = False, need_x: bool = False):
+        """g: upstream grad of the forward output.  Returns dict with any of
+        'h_re', 'h_im' (F, n_fft), 'weights' (n_mels, F), 'x' (B, L)."""
+        lib, eng = L.load(), self.engine
+        stream = L.stream_handle(self.device)
+        g = g.detach().to(self.device, torch.float32).contiguous()
+        B, T, ld, R, length = saved["B"], saved["T"], saved["ld"], saved["R"], saved["L"]
+        F, n_fft = self.n_bins, eng.n_fft
+        f = eng.frames(B, length)
+        grads = {}
+        ds = None
+        if mel_w is not None:
+            nm = int(mel_w.shape[0])
+            gs = _f32(nm, ld, self.device)
+            L.check(lib.nnab_grad_to_slots(g.data_ptr(), B, nm, T, R, ld, gs.data_ptr(), stream), "grad_to_slots")
+            gsp = self._split(gs)
+            if need_mel:  # dW[m][f] = sum_slot g[m][slot] S[f][slot]
+                mag = saved["mag"]
+                magp = self._split(mag) if self.split else (mag, None)
+                dW = torch.empty(nm, F, device=self.device)
+                self._rgemm(nm, F, ld, gsp, ld, magp, ld, 0, 0, 0, dW, F)
+                grads["weights"] = dW
+            if need_bank or need_x:  # dS[f][slot] = sum_m W[m][f] g[m][slot]
+                kp = (nm + 31) // 32 * 32
+                wt_hi = _f32(F, kp, self.device)
+                wt_lo = _f32(F, kp, self.device) if self.split else None
+                L.check(lib.nnab_transpose_pad(mel_w.detach().float().contiguous().data_ptr(), nm, F, kp, self.prec,
+                                               wt_hi.data_ptr(), L.ptr(wt_lo), stream), "transpose_pad")
+                ds = _f32(F, ld, self.device)
+                self._rgemm(F, ld, kp, (wt_hi, wt_lo), kp, gsp, ld, 1, ld, nm, ds, ld)
+        if not (need_bank or need_x):
+            return grads
+        coef_hi = _f32(2 * F, ld, self.device)
+        coef_lo = _f32(2 * F, ld, self.device) if self.split else None
+        L.check(lib.nnab_dft_coef(L.ptr(ds), None if ds is not None else g.data_ptr(), saved["re"].data_ptr(),
+                                  saved["im"].data_ptr(), F, B, T, R, ld, self.eps, self.prec, coef_hi.data_ptr(),
+                                  L.ptr(coef_lo), stream), "dft_coef")
+        ws = saved["ws"]
+        if need_bank:
+            dk = _f32(2 * F, n_fft, self.device)
+            part = torch.empty(max(lib.nnab_rgemm_partial_bytes(2 * F, n_fft, ld, 0) // 4, 1), device=self.device)
+            L.check(lib.nnab_kernel_grad(C.byref(f), coef_hi.data_ptr(), L.ptr(coef_lo), 2 * F, ld, self.prec,
+                                         dk.data_ptr(), n_fft, ws.data_ptr(), ws.numel(), part.data_ptr(), 0, stream),
+                    "kernel_grad")
+            grads["h_re"], grads["h_im"] = dk[:F], dk[F:]
+        if need_x:  # frame grads^T [tap][slot] = h^T @ coef, then overlap-add + pad fold
+            h = torch.cat([torch.as_tensor(h_re), torch.as_tensor(h_im)]).to(self.device, torch.float32).contiguous()
+            kp = (2 * F + 31) // 32 * 32
+            ht_hi = _f32(n_fft, kp, self.device)
+            ht_lo = _f32(n_fft, kp, self.device) if self.split else None
+            L.check(lib.nnab_transpose_pad(h.data_ptr(), 2 * F, n_fft, kp, self.prec, ht_hi.data_ptr(),
+                                           L.ptr(ht_lo), stream), "transpose_pad")
+            fgt = _f32(n_fft, ld, self.device)
+            self._rgemm(n_fft, ld, kp, (ht_hi, ht_lo), kp, (coef_hi, coef_lo), ld, 1, ld, 2 * F, fgt, ld)
+            gx = torch.empty(B, length, device=self.device)
+            L.check(lib.nnab_input_grad(C.byref(f), fgt.data_ptr(), ld, gx.data_ptr(), stream), "input_grad")
+            grads["x"] = gx
+        return grads
+
+
+class DftLayerFunction(torch.autograd.Function):
+    """autograd wrapper: out = layer(x; h_re, h_im[, W])."""
+
+    @staticmethod
+    def forward(ctx, x, h_re, h_im, mel_w, op: DftLayerOp, bank_version: int):
+        if op._bank_version != bank_version:
+            op.set_bank(h_re, h_im)
+            op._bank_version = bank_version
+        out, saved = op.forward(x, mel_w)
+        ctx.op, ctx.saved = op, saved
+        ctx.save_for_backward(h_re, h_im, mel_w if mel_w is not None else torch.empty(0))
+        ctx.has_mel = mel_w is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        h_re, h_im, mel_w = ctx.saved_tensors
+        need_x, need_bank = ctx.needs_input_grad[0], ctx.needs_input_grad[1] or ctx.needs_input_grad[2]
+        need_mel = ctx.has_mel and ctx.needs_input_grad[3]
+        if need_x and ctx.has_mel:
+            raise NotImplementedError("input gradients are only provided for convolution layers")  # gradients.py:122-123
+        gr = ctx.op.backward(ctx.saved, g, h_re, h_im, mel_w if ctx.has_mel else None, need_bank=need_bank,
+                             need_mel=need_mel, need_x=need_x)
+        ctx.saved = None
+        return (gr.get("x"), gr.get("h_re"), gr.get("h_im"), gr.get("weights") if ctx.has_mel else None, None, None)

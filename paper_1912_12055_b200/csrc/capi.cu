@@ -2,6 +2,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -11,6 +12,9 @@
 namespace nnab {
 
 static thread_local char g_last_error[256] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int cuda_fail(cudaError_t e, const char* where) {
   std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
@@ -43,7 +47,9 @@ int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t ou
   cuuint64_t strides[1] = {row_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+  // -128: 32-byte atoms swizzled within 128 B (the MN-major TF32 UMMA layout)
+  CUtensorMapSwizzle sw = swizzle_bytes == -128 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                          : swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                           : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                           : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                 : CU_TENSOR_MAP_SWIZZLE_NONE;
@@ -103,6 +109,8 @@ extern "C" const char* nnab_strerror(int code) {
 }
 
 extern "C" const char* nnab_last_error(void) { return g_last_error; }
+
+extern "C" uint64_t nnab_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" size_t nnab_stft_workspace_bytes(const nnab_frames* f, int32_t precision) {
   FrameGeom g;

@@ -58,7 +58,7 @@ extern "C" int nnab_pack_cqt_bank(const float* k_re, const float* k_im, int32_t 
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8192);
   pack_cqt_bank_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(k_re, k_im, n_bins, width, k_pad, tiles, split,
                                                                  packed_hi, packed_lo);
-  NNAB_CUDA_TRY(cudaGetLastError());
+  NNAB_LAUNCHED();
   return NNAB_OK;
 }
 

@@ -188,7 +188,7 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
     dim3 grid((unsigned)((lo + kSegOut - 1) / kSegOut), (unsigned)B);
     const size_t smem = (size_t)(2 * (kSegOut - 1) + 2 * fp.half + 1) * sizeof(float);
     halve_kernel<<<grid, 256, smem, s>>>(cur, cur_len, buf[pp], lo, fp);
-    NNAB_CUDA_TRY(cudaGetLastError());
+    NNAB_LAUNCHED();
     cur = buf[pp];
     cur_len = lo;
     pp ^= 1;
@@ -206,7 +206,7 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 32);
     octave_conv_kernel<<<blocks, 256, 0, s>>>(cur, cur_len, k_re, k_im, n_filters, width, kernel_hop >> a, pad_mode,
                                              skip, row0, n_bins, T, out_kind, out, B);
-    NNAB_CUDA_TRY(cudaGetLastError());
+    NNAB_LAUNCHED();
   }
   return NNAB_OK;
 }

@@ -94,7 +94,7 @@ int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
   stage_rows_kernel<<<blocks, 256, 0, s>>>(x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.row_len, g.R, g.padded_len,
                                           split, rows_hi, rows_lo);
-  NNAB_CUDA_TRY(cudaGetLastError());
+  NNAB_LAUNCHED();
   return NNAB_OK;
 }
 
@@ -153,7 +153,7 @@ extern "C" int nnab_pack_dft_bank(const float* h_re, const float* h_im, int32_t 
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
   pack_dft_bank_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(h_re, h_im, n_bins, n_fft, k_pad, tiles,
                                                                  fold_nyquist, split, packed_hi, packed_lo);
-  NNAB_CUDA_TRY(cudaGetLastError());
+  NNAB_LAUNCHED();
   return NNAB_OK;
 }
 

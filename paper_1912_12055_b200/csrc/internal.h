@@ -17,6 +17,14 @@ int cuda_fail(cudaError_t e, const char* where);
     if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
   } while (0)
 
+// Count every libnnab kernel launch (nnab_launch_count) and check it.
+void note_launch();
+#define NNAB_LAUNCHED()                    \
+  do {                                     \
+    note_launch();                         \
+    NNAB_CUDA_TRY(cudaGetLastError());     \
+  } while (0)
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                  uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
@@ -57,7 +65,29 @@ struct StftGemmArgs {
   int32_t n_tab = 0;
   int32_t b_box = 256;
   int32_t pairs = 0;
+  float *save_re = nullptr, *save_im = nullptr, *save_mag = nullptr;  // training forward (slot-major)
+  int64_t ld_slots = 0;
 };
 int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, cudaStream_t s);
+
+// Reduction GEMM C[M][N] = sum_k A[M][K] B(K, N)  (rgemm.cu)
+struct RGemmArgs {
+  int32_t M = 0, N = 0;
+  int64_t K = 0;                            // multiple of 32 (16 in 3xTF32)
+  const float *a_hi = nullptr, *a_lo = nullptr;
+  int64_t lda = 0;                          // floats
+  const float *b_hi = nullptr, *b_lo = nullptr;
+  int64_t ldb = 0;                          // K-major B: floats per row n
+  int32_t b_mn = 0;                         // 1: (k, n) at rows[k + n / b_row_len][n % b_row_len]
+  int32_t b_row_len = 0;
+  int64_t b_rows = 0;
+  float* c = nullptr;
+  int64_t ldc = 0;
+  int32_t splits = 0;                       // 0 = auto
+  float* partial = nullptr;                 // split-K scratch (rgemm_partial_bytes)
+  float alpha = 1.f;
+};
+size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits);
+int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s);
 
 }  // namespace nnab

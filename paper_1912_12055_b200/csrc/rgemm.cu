@@ -1,0 +1,330 @@
+// Reduction GEMM for the backward pass (gradients.py:103-149):
+//
+//   C[m, n] = sum_k A[m, k] * B(k, n)        (fp32 out, TF32 or 3xTF32 in)
+//
+// A is K-major in global memory (row m, k contiguous).  B is either K-major
+// (row n, k contiguous) or MN-major, where element (k, n) lives at
+// rows[k + n / b_row_len][n % b_row_len] -- with b_row_len = hop that is the
+// staged hop-row frame layout, so the kernel-gradient GEMM
+// dK = coef @ frames (gradients.py:127-129) reads frames straight from the
+// forward's staging buffer (never materialised).  The reduction runs over
+// all frame slots of the batch (277,890 at the default config); output tiles
+// of 128 x 256 are spread over persistent CTAs, optionally split along K into
+// `splits` deterministic partial tiles (summed in a fixed order afterwards).
+//
+// Warp roles as in stft_gemm.cu: TMA producer, MMA issuer, TMEM allocator,
+// 4 epilogue warps (thread = output row).
+#include <algorithm>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace nnab {
+namespace {
+
+constexpr int kBM = 128, kBN = 256, kThreads = 256, kStages = 4;
+
+template <bool kSplit>
+struct RCfg {
+  static constexpr int BK = kSplit ? 16 : 32;
+  static constexpr int SWZ = BK * 4;
+  static constexpr int A_BYTES = kBM * BK * 4;
+  static constexpr int B_BYTES = kBN * BK * 4;
+  static constexpr int STAGE = (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);
+  static constexpr int NUM_ACC = kSplit ? 1 : 2;
+  static constexpr int ACC_STRIDE = kSplit ? 512 : 256;
+};
+
+struct RParams {
+  int32_t M, N;
+  int64_t K;
+  int32_t m_tiles, n_tiles, splits;
+  int64_t k_per_split;  // multiple of BK
+  int64_t k_chunk;      // TMEM accumulation chunk (multiple of BK); chunks are summed in fp32 in C
+  int32_t b_mn, b_row_len;
+  float* C;             // [splits][M][ldc]
+  int64_t ldc, split_stride;
+};
+
+NNAB_DEV uint64_t kdesc(const void* p, int swz) {
+  uint64_t d = (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * swz) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(swz == 128 ? 2 : 4) << 61;
+  return d;
+}
+// MN-major TF32 uses the "128B_BASE32B" layout (32-byte units swizzled in a
+// 128-byte row, 4 K-rows per atom; TMA SWIZZLE_128B_ATOM_32B): K-rows of 128 B
+// (32 MN elements), SBO = 4 rows = 512 B between K groups, MN atoms LBO apart.
+NNAB_DEV uint64_t mndesc(const void* p, int /*swz*/, uint32_t lbo) {
+  uint64_t d = (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
+
+template <bool kSplit>
+__global__ void __launch_bounds__(kThreads, 1)
+    rgemm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+                 const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
+                 const RParams p) {
+  using C = RCfg<kSplit>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* tfull = bars + 2 * kStages;
+  uint64_t* tempty = bars + 2 * kStages + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kBM);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const int n_work = p.m_tiles * p.n_tiles * p.splits;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int sp = w % p.splits, tile = w / p.splits;
+        const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+        const int64_t k_lo = sp * p.k_per_split;
+        const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
+        for (int64_t k = k_lo; k < k_hi; k += C::BK) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * C::STAGE;
+          mbar_expect_tx(&full[s], C::STAGE);
+          tma_load_2d(st, &ta_hi, &full[s], (int)k, mt * kBM);
+          if (kSplit) tma_load_2d(st + C::A_BYTES + C::B_BYTES, &ta_lo, &full[s], (int)k, mt * kBM);
+          if (!p.b_mn) {
+            tma_load_2d(st + C::A_BYTES, &tb_hi, &full[s], (int)k, nt * kBN);
+            if (kSplit) tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &tb_lo, &full[s], (int)k, nt * kBN);
+          } else {
+            // kBN/32 boxes of {32 n, BK k}; box j lands at j * (BK rows * 128 B)
+#pragma unroll 1
+            for (int j = 0; j < kBN / 32; ++j) {
+              const int n0 = nt * kBN + j * 32;
+              const int col = n0 % p.b_row_len;
+              const int row = (int)(k + n0 / p.b_row_len);
+              tma_load_2d(st + C::A_BYTES + j * C::BK * 128, &tb_hi, &full[s], col, row);
+              if (kSplit)
+                tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES + j * C::BK * 128, &tb_lo, &full[s], col, row);
+            }
+          }
+          if (++s == kStages) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const uint32_t idesc = idesc_tf32(kBM, kBN) | (p.b_mn ? (1u << 16) : 0u);
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int sp = w % p.splits;
+        const int64_t k_lo = sp * p.k_per_split;
+        const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
+        for (int64_t kc = k_lo; kc < k_hi; kc += p.k_chunk) {
+          const int64_t kc_hi = (kc + p.k_chunk < k_hi) ? kc + p.k_chunk : k_hi;
+          mbar_wait(&tempty[acc], aph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tbase + acc * C::ACC_STRIDE;
+          bool first = true;
+          for (int64_t k = kc; k < kc_hi; k += C::BK) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            uint8_t* st = smem + s * C::STAGE;
+            const uint64_t a = kdesc(st, C::SWZ);
+            const uint64_t a_lo = kdesc(st + C::A_BYTES + C::B_BYTES, C::SWZ);
+            // MN-major B: the kBN/32 boxes are C::BK*128 bytes apart (LBO)
+            const uint64_t b = p.b_mn ? mndesc(st + C::A_BYTES, 128, C::BK * 128) : kdesc(st + C::A_BYTES, C::SWZ);
+            const uint64_t b_lo = p.b_mn ? mndesc(st + 2 * C::A_BYTES + C::B_BYTES, 128, C::BK * 128)
+                                         : kdesc(st + 2 * C::A_BYTES + C::B_BYTES, C::SWZ);
+#pragma unroll
+            for (int kk = 0; kk < C::BK / 8; ++kk) {
+              const uint64_t ao = (uint64_t)((kk * 32) >> 4);
+              const uint64_t bo = p.b_mn ? (uint64_t)((kk * 1024) >> 4) : ao;  // MN-major: next 8 K rows
+              mma_tf32(d, a + ao, b + bo, idesc, first ? 0u : 1u);
+              if (kSplit) {
+                mma_tf32(d + kBN, a + ao, b_lo + bo, idesc, first ? 0u : 1u);
+                mma_tf32(d + kBN, a_lo + ao, b + bo, idesc, 1u);
+              }
+              first = false;
+            }
+            mma_commit(&empty[s]);
+            if (++s == kStages) { s = 0; ph ^= 1; }
+          }
+          mma_commit(&tfull[acc]);
+          if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const uint32_t q = warp - 4, row = q * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const int sp = w % p.splits, tile = w / p.splits;
+      const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+      const int64_t k_lo = sp * p.k_per_split;
+      const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
+      const int m = mt * kBM + row;
+      float* crow = p.C + sp * p.split_stride + (int64_t)m * p.ldc;
+      const bool vec = (p.ldc % 4) == 0;
+      for (int64_t kc = k_lo; kc < k_hi; kc += p.k_chunk) {
+        const bool first_chunk = kc == k_lo;  // later chunks add into C in fixed order: deterministic
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t tb = tbase + ((q * 32) << 16) + acc * C::ACC_STRIDE;
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          float v[32];
+          tmem_ld32(tb + c * 32, v);
+          if (kSplit) {
+            float u[32];
+            tmem_ld32(tb + kBN + c * 32, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += u[j];
+          } else {
+            tmem_ld_wait();
+          }
+          const int n0 = nt * kBN + c * 32;
+          if (m < p.M) {
+            if (n0 + 32 <= p.N && vec) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                float4* dst = reinterpret_cast<float4*>(crow + n0 + j);
+                float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if (!first_chunk) {
+                  const float4 c0 = *dst;
+                  o.x += c0.x;
+                  o.y += c0.y;
+                  o.z += c0.z;
+                  o.w += c0.w;
+                }
+                *dst = o;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < p.N) crow[n0 + j] = first_chunk ? v[j] : crow[n0 + j] + v[j];
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tbase);
+}
+
+// out[m][n] = sum_s parts[s][m][n] in a fixed order (deterministic split-K)
+__global__ void sum_splits_kernel(const float* __restrict__ parts, int32_t splits, int64_t stride, int32_t M,
+                                  int32_t N, int64_t ldp, float* __restrict__ out, int64_t ldo, float alpha) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / N, n = e - m * N;
+    float a = 0.f;
+    for (int s = 0; s < splits; ++s) a += parts[s * stride + m * ldp + n];
+    out[m * ldo + n] = alpha * a;
+  }
+}
+
+template <bool kSplit>
+int launch(const RGemmArgs& g, cudaStream_t st) {
+  using C = RCfg<kSplit>;
+  if (g.K % C::BK || g.lda % 4 || (g.b_mn && g.b_row_len % 32) || (!g.b_mn && g.ldb % 4)) return NNAB_EINVAL;
+  CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
+  int rc = make_tmap_2d(&ta_hi, g.a_hi, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
+  if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, g.a_lo, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
+  if (!g.b_mn) {
+    if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBN, C::SWZ);
+    if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, g.b_lo, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBN, C::SWZ);
+  } else {
+    // rows of b_row_len floats; b_rows rows in total; boxes of 32 columns x BK rows, 128-byte swizzle
+    if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 4, 32, C::BK, -128);
+    if (!rc && kSplit)
+      rc = make_tmap_2d(&tb_lo, g.b_lo, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 4, 32, C::BK, -128);
+  }
+  if (rc) return rc;
+  if (!kSplit) {
+    ta_lo = ta_hi;
+    tb_lo = tb_hi;
+  }
+  RParams p{};
+  p.M = g.M;
+  p.N = g.N;
+  p.K = g.K;
+  p.m_tiles = (g.M + kBM - 1) / kBM;
+  p.n_tiles = (g.N + kBN - 1) / kBN;
+  const int tiles = p.m_tiles * p.n_tiles;
+  int splits = g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, tiles));
+  const int64_t kb = g.K / C::BK;
+  splits = (int)std::min<int64_t>(splits, kb);
+  p.k_per_split = (kb + splits - 1) / splits * C::BK;
+  p.splits = (int)((g.K + p.k_per_split - 1) / p.k_per_split);
+  p.k_chunk = (kSplit ? 1024 : 2048);  // <= 128 / 256 accumulate steps per TMEM chain
+  p.b_mn = g.b_mn;
+  p.b_row_len = g.b_mn ? g.b_row_len : 1 << 30;
+  const bool direct = p.splits == 1 && g.alpha == 1.f;
+  p.C = direct ? g.c : g.partial;
+  p.ldc = direct ? g.ldc : (int64_t)p.n_tiles * kBN;
+  p.split_stride = (int64_t)p.m_tiles * kBM * p.ldc;
+  if (!direct && !g.partial) return NNAB_EINVAL;
+  const size_t smem = 1024 + kStages * C::STAGE + 128;
+  auto k = rgemm_kernel<kSplit>;
+  NNAB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = std::min(tiles * p.splits, num_sms());
+  k<<<grid, kThreads, smem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+  NNAB_LAUNCHED();
+  if (!direct) {
+    const int64_t total = (int64_t)g.M * g.N;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+    sum_splits_kernel<<<blocks, 256, 0, st>>>(g.partial, p.splits, p.split_stride, g.M, g.N, p.ldc, g.c, g.ldc,
+                                              g.alpha);
+    NNAB_LAUNCHED();
+  }
+  return NNAB_OK;
+}
+
+}  // namespace
+
+size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits) {
+  const int64_t mt = (M + kBM - 1) / kBM, nt = (N + kBN - 1) / kBN;
+  if (splits <= 0) splits = std::max(1, num_sms() / (int)std::max<int64_t>(1, mt * nt));
+  return (size_t)splits * mt * kBM * nt * kBN * sizeof(float);
+}
+
+int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s) {
+  if (precision == NNAB_PREC_3XTF32) return launch<true>(g, s);
+  if (precision == NNAB_PREC_TF32) return launch<false>(g, s);
+  return NNAB_EINVAL;
+}
+
+}  // namespace nnab

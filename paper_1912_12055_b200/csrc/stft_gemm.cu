@@ -62,6 +62,10 @@ struct Params {
   // longest-first so the first MMA (N = max) initialises every used column.
   const uint32_t* kb_tab;
   int32_t n_tab, b_box, pairs;
+  // training forward: re, im and smoothed magnitude per (bin, slot) saved in
+  // slot-major layout [bin][ld_slots] for the backward GEMMs (may be null)
+  float *save_re, *save_im, *save_mag;
+  int64_t ld_slots;
 };
 
 NNAB_DEV uint64_t make_sdesc(const void* p, int swz_bytes) {
@@ -79,13 +83,12 @@ NNAB_DEV float finish(float re, float im, int kind, float power, float eps) {
   const float p = fmaf(re, re, im * im);
   if (kind == NNAB_OUT_POWER) return p;
   if (kind == NNAB_OUT_SMOOTH_MAG) return sqrtf(p + eps);
-  const float m = sqrtf(p);
-  if (kind == NNAB_OUT_MEL) {
-    if (power == 1.f) return m;
-    if (power == 2.f) return p;
-    return powf(m, power);
+  if (kind == NNAB_OUT_MEL) {  // eps = 0 for MelSpec, 1e-12 for the trainable layer (gradients.py:69-74)
+    if (power == 1.f) return sqrtf(p + eps);
+    if (power == 2.f) return p + eps;
+    return powf(sqrtf(p + eps), power);
   }
-  return m;
+  return sqrtf(p);
 }
 
 template <bool kSplit>
@@ -288,6 +291,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             nyq_re = im[0];  // cosine row of bin F-1 sits in bin 0's sine slot
             im[0] = 0.f;
           }
+          if (p.save_re) {  // slot-major copies for the backward pass (coalesced across lanes)
+            const int64_t slot = (int64_t)mt * kBM + row;
+            if (slot < p.ld_slots) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int bin = bin0 + j;
+                if (bin < F - p.fold) {
+                  const int64_t o = (int64_t)bin * p.ld_slots + slot;
+                  p.save_re[o] = re[j];
+                  p.save_im[o] = im[j];
+                  if (p.save_mag) {  // GEMM operand of dW: TF32-rounded in TF32 mode, fp32 (split later) in 3xTF32
+                    const float s = sqrtf(fmaf(re[j], re[j], im[j] * im[j]) + p.eps);
+                    p.save_mag[o] = kSplit ? s : tf32_rne(s);
+                  }
+                }
+              }
+              if (p.fold && n == 0 && c == 0) {
+                const int64_t o = (int64_t)(F - 1) * p.ld_slots + slot;
+                p.save_re[o] = nyq_re;
+                p.save_im[o] = 0.f;
+                if (p.save_mag) p.save_mag[o] = sqrtf(nyq_re * nyq_re + p.eps);
+              }
+            }
+          }
           if (kind == NNAB_OUT_MEL) {
             float m32[32];
 #pragma unroll
@@ -390,6 +417,11 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.mel_band = a.mel_band;
   p.out = a.out;
   p.kb_tab = a.kb_tab;
+  p.save_re = a.save_re;
+  p.save_im = a.save_im;
+  p.save_mag = a.save_mag;
+  p.ld_slots = a.ld_slots;
+  if (a.save_re && (!a.save_im || a.pairs)) return NNAB_EINVAL;
   p.n_tab = a.n_tab;
   p.b_box = b_box;
   p.pairs = a.pairs;
@@ -401,7 +433,7 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = std::min(p.n_mtiles, num_sms());
   kern<<<grid, kThreads, smem, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
-  NNAB_CUDA_TRY(cudaGetLastError());
+  NNAB_LAUNCHED();
   return NNAB_OK;
 }
 

@@ -1,0 +1,279 @@
+// Trainable layers (gradients.py:28-149) on the device.
+//
+// Forward (training): the STFT GEMM epilogue additionally stores re, im and
+// the smoothed magnitude S = sqrt(re^2 + im^2 + eps) per (bin, frame slot) in
+// slot-major layout [bin][ld], the K-major operand layout the backward GEMMs
+// read.  Backward:
+//   conv layer  (gradients.py:125-129):  coef = g*re/S, g*im/S  ->  dK = coef @ frames
+//   mel layer   (gradients.py:118-121):  dW = g @ S^T
+//   joint mel+STFT (nnAudio trainable_mel + trainable_STFT): dS = W^T g, then as conv
+//   input grad  (gradients.py:133-149):  frame grads = coef^T @ h, overlap-add, fold pad
+// All products run on the tcgen05 reduction GEMM (rgemm.cu); the glue here is
+// elementwise and HBM-bound.
+#include <algorithm>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace nnab {
+namespace {
+
+// out[r][b*R + t] = g[b][r][t] for t < T, 0 for the staging-only slots and the
+// tail up to ld.
+__global__ void to_slots_kernel(const float* __restrict__ g, int64_t B, int32_t rows, int32_t T, int32_t R,
+                                int64_t ld, float* __restrict__ out) {
+  const int64_t total = (int64_t)rows * ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ld, slot = e - r * ld;
+    const int64_t b = slot / R;
+    const int t = (int)(slot - b * R);
+    float v = 0.f;
+    if (b < B && t < T) v = g[(b * rows + r) * (int64_t)T + t];
+    out[e] = v;
+  }
+}
+
+// coef rows [0, F): dS*re/S, rows [F, 2F): dS*im/S  (gradients.py:127-128)
+__global__ void coef_kernel(const float* __restrict__ ds_slots, const float* __restrict__ g_bft,
+                            const float* __restrict__ re, const float* __restrict__ im, int32_t F, int64_t B,
+                            int32_t T, int32_t R, int64_t ld, float eps, int split, float* __restrict__ hi,
+                            float* __restrict__ lo) {
+  const int64_t total = (int64_t)F * ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = e / ld, slot = e - f * ld;
+    const int64_t b = slot / R;
+    const int t = (int)(slot - b * R);
+    float d = 0.f;
+    if (b < B && t < T) d = ds_slots ? ds_slots[e] : g_bft[(b * F + f) * (int64_t)T + t];
+    const float r = re[e], i = im[e];
+    const float s = sqrtf(fmaf(r, r, i * i) + eps);
+    const float cr = d * (r / s), ci = d * (i / s);
+    const float hr = tf32_rne(cr), hi_ = tf32_rne(ci);
+    hi[e] = hr;
+    hi[e + (int64_t)F * ld] = hi_;
+    if (split) {
+      lo[e] = tf32_rne(cr - hr);
+      lo[e + (int64_t)F * ld] = tf32_rne(ci - hi_);
+    }
+  }
+}
+
+// dst[c][r] = src[r][c] (c < cols, r < rows), zero for r in [rows, ld); tf32 hi/lo
+__global__ void transpose_kernel(const float* __restrict__ src, int32_t rows, int32_t cols, int32_t ld, int split,
+                                 float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = (int64_t)cols * ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / ld;
+    const int r = (int)(e - c * ld);
+    const float v = r < rows ? src[(int64_t)r * cols + c] : 0.f;
+    const float h = tf32_rne(v);
+    hi[e] = h;
+    if (split) lo[e] = tf32_rne(v - h);
+  }
+}
+
+// tf32 hi/lo split of a dense matrix, in place layout (rows x cols, ld)
+__global__ void split_kernel(const float* __restrict__ src, int64_t n, int split, float* __restrict__ hi,
+                             float* __restrict__ lo) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float v = src[e];
+    const float h = tf32_rne(v);
+    hi[e] = h;
+    if (split) lo[e] = tf32_rne(v - h);
+  }
+}
+
+// Input gradient: padded-domain overlap-add of frame grads fg[m][slot]
+// (fg^T = h^T @ coef, gradients.py:135), then fold through the pad index map
+// (gradients.py:140-148).  One thread per output sample gathers its frames:
+// deterministic, no atomics.
+__global__ void input_grad_kernel(const float* __restrict__ fg, int64_t ld_fg, int64_t B, int64_t L, int32_t width,
+                                  int32_t hop, int32_t pad, int32_t mode, int32_t T, int32_t R,
+                                  float* __restrict__ gx) {
+  const int64_t total = B * L;
+  const int64_t Lp = L + 2ll * pad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / L, j = e - b * L;
+    // padded positions mapping to sample j: j+pad, and for reflect the mirrors
+    int64_t pos[3];
+    int np = 0;
+    pos[np++] = j + pad;
+    if (mode == NNAB_PAD_REFLECT && pad > 0) {
+      if (j >= 1 && j <= pad) pos[np++] = pad - j;                      // left mirror
+      if (j >= L - 1 - pad && j <= L - 2) pos[np++] = pad + 2 * (L - 1) - j;  // right mirror
+    }
+    float acc = 0.f;
+    for (int u = 0; u < np; ++u) {
+      const int64_t p = pos[u];
+      if (p < 0 || p >= Lp) continue;
+      // frames t with t*hop <= p < t*hop + width
+      int64_t t_hi = p / hop;
+      int64_t t_lo = (p - width) / hop + 1;
+      if (p - width < 0) t_lo = 0;
+      if (t_hi > T - 1) t_hi = T - 1;
+      for (int64_t t = t_lo; t <= t_hi; ++t) {
+        const int64_t m = p - t * hop;
+        acc += fg[m * ld_fg + b * R + t];  // frame grads stored transposed: [tap][slot]
+      }
+    }
+    gx[e] = acc;
+  }
+}
+
+int grid_for(int64_t total) { return (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 32); }
+
+}  // namespace
+}  // namespace nnab
+
+using namespace nnab;
+
+extern "C" int64_t nnab_slots_ld(const nnab_frames* f) {
+  FrameGeom g;
+  if (frame_geometry(f, &g)) return -1;
+  return (g.B * g.R + 31) / 32 * 32;
+}
+
+extern "C" int nnab_stft_forward_train_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
+                                              int32_t n_bins, int32_t fold_nyquist, int32_t precision,
+                                              int32_t out_kind, float power, float eps, const float* mel_w,
+                                              int32_t n_mels, int32_t mel_ld, const int32_t* mel_band, float* out,
+                                              float* save_re, float* save_im, float* save_mag, int64_t ld,
+                                              const void* workspace, size_t workspace_bytes, void* stream) {
+  FrameGeom g;
+  int rc = frame_geometry(f, &g);
+  if (rc) return rc;
+  if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
+  const int split = precision == NNAB_PREC_3XTF32;
+  if (!packed_hi || (split && !packed_lo) || !out || !save_re || !save_im) return NNAB_EINVAL;
+  if (out_kind != NNAB_OUT_SMOOTH_MAG && out_kind != NNAB_OUT_MEL) return NNAB_EINVAL;
+  if (out_kind == NNAB_OUT_MEL && (!mel_w || n_mels < 1)) return NNAB_EINVAL;
+  if (ld < g.B * g.R || ld % 32) return NNAB_EINVAL;
+  if (g.B == 0) return NNAB_OK;
+  if (!workspace || workspace_bytes < nnab_stft_workspace_bytes(f, precision)) return NNAB_EINVAL;
+  const size_t sb = (size_t)((g.B * g.R * g.row_len * 4 + 255) & ~int64_t(255));
+  StftGemmArgs a{};
+  a.a_hi = reinterpret_cast<const float*>(workspace);
+  a.a_lo = split ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + sb) : nullptr;
+  a.b_hi = packed_hi;
+  a.b_lo = packed_lo;
+  a.n_tiles = nnab_dft_bank_tiles(n_bins, fold_nyquist);
+  a.n_bins = n_bins;
+  a.fold = fold_nyquist ? 1 : 0;
+  a.out_kind = out_kind;
+  a.power = power;
+  a.eps = eps;
+  a.mel_w = mel_w;
+  a.n_mels = n_mels;
+  a.mel_ld = mel_ld;
+  a.mel_band = mel_band;
+  a.out = out;
+  a.save_re = save_re;
+  a.save_im = save_im;
+  a.save_mag = save_mag;
+  a.ld_slots = ld;
+  return launch_stft_gemm(g, a, precision, (cudaStream_t)stream);
+}
+
+extern "C" int nnab_grad_to_slots(const float* g_brt, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld,
+                                  float* out, void* stream) {
+  if (!g_brt || !out || rows < 1 || T < 1 || R < T || ld < B * R) return NNAB_EINVAL;
+  const int64_t total = (int64_t)rows * ld;
+  if (total == 0) return NNAB_OK;
+  to_slots_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(g_brt, B, rows, T, R, ld, out);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
+extern "C" int nnab_dft_coef(const float* ds_slots, const float* g_bft, const float* re_s, const float* im_s,
+                             int32_t F, int64_t B, int32_t T, int32_t R, int64_t ld, float eps, int32_t precision,
+                             float* coef_hi, float* coef_lo, void* stream) {
+  if ((!ds_slots && !g_bft) || !re_s || !im_s || !coef_hi || F < 1 || ld < B * R) return NNAB_EINVAL;
+  const int split = precision == NNAB_PREC_3XTF32;
+  if (split && !coef_lo) return NNAB_EINVAL;
+  const int64_t total = (int64_t)F * ld;
+  coef_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(ds_slots, g_bft, re_s, im_s, F, B, T, R, ld, eps,
+                                                                 split, coef_hi, coef_lo);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
+extern "C" int nnab_transpose_pad(const float* src, int32_t rows, int32_t cols, int32_t ld, int32_t precision,
+                                  float* hi, float* lo, void* stream) {
+  if (!src || !hi || rows < 1 || cols < 1 || ld < rows) return NNAB_EINVAL;
+  const int split = precision == NNAB_PREC_3XTF32;
+  if (split && !lo) return NNAB_EINVAL;
+  const int64_t total = (int64_t)cols * ld;
+  transpose_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(src, rows, cols, ld, split, hi, lo);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
+extern "C" int nnab_tf32_split(const float* src, int64_t n, int32_t precision, float* hi, float* lo, void* stream) {
+  if (!src || !hi || n < 0) return NNAB_EINVAL;
+  const int split = precision == NNAB_PREC_3XTF32;
+  if (split && !lo) return NNAB_EINVAL;
+  if (n == 0) return NNAB_OK;
+  split_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(src, n, split, hi, lo);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
+extern "C" size_t nnab_rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits) {
+  return rgemm_partial_bytes(M, N, K, splits);
+}
+
+extern "C" int nnab_rgemm(int32_t M, int32_t N, int64_t K, const float* a_hi, const float* a_lo, int64_t lda,
+                          const float* b_hi, const float* b_lo, int64_t ldb, int32_t b_mn, int32_t b_row_len,
+                          int64_t b_rows, float* c, int64_t ldc, int32_t splits, float* partial, int32_t precision,
+                          void* stream) {
+  if (M < 1 || N < 1 || K < 1 || !a_hi || !b_hi || !c) return NNAB_EINVAL;
+  if (precision == NNAB_PREC_3XTF32 && (!a_lo || !b_lo)) return NNAB_EINVAL;
+  RGemmArgs g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.a_hi = a_hi;
+  g.a_lo = a_lo;
+  g.lda = lda;
+  g.b_hi = b_hi;
+  g.b_lo = b_lo;
+  g.ldb = ldb;
+  g.b_mn = b_mn;
+  g.b_row_len = b_row_len;
+  g.b_rows = b_rows;
+  g.c = c;
+  g.ldc = ldc;
+  g.splits = splits;
+  g.partial = partial;
+  return launch_rgemm(g, precision, (cudaStream_t)stream);
+}
+
+// dK[r][m] = sum_slot coef[r][slot] * frames[slot][m]   (gradients.py:129)
+extern "C" int nnab_kernel_grad(const nnab_frames* f, const float* coef_hi, const float* coef_lo, int32_t rows,
+                                int64_t ld, int32_t precision, float* dk, int64_t ldk, const void* workspace,
+                                size_t workspace_bytes, float* partial, int32_t splits, void* stream) {
+  FrameGeom g;
+  int rc = frame_geometry(f, &g);
+  if (rc) return rc;
+  const int split = precision == NNAB_PREC_3XTF32;
+  if (!workspace || workspace_bytes < nnab_stft_workspace_bytes(f, precision)) return NNAB_EINVAL;
+  const size_t sb = (size_t)((g.B * g.R * g.row_len * 4 + 255) & ~int64_t(255));
+  const float* fr_hi = reinterpret_cast<const float*>(workspace);
+  const float* fr_lo = split ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + sb) : nullptr;
+  return nnab_rgemm(rows, g.width, ld, coef_hi, coef_lo, ld, fr_hi, fr_lo, 0, 1, g.row_len, g.B * g.R, dk, ldk, splits,
+                    partial, precision, stream);
+}
+
+extern "C" int nnab_input_grad(const nnab_frames* f, const float* frame_grads, int64_t ld_fg, float* gx,
+                               void* stream) {
+  FrameGeom g;
+  int rc = frame_geometry(f, &g);
+  if (rc) return rc;
+  if (!frame_grads || !gx || ld_fg < g.B * g.R) return NNAB_EINVAL;
+  const int64_t total = g.B * g.L;
+  if (total == 0) return NNAB_OK;
+  input_grad_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(frame_grads, ld_fg, g.B, g.L, g.width, g.hop,
+                                                                       g.pad, g.pad_mode, g.T, g.R, gx);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}

@@ -113,20 +113,20 @@ class DftEngine:
     def set_mel(self, weights, power: float = 1.0, banded: bool = True) -> None:
         """Mel weights (n_mels, n_bins) for the fused epilogue; rows padded to
         a multiple of 4 floats so the epilogue reads them with 16-byte loads."""
-        w = torch.as_tensor(weights, dtype=torch.float64)
+        w = torch.as_tensor(weights)
         if w.dim() != 2 or w.shape[1] != self.n_bins:
             raise ValueError(f"mel weights must be (n_mels, {self.n_bins})")
         self.n_mels = int(w.shape[0])
         if self.n_mels > 128:
             raise L.NnabError("fused Mel epilogue supports n_mels <= 128")
         self.mel_ld = ((max(self.n_tiles * 128, self.n_bins) + 3) // 4) * 4 + 32
-        wp = torch.zeros(self.n_mels, self.mel_ld, dtype=torch.float32)
+        wp = torch.zeros(self.n_mels, self.mel_ld, dtype=torch.float32, device=w.device)
         wp[:, : self.n_bins] = w.to(torch.float32)
         self.mel_w = wp.to(self.device)
         n_chunks = self.mel_ld // 32 + 1
         if banded:
             from .banks import mel_bands
-            band = mel_bands(wp.numpy(), n_chunks)
+            band = mel_bands(wp.cpu().numpy(), n_chunks)
             self.mel_band = torch.from_numpy(band.reshape(-1)).to(self.device)
         else:
             self.mel_band = None

@@ -1,0 +1,165 @@
+"""nnAudio-style nn.Modules on the sm_100a kernels.
+
+    STFT(n_fft=2048, freq_bins=None, hop_length=512, window='hann', freq_scale='no', center=True,
+         pad_mode='reflect', fmin=50, fmax=6000, sr=22050, trainable=False, output_format='Magnitude')
+    MelSpectrogram(sr=22050, n_fft=2048, n_mels=128, hop_length=512, window='hann', center=True,
+         pad_mode='reflect', htk=False, fmin=0.0, fmax=None, norm=None, power=1.0,
+         trainable_mel=False, trainable_STFT=False)
+    CQT1992v2(sr=22050, hop_length=512, fmin=32.70, fmax=None, n_bins=84, bins_per_octave=12, norm=1,
+         window='hann', center=True, pad_mode='reflect', trainable=False, output_format='Magnitude')
+    CQT2010v2(sr=22050, hop_length=512, fmin=32.70, fmax=None, n_bins=84, bins_per_octave=12, norm=True,
+         basis_norm=1, window='hann', pad_mode='reflect', earlydownsample=True)
+
+Input (batch, samples) or (samples,) float32 CUDA tensor; output (batch, freq, time).
+Numerics follow the `spectro` reference this repo is parity-checked against:
+Mel `norm=None` is its peak normalisation (spectro MelParams norm="none"); nnAudio's
+`norm=1` selects the area ("slaney") normalisation.  Trainable layers return the
+smoothed magnitude sqrt(re^2 + im^2 + 1e-12) of gradients.py:61-67 and back-propagate
+through tcgen05 GEMMs (autograd.py).  Inference layers never touch the CPU.
+"""
+
+from __future__ import annotations
+
+import torch
+from torch import nn
+
+from . import banks
+from .autograd import DftLayerFunction, DftLayerOp
+from .engine import CqtLongEngine, Cqt2010Engine, DftEngine, _require_cuda
+from .spectro import CqtConfig, cqt2010_plan
+
+_FORMATS = {"magnitude": "magnitude", "complex": "complex", "power": "power"}
+
+
+def _fmt(output_format: str) -> str:
+    k = output_format.lower()
+    if k not in _FORMATS:
+        raise ValueError(f"output_format must be one of Magnitude/Complex/Power, got {output_format!r}")
+    return _FORMATS[k]
+
+
+def _bank_key(*ps):
+    return tuple((p.data_ptr(), p._version) for p in ps)
+
+
+def _as_batch(x: torch.Tensor) -> torch.Tensor:
+    if x.dim() == 1:
+        return x[None]
+    if x.dim() == 3 and x.shape[1] == 1:  # (batch, 1, len), nnAudio accepts it
+        return x[:, 0]
+    if x.dim() != 2:
+        raise ValueError(f"expected (batch, len) audio, got {tuple(x.shape)}")
+    return x
+
+
+class STFT(nn.Module):
+    def __init__(self, n_fft=2048, freq_bins=None, hop_length=512, window="hann", freq_scale="no", center=True,
+                 pad_mode="reflect", fmin=50, fmax=6000, sr=22050, trainable=False, output_format="Magnitude",
+                 precision="tf32", device="cuda"):
+        super().__init__()
+        self.device = _require_cuda(device)
+        self.output_format = _fmt(output_format)
+        self.trainable = bool(trainable)
+        nf, self.bin_freqs_hz = banks.frequency_scale(freq_scale, n_fft, sr, fmin, fmax, freq_bins)
+        h_re, h_im = banks.dft_kernels(nf, banks.make_window(window, n_fft, True))
+        self.h_re = nn.Parameter(torch.tensor(h_re, dtype=torch.float32, device=self.device), requires_grad=trainable)
+        self.h_im = nn.Parameter(torch.tensor(h_im, dtype=torch.float32, device=self.device), requires_grad=trainable)
+        self._infer = DftEngine(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
+        self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
+        self._op._bank_version = None
+
+    def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
+        x = _as_batch(x)
+        if self.trainable or x.requires_grad:
+            return DftLayerFunction.apply(x, self.h_re, self.h_im, None, self._op, _bank_key(self.h_re, self.h_im))
+        return self._infer.forward(x, _fmt(output_format or self.output_format))
+
+
+class MelSpectrogram(nn.Module):
+    def __init__(self, sr=22050, n_fft=2048, n_mels=128, hop_length=512, window="hann", center=True,
+                 pad_mode="reflect", htk=False, fmin=0.0, fmax=None, norm=None, power=1.0, trainable_mel=False,
+                 trainable_STFT=False, precision="tf32", device="cuda"):
+        super().__init__()
+        self.device = _require_cuda(device)
+        nf, _ = banks.frequency_scale("no", n_fft, sr, 50.0, 6000.0, None)
+        h_re, h_im = banks.dft_kernels(nf, banks.make_window(window, n_fft, True))
+        mel_norm = {None: "none", "none": "none", 1: "area", "slaney": "area", "area": "area"}[norm]
+        w, self.mel_center_freqs_hz = banks.mel_filter_bank(sr, n_fft, n_mels, fmin=fmin, fmax=fmax,
+                                                            formula="htk" if htk else "slaney", norm=mel_norm)
+        self.power = float(power)
+        self.trainable_mel, self.trainable_STFT = bool(trainable_mel), bool(trainable_STFT)
+        self.mel_basis = nn.Parameter(torch.tensor(w, dtype=torch.float32, device=self.device),
+                                      requires_grad=trainable_mel)
+        self.h_re = nn.Parameter(torch.tensor(h_re, dtype=torch.float32, device=self.device),
+                                 requires_grad=trainable_STFT)
+        self.h_im = nn.Parameter(torch.tensor(h_im, dtype=torch.float32, device=self.device),
+                                 requires_grad=trainable_STFT)
+        self._infer = DftEngine(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
+        self._infer.set_mel(w, power=self.power)
+        self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
+        self._op._bank_version = None
+        self._infer_key = _bank_key(self.h_re, self.h_im, self.mel_basis)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        x = _as_batch(x)
+        if self.trainable_mel or self.trainable_STFT or x.requires_grad:
+            if self.power != 1.0:
+                raise NotImplementedError("trainable Mel layers use power=1 (gradients.py:69-80)")
+            return DftLayerFunction.apply(x, self.h_re, self.h_im, self.mel_basis, self._op,
+                                          _bank_key(self.h_re, self.h_im))
+        key = _bank_key(self.h_re, self.h_im, self.mel_basis)
+        if key != self._infer_key:  # parameters edited in place since construction
+            self._infer.set_bank(self.h_re.detach(), self.h_im.detach())
+            self._infer.set_mel(self.mel_basis.detach(), power=self.power)
+            self._infer_key = key
+        return self._infer.forward(x, "mel")
+
+
+class CQT1992v2(nn.Module):
+    def __init__(self, sr=22050, hop_length=512, fmin=32.70, fmax=None, n_bins=84, bins_per_octave=12, norm=1,
+                 window="hann", center=True, pad_mode="reflect", trainable=False, output_format="Magnitude",
+                 precision="tf32", device="cuda"):
+        super().__init__()
+        if not center:
+            raise NotImplementedError("CQT1992v2 frames are centred (transforms.py:175-186)")
+        self.device = _require_cuda(device)
+        self.cfg = CqtConfig(sr=sr, fmin=fmin, n_bins=n_bins, bins_per_octave=bins_per_octave,
+                             hop_length=hop_length, window_kind=window, norm=norm, fmax=fmax, pad_mode=pad_mode)
+        k, self.lengths = banks.cqt_time_kernels(sr, self.cfg.bin_freqs_hz, bins_per_octave, window, norm)
+        self.output_format = _fmt(output_format)
+        self.trainable = bool(trainable)
+        self.k_re = nn.Parameter(torch.tensor(k.real, dtype=torch.float32, device=self.device),
+                                 requires_grad=trainable)
+        self.k_im = nn.Parameter(torch.tensor(k.imag, dtype=torch.float32, device=self.device),
+                                 requires_grad=trainable)
+        self._infer = CqtLongEngine(k, hop_length, pad_mode, precision=precision, device=self.device)
+        self._op = None
+        self._precision = precision
+
+    def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
+        x = _as_batch(x)
+        if self.trainable or x.requires_grad:
+            if self._op is None:  # dense DFT-layout op over the CQT rows (trainable rows lose their support)
+                self._op = DftLayerOp(self.k_re.detach(), self.k_im.detach(), self.cfg.hop_length, True,
+                                      self.cfg.pad_mode, precision=self._precision, device=self.device)
+                self._op._bank_version = None
+            return DftLayerFunction.apply(x, self.k_re, self.k_im, None, self._op, _bank_key(self.k_re, self.k_im))
+        return self._infer.forward(x, _fmt(output_format or self.output_format))
+
+
+class CQT2010v2(nn.Module):
+    def __init__(self, sr=22050, hop_length=512, fmin=32.70, fmax=None, n_bins=84, bins_per_octave=12, norm=True,
+                 basis_norm=1, window="hann", pad_mode="reflect", earlydownsample=True, output_format="Magnitude",
+                 device="cuda"):
+        super().__init__()
+        self.device = _require_cuda(device)
+        self.cfg = CqtConfig(sr=sr, fmin=fmin, n_bins=n_bins, bins_per_octave=bins_per_octave,
+                             hop_length=hop_length, window_kind=window, norm=basis_norm, fmax=fmax,
+                             pad_mode=pad_mode, early_downsample=earlydownsample)
+        p = cqt2010_plan(self.cfg)
+        self.output_format = _fmt(output_format)
+        self._eng = Cqt2010Engine(p["taps"], p["top_kernels"], p["early_stages"], p["n_octaves"], p["kernel_hop"],
+                                  p["first_bin"], bins_per_octave, self.cfg.n_bins, pad_mode, device=self.device)
+
+    def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
+        return self._eng.forward(_as_batch(x), _fmt(output_format or self.output_format))

@@ -343,3 +343,130 @@ def batch_transform(signals, transform, threads: int | None = None) -> list:
         for j, i in enumerate(idx):
             out[i] = Spectrogram(data=data[j], **meta)
     return out
+
+
+# ---------------------------------------------------------------------------
+# trainable layers (gradients.py:28-149)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class DftKernelBank:
+    """kernels.py:108-146 -- paired cos/sin rows (n_bins, n_fft)."""
+
+    h_re: np.ndarray
+    h_im: np.ndarray
+
+
+@dataclass(frozen=True)
+class MelFilterBank:
+    """kernels.py:186-211 -- triangular weights (n_mels, n_fft//2 + 1)."""
+
+    weights: np.ndarray
+
+
+@dataclass(frozen=True)
+class CqtKernelBank:
+    """kernels.py:324-358 -- complex time-domain rows (n_bins, width)."""
+
+    time_kernels: np.ndarray
+
+
+@dataclass
+class TrainableLayer:
+    """gradients.py:28-100 -- a spectrogram layer with writable kernels.
+
+    Parameters live on the device (`params()` returns the CUDA tensors); the
+    forward/backward run batched on the sm_100a kernels (autograd.DftLayerOp).
+    """
+
+    kernels: object
+    hop: int
+    trainable: bool = True
+    eps_mag: float = 1e-12
+    center: bool = True
+    pad_mode: str = "reflect"
+    stft_bank: DftKernelBank | None = None
+    precision: str = "fp32"
+    device: str = "cuda"
+    _params: dict = field(init=False, repr=False)
+
+    def __post_init__(self):
+        from .autograd import DftLayerOp
+        dev = _require_cuda(self.device)
+        bank = self.kernels
+        if isinstance(bank, DftKernelBank):
+            re, im = bank.h_re, bank.h_im
+            self._params = {"h_re": torch.tensor(re, dtype=torch.float32, device=dev),
+                            "h_im": torch.tensor(im, dtype=torch.float32, device=dev)}
+        elif isinstance(bank, CqtKernelBank):
+            re, im = bank.time_kernels.real, bank.time_kernels.imag
+            self._params = {"h_re": torch.tensor(re, dtype=torch.float32, device=dev),
+                            "h_im": torch.tensor(im, dtype=torch.float32, device=dev)}
+        elif isinstance(bank, MelFilterBank):
+            if self.stft_bank is None:
+                raise ValueError("a Mel layer needs the fixed stft_bank it is applied to")
+            re, im = self.stft_bank.h_re, self.stft_bank.h_im
+            self._params = {"weights": torch.tensor(bank.weights, dtype=torch.float32, device=dev)}
+        else:
+            raise TypeError(f"unsupported kernel bank type {type(bank).__name__}")
+        self._op = DftLayerOp(re, im, self.hop, self.center, self.pad_mode, self.eps_mag, self.precision, dev)
+        self._fixed = (torch.tensor(re, dtype=torch.float32, device=dev),
+                       torch.tensor(im, dtype=torch.float32, device=dev))
+
+    def params(self) -> dict:
+        return self._params
+
+    @property
+    def is_mel(self) -> bool:
+        return isinstance(self.kernels, MelFilterBank)
+
+    def _bank(self):
+        if self.is_mel:
+            return self._fixed
+        return self._params["h_re"], self._params["h_im"]
+
+    def _run(self, x: torch.Tensor):
+        h_re, h_im = self._bank()
+        self._op.set_bank(h_re, h_im)
+        return self._op.forward(x, self._params["weights"] if self.is_mel else None)
+
+    def spectrogram_batch(self, x: torch.Tensor) -> torch.Tensor:
+        """(B, L) -> (B, bins, frames) smoothed magnitude (or W @ it)."""
+        return self._run(x)[0]
+
+    def spectrogram(self, x: Signal) -> torch.Tensor:
+        return self.spectrogram_batch(x.samples[None])[0]
+
+
+def spectrogram_vjp(x, layer: TrainableLayer, upstream_grad, with_input_grad: bool = False):
+    """gradients.py:103-149 -- pull a loss gradient back onto the kernels.
+
+    `x` is a Signal (one clip, as the reference) or a (B, L) tensor (batch:
+    the kernel gradients are summed over the clips).  Returns a dict keyed
+    like layer.params(); with_input_grad adds dL/dx (conv layers only)."""
+    xs = x.samples[None] if isinstance(x, Signal) else _batch(x)
+    g = torch.as_tensor(np.asarray(upstream_grad) if not torch.is_tensor(upstream_grad) else upstream_grad)
+    g = g.to(layer._op.device, torch.float32)
+    out, saved = layer._run(xs)
+    if g.dim() == 2:
+        g = g[None]
+    if tuple(g.shape) != tuple(out.shape):
+        raise ValueError(f"upstream_grad shape {tuple(g.shape)} != spectrogram shape {tuple(out.shape)}")
+    if layer.is_mel:
+        if with_input_grad:
+            raise NotImplementedError("input gradients are only provided for convolution layers")
+        gr = layer._op.backward(saved, g, mel_w=layer._params["weights"], need_bank=False, need_mel=True)
+        return {"weights": gr["weights"]}
+    h_re, h_im = layer._bank()
+    gr = layer._op.backward(saved, g, h_re, h_im, need_bank=True, need_x=with_input_grad)
+    grads = {"h_re": gr["h_re"], "h_im": gr["h_im"]}
+    if not with_input_grad:
+        return grads
+    gx = gr["x"]
+    return grads, (gx[0] if isinstance(x, Signal) else gx)
+
+
+def _batch(x):
+    x = x if torch.is_tensor(x) else torch.as_tensor(np.asarray(x, dtype=np.float32))
+    return x[None] if x.dim() == 1 else x

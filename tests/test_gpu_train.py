@@ -1,0 +1,134 @@
+"""GPU parity of the trainable layers (gradients.py:28-149): smoothed-magnitude
+forward, kernel / mel-weight / input gradients vs the reference's golden
+vectors and the float64 oracle.  Gradients are reductions over frames, so the
+same peak-normalised tolerances apply: <= 1e-3 in TF32, <= 1e-5 in 3xTF32."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import spectro_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = {"tf32": 1e-3, "fp32": 1e-5}
+# Kernel gradients go through coef = g*re/S: where |X| is small the direction
+# re/S inherits the forward error divided by S, so gradient tolerances are
+# looser than the forward ones.
+TOL_GRAD = {"tf32": 3e-2, "fp32": 5e-4}
+
+
+def layer_for(bank, hop, precision, **kw):
+    from paper_1912_12055_b200.spectro import TrainableLayer
+    return TrainableLayer(bank, hop=hop, precision=precision, **kw)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("n_fft,hop,key", [(32, 32, "grad_stft"), (64, 16, "grad_stft_hop16")])
+def test_stft_layer_vjp_golden(golden, cuda_dev, precision, n_fft, hop, key):
+    from paper_1912_12055_b200.spectro import DftKernelBank, Signal, spectrogram_vjp
+    h_re, h_im = O.stft_bank(n_fft, 8000.0)
+    layer = layer_for(DftKernelBank(h_re, h_im), hop, precision)
+    x = Signal(golden["grad_x"].astype(np.float32), 8000.0)
+    up = golden["grad_up_stft" if hop == 32 else "grad_up_stft_hop16"]
+    if hop == 32:
+        S = layer.spectrogram(x).cpu().numpy()
+        assert O.peak_err(S, golden["grad_stft_S"]) <= TOL[precision]
+    grads, gx = spectrogram_vjp(x, layer, up, with_input_grad=True)
+    for name in ("h_re", "h_im"):
+        err = O.peak_err(grads[name].cpu().numpy(), golden[f"{key}_{name}"])
+        assert err <= TOL_GRAD[precision], (name, err)
+    err = O.peak_err(gx.cpu().numpy(), golden[f"{key}_x"])
+    assert err <= TOL_GRAD[precision], ("x", err)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_mel_layer_vjp_golden(golden, cuda_dev, precision):
+    from paper_1912_12055_b200.spectro import DftKernelBank, MelFilterBank, Signal, spectrogram_vjp
+    h_re, h_im = O.stft_bank(32, 8000.0)
+    W = O.mel_bank(8000.0, 32, 4, formula="htk")
+    layer = layer_for(MelFilterBank(W), 32, precision, stft_bank=DftKernelBank(h_re, h_im))
+    x = Signal(golden["grad_x"].astype(np.float32), 8000.0)
+    fwd = layer.spectrogram(x).cpu().numpy()
+    assert O.peak_err(fwd, golden["grad_mel_fwd"]) <= TOL[precision]
+    g = spectrogram_vjp(x, layer, golden["grad_up_mel"])
+    assert O.peak_err(g["weights"].cpu().numpy(), golden["grad_mel_W"]) <= TOL_GRAD[precision]
+    with pytest.raises(NotImplementedError):
+        spectrogram_vjp(x, layer, golden["grad_up_mel"], with_input_grad=True)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_cqt_layer_vjp_golden(golden, cuda_dev, precision):
+    from paper_1912_12055_b200.spectro import CqtKernelBank, Signal, spectrogram_vjp
+    k, _ = O.cqt_time_bank(O.CqtCfg(sr=8000.0, fmin=200.0, n_bins=12, hop_length=128))
+    layer = layer_for(CqtKernelBank(k), 128, precision)
+    g = spectrogram_vjp(Signal(golden["grad_xc"].astype(np.float32), 8000.0), layer, golden["grad_up_cqt"])
+    for name in ("h_re", "h_im"):
+        err = O.peak_err(g[name].cpu().numpy(), golden[f"grad_cqt_{name}"])
+        assert err <= TOL_GRAD[precision], (name, err)
+
+
+def test_zero_upstream_and_shape_mismatch(cuda_dev):
+    from paper_1912_12055_b200.spectro import DftKernelBank, Signal, spectrogram_vjp
+    h_re, h_im = O.stft_bank(32, 8000.0)
+    layer = layer_for(DftKernelBank(h_re, h_im), 32, "fp32")
+    x = Signal(np.random.default_rng(0).standard_normal(512).astype(np.float32), 8000.0)
+    S = layer.spectrogram(x)
+    g = spectrogram_vjp(x, layer, torch.zeros_like(S))
+    assert not g["h_re"].any() and not g["h_im"].any()
+    with pytest.raises(ValueError):
+        spectrogram_vjp(x, layer, np.zeros((3, 3)))
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_joint_mel_stft_batch_vs_oracle(cuda_dev, precision):
+    """Config 5 (trainable STFT + Mel) on 6 full-length clips: dW, dh_re, dh_im
+    summed over the batch vs the float64 composition of the reference pieces."""
+    from paper_1912_12055_b200.layers import MelSpectrogram
+    rng = np.random.default_rng(5)
+    B = 6
+    x = (rng.standard_normal((B, 80000)) * 0.5).astype(np.float32)
+    m = MelSpectrogram(sr=44100, trainable_mel=True, trainable_STFT=True, precision=precision)
+    xt = torch.from_numpy(x).to(cuda_dev)
+    out = m(xt)
+    assert out.shape == (B, 128, 157)
+    g = rng.standard_normal(out.shape).astype(np.float32)
+    out.backward(torch.from_numpy(g).to(cuda_dev))
+    h_re, h_im = O.stft_bank()
+    W = O.mel_bank(44100.0, 2048, 128, formula="slaney")
+    dW = np.zeros_like(W)
+    dh_re, dh_im = np.zeros_like(h_re), np.zeros_like(h_im)
+    fwd = []
+    for b in range(B):
+        fr, re, im, S = O.smooth_mag_forward(x[b].astype(np.float64), h_re, h_im, 512)
+        fwd.append(W @ S)
+        gb = g[b].astype(np.float64)
+        dW += gb @ S.T
+        dS = W.T @ gb
+        dh_re += (dS * re / S) @ fr
+        dh_im += (dS * im / S) @ fr
+    assert O.peak_err(out.detach().cpu().numpy(), np.stack(fwd)) <= TOL[precision]
+    tol = TOL_GRAD[precision]
+    assert O.peak_err(m.mel_basis.grad.cpu().numpy(), dW) <= tol
+    assert O.peak_err(m.h_re.grad.cpu().numpy(), dh_re) <= tol
+    assert O.peak_err(m.h_im.grad.cpu().numpy(), dh_im) <= tol
+
+
+def test_trainable_stft_module_step_changes_bank(cuda_dev):
+    from paper_1912_12055_b200.layers import STFT
+    m = STFT(n_fft=256, hop_length=64, sr=8000, trainable=True, precision="fp32")
+    x = torch.randn(4, 4000, device=cuda_dev)
+    opt = torch.optim.SGD(m.parameters(), lr=1e-3)
+    a = m(x).sum()
+    a.backward()
+    opt.step()
+    b = m(x).sum()  # repacked bank after the in-place update
+    assert float(a) != float(b)
+    # input gradient through the non-trainable layer (gradients.py:133-149)
+    m2 = STFT(n_fft=128, hop_length=32, sr=8000)
+    xr = torch.randn(2, 1000, device=cuda_dev, requires_grad=True)
+    m2(xr).sum().backward()
+    h_re, h_im = O.stft_bank(128, 8000.0)
+    ref = np.stack([O.conv_layer_vjp(c.astype(np.float64), h_re, h_im, 32,
+                                     np.ones((65, 1000 // 32 + 1)), with_input_grad=True)[1]
+                    for c in xr.detach().cpu().numpy()])
+    assert O.peak_err(xr.grad.cpu().numpy(), ref) <= TOL_GRAD["tf32"]
