@@ -145,6 +145,9 @@ int nnab_stft_forward_train_staged(const nnab_frames* f, const float* packed_hi,
 /* (B, rows, T) -> slot-major [rows][ld], zero on non-frame slots */
 int nnab_grad_to_slots(const float* g_brt, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld, float* out,
                        void* stream);
+/* slot-major [rows][ld] -> (B, rows, T) */
+int nnab_from_slots(const float* src, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld, float* out_brt,
+                    void* stream);
 /* coef = dS*re/S (rows 0..F-1) and dS*im/S (rows F..2F-1), gradients.py:127-128;
  * dS from ds_slots ([F][ld]) or g_bft ((B, F, T)); TF32 hi (+ lo residual). */
 int nnab_dft_coef(const float* ds_slots, const float* g_bft, const float* re_s, const float* im_s, int32_t F,

@@ -66,21 +66,29 @@ class DftLayerOp:
                 "stage_frames")
         ld = lib.nnab_slots_ld(C.byref(f))
         F = self.n_bins
+        R = self._rows_per_clip(length)
         re_s, im_s = _f32(F, ld, self.device), _f32(F, ld, self.device)
         mag_s = _f32(F, ld, self.device) if mel_w is not None else None
-        if mel_w is not None:
-            eng.set_mel(mel_w.detach(), power=1.0, banded=False)
-            out = torch.empty(B, eng.n_mels, T, device=self.device)
-            kind, mw, nm, mld = L.OUT_MEL, eng.mel_w.data_ptr(), eng.n_mels, eng.mel_ld
-        else:
-            out = torch.empty(B, F, T, device=self.device)
-            kind, mw, nm, mld = L.OUT_SMOOTH_MAG, None, 0, 0
+        # mel layer: the STFT GEMM only saves re/im/S per slot; W @ S then runs as a
+        # tcgen05 GEMM (a trained W is dense, so the epilogue's banded CUDA-core path
+        # would be latency-bound)
+        out = None if mel_w is not None else torch.empty(B, F, T, device=self.device)
         L.check(lib.nnab_stft_forward_train_staged(
-            C.byref(f), eng.packed_hi.data_ptr(), L.ptr(eng.packed_lo), F, eng.fold, self.prec, kind, 1.0, self.eps,
-            mw, nm, mld, None, out.data_ptr(), re_s.data_ptr(), im_s.data_ptr(), L.ptr(mag_s), ld, ws.data_ptr(),
-            ws.numel(), stream), "stft_forward_train")
-        saved = {"ws": ws, "re": re_s, "im": im_s, "mag": mag_s, "B": B, "L": length, "T": T, "ld": ld,
-                 "R": self._rows_per_clip(length)}
+            C.byref(f), eng.packed_hi.data_ptr(), L.ptr(eng.packed_lo), F, eng.fold, self.prec, L.OUT_SMOOTH_MAG,
+            1.0, self.eps, None, 0, 0, None, L.ptr(out), re_s.data_ptr(), im_s.data_ptr(), L.ptr(mag_s), ld,
+            ws.data_ptr(), ws.numel(), stream), "stft_forward_train")
+        saved = {"ws": ws, "re": re_s, "im": im_s, "mag": mag_s, "B": B, "L": length, "T": T, "ld": ld, "R": R}
+        if mel_w is not None:
+            nm = int(mel_w.shape[0])
+            kp = (F + 31) // 32 * 32
+            wp = torch.zeros(nm, kp, device=self.device)
+            wp[:, :F] = mel_w.detach().to(self.device, torch.float32)
+            magp = self._split(mag_s) if self.split else (mag_s, None)
+            saved["magp"] = magp
+            mel_s = _f32(nm, ld, self.device)
+            self._rgemm(nm, ld, kp, self._split(wp), kp, magp, ld, 1, ld, F, mel_s, ld)
+            out = torch.empty(B, nm, T, device=self.device)
+            L.check(lib.nnab_from_slots(mel_s.data_ptr(), B, nm, T, R, ld, out.data_ptr(), stream), "from_slots")
         return out, saved
 
     def _rows_per_clip(self, length):
@@ -124,8 +132,7 @@ class DftLayerOp:
             L.check(lib.nnab_grad_to_slots(g.data_ptr(), B, nm, T, R, ld, gs.data_ptr(), stream), "grad_to_slots")
             gsp = self._split(gs)
             if need_mel:  # dW[m][f] = sum_slot g[m][slot] S[f][slot]
-                mag = saved["mag"]
-                magp = self._split(mag) if self.split else (mag, None)
+                magp = saved["magp"]
                 dW = torch.empty(nm, F, device=self.device)
                 self._rgemm(nm, F, ld, gsp, ld, magp, ld, 0, 0, 0, dW, F)
                 grads["weights"] = dW

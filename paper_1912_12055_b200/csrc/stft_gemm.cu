@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               mel_acc[m * kBM + row] = a;
             }
             if (p.fold && n == 0 && c == 0) nyq_val = finish(nyq_re, 0.f, kind, p.power, p.eps);
-          } else if (valid) {
+          } else if (valid && p.out) {  // out == null: training forward that only saves slots
             const int64_t ob = b * (int64_t)F;
             if (kind == NNAB_OUT_COMPLEX) {
               float2* o = reinterpret_cast<float2*>(p.out);

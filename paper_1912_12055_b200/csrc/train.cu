@@ -33,6 +33,19 @@ __global__ void to_slots_kernel(const float* __restrict__ g, int64_t B, int32_t 
   }
 }
 
+// out[b][r][t] = src[r][b*R + t]   (slot-major GEMM output -> (B, rows, T))
+__global__ void from_slots_kernel(const float* __restrict__ src, int64_t B, int32_t rows, int32_t T, int32_t R,
+                                  int64_t ld, float* __restrict__ out) {
+  const int64_t total = B * rows * (int64_t)T;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e % T);
+    const int64_t br = e / T;
+    const int r = (int)(br % rows);
+    const int64_t b = br / rows;
+    out[e] = src[(int64_t)r * ld + b * R + t];
+  }
+}
+
 // coef rows [0, F): dS*re/S, rows [F, 2F): dS*im/S  (gradients.py:127-128)
 __global__ void coef_kernel(const float* __restrict__ ds_slots, const float* __restrict__ g_bft,
                             const float* __restrict__ re, const float* __restrict__ im, int32_t F, int64_t B,
@@ -144,8 +157,9 @@ extern "C" int nnab_stft_forward_train_staged(const nnab_frames* f, const float*
   if (rc) return rc;
   if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
   const int split = precision == NNAB_PREC_3XTF32;
-  if (!packed_hi || (split && !packed_lo) || !out || !save_re || !save_im) return NNAB_EINVAL;
+  if (!packed_hi || (split && !packed_lo) || !save_re || !save_im) return NNAB_EINVAL;
   if (out_kind != NNAB_OUT_SMOOTH_MAG && out_kind != NNAB_OUT_MEL) return NNAB_EINVAL;
+  if (!out && out_kind != NNAB_OUT_SMOOTH_MAG) return NNAB_EINVAL;  // out may be null: save slots only
   if (out_kind == NNAB_OUT_MEL && (!mel_w || n_mels < 1)) return NNAB_EINVAL;
   if (ld < g.B * g.R || ld % 32) return NNAB_EINVAL;
   if (g.B == 0) return NNAB_OK;
@@ -180,6 +194,16 @@ extern "C" int nnab_grad_to_slots(const float* g_brt, int64_t B, int32_t rows, i
   const int64_t total = (int64_t)rows * ld;
   if (total == 0) return NNAB_OK;
   to_slots_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(g_brt, B, rows, T, R, ld, out);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
+extern "C" int nnab_from_slots(const float* src, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld,
+                               float* out_brt, void* stream) {
+  if (!src || !out_brt || rows < 1 || T < 1 || R < T || ld < B * R) return NNAB_EINVAL;
+  const int64_t total = B * rows * (int64_t)T;
+  if (total == 0) return NNAB_OK;
+  from_slots_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(src, B, rows, T, R, ld, out_brt);
   NNAB_LAUNCHED();
   return NNAB_OK;
 }
