@@ -176,7 +176,7 @@ def build_workload(name: str, device, precision: str):
         cfg = CqtConfig(sr=SR)
         p = cqt2010_plan(cfg)
         eng = Cqt2010Engine(p["taps"], p["top_kernels"], p["early_stages"], p["n_octaves"], p["kernel_hop"],
-                            p["first_bin"], 12, 84, "reflect", device=device)
+                            p["first_bin"], 12, 84, "reflect", device=device, precision=precision)
         work = {"bound": "hbm", "per_batch": float(BYTES_CQT2010), "unit": "GB/s", "kernel": "cqt2010v2 chain"}
         return eng, "magnitude", work, 2 + (p["early_stages"] - 2) + 6 + 7
     raise ValueError(name)
@@ -408,10 +408,10 @@ def main():
     breakdown = {}
     if rank == 0 and world == 1 and not args.no_breakdown:
         for name in ["stft", "mel", "cqt1992v2", "cqt2010v2", "train"]:
-            for prec in (["tf32", "fp32"] if name != "cqt2010v2" else ["fp32"]):
+            for prec in ["tf32", "fp32"]:
                 if name == args.workload and prec == args.precision:
                     continue
-                e, k, w, _ = build_workload(name, device, "tf32" if name == "cqt2010v2" else prec)
+                e, k, w, _ = build_workload(name, device, prec)
                 st = name not in ("cqt2010v2", "train")
                 m, gm = run_timed(e, k, x, 20 if name != "train" else 5, 3, torch, stream, time_gemm=st)
                 r = roofline(w, m, gm if st else m)

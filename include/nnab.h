@@ -204,13 +204,18 @@ int nnab_cqt1992v2_forward_staged(const nnab_frames* f, const float* packed_hi, 
  * and the centred complex conv with the top-octave bank (n_filters, width) at
  * hop kernel_hop >> alpha; rows scattered to first_bin + j - alpha*bins_per_octave.
  * taps: the (odd, symmetric) anti-alias FIR, HOST float32 (n_taps values).
- * out (B, n_bins, T) with T = the shortest octave's frame count (returned). */
+ * out (B, n_bins, T) with T = the shortest octave's frame count (returned).
+ * precision NNAB_PREC_TF32: the fused tensor-core chain (half-band FIR as a
+ * TMEM-resident Toeplitz MMA, the whole clip in shared memory) when the clip
+ * fits; NNAB_PREC_3XTF32 (and configurations outside that envelope): FP32
+ * CUDA-core stage kernels. */
 size_t nnab_cqt2010v2_workspace_bytes(int64_t B, int64_t L, int32_t early_stages);
 int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, const float* taps, int32_t n_taps,
                            const float* k_re, const float* k_im, int32_t n_filters, int32_t width,
                            int32_t early_stages, int32_t n_octaves, int32_t kernel_hop, int32_t first_bin,
-                           int32_t bins_per_octave, int32_t n_bins, int32_t pad_mode, int32_t out_kind, float* out,
-                           int32_t* n_frames_out, void* workspace, size_t workspace_bytes, void* stream);
+                           int32_t bins_per_octave, int32_t n_bins, int32_t pad_mode, int32_t out_kind,
+                           int32_t precision, float* out, int32_t* n_frames_out, void* workspace,
+                           size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

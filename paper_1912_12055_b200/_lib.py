@@ -75,7 +75,7 @@ SIGNATURES = {
                                          _vp]),
     "nnab_cqt2010v2_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "nnab_cqt2010v2_forward": (C.c_int, [_fp, _i64, _i64, _fp, _i32, _fp, _fp, _i32, _i32, _i32, _i32, _i32, _i32,
-                                         _i32, _i32, _i32, _i32, _fp, C.POINTER(_i32), _vp, _sz, _vp]),
+                                         _i32, _i32, _i32, _i32, _i32, _fp, C.POINTER(_i32), _vp, _sz, _vp]),
 }
 
 _lib = None

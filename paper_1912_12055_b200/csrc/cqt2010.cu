@@ -130,8 +130,8 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
                                       const float* k_re, const float* k_im, int32_t n_filters, int32_t width,
                                       int32_t early_stages, int32_t n_octaves, int32_t kernel_hop, int32_t first_bin,
                                       int32_t bins_per_octave, int32_t n_bins, int32_t pad_mode, int32_t out_kind,
-                                      float* out, int32_t* n_frames_out, void* workspace, size_t workspace_bytes,
-                                      void* stream) {
+                                      int32_t precision, float* out, int32_t* n_frames_out, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
   if (!x || !taps || !k_re || !k_im || !out || n_taps < 3 || n_taps % 2 == 0) return NNAB_EINVAL;
   if (n_octaves < 1 || kernel_hop < 1 || width < 1 || n_filters < 1 || early_stages < 0) return NNAB_EINVAL;
   if ((kernel_hop >> (n_octaves - 1)) < 1) return NNAB_EINVAL;  // transforms.py:253-257
@@ -157,11 +157,16 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
   }
   if (n_frames_out) *n_frames_out = T;
   if (B == 0) return NNAB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == NNAB_PREC_TF32) {  // fused tensor-core chain when the clip fits in shared memory
+    const int rc = launch_cqt2010_tc(x, B, L, taps, n_taps, k_re, k_im, n_filters, width, early_stages, n_octaves,
+                                     kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind, T, out, s);
+    if (rc != NNAB_ENOTSUP) return rc;
+  }
   if (!workspace || workspace_bytes < nnab_cqt2010v2_workspace_bytes(B, L, early_stages)) return NNAB_EINVAL;
 
   // symmetric pair list of the non-negligible taps (taps are a HOST array)
   const float* h = taps;
-  cudaStream_t s = (cudaStream_t)stream;
   FirPairs fp{};
   fp.half = (n_taps - 1) / 2;
   fp.centre = h[fp.half];

@@ -331,8 +331,11 @@ class Cqt2010Engine:
 
     def __init__(self, taps: np.ndarray, top_kernels: np.ndarray, early_stages: int, n_octaves: int,
                  kernel_hop: int, first_bin: int, bins_per_octave: int, n_bins: int, pad_mode: str = "reflect",
-                 device="cuda"):
+                 device="cuda", precision: str = "tf32"):
         self.device = _require_cuda(device)
+        if precision not in L.PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
+        self.precision = L.PRECISIONS[precision]
         self.taps = np.ascontiguousarray(np.asarray(taps, dtype=np.float32))
         k = np.asarray(top_kernels)
         self.k_re = torch.from_numpy(np.ascontiguousarray(k.real, dtype=np.float32)).to(self.device)
@@ -358,7 +361,8 @@ class Cqt2010Engine:
             None if x is None else x.data_ptr(), B, length, self.taps.ctypes.data, self.taps.size,
             self.k_re.data_ptr(), self.k_im.data_ptr(), self.n_filters, self.width, self.early_stages,
             self.n_octaves, self.kernel_hop, self.first_bin, self.bins_per_octave, self.n_bins, self.pad_mode,
-            kinds[kind], None if out is None else out.data_ptr(), C.byref(T), None if ws is None else ws.data_ptr(),
+            kinds[kind], self.precision, None if out is None else out.data_ptr(), C.byref(T),
+            None if ws is None else ws.data_ptr(),
             0 if ws is None else ws.numel(), L.stream_handle(self.device))
         return rc, T.value
 
@@ -369,7 +373,7 @@ class Cqt2010Engine:
         rc = lib.nnab_cqt2010v2_forward(dummy.data_ptr(), 0, length, self.taps.ctypes.data, self.taps.size,
                                         self.k_re.data_ptr(), self.k_im.data_ptr(), self.n_filters, self.width,
                                         self.early_stages, self.n_octaves, self.kernel_hop, self.first_bin,
-                                        self.bins_per_octave, self.n_bins, self.pad_mode, L.OUT_MAGNITUDE,
+                                        self.bins_per_octave, self.n_bins, self.pad_mode, L.OUT_MAGNITUDE, self.precision,
                                         dummy.data_ptr(), C.byref(T), None, 0, L.stream_handle(self.device))
         L.check(rc, "cqt2010v2_forward")
         return T.value

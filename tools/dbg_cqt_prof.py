@@ -1,0 +1,23 @@
+import sys, ctypes as C
+sys.path.insert(0, ".")
+import torch
+from paper_1912_12055_b200 import _lib as L
+from paper_1912_12055_b200.engine import Cqt2010Engine
+from paper_1912_12055_b200.spectro import CqtConfig, cqt2010_plan
+lib = L.load()
+fn = lib.nnab_debug_cqt2010_profile
+fn.restype = C.c_int; fn.argtypes = [C.c_int, C.c_void_p]
+dev = torch.device("cuda:0")
+p = cqt2010_plan(CqtConfig(sr=44100.0))
+eng = Cqt2010Engine(p["taps"], p["top_kernels"], p["early_stages"], p["n_octaves"], p["kernel_hop"], p["first_bin"], 12, 84, "reflect", device=dev)
+x = torch.randn(1770, 80000, device=dev) * 0.5
+eng.forward(x); torch.cuda.synchronize()
+fn(1, None)
+eng.forward(x); torch.cuda.synchronize()
+out = (C.c_ulonglong * 16)()
+fn(0, out)
+names = ["E1 build", "E1 mma", "E1 epi", "E2 build", "E2 mma", "E2 epi", "oct build", "oct mma", "oct epi",
+         "conv build", "conv mma", "conv epi", "E1 prefetch", "E1 wait", "reflect/shift", "margins"]
+tot = sum(out)
+for n, v in zip(names, out):
+    print(f"{n:14s} {v/148/12:10.0f} cycles/clip  {100*v/tot:5.1f}%")
