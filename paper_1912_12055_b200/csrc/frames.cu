@@ -46,52 +46,74 @@ int frame_geometry(const nnab_frames* f, FrameGeom* g) {
 
 // rows[(b*R + r)*row_len + c] = padded_b[r*hop + c]  (0 beyond the padded clip),
 // TF32-rounded (split=0) or split into tf32 hi + tf32 lo residual (split=1).
+// One CTA walks whole rows (no 64-bit divisions per element); interior groups of
+// 4 samples are one aligned 16-byte load, the reflect/zero edges go element-wise.
 __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict__ x, int64_t B, int64_t L,
                                                          int32_t pad, int32_t mode, int32_t hop, int32_t row_len,
                                                          int32_t R, int64_t padded_len, int split,
                                                          float* __restrict__ hi, float* __restrict__ lo) {
   const int32_t q_per_row = row_len / 4;
-  const int64_t total = B * (int64_t)R * q_per_row;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t grow = e / q_per_row;
-    const int32_t c0 = (int32_t)(e - grow * q_per_row) * 4;
+  const int64_t rows = B * (int64_t)R;
+  const bool aligned_clips = (L % 4) == 0 && (pad % 4) == 0 && (hop % 4) == 0;
+  const int per = q_per_row < (int)blockDim.x ? q_per_row : (int)blockDim.x;  // threads per row
+  const int rpb = blockDim.x / per;                                           // rows per block step
+  const int sub = threadIdx.x / per, lane = threadIdx.x - sub * per;
+  if (sub >= rpb) return;
+  for (int64_t grow = (int64_t)blockIdx.x * rpb + sub; grow < rows; grow += (int64_t)gridDim.x * rpb) {
     const int64_t b = grow / R;
     const int64_t r = grow - b * R;
     const float* xb = x + b * L;
-    float v[4];
+    float4* hrow = reinterpret_cast<float4*>(hi) + grow * q_per_row;
+    float4* lrow = reinterpret_cast<float4*>(lo) + grow * q_per_row;
+    for (int32_t q = lane; q < q_per_row; q += per) {
+      const int64_t i0 = r * hop + 4 * q;  // padded position of the first sample
+      const int64_t j0 = i0 - pad;         // source sample
+      float v[4];
+      if (aligned_clips && j0 >= 0 && j0 + 3 < L && i0 + 3 < padded_len) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(xb + j0));
+        v[0] = w.x;
+        v[1] = w.y;
+        v[2] = w.z;
+        v[3] = w.w;
+      } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = r * hop + c0 + u;  // position in the padded clip
-      float s = 0.f;
-      if (i < padded_len) {
-        int64_t j = i - pad;
-        if (mode == NNAB_PAD_REFLECT) {
-          if (j < 0) j = -j;
-          if (j >= L) j = 2 * (L - 1) - j;
-          s = __ldg(xb + j);
-        } else if (j >= 0 && j < L) {
-          s = __ldg(xb + j);
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = i0 + u;
+          float sv = 0.f;
+          if (i < padded_len) {
+            int64_t j = i - pad;
+            if (mode == NNAB_PAD_REFLECT) {
+              if (j < 0) j = -j;
+              if (j >= L) j = 2 * (L - 1) - j;
+              sv = __ldg(xb + j);
+            } else if (j >= 0 && j < L) {
+              sv = __ldg(xb + j);
+            }
+          }
+          v[u] = sv;
         }
       }
-      v[u] = s;
+      float4 h, l;
+      h.x = tf32_rne(v[0]);
+      h.y = tf32_rne(v[1]);
+      h.z = tf32_rne(v[2]);
+      h.w = tf32_rne(v[3]);
+      hrow[q] = h;
+      if (split) {
+        l.x = tf32_rne(v[0] - h.x);
+        l.y = tf32_rne(v[1] - h.y);
+        l.z = tf32_rne(v[2] - h.z);
+        l.w = tf32_rne(v[3] - h.w);
+        lrow[q] = l;
+      }
     }
-    float4 h, l;
-    float* hp = &h.x;
-    float* lp = &l.x;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      hp[u] = tf32_rne(v[u]);
-      lp[u] = tf32_rne(v[u] - hp[u]);
-    }
-    reinterpret_cast<float4*>(hi)[e] = h;
-    if (split) reinterpret_cast<float4*>(lo)[e] = l;
   }
 }
 
 int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows_lo, int split, cudaStream_t s) {
-  const int64_t total = g.B * (int64_t)g.R * (g.row_len / 4);
-  if (total == 0) return NNAB_OK;
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+  const int64_t rows = g.B * (int64_t)g.R;
+  if (rows == 0) return NNAB_OK;
+  const int blocks = (int)std::min<int64_t>(rows, (int64_t)num_sms() * 16);
   stage_rows_kernel<<<blocks, 256, 0, s>>>(x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.row_len, g.R, g.padded_len,
                                           split, rows_hi, rows_lo);
   NNAB_LAUNCHED();

@@ -21,6 +21,7 @@
 //   warp 2      TMEM allocator
 //   warps 4..7  epilogue: thread = accumulator row = one frame slot
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -34,13 +35,14 @@ constexpr int kBN = 256;  // 128 bins x {cos, sin}
 constexpr int kThreads = 256;
 constexpr int kMelRows = 128;  // mel accumulator rows resident in smem
 
-template <bool kSplit>
+template <bool kSplit, bool kPair>
 struct Cfg {
   static constexpr int BK = kSplit ? 16 : 32;            // fp32 elements per K block
   static constexpr int SWZ = BK * 4;                     // swizzle span in bytes (64 or 128)
   static constexpr int A_BYTES = kBM * BK * 4;           // 16 KB | 8 KB
-  static constexpr int B_BYTES = kBN * BK * 4;           // 32 KB | 16 KB
-  static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);  // 48 KB either way
+  // a CTA pair splits the N = 256 bank rows: each CTA stages 128 of them
+  static constexpr int B_BYTES = (kPair ? kBN / 2 : kBN) * BK * 4;
+  static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);  // 48 KB | 32 KB (pair)
   // TF32: two 256-column accumulators (double buffer).  3xTF32: one buffer of
   // main (hi*hi) + correction (hi*lo + lo*hi) accumulators.  Keeping the large
   // hi*hi chain apart from the small cross terms cuts the number of
@@ -62,6 +64,7 @@ struct Params {
   // longest-first so the first MMA (N = max) initialises every used column.
   const uint32_t* kb_tab;
   int32_t n_tab, b_box, pairs;
+  int32_t stages;  // smem pipeline depth (4, or 3 when the Mel accumulator takes 64 KB)
   // training forward: re, im and smoothed magnitude per (bin, slot) saved in
   // slot-major layout [bin][ld_slots] for the backward GEMMs (may be null)
   float *save_re, *save_im, *save_mag;
@@ -91,24 +94,25 @@ NNAB_DEV float finish(float re, float im, int kind, float power, float eps) {
   return sqrtf(p);
 }
 
-template <bool kSplit>
+template <bool kSplit, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     stft_gemm_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                      const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
                      const Params p) {
-  using C = Cfg<kSplit>;
+  using C = Cfg<kSplit, kPair>;
   const bool mel = p.out_kind == NNAB_OUT_MEL;
-  const int stages = mel ? 3 : 4;
+  const int stages = p.stages;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0;  // 0 = leader (issues the pair's MMAs)
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* mel_acc = reinterpret_cast<float*>(smem + stages * C::STAGE_BYTES);  // [kMelRows][kBM]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * C::STAGE_BYTES + (mel ? kMelRows * kBM * 4 : 0));
-  uint64_t* full = bars;            // [stages]
-  uint64_t* empty = bars + 4;       // [stages]
-  uint64_t* tmem_full = bars + 8;   // [2]
-  uint64_t* tmem_empty = bars + 10; // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* full = bars;            // [stages]  (pair: only the leader's are used)
+  uint64_t* empty = bars + 8;       // [stages]
+  uint64_t* tmem_full = bars + 16;  // [2]
+  uint64_t* tmem_empty = bars + 18; // [2]       (pair: the leader's counts both CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -126,11 +130,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], kBM);
+      mbar_init(&tmem_empty[i], kPair ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (kPair) cluster_sync();  // the peer's TMA / arrives target the leader's barriers
+  if (warp == 2) {
+    if (kPair) tmem_alloc_pair<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   if (mel) {
     for (int i = threadIdx.x; i < kMelRows * kBM; i += kThreads) mel_acc[i] = 0.f;
   }
@@ -138,10 +146,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // M-tile walk: one CTA per M tile, or one pair per two consecutive M tiles
+  const int m_start = kPair ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int m_step = kPair ? (int)nclusters_x() : (int)gridDim.x;
+  const int m_end = kPair ? (p.n_mtiles + 1) / 2 : p.n_mtiles;
 
   const int nt = p.n_tiles;
   const int n_iter = p.kb_tab ? p.n_tab : p.kblocks;
-  const uint32_t stage_tx = (uint32_t)(C::A_BYTES + p.b_box * C::BK * 4) * (kSplit ? 2 : 1);
+  const int b_rows = kPair ? p.b_box / 2 : p.b_box;  // bank rows this CTA stages per K block
+  const uint32_t stage_tx = (uint32_t)(C::A_BYTES + b_rows * C::BK * 4) * (kSplit ? 2 : 1) * (kPair ? 2 : 1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -149,21 +162,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t keep = policy_evict_last();
       int s = 0;
       uint32_t ph = 0;
-      for (int mt = blockIdx.x; mt < p.n_mtiles; mt += gridDim.x) {
+      for (int mi = m_start; mi < m_end; mi += m_step) {
+        const int mt = kPair ? 2 * mi + (int)rank : mi;
         for (int n = 0; n < nt; ++n) {
           for (int it = 0; it < n_iter; ++it) {
-            const int kb = p.kb_tab ? (int)(__ldg(p.kb_tab + n * p.n_tab + it) >> 16) : it;
+            const uint32_t e = p.kb_tab ? __ldg(p.kb_tab + n * p.n_tab + it) : 0u;
+            const int kb = p.kb_tab ? (int)(e >> 16) : it;
+            // pair: the peer stages bank rows [N/2, N) of this K block's MMA width N
+            const int b_row = n * kBN + (kPair && rank ? (p.kb_tab ? (int)(e & 0xffffu) / 2 : kBN / 2) : 0);
             mbar_wait(&empty[s], ph ^ 1);
             uint8_t* st = smem + s * C::STAGE_BYTES;
-            mbar_expect_tx(&full[s], stage_tx);
             const int k = kb * C::BK;
             const int a_col = k % p.row_len;
             const int a_row = mt * kBM + k / p.row_len;
-            tma_load_2d_hint(st, &tm_a_hi, &full[s], a_col, a_row, keep);
-            tma_load_2d_hint(st + C::A_BYTES, &tm_b_hi, &full[s], k, n * kBN, keep);
-            if (kSplit) {
-              tma_load_2d_hint(st + C::A_BYTES + C::B_BYTES, &tm_a_lo, &full[s], a_col, a_row, keep);
-              tma_load_2d_hint(st + 2 * C::A_BYTES + C::B_BYTES, &tm_b_lo, &full[s], k, n * kBN, keep);
+            if (kPair) {
+              const uint32_t fb = mapa(&full[s], 0);
+              if (rank == 0) mbar_expect_tx(&full[s], stage_tx);
+              tma_load_2d_pair(st, &tm_a_hi, fb, a_col, a_row, keep);
+              tma_load_2d_pair(st + C::A_BYTES, &tm_b_hi, fb, k, b_row, keep);
+              if (kSplit) {
+                tma_load_2d_pair(st + C::A_BYTES + C::B_BYTES, &tm_a_lo, fb, a_col, a_row, keep);
+                tma_load_2d_pair(st + 2 * C::A_BYTES + C::B_BYTES, &tm_b_lo, fb, k, b_row, keep);
+              }
+            } else {
+              mbar_expect_tx(&full[s], stage_tx);
+              tma_load_2d_hint(st, &tm_a_hi, &full[s], a_col, a_row, keep);
+              tma_load_2d_hint(st + C::A_BYTES, &tm_b_hi, &full[s], k, b_row, keep);
+              if (kSplit) {
+                tma_load_2d_hint(st + C::A_BYTES + C::B_BYTES, &tm_a_lo, &full[s], a_col, a_row, keep);
+                tma_load_2d_hint(st + 2 * C::A_BYTES + C::B_BYTES, &tm_b_lo, &full[s], k, b_row, keep);
+              }
             }
             if (++s == stages) { s = 0; ph ^= 1; }
           }
@@ -173,20 +201,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (elect_one()) {
-      constexpr uint32_t idesc_full = idesc_tf32(kBM, kBN);
+    if (rank == 0 && elect_one()) {
+      constexpr uint32_t kM = kPair ? 2 * kBM : kBM;
+      constexpr uint32_t idesc_full = idesc_tf32(kM, kBN);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (int mt = blockIdx.x; mt < p.n_mtiles; mt += gridDim.x) {
+      for (int mi = m_start; mi < m_end; mi += m_step) {
         for (int n = 0; n < nt; ++n) {
           mbar_wait(&tmem_empty[acc], aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem_base + acc * C::ACC_STRIDE;
           for (int kb = 0; kb < n_iter; ++kb) {
             uint32_t idesc = idesc_full;
-            if (p.kb_tab) idesc = idesc_tf32(kBM, __ldg(p.kb_tab + n * p.n_tab + kb) & 0xffffu);
+            if (p.kb_tab) idesc = idesc_tf32(kM, __ldg(p.kb_tab + n * p.n_tab + kb) & 0xffffu);
             mbar_wait(&full[s], ph);
             tc_fence_after();
             uint8_t* st = smem + s * C::STAGE_BYTES;
@@ -195,18 +224,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < C::BK / 8; ++k) {
               const uint64_t off = (uint64_t)((k * 32) >> 4);  // 8 tf32 = 32 bytes along K
-              mma_tf32(d, a_hi + off, b_hi + off, idesc, (kb | k) != 0);
-              if (kSplit) {
-                const uint64_t a_lo = make_sdesc(st + C::A_BYTES + C::B_BYTES, C::SWZ);
-                const uint64_t b_lo = make_sdesc(st + 2 * C::A_BYTES + C::B_BYTES, C::SWZ);
-                mma_tf32(d + kBN, a_hi + off, b_lo + off, idesc, (kb | k) != 0);
-                mma_tf32(d + kBN, a_lo + off, b_hi + off, idesc, 1);
+              const uint64_t a_lo = make_sdesc(st + C::A_BYTES + C::B_BYTES, C::SWZ);
+              const uint64_t b_lo = make_sdesc(st + 2 * C::A_BYTES + C::B_BYTES, C::SWZ);
+              if (kPair) {
+                mma_tf32_pair(d, a_hi + off, b_hi + off, idesc, (kb | k) != 0);
+                if (kSplit) {
+                  mma_tf32_pair(d + kBN, a_hi + off, b_lo + off, idesc, (kb | k) != 0);
+                  mma_tf32_pair(d + kBN, a_lo + off, b_hi + off, idesc, 1);
+                }
+              } else {
+                mma_tf32(d, a_hi + off, b_hi + off, idesc, (kb | k) != 0);
+                if (kSplit) {
+                  mma_tf32(d + kBN, a_hi + off, b_lo + off, idesc, (kb | k) != 0);
+                  mma_tf32(d + kBN, a_lo + off, b_hi + off, idesc, 1);
+                }
               }
             }
-            mma_commit(&empty[s]);
+            if (kPair) mma_commit_pair(&empty[s], 0x3);
+            else mma_commit(&empty[s]);
             if (++s == stages) { s = 0; ph ^= 1; }
           }
-          mma_commit(&tmem_full[acc]);
+          if (kPair) mma_commit_pair(&tmem_full[acc], 0x3);
+          else mma_commit(&tmem_full[acc]);
           if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
         }
       }
@@ -220,7 +259,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int F = p.n_bins;
     int acc = 0;
     uint32_t aph = 0;
-    for (int mt = blockIdx.x; mt < p.n_mtiles; mt += gridDim.x) {
+    const uint32_t empty_addr0 = kPair ? mapa(&tmem_empty[0], 0) : smem_u32(&tmem_empty[0]);
+    auto release_acc = [&](int a) {  // one arrive per warp on the (leader's) tmem_empty
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(empty_addr0 + 8 * a);
+    };
+    for (int mi = m_start; mi < m_end; mi += m_step) {
+      const int mt = kPair ? 2 * mi + (int)rank : mi;
       const int64_t g = (int64_t)mt * kBM + row;
       const int64_t b = g / p.R;
       const int t = (int)(g - b * p.R);
@@ -262,8 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
-          tc_fence_before();
-          mbar_arrive(&tmem_empty[acc]);
+          release_acc(acc);
           if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
           continue;
         }
@@ -352,8 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tmem_empty[acc]);
+        release_acc(acc);
         if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
       }
       if (kind == NNAB_OUT_MEL) {
@@ -374,25 +418,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync();  // the peer's TMEM is written by the leader's MMAs until the end
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<512>(tmem_base);
+  if (warp == 2) {
+    if (kPair) tmem_dealloc_pair<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
+  }
 }
 
-template <bool kSplit>
+template <bool kSplit, bool kPair>
 int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
-  using C = Cfg<kSplit>;
+  using C = Cfg<kSplit, kPair>;
   const bool mel = a.out_kind == NNAB_OUT_MEL;
   if (mel && (a.n_mels < 1 || a.n_mels > kMelRows || !a.mel_w || a.mel_ld % 4 != 0)) return NNAB_ENOTSUP;
   if (g.row_len % C::BK != 0) return NNAB_ENOTSUP;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   const uint64_t rows_total = (uint64_t)g.B * g.R;
   const uint64_t bank_rows = (uint64_t)a.n_tiles * kBN;
-  int rc = make_tmap_2d(&ta_hi, a.a_hi, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
   const int b_box = a.b_box > 0 ? a.b_box : kBN;
   if (b_box % 16 != 0 || b_box > kBN) return NNAB_EINVAL;
-  if (!rc) rc = make_tmap_2d(&tb_hi, a.b_hi, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, b_box, C::SWZ);
+  const int b_rows = kPair ? b_box / 2 : b_box;  // each CTA of a pair stages half the bank rows
+  int rc = make_tmap_2d(&ta_hi, a.a_hi, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
+  if (!rc) rc = make_tmap_2d(&tb_hi, a.b_hi, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, b_rows, C::SWZ);
   if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, a.a_lo, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
-  if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, a.b_lo, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, b_box, C::SWZ);
+  if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, a.b_lo, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, b_rows, C::SWZ);
   if (rc) return rc;
   if (!kSplit) {
     ta_lo = ta_hi;
@@ -427,12 +476,35 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.pairs = a.pairs;
   if (a.kb_tab && (a.n_tab < 1 || mel)) return NNAB_EINVAL;
   if (p.n_mtiles == 0) return NNAB_OK;
-  const int stages = mel ? 3 : 4;
-  const size_t smem = 1024 + (size_t)stages * C::STAGE_BYTES + (mel ? kMelRows * kBM * 4 : 0) + 128;
-  auto kern = stft_gemm_kernel<kSplit>;
+  // as many pipeline stages as fit next to the Mel accumulator (<= 8)
+  const size_t mel_bytes = mel ? (size_t)kMelRows * kBM * 4 : 0;
+  constexpr size_t kBudget = 227 * 1024 - 1024 - 256;  // max dynamic smem - alignment slack - barriers
+  int stages = (int)std::min<size_t>(8, (kBudget - mel_bytes) / C::STAGE_BYTES);
+  if (const char* e = getenv("NNAB_DEBUG_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));
+  p.stages = stages;
+  const size_t smem = 1024 + (size_t)stages * C::STAGE_BYTES + mel_bytes + 256;
+  auto kern = stft_gemm_kernel<kSplit, kPair>;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = std::min(p.n_mtiles, num_sms());
-  kern<<<grid, kThreads, smem, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+  if (!kPair) {
+    const int grid = std::min(p.n_mtiles, num_sms());
+    kern<<<grid, kThreads, smem, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+  } else {
+    const int pairs = (p.n_mtiles + 1) / 2;
+    const int grid = 2 * std::min(pairs, num_sms() / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    NNAB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta_hi, ta_lo, tb_hi, tb_lo, p));
+  }
   NNAB_LAUNCHED();
   return NNAB_OK;
 }
@@ -440,8 +512,13 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
 }  // namespace
 
 int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, cudaStream_t s) {
-  if (precision == NNAB_PREC_3XTF32) return launch_impl<true>(g, a, s);
-  if (precision == NNAB_PREC_TF32) return launch_impl<false>(g, a, s);
+  // CTA pairs (cta_group::2, M = 256) by default; NNAB_CTA_PAIR=0 selects one CTA per M tile
+  static const bool pair = [] {
+    const char* e = getenv("NNAB_CTA_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  if (precision == NNAB_PREC_3XTF32) return pair ? launch_impl<true, true>(g, a, s) : launch_impl<true, false>(g, a, s);
+  if (precision == NNAB_PREC_TF32) return pair ? launch_impl<false, true>(g, a, s) : launch_impl<false, false>(g, a, s);
   return NNAB_EINVAL;
 }
 
