@@ -16,8 +16,8 @@ fn(1, None)
 eng.forward(x); torch.cuda.synchronize()
 out = (C.c_ulonglong * 16)()
 fn(0, out)
-names = ["E1 build", "E1 mma", "E1 epi", "E2 build", "E2 mma", "E2 epi", "oct build", "oct mma", "oct epi",
-         "conv build", "conv mma", "conv epi", "E1 prefetch", "E1 wait", "reflect/shift", "margins"]
+names = ["S1 planes", "S1 mma wait", "S1 epi", "-", "S2 mma", "S2 epi", "-", "oct mma", "oct epi/cuda",
+         "conv im2col", "conv mma", "conv epi", "scale scan", "-", "-", "tail"]
 tot = sum(out)
 for n, v in zip(names, out):
-    print(f"{n:14s} {v/148/12:10.0f} cycles/clip  {100*v/tot:5.1f}%")
+    print(f"{n:14s} {v/1770:10.0f} cycles/clip/CTA  {100*v/tot:5.1f}%")
