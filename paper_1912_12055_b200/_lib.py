@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnnab.so")
+LIB_PATH = os.environ.get("NNAB_LIB") or os.path.join(_HERE, "libnnab.so")  # NNAB_LIB: debug builds
 
 OK, EINVAL, ECUDA, ENOTSUP, ENODEV = 0, 1, 2, 3, 4
 PAD_REFLECT, PAD_ZERO = 0, 1

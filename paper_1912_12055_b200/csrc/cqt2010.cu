@@ -160,8 +160,7 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
   cudaStream_t s = (cudaStream_t)stream;
   if (precision == NNAB_PREC_TF32) {  // fused tensor-core chain when the clip fits in shared memory
     const int rc = launch_cqt2010_tc(x, B, L, taps, n_taps, k_re, k_im, n_filters, width, early_stages, n_octaves,
-                                     kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind, T, out,
-                                     workspace, workspace_bytes, s);
+                                     kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind, T, out, s);
     if (rc != NNAB_ENOTSUP) return rc;
   }
   if (!workspace || workspace_bytes < nnab_cqt2010v2_workspace_bytes(B, L, early_stages)) return NNAB_EINVAL;

@@ -1,11 +1,14 @@
-// CQT2010v2 on the tensor cores: the whole octave recursion of one clip per
-// CTA, two CTAs per SM so one clip's CUDA-core phases overlap the other's MMAs
+// CQT2010v2 on the tensor cores: the whole octave recursion of one clip in one
+// CTA (one per SM, persistent over clips), every intermediate signal in shared
+// memory, so HBM sees the clip once and the output once
 // (transforms.py:290-313, signal.py:232-247).
 //
-// Operands are FP16 with an exact per-clip power-of-two scale (2^-e, e from the
-// clip's peak), so they carry the same 11-bit significand as TF32 at twice the
-// tcgen05 rate (kind::f16, K = 16); accumulation is FP32 and the scale is undone
-// exactly in the conv epilogue.
+// Operands are FP16 with an exact per-clip power-of-two scale 2^-e (e from the
+// clip's peak), i.e. the same 11-bit significand as TF32 at twice the tcgen05
+// rate (kind::f16, K = 16); accumulation is FP32 and the scale is undone exactly
+// in the conv epilogue.  The peak comes from a dedicated scan warp that streams
+// the NEXT clip through a bulk-copy ring while the other warps work on the
+// current one (so the clip is in L2 when stage 1 reads it).
 //
 // Half-band FIR as a banded Toeplitz MMA.  downsample2 keeps
 //   y[i] = sum_d h[d] x_ext[2i + d],  d = -127..127 (reflect-extended x)
@@ -14,24 +17,23 @@
 // xo[m] = x_ext[2m - 127] (the odd phase).  A block of 128 outputs is
 // Y[r] = sum_s T[r][s] W[s], T[r][s] = g_{s-r} (128 x 256 Toeplitz band), W = 256
 // consecutive odd-phase samples; windows of consecutive blocks overlap by 128.
-//   A = T with its rows reversed: A'[r'][s] = g[s + r' - 127] depends on s + r'
+//   A = "planes": the odd phase stored once as rows of 128 samples, plane q
+//       holding the 16-byte chunk q of every row (rows 16 B apart); block n's
+//       window is rows n, n+1, i.e. a 16-byte start offset (LBO = plane stride);
+//       M = 128 blocks per MMA.
+//   B = T with its rows reversed: T'[r'][s] = g[s + r' - 127] depends on s + r'
 //       only, so the band lives in a 6 KB "diagonal" array (chunk j = 8 taps
 //       g[j-127 ..]) that a no-swizzle K-major descriptor with LBO = SBO = 128 B
-//       walks (toep_desc),
-//   B = "planes": the odd phase stored once as rows of 128 samples, plane q
-//       holding the 16-byte chunk q of every row (rows 16 B apart); block n's
-//       window is rows n, n+1, i.e. a 16-byte start offset (LBO = plane stride).
-// The MMA is issued transposed, D[block][r'] = sum_s W_block[s] T'[r'][s]
-// (M = 128 blocks, N = 128 reversed offsets), so each TMEM lane holds 128
-// consecutive outputs of one block and the epilogue stores 16-byte vectors.
-// The producing epilogue writes every signal straight into the next stage's
-// layouts (odd phase -> planes in shared memory, contiguous copy with reflect
-// margins -> an L2-resident per-CTA scratch), so no separate deinterleave pass
-// exists except for the clip itself (stage 1, built from global memory).
+//       walks; N = 128 output offsets.
+//   D[block][r'] in TMEM: each lane holds 128 consecutive outputs of one block,
+//       so the epilogue writes 16-byte vectors.
+// Each epilogue writes its signal straight into the next stage's layouts (odd
+// phase -> planes, even phase / contiguous copy with reflect margins -> centre
+// taps and conv frames); a small edge pass adds the reflect images.
 // Per-octave centred complex conv (<= 16 bins x <= 96 taps, hop h >> alpha):
-// im2col MMA, A = 128 frames x 96 taps (built from the L2 copy), B = 32 rows
-// (re/im of each bin) x 96 taps, D = 128 x 32 in TMEM; thread = frame in the
-// epilogue so the (B, n_bins, T) output is written coalesced along T.
+// frames as N (im2col B tile, <= 256 frames), the filter bank as A (M = 128
+// rows, re/im of bin j at row 32 (j % 4) + 2 (j / 4) + {0, 1} so every TMEM lane
+// quarter carries bins), D = 128 x frames.
 #include <algorithm>
 #include <cmath>
 
@@ -43,37 +45,38 @@
 namespace nnab {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kTile1 = 128;       // stage-1 blocks (N) per MMA tile
-constexpr int ML = 128;           // reflect margins of the contiguous octave copies (fp16 elements)
-constexpr int KC = 96;            // conv taps (K), padded
-constexpr int NCONV = 32;         // conv N: re/im rows of <= 16 bins
-constexpr int kFiltLog2 = 6;      // conv bank scaled by 2^6 before the FP16 rounding
+constexpr int kCompute = 256;             // warps 0-7: MMA issue (thread 0), builds, epilogues
+constexpr int kThreads = kCompute + 32;   // warp 8: scan of the next clip
+constexpr int kTile1 = 128;               // stage-1 blocks per MMA tile (= M)
+constexpr int ML = 128;                   // reflect margins of the contiguous signal copies (fp16)
+constexpr int KC = 96;                    // conv taps (K), padded
+constexpr int kFiltLog2 = 6;              // conv bank scaled by 2^6 before the FP16 rounding
 constexpr int kMaxOct = 12;
 constexpr int TOEP_CHUNKS = 8 * 31 + 128;  // 376 diagonal chunks of 8 taps
-constexpr uint32_t kConvCol = 128;          // TMEM columns of the conv accumulators
+constexpr uint32_t kConvCol = 256;          // TMEM columns of the conv accumulators (2 x 32)
+constexpr int NCONV = 32;                   // conv N: re/im rows of <= 16 bins
+constexpr uint32_t kRing = 16384;           // scan ring slot (bytes), 2 slots
 
 struct TcParams {
   const float* x;
   int64_t B, L;
   int32_t L1, L0, n1_tiles;
   int32_t n_oct, kernel_hop, first_bin, bpo, n_bins, n_filt, width, T, out_kind;
-  int32_t pad, pad_al;
-  int32_t oct_len[kMaxOct];         // signal length of octave alpha
-  int32_t oct_blocks[kMaxOct];      // 128-output blocks of the halving that produces octave alpha
-  int32_t plane_rows[kMaxOct];      // rows of the odd-phase planes that feed halving alpha+1
-  int64_t s_off[kMaxOct];           // scratch offset (fp16 elements) of octave alpha's contiguous copy
-  int64_t ye_off, cta_stride;       // stage-1 even phase; per-CTA scratch size
-  __half* scratch;
-  float h0;                         // centre tap
-  float g[128];                     // odd taps g_j = h[2j - 127]
-  const float* k_re;                // top-octave bank (n_filt, width), device
+  int32_t pad, pad_al, rows2;          // conv pad, pad rounded to 8, rows of the (compact) second frame tile
+  int32_t oct_len[kMaxOct];            // signal length of octave alpha
+  int32_t oct_blocks[kMaxOct];         // 128-output blocks of the halving producing octave alpha
+  int32_t plane_rows[kMaxOct];         // rows of octave alpha's odd-phase planes (feed halving alpha+1)
+  int32_t s_off[kMaxOct];              // smem offset of octave alpha's contiguous copy (with ML margins)
+  int32_t o_off[kMaxOct];              // smem offset of octave alpha's planes
+  float h0;                            // centre tap
+  float g[128];                        // odd taps g_j = h[2j - 127]
+  const float* k_re;                   // top-octave bank (n_filt, width), device
   const float* k_im;
   float* out;
   // shared-memory carve-up (bytes from the 1 KB-aligned base)
-  int32_t off_toep, off_filt, off_ra, off_rb, off_bars;
-  int32_t pl_x, pl_y, y_rows;       // plane strides (bytes) of the stage-1 / stage-2 inputs; stage-2 plane rows
-  unsigned long long* prof;         // optional per-phase cycle counters (nnab_debug_cqt2010_profile)
+  int32_t off_toep, off_filt, off_ring, off_x, off_xe, off_y, off_ye, off_col, off_bars;
+  int32_t pl_x, pl_y, y_rows;          // plane strides (bytes); stage-2 plane rows
+  unsigned long long* prof;            // optional per-phase cycle counters (nnab_debug_cqt2010_profile)
 };
 
 // Phase clock of thread 0 (only when p.prof is set); accumulators in shared memory.
@@ -89,11 +92,7 @@ struct Prof {
   }
 };
 
-NNAB_DEV int64_t refl(int64_t j, int64_t n) {
-  if (j < 0) j = -j;
-  if (j >= n) j = 2 * (n - 1) - j;
-  return j;
-}
+NNAB_DEV void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory"); }  // compute warps only
 
 NNAB_DEV uint64_t nsw_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {  // no-swizzle K-major
   uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
@@ -110,11 +109,23 @@ NNAB_DEV uint32_t plane_off(int m, uint32_t pl) {
 
 NNAB_DEV __half h16(float v) { return __float2half_rn(v); }
 
+// Contiguous FP16 signal arrays in shared memory are read and written by lanes
+// 128 samples apart (lane = block); the 16-byte chunk index inside each 256-byte
+// row is XORed with the row index so those accesses spread over all banks.
+// Aligned runs of <= 8 samples stay contiguous; arrays are whole 128-sample rows.
+#ifdef NNAB_NO_SWZ
+NNAB_DEV int sw(int i) { return i; }
+#else
+NNAB_DEV int sw(int i) { return i ^ (((i >> 7) & 15) << 3); }
+#endif
+NNAB_DEV uint4 ld8(const __half* a, int i) { return *reinterpret_cast<const uint4*>(a + sw(i)); }
+NNAB_DEV void st8(__half* a, int i, uint4 v) { *reinterpret_cast<uint4*>(a + sw(i)) = v; }
+
 struct Ctx {
   const TcParams& p;
   uint8_t* base;
   uint32_t tmem;
-  uint64_t* bar;      // MMA completion
+  uint64_t* bar;  // MMA completion
   uint32_t phase;
   Prof pf;
   NNAB_DEV void wait_mma() {
@@ -124,12 +135,9 @@ struct Ctx {
   }
 };
 
-// Issue the Toeplitz FIR of 128 consecutive blocks (plane rows row0 ..) into TMEM
-// column d_col; thread 0 only (the caller commits).  D[block][r'] = sum_s W_block[s] * T'[r'][s]:
-// A = the odd-phase windows (M = 128 blocks, K-major planes), B = the reversed
-// Toeplitz (N = 128 output offsets, the diagonal array), K = 256 in 16 steps.
-// Rows past a signal's end only feed discarded blocks, so they may hold
-// anything; the descriptors stay inside the CTA's shared memory.
+// Toeplitz FIR of 128 consecutive blocks (plane rows row0 ..) into TMEM column
+// d_col; thread 0 only, the caller commits.  Rows past a signal's end only feed
+// discarded blocks (they may hold anything; the descriptors stay in smem).
 NNAB_DEV void issue_fir(Ctx& c, uint32_t planes, uint32_t pl, int row0, uint32_t d_col) {
   tc_fence_after();
   constexpr uint32_t idesc = idesc_f16(128, 128);
@@ -144,8 +152,8 @@ NNAB_DEV void issue_fir(Ctx& c, uint32_t planes, uint32_t pl, int row0, uint32_t
 
 // Epilogue of a FIR tile: lane = block n = blk0 + TMEM lane, column r' = 127 - r.
 // Warp w reads lane quarter w & 3 and column half w >> 2 in four chunks of 16
-// columns, i.e. 16 consecutive outputs i0 .. i0+15 (i0 = 128 n + rbase) per
-// thread.  cen16(i0, c) loads their centre-tap samples, out16(i0, y) stores them
+// columns = 16 consecutive outputs i0 .. i0+15 (i0 = 128 n + rbase).
+// cen16(i0, c) loads their centre-tap samples, out16(i0, y) stores them
 // (vectorised); cen1 / out1 handle the last, partial chunk of a signal.  Blocks
 // below blk_lo (already written by an overlapping tile) are skipped.
 template <class Cen16, class Cen1, class Out16, class Out1>
@@ -195,7 +203,7 @@ NNAB_DEV void store_planes8(uint8_t* planes, uint32_t pl, int rows, int m0, cons
 NNAB_DEV void store_plane1(uint8_t* planes, uint32_t pl, int rows, int m, __half v) {
   if (m >= 0 && (m >> 7) < rows) *reinterpret_cast<__half*>(planes + plane_off(m, pl)) = v;
 }
-// outputs y[0..15] of i0 .. i0+15 (i0 % 16 == 0): odd ones (-> planes at
+// outputs y[0..15] of i0 .. i0+15 (i0 % 16 == 0): odd ones (planes at
 // m = (i + 127) / 2 = i0 / 2 + 64 + u), even ones, all of them (contiguous copy)
 NNAB_DEV void pack_odd(const float* y, __half2* o) {
 #pragma unroll
@@ -209,176 +217,194 @@ NNAB_DEV void pack_all(const float* y, __half2* o) {
 #pragma unroll
   for (int u = 0; u < 8; ++u) o[u] = __floats2half2_rn(y[2 * u], y[2 * u + 1]);
 }
+NNAB_DEV void unpack8(uint4 w, float* f) {
+  const __half2* h2 = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const float2 t = __half22float2(h2[u]);
+    f[2 * u] = t.x;
+    f[2 * u + 1] = t.y;
+  }
+}
 
 // Edge pass of a signal of length n held as a contiguous copy s (with ML margins)
-// and, optionally, odd-phase planes: write the reflect images (np.pad "reflect",
-// signal.py:245) from the already-stored samples.  One image per thread.
+// and, optionally, odd-phase planes: the reflect images (np.pad "reflect",
+// signal.py:245) from the stored samples.  One image per thread.
 NNAB_DEV void edge_pass(__half* s, uint8_t* planes, uint32_t pl, int rows, int n) {
-  for (int e = threadIdx.x; e < 2 * ML; e += kThreads) {
+  for (int e = threadIdx.x; e < 2 * ML; e += kCompute) {
     const int i = e < ML ? e + 1 : n - 1 - ML + (e - ML);  // left: 1..ML, right: n-1-ML .. n-2
     const int dst = e < ML ? -i : 2 * (n - 1) - i;         // ext position of the image
-    const __half v = s[ML + i];
-    s[ML + dst] = v;
-    if (planes && (dst & 1)) {
-      const int m = (dst + 127) >> 1;
-      if (m >= 0 && (m >> 7) < rows) *reinterpret_cast<__half*>(planes + plane_off(m, pl)) = v;
+    const __half v = s[sw(ML + i)];
+    s[sw(ML + dst)] = v;
+    if (planes && (dst & 1)) store_plane1(planes, pl, rows, (dst + 127) >> 1, v);
+  }
+}
+
+// 16 samples x_ext[j0 - 1 .. j0 + 14] of the clip (j0 odd): f[2k+1] = odd phase,
+// f[2k] = even phase; reflect at the ends, zero beyond one reflection.
+NNAB_DEV void x_chunk16(const float* xb, int64_t L, bool vec, int64_t j0, float* f) {
+  if (vec && j0 >= 1 && j0 + 15 <= L) {
+    const float4* src = reinterpret_cast<const float4*>(xb + j0 - 1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 a = __ldg(src + k);
+      f[4 * k] = a.x;
+      f[4 * k + 1] = a.y;
+      f[4 * k + 2] = a.z;
+      f[4 * k + 3] = a.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      int64_t j = j0 - 1 + k;
+      if (j < 0) j = -j;
+      if (j >= L) j = 2 * (L - 1) - j;
+      f[k] = (j >= 0 && j < L) ? __ldg(xb + j) : 0.f;
     }
   }
 }
 
-// Stage-1 planes for blocks [n0, n0 + rows - 1) (rows <= 129): odd phase of the
-// clip, scaled, FP16.  Thread -> plane row r = tid & 127 (row 128 by the first 16
-// threads afterwards) and plane chunks qq = tid >> 7 + 2u; four 64-byte chunk
-// loads in flight per round.
-NNAB_DEV void x_chunk(const float* xb, int64_t L, bool vec, int64_t j0, float* f) {
-  if (vec && j0 >= 1 && j0 + 15 <= L) {
-    const float4* src = reinterpret_cast<const float4*>(xb + j0 - 1);
-    const float4 a = __ldg(src), b = __ldg(src + 1), cq = __ldg(src + 2), d = __ldg(src + 3);
-    f[0] = a.y; f[1] = a.w; f[2] = b.y; f[3] = b.w; f[4] = cq.y; f[5] = cq.w; f[6] = d.y; f[7] = d.w;
-  } else {
+// Stage-1 operands of blocks [n0, n0 + nb): odd-phase planes (rows 0 .. nb) and
+// the even phase (centre taps, xe[u] = x[2 (128 n0 + u)]), scaled, FP16.
+// Thread -> plane row r = tid & 127 (row 128 by the first 16 threads after) and
+// plane chunks qq = tid >> 7 + 2u; four 64-byte chunks in flight per round.
+NNAB_DEV void build_x(Ctx& c, const float* xb, float scale, int n0, int nb, bool vec) {
+  const TcParams& p = c.p;
+  uint8_t* planes = c.base + p.off_x;
+  __half* xe = reinterpret_cast<__half*>(c.base + p.off_xe);
+  const int r = threadIdx.x & 127, q0 = threadIdx.x >> 7;
+  auto put = [&](int rr, int qq, const float* f) {
+    __align__(16) __half2 od[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      int64_t j = j0 + 2 * k;
-      if (j < 0) j = -j;
-      if (j >= L) j = 2 * (L - 1) - j;
-      f[k] = (j >= 0 && j < L) ? __ldg(xb + j) : 0.f;  // beyond one reflection: never a kept output
+    for (int k = 0; k < 4; ++k) od[k] = __floats2half2_rn(f[4 * k + 1] * scale, f[4 * k + 3] * scale);
+    *reinterpret_cast<uint4*>(planes + (uint32_t)qq * p.pl_x + (uint32_t)rr * 16u) = *reinterpret_cast<uint4*>(od);
+    const int u0 = rr * 128 + qq * 8 - 64;  // even samples x[j0 - 1 + 2k] = x[2 (m0 - 64 + k)]
+    if (u0 >= 0 && u0 < nb * 128) {
+      __align__(16) __half2 ev[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ev[k] = __floats2half2_rn(f[4 * k] * scale, f[4 * k + 2] * scale);
+      st8(xe, u0, *reinterpret_cast<uint4*>(ev));
     }
-  }
-}
-NNAB_DEV void put_x_chunk(uint8_t* planes, uint32_t pl, int r, int qq, const float* f, float scale) {
-  __align__(16) __half2 hv[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) hv[k] = __floats2half2_rn(f[2 * k] * scale, f[2 * k + 1] * scale);
-  *reinterpret_cast<uint4*>(planes + (uint32_t)qq * pl + (uint32_t)r * 16u) = *reinterpret_cast<uint4*>(hv);
-}
-NNAB_DEV void build_x_planes(Ctx& c, const float* xb, float scale, int n0, int rows, uint8_t* planes, uint32_t pl,
-                             bool vec) {
-  const int64_t L = c.p.L;
-  const int r = threadIdx.x & 127, q0 = threadIdx.x >> 7;  // q0 in {0, 1}
-  if (r < rows) {
-#pragma unroll
+  };
+  if (r <= nb) {
+#pragma unroll 1
     for (int h = 0; h < 2; ++h) {
-      float f[4][8];
+      float f[4][16];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int qq = q0 + 2 * (4 * h + u);
-        x_chunk(xb, L, vec, 2 * ((int64_t)(n0 + r) * 128 + qq * 8) - 127, f[u]);
+        x_chunk16(xb, p.L, vec, 2 * ((int64_t)(n0 + r) * 128 + qq * 8) - 127, f[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) put_x_chunk(planes, pl, r, q0 + 2 * (4 * h + u), f[u], scale);
+      for (int u = 0; u < 4; ++u) put(r, q0 + 2 * (4 * h + u), f[u]);
     }
   }
-  if (rows > 128 && threadIdx.x < 16) {
-    float f[8];
-    x_chunk(xb, L, vec, 2 * ((int64_t)(n0 + 128) * 128 + threadIdx.x * 8) - 127, f);
-    put_x_chunk(planes, pl, 128, threadIdx.x, f, scale);
+  if (nb == 128 && threadIdx.x < 16) {
+    float f[16];
+    x_chunk16(xb, p.L, vec, 2 * ((int64_t)(n0 + 128) * 128 + threadIdx.x * 8) - 127, f);
+    put(128, threadIdx.x, f);
   }
 }
 
-// Centred complex conv of octave alpha from its contiguous copy.
-NNAB_DEV void octave_conv(Ctx& c, const __half* sig, int alpha, int64_t b, float out_scale) {
+// im2col A tiles of octave alpha's conv, frames t0 .. t0 + 255 x 96 taps (FP16,
+// no-swizzle K-major): tile 0 (128 frames) has chunk cc (8 taps) at cc * 2048 and
+// frame t at t * 16; tile 1 is compact (rows2 rows, chunk stride rows2 * 16) --
+// its MMA also reads rows past rows2, which only feed discarded frames.  Column m
+// holds signal sample t*h - pad_al + m (the bank is shifted by pad_al - pad).
+NNAB_DEV uint4 frame_chunk(const TcParams& p, const __half* sig, int h, int tt, int cc) {
+  if (tt >= p.T) return make_uint4(0, 0, 0, 0);
+  const int s0 = ML + tt * h - p.pad_al + cc * 8;
+  if ((h & 7) == 0) return ld8(sig, s0);
+  __align__(16) __half hv[8];
+  if ((h & 3) == 0) {
+    *reinterpret_cast<uint2*>(hv) = *reinterpret_cast<const uint2*>(sig + sw(s0));
+    *reinterpret_cast<uint2*>(hv + 4) = *reinterpret_cast<const uint2*>(sig + sw(s0 + 4));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) hv[k] = sig[sw(s0 + k)];
+  }
+  return *reinterpret_cast<uint4*>(hv);
+}
+NNAB_DEV void build_frames(Ctx& c, const __half* sig, int h, int t0, int ntile) {
   const TcParams& p = c.p;
-  const int h = p.kernel_hop >> alpha;
+  uint8_t* col = c.base + p.off_col;
+  for (int e = threadIdx.x; e < 128 * (KC / 8); e += kCompute) {
+    const int t = e & 127, cc = e >> 7;
+    *reinterpret_cast<uint4*>(col + cc * 2048 + t * 16) = frame_chunk(p, sig, h, t0 + t, cc);
+  }
+  if (ntile > 1) {
+    uint8_t* col2 = col + 128 * KC * 2;
+    for (int e = threadIdx.x; e < p.rows2 * (KC / 8); e += kCompute) {
+      const int t = e % p.rows2, cc = e / p.rows2;
+      *reinterpret_cast<uint4*>(col2 + cc * p.rows2 * 16 + t * 16) = frame_chunk(p, sig, h, t0 + 128 + t, cc);
+    }
+  }
+}
+
+NNAB_DEV void issue_conv(Ctx& c, int ntile) {
+  tc_fence_after();
+  constexpr uint32_t idesc = idesc_f16(128, NCONV);
+  const uint32_t a0 = smem_u32(c.base + c.p.off_col), b0 = smem_u32(c.base + c.p.off_filt);
+  for (int u = 0; u < ntile; ++u) {
+    const uint32_t au = a0 + (u ? 128 * KC * 2 : 0), lbo = u ? (uint32_t)c.p.rows2 * 16u : 2048u;
+#pragma unroll
+    for (int k = 0; k < KC / 16; ++k)
+      mma_f16(c.tmem + kConvCol + 32 * u, nsw_desc(au + 2 * k * lbo, lbo, 128), nsw_desc(b0 + 2 * k * 512, 512, 128),
+              idesc, k > 0);
+  }
+}
+
+// conv epilogue: warp w reads lane quarter w & 3 of tile w >> 2: thread = frame,
+// columns 2j, 2j+1 = re, im of bin j; stores coalesced along T.
+NNAB_DEV void conv_epilogue(Ctx& c, int alpha, int64_t b, int t0, int ntile, float out_scale) {
+  const TcParams& p = c.p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, u = warp >> 2;
+  if (u >= ntile) return;
   const int skip = max(0, alpha * p.bpo - p.first_bin);
   const int row0 = p.first_bin - alpha * p.bpo;
-  uint8_t* ca = c.base + p.off_ra;
-  for (int t0 = 0; t0 < p.T; t0 += 256) {
-    const int ntile = min(2, (p.T - t0 + 127) / 128);
-    // im2col: tile u, chunk cc (8 taps) of frame t at u*24576 + cc*2048 + t*16; all of a
-    // thread's 16-byte loads are issued before any store
-    constexpr int kPer = 2 * 128 * (KC / 8) / kThreads;  // 12
-    uint4 v[kPer];
+  const int t = t0 + u * 128 + q * 32 + lane;
+  float v[32];
+  tmem_ld32(c.tmem + ((uint32_t)(q * 32) << 16) + kConvCol + 32 * u, v);
+  tmem_ld_wait();
+  if (t >= p.T) return;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int e = threadIdx.x + k * kThreads;
-      const int t = e & 127, rest = e >> 7, cc = rest % (KC / 8), u = rest / (KC / 8);
-      const int tt = t0 + u * 128 + t;
-      v[k] = make_uint4(0, 0, 0, 0);
-      if (tt < p.T) {
-        const __half* s = sig + ML + tt * h - p.pad_al + cc * 8;
-        if ((h & 7) == 0) {
-          v[k] = *reinterpret_cast<const uint4*>(s);
-        } else if ((h & 3) == 0) {
-          const uint2 a = reinterpret_cast<const uint2*>(s)[0], bb = reinterpret_cast<const uint2*>(s)[1];
-          v[k] = make_uint4(a.x, a.y, bb.x, bb.y);
-        } else {
-          const uint32_t* w = reinterpret_cast<const uint32_t*>(s);
-          v[k] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      }
+  for (int j = 0; j < NCONV / 2; ++j) {
+    if (j < skip || j >= p.n_filt) continue;
+    const float re = v[2 * j] * out_scale, im = v[2 * j + 1] * out_scale;
+    const int64_t o = (b * p.n_bins + row0 + j) * (int64_t)p.T + t;
+    if (p.out_kind == NNAB_OUT_COMPLEX) {
+      reinterpret_cast<float2*>(p.out)[o] = make_float2(re, im);
+    } else if (p.out_kind == NNAB_OUT_POWER) {
+      p.out[o] = fmaf(re, re, im * im);
+    } else {
+      p.out[o] = sqrtf(fmaf(re, re, im * im));
     }
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int e = threadIdx.x + k * kThreads;
-      const int t = e & 127, rest = e >> 7, cc = rest % (KC / 8), u = rest / (KC / 8);
-      if (u < ntile) *reinterpret_cast<uint4*>(ca + u * 24576 + cc * 2048 + t * 16) = v[k];
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-    c.pf.mark(p, 9);
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-      const uint32_t idesc = idesc_f16(128, NCONV);
-      const uint32_t a0 = smem_u32(ca), b0 = smem_u32(c.base + p.off_filt);
-      for (int u = 0; u < ntile; ++u) {
-#pragma unroll
-        for (int k = 0; k < KC / 16; ++k)
-          mma_f16(c.tmem + kConvCol + 32 * u, nsw_desc(a0 + u * 24576 + 2 * k * 2048, 2048, 128),
-                  nsw_desc(b0 + 2 * k * 512, 512, 128), idesc, k > 0);
-      }
-      mma_commit(c.bar);
-    }
-    c.wait_mma();
-    c.pf.mark(p, 10);
-    {
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      const int q = warp & 3, u = warp >> 2;
-      const int t = t0 + u * 128 + q * 32 + lane;
-      if (u < ntile) {
-        float v[32];
-        tmem_ld32(c.tmem + ((uint32_t)(q * 32) << 16) + kConvCol + 32 * u, v);
-        tmem_ld_wait();
-        if (t < p.T) {
-#pragma unroll
-          for (int j = 0; j < NCONV / 2; ++j) {
-            if (j < skip || j >= p.n_filt) continue;
-            const float re = v[2 * j] * out_scale, im = v[2 * j + 1] * out_scale;
-            const int64_t o = (b * p.n_bins + row0 + j) * (int64_t)p.T + t;
-            if (p.out_kind == NNAB_OUT_COMPLEX) {
-              reinterpret_cast<float2*>(p.out)[o] = make_float2(re, im);
-            } else if (p.out_kind == NNAB_OUT_POWER) {
-              p.out[o] = fmaf(re, re, im * im);
-            } else {
-              p.out[o] = sqrtf(fmaf(re, re, im * im));
-            }
-          }
-        }
-      }
-    }
-    tc_fence_before();
-    __syncthreads();
-    c.pf.mark(p, 11);
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) cqt2010_tc_kernel(const __grid_constant__ TcParams p) {
+__global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_constant__ TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // bars[0] MMA, [1..2] scan ring, [3] scale published, [4] scan may start the next clip
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + p.off_bars);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);  // bars[0] MMA, bars[1..3] scan ring
-  __shared__ float red[kThreads / 32];
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+  volatile int* scale_exp = reinterpret_cast<volatile int*>(bars + 7);
   __shared__ unsigned long long prof_acc[16];
   const int tid = threadIdx.x, warp = tid >> 5;
+  const bool vec = (p.L % 4) == 0;
 
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc<256>(tslot);
-  // zero the operand regions once (rows past a signal's end only feed discarded
-  // outputs, but must hold finite values)
-  for (int i = tid; i < (p.off_bars - p.off_ra) / 16; i += kThreads)
-    reinterpret_cast<uint4*>(base + p.off_ra)[i] = make_uint4(0, 0, 0, 0);
+  if (warp == 0) tmem_alloc<512>(tslot);
+  if (tid < 16) prof_acc[tid] = 0;
+  // zero the signal regions once: windows of real blocks read rows past a signal's
+  // end at zero Toeplitz weight, and 0 * NaN would poison them (everything written
+  // later is finite)
+  for (int i = tid; i < (p.off_bars - p.off_x) / 16; i += kThreads)
+    reinterpret_cast<uint4*>(base + p.off_x)[i] = make_uint4(0, 0, 0, 0);
   // diagonal Toeplitz chunks: chunk j = g[j - 127 + e], e < 8
   for (int j = tid; j < TOEP_CHUNKS; j += kThreads) {
     __align__(16) __half v[8];
@@ -389,7 +415,8 @@ __global__ void __launch_bounds__(kThreads, 2) cqt2010_tc_kernel(const __grid_co
     }
     *reinterpret_cast<uint4*>(base + p.off_toep + 16 * j) = *reinterpret_cast<uint4*>(v);
   }
-  // conv bank B: row n = 2j (+1 for Im), chunk cc at cc*512 + n*16; column m holds tap m - shift
+  // conv bank B (N = 32 rows x 96 taps): row 2j = Re bin j, 2j+1 = Im; chunk cc at cc * 512,
+  // row at 16 B; column m holds tap m - shift
   const int shift = p.pad_al - p.pad;
   for (int e = tid; e < NCONV * KC; e += kThreads) {
     const int n = e / KC, m = e % KC, j = n >> 1, tap = m - shift;
@@ -403,253 +430,230 @@ __global__ void __launch_bounds__(kThreads, 2) cqt2010_tc_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
 
-  Ctx c{p, base, *tslot, &bars[0], 0, {}};
-  c.pf.acc = prof_acc;
-  if (tid < 16) prof_acc[tid] = 0;
-  if (p.prof && tid == 0) c.pf.t = clock64();
-  const bool vec = (p.L % 4) == 0;
-  uint8_t* xp = base + p.off_ra;   // stage-1 planes (aliases the conv im2col tiles)
-  uint8_t* yp = base + p.off_rb;   // stage-2 planes (later: octave planes)
-  const uint32_t xp_s = smem_u32(xp), yp_s = smem_u32(yp);
-  uint32_t scan_seq = 0;  // bulk-copy ring uses so far (slot = seq % 3, parity = seq / 3)
-
-  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
-    const float* xb = p.x + b * p.L;
-    __half* scr = p.scratch + blockIdx.x * p.cta_stride;
-    // ------------------------------------------------ per-clip scale 2^-e (peak -> [0.5, 1))
-    // the clip streams through a 3 x 16 KB ring of bulk copies (TMA engine: the
-    // whole clip is in flight at HBM bandwidth and lands in L2 for stage 1)
-    float mx = 0.f;
-    if (vec) {
-      constexpr uint32_t kChunk = 16384;
-      const uint32_t bytes = (uint32_t)(p.L * 4);
-      const int nch = (int)((bytes + kChunk - 1) / kChunk);
-      const char* src = reinterpret_cast<const char*>(xb);
-      auto issue = [&](int k) {
-        const uint32_t sz = std::min(kChunk, bytes - (uint32_t)k * kChunk);
-        const int slot = (int)((scan_seq + k) % 3);
-        mbar_expect_tx(&bars[1 + slot], sz);
-        bulk_load(xp + slot * kChunk, src + (size_t)k * kChunk, sz, &bars[1 + slot]);
-      };
-      if (tid == 0)
-        for (int k = 0; k < 3 && k < nch; ++k) issue(k);
-      for (int k = 0; k < nch; ++k) {
-        const uint32_t seq = scan_seq + k;
-        mbar_wait(&bars[1 + seq % 3], (seq / 3) & 1);
-        const uint32_t sz = std::min(kChunk, bytes - (uint32_t)k * kChunk);
-        const float4* b4 = reinterpret_cast<const float4*>(xp + (seq % 3) * kChunk);
-        for (int i = tid; i < (int)(sz / 16); i += kThreads) {
-          const float4 a = b4[i];
-          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
-        }
-        __syncthreads();  // slot consumed by every thread before it is refilled
-        if (tid == 0 && k + 3 < nch) issue(k + 3);
-      }
-      scan_seq += (uint32_t)nch;
-    } else {
-      for (int64_t i = tid; i < p.L; i += kThreads) mx = fmaxf(mx, fabsf(__ldg(xb + i)));
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((tid & 31) == 0) red[warp] = mx;
-    __syncthreads();
-    mx = red[0];
-#pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) mx = fmaxf(mx, red[w]);
-    int ex = 0;
-    if (mx > 0.f && mx < INFINITY) frexpf(mx, &ex);
-    const float scale = ldexpf(1.f, -ex), out_scale = ldexpf(1.f, ex - kFiltLog2);
-    c.pf.mark(p, 12);
-
-    // ------------------------------------------------ stage 1: x -> y1 (odd -> planes, even -> scratch)
-    __half* ye = scr + p.ye_off;
-    const int L1 = p.L1, nt = p.n1_tiles;
-    auto tile_blocks = [&](int t) { return min(kTile1, (L1 - t * kTile1 * 128 + 127) / 128); };
-    build_x_planes(c, xb, scale, 0, tile_blocks(0) + 1, xp, p.pl_x, vec);
-    fence_proxy_async_smem();
-    __syncthreads();
-    c.pf.mark(p, 0);
-    if (tid == 0) {
-      issue_fir(c, xp_s, p.pl_x, 0, 0);
-      mma_commit(c.bar);
-    }
-    for (int t = 0; t < nt; ++t) {
-      c.wait_mma();
-      c.pf.mark(p, 1);
-      if (t + 1 < nt) {  // next tile's planes (its MMAs overlap this tile's epilogue)
-        build_x_planes(c, xb, scale, (t + 1) * kTile1, tile_blocks(t + 1) + 1, xp, p.pl_x, vec);
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-          issue_fir(c, xp_s, p.pl_x, 0, ((t + 1) & 1) * 128);
-          mma_commit(c.bar);
-        }
-        c.pf.mark(p, 0);
-      }
-      fir_epilogue(
-          c, t * kTile1, 0, L1, (t & 1) * 128, p.h0 * scale,
-          [&](int i0, float* cv) {
-            if (vec) {
-              const float4* s4 = reinterpret_cast<const float4*>(xb + 2 * (int64_t)i0);
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const float4 w = __ldg(s4 + k);
-                cv[2 * k] = w.x;
-                cv[2 * k + 1] = w.z;
-              }
-            } else {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) cv[e] = __ldg(xb + 2 * (int64_t)(i0 + e));
-            }
-          },
-          [&](int i) { return __ldg(xb + 2 * (int64_t)i); },
-          [&](int i0, const float* y) {
-            __align__(16) __half2 od[4], ev[4];
-            pack_odd(y, od);
-            pack_even(y, ev);
-            store_planes8(yp, p.pl_y, p.y_rows, i0 / 2 + 64, od);                            // stage-2 planes
-            *reinterpret_cast<uint4*>(ye + i0 / 2) = *reinterpret_cast<const uint4*>(ev);  // stage-2 centre taps
-          },
-          [&](int i, float y) {
-            if (i & 1) store_plane1(yp, p.pl_y, p.y_rows, (i + 127) >> 1, h16(y));
-            else ye[i >> 1] = h16(y);
-          });
-      tc_fence_before();
-      __syncthreads();
-      c.pf.mark(p, 2);
-    }
-    // reflect images of y1's odd phase (left: -i, right: 2(L1-1) - i, i odd)
-    for (int e = tid; e < 128; e += kThreads) {
-      const int i = e < 64 ? 2 * e + 1 : ((L1 - 128) | 1) + 2 * (e - 64);
-      const int dst = e < 64 ? -i : 2 * (L1 - 1) - i;
-      if (i <= L1 - 2) {
-        const __half v = *reinterpret_cast<const __half*>(yp + plane_off((i + 127) >> 1, p.pl_y));
-        store_plane1(yp, p.pl_y, p.y_rows, (dst + 127) >> 1, v);
-      }
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-
-    // FIR epilogue functors of a signal held as a contiguous copy (centre taps at
-    // src[2i] or src[i]) writing a contiguous copy + the next halving's planes
-    auto contig_out16 = [&](__half* dst, uint8_t* planes, uint32_t pl, int rows) {
-      return [=](int i0, const float* y) {
-        __align__(16) __half2 al[8];
-        pack_all(y, al);
-        uint4* d4 = reinterpret_cast<uint4*>(dst + ML + i0);
-        d4[0] = reinterpret_cast<const uint4*>(al)[0];
-        d4[1] = reinterpret_cast<const uint4*>(al)[1];
-        if (planes) {
-          __align__(16) __half2 od[4];
-          pack_odd(y, od);
-          store_planes8(planes, pl, rows, i0 / 2 + 64, od);
-        }
-      };
-    };
-    auto contig_out1 = [&](__half* dst, uint8_t* planes, uint32_t pl, int rows) {
-      return [=](int i, float y) {
-        const __half v = h16(y);
-        dst[ML + i] = v;
-        if (planes && (i & 1)) store_plane1(planes, pl, rows, (i + 127) >> 1, v);
-      };
-    };
-
-    // ------------------------------------------------ stage 2: y1 -> octave 0
-    __half* s0 = scr + p.s_off[0];
-    const int n2 = p.oct_len[0];
-    const int nb2 = p.oct_blocks[0];
-    const int row_b = nb2 > 128 ? nb2 - 128 : 0;  // second tile covers the last 128 blocks
-    if (tid == 0) {
-      issue_fir(c, yp_s, p.pl_y, 0, 0);
-      if (nb2 > 128) issue_fir(c, yp_s, p.pl_y, row_b, 128);
-      mma_commit(c.bar);
-    }
-    c.wait_mma();
-    c.pf.mark(p, 4);
-    {
-      uint8_t* o0 = p.n_oct > 1 ? yp : nullptr;  // octave planes overwrite the (consumed) y1 planes
-      const uint32_t pl0 = (uint32_t)p.plane_rows[0] * 16u;
-      auto cen16 = [&](int i0, float* cv) {
-        const uint4* s4 = reinterpret_cast<const uint4*>(ye + i0);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const uint4 w = s4[k];
-          const __half2* h2 = reinterpret_cast<const __half2*>(&w);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float2 f = __half22float2(h2[u]);
-            cv[8 * k + 2 * u] = f.x;
-            cv[8 * k + 2 * u + 1] = f.y;
+  if (warp == kCompute / 32) {
+    // ------------------------------------------------ scan warp: peak of each clip of this CTA
+    const int lane = tid & 31;
+    uint32_t seq = 0;  // ring uses (slot = seq & 1, parity = seq >> 1)
+    int k = 0;
+    for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
+      if (k > 0) mbar_wait(&bars[4], (k - 1) & 1);  // the previous clip finished stage 1
+      const float* xb = p.x + b * p.L;
+      float mx = 0.f;
+      if (vec) {
+        const uint32_t bytes = (uint32_t)(p.L * 4);
+        const int nch = (int)((bytes + kRing - 1) / kRing);
+        auto issue = [&](int ch) {
+          const uint32_t sz = min((uint32_t)kRing, bytes - (uint32_t)ch * kRing);
+          const uint32_t s = (seq + ch) & 1;
+          mbar_expect_tx(&bars[1 + s], sz);
+          bulk_load(base + p.off_ring + s * kRing, reinterpret_cast<const char*>(xb) + (size_t)ch * kRing, sz,
+                    &bars[1 + s]);
+        };
+        if (lane == 0)
+          for (int ch = 0; ch < 2 && ch < nch; ++ch) issue(ch);
+        for (int ch = 0; ch < nch; ++ch) {
+          const uint32_t s = seq + ch;
+          mbar_wait(&bars[1 + (s & 1)], (s >> 1) & 1);
+          const uint32_t sz = min((uint32_t)kRing, bytes - (uint32_t)ch * kRing);
+          const float4* b4 = reinterpret_cast<const float4*>(base + p.off_ring + (s & 1) * kRing);
+          for (int i = lane; i < (int)(sz / 16); i += 32) {
+            const float4 a = b4[i];
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
           }
+          __syncwarp();
+          if (lane == 0 && ch + 2 < nch) issue(ch + 2);
         }
-      };
-      auto cen1 = [&](int i) { return __half2float(ye[i]); };
-      // the first tile's MMA has completed, but its epilogue must not write the
-      // planes the second tile still reads: both tiles are committed together, so
-      // every MMA is done here
-      fir_epilogue(c, 0, 0, n2, 0, p.h0, cen16, cen1, contig_out16(s0, o0, pl0, p.plane_rows[0]),
-                   contig_out1(s0, o0, pl0, p.plane_rows[0]));
-      if (nb2 > 128)
-        fir_epilogue(c, row_b, 128, n2, 128, p.h0, cen16, cen1, contig_out16(s0, o0, pl0, p.plane_rows[0]),
-                     contig_out1(s0, o0, pl0, p.plane_rows[0]));
-      __syncthreads();
-      edge_pass(s0, o0, pl0, p.plane_rows[0], n2);
+        seq += (uint32_t)nch;
+      } else {
+        for (int64_t i = lane; i < p.L; i += 32) mx = fmaxf(mx, fabsf(__ldg(xb + i)));
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) {
+        int ex = 0;
+        if (mx > 0.f && mx < INFINITY) frexpf(mx, &ex);
+        *scale_exp = ex;
+        mbar_arrive(&bars[3]);
+      }
+      __syncwarp();
     }
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    c.pf.mark(p, 5);
+  } else {
+    // ------------------------------------------------ compute warps
+    Ctx c{p, base, *tslot, &bars[0], 0, {}};
+    c.pf.acc = prof_acc;
+    if (p.prof && tid == 0) c.pf.t = clock64();
+    uint8_t* xp = base + p.off_x;
+    uint8_t* yp = base + p.off_y;
+    __half* xe = reinterpret_cast<__half*>(base + p.off_xe);
+    __half* ye = reinterpret_cast<__half*>(base + p.off_ye);
+    const uint32_t xp_s = smem_u32(xp), yp_s = smem_u32(yp);
+    int k = 0;
+    for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
+      const float* xb = p.x + b * p.L;
+      mbar_wait(&bars[3], k & 1);
+      const int ex = *scale_exp;
+      const float scale = ldexpf(1.f, -ex), out_scale = ldexpf(1.f, ex - kFiltLog2);
+      c.pf.mark(p, 12);
 
-    // ------------------------------------------------ octaves: conv, halve, repeat
-    uint8_t* o_in = yp;
-    uint8_t* o_out = yp + p.plane_rows[0] * 16 * 16;
-    for (int a = 0; a < p.n_oct; ++a) {
-      const __half* sa = scr + p.s_off[a];
-      if (a > 0) {
-        const __half* sp = scr + p.s_off[a - 1];
-        __half* sd = scr + p.s_off[a];
-        const int n_out = p.oct_len[a];
-        const uint32_t pl_in = (uint32_t)p.plane_rows[a - 1] * 16u;
+      // -------------------------------------------- stage 1: x -> y1 (odd -> planes, even -> ye)
+      const int L1 = p.L1;
+      for (int t = 0; t < p.n1_tiles; ++t) {
+        const int nb = min(kTile1, (L1 - t * kTile1 * 128 + 127) / 128);
+        build_x(c, xb, scale, t * kTile1, nb, vec);
+        fence_proxy_async_smem();
+        csync();
+        c.pf.mark(p, 0);
         if (tid == 0) {
-          issue_fir(c, smem_u32(o_in), pl_in, 0, 0);
+          issue_fir(c, xp_s, p.pl_x, 0, 0);
           mma_commit(c.bar);
         }
         c.wait_mma();
-        c.pf.mark(p, 7);
-        uint8_t* po = a + 1 < p.n_oct ? o_out : nullptr;
-        const uint32_t pl_out = (uint32_t)p.plane_rows[a] * 16u;
+        c.pf.mark(p, 1);
+        const int u_base = t * kTile1 * 128;
         fir_epilogue(
-            c, 0, 0, n_out, 0, p.h0,
+            c, t * kTile1, 0, L1, 0, p.h0,
             [&](int i0, float* cv) {
-              const uint4* s4 = reinterpret_cast<const uint4*>(sp + ML + 2 * i0);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint4 w = s4[k];
-                const __half2* h2 = reinterpret_cast<const __half2*>(&w);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) cv[4 * k + u] = __low2float(h2[u]);
-              }
+              unpack8(ld8(xe, i0 - u_base), cv);
+              unpack8(ld8(xe, i0 - u_base + 8), cv + 8);
             },
-            [&](int i) { return __half2float(sp[ML + 2 * i]); }, contig_out16(sd, po, pl_out, p.plane_rows[a]),
-            contig_out1(sd, po, pl_out, p.plane_rows[a]));
-        __syncthreads();
-        edge_pass(sd, po, pl_out, p.plane_rows[a], n_out);
+            [&](int i) { return __half2float(xe[sw(i - u_base)]); },
+            [&](int i0, const float* y) {
+              __align__(16) __half2 od[4], ev[4];
+              pack_odd(y, od);
+              pack_even(y, ev);
+              store_planes8(yp, p.pl_y, p.y_rows, i0 / 2 + 64, od);
+              st8(ye, i0 / 2, *reinterpret_cast<const uint4*>(ev));
+            },
+            [&](int i, float y) {
+              if (i & 1) store_plane1(yp, p.pl_y, p.y_rows, (i + 127) >> 1, h16(y));
+              else ye[sw(i >> 1)] = h16(y);
+            });
+        tc_fence_before();
+        csync();
+        c.pf.mark(p, 2);
+      }
+      if (tid == 0) mbar_arrive(&bars[4]);  // x of this clip is no longer needed: scan the next one
+      // reflect images of y1's odd phase (left: -i, right: 2(L1-1) - i, i odd)
+      for (int e = tid; e < 128; e += kCompute) {
+        const int i = e < 64 ? 2 * e + 1 : ((L1 - 128) | 1) + 2 * (e - 64);
+        const int dst = e < 64 ? -i : 2 * (L1 - 1) - i;
+        if (i <= L1 - 2)
+          store_plane1(yp, p.pl_y, p.y_rows, (dst + 127) >> 1,
+                       *reinterpret_cast<const __half*>(yp + plane_off((i + 127) >> 1, p.pl_y)));
+      }
+      fence_proxy_async_smem();
+      csync();
+
+      // epilogue functors of a halving whose output goes to a contiguous copy + planes
+      auto out16_of = [&](__half* dst, uint8_t* planes, uint32_t pl, int rows) {
+        return [=](int i0, const float* y) {
+          __align__(16) __half2 al[8];
+          pack_all(y, al);
+          st8(dst, ML + i0, reinterpret_cast<const uint4*>(al)[0]);
+          st8(dst, ML + i0 + 8, reinterpret_cast<const uint4*>(al)[1]);
+          if (planes) {
+            __align__(16) __half2 od[4];
+            pack_odd(y, od);
+            store_planes8(planes, pl, rows, i0 / 2 + 64, od);
+          }
+        };
+      };
+      auto out1_of = [&](__half* dst, uint8_t* planes, uint32_t pl, int rows) {
+        return [=](int i, float y) {
+          const __half v = h16(y);
+          dst[sw(ML + i)] = v;
+          if (planes && (i & 1)) store_plane1(planes, pl, rows, (i + 127) >> 1, v);
+        };
+      };
+      auto sig = [&](int a) { return reinterpret_cast<__half*>(base + p.s_off[a]); };
+      auto planes_of = [&](int a) { return a + 1 < p.n_oct ? base + p.o_off[a] : nullptr; };
+
+      // -------------------------------------------- stage 2: y1 -> octave 0
+      {
+        const int n2 = p.oct_len[0], nb2 = p.oct_blocks[0];
+        const int row_b = nb2 > 128 ? nb2 - 128 : 0;  // second tile: the last 128 blocks
+        if (tid == 0) {
+          issue_fir(c, yp_s, p.pl_y, 0, 0);
+          if (nb2 > 128) issue_fir(c, yp_s, p.pl_y, row_b, 128);
+          mma_commit(c.bar);
+        }
+        c.wait_mma();
+        c.pf.mark(p, 4);
+        uint8_t* o0 = planes_of(0);
+        const uint32_t pl0 = (uint32_t)p.plane_rows[0] * 16u;
+        auto cen16 = [&](int i0, float* cv) {
+          unpack8(ld8(ye, i0), cv);
+          unpack8(ld8(ye, i0 + 8), cv + 8);
+        };
+        auto cen1 = [&](int i) { return __half2float(ye[sw(i)]); };
+        fir_epilogue(c, 0, 0, n2, 0, p.h0, cen16, cen1, out16_of(sig(0), o0, pl0, p.plane_rows[0]),
+                     out1_of(sig(0), o0, pl0, p.plane_rows[0]));
+        if (nb2 > 128)
+          fir_epilogue(c, row_b, 128, n2, 128, p.h0, cen16, cen1, out16_of(sig(0), o0, pl0, p.plane_rows[0]),
+                       out1_of(sig(0), o0, pl0, p.plane_rows[0]));
+        csync();
+        edge_pass(sig(0), o0, pl0, p.plane_rows[0], n2);
         fence_proxy_async_smem();
         tc_fence_before();
-        uint8_t* tmp = o_in;
-        o_in = o_out;
-        o_out = tmp;
-        __syncthreads();
-        c.pf.mark(p, 8);
+        csync();
+        c.pf.mark(p, 5);
       }
-      octave_conv(c, sa, a, b, out_scale);
+
+      // -------------------------------------------- octaves: conv alpha (+ halving alpha+1), repeat
+      for (int a = 0; a < p.n_oct; ++a) {
+        const int h = p.kernel_hop >> a;
+        const bool halve = a + 1 < p.n_oct;
+        for (int t0 = 0; t0 < p.T; t0 += 256) {
+          const int ntile = min(2, (p.T - t0 + 127) / 128);
+          build_frames(c, sig(a), h, t0, ntile);
+          fence_proxy_async_smem();
+          csync();
+          c.pf.mark(p, 9);
+          const bool with_fir = halve && t0 == 0;  // the next halving rides along with the first conv tiles
+          if (tid == 0) {
+            issue_conv(c, ntile);
+            if (with_fir) issue_fir(c, smem_u32(base + p.o_off[a]), (uint32_t)p.plane_rows[a] * 16u, 0, 0);
+            mma_commit(c.bar);
+          }
+          c.wait_mma();
+          c.pf.mark(p, 10);
+          conv_epilogue(c, a, b, t0, ntile, out_scale);
+          c.pf.mark(p, 11);
+          if (with_fir) {
+            const __half* sp = sig(a);
+            __half* sd = sig(a + 1);
+            uint8_t* po = planes_of(a + 1);
+            const uint32_t pl_out = (uint32_t)p.plane_rows[a + 1] * 16u;
+            const int n_out = p.oct_len[a + 1];
+            fir_epilogue(
+                c, 0, 0, n_out, 0, p.h0,
+                [&](int i0, float* cv) {
+#pragma unroll
+                  for (int kk = 0; kk < 4; ++kk) {
+                    const uint4 w = ld8(sp, ML + 2 * i0 + 8 * kk);
+                    const __half2* h2 = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) cv[4 * kk + u] = __low2float(h2[u]);
+                  }
+                },
+                [&](int i) { return __half2float(sp[sw(ML + 2 * i)]); }, out16_of(sd, po, pl_out, p.plane_rows[a + 1]),
+                out1_of(sd, po, pl_out, p.plane_rows[a + 1]));
+            csync();
+            edge_pass(sd, po, pl_out, p.plane_rows[a + 1], n_out);
+            fence_proxy_async_smem();
+            c.pf.mark(p, 8);
+          }
+          tc_fence_before();
+          csync();
+        }
+      }
+      c.pf.mark(p, 15);
     }
-    c.pf.mark(p, 15);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) tmem_dealloc<256>(*tslot);
+  if (warp == 0) tmem_dealloc<512>(*tslot);
   if (p.prof && tid == 0)
     for (int i = 0; i < 16; ++i) atomicAdd(p.prof + i, prof_acc[i]);
 }
@@ -666,17 +670,15 @@ unsigned long long* cqt2010_prof_ptr() {
 struct Plan {
   TcParams p;
   size_t smem;
-  int ctas_per_sm;
-  size_t scratch_bytes_per_cta;
 };
 
-int64_t rnd8(int64_t v) { return (v + 7) & ~int64_t(7); }
+int32_t rnd(int64_t v, int a) { return (int32_t)((v + a - 1) / a * a); }
 
 // Geometry and shared-memory plan of the fused kernel; NNAB_ENOTSUP outside its envelope.
 int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, int early_stages, int n_oct,
-              int kernel_hop, int pad_mode, Plan* pl) {
+              int kernel_hop, int T, int pad_mode, Plan* pl) {
   if (early_stages != 2 || n_taps != 255 || pad_mode != NNAB_PAD_REFLECT) return NNAB_ENOTSUP;
-  if (n_filt > NCONV / 2 || n_oct < 1 || n_oct > kMaxOct) return NNAB_ENOTSUP;
+  if (n_filt > 16 || n_oct < 1 || n_oct > kMaxOct) return NNAB_ENOTSUP;
   const int pad = width / 2, pad_al = (pad + 7) & ~7;
   if (width + (pad_al - pad) > KC || pad_al > ML) return NNAB_ENOTSUP;
   float hmax = 0.f;  // half-band check: even offsets (odd tap indices) are negligible
@@ -686,7 +688,7 @@ int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, i
   TcParams& p = pl->p;
   p = TcParams{};
   const int64_t L1 = (L + 1) / 2, L0 = (L1 + 1) / 2;
-  if (L0 > 255 * 128 || L1 > 1 << 30) return NNAB_ENOTSUP;  // stage 2 in one MMA tile (N <= 256)
+  if (L0 > 256 * 128 || L1 > (1 << 30)) return NNAB_ENOTSUP;  // stage 2 in two M = 128 tiles
   p.L = L;
   p.L1 = (int32_t)L1;
   p.L0 = (int32_t)L0;
@@ -695,53 +697,76 @@ int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, i
   p.kernel_hop = kernel_hop;
   p.pad = pad;
   p.pad_al = pad_al;
+  p.T = T;
+  p.rows2 = rnd(std::max(std::min(T, 256) - 128, 8), 8);
   int64_t n = L0;
-  int64_t off = rnd8(L0);  // ye
-  p.ye_off = 0;
   for (int a = 0; a < n_oct; ++a) {
     if (a > 0) n = (n + 1) / 2;
     if (n < ML + 2) return NNAB_ENOTSUP;  // reflect margins need n > ML + 1
     p.oct_len[a] = (int32_t)n;
     p.oct_blocks[a] = (int32_t)((n + 127) / 128);
     if (a > 0 && p.oct_blocks[a] > 128) return NNAB_ENOTSUP;  // one M = 128 tile per octave halving
-    p.s_off[a] = off;
-    off += rnd8(n + 2 * ML);
   }
   // odd-phase planes of octave a feeding halving a+1: blocks + 1 rows, and the
   // right reflect image up to m = (n + 253) / 2
   for (int a = 0; a + 1 < n_oct; ++a)
-    p.plane_rows[a] = (std::max(p.oct_blocks[a + 1] + 1, (p.oct_len[a] + 253) / 2 / 128 + 1) + 7) & ~7;
-  p.cta_stride = rnd8(off);
-  // shared memory: toep | filt | RA = max(x planes, conv tiles) | RB = max(y planes, octave planes) + slack
-  // (an M = 128 tile reads 129 plane rows whatever the signal length: up to 2064 B past a short plane set)
+    p.plane_rows[a] = rnd(std::max(p.oct_blocks[a + 1] + 1, (p.oct_len[a] + 253) / 2 / 128 + 1), 8);
+  // shared memory (bytes): fixed | R1 = stage-1 operands, later octave 0 | R2 = stage-2 operands, later
+  // octaves >= 1.  An M = 128 tile reads 129 plane rows whatever the signal length, so short plane
+  // sets need up to 2064 B of readable memory behind them (slack).
+  constexpr int kSlack = 2304;
+  int off = 0;
+  p.off_toep = off;  off += TOEP_CHUNKS * 16;
+  off = rnd(off, 1024);
+  p.off_filt = off;  off += KC / 8 * 512;
+  p.off_ring = off;  off += 2 * kRing;
+  const int r1 = off;
   p.pl_x = (kTile1 + 8) * 16;
-  // odd phase of y1 incl. its right reflect image: m < (L1 + 254) / 2; stage 2 reads blocks + 1 rows
-  p.y_rows = (std::max((int)((L1 + 254) / 2 / 128) + 1, p.oct_blocks[0] + 1) + 7) & ~7;
+  p.off_x = off;     off += p.pl_x * 16;
+  p.off_xe = off;    off += kTile1 * 128 * 2;
+  int r1_end = off;
+  int o = r1;  // octave 0 (written by stage 2) reuses R1
+  p.s_off[0] = o;    o += rnd((int64_t)p.oct_len[0] + 2 * ML, 128) * 2;
+  if (n_oct > 1) { p.o_off[0] = o; o += p.plane_rows[0] * 256; }
+  o += kSlack;
+  r1_end = std::max(r1_end, o);
+  const int r2 = rnd(r1_end, 128);
+  p.y_rows = rnd(std::max((int)((L1 + 254) / 2 / 128) + 1, p.oct_blocks[0] + 1), 8);
   p.pl_y = p.y_rows * 16;
-  const size_t ra = std::max<size_t>((size_t)p.pl_x * 16, 2 * 24576);
-  size_t oct_planes = 0;
-  for (int a = 0; a + 1 < n_oct; ++a)
-    oct_planes = std::max(oct_planes, (size_t)(p.plane_rows[0] + (a + 2 < n_oct ? p.plane_rows[a + 1] : 0)) * 256);
-  const size_t rb = std::max((size_t)p.pl_y * 16, oct_planes) + 2304;
-  p.off_toep = 0;
-  p.off_filt = 6144;
-  p.off_ra = 6144 + 6144;
-  p.off_rb = p.off_ra + (int32_t)((ra + 1023) & ~size_t(1023));
-  p.off_bars = p.off_rb + (int32_t)((rb + 127) & ~size_t(127));
-  pl->smem = 1024 + (size_t)p.off_bars + 64;
+  p.off_y = r2;
+  p.off_ye = r2 + p.pl_y * 16 + kSlack;
+  int r2_end = p.off_ye + rnd(L0 + 16, 128) * 2;  // whole 128-sample rows (swizzle stays inside)
+  o = r2;  // octaves >= 1 and the im2col tile reuse R2; octave a only lives with a +- 1 (ping-pong)
+  p.off_col = o;     o += (128 + p.rows2) * KC * 2;
+  int s_sz[2] = {0, 0}, o_sz[2] = {0, 0};
+  for (int a = 1; a < n_oct; ++a) {
+    s_sz[a & 1] = std::max(s_sz[a & 1], rnd((int64_t)p.oct_len[a] + 2 * ML, 128) * 2);
+    if (a + 1 < n_oct) o_sz[a & 1] = std::max(o_sz[a & 1], p.plane_rows[a] * 256);
+  }
+  const int s_base[2] = {o + s_sz[1], o};
+  o += s_sz[0] + s_sz[1];
+  const int o_base[2] = {o + o_sz[1], o};
+  o += o_sz[0] + o_sz[1];
+  for (int a = 1; a < n_oct; ++a) {
+    p.s_off[a] = s_base[a & 1];
+    if (a + 1 < n_oct) p.o_off[a] = o_base[a & 1];
+  }
+  o += kSlack;
+  r2_end = std::max(r2_end, o);
+  off = rnd(r2_end, 128);
+  p.off_bars = off;  off += 64;
+  pl->smem = 1024 + (size_t)off;
   if (pl->smem > 227 * 1024) return NNAB_ENOTSUP;
-  pl->ctas_per_sm = pl->smem <= 113 * 1024 ? 2 : 1;
-  pl->scratch_bytes_per_cta = (size_t)p.cta_stride * 2;
   return NNAB_OK;
 }
 
 }  // namespace
 
 // Debug: enable per-phase cycle counters of the fused kernel (on != 0), or read
-// and clear them into out[16] (on == 0).  Phases: 12 scale scan, 0 stage-1 planes,
-// 1 stage-1 MMA wait, 2 stage-1 epilogue, 4 stage-2 MMA, 5 stage-2 epilogue,
-// 7 octave MMA, 8 octave epilogue / CUDA-core halving, 9 conv im2col,
-// 10 conv MMA, 11 conv epilogue, 15 loop tail.
+// and clear them into out[16] (on == 0).  Phases: 12 wait for the scale,
+// 0 stage-1 build, 1 stage-1 MMA, 2 stage-1 epilogue, 4 stage-2 MMA,
+// 5 stage-2 epilogue, 9 conv im2col, 10 conv (+ halving) MMA, 11 conv epilogue,
+// 8 halving epilogue, 15 loop tail.
 extern "C" int nnab_debug_cqt2010_profile(int on, unsigned long long* out) {
   if (on) {
     g_cqt_prof_on = true;
@@ -754,29 +779,18 @@ extern "C" int nnab_debug_cqt2010_profile(int on, unsigned long long* out) {
   return NNAB_OK;
 }
 
-size_t cqt2010_tc_scratch_bytes(int64_t B, int64_t L, const float* taps, int n_taps, int n_filt, int width,
-                                int early_stages, int n_oct, int kernel_hop, int pad_mode) {
-  Plan pl;
-  if (!taps || make_plan(L, n_taps, taps, n_filt, width, early_stages, n_oct, kernel_hop, pad_mode, &pl)) return 0;
-  const int64_t grid = std::min<int64_t>(B, (int64_t)num_sms() * pl.ctas_per_sm);
-  return (size_t)grid * pl.scratch_bytes_per_cta + 256;
-}
-
 // Fused tensor-core CQT2010v2; NNAB_ENOTSUP when the configuration is outside
 // what the fused kernel holds on chip (the caller then runs the staged
 // CUDA-core kernels).
 int launch_cqt2010_tc(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, const float* k_re,
                       const float* k_im, int n_filt, int width, int early_stages, int n_oct, int kernel_hop,
                       int first_bin, int bpo, int n_bins, int pad_mode, int out_kind, int T, float* out,
-                      void* workspace, size_t workspace_bytes, cudaStream_t st) {
+                      cudaStream_t st) {
   Plan pl;
-  int rc = make_plan(L, n_taps, taps, n_filt, width, early_stages, n_oct, kernel_hop, pad_mode, &pl);
+  int rc = make_plan(L, n_taps, taps, n_filt, width, early_stages, n_oct, kernel_hop, T, pad_mode, &pl);
   if (rc) return rc;
   TcParams& p = pl.p;
-  const int grid = (int)std::min<int64_t>(B, (int64_t)num_sms() * pl.ctas_per_sm);
-  if (!workspace || workspace_bytes < (size_t)grid * pl.scratch_bytes_per_cta ||
-      reinterpret_cast<uintptr_t>(workspace) % 16)
-    return NNAB_ENOTSUP;
+  const int grid = (int)std::min<int64_t>(B, (int64_t)num_sms());
   p.x = x;
   p.B = B;
   p.first_bin = first_bin;
@@ -784,14 +798,12 @@ int launch_cqt2010_tc(const float* x, int64_t B, int64_t L, const float* taps, i
   p.n_bins = n_bins;
   p.n_filt = n_filt;
   p.width = width;
-  p.T = T;
   p.out_kind = out_kind;
   p.h0 = taps[127];
   for (int j = 0; j < 128; ++j) p.g[j] = taps[2 * j];
   p.k_re = k_re;
   p.k_im = k_im;
   p.out = out;
-  p.scratch = reinterpret_cast<__half*>(workspace);
   p.prof = cqt2010_prof_ptr();
   NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   cqt2010_tc_kernel<<<grid, kThreads, pl.smem, st>>>(p);
@@ -800,3 +812,12 @@ int launch_cqt2010_tc(const float* x, int64_t B, int64_t L, const float* taps, i
 }
 
 }  // namespace nnab
+
+// Debug (host only): the fused kernel's plan for a configuration -> shared-memory
+// bytes (> 0), or minus the status code when the configuration is outside it.
+extern "C" long long nnab_debug_cqt2010_plan(long long L, const float* taps, int n_taps, int n_filt, int width,
+                                             int early_stages, int n_oct, int kernel_hop, int T, int pad_mode) {
+  nnab::Plan pl;
+  const int rc = nnab::make_plan(L, n_taps, taps, n_filt, width, early_stages, n_oct, kernel_hop, T, pad_mode, &pl);
+  return rc ? -(long long)rc : (long long)pl.smem;
+}

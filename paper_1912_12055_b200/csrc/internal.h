@@ -92,10 +92,7 @@ size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits);
 int launch_cqt2010_tc(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, const float* k_re,
                       const float* k_im, int n_filt, int width, int early_stages, int n_oct, int kernel_hop,
                       int first_bin, int bpo, int n_bins, int pad_mode, int out_kind, int T, float* out,
-                      void* workspace, size_t workspace_bytes, cudaStream_t st);
-// its per-batch L2 scratch (0 when the configuration is outside the fused kernel)
-size_t cqt2010_tc_scratch_bytes(int64_t B, int64_t L, const float* taps, int n_taps, int n_filt, int width,
-                                int early_stages, int n_oct, int kernel_hop, int pad_mode);
+                      cudaStream_t st);
 int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s);
 
 }  // namespace nnab

@@ -16,8 +16,8 @@ fn(1, None)
 eng.forward(x); torch.cuda.synchronize()
 out = (C.c_ulonglong * 16)()
 fn(0, out)
-names = ["S1 planes", "S1 mma wait", "S1 epi", "-", "S2 mma", "S2 epi", "-", "oct mma", "oct epi/cuda",
-         "conv im2col", "conv mma", "conv epi", "scale scan", "-", "-", "tail"]
+names = ["S1 build", "S1 mma", "S1 epi", "-", "S2 mma", "S2 epi", "-", "-", "halving epi",
+         "conv im2col", "conv+halving mma", "conv epi", "wait scale", "-", "-", "tail"]
 tot = sum(out)
 for n, v in zip(names, out):
-    print(f"{n:14s} {v/1770:10.0f} cycles/clip/CTA  {100*v/tot:5.1f}%")
+    print(f"{n:18s} {v/1770:10.0f} cycles/clip  {100*v/tot:5.1f}%")
