@@ -113,11 +113,7 @@ NNAB_DEV __half h16(float v) { return __float2half_rn(v); }
 // 128 samples apart (lane = block); the 16-byte chunk index inside each 256-byte
 // row is XORed with the row index so those accesses spread over all banks.
 // Aligned runs of <= 8 samples stay contiguous; arrays are whole 128-sample rows.
-#ifdef NNAB_NO_SWZ
-NNAB_DEV int sw(int i) { return i; }
-#else
 NNAB_DEV int sw(int i) { return i ^ (((i >> 7) & 15) << 3); }
-#endif
 NNAB_DEV uint4 ld8(const __half* a, int i) { return *reinterpret_cast<const uint4*>(a + sw(i)); }
 NNAB_DEV void st8(__half* a, int i, uint4 v) { *reinterpret_cast<uint4*>(a + sw(i)) = v; }
 
@@ -378,7 +374,7 @@ NNAB_DEV void conv_epilogue(Ctx& c, int alpha, int64_t b, int t0, int ntile, flo
     } else if (p.out_kind == NNAB_OUT_POWER) {
       p.out[o] = fmaf(re, re, im * im);
     } else {
-      p.out[o] = sqrtf(fmaf(re, re, im * im));
+      p.out[o] = fast_sqrt(fmaf(re, re, im * im));
     }
   }
 }
@@ -386,7 +382,7 @@ NNAB_DEV void conv_epilogue(Ctx& c, int alpha, int64_t b, int t0, int ntile, flo
 __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_constant__ TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // bars[0] MMA, [1..2] scan ring, [3] scale published, [4] scan may start the next clip
+  // bars[0] FIR MMAs, [1..2] scan ring, [3] scale published, [4] scan may start the next clip, [5] conv MMAs
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + p.off_bars);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
   volatile int* scale_exp = reinterpret_cast<volatile int*>(bars + 7);
@@ -395,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
   const bool vec = (p.L % 4) == 0;
 
   if (tid == 0) {
-    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(tslot);
@@ -433,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
   if (warp == kCompute / 32) {
     // ------------------------------------------------ scan warp: peak of each clip of this CTA
     const int lane = tid & 31;
+    const uint64_t keep = policy_evict_last();
     uint32_t seq = 0;  // ring uses (slot = seq & 1, parity = seq >> 1)
     int k = 0;
     for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
@@ -446,8 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
           const uint32_t sz = min((uint32_t)kRing, bytes - (uint32_t)ch * kRing);
           const uint32_t s = (seq + ch) & 1;
           mbar_expect_tx(&bars[1 + s], sz);
-          bulk_load(base + p.off_ring + s * kRing, reinterpret_cast<const char*>(xb) + (size_t)ch * kRing, sz,
-                    &bars[1 + s]);
+          // keep the clip in L2 for stage 1, which reads it again after this scan
+          bulk_load_hint(base + p.off_ring + s * kRing, reinterpret_cast<const char*>(xb) + (size_t)ch * kRing, sz,
+                         &bars[1 + s], keep);
         };
         if (lane == 0)
           for (int ch = 0; ch < 2 && ch < nch; ++ch) issue(ch);
@@ -487,6 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
     __half* xe = reinterpret_cast<__half*>(base + p.off_xe);
     __half* ye = reinterpret_cast<__half*>(base + p.off_ye);
     const uint32_t xp_s = smem_u32(xp), yp_s = smem_u32(yp);
+    uint64_t* conv_bar = &bars[5];
+    uint32_t conv_phase = 0;
     int k = 0;
     for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
       const float* xb = p.x + b * p.L;
@@ -599,27 +599,29 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
         c.pf.mark(p, 5);
       }
 
-      // -------------------------------------------- octaves: conv alpha (+ halving alpha+1), repeat
+      // -------------------------------------------- octaves, software-pipelined: the halving
+      // alpha+1 MMA runs under the im2col of alpha, the conv alpha MMA under the
+      // halving alpha+1 epilogue
       for (int a = 0; a < p.n_oct; ++a) {
         const int h = p.kernel_hop >> a;
         const bool halve = a + 1 < p.n_oct;
+        if (halve && tid == 0) {
+          issue_fir(c, smem_u32(base + p.o_off[a]), (uint32_t)p.plane_rows[a] * 16u, 0, 0);
+          mma_commit(c.bar);
+        }
         for (int t0 = 0; t0 < p.T; t0 += 256) {
           const int ntile = min(2, (p.T - t0 + 127) / 128);
           build_frames(c, sig(a), h, t0, ntile);
           fence_proxy_async_smem();
           csync();
           c.pf.mark(p, 9);
-          const bool with_fir = halve && t0 == 0;  // the next halving rides along with the first conv tiles
           if (tid == 0) {
             issue_conv(c, ntile);
-            if (with_fir) issue_fir(c, smem_u32(base + p.o_off[a]), (uint32_t)p.plane_rows[a] * 16u, 0, 0);
-            mma_commit(c.bar);
+            mma_commit(conv_bar);
           }
-          c.wait_mma();
-          c.pf.mark(p, 10);
-          conv_epilogue(c, a, b, t0, ntile, out_scale);
-          c.pf.mark(p, 11);
-          if (with_fir) {
+          if (halve && t0 == 0) {
+            c.wait_mma();
+            c.pf.mark(p, 7);
             const __half* sp = sig(a);
             __half* sd = sig(a + 1);
             uint8_t* po = planes_of(a + 1);
@@ -643,6 +645,12 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
             fence_proxy_async_smem();
             c.pf.mark(p, 8);
           }
+          mbar_wait(conv_bar, conv_phase);
+          conv_phase ^= 1;
+          tc_fence_after();
+          c.pf.mark(p, 10);
+          conv_epilogue(c, a, b, t0, ntile, out_scale);
+          c.pf.mark(p, 11);
           tc_fence_before();
           csync();
         }

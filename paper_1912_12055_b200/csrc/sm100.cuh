@@ -155,6 +155,15 @@ NNAB_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* ba
       : "memory");
 }
 
+// 1-D bulk copy with an L2 eviction-priority policy (createpolicy).
+NNAB_DEV void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 // Arrive on an mbarrier once all prior tcgen05 ops of this thread completed.
 NNAB_DEV void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -305,6 +314,14 @@ NNAB_DEV void mma_commit_pair(uint64_t* bar, uint16_t mask) {
           smem_u32(bar)),
       "h"(mask)
       : "memory");
+}
+
+// MUFU square root (relative error ~2^-23): the IEEE sqrtf's special-case
+// path costs ~10x more in epilogues that take one per output.
+NNAB_DEV float fast_sqrt(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 // Round-to-nearest-even to TF32 (10-bit mantissa), kept in an fp32 container.

@@ -85,13 +85,13 @@ NNAB_DEV uint64_t make_sdesc(const void* p, int swz_bytes) {
 NNAB_DEV float finish(float re, float im, int kind, float power, float eps) {
   const float p = fmaf(re, re, im * im);
   if (kind == NNAB_OUT_POWER) return p;
-  if (kind == NNAB_OUT_SMOOTH_MAG) return sqrtf(p + eps);
+  if (kind == NNAB_OUT_SMOOTH_MAG) return fast_sqrt(p + eps);
   if (kind == NNAB_OUT_MEL) {  // eps = 0 for MelSpec, 1e-12 for the trainable layer (gradients.py:69-74)
-    if (power == 1.f) return sqrtf(p + eps);
+    if (power == 1.f) return fast_sqrt(p + eps);
     if (power == 2.f) return p + eps;
-    return powf(sqrtf(p + eps), power);
+    return powf(fast_sqrt(p + eps), power);
   }
-  return sqrtf(p);
+  return fast_sqrt(p);
 }
 
 template <bool kSplit, bool kPair>
