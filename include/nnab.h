@@ -198,6 +198,16 @@ int nnab_cqt1992v2_forward_staged(const nnab_frames* f, const float* packed_hi, 
                                   int32_t out_kind, float eps, float* out, const void* workspace,
                                   size_t workspace_bytes, void* stream);
 
+/* Host-buffer end-to-end variant of nnab_cqt1992v2_forward (pinned x_host ->
+ * pinned out_host, chunks of clips streamed through the device with H2D /
+ * compute / D2H overlap); device buffers come from `device_scratch`. */
+size_t nnab_cqt1992v2_host_scratch_bytes(const nnab_frames* f, int32_t precision, int32_t n_bins, int32_t out_kind,
+                                         int64_t chunk_clips);
+int nnab_cqt1992v2_forward_host(const nnab_frames* f, const float* x_host, const float* packed_hi,
+                                const float* packed_lo, int32_t n_bins, const uint32_t* schedule, int32_t n_entries,
+                                int32_t precision, int32_t out_kind, float eps, float* out_host, int64_t chunk_clips,
+                                void* device_scratch, size_t scratch_bytes, void* stream);
+
 /* ------------------------------------------------------- CQT2010v2
  * Cqt2010v2.__call__ (transforms.py:290-313, 319-323): early_stages x
  * downsample2 (signal.py:232-247), then per octave alpha: downsample2 (alpha>0)
@@ -216,6 +226,17 @@ int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, const float* ta
                            int32_t bins_per_octave, int32_t n_bins, int32_t pad_mode, int32_t out_kind,
                            int32_t precision, float* out, int32_t* n_frames_out, void* workspace,
                            size_t workspace_bytes, void* stream);
+
+/* Host-buffer end-to-end variant of nnab_cqt2010v2_forward (same pipeline as
+ * nnab_stft_forward_host); T = the frame count nnab_cqt2010v2_forward reports. */
+size_t nnab_cqt2010v2_host_scratch_bytes(int64_t L, int32_t early_stages, int32_t n_bins, int32_t T, int32_t out_kind,
+                                         int64_t chunk_clips);
+int nnab_cqt2010v2_forward_host(const float* x_host, int64_t B, int64_t L, const float* taps, int32_t n_taps,
+                                const float* k_re, const float* k_im, int32_t n_filters, int32_t width,
+                                int32_t early_stages, int32_t n_octaves, int32_t kernel_hop, int32_t first_bin,
+                                int32_t bins_per_octave, int32_t n_bins, int32_t pad_mode, int32_t out_kind,
+                                int32_t precision, float* out_host, int64_t chunk_clips, void* device_scratch,
+                                size_t scratch_bytes, void* stream);
 
 #ifdef __cplusplus
 }

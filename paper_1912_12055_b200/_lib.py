@@ -73,7 +73,13 @@ SIGNATURES = {
     "nnab_cqt_schedule": (C.c_int, [_ip, _i32, _i32, _i32, _ip, C.POINTER(_i32)]),
     "nnab_cqt1992v2_forward": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _ip, _i32, _i32, _i32, _f32, _fp, _vp, _sz,
                                          _vp]),
+    "nnab_cqt1992v2_host_scratch_bytes": (_sz, [_FR, _i32, _i32, _i32, _i64]),
+    "nnab_cqt1992v2_forward_host": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _ip, _i32, _i32, _i32, _f32, _fp, _i64,
+                                              _vp, _sz, _vp]),
     "nnab_cqt2010v2_workspace_bytes": (_sz, [_i64, _i64, _i32]),
+    "nnab_cqt2010v2_host_scratch_bytes": (_sz, [_i64, _i32, _i32, _i32, _i32, _i64]),
+    "nnab_cqt2010v2_forward_host": (C.c_int, [_fp, _i64, _i64, _fp, _i32, _fp, _fp, _i32, _i32, _i32, _i32, _i32,
+                                              _i32, _i32, _i32, _i32, _i32, _i32, _fp, _i64, _vp, _sz, _vp]),
     "nnab_cqt2010v2_forward": (C.c_int, [_fp, _i64, _i64, _fp, _i32, _fp, _fp, _i32, _i32, _i32, _i32, _i32, _i32,
                                          _i32, _i32, _i32, _i32, _i32, _fp, C.POINTER(_i32), _vp, _sz, _vp]),
 }

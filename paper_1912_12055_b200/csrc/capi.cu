@@ -205,6 +205,10 @@ extern "C" int nnab_stft_forward_staged(const nnab_frames* f, const float* packe
 }
 
 // ------------------------------------------------------------ host variant
+static size_t pipeline_bytes(int64_t chunk, int64_t L, int64_t out_per_clip) {
+  return 2 * (align256((size_t)chunk * L * 4) + align256((size_t)chunk * out_per_clip * 4));
+}
+
 static int64_t out_elems_per_clip(int32_t out_kind, int32_t n_bins, int32_t n_mels, int32_t T) {
   if (out_kind == NNAB_OUT_MEL) return (int64_t)n_mels * T;
   if (out_kind == NNAB_OUT_COMPLEX) return 2ll * n_bins * T;
@@ -217,10 +221,62 @@ extern "C" size_t nnab_stft_host_scratch_bytes(const nnab_frames* f, int32_t pre
   if (frame_geometry(f, &g) || chunk_clips < 1) return 0;
   nnab_frames fc = *f;
   fc.batch = std::min<int64_t>(chunk_clips, f->batch);
-  const size_t ws = nnab_stft_workspace_bytes(&fc, precision);
-  const size_t xin = align256((size_t)fc.batch * g.L * 4);
-  const size_t o = align256((size_t)fc.batch * out_rows * g.T * 4);
-  return 2 * (xin + o) + ws;
+  return pipeline_bytes(fc.batch, g.L, (int64_t)out_rows * g.T) + nnab_stft_workspace_bytes(&fc, precision);
+}
+
+// Three-stage software pipeline over clip chunks shared by the host-buffer entry
+// points: copy-in on `cin`, compute(x_dev, n_clips, out_dev) on the caller's
+// stream, copy-out on `cout`; events order the hand-offs, two slots each.
+template <class Compute>
+static int host_pipeline(int64_t B, int64_t L, int64_t out_per_clip, int64_t chunk, const float* x_host,
+                         float* out_host, char* base, cudaStream_t s, Compute compute) {
+  const size_t xin = align256((size_t)chunk * L * 4);
+  const size_t ob = align256((size_t)chunk * out_per_clip * 4);
+  float* xd[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + xin)};
+  float* od[2] = {reinterpret_cast<float*>(base + 2 * xin), reinterpret_cast<float*>(base + 2 * xin + ob)};
+  cudaStream_t cin = nullptr, cout = nullptr;
+  NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+  NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+  cudaEvent_t start, in_done[2], comp_done[2], out_done[2];
+  NNAB_CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming));
+    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming));
+    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
+  }
+  NNAB_CUDA_TRY(cudaEventRecord(start, s));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(cin, start, 0));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(cout, start, 0));
+  int rc = NNAB_OK;
+  const int64_t n_chunks = (B + chunk - 1) / chunk;
+  for (int64_t i = 0; i < n_chunks && rc == NNAB_OK; ++i) {
+    const int slot = (int)(i & 1);
+    const int64_t c0 = i * chunk;
+    const int64_t nb = std::min<int64_t>(chunk, B - c0);
+    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(cin, comp_done[slot], 0));  // x slot free
+    NNAB_CUDA_TRY(cudaMemcpyAsync(xd[slot], x_host + c0 * L, (size_t)nb * L * 4, cudaMemcpyHostToDevice, cin));
+    NNAB_CUDA_TRY(cudaEventRecord(in_done[slot], cin));
+    NNAB_CUDA_TRY(cudaStreamWaitEvent(s, in_done[slot], 0));
+    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(s, out_done[slot], 0));  // out slot drained
+    rc = compute(xd[slot], nb, od[slot]);
+    NNAB_CUDA_TRY(cudaEventRecord(comp_done[slot], s));
+    NNAB_CUDA_TRY(cudaStreamWaitEvent(cout, comp_done[slot], 0));
+    NNAB_CUDA_TRY(cudaMemcpyAsync(out_host + c0 * out_per_clip, od[slot], (size_t)nb * out_per_clip * 4,
+                                  cudaMemcpyDeviceToHost, cout));
+    NNAB_CUDA_TRY(cudaEventRecord(out_done[slot], cout));
+  }
+  // join: the caller's stream waits for the last copy-out
+  NNAB_CUDA_TRY(cudaEventRecord(out_done[0], cout));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(s, out_done[0], 0));
+  cudaStreamDestroy(cin);
+  cudaStreamDestroy(cout);
+  cudaEventDestroy(start);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(in_done[i]);
+    cudaEventDestroy(comp_done[i]);
+    cudaEventDestroy(out_done[i]);
+  }
+  return rc;
 }
 
 extern "C" int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const float* packed_hi,
@@ -238,61 +294,96 @@ extern "C" int nnab_stft_forward_host(const nnab_frames* f, const float* x_host,
   const int64_t per_clip_out = out_elems_per_clip(out_kind, n_bins, n_mels, g.T);
   const int32_t out_rows = (int32_t)(per_clip_out / g.T);
   const int64_t chunk = std::min<int64_t>(chunk_clips, g.B);
-  if (scratch_bytes < nnab_stft_host_scratch_bytes(f, precision, out_rows, chunk)) return NNAB_EINVAL;
+  if (!device_scratch || scratch_bytes < nnab_stft_host_scratch_bytes(f, precision, out_rows, chunk))
+    return NNAB_EINVAL;
   nnab_frames fc = *f;
   fc.batch = chunk;
-  const size_t xin = align256((size_t)chunk * g.L * 4);
-  const size_t ob = align256((size_t)chunk * per_clip_out * 4);
   char* base = reinterpret_cast<char*>(device_scratch);
-  float* xd[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + xin)};
-  float* od[2] = {reinterpret_cast<float*>(base + 2 * xin), reinterpret_cast<float*>(base + 2 * xin + ob)};
-  void* ws = base + 2 * xin + 2 * ob;
+  void* ws = base + pipeline_bytes(chunk, g.L, per_clip_out);
   const size_t ws_bytes = nnab_stft_workspace_bytes(&fc, precision);
+  return host_pipeline(g.B, g.L, per_clip_out, chunk, x_host, out_host, base, (cudaStream_t)stream,
+                       [&](const float* xd, int64_t nb, float* od) {
+                         fc.batch = nb;
+                         return nnab_stft_forward(&fc, xd, packed_hi, packed_lo, n_bins, fold_nyquist, precision,
+                                                  out_kind, power, eps, mel_w, n_mels, mel_ld, mel_band, od, ws,
+                                                  ws_bytes, stream);
+                       });
+}
 
-  // Three-stage software pipeline over clip chunks: copy-in on `cin`, compute
-  // on the caller's stream, copy-out on `cout`; events order the hand-offs.
-  cudaStream_t s = (cudaStream_t)stream, cin = nullptr, cout = nullptr;
-  NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
-  NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
-  cudaEvent_t start, in_done[2], comp_done[2], out_done[2];
-  NNAB_CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-  for (int i = 0; i < 2; ++i) {
-    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming));
-    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming));
-    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
-  }
-  NNAB_CUDA_TRY(cudaEventRecord(start, s));
-  NNAB_CUDA_TRY(cudaStreamWaitEvent(cin, start, 0));
-  NNAB_CUDA_TRY(cudaStreamWaitEvent(cout, start, 0));
-  const int64_t n_chunks = (g.B + chunk - 1) / chunk;
-  for (int64_t i = 0; i < n_chunks && rc == NNAB_OK; ++i) {
-    const int slot = (int)(i & 1);
-    const int64_t c0 = i * chunk;
-    const int64_t nb = std::min<int64_t>(chunk, g.B - c0);
-    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(cin, comp_done[slot], 0));  // x slot free
-    NNAB_CUDA_TRY(cudaMemcpyAsync(xd[slot], x_host + c0 * g.L, (size_t)nb * g.L * 4, cudaMemcpyHostToDevice, cin));
-    NNAB_CUDA_TRY(cudaEventRecord(in_done[slot], cin));
-    NNAB_CUDA_TRY(cudaStreamWaitEvent(s, in_done[slot], 0));
-    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(s, out_done[slot], 0));  // out slot drained
-    fc.batch = nb;
-    rc = nnab_stft_forward(&fc, xd[slot], packed_hi, packed_lo, n_bins, fold_nyquist, precision, out_kind, power,
-                           eps, mel_w, n_mels, mel_ld, mel_band, od[slot], ws, ws_bytes, s);
-    NNAB_CUDA_TRY(cudaEventRecord(comp_done[slot], s));
-    NNAB_CUDA_TRY(cudaStreamWaitEvent(cout, comp_done[slot], 0));
-    NNAB_CUDA_TRY(cudaMemcpyAsync(out_host + c0 * per_clip_out, od[slot], (size_t)nb * per_clip_out * 4,
-                                  cudaMemcpyDeviceToHost, cout));
-    NNAB_CUDA_TRY(cudaEventRecord(out_done[slot], cout));
-  }
-  // join: the caller's stream waits for the last copy-out
-  NNAB_CUDA_TRY(cudaEventRecord(out_done[0], cout));
-  NNAB_CUDA_TRY(cudaStreamWaitEvent(s, out_done[0], 0));
-  cudaStreamDestroy(cin);
-  cudaStreamDestroy(cout);
-  cudaEventDestroy(start);
-  for (int i = 0; i < 2; ++i) {
-    cudaEventDestroy(in_done[i]);
-    cudaEventDestroy(comp_done[i]);
-    cudaEventDestroy(out_done[i]);
-  }
-  return rc;
+extern "C" size_t nnab_cqt1992v2_host_scratch_bytes(const nnab_frames* f, int32_t precision, int32_t n_bins,
+                                                    int32_t out_kind, int64_t chunk_clips) {
+  FrameGeom g;
+  if (frame_geometry(f, &g) || chunk_clips < 1) return 0;
+  nnab_frames fc = *f;
+  fc.batch = std::min<int64_t>(chunk_clips, f->batch);
+  const int64_t per = (out_kind == NNAB_OUT_COMPLEX ? 2ll : 1ll) * n_bins * g.T;
+  return pipeline_bytes(fc.batch, g.L, per) + nnab_stft_workspace_bytes(&fc, precision);
+}
+
+extern "C" int nnab_cqt1992v2_forward_host(const nnab_frames* f, const float* x_host, const float* packed_hi,
+                                           const float* packed_lo, int32_t n_bins, const uint32_t* schedule,
+                                           int32_t n_entries, int32_t precision, int32_t out_kind, float eps,
+                                           float* out_host, int64_t chunk_clips, void* device_scratch,
+                                           size_t scratch_bytes, void* stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  FrameGeom g;
+  if ((rc = frame_geometry(f, &g))) return rc;
+  if (!x_host || !out_host || chunk_clips < 1) return NNAB_EINVAL;
+  if (g.B == 0) return NNAB_OK;
+  const int64_t chunk = std::min<int64_t>(chunk_clips, g.B);
+  if (!device_scratch || scratch_bytes < nnab_cqt1992v2_host_scratch_bytes(f, precision, n_bins, out_kind, chunk))
+    return NNAB_EINVAL;
+  const int64_t per = (out_kind == NNAB_OUT_COMPLEX ? 2ll : 1ll) * n_bins * g.T;
+  nnab_frames fc = *f;
+  fc.batch = chunk;
+  char* base = reinterpret_cast<char*>(device_scratch);
+  void* ws = base + pipeline_bytes(chunk, g.L, per);
+  const size_t ws_bytes = nnab_stft_workspace_bytes(&fc, precision);
+  return host_pipeline(g.B, g.L, per, chunk, x_host, out_host, base, (cudaStream_t)stream,
+                       [&](const float* xd, int64_t nb, float* od) {
+                         fc.batch = nb;
+                         return nnab_cqt1992v2_forward(&fc, xd, packed_hi, packed_lo, n_bins, schedule, n_entries,
+                                                       precision, out_kind, eps, od, ws, ws_bytes, stream);
+                       });
+}
+
+extern "C" size_t nnab_cqt2010v2_host_scratch_bytes(int64_t L, int32_t early_stages, int32_t n_bins, int32_t T,
+                                                    int32_t out_kind, int64_t chunk_clips) {
+  if (chunk_clips < 1 || L < 1) return 0;
+  const int64_t per = (out_kind == NNAB_OUT_COMPLEX ? 2ll : 1ll) * n_bins * T;
+  return pipeline_bytes(chunk_clips, L, per) + nnab_cqt2010v2_workspace_bytes(chunk_clips, L, early_stages);
+}
+
+extern "C" int nnab_cqt2010v2_forward_host(const float* x_host, int64_t B, int64_t L, const float* taps,
+                                           int32_t n_taps, const float* k_re, const float* k_im, int32_t n_filters,
+                                           int32_t width, int32_t early_stages, int32_t n_octaves,
+                                           int32_t kernel_hop, int32_t first_bin, int32_t bins_per_octave,
+                                           int32_t n_bins, int32_t pad_mode, int32_t out_kind, int32_t precision,
+                                           float* out_host, int64_t chunk_clips, void* device_scratch,
+                                           size_t scratch_bytes, void* stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  if (!x_host || !out_host || chunk_clips < 1 || B < 0) return NNAB_EINVAL;
+  int32_t T = 0;  // validate the configuration and get the frame count (B = 0: no launch)
+  float dummy = 0.f;
+  if ((rc = nnab_cqt2010v2_forward(&dummy, 0, L, taps, n_taps, k_re, k_im, n_filters, width, early_stages,
+                                   n_octaves, kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind,
+                                   precision, &dummy, &T, nullptr, 0, stream)))
+    return rc;
+  if (B == 0) return NNAB_OK;
+  const int64_t chunk = std::min<int64_t>(chunk_clips, B);
+  if (!device_scratch || scratch_bytes < nnab_cqt2010v2_host_scratch_bytes(L, early_stages, n_bins, T, out_kind, chunk))
+    return NNAB_EINVAL;
+  const int64_t per = (out_kind == NNAB_OUT_COMPLEX ? 2ll : 1ll) * n_bins * T;
+  char* base = reinterpret_cast<char*>(device_scratch);
+  void* ws = base + pipeline_bytes(chunk, L, per);
+  const size_t ws_bytes = nnab_cqt2010v2_workspace_bytes(chunk, L, early_stages);
+  return host_pipeline(B, L, per, chunk, x_host, out_host, base, (cudaStream_t)stream,
+                       [&](const float* xd, int64_t nb, float* od) {
+                         return nnab_cqt2010v2_forward(xd, nb, L, taps, n_taps, k_re, k_im, n_filters, width,
+                                                       early_stages, n_octaves, kernel_hop, first_bin,
+                                                       bins_per_octave, n_bins, pad_mode, out_kind, precision, od,
+                                                       nullptr, ws, ws_bytes, stream);
+                       });
 }

@@ -324,6 +324,26 @@ class CqtLongEngine:
                 "cqt1992v2_forward_staged")
         return out
 
+    def forward_host(self, x_host: torch.Tensor, kind: str = "magnitude", chunk_clips: int = 148,
+                     out_host: torch.Tensor | None = None, eps: float = 1e-12) -> torch.Tensor:
+        """Pinned host (B, L) -> pinned host (B, n_bins, T), streamed through the
+        GPU in chunks with copy/compute overlap (nnab_cqt1992v2_forward_host)."""
+        lib = L.load()
+        B, length = int(x_host.shape[0]), int(x_host.shape[1])
+        T = self.n_frames(length)
+        k = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX}[kind]
+        if out_host is None:
+            dt = torch.complex64 if kind == "complex" else torch.float32
+            out_host = torch.empty(B, self.n_bins, T, dtype=dt, pin_memory=True)
+        f = self.frames(B, length)
+        ws = self._ws.get(lib.nnab_cqt1992v2_host_scratch_bytes(C.byref(f), self.precision, self.n_bins, k,
+                                                                 chunk_clips), self.device)
+        L.check(lib.nnab_cqt1992v2_forward_host(
+            C.byref(f), x_host.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins,
+            self.schedule.data_ptr(), self.n_entries, self.precision, k, float(eps), out_host.data_ptr(),
+            int(chunk_clips), ws.data_ptr(), ws.numel(), L.stream_handle(self.device)), "cqt1992v2_forward_host")
+        return out_host
+
 
 class Cqt2010Engine:
     """CQT2010v2's octave recursion (transforms.py:241-323): FIR halvings and
@@ -378,6 +398,27 @@ class Cqt2010Engine:
         L.check(rc, "cqt2010v2_forward")
         return T.value
 
+    def forward_host(self, x_host: torch.Tensor, kind: str = "magnitude", chunk_clips: int = 148,
+                     out_host: torch.Tensor | None = None) -> torch.Tensor:
+        """Pinned host (B, L) -> pinned host (B, n_bins, T) through
+        nnab_cqt2010v2_forward_host (chunked H2D / compute / D2H overlap)."""
+        lib = L.load()
+        B, length = int(x_host.shape[0]), int(x_host.shape[1])
+        T = self.n_frames(length)
+        k = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX}[kind]
+        if out_host is None:
+            dt = torch.complex64 if kind == "complex" else torch.float32
+            out_host = torch.empty(B, self.n_bins, T, dtype=dt, pin_memory=True)
+        ws = self._ws.get(lib.nnab_cqt2010v2_host_scratch_bytes(length, self.early_stages, self.n_bins, T, k,
+                                                                 chunk_clips), self.device)
+        L.check(lib.nnab_cqt2010v2_forward_host(
+            x_host.data_ptr(), B, length, self.taps.ctypes.data, self.taps.size, self.k_re.data_ptr(),
+            self.k_im.data_ptr(), self.n_filters, self.width, self.early_stages, self.n_octaves, self.kernel_hop,
+            self.first_bin, self.bins_per_octave, self.n_bins, self.pad_mode, k, self.precision,
+            out_host.data_ptr(), int(chunk_clips), ws.data_ptr(), ws.numel(), L.stream_handle(self.device)),
+            "cqt2010v2_forward_host")
+        return out_host
+
     def forward(self, x: torch.Tensor, kind: str = "magnitude") -> torch.Tensor:
         if x.dim() == 1:
             x = x[None]
@@ -387,7 +428,7 @@ class Cqt2010Engine:
         B, length = int(x.shape[0]), int(x.shape[1])
         T = self.n_frames(length)
         dt = torch.complex64 if kind == "complex" else torch.float32
-        out = torch.zeros(B, self.n_bins, T, dtype=dt, device=self.device)
+        out = torch.empty(B, self.n_bins, T, dtype=dt, device=self.device)  # every row is written
         if B == 0:
             return out
         rc, _ = self._call(x, B, length, kind, out)

@@ -98,3 +98,22 @@ def test_cqt2010v2_batch_matches_oracle(cuda_dev, precision):
     ref2 = O.cqt2010v2_clip(sweep.astype(np.float64), cfg, plan)
     got2 = rec_engine(cfg, precision).forward(torch.from_numpy(sweep).to(cuda_dev))[0].cpu().numpy()
     assert O.peak_err(got2, ref2) <= TOL[precision]
+
+
+def test_cqt_host_paths_match_device(cuda_dev):
+    """The C-ABI host entry points (pinned buffers, chunked H2D / compute / D2H)
+    give the device path's results, including a ragged last chunk."""
+    cfg = O.CqtCfg(sr=SR)
+    rng = np.random.default_rng(3)
+    x = torch.from_numpy((rng.standard_normal((7, 80000)) * 0.5).astype(np.float32))
+    xh = x.pin_memory()
+    e1 = long_engine(cfg, "tf32")
+    want = e1.forward(x.to(cuda_dev)).cpu()
+    got = e1.forward_host(xh, chunk_clips=3)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    e2 = rec_engine(cfg, "tf32")
+    want2 = e2.forward(x.to(cuda_dev)).cpu()
+    got2 = e2.forward_host(xh, chunk_clips=3)
+    torch.cuda.synchronize()
+    assert torch.equal(got2, want2)
