@@ -22,6 +22,8 @@ KEYS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
     "smsp__average_warp_latency_issue_stalled_barrier", "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "lts__t_sector_hit_rate.pct", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum",
 ]
 
 
