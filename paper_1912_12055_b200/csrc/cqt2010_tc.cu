@@ -236,69 +236,53 @@ NNAB_DEV void edge_pass(__half* s, uint8_t* planes, uint32_t pl, int rows, int n
   }
 }
 
-// 16 samples x_ext[j0 - 1 .. j0 + 14] of the clip (j0 odd): f[2k+1] = odd phase,
-// f[2k] = even phase; reflect at the ends, zero beyond one reflection.
-NNAB_DEV void x_chunk16(const float* xb, int64_t L, bool vec, int64_t j0, float* f) {
-  if (vec && j0 >= 1 && j0 + 15 <= L) {
-    const float4* src = reinterpret_cast<const float4*>(xb + j0 - 1);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 a = __ldg(src + k);
-      f[4 * k] = a.x;
-      f[4 * k + 1] = a.y;
-      f[4 * k + 2] = a.z;
-      f[4 * k + 3] = a.w;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      int64_t j = j0 - 1 + k;
-      if (j < 0) j = -j;
-      if (j >= L) j = 2 * (L - 1) - j;
-      f[k] = (j >= 0 && j < L) ? __ldg(xb + j) : 0.f;
-    }
-  }
-}
-
 // Stage-1 operands of blocks [n0, n0 + nb): odd-phase planes (rows 0 .. nb) and
 // the even phase (centre taps, xe[u] = x[2 (128 n0 + u)]), scaled, FP16.
-// Thread -> plane row r = tid & 127 (row 128 by the first 16 threads after) and
-// plane chunks qq = tid >> 7 + 2u; four 64-byte chunks in flight per round.
+// The tile's clip range x_ext[256 n0 - 128 .. 256 (n0 + nb + 1) - 128) is read
+// with coalesced float4 loads (lane = consecutive 16 bytes): float4 g holds odd
+// samples m = 128 n0 + 2g, +1 (one 4-byte store into the planes, whose stride is
+// padded off 128 B so the eight chunks a warp touches hit different banks) and
+// even samples u = 2g - 64, +1 (one 4-byte store into xe).
 NNAB_DEV void build_x(Ctx& c, const float* xb, float scale, int n0, int nb, bool vec) {
   const TcParams& p = c.p;
   uint8_t* planes = c.base + p.off_x;
   __half* xe = reinterpret_cast<__half*>(c.base + p.off_xe);
-  const int r = threadIdx.x & 127, q0 = threadIdx.x >> 7;
-  auto put = [&](int rr, int qq, const float* f) {
-    __align__(16) __half2 od[4];
+  const int64_t L = p.L;
+  const int64_t j_start = 256 * (int64_t)n0 - 128;
+  const int n4 = (nb + 1) * 64;  // float4 groups
+  constexpr int kPer = 8;        // groups in flight per thread
+  for (int g0 = threadIdx.x; g0 < n4; g0 += kPer * kCompute) {
+    float4 f[kPer];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) od[k] = __floats2half2_rn(f[4 * k + 1] * scale, f[4 * k + 3] * scale);
-    *reinterpret_cast<uint4*>(planes + (uint32_t)qq * p.pl_x + (uint32_t)rr * 16u) = *reinterpret_cast<uint4*>(od);
-    const int u0 = rr * 128 + qq * 8 - 64;  // even samples x[j0 - 1 + 2k] = x[2 (m0 - 64 + k)]
-    if (u0 >= 0 && u0 < nb * 128) {
-      __align__(16) __half2 ev[4];
+    for (int u = 0; u < kPer; ++u) {
+      const int g = g0 + u * kCompute;
+      const int64_t j = j_start + 4 * (int64_t)g;
+      if (g >= n4) {
+        f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if (vec && j >= 0 && j + 4 <= L) {
+        f[u] = __ldg(reinterpret_cast<const float4*>(xb + j));
+      } else {
+        float e[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) ev[k] = __floats2half2_rn(f[4 * k] * scale, f[4 * k + 2] * scale);
-      st8(xe, u0, *reinterpret_cast<uint4*>(ev));
-    }
-  };
-  if (r <= nb) {
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      float f[4][16];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int qq = q0 + 2 * (4 * h + u);
-        x_chunk16(xb, p.L, vec, 2 * ((int64_t)(n0 + r) * 128 + qq * 8) - 127, f[u]);
+        for (int k = 0; k < 4; ++k) {
+          int64_t jj = j + k;
+          if (jj < 0) jj = -jj;
+          if (jj >= L) jj = 2 * (L - 1) - jj;
+          e[k] = (jj >= 0 && jj < L) ? __ldg(xb + jj) : 0.f;  // beyond one reflection: never a kept output
+        }
+        f[u] = make_float4(e[0], e[1], e[2], e[3]);
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) put(r, q0 + 2 * (4 * h + u), f[u]);
     }
-  }
-  if (nb == 128 && threadIdx.x < 16) {
-    float f[16];
-    x_chunk16(xb, p.L, vec, 2 * ((int64_t)(n0 + 128) * 128 + threadIdx.x * 8) - 127, f);
-    put(128, threadIdx.x, f);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int g = g0 + u * kCompute;
+      if (g >= n4) continue;
+      const int m = 2 * g;  // odd-phase index relative to 128 n0
+      *reinterpret_cast<__half2*>(planes + (uint32_t)((m & 127) >> 3) * p.pl_x + (uint32_t)(m >> 7) * 16u +
+                                  (uint32_t)(m & 7) * 2u) = __floats2half2_rn(f[u].y * scale, f[u].w * scale);
+      const int ue = 2 * g - 64;
+      if (ue >= 0 && ue < nb * 128) *reinterpret_cast<__half2*>(xe + sw(ue)) = __floats2half2_rn(f[u].x * scale, f[u].z * scale);
+    }
   }
 }
 
@@ -352,7 +336,7 @@ NNAB_DEV void issue_conv(Ctx& c, int ntile) {
 
 // conv epilogue: warp w reads lane quarter w & 3 of tile w >> 2: thread = frame,
 // columns 2j, 2j+1 = re, im of bin j; stores coalesced along T.
-NNAB_DEV void conv_epilogue(Ctx& c, int alpha, int64_t b, int t0, int ntile, float out_scale) {
+NNAB_DEV void conv_epilogue(Ctx& c, int alpha, int64_t b, int t0, int ntile, float out_scale, float* stage) {
   const TcParams& p = c.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, u = warp >> 2;
@@ -368,6 +352,11 @@ NNAB_DEV void conv_epilogue(Ctx& c, int alpha, int64_t b, int t0, int ntile, flo
   for (int j = 0; j < NCONV / 2; ++j) {
     if (j < skip || j >= p.n_filt) continue;
     const float re = v[2 * j] * out_scale, im = v[2 * j + 1] * out_scale;
+    if (stage) {  // the octave's rows are one aligned block of the output: staged, bulk-stored
+      stage[(j - skip) * p.T + t] = p.out_kind == NNAB_OUT_POWER ? fmaf(re, re, im * im)
+                                                                 : fast_sqrt(fmaf(re, re, im * im));
+      continue;
+    }
     const int64_t o = (b * p.n_bins + row0 + j) * (int64_t)p.T + t;
     if (p.out_kind == NNAB_OUT_COMPLEX) {
       reinterpret_cast<float2*>(p.out)[o] = make_float2(re, im);
@@ -611,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
         }
         for (int t0 = 0; t0 < p.T; t0 += 256) {
           const int ntile = min(2, (p.T - t0 + 127) / 128);
+          if (a > 0 || t0 > 0) csync();  // thread 0 has drained the previous bulk store's reads
           build_frames(c, sig(a), h, t0, ntile);
           fence_proxy_async_smem();
           csync();
@@ -649,15 +639,30 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
           conv_phase ^= 1;
           tc_fence_after();
           c.pf.mark(p, 10);
-          conv_epilogue(c, a, b, t0, ntile, out_scale);
+          // the octave's rows (row0 + skip ..) are contiguous in the (B, n_bins, T) output;
+          // when that block is 16-byte aligned it is staged in the (consumed) im2col
+          // tile and written with one bulk copy
+          const int skip = max(0, a * p.bpo - p.first_bin);
+          const int64_t o0 = (b * p.n_bins + p.first_bin - a * p.bpo + skip) * (int64_t)p.T;
+          const uint32_t bytes = (uint32_t)((p.n_filt - skip) * p.T * 4);
+          const bool staged = p.out_kind != NNAB_OUT_COMPLEX && p.T <= 256 && (o0 & 3) == 0 && (bytes & 15) == 0 &&
+                              bytes <= (uint32_t)((128 + p.rows2) * KC * 2);
+          float* stage = staged ? reinterpret_cast<float*>(base + p.off_col) : nullptr;
+          conv_epilogue(c, a, b, t0, ntile, out_scale, stage);
           c.pf.mark(p, 11);
           tc_fence_before();
+          if (staged) fence_proxy_async_smem();
           csync();
+          if (staged && tid == 0) {
+            bulk_store(p.out + o0, stage, bytes);
+            bulk_wait_read();  // the next octave's im2col overwrites the stage
+          }
         }
       }
       c.pf.mark(p, 15);
     }
   }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // output bulk stores performed
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -729,7 +734,7 @@ int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, i
   p.off_filt = off;  off += KC / 8 * 512;
   p.off_ring = off;  off += 2 * kRing;
   const int r1 = off;
-  p.pl_x = (kTile1 + 8) * 16;
+  p.pl_x = (kTile1 + 8) * 16 + 16;  // +16 B: consecutive planes start in different banks
   p.off_x = off;     off += p.pl_x * 16;
   p.off_xe = off;    off += kTile1 * 128 * 2;
   int r1_end = off;

@@ -164,6 +164,16 @@ NNAB_DEV void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_
       : "memory");
 }
 
+// 1-D bulk copy shared -> global (TMA engine), bulk-group completion.
+NNAB_DEV void bulk_store(void* gdst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// Wait until the bulk stores committed so far have read their shared-memory source.
+NNAB_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 // Arrive on an mbarrier once all prior tcgen05 ops of this thread completed.
 NNAB_DEV void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
