@@ -46,7 +46,7 @@ namespace nnab {
 namespace {
 
 constexpr int kCompute = 256;             // warps 0-7: MMA issue (thread 0), builds, epilogues
-constexpr int kThreads = kCompute + 32;   // warp 8: scan of the next clip
+constexpr int kThreads = kCompute + 64;   // warp 8: scan of the next clip; warp 9: MMA issue
 constexpr int kTile1 = 128;               // stage-1 blocks per MMA tile (= M)
 constexpr int ML = 128;                   // reflect margins of the contiguous signal copies (fp16)
 constexpr int KC = 96;                    // conv taps (K), padded
@@ -74,7 +74,7 @@ struct TcParams {
   const float* k_im;
   float* out;
   // shared-memory carve-up (bytes from the 1 KB-aligned base)
-  int32_t off_toep, off_filt, off_ring, off_x, off_xe, off_y, off_ye, off_col, off_bars;
+  int32_t off_toep, off_filt, off_ring, off_x, off_xe, off_y, off_ye, off_col, off_stage, off_bars;
   int32_t pl_x, pl_y, y_rows;          // plane strides (bytes); stage-2 plane rows
   unsigned long long* prof;            // optional per-phase cycle counters (nnab_debug_cqt2010_profile)
 };
@@ -306,19 +306,25 @@ NNAB_DEV uint4 frame_chunk(const TcParams& p, const __half* sig, int h, int tt, 
   return *reinterpret_cast<uint4*>(hv);
 }
 NNAB_DEV void build_frames(Ctx& c, const __half* sig, int h, int t0, int ntile) {
+  // thread = frame t0 + tid (tile 0: tid < 128, tile 1: the first rows2 frames after);
+  // its 12 chunk loads are issued before any store
   const TcParams& p = c.p;
-  uint8_t* col = c.base + p.off_col;
-  for (int e = threadIdx.x; e < 128 * (KC / 8); e += kCompute) {
-    const int t = e & 127, cc = e >> 7;
-    *reinterpret_cast<uint4*>(col + cc * 2048 + t * 16) = frame_chunk(p, sig, h, t0 + t, cc);
+  const int t = threadIdx.x;
+  uint8_t* dst;
+  uint32_t cstride;
+  if (t < 128) {
+    dst = c.base + p.off_col + t * 16;
+    cstride = 2048;
+  } else {
+    if (ntile < 2 || t - 128 >= p.rows2) return;
+    dst = c.base + p.off_col + 128 * KC * 2 + (t - 128) * 16;
+    cstride = (uint32_t)p.rows2 * 16u;
   }
-  if (ntile > 1) {
-    uint8_t* col2 = col + 128 * KC * 2;
-    for (int e = threadIdx.x; e < p.rows2 * (KC / 8); e += kCompute) {
-      const int t = e % p.rows2, cc = e / p.rows2;
-      *reinterpret_cast<uint4*>(col2 + cc * p.rows2 * 16 + t * 16) = frame_chunk(p, sig, h, t0 + 128 + t, cc);
-    }
-  }
+  uint4 v[KC / 8];
+#pragma unroll
+  for (int cc = 0; cc < KC / 8; ++cc) v[cc] = frame_chunk(p, sig, h, t0 + t, cc);
+#pragma unroll
+  for (int cc = 0; cc < KC / 8; ++cc) *reinterpret_cast<uint4*>(dst + cc * cstride) = v[cc];
 }
 
 NNAB_DEV void issue_conv(Ctx& c, int ntile) {
@@ -371,16 +377,17 @@ NNAB_DEV void conv_epilogue(Ctx& c, int alpha, int64_t b, int t0, int ntile, flo
 __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_constant__ TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // bars[0] FIR MMAs, [1..2] scan ring, [3] scale published, [4] scan may start the next clip, [5] conv MMAs
+  // bars[0] FIR MMAs done, [1..2] scan ring, [3] scale published, [4] scan may start the next clip,
+  // [5] conv MMAs done, [6] FIR operands ready, [7] conv operands ready
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + p.off_bars);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
-  volatile int* scale_exp = reinterpret_cast<volatile int*>(bars + 7);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
+  volatile int* scale_exp = reinterpret_cast<volatile int*>(bars + 9);
   __shared__ unsigned long long prof_acc[16];
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool vec = (p.L % 4) == 0;
 
   if (tid == 0) {
-    for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(tslot);
@@ -464,6 +471,41 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
       }
       __syncwarp();
     }
+  } else if (warp == kCompute / 32 + 1) {
+    // ------------------------------------------------ MMA issue warp: the compute warps' schedule,
+    // each step waiting for its operands to be ready (the issue of a tcgen05.mma chain
+    // blocks its thread for ~100 cycles per instruction, which no compute warp pays now)
+    if (elect_one()) {
+      Ctx c{p, base, *tslot, &bars[0], 0, {}};
+      uint32_t go_fir = 0, go_conv = 0;
+      auto wait_fir = [&]() { mbar_wait(&bars[6], go_fir); go_fir ^= 1; };
+      auto wait_conv = [&]() { mbar_wait(&bars[7], go_conv); go_conv ^= 1; };
+      const uint32_t xp_s = smem_u32(base + p.off_x), yp_s = smem_u32(base + p.off_y);
+      for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+        for (int t = 0; t < p.n1_tiles; ++t) {
+          wait_fir();
+          issue_fir(c, xp_s, p.pl_x, 0, 0);
+          mma_commit(&bars[0]);
+        }
+        wait_fir();
+        issue_fir(c, yp_s, p.pl_y, 0, 0);
+        if (p.oct_blocks[0] > 128) issue_fir(c, yp_s, p.pl_y, p.oct_blocks[0] - 128, 128);
+        mma_commit(&bars[0]);
+        for (int a = 0; a < p.n_oct; ++a) {
+          if (a + 1 < p.n_oct) {
+            wait_fir();
+            issue_fir(c, smem_u32(base + p.o_off[a]), (uint32_t)p.plane_rows[a] * 16u, 0, 0);
+            mma_commit(&bars[0]);
+          }
+          for (int t0 = 0; t0 < p.T; t0 += 256) {
+            wait_conv();
+            issue_conv(c, min(2, (p.T - t0 + 127) / 128));
+            mma_commit(&bars[5]);
+          }
+        }
+      }
+    }
+    __syncwarp();
   } else {
     // ------------------------------------------------ compute warps
     Ctx c{p, base, *tslot, &bars[0], 0, {}};
@@ -492,10 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
         fence_proxy_async_smem();
         csync();
         c.pf.mark(p, 0);
-        if (tid == 0) {
-          issue_fir(c, xp_s, p.pl_x, 0, 0);
-          mma_commit(c.bar);
-        }
+        if (tid == 0) mbar_arrive(&bars[6]);  // operands ready: the issue warp runs the FIR
         c.wait_mma();
         c.pf.mark(p, 1);
         const int u_base = t * kTile1 * 128;
@@ -561,11 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
       {
         const int n2 = p.oct_len[0], nb2 = p.oct_blocks[0];
         const int row_b = nb2 > 128 ? nb2 - 128 : 0;  // second tile: the last 128 blocks
-        if (tid == 0) {
-          issue_fir(c, yp_s, p.pl_y, 0, 0);
-          if (nb2 > 128) issue_fir(c, yp_s, p.pl_y, row_b, 128);
-          mma_commit(c.bar);
-        }
+        if (tid == 0) mbar_arrive(&bars[6]);
         c.wait_mma();
         c.pf.mark(p, 4);
         uint8_t* o0 = planes_of(0);
@@ -594,21 +629,18 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
       for (int a = 0; a < p.n_oct; ++a) {
         const int h = p.kernel_hop >> a;
         const bool halve = a + 1 < p.n_oct;
-        if (halve && tid == 0) {
-          issue_fir(c, smem_u32(base + p.o_off[a]), (uint32_t)p.plane_rows[a] * 16u, 0, 0);
-          mma_commit(c.bar);
-        }
+        if (halve && tid == 0) mbar_arrive(&bars[6]);
         for (int t0 = 0; t0 < p.T; t0 += 256) {
           const int ntile = min(2, (p.T - t0 + 127) / 128);
-          if (a > 0 || t0 > 0) csync();  // thread 0 has drained the previous bulk store's reads
+          c.pf.mark(p, 3);
           build_frames(c, sig(a), h, t0, ntile);
+          c.pf.mark(p, 6);
           fence_proxy_async_smem();
+          if (tid == 0) bulk_wait_read();  // the previous octave's output stage may be rewritten after this sync
+          c.pf.mark(p, 13);
           csync();
           c.pf.mark(p, 9);
-          if (tid == 0) {
-            issue_conv(c, ntile);
-            mma_commit(conv_bar);
-          }
+          if (tid == 0) mbar_arrive(&bars[7]);
           if (halve && t0 == 0) {
             c.wait_mma();
             c.pf.mark(p, 7);
@@ -645,18 +677,15 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
           const int skip = max(0, a * p.bpo - p.first_bin);
           const int64_t o0 = (b * p.n_bins + p.first_bin - a * p.bpo + skip) * (int64_t)p.T;
           const uint32_t bytes = (uint32_t)((p.n_filt - skip) * p.T * 4);
-          const bool staged = p.out_kind != NNAB_OUT_COMPLEX && p.T <= 256 && (o0 & 3) == 0 && (bytes & 15) == 0 &&
-                              bytes <= (uint32_t)((128 + p.rows2) * KC * 2);
-          float* stage = staged ? reinterpret_cast<float*>(base + p.off_col) : nullptr;
+          const bool staged = p.out_kind != NNAB_OUT_COMPLEX && p.T <= 256 && (o0 & 3) == 0 && (bytes & 15) == 0;
+          float* stage = staged ? reinterpret_cast<float*>(base + p.off_stage) : nullptr;
           conv_epilogue(c, a, b, t0, ntile, out_scale, stage);
           c.pf.mark(p, 11);
           tc_fence_before();
           if (staged) fence_proxy_async_smem();
           csync();
-          if (staged && tid == 0) {
-            bulk_store(p.out + o0, stage, bytes);
-            bulk_wait_read();  // the next octave's im2col overwrites the stage
-          }
+          c.pf.mark(p, 14);
+          if (staged && tid == 0) bulk_store(p.out + o0, stage, bytes);  // drained before the next octave's epilogue
         }
       }
       c.pf.mark(p, 15);
@@ -748,6 +777,7 @@ int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, i
   p.pl_y = p.y_rows * 16;
   p.off_y = r2;
   p.off_ye = r2 + p.pl_y * 16 + kSlack;
+  p.off_stage = 0;  // set below (after the octave region)
   int r2_end = p.off_ye + rnd(L0 + 16, 128) * 2;  // whole 128-sample rows (swizzle stays inside)
   o = r2;  // octaves >= 1 and the im2col tile reuse R2; octave a only lives with a +- 1 (ping-pong)
   p.off_col = o;     o += (128 + p.rows2) * KC * 2;
@@ -767,7 +797,8 @@ int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, i
   o += kSlack;
   r2_end = std::max(r2_end, o);
   off = rnd(r2_end, 128);
-  p.off_bars = off;  off += 64;
+  p.off_stage = off; off += rnd((int64_t)n_filt * std::min(T, 256) * 4, 128);  // one octave's output rows
+  p.off_bars = off;  off += 128;
   pl->smem = 1024 + (size_t)off;
   if (pl->smem > 227 * 1024) return NNAB_ENOTSUP;
   return NNAB_OK;

@@ -16,8 +16,8 @@ fn(1, None)
 eng.forward(x); torch.cuda.synchronize()
 out = (C.c_ulonglong * 16)()
 fn(0, out)
-names = ["S1 build", "S1 mma", "S1 epi", "-", "S2 mma", "S2 epi", "-", "-", "halving epi",
-         "conv im2col", "conv+halving mma", "conv epi", "wait scale", "-", "-", "tail"]
+names = ["S1 build", "S1 mma", "S1 epi", "FIR issue", "S2 mma", "S2 epi", "frames build", "halving mma wait",
+         "halving epi", "im2col sync", "conv mma wait", "conv epi", "wait scale", "bulk wait", "conv epi sync", "tail"]
 tot = sum(out)
 for n, v in zip(names, out):
     print(f"{n:18s} {v/1770:10.0f} cycles/clip  {100*v/tot:5.1f}%")
