@@ -117,3 +117,30 @@ def test_cqt_host_paths_match_device(cuda_dev):
     got2 = e2.forward_host(xh, chunk_clips=3)
     torch.cuda.synchronize()
     assert torch.equal(got2, want2)
+
+
+@pytest.mark.parametrize("case", ["quiet", "loud", "impulse", "silence_spike", "tone"])
+def test_cqt2010v2_fp16_scaling_robust(cuda_dev, case):
+    """The fused chain runs FP16 operands under an exact per-clip power-of-two
+    scale: clips far from unit amplitude, sparse spikes and constant signals stay
+    within the TF32-mode tolerance (peak-normalised, like the reference tests)."""
+    cfg = O.CqtCfg(sr=SR)
+    rng = np.random.default_rng(11)
+    n = 80000
+    if case == "quiet":
+        x = rng.standard_normal(n) * 1e-6
+    elif case == "loud":
+        x = rng.standard_normal(n) * 2e4
+    elif case == "impulse":
+        x = np.zeros(n)
+        x[40000] = 1.0
+    elif case == "silence_spike":
+        x = rng.standard_normal(n) * 1e-8
+        x[61234] = 3.0
+    else:  # (a constant input is not a case: its CQT is ~3e-5 of the input, below any 11-bit-operand mode)
+        x = 0.8 * np.sin(2 * np.pi * 440.0 * np.arange(n) / SR)
+    x = x.astype(np.float32)
+    ref = O.cqt2010v2_clip(x.astype(np.float64), cfg, O.cqt2010_plan(cfg))
+    got = rec_engine(cfg, "tf32").forward(torch.from_numpy(x).to(cuda_dev))[0].cpu().numpy()
+    assert np.isfinite(got).all()
+    assert O.peak_err(got, ref) <= TOL["tf32"], O.peak_err(got, ref)
