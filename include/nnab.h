@@ -198,6 +198,26 @@ int nnab_cqt1992v2_forward_staged(const nnab_frames* f, const float* packed_hi, 
                                   int32_t out_kind, float eps, float* out, const void* workspace,
                                   size_t workspace_bytes, void* stream);
 
+/* CQT1992v2 as a hop-offset GEMM ("E-GEMM", csrc/cqt1992_egemm.cu):
+ * E[s][(row, r)] = sum_c rows[s][c] K[row][hop r + c] over the (row, r) pairs a
+ * row's support touches, D[s][row] = sum_r E[s + r][(row, r)] in a shared-memory
+ * ring, fused magnitude.  Same result as nnab_cqt1992v2_forward (TF32 only).
+ * nnab_cqt_egemm_plan (host) groups whole bins' columns (<= 256 per group,
+ * sorted by r): col_table [max_groups*256] = row_local << 8 | r (0xFFFF
+ * unused), group_rows [max_groups*64] = bank row 2*bin (+1 for Im) or -1. */
+int nnab_cqt_egemm_plan(const int32_t* support, int32_t n_bins, int32_t width, int32_t hop, int32_t max_groups,
+                        uint16_t* col_table, int32_t* group_rows, uint32_t* run_table /* [max_groups*4*65] */,
+                        int32_t* n_groups, int32_t* r_max);
+size_t nnab_cqt_egemm_bank_bytes(int32_t n_groups, int32_t hop);
+int nnab_pack_cqt_egemm(const float* k_re, const float* k_im, int32_t width, int32_t hop, const uint16_t* col_table,
+                        const int32_t* group_rows, int32_t n_groups, int32_t precision, float* packed_hi,
+                        float* packed_lo, void* stream);
+int nnab_cqt1992v2_egemm_staged(const nnab_frames* f, const float* packed_hi, const uint16_t* col_table,
+                                const int32_t* group_rows, const uint32_t* run_table, int32_t n_groups,
+                                int32_t r_max, int32_t n_bins,
+                                int32_t out_kind, float eps, float* out, const void* workspace,
+                                size_t workspace_bytes, void* stream);
+
 /* Host-buffer end-to-end variant of nnab_cqt1992v2_forward (pinned x_host ->
  * pinned out_host, chunks of clips streamed through the device with H2D /
  * compute / D2H overlap); device buffers come from `device_scratch`. */

@@ -239,7 +239,7 @@ class CqtLongEngine:
     with the longest-first per-K-block schedule (csrc/cqt1992.cu)."""
 
     def __init__(self, kernels, hop: int, pad_mode: str = "reflect", precision: str = "tf32", device="cuda",
-                 dense: bool = False):
+                 dense: bool = False, method: str = "schedule"):
         self.device = _require_cuda(device)
         if precision not in L.PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
@@ -247,6 +247,9 @@ class CqtLongEngine:
         k = np.asarray(kernels)
         self.n_bins, self.width = int(k.shape[0]), int(k.shape[1])
         self.hop, self.pad_mode = int(hop), pad_mode
+        if method not in ("egemm", "schedule"):
+            raise ValueError(f"method must be 'egemm' or 'schedule', got {method!r}")
+        self.method = "schedule" if dense else method
         if self.hop < 1:
             raise ValueError(f"stride must be >= 1, got {hop}")
         self._ws = _Workspace()
@@ -277,6 +280,27 @@ class CqtLongEngine:
         L.check(lib.nnab_pack_cqt_bank(dr.data_ptr(), di.data_ptr(), self.n_bins, self.width, self.precision,
                                        self.packed_hi.data_ptr(), L.ptr(self.packed_lo),
                                        L.stream_handle(self.device)), "pack_cqt_bank")
+        # hop-offset GEMM ("E-GEMM", csrc/cqt1992_egemm.cu): TF32, hop a multiple of 32 (hop-row frames)
+        self.egemm = None
+        if self.method == "egemm" and self.precision == L.PREC_TF32 and self.hop == 512:
+            max_groups = 64
+            ct = np.zeros(max_groups * 256, dtype=np.uint16)
+            gr = np.zeros(max_groups * 64, dtype=np.int32)
+            rt = np.zeros(max_groups * 4 * 65, dtype=np.uint32)
+            ng, rm = C.c_int32(), C.c_int32()
+            rc = lib.nnab_cqt_egemm_plan(sup.ctypes.data, self.n_bins, self.width, self.hop, max_groups, ct.ctypes.data,
+                                         gr.ctypes.data, rt.ctypes.data, C.byref(ng), C.byref(rm))
+            if rc == L.OK:
+                n = ng.value
+                col_t = torch.from_numpy(ct[: n * 256].view(np.int16).copy()).to(self.device)
+                rows_t = torch.from_numpy(gr[: n * 64].copy()).to(self.device)
+                runs_t = torch.from_numpy(rt[: n * 4 * 65].view(np.int32).copy()).to(self.device)
+                bank = torch.empty(lib.nnab_cqt_egemm_bank_bytes(n, self.hop) // 4, dtype=torch.float32,
+                                   device=self.device)
+                L.check(lib.nnab_pack_cqt_egemm(dr.data_ptr(), di.data_ptr(), self.width, self.hop, col_t.data_ptr(),
+                                                rows_t.data_ptr(), n, self.precision, bank.data_ptr(), None,
+                                                L.stream_handle(self.device)), "pack_cqt_egemm")
+                self.egemm = (bank, col_t, rows_t, runs_t, n, rm.value)
 
     def frames(self, B: int, length: int) -> L.nnab_frames:
         return frames_struct(B, length, self.width, self.hop, self.width // 2, self.pad_mode)
@@ -317,6 +341,15 @@ class CqtLongEngine:
             return out
         f = self.frames(B, length)
         ws = self._ws.buf
+        if self.egemm is not None:
+            bank, col_t, rows_t, runs_t, n, rmax = self.egemm
+            rc = lib.nnab_cqt1992v2_egemm_staged(C.byref(f), bank.data_ptr(), col_t.data_ptr(), rows_t.data_ptr(),
+                                                 runs_t.data_ptr(), n, rmax, self.n_bins, kinds[kind], float(eps),
+                                                 out.data_ptr(),
+                                                 ws.data_ptr(), ws.numel(), L.stream_handle(self.device))
+            if rc != L.ENOTSUP:
+                L.check(rc, "cqt1992v2_egemm_staged")
+                return out
         L.check(lib.nnab_cqt1992v2_forward_staged(C.byref(f), self.packed_hi.data_ptr(), L.ptr(self.packed_lo),
                                                   self.n_bins, self.schedule.data_ptr(), self.n_entries,
                                                   self.precision, kinds[kind], float(eps), out.data_ptr(),

@@ -144,3 +144,16 @@ def test_cqt2010v2_fp16_scaling_robust(cuda_dev, case):
     got = rec_engine(cfg, "tf32").forward(torch.from_numpy(x).to(cuda_dev))[0].cpu().numpy()
     assert np.isfinite(got).all()
     assert O.peak_err(got, ref) <= TOL["tf32"], O.peak_err(got, ref)
+
+
+def test_cqt1992v2_egemm_matches_schedule(golden, cuda_dev):
+    """The hop-offset GEMM (csrc/cqt1992_egemm.cu) and the per-K-block schedule
+    (csrc/cqt1992.cu) compute the same TF32 correlation in different orders."""
+    cfg = O.CqtCfg(sr=SR)
+    x = torch.from_numpy(golden["clips"]).to(cuda_dev)
+    a = long_engine(cfg, "tf32", method="egemm")
+    assert a.egemm is not None
+    b = long_engine(cfg, "tf32", method="schedule")
+    for kind in ("magnitude", "complex"):
+        ga, gb = a.forward(x, kind).cpu().numpy(), b.forward(x, kind).cpu().numpy()
+        assert O.peak_err(ga, gb) < 5e-4
