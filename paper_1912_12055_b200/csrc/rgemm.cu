@@ -212,19 +212,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int n0 = nt * kBN + c * 32;
           if (m < p.M) {
             if (n0 + 32 <= p.N && vec) {
+              // the running sum lives in C (L2): all 8 loads of the 32 columns are in
+              // flight before any add, so a drain costs one L2 round trip per 32 columns
+              float4* dst = reinterpret_cast<float4*>(crow + n0);
+              float4 cur[8];
 #pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                float4* dst = reinterpret_cast<float4*>(crow + n0 + j);
-                float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                if (!first_chunk) {
-                  const float4 c0 = *dst;
-                  o.x += c0.x;
-                  o.y += c0.y;
-                  o.z += c0.z;
-                  o.w += c0.w;
-                }
-                *dst = o;
-              }
+              for (int j = 0; j < 8; ++j) cur[j] = first_chunk ? make_float4(0.f, 0.f, 0.f, 0.f) : dst[j];
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                dst[j] = make_float4(cur[j].x + v[4 * j], cur[j].y + v[4 * j + 1], cur[j].z + v[4 * j + 2],
+                                     cur[j].w + v[4 * j + 3]);
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
