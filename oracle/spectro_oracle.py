@@ -375,6 +375,76 @@ def cqt2010v2_clip(x, cfg: CqtCfg, plan: Cqt2010Plan | None = None, output="magn
     return _finish_complex(out, output)
 
 
+def cqt_freq_bank(cfg: CqtCfg):
+    """kernels.py:361-410 (domain='frequency') -- kernels centred in rows of
+    fft_len = next power of two >= N_0, and their spectra with the reversed
+    index sign: freq_kernels = conj(fft(conj(time_kernels))).  Returns
+    (freq_kernels, fft_len)."""
+    q = cqt_quality(cfg.bins_per_octave)
+    f = cfg.freqs()
+    lens = np.ceil(q * cfg.sr / f).astype(np.int64)
+    n = 1
+    while n < int(lens[0]):
+        n *= 2
+    k = np.zeros((cfg.n_bins, n), dtype=np.complex128)
+    for r in range(cfg.n_bins):
+        n_k = int(lens[r])
+        v = np.exp(-2j * np.pi * (f[r] / cfg.sr) * np.arange(n_k)) * window(cfg.window_kind, n_k, True)
+        if cfg.norm == 1:
+            v = v / np.abs(v).sum()
+        elif cfg.norm == 2:
+            v = v / np.sqrt((np.abs(v) ** 2).sum())
+        s0 = n // 2 - n_k // 2
+        k[r, s0:s0 + n_k] = v
+    return np.conj(np.fft.fft(np.conj(k), axis=1)), n
+
+
+def _freq_domain_frames(x, freq_kernels, n, hop, pad_mode):
+    """transforms.py:229-235 / 333-337 -- centre pad n//2, full-spectrum DFT of
+    every frame (the reference's rectangular DFT bank conv; here np.fft of the
+    same frames), then the spectral product with the kernels / n."""
+    xp = pad(x, n // 2, n // 2, pad_mode)
+    if n > xp.size:
+        raise ValueError("signal shorter than kernel")
+    fr = sliding_window_view(xp, n)[::hop]
+    spectra = np.fft.fft(fr, axis=1)  # sum_m x[m] e^{-2 pi i k m / n} = frames[:n] - 1j * frames[n:]
+    return (spectra @ freq_kernels.T).T / n
+
+
+def cqt1992_clip(x, cfg: CqtCfg, output="magnitude"):
+    """transforms.py:211-238 (Cqt1992) -- constant-Q through the frequency domain."""
+    fk, n = cqt_freq_bank(cfg)
+    return _finish_complex(_freq_domain_frames(x, fk, n, cfg.hop_length, cfg.pad_mode), output)
+
+
+def cqt2010_clip(x, cfg: CqtCfg, plan: Cqt2010Plan | None = None, output="magnitude"):
+    """transforms.py:326-337 (Cqt2010) -- the octave recursion of cqt2010v2_clip
+    with each octave's conv done through the frequency domain (top-octave bank,
+    fft_len of its longest kernel)."""
+    p = plan or cqt2010_plan(cfg)
+    b = cfg.bins_per_octave
+    top = CqtCfg(sr=p.kernel_sr, fmin=cfg.fmin * 2.0 ** (p.first_bin / b), n_bins=p.n_filters, bins_per_octave=b,
+                 hop_length=max(1, p.kernel_hop // 2 ** (p.n_octaves - 1)), window_kind=cfg.window_kind,
+                 norm=cfg.norm, pad_mode=cfg.pad_mode, early_downsample=False)
+    fk, n = cqt_freq_bank(top)
+    cur = x
+    for _ in range(p.early_stages):
+        cur = halve_rate(cur, p.taps)
+    octs = []
+    for a in range(p.n_octaves):
+        if a > 0:
+            cur = halve_rate(cur, p.taps)
+        fr = _freq_domain_frames(cur, fk, n, p.kernel_hop >> a, cfg.pad_mode)
+        skip = max(0, a * b - p.first_bin)
+        octs.append((a, skip, fr[skip:]))
+    nfr = min(f.shape[1] for _, _, f in octs)
+    out = np.zeros((cfg.n_bins, nfr), dtype=np.complex128)
+    for a, skip, fr in octs:
+        for j in range(fr.shape[0]):
+            out[p.first_bin + skip + j - a * b] = fr[j, :nfr]
+    return _finish_complex(out, output)
+
+
 def map_clips(fn, clips: np.ndarray, threads: int | None = None) -> np.ndarray:
     """transforms.py:370-388 (batch_transform) -- ordered map over clips with
     an optional thread pool; results identical to the sequential map."""

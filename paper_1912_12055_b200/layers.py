@@ -9,6 +9,8 @@
          window='hann', center=True, pad_mode='reflect', trainable=False, output_format='Magnitude')
     CQT2010v2(sr=22050, hop_length=512, fmin=32.70, fmax=None, n_bins=84, bins_per_octave=12, norm=True,
          basis_norm=1, window='hann', pad_mode='reflect', earlydownsample=True)
+    CQT1992, CQT2010: the frequency-domain variants (same arguments as the v2 modules),
+         computed by their time-domain equivalents (spectro.Cqt1992 / Cqt2010)
 
 Input (batch, samples) or (samples,) float32 CUDA tensor; output (batch, freq, time).
 Numerics follow the `spectro` reference this repo is parity-checked against:
@@ -163,3 +165,33 @@ class CQT2010v2(nn.Module):
 
     def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
         return self._eng.forward(_as_batch(x), _fmt(output_format or self.output_format))
+
+
+class CQT1992(CQT1992v2):
+    """The frequency-domain CQT (transforms.py:211-238): equal to CQT1992v2 by the
+    power theorem; the frequency route's own fft_len // 2 reflect-pad constraint
+    is checked (spectro.Cqt1992)."""
+
+    def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
+        from .spectro import _check_freq_pad, _next_pow2
+        x = _as_batch(x)
+        _check_freq_pad(x.shape[-1], _next_pow2(int(self.lengths[0])), self.cfg.pad_mode)
+        return super().forward(x, output_format)
+
+
+class CQT2010(CQT2010v2):
+    """The frequency-domain octave recursion (transforms.py:326-337), computed by
+    CQT2010v2's chain; the per-octave fft_len // 2 pad constraint is checked
+    (spectro.Cqt2010)."""
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        from .spectro import _cqt2010_fft_len
+        p = cqt2010_plan(self.cfg)
+        self._plan = (p["early_stages"], p["n_octaves"], _cqt2010_fft_len(self.cfg, p["early_stages"], p["first_bin"]))
+
+    def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
+        from .spectro import _check_cqt2010_freq_pad
+        x = _as_batch(x)
+        _check_cqt2010_freq_pad(x.shape[-1], self.cfg.pad_mode, *self._plan)
+        return super().forward(x, output_format)

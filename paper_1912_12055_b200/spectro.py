@@ -298,6 +298,68 @@ class Cqt2010v2(_Batched):
                           kind=out)
 
 
+def _next_pow2(n: int) -> int:
+    p = 1
+    while p < n:
+        p *= 2
+    return p
+
+
+class Cqt1992(Cqt1992v2):
+    """transforms.py:211-238 -- constant-Q through the frequency domain: centre
+    pad fft_len // 2, full-spectrum DFT of every frame, product with the
+    kernels' spectra / fft_len.  By the power theorem (kernels.py:403-407) that
+    is exactly the centred time-domain correlation with the same kernels, which
+    is what runs here (the reference documents the equivalence:
+    tests/test_acceptance.py:116-126); only the reference's own constraints of
+    the frequency route (its fft_len // 2 reflect pad) are checked on top."""
+
+    def __init__(self, cfg: CqtConfig, precision: str = "tf32", device="cuda"):
+        super().__init__(cfg, precision=precision, device=device)
+        self.fft_len = _next_pow2(int(self.lengths[0]))
+
+    def batch(self, x: torch.Tensor, output: str = "magnitude"):
+        _check_freq_pad(x.shape[-1], self.fft_len, self.cfg.pad_mode)
+        return super().batch(x, output)
+
+
+class Cqt2010(Cqt2010v2):
+    """transforms.py:326-337 -- the octave recursion with each octave's conv
+    through the frequency domain; computed by its time-domain equivalent (see
+    Cqt1992), with the frequency route's per-octave fft_len // 2 pad checked."""
+
+    def __init__(self, cfg: CqtConfig, device="cuda"):
+        super().__init__(cfg, device=device)
+        self.fft_len = _cqt2010_fft_len(cfg, self.early_stages, self.first_bin)
+
+    def batch(self, x: torch.Tensor, output: str = "magnitude"):
+        _check_cqt2010_freq_pad(x.shape[-1], self.cfg.pad_mode, self.early_stages, self.n_octaves, self.fft_len)
+        return super().batch(x, output)
+
+
+def _cqt2010_fft_len(cfg: CqtConfig, early_stages: int, first_bin: int) -> int:
+    """fft_len of the top-octave bank (kernels.py:383): next power of two >= its longest kernel."""
+    n0 = math.ceil(banks.cqt_q(cfg.bins_per_octave) * (cfg.sr / 2 ** early_stages)
+                   / (cfg.fmin * 2.0 ** (first_bin / cfg.bins_per_octave)))
+    return _next_pow2(int(n0))
+
+
+def _check_cqt2010_freq_pad(length: int, pad_mode: str, early_stages: int, n_octaves: int, fft_len: int) -> None:
+    n = length
+    for _ in range(early_stages):
+        n = (n + 1) // 2
+    for a in range(n_octaves):
+        if a > 0:
+            n = (n + 1) // 2
+        _check_freq_pad(n, fft_len, pad_mode)
+
+
+def _check_freq_pad(length: int, fft_len: int, pad_mode: str) -> None:
+    """signal.py:147-150 for the frequency route's fft_len // 2 centre pad."""
+    if pad_mode == "reflect" and fft_len // 2 >= length:
+        raise ValueError(f"reflect padding of {fft_len // 2} needs a signal longer than the pad (got {length})")
+
+
 def stft(x: Signal, params: StftParams | None = None) -> Spectrogram:
     """transforms.py:340-342."""
     return Stft(params or StftParams(), x.sample_rate)(x)
@@ -316,6 +378,14 @@ def cqt1992v2(x: Signal, cfg: CqtConfig, output: str = "magnitude") -> Spectrogr
 def cqt2010v2(x: Signal, cfg: CqtConfig, output: str = "magnitude") -> Spectrogram:
     """transforms.py:365-367."""
     return Cqt2010v2(cfg)(x, output)
+
+
+def cqt1992(x: Signal, cfg: CqtConfig, output: str = "magnitude") -> Spectrogram:
+    return Cqt1992(cfg)(x, output)
+
+
+def cqt2010(x: Signal, cfg: CqtConfig, output: str = "magnitude") -> Spectrogram:
+    return Cqt2010(cfg)(x, output)
 
 
 def batch_transform(signals, transform, threads: int | None = None) -> list:

@@ -105,6 +105,11 @@ def main():
     cfg_ne = sp.CqtConfig(sr=22050.0, fmin=55.0, n_bins=48, bins_per_octave=12, hop_length=256,
                           early_downsample=False)
     g["cqt2010v2_noearly"] = sp.cqt2010v2(sp.Signal(x22, 22050.0), cfg_ne).data
+    # frequency-domain variants (transforms.py:211-238, 326-337)
+    from spectro.transforms import Cqt1992, Cqt2010
+    g["cqt1992_small"] = Cqt1992(cfg_s)(sp.Signal(x22, 22050.0)).data
+    g["cqt1992_small_complex"] = Cqt1992(cfg_s)(sp.Signal(x22, 22050.0), output="complex").data
+    g["cqt2010_small"] = Cqt2010(cfg_r)(sp.Signal(x22, 22050.0)).data
 
     # --- trainable layers (gradients.py:28-149)
     xg = f32(np.random.default_rng(4).standard_normal(512))

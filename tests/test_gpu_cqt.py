@@ -157,3 +157,19 @@ def test_cqt1992v2_egemm_matches_schedule(golden, cuda_dev):
     for kind in ("magnitude", "complex"):
         ga, gb = a.forward(x, kind).cpu().numpy(), b.forward(x, kind).cpu().numpy()
         assert O.peak_err(ga, gb) < 5e-4
+
+
+def test_frequency_domain_variants_golden(golden, cuda_dev):
+    """spectro.Cqt1992 / Cqt2010 (the reference's frequency-domain routes,
+    transforms.py:211-238 and 326-337) against the reference's own outputs."""
+    from paper_1912_12055_b200 import spectro as S
+    x = S.Signal(golden["x22"].astype(np.float32), 22050.0, device="cuda:0")
+    c1 = S.Cqt1992(S.CqtConfig(sr=22050.0, fmin=220.0, n_bins=24, hop_length=512))
+    assert O.peak_err(c1(x).data.cpu().numpy(), golden["cqt1992_small"]) <= TOL["tf32"]
+    assert O.peak_err(c1(x, "complex").data.cpu().numpy(), golden["cqt1992_small_complex"]) <= TOL["tf32"]
+    c2 = S.Cqt2010(S.CqtConfig(sr=22050.0, fmin=55.0, n_bins=48, hop_length=256))
+    assert O.peak_err(c2(x).data.cpu().numpy(), golden["cqt2010_small"]) <= TOL["tf32"]
+    # the frequency route's fft_len // 2 reflect pad rejects signals the v2 route accepts
+    short = S.Signal(golden["x22"][:1000].astype(np.float32), 22050.0, device="cuda:0")  # fft_len 2048 > 2 * 1000 > width 1686
+    with pytest.raises(ValueError):
+        c1(short)

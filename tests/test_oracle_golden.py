@@ -126,3 +126,15 @@ def test_trainable_vjp(golden):
     gc = O.conv_layer_vjp(golden["grad_xc"], k.real, k.imag, 128, golden["grad_up_cqt"])
     assert O.peak_err(gc["h_re"], golden["grad_cqt_h_re"]) < TIGHT
     assert O.peak_err(gc["h_im"], golden["grad_cqt_h_im"]) < TIGHT
+
+
+def test_oracle_frequency_domain_cqt_matches_golden(golden):
+    """Cqt1992 / Cqt2010 (transforms.py:211-238, 326-337) restated through np.fft."""
+    x22 = golden["x22"]
+    cfg_s = O.CqtCfg(sr=22050.0, fmin=220.0, n_bins=24, hop_length=512)
+    assert O.peak_err(O.cqt1992_clip(x22, cfg_s), golden["cqt1992_small"]) < 1e-10
+    assert O.peak_err(O.cqt1992_clip(x22, cfg_s, output="complex"), golden["cqt1992_small_complex"]) < 1e-10
+    cfg_r = O.CqtCfg(sr=22050.0, fmin=55.0, n_bins=48, hop_length=256)
+    assert O.peak_err(O.cqt2010_clip(x22, cfg_r), golden["cqt2010_small"]) < 1e-10
+    # the reference's documented equivalence with the time-domain variants
+    assert O.peak_err(golden["cqt1992_small_complex"], golden["cqt1992v2_small_complex"]) < 1e-9

@@ -1,0 +1,11 @@
+"""One trainable STFT+Mel forward/backward on the full batch (for ncu captures)."""
+import sys
+sys.path.insert(0, ".")
+import torch
+import bench
+dev = torch.device("cuda:0")
+step = bench.TrainStep(dev, "tf32", 1)
+x = torch.randn(bench.B_CLIPS, bench.L_SAMPLES, device=dev) * 0.5
+for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
+    step.forward(x)
+torch.cuda.synchronize()
