@@ -258,6 +258,15 @@ int nnab_cqt2010v2_forward_host(const float* x_host, int64_t B, int64_t L, const
                                 int32_t precision, float* out_host, int64_t chunk_clips, void* device_scratch,
                                 size_t scratch_bytes, void* stream);
 
+/* ------------------------------------------------------- file formats (csrc/io.cu)
+ * WAV ingestion (wavio.py:19-68): the data chunk's bytes on the device ->
+ * mono float32 (PCM16 / 32768, channel mean); equals float32(reference).
+ * format 1 = PCM 16-bit, 3 = IEEE float 32-bit. */
+int nnab_decode_wav(const void* payload, int64_t n_frames, int32_t channels, int32_t format, float* out,
+                    void* stream);
+/* SpecFile payload (specfile.py:26-43): float32 cells -> float64 on the device. */
+int nnab_widen_f64(const float* src, int64_t n, double* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

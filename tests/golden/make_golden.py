@@ -111,6 +111,56 @@ def main():
     g["cqt1992_small_complex"] = Cqt1992(cfg_s)(sp.Signal(x22, 22050.0), output="complex").data
     g["cqt2010_small"] = Cqt2010(cfg_r)(sp.Signal(x22, 22050.0)).data
 
+    # --- file formats either side of the path: WAV bytes the
+    # reference reads, and SpecFile bytes it writes
+    import struct
+    import tempfile
+    from spectro.specfile import write_spec
+    from spectro.wavio import read_wav, write_wav
+    from spectro.transforms import Spectrogram
+
+    def crafted_wav(samples_frames, fmt_tag, bits, sr, extra_chunk=True):
+        ch = samples_frames.shape[1]
+        if fmt_tag == 1:
+            payload = samples_frames.astype("<i2").tobytes()
+        else:
+            payload = samples_frames.astype("<f4").tobytes()
+        block = ch * bits // 8
+        fmt = struct.pack("<HHIIHH", fmt_tag, ch, sr, sr * block, block, bits)
+        body = b"WAVE" + b"fmt " + struct.pack("<I", len(fmt)) + fmt
+        if extra_chunk:  # an odd-sized unknown chunk the reader must skip (word alignment)
+            body += b"LIST" + struct.pack("<I", 5) + b"abcde" + b"\x00"
+        body += b"data" + struct.pack("<I", len(payload)) + payload + (b"\x00" if len(payload) % 2 else b"")
+        return b"RIFF" + struct.pack("<I", len(body)) + body
+
+    rw = np.random.default_rng(8)
+    wavs = {
+        "wav_pcm16_stereo": crafted_wav(rw.integers(-32768, 32768, size=(3001, 2)), 1, 16, 16000),
+        "wav_pcm16_3ch": crafted_wav(rw.integers(-32768, 32768, size=(2000, 3)), 1, 16, 22050),
+        "wav_f32_stereo": crafted_wav(rw.standard_normal((2500, 2)).astype(np.float32) * 0.3, 3, 32, 44100),
+    }
+    with tempfile.TemporaryDirectory() as td:
+        for enc in ("pcm16", "float32"):
+            pth = os.path.join(td, enc + ".wav")
+            write_wav(pth, sp.Signal(f32(rw.standard_normal(1999) * 0.2), 8000.0), encoding=enc)
+            wavs["wav_" + enc + "_mono"] = open(pth, "rb").read()
+        for name, blob in wavs.items():
+            pth = os.path.join(td, name + ".wav")
+            open(pth, "wb").write(blob)
+            sig = read_wav(pth)
+            g[name + "_bytes"] = np.frombuffer(blob, dtype=np.uint8).copy()
+            g[name + "_decoded"] = np.asarray(sig.samples)
+            g[name + "_sr"] = np.array(sig.sample_rate)
+        spec_c = Spectrogram(data=g["stft_small_complex"].astype(np.complex64).astype(np.complex128),
+                             bin_freqs_hz=None, hop=64, sample_rate=8000.0, kind="complex")
+        spec_m = Spectrogram(data=np.abs(g["stft_small_complex"]).astype(np.float32).astype(np.float64),
+                             bin_freqs_hz=None, hop=64, sample_rate=8000.0, kind="magnitude")
+        for name, spec in (("specfile_complex", spec_c), ("specfile_mag", spec_m)):
+            for dt in ("f32", "f64"):
+                pth = os.path.join(td, name + dt + ".nasp")
+                write_spec(pth, spec, dtype=dt)
+                g[name + "_" + dt] = np.frombuffer(open(pth, "rb").read(), dtype=np.uint8).copy()
+
     # --- trainable layers (gradients.py:28-149)
     xg = f32(np.random.default_rng(4).standard_normal(512))
     g["grad_x"] = xg

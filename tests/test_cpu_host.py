@@ -141,3 +141,24 @@ def test_shard_range():
     assert all(sizes[i][1] == sizes[i + 1][0] for i in range(7))
     with pytest.raises(ValueError):
         shard_range(10, 3, 3)
+
+
+def test_wav_header_errors(tmp_path):
+    """wavio.py:26-63 error behaviour, mirrored by the host-side parser (no GPU)."""
+    import struct
+    from paper_1912_12055_b200 import fileio
+    bad = tmp_path / "bad.wav"
+    bad.write_bytes(b"RIFX0000WAVE")
+    with pytest.raises(fileio.CorruptFileError):
+        fileio._parse_wav(str(bad))
+    fmt = struct.pack("<HHIIHH", 1, 1, 8000, 24000, 3, 24)  # 24-bit PCM
+    body = b"WAVE" + b"fmt " + struct.pack("<I", 16) + fmt + b"data" + struct.pack("<I", 6) + b"\x00" * 6
+    w24 = tmp_path / "w24.wav"
+    w24.write_bytes(b"RIFF" + struct.pack("<I", len(body)) + body)
+    with pytest.raises(fileio.UnsupportedFormatError):
+        fileio._parse_wav(str(w24))
+    trunc = tmp_path / "t.wav"
+    trunc.write_bytes(b"RIFF" + struct.pack("<I", 100) + b"WAVE" + b"data" + struct.pack("<I", 50) + b"\x00" * 10)
+    with pytest.raises(fileio.CorruptFileError):
+        fileio._parse_wav(str(trunc))
+    assert issubclass(fileio.CorruptFileError, ValueError) and issubclass(fileio.UnsupportedFormatError, ValueError)
