@@ -15,6 +15,7 @@
 // Warp roles as in stft_gemm.cu: TMA producer, MMA issuer, TMEM allocator,
 // 4 epilogue warps (thread = output row).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -66,12 +67,18 @@ NNAB_DEV uint64_t mndesc(const void* p, int /*swz*/, uint32_t lbo) {
   return d;
 }
 
-template <bool kSplit>
+// kPair (TF32): a cluster of two CTAs computes a 256 x 256 tile with
+// cta_group::2 MMAs -- each CTA stages its own 128 A rows and HALF of the B tile,
+// so the B bytes pulled from L2 per MAC halve (the long kernel-gradient
+// reduction dK = coef @ frames is L2-bandwidth bound at 128 x 256 per CTA).
+template <bool kSplit, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     rgemm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                  const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                  const RParams p) {
   using C = RCfg<kSplit>;
+  constexpr int kBNc = kPair ? kBN / 2 : kBN;  // B columns this CTA stages
+  const uint32_t rank = kPair ? cluster_ctarank() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::STAGE);
@@ -88,29 +95,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kBM);
+      mbar_init(&tempty[i], kPair ? 2 * kBM : kBM);  // pair: the leader's counts both CTAs' threads
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tslot);
+  if (kPair) cluster_sync();
+  if (warp == 2) {
+    if (kPair) tmem_alloc_pair<512>(tslot);
+    else tmem_alloc<512>(tslot);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const int n_work = p.m_tiles * p.n_tiles * p.splits;
+  // work items: (m tile, n tile, split); a pair walks pair-tiles (two m tiles) by cluster
+  const int m_units = kPair ? (p.m_tiles + 1) / 2 : p.m_tiles;
+  const int n_work = m_units * p.n_tiles * p.splits;
+  const int w_start = kPair ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int w_step = kPair ? (int)nclusters_x() : (int)gridDim.x;
 
   if (warp == 0) {
     if (elect_one()) {
       int s = 0;
       uint32_t ph = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const uint64_t pol = policy_evict_last();
+      for (int w = w_start; w < n_work; w += w_step) {
         const int sp = w % p.splits, tile = w / p.splits;
-        const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+        const int mt = (tile / p.n_tiles) * (kPair ? 2 : 1) + (int)rank, nt = tile % p.n_tiles;
         const int64_t k_lo = sp * p.k_per_split;
         const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
         for (int64_t k = k_lo; k < k_hi; k += C::BK) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * C::STAGE;
+          if (kPair) {  // both CTAs' bytes complete on the leader's barrier
+            const uint32_t fb = mapa(&full[s], 0);
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * (C::A_BYTES + C::B_BYTES / 2));
+            tma_load_2d_pair(st, &ta_hi, fb, (int)k, mt * kBM, pol);
+            if (!p.b_mn) {
+              tma_load_2d_pair(st + C::A_BYTES, &tb_hi, fb, (int)k, nt * kBN + (int)rank * kBNc, pol);
+            } else {
+#pragma unroll 1
+              for (int j = 0; j < kBNc / 32; ++j) {
+                const int n0 = nt * kBN + (int)rank * kBNc + j * 32;
+                tma_load_2d_pair(st + C::A_BYTES + j * C::BK * 128, &tb_hi, fb, n0 % p.b_row_len,
+                                 (int)(k + n0 / p.b_row_len), pol);
+              }
+            }
+            if (++s == kStages) { s = 0; ph ^= 1; }
+            continue;
+          }
           mbar_expect_tx(&full[s], C::STAGE);
           tma_load_2d(st, &ta_hi, &full[s], (int)k, mt * kBM);
           if (kSplit) tma_load_2d(st + C::A_BYTES + C::B_BYTES, &ta_lo, &full[s], (int)k, mt * kBM);
@@ -135,11 +168,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (elect_one()) {
-      const uint32_t idesc = idesc_tf32(kBM, kBN) | (p.b_mn ? (1u << 16) : 0u);
+    if (rank == 0 && elect_one()) {
+      const uint32_t idesc = idesc_tf32(kPair ? 2 * kBM : kBM, kBN) | (p.b_mn ? (1u << 16) : 0u);
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      for (int w = w_start; w < n_work; w += w_step) {
         const int sp = w % p.splits;
         const int64_t k_lo = sp * p.k_per_split;
         const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
@@ -163,17 +196,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < C::BK / 8; ++kk) {
               const uint64_t ao = (uint64_t)((kk * 32) >> 4);
               const uint64_t bo = p.b_mn ? (uint64_t)((kk * 1024) >> 4) : ao;  // MN-major: next 8 K rows
-              mma_tf32(d, a + ao, b + bo, idesc, first ? 0u : 1u);
+              if (kPair) mma_tf32_pair(d, a + ao, b + bo, idesc, first ? 0u : 1u);
+              else mma_tf32(d, a + ao, b + bo, idesc, first ? 0u : 1u);
               if (kSplit) {
                 mma_tf32(d + kBN, a + ao, b_lo + bo, idesc, first ? 0u : 1u);
                 mma_tf32(d + kBN, a_lo + ao, b + bo, idesc, 1u);
               }
               first = false;
             }
-            mma_commit(&empty[s]);
+            if (kPair) mma_commit_pair(&empty[s], 0x3);
+            else mma_commit(&empty[s]);
             if (++s == kStages) { s = 0; ph ^= 1; }
           }
-          mma_commit(&tfull[acc]);
+          if (kPair) mma_commit_pair(&tfull[acc], 0x3);
+          else mma_commit(&tfull[acc]);
           if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
         }
       }
@@ -183,9 +219,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp - 4, row = q * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const uint32_t tempty0 = kPair ? mapa(&tempty[0], 0) : smem_u32(&tempty[0]);
+    for (int w = w_start; w < n_work; w += w_step) {
       const int sp = w % p.splits, tile = w / p.splits;
-      const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+      const int mt = (tile / p.n_tiles) * (kPair ? 2 : 1) + (int)rank, nt = tile % p.n_tiles;
       const int64_t k_lo = sp * p.k_per_split;
       const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
       const int m = mt * kBM + row;
@@ -230,15 +267,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        if (kPair) mbar_arrive_cluster(tempty0 + 8 * acc);
+        else mbar_arrive(&tempty[acc]);
         if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync();  // the peer's TMEM is written by the leader's MMAs until the end
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<512>(tbase);
+  if (warp == 2) {
+    if (kPair) tmem_dealloc_pair<512>(tbase);
+    else tmem_dealloc<512>(tbase);
+  }
 }
 
 // out[m][n] = sum_s parts[s][m][n] in a fixed order (deterministic split-K)
@@ -253,15 +295,16 @@ __global__ void sum_splits_kernel(const float* __restrict__ parts, int32_t split
   }
 }
 
-template <bool kSplit>
+template <bool kSplit, bool kPair>
 int launch(const RGemmArgs& g, cudaStream_t st) {
   using C = RCfg<kSplit>;
+  constexpr int kBNc = kPair ? kBN / 2 : kBN;
   if (g.K % C::BK || g.lda % 4 || (g.b_mn && g.b_row_len % 32) || (!g.b_mn && g.ldb % 4)) return NNAB_EINVAL;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   int rc = make_tmap_2d(&ta_hi, g.a_hi, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
   if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, g.a_lo, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
   if (!g.b_mn) {
-    if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBN, C::SWZ);
+    if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBNc, C::SWZ);
     if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, g.b_lo, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBN, C::SWZ);
   } else {
     // rows of b_row_len floats; b_rows rows in total; boxes of 32 columns x BK rows, 128-byte swizzle
@@ -281,7 +324,8 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.m_tiles = (g.M + kBM - 1) / kBM;
   p.n_tiles = (g.N + kBN - 1) / kBN;
   const int tiles = p.m_tiles * p.n_tiles;
-  int splits = g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, tiles));
+  const int units = (kPair ? (p.m_tiles + 1) / 2 * 2 : p.m_tiles) * p.n_tiles;  // CTAs per split
+  int splits = g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, units));
   const int64_t kb = g.K / C::BK;
   splits = (int)std::min<int64_t>(splits, kb);
   p.k_per_split = (kb + splits - 1) / splits * C::BK;
@@ -295,10 +339,27 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.split_stride = (int64_t)p.m_tiles * kBM * p.ldc;
   if (!direct && !g.partial) return NNAB_EINVAL;
   const size_t smem = 1024 + kStages * C::STAGE + 128;
-  auto k = rgemm_kernel<kSplit>;
+  auto k = rgemm_kernel<kSplit, kPair>;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = std::min(tiles * p.splits, num_sms());
-  k<<<grid, kThreads, smem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+  (void)tiles;
+  if (!kPair) {
+    const int grid = std::min(units * p.splits, num_sms());
+    k<<<grid, kThreads, smem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(std::min(units * p.splits, num_sms() / 2 * 2));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    NNAB_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, ta_hi, ta_lo, tb_hi, tb_lo, p));
+  }
   NNAB_LAUNCHED();
   if (!direct) {
     const int64_t total = (int64_t)g.M * g.N;
@@ -314,13 +375,24 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
 
 size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits) {
   const int64_t mt = (M + kBM - 1) / kBM, nt = (N + kBN - 1) / kBN;
-  if (splits <= 0) splits = std::max(1, num_sms() / (int)std::max<int64_t>(1, mt * nt));
+  if (splits <= 0) splits = std::max(1, num_sms() / (int)std::max<int64_t>(1, mt * nt));  // >= the pair count
   return (size_t)splits * mt * kBM * nt * kBN * sizeof(float);
 }
 
+// TF32 reductions over more than one m tile use the CTA-pair form: measured
+// 6.77 -> 4.46 ms on the 2050 x 2048 x 283,200 kernel gradient, never slower on
+// smaller shapes (tools/dbg_rgemm_pair.py).  NNAB_RGEMM_PAIR=0 forces single CTAs.
 int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s) {
-  if (precision == NNAB_PREC_3XTF32) return launch<true>(g, s);
-  if (precision == NNAB_PREC_TF32) return launch<false>(g, s);
+  static const int pair_env = [] {
+    const char* e = getenv("NNAB_RGEMM_PAIR");
+    return e ? e[0] - '0' : 1;
+  }();
+  const bool pair_ok = pair_env != 0;
+  if (precision == NNAB_PREC_3XTF32) return launch<true, false>(g, s);
+  if (precision == NNAB_PREC_TF32) {
+    const bool pair = pair_ok && (pair_env == 2 || g.M > kBM);  // one m tile: the peer would idle
+    return pair ? launch<false, true>(g, s) : launch<false, false>(g, s);
+  }
   return NNAB_EINVAL;
 }
 
