@@ -153,6 +153,14 @@ int nnab_from_slots(const float* src, int64_t B, int32_t rows, int32_t T, int32_
 int nnab_dft_coef(const float* ds_slots, const float* g_bft, const float* re_s, const float* im_s, int32_t F,
                   int64_t B, int32_t T, int32_t R, int64_t ld, float eps, int32_t precision, float* coef_hi,
                   float* coef_lo, void* stream);
+/* Joint mel + trainable STFT backward: dS = W^T g computed on the tensor cores
+ * with the coef step (gradients.py:125-128) in the GEMM epilogue, so dS never
+ * reaches HBM.  wt = W^T zero-padded to [F][kp] (kp = n_mels rounded up to 32,
+ * <= 1024), gs = upstream grad in slot layout [n_mels][ld]; writes coef [2F][ld]
+ * like nnab_dft_coef(ds_slots = W^T g). */
+int nnab_mel_dft_coef(int32_t F, int64_t ld, int32_t kp, const float* wt_hi, const float* wt_lo, const float* gs_hi,
+                      const float* gs_lo, int32_t n_mels, const float* re_s, const float* im_s, float eps,
+                      int32_t precision, float* coef_hi, float* coef_lo, void* stream);
 /* dst[c][r] = src[r][c] zero-padded to ld rows, TF32 hi (+ lo) */
 int nnab_transpose_pad(const float* src, int32_t rows, int32_t cols, int32_t ld, int32_t precision, float* hi,
                        float* lo, void* stream);

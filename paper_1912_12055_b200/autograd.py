@@ -142,15 +142,22 @@ class DftLayerOp:
                 wt_lo = _f32(F, kp, self.device) if self.split else None
                 L.check(lib.nnab_transpose_pad(mel_w.detach().float().contiguous().data_ptr(), nm, F, kp, self.prec,
                                                wt_hi.data_ptr(), L.ptr(wt_lo), stream), "transpose_pad")
-                ds = _f32(F, ld, self.device)
-                self._rgemm(F, ld, kp, (wt_hi, wt_lo), kp, gsp, ld, 1, ld, nm, ds, ld)
+                # coef = (dS*re/S, dS*im/S) straight from the dS GEMM's epilogue
+                coef_hi = _f32(2 * F, ld, self.device)
+                coef_lo = _f32(2 * F, ld, self.device) if self.split else None
+                L.check(lib.nnab_mel_dft_coef(F, ld, kp, wt_hi.data_ptr(), L.ptr(wt_lo), gsp[0].data_ptr(),
+                                              L.ptr(gsp[1]), nm, saved["re"].data_ptr(), saved["im"].data_ptr(),
+                                              self.eps, self.prec, coef_hi.data_ptr(), L.ptr(coef_lo), stream),
+                        "mel_dft_coef")
+                ds = True
         if not (need_bank or need_x):
             return grads
-        coef_hi = _f32(2 * F, ld, self.device)
-        coef_lo = _f32(2 * F, ld, self.device) if self.split else None
-        L.check(lib.nnab_dft_coef(L.ptr(ds), None if ds is not None else g.data_ptr(), saved["re"].data_ptr(),
-                                  saved["im"].data_ptr(), F, B, T, R, ld, self.eps, self.prec, coef_hi.data_ptr(),
-                                  L.ptr(coef_lo), stream), "dft_coef")
+        if ds is None:
+            coef_hi = _f32(2 * F, ld, self.device)
+            coef_lo = _f32(2 * F, ld, self.device) if self.split else None
+            L.check(lib.nnab_dft_coef(None, g.data_ptr(), saved["re"].data_ptr(), saved["im"].data_ptr(), F, B, T,
+                                      R, ld, self.eps, self.prec, coef_hi.data_ptr(), L.ptr(coef_lo), stream),
+                    "dft_coef")
         ws = saved["ws"]
         if need_bank:
             dk = _f32(2 * F, n_fft, self.device)

@@ -86,6 +86,12 @@ struct RGemmArgs {
   int32_t splits = 0;                       // 0 = auto
   float* partial = nullptr;                 // split-K scratch (rgemm_partial_bytes)
   float alpha = 1.f;
+  // coef epilogue (dS GEMM of the joint mel + STFT layer): instead of C = dS,
+  // write coef rows f: dS*re/S and f + M: dS*im/S (tf32 hi [/lo]) at
+  // coef[(f or f+M) * ldc + slot]; re/im are [M][ldc] (gradients.py:127-128)
+  const float *coef_re = nullptr, *coef_im = nullptr;
+  float* coef_lo = nullptr;
+  float coef_eps = 0.f;
 };
 size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits);
 // fused tensor-core CQT2010v2 (cqt2010_tc.cu); NNAB_ENOTSUP outside its envelope

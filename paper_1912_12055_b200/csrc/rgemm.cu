@@ -24,6 +24,7 @@ namespace nnab {
 namespace {
 
 constexpr int kBM = 128, kBN = 256, kThreads = 256, kStages = 4;
+constexpr int kStg = 36;  // epilogue transpose row stride (floats)
 
 template <bool kSplit>
 struct RCfg {
@@ -45,7 +46,25 @@ struct RParams {
   int32_t b_mn, b_row_len;
   float* C;             // [splits][M][ldc]
   int64_t ldc, split_stride;
+  const float *re, *im;  // coef epilogue (RGemmArgs::coef_re): C is coef_hi
+  float* c_lo;
+  float eps;
 };
+
+NNAB_DEV float4 tf32_hi4(float4 a) { return make_float4(tf32_rne(a.x), tf32_rne(a.y), tf32_rne(a.z), tf32_rne(a.w)); }
+NNAB_DEV float4 tf32_lo4(float4 a) {
+  return make_float4(tf32_rne(a.x - tf32_rne(a.x)), tf32_rne(a.y - tf32_rne(a.y)), tf32_rne(a.z - tf32_rne(a.z)),
+                     tf32_rne(a.w - tf32_rne(a.w)));
+}
+// coef pair (gradients.py:127-128), same arithmetic as coef_kernel: MUFU
+// rsqrt (rel. error < 2^-22, far below the TF32 rounding of the result) instead
+// of IEEE sqrt + two divisions -- the epilogue's 4 warps are issue-bound on those
+NNAB_DEV void coef_store(float d, float r, float i, float eps, float& cr, float& ci) {
+  const float inv = rsqrtf(fmaf(r, r, i * i) + eps);
+  const float di = d * inv;
+  cr = di * r;
+  ci = di * i;
+}
 
 NNAB_DEV uint64_t kdesc(const void* p, int swz) {
   uint64_t d = (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
@@ -216,18 +235,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp >= 4) {
-    const uint32_t q = warp - 4, row = q * 32 + lane;
+    // Epilogue: TMEM row = thread, so each 32-column chunk goes through a
+    // per-warp shared-memory transpose (32 rows x 36-float stride, conflict-free
+    // for float4) and leaves as float4 runs of 8 lanes per row: every global
+    // access is a full 128-byte line instead of 32 rows x 16 B.
+    const uint32_t q = warp - 4;
+    float* stg = reinterpret_cast<float*>(smem + kStages * C::STAGE + 128) + q * 32 * kStg;
+    const int sr = (int)(lane >> 3), sc = (int)(lane & 7) * 4;  // this lane's (row in 4, float4 column)
     int acc = 0;
     uint32_t aph = 0;
     const uint32_t tempty0 = kPair ? mapa(&tempty[0], 0) : smem_u32(&tempty[0]);
+    const bool vec = (p.ldc % 4) == 0;
     for (int w = w_start; w < n_work; w += w_step) {
       const int sp = w % p.splits, tile = w / p.splits;
       const int mt = (tile / p.n_tiles) * (kPair ? 2 : 1) + (int)rank, nt = tile % p.n_tiles;
       const int64_t k_lo = sp * p.k_per_split;
       const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
-      const int m = mt * kBM + row;
-      float* crow = p.C + sp * p.split_stride + (int64_t)m * p.ldc;
-      const bool vec = (p.ldc % 4) == 0;
+      const int m_base = mt * kBM + (int)q * 32;
+      float* cbase = p.C + sp * p.split_stride;
       for (int64_t kc = k_lo; kc < k_hi; kc += p.k_chunk) {
         const bool first_chunk = kc == k_lo;  // later chunks add into C in fixed order: deterministic
         mbar_wait(&tfull[acc], aph);
@@ -246,23 +271,86 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             tmem_ld_wait();
           }
-          const int n0 = nt * kBN + c * 32;
-          if (m < p.M) {
-            if (n0 + 32 <= p.N && vec) {
-              // the running sum lives in C (L2): all 8 loads of the 32 columns are in
-              // flight before any add, so a drain costs one L2 round trip per 32 columns
-              float4* dst = reinterpret_cast<float4*>(crow + n0);
-              float4 cur[8];
+          __syncwarp();  // the previous chunk's reads of stg are done
 #pragma unroll
-              for (int j = 0; j < 8; ++j) cur[j] = first_chunk ? make_float4(0.f, 0.f, 0.f, 0.f) : dst[j];
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(stg + lane * kStg + 4 * j) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          __syncwarp();
+          const int n = nt * kBN + c * 32 + sc;
+          if (n >= p.N || m_base >= p.M) continue;
+          const bool full4 = vec && n + 4 <= p.N;
+          float4 d[8];
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                dst[j] = make_float4(cur[j].x + v[4 * j], cur[j].y + v[4 * j + 1], cur[j].z + v[4 * j + 2],
-                                     cur[j].w + v[4 * j + 3]);
-            } else {
+          for (int it = 0; it < 8; ++it) d[it] = *reinterpret_cast<const float4*>(stg + (it * 4 + sr) * kStg + sc);
+          if (p.re) {  // coef epilogue: the dS tile never leaves the SM
+            float4 rr[8], ii[8];
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (n0 + j < p.N) crow[n0 + j] = first_chunk ? v[j] : crow[n0 + j] + v[j];
+            for (int it = 0; it < 8; ++it) {
+              const int m = m_base + it * 4 + sr;
+              const int64_t o = (int64_t)m * p.ldc + n;
+              if (m < p.M && full4) {
+                rr[it] = __ldcs(reinterpret_cast<const float4*>(p.re + o));  // read once: stream
+                ii[it] = __ldcs(reinterpret_cast<const float4*>(p.im + o));
+              }
+            }
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int m = m_base + it * 4 + sr;
+              if (m >= p.M) continue;
+              const int64_t o = (int64_t)m * p.ldc + n, o2 = o + (int64_t)p.M * p.ldc;
+              if (full4) {
+                float4 hr, hi;
+                coef_store(d[it].x, rr[it].x, ii[it].x, p.eps, hr.x, hi.x);
+                coef_store(d[it].y, rr[it].y, ii[it].y, p.eps, hr.y, hi.y);
+                coef_store(d[it].z, rr[it].z, ii[it].z, p.eps, hr.z, hi.z);
+                coef_store(d[it].w, rr[it].w, ii[it].w, p.eps, hr.w, hi.w);
+                if (kSplit) {
+                  __stcs(reinterpret_cast<float4*>(p.c_lo + o), tf32_lo4(hr));
+                  __stcs(reinterpret_cast<float4*>(p.c_lo + o2), tf32_lo4(hi));
+                }
+                __stcs(reinterpret_cast<float4*>(p.C + o), tf32_hi4(hr));
+                __stcs(reinterpret_cast<float4*>(p.C + o2), tf32_hi4(hi));
+              } else {
+                const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  if (n + j >= p.N) continue;
+                  float cr, ci;
+                  coef_store(dv[j], p.re[o + j], p.im[o + j], p.eps, cr, ci);
+                  p.C[o + j] = tf32_rne(cr);
+                  p.C[o2 + j] = tf32_rne(ci);
+                  if (kSplit) {
+                    p.c_lo[o + j] = tf32_rne(cr - tf32_rne(cr));
+                    p.c_lo[o2 + j] = tf32_rne(ci - tf32_rne(ci));
+                  }
+                }
+              }
+            }
+          } else {
+            // the running sum lives in C (L2): all loads are in flight before any add
+            float4 cur[8];
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int m = m_base + it * 4 + sr;
+              cur[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (!first_chunk && m < p.M && full4)
+                cur[it] = *reinterpret_cast<const float4*>(cbase + (int64_t)m * p.ldc + n);
+            }
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int m = m_base + it * 4 + sr;
+              if (m >= p.M) continue;
+              float* crow = cbase + (int64_t)m * p.ldc + n;
+              if (full4) {
+                *reinterpret_cast<float4*>(crow) = make_float4(cur[it].x + d[it].x, cur[it].y + d[it].y,
+                                                               cur[it].z + d[it].z, cur[it].w + d[it].w);
+              } else {
+                const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  if (n + j < p.N) crow[j] = first_chunk ? dv[j] : crow[j] + dv[j];
+              }
             }
           }
         }
@@ -325,7 +413,7 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.n_tiles = (g.N + kBN - 1) / kBN;
   const int tiles = p.m_tiles * p.n_tiles;
   const int units = (kPair ? (p.m_tiles + 1) / 2 * 2 : p.m_tiles) * p.n_tiles;  // CTAs per split
-  int splits = g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, units));
+  int splits = g.coef_re ? 1 : g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, units));
   const int64_t kb = g.K / C::BK;
   splits = (int)std::min<int64_t>(splits, kb);
   p.k_per_split = (kb + splits - 1) / splits * C::BK;
@@ -333,12 +421,17 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.k_chunk = (kSplit ? 1024 : 2048);  // <= 128 / 256 accumulate steps per TMEM chain
   p.b_mn = g.b_mn;
   p.b_row_len = g.b_mn ? g.b_row_len : 1 << 30;
+  p.re = g.coef_re;
+  p.im = g.coef_im;
+  p.c_lo = g.coef_lo;
+  p.eps = g.coef_eps;
+  if (p.re && (p.splits != 1 || kb > p.k_chunk / C::BK || g.alpha != 1.f)) return NNAB_EINVAL;  // one TMEM chain
   const bool direct = p.splits == 1 && g.alpha == 1.f;
   p.C = direct ? g.c : g.partial;
   p.ldc = direct ? g.ldc : (int64_t)p.n_tiles * kBN;
   p.split_stride = (int64_t)p.m_tiles * kBM * p.ldc;
   if (!direct && !g.partial) return NNAB_EINVAL;
-  const size_t smem = 1024 + kStages * C::STAGE + 128;
+  const size_t smem = 1024 + kStages * C::STAGE + 128 + 4 * 32 * kStg * 4;
   auto k = rgemm_kernel<kSplit, kPair>;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   (void)tiles;

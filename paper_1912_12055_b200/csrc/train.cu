@@ -59,8 +59,8 @@ __global__ void coef_kernel(const float* __restrict__ ds_slots, const float* __r
     float d = 0.f;
     if (b < B && t < T) d = ds_slots ? ds_slots[e] : g_bft[(b * F + f) * (int64_t)T + t];
     const float r = re[e], i = im[e];
-    const float s = sqrtf(fmaf(r, r, i * i) + eps);
-    const float cr = d * (r / s), ci = d * (i / s);
+    const float di = d * rsqrtf(fmaf(r, r, i * i) + eps);  // as rgemm.cu coef_store
+    const float cr = di * r, ci = di * i;
     const float hr = tf32_rne(cr), hi_ = tf32_rne(ci);
     hi[e] = hr;
     hi[e + (int64_t)F * ld] = hi_;
@@ -269,6 +269,43 @@ extern "C" int nnab_rgemm(int32_t M, int32_t N, int64_t K, const float* a_hi, co
   g.ldc = ldc;
   g.splits = splits;
   g.partial = partial;
+  return launch_rgemm(g, precision, (cudaStream_t)stream);
+}
+
+// Joint mel + trainable STFT backward, dS = W^T g fused with the coef step:
+// coef rows [0, F) = dS*re/S, [F, 2F) = dS*im/S (gradients.py:125-128,
+// nnAudio trainable_mel over trainable_STFT).  wt: W^T zero-padded to
+// [F][kp] (kp = n_mels rounded up to 32); gs: the upstream grad in slot
+// layout [n_mels][ld] (nnab_grad_to_slots); re/im: [F][ld] from the training
+// forward.  dS never reaches HBM: the GEMM epilogue reads re/im and writes coef.
+extern "C" int nnab_mel_dft_coef(int32_t F, int64_t ld, int32_t kp, const float* wt_hi, const float* wt_lo,
+                                 const float* gs_hi, const float* gs_lo, int32_t n_mels, const float* re_s,
+                                 const float* im_s, float eps, int32_t precision, float* coef_hi, float* coef_lo,
+                                 void* stream) {
+  if (F < 1 || ld < 1 || kp < n_mels || n_mels < 1 || !wt_hi || !gs_hi || !re_s || !im_s || !coef_hi)
+    return NNAB_EINVAL;
+  if (precision == NNAB_PREC_3XTF32 && (!wt_lo || !gs_lo || !coef_lo)) return NNAB_EINVAL;
+  if (ld > INT32_MAX) return NNAB_EINVAL;
+  if (kp > 1024) return NNAB_ENOTSUP;  // one TMEM accumulation chain per tile
+  RGemmArgs g;
+  g.M = F;
+  g.N = (int32_t)ld;
+  g.K = kp;
+  g.a_hi = wt_hi;
+  g.a_lo = wt_lo;
+  g.lda = kp;
+  g.b_hi = gs_hi;
+  g.b_lo = gs_lo;
+  g.b_mn = 1;
+  g.b_row_len = (int32_t)ld;
+  g.b_rows = n_mels;
+  g.c = coef_hi;
+  g.ldc = ld;
+  g.splits = 1;
+  g.coef_re = re_s;
+  g.coef_im = im_s;
+  g.coef_lo = coef_lo;
+  g.coef_eps = eps;
   return launch_rgemm(g, precision, (cudaStream_t)stream);
 }
 
