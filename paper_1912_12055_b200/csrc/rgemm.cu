@@ -90,13 +90,19 @@ NNAB_DEV uint64_t mndesc(const void* p, int /*swz*/, uint32_t lbo) {
 // cta_group::2 MMAs -- each CTA stages its own 128 A rows and HALF of the B tile,
 // so the B bytes pulled from L2 per MAC halve (the long kernel-gradient
 // reduction dK = coef @ frames is L2-bandwidth bound at 128 x 256 per CTA).
-template <bool kSplit, bool kPair>
+// kWide (with kPair): 256 x 512 tiles -- two N=256 MMAs per K step into all
+// 512 TMEM columns (one accumulator), a quarter less L2 traffic per MAC again.
+template <bool kSplit, bool kPair, bool kWide>
 __global__ void __launch_bounds__(kThreads, 1)
     rgemm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                  const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                  const RParams p) {
   using C = RCfg<kSplit>;
-  constexpr int kBNc = kPair ? kBN / 2 : kBN;  // B columns this CTA stages
+  static_assert(!kWide || (kPair && !kSplit), "wide tiles are a TF32 pair mode");
+  constexpr int TBN = kWide ? 2 * kBN : kBN;     // tile columns
+  constexpr int NACC = kWide ? 1 : C::NUM_ACC;   // TMEM accumulators
+  constexpr int kBNc = kPair ? kBN / 2 : kBN;  // B columns this CTA stages per MMA
+  constexpr int kHalves = kWide ? 2 : 1;       // N=256 MMAs per K step
   const uint32_t rank = kPair ? cluster_ctarank() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -148,16 +154,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* st = smem + s * C::STAGE;
           if (kPair) {  // both CTAs' bytes complete on the leader's barrier
             const uint32_t fb = mapa(&full[s], 0);
-            if (rank == 0) mbar_expect_tx(&full[s], 2 * (C::A_BYTES + C::B_BYTES / 2));
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * (C::A_BYTES + kHalves * C::B_BYTES / 2));
             tma_load_2d_pair(st, &ta_hi, fb, (int)k, mt * kBM, pol);
-            if (!p.b_mn) {
-              tma_load_2d_pair(st + C::A_BYTES, &tb_hi, fb, (int)k, nt * kBN + (int)rank * kBNc, pol);
-            } else {
+#pragma unroll
+            for (int h = 0; h < kHalves; ++h) {  // this CTA's half of each MMA's 256 columns
+              const int nb = nt * TBN + h * kBN + (int)rank * kBNc;
+              uint8_t* sb = st + C::A_BYTES + h * (C::B_BYTES / 2);
+              if (!p.b_mn) {
+                tma_load_2d_pair(sb, &tb_hi, fb, (int)k, nb, pol);
+              } else {
+                int col = nb % p.b_row_len, row = (int)(k + nb / p.b_row_len);
 #pragma unroll 1
-              for (int j = 0; j < kBNc / 32; ++j) {
-                const int n0 = nt * kBN + (int)rank * kBNc + j * 32;
-                tma_load_2d_pair(st + C::A_BYTES + j * C::BK * 128, &tb_hi, fb, n0 % p.b_row_len,
-                                 (int)(k + n0 / p.b_row_len), pol);
+                for (int j = 0; j < kBNc / 32; ++j) {
+                  tma_load_2d_pair(sb + j * C::BK * 128, &tb_hi, fb, col, row, pol);
+                  if ((col += 32) == p.b_row_len) col = 0, ++row;  // b_row_len % 32 == 0
+                }
               }
             }
             if (++s == kStages) { s = 0; ph ^= 1; }
@@ -189,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (rank == 0 && elect_one()) {
       const uint32_t idesc = idesc_tf32(kPair ? 2 * kBM : kBM, kBN) | (p.b_mn ? (1u << 16) : 0u);
+      (void)idesc;
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int w = w_start; w < n_work; w += w_step) {
@@ -199,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t kc_hi = (kc + p.k_chunk < k_hi) ? kc + p.k_chunk : k_hi;
           mbar_wait(&tempty[acc], aph ^ 1);
           tc_fence_after();
-          const uint32_t d = tbase + acc * C::ACC_STRIDE;
+          const uint32_t d = tbase + (NACC > 1 ? acc * C::ACC_STRIDE : 0);
           bool first = true;
           for (int64_t k = kc; k < kc_hi; k += C::BK) {
             mbar_wait(&full[s], ph);
@@ -215,8 +227,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < C::BK / 8; ++kk) {
               const uint64_t ao = (uint64_t)((kk * 32) >> 4);
               const uint64_t bo = p.b_mn ? (uint64_t)((kk * 1024) >> 4) : ao;  // MN-major: next 8 K rows
-              if (kPair) mma_tf32_pair(d, a + ao, b + bo, idesc, first ? 0u : 1u);
-              else mma_tf32(d, a + ao, b + bo, idesc, first ? 0u : 1u);
+              if (kPair) {
+                mma_tf32_pair(d, a + ao, b + bo, idesc, first ? 0u : 1u);
+                if (kWide)  // second 256 columns: B half staged B_BYTES/2 further on
+                  mma_tf32_pair(d + kBN, a + ao, b + bo + (uint64_t)((C::B_BYTES / 2) >> 4), idesc, first ? 0u : 1u);
+              } else {
+                mma_tf32(d, a + ao, b + bo, idesc, first ? 0u : 1u);
+              }
               if (kSplit) {
                 mma_tf32(d + kBN, a + ao, b_lo + bo, idesc, first ? 0u : 1u);
                 mma_tf32(d + kBN, a_lo + ao, b + bo, idesc, 1u);
@@ -229,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (kPair) mma_commit_pair(&tfull[acc], 0x3);
           else mma_commit(&tfull[acc]);
-          if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
+          if (++acc == NACC) { acc = 0; aph ^= 1; }
         }
       }
     }
@@ -257,9 +274,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool first_chunk = kc == k_lo;  // later chunks add into C in fixed order: deterministic
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
-        const uint32_t tb = tbase + ((q * 32) << 16) + acc * C::ACC_STRIDE;
+        const uint32_t tb = tbase + ((q * 32) << 16) + (NACC > 1 ? acc * C::ACC_STRIDE : 0);
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = 0; c < TBN / 32; ++c) {
           float v[32];
           tmem_ld32(tb + c * 32, v);
           if (kSplit) {
@@ -277,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<float4*>(stg + lane * kStg + 4 * j) =
                 make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           __syncwarp();
-          const int n = nt * kBN + c * 32 + sc;
+          const int n = nt * TBN + c * 32 + sc;
           if (n >= p.N || m_base >= p.M) continue;
           const bool full4 = vec && n + 4 <= p.N;
           float4 d[8];
@@ -357,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         if (kPair) mbar_arrive_cluster(tempty0 + 8 * acc);
         else mbar_arrive(&tempty[acc]);
-        if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
+        if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
     }
   }
@@ -383,10 +400,11 @@ __global__ void sum_splits_kernel(const float* __restrict__ parts, int32_t split
   }
 }
 
-template <bool kSplit, bool kPair>
+template <bool kSplit, bool kPair, bool kWide = false>
 int launch(const RGemmArgs& g, cudaStream_t st) {
   using C = RCfg<kSplit>;
   constexpr int kBNc = kPair ? kBN / 2 : kBN;
+  constexpr int TBN = kWide ? 2 * kBN : kBN;
   if (g.K % C::BK || g.lda % 4 || (g.b_mn && g.b_row_len % 32) || (!g.b_mn && g.ldb % 4)) return NNAB_EINVAL;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   int rc = make_tmap_2d(&ta_hi, g.a_hi, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
@@ -410,7 +428,7 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.N = g.N;
   p.K = g.K;
   p.m_tiles = (g.M + kBM - 1) / kBM;
-  p.n_tiles = (g.N + kBN - 1) / kBN;
+  p.n_tiles = (g.N + TBN - 1) / TBN;
   const int tiles = p.m_tiles * p.n_tiles;
   const int units = (kPair ? (p.m_tiles + 1) / 2 * 2 : p.m_tiles) * p.n_tiles;  // CTAs per split
   int splits = g.coef_re ? 1 : g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, units));
@@ -418,7 +436,8 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   splits = (int)std::min<int64_t>(splits, kb);
   p.k_per_split = (kb + splits - 1) / splits * C::BK;
   p.splits = (int)((g.K + p.k_per_split - 1) / p.k_per_split);
-  p.k_chunk = (kSplit ? 1024 : 2048);  // <= 128 / 256 accumulate steps per TMEM chain
+  p.k_chunk = (kSplit ? 1024 : kWide ? 8192 : 2048);  // accumulate steps per TMEM chain (wide: no
+                                                       // second accumulator, so drain less often)
   p.b_mn = g.b_mn;
   p.b_row_len = g.b_mn ? g.b_row_len : 1 << 30;
   p.re = g.coef_re;
@@ -428,11 +447,11 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   if (p.re && (p.splits != 1 || kb > p.k_chunk / C::BK || g.alpha != 1.f)) return NNAB_EINVAL;  // one TMEM chain
   const bool direct = p.splits == 1 && g.alpha == 1.f;
   p.C = direct ? g.c : g.partial;
-  p.ldc = direct ? g.ldc : (int64_t)p.n_tiles * kBN;
+  p.ldc = direct ? g.ldc : (int64_t)p.n_tiles * TBN;
   p.split_stride = (int64_t)p.m_tiles * kBM * p.ldc;
   if (!direct && !g.partial) return NNAB_EINVAL;
   const size_t smem = 1024 + kStages * C::STAGE + 128 + 4 * 32 * kStg * 4;
-  auto k = rgemm_kernel<kSplit, kPair>;
+  auto k = rgemm_kernel<kSplit, kPair, kWide>;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   (void)tiles;
   if (!kPair) {
@@ -467,8 +486,11 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
 }  // namespace
 
 size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits) {
-  const int64_t mt = (M + kBM - 1) / kBM, nt = (N + kBN - 1) / kBN;
-  if (splits <= 0) splits = std::max(1, num_sms() / (int)std::max<int64_t>(1, mt * nt));  // >= the pair count
+  const int64_t mt = (M + kBM - 1) / kBM;
+  const int64_t nt = (N + 2 * kBN - 1) / (2 * kBN) * 2;  // 256-column tiles, even: covers the wide layout
+  // auto split count: the largest any mode picks (fewest CTAs per split: wide pairs)
+  const int64_t units = std::min<int64_t>(mt * ((N + kBN - 1) / kBN), (mt + 1) / 2 * 2 * (nt / 2));
+  if (splits <= 0) splits = std::max(1, num_sms() / (int)std::max<int64_t>(1, units));
   return (size_t)splits * mt * kBM * nt * kBN * sizeof(float);
 }
 
@@ -483,7 +505,9 @@ int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s) {
   const bool pair_ok = pair_env != 0;
   if (precision == NNAB_PREC_3XTF32) return launch<true, false>(g, s);
   if (precision == NNAB_PREC_TF32) {
-    const bool pair = pair_ok && (pair_env == 2 || g.M > kBM);  // one m tile: the peer would idle
+    const bool pair = pair_ok && (pair_env >= 2 || g.M > kBM);  // one m tile: the peer would idle
+    const bool wide = pair && !g.coef_re && (pair_env == 3 || (pair_env == 1 && g.N > kBN && g.K >= 65536));
+    if (wide) return launch<false, true, true>(g, s);
     return pair ? launch<false, true>(g, s) : launch<false, false>(g, s);
   }
   return NNAB_EINVAL;
