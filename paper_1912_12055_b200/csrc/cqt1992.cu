@@ -117,10 +117,27 @@ extern "C" int nnab_cqt1992v2_forward(const nnab_frames* f, const float* x, cons
                                        eps, out, workspace, workspace_bytes, stream);
 }
 
+namespace nnab {
+// The scheduled long-bank GEMM on staged frames; out_bins = bins per clip of
+// the (possibly larger) output this bank's rows are written into.
+int cqt_schedule_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo, int32_t n_bins,
+                        const uint32_t* schedule, int32_t n_entries, int32_t precision, int32_t out_kind, float eps,
+                        float* out, int32_t out_bins, const void* workspace, size_t workspace_bytes,
+                        cudaStream_t s);
+}  // namespace nnab
+
 extern "C" int nnab_cqt1992v2_forward_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
                                              int32_t n_bins, const uint32_t* schedule, int32_t n_entries,
                                              int32_t precision, int32_t out_kind, float eps, float* out,
                                              const void* workspace, size_t workspace_bytes, void* stream) {
+  return nnab::cqt_schedule_staged(f, packed_hi, packed_lo, n_bins, schedule, n_entries, precision, out_kind, eps,
+                                   out, n_bins, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int nnab::cqt_schedule_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo, int32_t n_bins,
+                              const uint32_t* schedule, int32_t n_entries, int32_t precision, int32_t out_kind,
+                              float eps, float* out, int32_t out_bins, const void* workspace,
+                              size_t workspace_bytes, cudaStream_t s) {
   FrameGeom g;
   int rc = frame_geometry(f, &g);
   if (rc) return rc;
@@ -133,8 +150,7 @@ extern "C" int nnab_cqt1992v2_forward_staged(const nnab_frames* f, const float* 
     return NNAB_EINVAL;
   if (g.B == 0) return NNAB_OK;
   const size_t need = nnab_stft_workspace_bytes(f, precision);
-  if (!workspace || workspace_bytes < need) return NNAB_EINVAL;
-  cudaStream_t s = (cudaStream_t)stream;
+  if (!workspace || workspace_bytes < need || out_bins < n_bins) return NNAB_EINVAL;
   const float* rows_hi = reinterpret_cast<const float*>(workspace);
   const float* rows_lo =
       split ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + need / 2) : nullptr;
@@ -154,5 +170,6 @@ extern "C" int nnab_cqt1992v2_forward_staged(const nnab_frames* f, const float* 
   a.n_tab = n_entries;
   a.b_box = std::min(256, (2 * std::min(n_bins, 128) + 15) / 16 * 16);
   a.pairs = 1;
+  a.out_bins = out_bins;
   return launch_stft_gemm(g, a, precision, s);
 }

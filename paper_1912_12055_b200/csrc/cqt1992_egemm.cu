@@ -11,24 +11,28 @@
 // direct schedule (cqt1992.cu) issues per M tile; the long low-frequency rows
 // become many columns instead of many tiny MMAs.
 //
-// Status (round 1): correct (tests/test_gpu_cqt.py) and its GEMM alone runs the
-// 1,770-clip batch in 0.95 ms, but the diagonal-sum epilogue (~30k cycles per
-// tile, mostly TMEM->smem staging and the short-bin groups' many runs) does not
-// yet keep up with the MMAs (11k cycles per tile), so the engine's default stays
-// the per-K-block schedule (CqtLongEngine(method="schedule")).  Next: E-GEMM for
-// the long bins only (few long runs), the schedule for the short ones.
+// Used for the long low-frequency bins of the default hybrid
+// (nnab_cqt1992v2_hybrid_staged; CqtLongEngine(method="hybrid")): bins whose
+// support spans >= 8 hops here, the per-K-block schedule (cqt1992.cu) for the
+// rest.  On the 1,770-clip batch: schedule alone 3.4 ms, E-GEMM alone 1.6 ms,
+// hybrid 1.45 ms (+ 0.4 ms frame staging).
 //
-// Columns are packed into groups of <= 256 columns / <= 64 rows (whole bins,
-// re and im together), sorted by (row, r) inside a group.  A persistent CTA owns
-// one group and a contiguous run of M tiles (128 hop rows each): TMA producer
-// warp, single-thread tcgen05.mma issuer (M = 128, N = 256, K = 8, TF32), and
-// 4 epilogue warps that stage each E tile through shared memory 32 columns at a
-// time and fold it into a ring of D rows (D[row][d & 255]); each D element has
-// one owner thread per pass, so the sum needs no atomics and is deterministic.  D rows
-// that can receive nothing more are turned into magnitude / power / complex
-// and written to the (B, n_bins, T) output, coalesced along T.  Each CTA also
-// computes the first tile past its run (a 1-in-~150 overlap) so its last D rows
-// are complete; D rows before its run belong to the previous CTA.
+// Columns are packed into groups of <= 256 columns / <= 8 bins (16 bank rows),
+// longest bins first; each row's columns are whole windows of 16 consecutive
+// hop offsets r (zero-weight past its support).  A persistent CTA owns one group
+// and a contiguous run of M tiles (128 hop rows each): TMA producer warp,
+// single-thread tcgen05.mma issuer (M = 128, N = 256, K = 8, TF32, two TMEM
+// accumulators), and 4 epilogue warps.  Epilogue: thread = E row s; for a
+// window (row, r0 .. r0+15) lane l gathers E[s_l + k][(row, r0 + k)] from lane
+// (l + k) mod 32 by shuffle, so the window folds into two register sums (the
+// pairs whose source lane wrapped belong to D row s_l - 32 - r0, the rest to
+// s_l - r0) and two read-modify-writes of the warp's private ring of D rows --
+// no atomics, no shared-memory staging of E, deterministic for a given tiling.
+// D rows that can receive nothing more are summed over the four warp rings,
+// turned into magnitude / power / complex and written to the (B, n_bins, T)
+// output, coalesced along T.  Each CTA also computes the first tile past its
+// run (a 1-in-~150 overlap) so its last D rows are complete; D rows before its
+// run belong to the previous CTA.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -42,15 +46,15 @@ namespace {
 constexpr int kBM = 128, kBN = 256, kBK = 32, kThreads = 256;
 constexpr int kStages = 3;
 constexpr int kA = kBM * kBK * 4, kB = kBN * kBK * 4, kStage = kA + kB;  // 16 + 32 KB
-constexpr int kRows = 64;   // D rows (bank rows: 2 per bin) per group
-constexpr int kChunk = 64;  // E columns staged in shared memory per reduction pass
-constexpr int kEB = kBM;  // staged E row stride (floats): writes and diagonal reads are both lane-consecutive
-constexpr int kRing = 192;  // D ring length (slots); >= 128 + max r
+constexpr int kRows = 16;   // D rows (bank rows: 2 per bin) per group
+constexpr int kRing = 256;  // D ring length (slots, power of two); >= 128 + max r
 constexpr uint16_t kUnused = 0xFFFF;
+constexpr int kWin = 16;  // a row's columns come in windows of 16 consecutive r
 
+constexpr int kChunk = 64;  // run-table granularity (host plan only)
 constexpr int kChunks = kBN / kChunk;
 constexpr int kRunSlots = kChunk + 1;  // per chunk: count, then up to 64 runs
-constexpr int kEpi = 192;  // warps 2-7 reduce; warps 4-7 also read TMEM
+constexpr int kEpi = 128;  // warps 4-7: TMEM readers and reducers
 
 struct EParams {
   int64_t B;
@@ -72,19 +76,16 @@ NNAB_DEV uint64_t sdesc(const void* p) {  // K-major, 128-byte swizzle, 8-row at
   return d;
 }
 
-NNAB_DEV void ep_sync() { asm volatile("bar.sync 1, 192;" ::: "memory"); }  // epilogue warps 2-7
+NNAB_DEV void ep_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // epilogue warps 4-7
 // ring slot of D row d (d >= -64): rows are offset by one ring length to stay non-negative
-NNAB_DEV int ring_slot(int64_t d) { return (int)((uint32_t)(d + kRing) % (uint32_t)kRing); }
 
 __global__ void __launch_bounds__(kThreads, 1)
     cqt1992_egemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                          const EParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* ring = reinterpret_cast<float*>(smem + kStages * kStage);  // [kRows][kRing]
-  float* ebuf = ring + kRows * kRing;                                // [kChunk][kEB]
-  uint32_t* runs = reinterpret_cast<uint32_t*>(ebuf + kChunk * kEB);  // [kChunks][kRunSlots]
-  uint16_t* cols = reinterpret_cast<uint16_t*>(runs + kChunks * kRunSlots);
+  float* ring = reinterpret_cast<float*>(smem + kStages * kStage);  // [4 warps][kRows][kRing]
+  uint16_t* cols = reinterpret_cast<uint16_t*>(ring + 4 * kRows * kRing);  // [kBN], 16-byte aligned
   int32_t* rows = reinterpret_cast<int32_t*>(cols + kBN);
   uint64_t* bars = reinterpret_cast<uint64_t*>(rows + kRows);  // 8-byte aligned: 512 + 256 bytes above
   uint64_t* full = bars;            // [kStages]
@@ -113,10 +114,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tslot);
-  for (int i = threadIdx.x; i < kRows * kRing; i += kThreads) ring[i] = 0.f;
+  for (int i = threadIdx.x; i < 4 * kRows * kRing; i += kThreads) ring[i] = 0.f;
   if (active) {
     for (int i = threadIdx.x; i < kBN; i += kThreads) cols[i] = p.col_table[g * kBN + i];
-    for (int i = threadIdx.x; i < kChunks * kRunSlots; i += kThreads) runs[i] = p.run_table[g * kChunks * kRunSlots + i];
     for (int i = threadIdx.x; i < kRows; i += kThreads) rows[i] = p.group_rows[g * kRows + i];
   }
   tc_fence_before();
@@ -176,97 +176,83 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       __syncwarp();
-    } else if (warp >= 2) {
+    } else if (warp >= 4) {
       // -------------------------------------------------------------- epilogue
-      const bool tm = warp >= 4;  // TMEM readers (lane quarter warp - 4)
-      const int q = warp & 3, row_in_tile = q * 32 + lane;
+      // Thread = E row s (TMEM lane).  Column (row, r) of E[s] belongs to
+      // D[s - r][row]: each warp adds its 32 rows' values into its own ring of
+      // D rows (ring[q][row][d & 255]); for one column the 32 lanes hit 32
+      // consecutive D rows, so every add is a conflict-free shared-memory RMW
+      // and no two threads ever touch the same element (no atomics).  Rows that
+      // can receive nothing more are summed over the four rings and emitted.
+      const int q = warp - 4, et = threadIdx.x - 128;  // et: 0 .. 127
+      float* myring = ring + q * (kRows * kRing);
       int acc = 0;
       uint32_t aph = 0;
       const int64_t own = (int64_t)m_a * kBM;  // D rows from here on are this CTA's to emit
       int n_gbins = 0;                          // bins of this group (rows are filled front to back)
       while (n_gbins < kRows / 2 && rows[2 * n_gbins] >= 0) ++n_gbins;
-      int64_t done = own - p.r_max;             // ring rows below this are cleared
+      int n_cols = 0;
+      while (n_cols < kBN && cols[n_cols] != kUnused) ++n_cols;
+      int64_t done = own - p.r_max;  // ring rows below this are cleared
       for (int m = m_a; m < m_end; ++m) {
-        if (tm) {
-          mbar_wait(&tfull[acc], aph);
-          tc_fence_after();
-        }
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * kBN;
-        // D[row][d] += sum over the row's columns (row, r) of E[d + r][(row, r)]: E goes
-        // through shared memory one 32-column chunk at a time, then thread et sums, for
-        // d_local = et and et + 128 (d = 128 m - r_max + d_local), the chunk's columns
-        // row by row (columns are sorted by (row, r)) and adds each row's sum into the
-        // ring once -- every D element has a single owner thread, no atomics or races.
-        const int et = threadIdx.x - 64;  // 0 .. 191
-        const int span = kBM + p.r_max;   // D rows this tile reaches (<= kEpi: one per thread)
+        const int s_row = m * kBM + q * 32 + lane;  // this thread's E row (global slot)
 #pragma unroll 1
-        for (int c0 = 0; c0 < kBN; c0 += kChunk) {
-          if (cols[c0] == kUnused) break;  // the rest of the table is empty
-          if (tm) {
+        for (int c0 = 0; c0 < n_cols; c0 += 32) {
+          float v[32];
+          tmem_ld32(ta + c0, v);
+          tmem_ld_wait();
+          // The plan lays each bank row's columns out as whole windows of 16
+          // consecutive r (zero-weight padding past the support).  Column k of a
+          // window (row, r0 + k): lane l gathers E[s_l + k][k] from lane (l + k) mod
+          // 32 -- pairs whose source lane did not wrap all belong to D row s_l - r0,
+          // the wrapped ones to s_l - 32 - r0 -- so a window costs 16 shuffles and
+          // two read-modify-writes per lane, cells distinct across lanes.
 #pragma unroll
-            for (int h = 0; h < kChunk; h += 32) {
-              float v[32];
-              tmem_ld32(ta + c0 + h, v);
-              tmem_ld_wait();
+          for (int w16 = 0; w16 < 2; ++w16) {
+            const uint32_t meta = cols[c0 + 16 * w16];  // warp-uniform
+            if (meta == kUnused) break;
+            const int r0 = (int)(meta & 0xFF);
+            float* rrow = myring + (meta >> 8) * kRing;
+            float hi = 0.f, lo = 0.f;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) ebuf[(h + j) * kEB + row_in_tile] = v[j];
+            for (int k = 0; k < 16; ++k) {
+              const float x = __shfl_sync(0xffffffffu, v[16 * w16 + k], (lane + k) & 31);
+              if (lane + k < 32) hi += x;
+              else lo += x;
             }
+            rrow[(s_row - r0) & (kRing - 1)] += hi;
+            rrow[(s_row - 32 - r0) & (kRing - 1)] += lo;
           }
-          ep_sync();
-          // run = consecutive columns of one D row with consecutive r: the row's sum for
-          // D row d is a diagonal of the staged chunk (stride kEB + 1), summed with 4
-          // independent accumulators over the in-tile range of E rows
-          const uint32_t* cr = runs + (c0 / kChunk) * kRunSlots;
-          const int n_runs = (int)cr[0];
-#pragma unroll 1
-          for (int dl = et; dl < span; dl += kEpi) {
-            const int slot = ring_slot((int64_t)m * kBM - p.r_max + dl);
-#pragma unroll 1
-            for (int k = 0; k < n_runs; ++k) {
-              const uint32_t run = cr[1 + k];
-              const int rl = (int)(run & 0xFF), j0 = (int)((run >> 8) & 0x3F), n = (int)((run >> 14) & 0x7F),
-                        r0 = (int)(run >> 21);
-              const int sl0 = dl - p.r_max + r0;  // E row of the run's first column
-              const int i0 = max(0, -sl0), i1 = min(n, kBM - sl0);
-              if (i0 >= i1) continue;
-              const float* e = ebuf + j0 * kEB + sl0;
-              float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-              int i = i0;
-              for (; i + 4 <= i1; i += 4) {
-                a0 += e[i * (kEB + 1)];
-                a1 += e[(i + 1) * (kEB + 1)];
-                a2 += e[(i + 2) * (kEB + 1)];
-                a3 += e[(i + 3) * (kEB + 1)];
-              }
-              for (; i < i1; ++i) a0 += e[i * (kEB + 1)];
-              ring[rl * kRing + slot] += (a0 + a1) + (a2 + a3);
-            }
-          }
-          ep_sync();
         }
-        if (tm) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
         }
         ep_sync();
-        // D rows < limit can receive nothing more: emit the CTA's own ones, clear the ring
+        // D rows < limit can receive nothing more: emit the CTA's own ones, clear the rings
         const int64_t limit = m + 1 == m_end ? (int64_t)m_b * kBM : (int64_t)(m + 1) * kBM - p.r_max;
         const int n_d = (int)(limit - done);
         for (int dd = et; dd < n_d; dd += kEpi) {  // consecutive threads: consecutive t
           const int64_t d = done + dd;
           const int b = (int)(d / p.R), t = (int)(d - (int64_t)b * p.R);
           const bool emit = d >= own && b < p.B && t < p.T;  // else: partial sums of another CTA's rows
-          const int slot = ring_slot(d);
+          const int slot = (int)(d & (kRing - 1));
           for (int bl = 0; bl < n_gbins; ++bl) {
-            float* pre = &ring[(2 * bl) * kRing + slot];
-            const float re = pre[0], im = pre[kRing];
-            pre[0] = 0.f;
-            pre[kRing] = 0.f;
+            float re = 0.f, im = 0.f;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              float* pre = ring + w * (kRows * kRing) + (2 * bl) * kRing + slot;
+              re += pre[0];
+              im += pre[kRing];
+              pre[0] = 0.f;
+              pre[kRing] = 0.f;
+            }
             if (!emit) continue;
             const int64_t o = ((int64_t)b * p.n_bins + (rows[2 * bl] >> 1)) * (int64_t)p.T + t;
             if (p.out_kind == NNAB_OUT_COMPLEX) {
@@ -337,7 +323,8 @@ extern "C" int nnab_cqt_egemm_plan(const int32_t* support, int32_t n_bins, int32
       k0 = 0;
       k1 = 1;
     }
-    const Bin x{b, k0 / hop, (k1 - 1) / hop};
+    Bin x{b, k0 / hop, (k1 - 1) / hop};
+    x.r1 = x.r0 + (x.r1 - x.r0 + kWin) / kWin * kWin - 1;  // whole 16-column windows (zero-weight tail)
     if (x.r1 > 254) return NNAB_ENOTSUP;
     rmax = std::max(rmax, x.r1);
     bins.push_back(x);
@@ -411,16 +398,23 @@ extern "C" int nnab_pack_cqt_egemm(const float* k_re, const float* k_im, int32_t
   return NNAB_OK;
 }
 
-// E-GEMM forward on frames staged by nnab_stage_frames (TF32 only).
-extern "C" int nnab_cqt1992v2_egemm_staged(const nnab_frames* f, const float* packed_hi, const uint16_t* col_table,
-                                           const int32_t* group_rows, const uint32_t* run_table,
-                                           int32_t n_groups, int32_t r_max,
-                                           int32_t n_bins, int32_t out_kind, float eps, float* out,
-                                           const void* workspace, size_t workspace_bytes, void* stream) {
+namespace nnab {
+int cqt_schedule_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo, int32_t n_bins,
+                        const uint32_t* schedule, int32_t n_entries, int32_t precision, int32_t out_kind, float eps,
+                        float* out, int32_t out_bins, const void* workspace, size_t workspace_bytes,
+                        cudaStream_t s);
+
+// E-GEMM on staged frames (TF32): the group tables' bins are written into an
+// output of out_bins bins per clip (group_rows hold global bank rows).
+static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const uint16_t* col_table,
+                            const int32_t* group_rows, int32_t n_groups, int32_t r_max, int32_t out_bins,
+                            int32_t out_kind, float eps, float* out, const void* workspace, size_t workspace_bytes,
+                            cudaStream_t stream) {
   FrameGeom g;
   int rc = frame_geometry(f, &g);
   if (rc) return rc;
-  if (!packed_hi || !col_table || !group_rows || !run_table || !out || n_groups < 1 || n_bins < 1) return NNAB_EINVAL;
+  if (!packed_hi || !col_table || !group_rows || !out || n_groups < 1 || out_bins < 1) return NNAB_EINVAL;
+  if (r_max < 0 || r_max + kBM > kRing) return NNAB_EINVAL;
   if (g.row_len != g.hop || g.hop % kBK != 0 || g.hop / kBK != 16) return NNAB_ENOTSUP;  // K = hop = 512
   if (out_kind != NNAB_OUT_MAGNITUDE && out_kind != NNAB_OUT_POWER && out_kind != NNAB_OUT_COMPLEX &&
       out_kind != NNAB_OUT_SMOOTH_MAG)
@@ -439,7 +433,7 @@ extern "C" int nnab_cqt1992v2_egemm_staged(const nnab_frames* f, const float* pa
   p.R = g.R;
   p.T = g.T;
   p.n_mtiles = (int32_t)((rows_total + kBM - 1) / kBM);
-  p.n_bins = n_bins;
+  p.n_bins = out_bins;
   p.out_kind = out_kind;
   p.n_groups = n_groups;
   p.ctas_per_group = nsm / n_groups;
@@ -447,12 +441,65 @@ extern "C" int nnab_cqt1992v2_egemm_staged(const nnab_frames* f, const float* pa
   p.eps = eps;
   p.col_table = col_table;
   p.group_rows = group_rows;
-  p.run_table = run_table;
   p.out = out;
-  const size_t smem = 1024 + (size_t)kStages * kStage + (size_t)kRows * kRing * 4 + (size_t)kChunk * kEB * 4 +
-                      kChunks * kRunSlots * 4 + kBN * 2 + kRows * 4 + 16 * 8;
+  const size_t smem = 1024 + (size_t)kStages * kStage + (size_t)4 * kRows * kRing * 4 + kBN * 2 + kRows * 4 + 16 * 8;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt1992_egemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  cqt1992_egemm_kernel<<<p.ctas_per_group * n_groups, kThreads, smem, (cudaStream_t)stream>>>(ta, tb, p);
+  cqt1992_egemm_kernel<<<p.ctas_per_group * n_groups, kThreads, smem, stream>>>(ta, tb, p);
   NNAB_LAUNCHED();
   return NNAB_OK;
+}
+}  // namespace nnab
+
+// E-GEMM forward on frames staged by nnab_stage_frames (TF32 only).  run_table
+// is reserved (the plan still emits it; the kernel reads col_table only).
+extern "C" int nnab_cqt1992v2_egemm_staged(const nnab_frames* f, const float* packed_hi, const uint16_t* col_table,
+                                           const int32_t* group_rows, const uint32_t* run_table,
+                                           int32_t n_groups, int32_t r_max,
+                                           int32_t n_bins, int32_t out_kind, float eps, float* out,
+                                           const void* workspace, size_t workspace_bytes, void* stream) {
+  (void)run_table;
+  if (n_bins < 1) return NNAB_EINVAL;
+  return cqt_egemm_staged(f, packed_hi, col_table, group_rows, n_groups, r_max, n_bins, out_kind, eps, out,
+                          workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+// CQT1992v2 hybrid on staged frames (TF32): bins [0, n_long) -- the long,
+// low-frequency kernels -- on the E-GEMM (tables from nnab_cqt_egemm_plan over
+// those bins), bins [n_long, n_bins) on the per-K-block schedule (bank and
+// schedule of those rows at the full width, so both share the staged frames).
+extern "C" int nnab_cqt1992v2_hybrid_staged(const nnab_frames* f, const float* eg_bank, const uint16_t* col_table,
+                                            const int32_t* group_rows, int32_t n_groups, int32_t r_max,
+                                            const float* sched_bank, const uint32_t* schedule, int32_t n_entries,
+                                            int32_t n_long, int32_t n_bins, int32_t out_kind, float eps, float* out,
+                                            const void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_long < 0 || n_long > n_bins || n_bins < 1 || !out) return NNAB_EINVAL;
+  FrameGeom g;
+  int rc = frame_geometry(f, &g);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_long > 0) {
+    rc = cqt_egemm_staged(f, eg_bank, col_table, group_rows, n_groups, r_max, n_bins, out_kind, eps, out, workspace,
+                          workspace_bytes, s);
+    if (rc) return rc;
+  }
+  if (n_long < n_bins) {
+    float* o = out + (int64_t)n_long * g.T * (out_kind == NNAB_OUT_COMPLEX ? 2 : 1);
+    rc = cqt_schedule_staged(f, sched_bank, nullptr, n_bins - n_long, schedule, n_entries, NNAB_PREC_TF32, out_kind,
+                             eps, o, n_bins, workspace, workspace_bytes, s);
+  }
+  return rc;
+}
+
+extern "C" int nnab_cqt1992v2_hybrid_forward(const nnab_frames* f, const float* x, const float* eg_bank,
+                                             const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups,
+                                             int32_t r_max, const float* sched_bank, const uint32_t* schedule,
+                                             int32_t n_entries, int32_t n_long, int32_t n_bins, int32_t out_kind,
+                                             float eps, float* out, void* workspace, size_t workspace_bytes,
+                                             void* stream) {
+  if (!x) return NNAB_EINVAL;
+  int rc = nnab_stage_frames(f, x, NNAB_PREC_TF32, workspace, workspace_bytes, stream);
+  if (rc) return rc;
+  return nnab_cqt1992v2_hybrid_staged(f, eg_bank, col_table, group_rows, n_groups, r_max, sched_bank, schedule,
+                                      n_entries, n_long, n_bins, out_kind, eps, out, workspace, workspace_bytes,
+                                      stream);
 }

@@ -65,6 +65,7 @@ struct StftGemmArgs {
   int32_t n_tab = 0;
   int32_t b_box = 256;
   int32_t pairs = 0;
+  int32_t out_bins = 0;  // pairs mode: bins per clip of the output (0 = n_bins; the caller offsets out)
   float *save_re = nullptr, *save_im = nullptr, *save_mag = nullptr;  // training forward (slot-major)
   int64_t ld_slots = 0;
 };

@@ -63,7 +63,7 @@ struct Params {
   // CQT1992v2 long-bank schedule: per N tile, n_tab entries (kblock << 16 | N),
   // longest-first so the first MMA (N = max) initialises every used column.
   const uint32_t* kb_tab;
-  int32_t n_tab, b_box, pairs;
+  int32_t n_tab, b_box, pairs, out_bins;
   int32_t stages;  // smem pipeline depth (4, or 3 when the Mel accumulator takes 64 KB)
   // training forward: re, im and smoothed magnitude per (bin, slot) saved in
   // slot-major layout [bin][ld_slots] for the backward GEMMs (may be null)
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (valid) {
               const int bin0 = n * 128 + c * 16;
-              const int64_t ob = b * (int64_t)F;
+              const int64_t ob = b * (int64_t)p.out_bins;
               if (kind == NNAB_OUT_COMPLEX) {
                 float2* o = reinterpret_cast<float2*>(p.out);
 #pragma unroll
@@ -474,6 +474,7 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.n_tab = a.n_tab;
   p.b_box = b_box;
   p.pairs = a.pairs;
+  p.out_bins = a.out_bins > 0 ? a.out_bins : a.n_bins;
   if (a.kb_tab && (a.n_tab < 1 || mel)) return NNAB_EINVAL;
   if (p.n_mtiles == 0) return NNAB_OK;
   // as many pipeline stages as fit next to the Mel accumulator (<= 8)

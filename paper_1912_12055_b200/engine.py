@@ -235,11 +235,18 @@ def _row_support(k_re: np.ndarray, k_im: np.ndarray) -> np.ndarray:
 
 
 class CqtLongEngine:
-    """CQT1992v2's long complex bank (kernels.py:361-402) on the tcgen05 GEMM
-    with the longest-first per-K-block schedule (csrc/cqt1992.cu)."""
+    """CQT1992v2's long complex bank (kernels.py:361-402) on the tcgen05 GEMM.
+
+    method "hybrid" (default; TF32, hop 512): the long low-frequency bins --
+    support >= 8 hops -- on the hop-offset E-GEMM (csrc/cqt1992_egemm.cu), the
+    rest on the longest-first per-K-block schedule (csrc/cqt1992.cu), from one
+    staging of the frames.  "schedule" / "egemm" run one method for every bin;
+    3xTF32 always uses the schedule."""
+
+    LONG_HOPS = 8  # hybrid: bins whose support spans >= this many hops go to the E-GEMM
 
     def __init__(self, kernels, hop: int, pad_mode: str = "reflect", precision: str = "tf32", device="cuda",
-                 dense: bool = False, method: str = "schedule"):
+                 dense: bool = False, method: str = "hybrid"):
         self.device = _require_cuda(device)
         if precision not in L.PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
@@ -247,13 +254,31 @@ class CqtLongEngine:
         k = np.asarray(kernels)
         self.n_bins, self.width = int(k.shape[0]), int(k.shape[1])
         self.hop, self.pad_mode = int(hop), pad_mode
-        if method not in ("egemm", "schedule"):
-            raise ValueError(f"method must be 'egemm' or 'schedule', got {method!r}")
+        if method not in ("egemm", "schedule", "hybrid"):
+            raise ValueError(f"method must be 'hybrid', 'egemm' or 'schedule', got {method!r}")
         self.method = "schedule" if dense else method
         if self.hop < 1:
             raise ValueError(f"stride must be >= 1, got {hop}")
         self._ws = _Workspace()
         self.set_bank(k.real, k.imag, dense=dense)
+
+    def _schedule(self, sup, dr, di):
+        """Per-K-block schedule + packed bank of the rows in dr/di (device) with supports sup."""
+        lib = L.load()
+        nb = int(sup.shape[0])
+        cap = lib.nnab_cqt_bank_tiles(nb) * (((self.width + 31) // 32 * 32) // 16) + 16
+        tab = np.zeros(cap, dtype=np.uint32)
+        n_ent = C.c_int32()
+        L.check(lib.nnab_cqt_schedule(np.ascontiguousarray(sup).ctypes.data, nb, self.width, self.precision,
+                                      tab.ctypes.data, C.byref(n_ent)), "cqt_schedule")
+        tiles = lib.nnab_cqt_bank_tiles(nb)
+        schedule = torch.from_numpy(tab[: tiles * n_ent.value].astype(np.int32)).to(self.device)
+        n = lib.nnab_cqt_bank_bytes(nb, self.width) // 4
+        hi = torch.empty(n, dtype=torch.float32, device=self.device)
+        lo = torch.empty(n, dtype=torch.float32, device=self.device) if self.precision == L.PREC_3XTF32 else None
+        L.check(lib.nnab_pack_cqt_bank(dr.data_ptr(), di.data_ptr(), nb, self.width, self.precision, hi.data_ptr(),
+                                       L.ptr(lo), L.stream_handle(self.device)), "pack_cqt_bank")
+        return schedule, n_ent.value, hi, lo
 
     def set_bank(self, k_re, k_im, dense: bool = False) -> None:
         lib = L.load()
@@ -263,44 +288,49 @@ class CqtLongEngine:
             sup = np.tile(np.array([0, self.width], dtype=np.int32), (self.n_bins, 1))
         else:
             sup = _row_support(kr, ki)
-        cap = lib.nnab_cqt_bank_tiles(self.n_bins) * (((self.width + 31) // 32 * 32) // 16) + 16
-        tab = np.zeros(cap, dtype=np.uint32)
-        n_ent = C.c_int32()
-        L.check(lib.nnab_cqt_schedule(sup.ctypes.data, self.n_bins, self.width, self.precision, tab.ctypes.data,
-                                      C.byref(n_ent)), "cqt_schedule")
-        self.n_entries = n_ent.value
-        tiles = lib.nnab_cqt_bank_tiles(self.n_bins)
-        self.schedule = torch.from_numpy(tab[: tiles * self.n_entries].astype(np.int32)).to(self.device)
         dr = torch.as_tensor(k_re).to(self.device, torch.float32).contiguous()
         di = torch.as_tensor(k_im).to(self.device, torch.float32).contiguous()
-        n = lib.nnab_cqt_bank_bytes(self.n_bins, self.width) // 4
-        self.packed_hi = torch.empty(n, dtype=torch.float32, device=self.device)
-        self.packed_lo = (torch.empty(n, dtype=torch.float32, device=self.device)
-                          if self.precision == L.PREC_3XTF32 else None)
-        L.check(lib.nnab_pack_cqt_bank(dr.data_ptr(), di.data_ptr(), self.n_bins, self.width, self.precision,
-                                       self.packed_hi.data_ptr(), L.ptr(self.packed_lo),
-                                       L.stream_handle(self.device)), "pack_cqt_bank")
-        # hop-offset GEMM ("E-GEMM", csrc/cqt1992_egemm.cu): TF32, hop a multiple of 32 (hop-row frames)
-        self.egemm = None
-        if self.method == "egemm" and self.precision == L.PREC_TF32 and self.hop == 512:
-            max_groups = 64
-            ct = np.zeros(max_groups * 256, dtype=np.uint16)
-            gr = np.zeros(max_groups * 64, dtype=np.int32)
-            rt = np.zeros(max_groups * 4 * 65, dtype=np.uint32)
-            ng, rm = C.c_int32(), C.c_int32()
-            rc = lib.nnab_cqt_egemm_plan(sup.ctypes.data, self.n_bins, self.width, self.hop, max_groups, ct.ctypes.data,
-                                         gr.ctypes.data, rt.ctypes.data, C.byref(ng), C.byref(rm))
-            if rc == L.OK:
-                n = ng.value
-                col_t = torch.from_numpy(ct[: n * 256].view(np.int16).copy()).to(self.device)
-                rows_t = torch.from_numpy(gr[: n * 64].copy()).to(self.device)
-                runs_t = torch.from_numpy(rt[: n * 4 * 65].view(np.int32).copy()).to(self.device)
-                bank = torch.empty(lib.nnab_cqt_egemm_bank_bytes(n, self.hop) // 4, dtype=torch.float32,
-                                   device=self.device)
-                L.check(lib.nnab_pack_cqt_egemm(dr.data_ptr(), di.data_ptr(), self.width, self.hop, col_t.data_ptr(),
-                                                rows_t.data_ptr(), n, self.precision, bank.data_ptr(), None,
-                                                L.stream_handle(self.device)), "pack_cqt_egemm")
-                self.egemm = (bank, col_t, rows_t, runs_t, n, rm.value)
+        self.schedule, self.n_entries, self.packed_hi, self.packed_lo = self._schedule(sup, dr, di)
+        self.egemm = self.hybrid = None
+        eg_ok = self.precision == L.PREC_TF32 and self.hop == 512 and kr is not None and not dense
+        if self.method == "hybrid" and eg_ok:
+            span = sup[:, 1] - sup[:, 0]
+            n_long = 0
+            while n_long < self.n_bins and span[n_long] >= self.LONG_HOPS * self.hop:
+                n_long += 1
+            eg = self._egemm_tables(sup[:n_long], dr[:n_long], di[:n_long]) if n_long else None
+            if n_long == self.n_bins:
+                self.egemm = eg
+            elif eg is not None:
+                sch, n_ent, hi, _ = self._schedule(sup[n_long:], dr[n_long:].contiguous(), di[n_long:].contiguous())
+                self.hybrid = (eg, sch, n_ent, hi, n_long)
+        elif self.method == "egemm" and eg_ok:
+            self.egemm = self._egemm_tables(sup, dr, di)
+
+    def _egemm_tables(self, sup, dr, di):
+        """Hop-offset GEMM ("E-GEMM", csrc/cqt1992_egemm.cu) tables and packed bank
+        for the rows in dr/di; None when the plan does not fit."""
+        lib = L.load()
+        max_groups = 64
+        ct = np.zeros(max_groups * 256, dtype=np.uint16)
+        gr = np.zeros(max_groups * 64, dtype=np.int32)
+        rt = np.zeros(max_groups * 4 * 65, dtype=np.uint32)
+        ng, rm = C.c_int32(), C.c_int32()
+        sup = np.ascontiguousarray(sup, dtype=np.int32)
+        rc = lib.nnab_cqt_egemm_plan(sup.ctypes.data, int(sup.shape[0]), self.width, self.hop, max_groups,
+                                     ct.ctypes.data, gr.ctypes.data, rt.ctypes.data, C.byref(ng), C.byref(rm))
+        if rc == L.OK:
+            n = ng.value
+            col_t = torch.from_numpy(ct[: n * 256].view(np.int16).copy()).to(self.device)
+            rows_t = torch.from_numpy(gr[: n * 64].copy()).to(self.device)
+            runs_t = torch.from_numpy(rt[: n * 4 * 65].view(np.int32).copy()).to(self.device)
+            bank = torch.empty(lib.nnab_cqt_egemm_bank_bytes(n, self.hop) // 4, dtype=torch.float32,
+                               device=self.device)
+            L.check(lib.nnab_pack_cqt_egemm(dr.data_ptr(), di.data_ptr(), self.width, self.hop, col_t.data_ptr(),
+                                            rows_t.data_ptr(), n, self.precision, bank.data_ptr(), None,
+                                            L.stream_handle(self.device)), "pack_cqt_egemm")
+            return (bank, col_t, rows_t, runs_t, n, rm.value)
+        return None
 
     def frames(self, B: int, length: int) -> L.nnab_frames:
         return frames_struct(B, length, self.width, self.hop, self.width // 2, self.pad_mode)
@@ -341,6 +371,14 @@ class CqtLongEngine:
             return out
         f = self.frames(B, length)
         ws = self._ws.buf
+        if self.hybrid is not None:
+            (bank, col_t, rows_t, _, n, rmax), sch, n_ent, s_hi, n_long = self.hybrid
+            L.check(lib.nnab_cqt1992v2_hybrid_staged(C.byref(f), bank.data_ptr(), col_t.data_ptr(), rows_t.data_ptr(),
+                                                     n, rmax, s_hi.data_ptr(), sch.data_ptr(), n_ent, n_long,
+                                                     self.n_bins, kinds[kind], float(eps), out.data_ptr(),
+                                                     ws.data_ptr(), ws.numel(), L.stream_handle(self.device)),
+                    "cqt1992v2_hybrid_staged")
+            return out
         if self.egemm is not None:
             bank, col_t, rows_t, runs_t, n, rmax = self.egemm
             rc = lib.nnab_cqt1992v2_egemm_staged(C.byref(f), bank.data_ptr(), col_t.data_ptr(), rows_t.data_ptr(),
@@ -371,6 +409,14 @@ class CqtLongEngine:
         f = self.frames(B, length)
         ws = self._ws.get(lib.nnab_cqt1992v2_host_scratch_bytes(C.byref(f), self.precision, self.n_bins, k,
                                                                  chunk_clips), self.device)
+        if self.hybrid is not None:
+            (bank, col_t, rows_t, _, n, rmax), sch, n_ent, s_hi, n_long = self.hybrid
+            L.check(lib.nnab_cqt1992v2_hybrid_forward_host(
+                C.byref(f), x_host.data_ptr(), bank.data_ptr(), col_t.data_ptr(), rows_t.data_ptr(), n, rmax,
+                s_hi.data_ptr(), sch.data_ptr(), n_ent, n_long, self.n_bins, k, float(eps), out_host.data_ptr(),
+                int(chunk_clips), ws.data_ptr(), ws.numel(), L.stream_handle(self.device)),
+                "cqt1992v2_hybrid_forward_host")
+            return out_host
         L.check(lib.nnab_cqt1992v2_forward_host(
             C.byref(f), x_host.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins,
             self.schedule.data_ptr(), self.n_entries, self.precision, k, float(eps), out_host.data_ptr(),

@@ -111,7 +111,14 @@ def test_cqt_host_paths_match_device(cuda_dev):
     want = e1.forward(x.to(cuda_dev)).cpu()
     got = e1.forward_host(xh, chunk_clips=3)
     torch.cuda.synchronize()
-    assert torch.equal(got, want)
+    # the hybrid's E-GEMM sums each output's hop-offset terms in an order set by
+    # the slot's position in its 128-slot tile, which moves with the chunking
+    assert O.peak_err(got.numpy(), want.numpy()) < 1e-6
+    e1s = long_engine(cfg, "tf32", method="schedule")
+    want_s = e1s.forward(x.to(cuda_dev)).cpu()
+    got_s = e1s.forward_host(xh, chunk_clips=3)
+    torch.cuda.synchronize()
+    assert torch.equal(got_s, want_s)
     e2 = rec_engine(cfg, "tf32")
     want2 = e2.forward(x.to(cuda_dev)).cpu()
     got2 = e2.forward_host(xh, chunk_clips=3)
@@ -146,17 +153,35 @@ def test_cqt2010v2_fp16_scaling_robust(cuda_dev, case):
     assert O.peak_err(got, ref) <= TOL["tf32"], O.peak_err(got, ref)
 
 
-def test_cqt1992v2_egemm_matches_schedule(golden, cuda_dev):
-    """The hop-offset GEMM (csrc/cqt1992_egemm.cu) and the per-K-block schedule
-    (csrc/cqt1992.cu) compute the same TF32 correlation in different orders."""
+@pytest.mark.parametrize("method", ["egemm", "hybrid"])
+def test_cqt1992v2_egemm_matches_schedule(golden, cuda_dev, method):
+    """The hop-offset GEMM (csrc/cqt1992_egemm.cu), alone or for the long bins
+    of the hybrid, and the per-K-block schedule (csrc/cqt1992.cu) compute the
+    same TF32 correlation in different orders."""
     cfg = O.CqtCfg(sr=SR)
     x = torch.from_numpy(golden["clips"]).to(cuda_dev)
-    a = long_engine(cfg, "tf32", method="egemm")
-    assert a.egemm is not None
+    a = long_engine(cfg, "tf32", method=method)
+    if method == "egemm":
+        assert a.egemm is not None
+    else:
+        assert a.hybrid is not None and 0 < a.hybrid[-1] < cfg.n_bins
     b = long_engine(cfg, "tf32", method="schedule")
-    for kind in ("magnitude", "complex"):
+    for kind in ("magnitude", "power", "complex"):
         ga, gb = a.forward(x, kind).cpu().numpy(), b.forward(x, kind).cpu().numpy()
-        assert O.peak_err(ga, gb) < 5e-4
+        assert O.peak_err(ga, gb) < 5e-4, (kind, O.peak_err(ga, gb))
+    # the long bins' E-GEMM output lands in rows [0, n_long), the schedule's after them
+    if method == "hybrid":
+        n_long = a.hybrid[-1]
+        ga, gb = a.forward(x).cpu().numpy(), b.forward(x).cpu().numpy()
+        for rows in (slice(0, n_long), slice(n_long, cfg.n_bins)):
+            assert O.peak_err(ga[:, rows], gb[:, rows]) < 5e-4
+
+
+def test_cqt1992v2_default_is_hybrid(cuda_dev):
+    cfg = O.CqtCfg(sr=SR)
+    e = long_engine(cfg, "tf32")
+    assert e.hybrid is not None
+    assert long_engine(cfg, "3xtf32").hybrid is None  # FP32-accurate mode: schedule only
 
 
 def test_frequency_domain_variants_golden(golden, cuda_dev):
