@@ -34,6 +34,7 @@
 // run (a 1-in-~150 overlap) so its last D rows are complete; D rows before its
 // run belong to the previous CTA.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -44,8 +45,7 @@ namespace nnab {
 namespace {
 
 constexpr int kBM = 128, kBN = 256, kBK = 32, kThreads = 256;
-constexpr int kStages = 3;
-constexpr int kA = kBM * kBK * 4, kB = kBN * kBK * 4, kStage = kA + kB;  // 16 + 32 KB
+constexpr int kA = kBM * kBK * 4;  // 16 KB A tile per stage
 constexpr int kRows = 16;   // D rows (bank rows: 2 per bin) per group
 constexpr int kRing = 256;  // D ring length (slots, power of two); >= 128 + max r
 constexpr uint16_t kUnused = 0xFFFF;
@@ -77,11 +77,31 @@ NNAB_DEV uint64_t sdesc(const void* p) {  // K-major, 128-byte swizzle, 8-row at
 }
 
 NNAB_DEV void ep_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // epilogue warps 4-7
-// ring slot of D row d (d >= -64): rows are offset by one ring length to stay non-negative
 
+// Pipeline geometry: single CTAs stage A (16 KB) + all of B (32 KB) x 3; a CTA
+// pair (kPair) stages A + half of B (16 + 16 KB) x 4.
+template <bool kPair>
+struct ECfg {
+  static constexpr int STAGES = kPair ? 4 : 3;
+  static constexpr int B_ROWS = kPair ? kBN / 2 : kBN;
+  static constexpr int STAGE = kA + B_ROWS * kBK * 4;
+};
+template <bool kPair>
+constexpr size_t egemm_smem() {
+  return 1024 + (size_t)ECfg<kPair>::STAGES * ECfg<kPair>::STAGE + (size_t)4 * kRows * kRing * 4 + kBN * 2 +
+         kRows * 4 + 16 * 8;
+}
+
+// kPair: a cluster of two CTAs of the same group runs two independent tile runs
+// in lockstep with cta_group::2 MMAs (M = 256: each CTA's A tile, the group's
+// B columns split between them), ~25 % more MMA throughput per SM; each CTA's
+// epilogue and D rings stay its own.
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     cqt1992_egemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                          const EParams p) {
+  using EC = ECfg<kPair>;
+  constexpr int kStages = EC::STAGES, kStage = EC::STAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* ring = reinterpret_cast<float*>(smem + kStages * kStage);  // [4 warps][kRows][kRing]
@@ -95,12 +115,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x / p.ctas_per_group, gi = blockIdx.x % p.ctas_per_group;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0;
+  const int g = blockIdx.x / p.ctas_per_group, gi = blockIdx.x % p.ctas_per_group;  // pairs: consecutive CTAs
   const bool active = g < p.n_groups;
-  // this CTA's run of M tiles, plus one extra tile past it
+  // this CTA's run of M tiles, plus one extra tile past it.  A pair runs both of
+  // its runs in lockstep, so it always walks per + 1 tiles (tiles past the data
+  // are zero-filled by TMA and emit nothing).
   const int per = (p.n_mtiles + p.ctas_per_group - 1) / p.ctas_per_group;
-  const int m_a = min(p.n_mtiles, gi * per), m_b = min(p.n_mtiles, m_a + per);
-  const int m_end = min(p.n_mtiles, m_b + 1);
+  const int m_a = kPair ? gi * per : min(p.n_mtiles, gi * per);
+  const int m_b = kPair ? m_a + per : min(p.n_mtiles, m_a + per);
+  const int m_end = kPair ? m_b + 1 : min(p.n_mtiles, m_b + 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -109,11 +133,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kPair ? 8 : 4);  // pair: the leader's counts both CTAs' epilogue warps
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tslot);
+  if (kPair) cluster_sync();
+  if (warp == 2) {
+    if (kPair) tmem_alloc_pair<512>(tslot);
+    else tmem_alloc<512>(tslot);
+  }
   for (int i = threadIdx.x; i < 4 * kRows * kRing; i += kThreads) ring[i] = 0.f;
   if (active) {
     for (int i = threadIdx.x; i < kBN; i += kThreads) cols[i] = p.col_table[g * kBN + i];
@@ -135,9 +163,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < 16; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             uint8_t* st = smem + s * kStage;
-            mbar_expect_tx(&full[s], kStage);
-            tma_load_2d_hint(st, &tm_a, &full[s], kb * kBK, m * kBM, keep);
-            tma_load_2d_hint(st + kA, &tm_b, &full[s], kb * kBK, g * kBN, keep);
+            if (kPair) {  // both CTAs' bytes complete on the leader's barrier
+              const uint32_t fb = mapa(&full[s], 0);
+              if (rank == 0) mbar_expect_tx(&full[s], 2 * kStage);
+              tma_load_2d_pair(st, &tm_a, fb, kb * kBK, m * kBM, keep);
+              tma_load_2d_pair(st + kA, &tm_b, fb, kb * kBK, g * kBN + (int)rank * EC::B_ROWS, keep);
+            } else {
+              mbar_expect_tx(&full[s], kStage);
+              tma_load_2d_hint(st, &tm_a, &full[s], kb * kBK, m * kBM, keep);
+              tma_load_2d_hint(st + kA, &tm_b, &full[s], kb * kBK, g * kBN, keep);
+            }
             if (++s == kStages) {
               s = 0;
               ph ^= 1;
@@ -147,8 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     } else if (warp == 1) {
       // -------------------------------------------------------------- MMA issuer
-      if (elect_one()) {
-        constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
+      if (rank == 0 && elect_one()) {
+        constexpr uint32_t idesc = idesc_tf32(kPair ? 2 * kBM : kBM, kBN);
         int s = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
         for (int m = m_a; m < m_end; ++m) {
@@ -161,14 +196,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* st = smem + s * kStage;
             const uint64_t a = sdesc(st), b = sdesc(st + kA);
 #pragma unroll
-            for (int k = 0; k < kBK / 8; ++k) mma_tf32(d, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
-            mma_commit(&empty[s]);
+            for (int k = 0; k < kBK / 8; ++k) {
+              if (kPair) mma_tf32_pair(d, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
+              else mma_tf32(d, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
+            }
+            if (kPair) mma_commit_pair(&empty[s], 0x3);
+            else mma_commit(&empty[s]);
             if (++s == kStages) {
               s = 0;
               ph ^= 1;
             }
           }
-          mma_commit(&tfull[acc]);
+          if (kPair) mma_commit_pair(&tfull[acc], 0x3);
+          else mma_commit(&tfull[acc]);
           if (++acc == 2) {
             acc = 0;
             aph ^= 1;
@@ -229,7 +269,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if (kPair) mbar_arrive_cluster(mapa(&tempty[acc], 0));
+          else mbar_arrive(&tempty[acc]);
+        }
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
@@ -272,8 +315,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync();  // the leader's MMAs write the peer's TMEM until the end
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<512>(tmem);
+  if (warp == 2) {
+    if (kPair) tmem_dealloc_pair<512>(tmem);
+    else tmem_dealloc<512>(tmem);
+  }
 }
 
 __global__ void pack_egemm_kernel(const float* __restrict__ k_re, const float* __restrict__ k_im, int32_t width,
@@ -423,10 +470,17 @@ static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const 
   if (!workspace || workspace_bytes < nnab_stft_workspace_bytes(f, NNAB_PREC_TF32)) return NNAB_EINVAL;
   const int nsm = num_sms();
   if (n_groups > nsm) return NNAB_ENOTSUP;
+  static const bool pair_ok = [] {
+    const char* e = getenv("NNAB_EGEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  const bool pair = pair_ok && nsm / n_groups >= 2;
   CUtensorMap ta, tb;
   const uint64_t rows_total = (uint64_t)g.B * g.R;
   rc = make_tmap_2d(&ta, workspace, g.row_len, rows_total, (uint64_t)g.row_len * 4, kBK, kBM, 128);
-  if (!rc) rc = make_tmap_2d(&tb, packed_hi, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * 4, kBK, kBN, 128);
+  if (!rc)
+    rc = make_tmap_2d(&tb, packed_hi, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * 4, kBK, pair ? kBN / 2 : kBN,
+                      128);
   if (rc) return rc;
   EParams p{};
   p.B = g.B;
@@ -436,15 +490,36 @@ static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const 
   p.n_bins = out_bins;
   p.out_kind = out_kind;
   p.n_groups = n_groups;
-  p.ctas_per_group = nsm / n_groups;
+  p.ctas_per_group = pair ? nsm / n_groups / 2 * 2 : nsm / n_groups;
   p.r_max = r_max;
   p.eps = eps;
   p.col_table = col_table;
   p.group_rows = group_rows;
   p.out = out;
-  const size_t smem = 1024 + (size_t)kStages * kStage + (size_t)4 * kRows * kRing * 4 + kBN * 2 + kRows * 4 + 16 * 8;
-  NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt1992_egemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  cqt1992_egemm_kernel<<<p.ctas_per_group * n_groups, kThreads, smem, stream>>>(ta, tb, p);
+  const int grid = p.ctas_per_group * n_groups;
+  if (!pair) {
+    const size_t smem = egemm_smem<false>();
+    NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt1992_egemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    cqt1992_egemm_kernel<false><<<grid, kThreads, smem, stream>>>(ta, tb, p);
+  } else {
+    const size_t smem = egemm_smem<true>();
+    NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt1992_egemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    NNAB_CUDA_TRY(cudaLaunchKernelEx(&cfg, cqt1992_egemm_kernel<true>, ta, tb, p));
+  }
   NNAB_LAUNCHED();
   return NNAB_OK;
 }

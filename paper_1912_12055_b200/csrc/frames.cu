@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
   const int32_t q_per_row = row_len / 4;
   const int64_t rows = B * (int64_t)R;
   const bool aligned_clips = (L % 4) == 0 && (pad % 4) == 0 && (hop % 4) == 0;
+  const bool x_aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   const int per = q_per_row < (int)blockDim.x ? q_per_row : (int)blockDim.x;  // threads per row
   const int rpb = blockDim.x / per;                                           // rows per block step
   const int sub = threadIdx.x / per, lane = threadIdx.x - sub * per;
@@ -69,12 +70,22 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
       const int64_t i0 = r * hop + 4 * q;  // padded position of the first sample
       const int64_t j0 = i0 - pad;         // source sample
       float v[4];
+      const int64_t ga = b * L + j0;  // absolute source index
       if (aligned_clips && j0 >= 0 && j0 + 3 < L && i0 + 3 < padded_len) {
         const float4 w = __ldg(reinterpret_cast<const float4*>(xb + j0));
         v[0] = w.x;
         v[1] = w.y;
         v[2] = w.z;
         v[3] = w.w;
+      } else if (x_aligned && j0 >= 0 && j0 - (ga & 3) + 7 < L && i0 + 3 < padded_len) {
+        // interior of a clip whose rows start off a 16-byte boundary (e.g. the CQT
+        // pad of 11,341): two aligned loads and a funnel by the misalignment
+        const float4* a4 = reinterpret_cast<const float4*>(x + (ga & ~int64_t(3)));
+        const float4 w0 = __ldg(a4), w1 = __ldg(a4 + 1);
+        const float e[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        const int m = (int)(ga & 3);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = m == 0 ? e[u] : m == 1 ? e[u + 1] : m == 2 ? e[u + 2] : e[u + 3];
       } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
