@@ -164,7 +164,7 @@ def build_workload(name: str, device, precision: str):
         k, lens = banks.cqt_time_kernels(SR, cfg.bin_freqs_hz, 12, "hann", 1)
         eng = CqtLongEngine(k, 512, "reflect", precision=precision, device=device)
         work = {"bound": "tensor", "per_batch": 4.0 * M_FRAMES * float(lens.sum()), "unit": "TFLOP/s",
-                "kernel": "stft_gemm_kernel"}
+                "kernel": "cqt1992 hybrid (egemm + schedule)"}
         return eng, "magnitude", work, 2
     if name == "train":
         import torch.distributed as dist
