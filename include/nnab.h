@@ -135,7 +135,11 @@ int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const floa
 int64_t nnab_slots_ld(const nnab_frames* f);
 /* Training forward on staged frames: out = smoothed magnitude sqrt(re^2+im^2+eps)
  * (NNAB_OUT_SMOOTH_MAG, gradients.py:61-67) or W @ that (NNAB_OUT_MEL,
- * gradients.py:69-80); also stores re, im and (if save_mag) S, slot-major. */
+ * gradients.py:69-80); also stores re, im and (if save_mag) S, slot-major.
+ * TF32 only: save_im = NULL stores the unit phasor (re/S, im/S) instead, as
+ * packed FP16 pairs (one 32-bit word per (bin, slot) in save_re) -- all the
+ * backward's coef step needs; nnab_dft_coef / nnab_mel_dft_coef then take
+ * im_s = NULL and re_s = that phasor array. */
 int nnab_stft_forward_train_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
                                    int32_t n_bins, int32_t fold_nyquist, int32_t precision, int32_t out_kind,
                                    float power, float eps, const float* mel_w, int32_t n_mels, int32_t mel_ld,

@@ -67,7 +67,10 @@ class DftLayerOp:
         ld = lib.nnab_slots_ld(C.byref(f))
         F = self.n_bins
         R = self._rows_per_clip(length)
-        re_s, im_s = _f32(F, ld, self.device), _f32(F, ld, self.device)
+        # TF32: the backward only needs the unit phasor (re/S, im/S), saved as FP16
+        # pairs in one 32-bit word per (bin, slot); 3xTF32 keeps re and im in FP32
+        re_s = _f32(F, ld, self.device)
+        im_s = _f32(F, ld, self.device) if self.split else None
         mag_s = _f32(F, ld, self.device) if mel_w is not None else None
         # mel layer: the STFT GEMM only saves re/im/S per slot; W @ S then runs as a
         # tcgen05 GEMM (a trained W is dense, so the epilogue's banded CUDA-core path
@@ -75,7 +78,7 @@ class DftLayerOp:
         out = None if mel_w is not None else torch.empty(B, F, T, device=self.device)
         L.check(lib.nnab_stft_forward_train_staged(
             C.byref(f), eng.packed_hi.data_ptr(), L.ptr(eng.packed_lo), F, eng.fold, self.prec, L.OUT_SMOOTH_MAG,
-            1.0, self.eps, None, 0, 0, None, L.ptr(out), re_s.data_ptr(), im_s.data_ptr(), L.ptr(mag_s), ld,
+            1.0, self.eps, None, 0, 0, None, L.ptr(out), re_s.data_ptr(), L.ptr(im_s), L.ptr(mag_s), ld,
             ws.data_ptr(), ws.numel(), stream), "stft_forward_train")
         saved = {"ws": ws, "re": re_s, "im": im_s, "mag": mag_s, "B": B, "L": length, "T": T, "ld": ld, "R": R}
         if mel_w is not None:
@@ -146,7 +149,7 @@ class DftLayerOp:
                 coef_hi = _f32(2 * F, ld, self.device)
                 coef_lo = _f32(2 * F, ld, self.device) if self.split else None
                 L.check(lib.nnab_mel_dft_coef(F, ld, kp, wt_hi.data_ptr(), L.ptr(wt_lo), gsp[0].data_ptr(),
-                                              L.ptr(gsp[1]), nm, saved["re"].data_ptr(), saved["im"].data_ptr(),
+                                              L.ptr(gsp[1]), nm, saved["re"].data_ptr(), L.ptr(saved["im"]),
                                               self.eps, self.prec, coef_hi.data_ptr(), L.ptr(coef_lo), stream),
                         "mel_dft_coef")
                 ds = True
@@ -155,7 +158,7 @@ class DftLayerOp:
         if ds is None:
             coef_hi = _f32(2 * F, ld, self.device)
             coef_lo = _f32(2 * F, ld, self.device) if self.split else None
-            L.check(lib.nnab_dft_coef(None, g.data_ptr(), saved["re"].data_ptr(), saved["im"].data_ptr(), F, B, T,
+            L.check(lib.nnab_dft_coef(None, g.data_ptr(), saved["re"].data_ptr(), L.ptr(saved["im"]), F, B, T,
                                       R, ld, self.eps, self.prec, coef_hi.data_ptr(), L.ptr(coef_lo), stream),
                     "dft_coef")
         ws = saved["ws"]

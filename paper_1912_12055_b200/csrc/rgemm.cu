@@ -14,6 +14,8 @@
 //
 // Warp roles as in stft_gemm.cu: TMA producer, MMA issuer, TMEM allocator,
 // 4 epilogue warps (thread = output row).
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -46,7 +48,7 @@ struct RParams {
   int32_t b_mn, b_row_len;
   float* C;             // [splits][M][ldc]
   int64_t ldc, split_stride;
-  const float *re, *im;  // coef epilogue (RGemmArgs::coef_re): C is coef_hi
+  const float *re, *im;  // coef epilogue (RGemmArgs::coef_re): C is coef_hi; im null: re holds FP16 phasor pairs
   float* c_lo;
   float eps;
 };
@@ -300,7 +302,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4 d[8];
 #pragma unroll
           for (int it = 0; it < 8; ++it) d[it] = *reinterpret_cast<const float4*>(stg + (it * 4 + sr) * kStg + sc);
-          if (p.re) {  // coef epilogue: the dS tile never leaves the SM
+          if (p.re && !p.im) {  // coef epilogue from the saved unit phasor (re/S, im/S) in FP16 pairs
+            uint4 ph[8];
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int m = m_base + it * 4 + sr;
+              if (m < p.M && full4)
+                ph[it] = __ldcs(reinterpret_cast<const uint4*>(p.re + (int64_t)m * p.ldc + n));  // read once
+            }
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int m = m_base + it * 4 + sr;
+              if (m >= p.M) continue;
+              const int64_t o = (int64_t)m * p.ldc + n, o2 = o + (int64_t)p.M * p.ldc;
+              if (full4) {
+                const __half2* h2 = reinterpret_cast<const __half2*>(&ph[it]);
+                const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]), f2 = __half22float2(h2[2]),
+                             f3 = __half22float2(h2[3]);
+                const float4 hr = make_float4(d[it].x * f0.x, d[it].y * f1.x, d[it].z * f2.x, d[it].w * f3.x);
+                const float4 hi = make_float4(d[it].x * f0.y, d[it].y * f1.y, d[it].z * f2.y, d[it].w * f3.y);
+                __stcs(reinterpret_cast<float4*>(p.C + o), tf32_hi4(hr));
+                __stcs(reinterpret_cast<float4*>(p.C + o2), tf32_hi4(hi));
+              } else {
+                const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  if (n + j >= p.N) continue;
+                  const float2 f = __half22float2(reinterpret_cast<const __half2*>(p.re)[o + j]);
+                  p.C[o + j] = tf32_rne(dv[j] * f.x);
+                  p.C[o2 + j] = tf32_rne(dv[j] * f.y);
+                }
+              }
+            }
+          } else if (p.re) {  // coef epilogue: the dS tile never leaves the SM
             float4 rr[8], ii[8];
 #pragma unroll
             for (int it = 0; it < 8; ++it) {

@@ -20,6 +20,8 @@
 //   warp 1      MMA issuer (one elected lane)
 //   warp 2      TMEM allocator
 //   warps 4..7  epilogue: thread = accumulator row = one frame slot
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -344,19 +346,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int bin = bin0 + j;
                 if (bin < F - p.fold) {
                   const int64_t o = (int64_t)bin * p.ld_slots + slot;
-                  p.save_re[o] = re[j];
-                  p.save_im[o] = im[j];
-                  if (p.save_mag) {  // GEMM operand of dW: TF32-rounded in TF32 mode, fp32 (split later) in 3xTF32
-                    const float s = sqrtf(fmaf(re[j], re[j], im[j] * im[j]) + p.eps);
-                    p.save_mag[o] = kSplit ? s : tf32_rne(s);
+                  const float pw = fmaf(re[j], re[j], im[j] * im[j]) + p.eps;
+                  if (p.save_im) {
+                    p.save_re[o] = re[j];
+                    p.save_im[o] = im[j];
+                  } else {  // TF32: the unit phasor (re/S, im/S) as packed FP16 (what coef needs)
+                    const float inv = rsqrtf(pw);
+                    const __half2 ph = __floats2half2_rn(re[j] * inv, im[j] * inv);
+                    reinterpret_cast<__half2*>(p.save_re)[o] = ph;
                   }
+                  if (p.save_mag)  // GEMM operand of dW: TF32-rounded in TF32 mode, fp32 (split later) in 3xTF32
+                    p.save_mag[o] = kSplit ? sqrtf(pw) : tf32_rne(fast_sqrt(pw));
                 }
               }
               if (p.fold && n == 0 && c == 0) {
                 const int64_t o = (int64_t)(F - 1) * p.ld_slots + slot;
-                p.save_re[o] = nyq_re;
-                p.save_im[o] = 0.f;
-                if (p.save_mag) p.save_mag[o] = sqrtf(nyq_re * nyq_re + p.eps);
+                const float pw = nyq_re * nyq_re + p.eps;
+                if (p.save_im) {
+                  p.save_re[o] = nyq_re;
+                  p.save_im[o] = 0.f;
+                } else {
+                  reinterpret_cast<__half2*>(p.save_re)[o] = __floats2half2_rn(nyq_re * rsqrtf(pw), 0.f);
+                }
+                if (p.save_mag) p.save_mag[o] = kSplit ? sqrtf(pw) : tf32_rne(fast_sqrt(pw));
               }
             }
           }
@@ -470,7 +482,8 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.save_im = a.save_im;
   p.save_mag = a.save_mag;
   p.ld_slots = a.ld_slots;
-  if (a.save_re && (!a.save_im || a.pairs)) return NNAB_EINVAL;
+  if (a.save_re && a.pairs) return NNAB_EINVAL;
+  if (a.save_re && !a.save_im && kSplit) return NNAB_EINVAL;  // phasor saves: TF32 only
   p.n_tab = a.n_tab;
   p.b_box = b_box;
   p.pairs = a.pairs;

@@ -10,6 +10,8 @@
 //   input grad  (gradients.py:133-149):  frame grads = coef^T @ h, overlap-add, fold pad
 // All products run on the tcgen05 reduction GEMM (rgemm.cu); the glue here is
 // elementwise and HBM-bound.
+#include <cuda_fp16.h>
+
 #include <algorithm>
 
 #include "internal.h"
@@ -58,9 +60,17 @@ __global__ void coef_kernel(const float* __restrict__ ds_slots, const float* __r
     const int t = (int)(slot - b * R);
     float d = 0.f;
     if (b < B && t < T) d = ds_slots ? ds_slots[e] : g_bft[(b * F + f) * (int64_t)T + t];
-    const float r = re[e], i = im[e];
-    const float di = d * rsqrtf(fmaf(r, r, i * i) + eps);  // as rgemm.cu coef_store
-    const float cr = di * r, ci = di * i;
+    float cr, ci;
+    if (im) {
+      const float r = re[e], i = im[e];
+      const float di = d * rsqrtf(fmaf(r, r, i * i) + eps);  // as rgemm.cu coef_store
+      cr = di * r;
+      ci = di * i;
+    } else {  // re holds the unit phasor (re/S, im/S) as FP16 pairs (TF32 training forward)
+      const float2 ph = __half22float2(reinterpret_cast<const __half2*>(re)[e]);
+      cr = d * ph.x;
+      ci = d * ph.y;
+    }
     const float hr = tf32_rne(cr), hi_ = tf32_rne(ci);
     hi[e] = hr;
     hi[e + (int64_t)F * ld] = hi_;
@@ -157,7 +167,7 @@ extern "C" int nnab_stft_forward_train_staged(const nnab_frames* f, const float*
   if (rc) return rc;
   if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
   const int split = precision == NNAB_PREC_3XTF32;
-  if (!packed_hi || (split && !packed_lo) || !save_re || !save_im) return NNAB_EINVAL;
+  if (!packed_hi || (split && !packed_lo) || !save_re || (split && !save_im)) return NNAB_EINVAL;
   if (out_kind != NNAB_OUT_SMOOTH_MAG && out_kind != NNAB_OUT_MEL) return NNAB_EINVAL;
   if (!out && out_kind != NNAB_OUT_SMOOTH_MAG) return NNAB_EINVAL;  // out may be null: save slots only
   if (out_kind == NNAB_OUT_MEL && (!mel_w || n_mels < 1)) return NNAB_EINVAL;
@@ -211,8 +221,9 @@ extern "C" int nnab_from_slots(const float* src, int64_t B, int32_t rows, int32_
 extern "C" int nnab_dft_coef(const float* ds_slots, const float* g_bft, const float* re_s, const float* im_s,
                              int32_t F, int64_t B, int32_t T, int32_t R, int64_t ld, float eps, int32_t precision,
                              float* coef_hi, float* coef_lo, void* stream) {
-  if ((!ds_slots && !g_bft) || !re_s || !im_s || !coef_hi || F < 1 || ld < B * R) return NNAB_EINVAL;
+  if ((!ds_slots && !g_bft) || !re_s || !coef_hi || F < 1 || ld < B * R) return NNAB_EINVAL;
   const int split = precision == NNAB_PREC_3XTF32;
+  if (!im_s && split) return NNAB_EINVAL;  // phasor input: TF32 only
   if (split && !coef_lo) return NNAB_EINVAL;
   const int64_t total = (int64_t)F * ld;
   coef_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(ds_slots, g_bft, re_s, im_s, F, B, T, R, ld, eps,
@@ -282,9 +293,8 @@ extern "C" int nnab_mel_dft_coef(int32_t F, int64_t ld, int32_t kp, const float*
                                  const float* gs_hi, const float* gs_lo, int32_t n_mels, const float* re_s,
                                  const float* im_s, float eps, int32_t precision, float* coef_hi, float* coef_lo,
                                  void* stream) {
-  if (F < 1 || ld < 1 || kp < n_mels || n_mels < 1 || !wt_hi || !gs_hi || !re_s || !im_s || !coef_hi)
-    return NNAB_EINVAL;
-  if (precision == NNAB_PREC_3XTF32 && (!wt_lo || !gs_lo || !coef_lo)) return NNAB_EINVAL;
+  if (F < 1 || ld < 1 || kp < n_mels || n_mels < 1 || !wt_hi || !gs_hi || !re_s || !coef_hi) return NNAB_EINVAL;
+  if (precision == NNAB_PREC_3XTF32 && (!wt_lo || !gs_lo || !coef_lo || !im_s)) return NNAB_EINVAL;
   if (ld > INT32_MAX) return NNAB_EINVAL;
   if (kp > 1024) return NNAB_ENOTSUP;  // one TMEM accumulation chain per tile
   RGemmArgs g;

@@ -10,7 +10,8 @@ fn.restype = C.c_int; fn.argtypes = [C.c_int, C.c_void_p]
 dev = torch.device("cuda:0")
 p = cqt2010_plan(CqtConfig(sr=44100.0))
 eng = Cqt2010Engine(p["taps"], p["top_kernels"], p["early_stages"], p["n_octaves"], p["kernel_hop"], p["first_bin"], 12, 84, "reflect", device=dev)
-x = torch.randn(1770, 80000, device=dev) * 0.5
+NB = int(sys.argv[1]) if len(sys.argv) > 1 else 1770
+x = torch.randn(NB, 80000, device=dev) * 0.5
 eng.forward(x); torch.cuda.synchronize()
 fn(1, None)
 eng.forward(x); torch.cuda.synchronize()
@@ -20,4 +21,4 @@ names = ["S1 build", "S1 mma", "S1 epi", "FIR issue", "S2 mma", "S2 epi", "frame
          "halving epi", "im2col sync", "conv mma wait", "conv epi", "wait scale", "bulk wait", "conv epi sync", "tail"]
 tot = sum(out)
 for n, v in zip(names, out):
-    print(f"{n:18s} {v/1770:10.0f} cycles/clip  {100*v/tot:5.1f}%")
+    print(f"{n:18s} {v/NB:10.0f} cycles/clip  {100*v/tot:5.1f}%")
