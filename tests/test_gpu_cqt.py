@@ -198,3 +198,23 @@ def test_frequency_domain_variants_golden(golden, cuda_dev):
     short = S.Signal(golden["x22"][:1000].astype(np.float32), 22050.0, device="cuda:0")  # fft_len 2048 > 2 * 1000 > width 1686
     with pytest.raises(ValueError):
         c1(short)
+
+
+@pytest.mark.parametrize("fmin,n_bins,bpo,length,batch", [
+    (32.70, 84, 12, 30000, 3),     # short clips: fewer hop rows than an M tile per clip
+    (55.0, 60, 12, 80001, 2),      # odd length, shorter bank
+    (27.5, 96, 24, 50000, 1),      # 24 bins per octave: many long bins, one clip
+])
+def test_cqt1992v2_hybrid_shapes(cuda_dev, fmin, n_bins, bpo, length, batch):
+    """Hybrid (E-GEMM long bins + schedule short bins) against the schedule on
+    other banks, ragged lengths and small batches (E-GEMM CTA pairs then walk
+    tiles past the data, which must emit nothing)."""
+    cfg = O.CqtCfg(sr=SR, fmin=fmin, n_bins=n_bins, bins_per_octave=bpo)
+    rng = np.random.default_rng(11)
+    x = torch.from_numpy((rng.standard_normal((batch, length)) * 0.5).astype(np.float32)).to(cuda_dev)
+    a = long_engine(cfg, "tf32")
+    b = long_engine(cfg, "tf32", method="schedule")
+    for kind in ("magnitude", "complex"):
+        ga, gb = a.forward(x, kind).cpu().numpy(), b.forward(x, kind).cpu().numpy()
+        assert np.isfinite(ga).all()
+        assert O.peak_err(ga, gb) < 5e-4, (kind, O.peak_err(ga, gb))
