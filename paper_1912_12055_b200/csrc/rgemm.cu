@@ -277,8 +277,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t tb = tbase + ((q * 32) << 16) + (NACC > 1 ? acc * C::ACC_STRIDE : 0);
+        // phasor coef epilogue: chunk c + 1's phasor loads are in flight while chunk c
+        // is drained (the epilogue is HBM-latency bound with 4 warps per SM)
+        const bool phasor = p.re && !p.im;
+        uint4 ph_cur[8], ph_nxt[8];
+        auto load_ph = [&](int c, uint4* dst) {
+          const int n = nt * TBN + c * 32 + sc;
+          const bool full4 = vec && n + 4 <= p.N;
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int m = m_base + it * 4 + sr;
+            if (m < p.M && full4) dst[it] = __ldcs(reinterpret_cast<const uint4*>(p.re + (int64_t)m * p.ldc + n));
+          }
+        };
+        if (phasor) load_ph(0, ph_cur);
 #pragma unroll 1
         for (int c = 0; c < TBN / 32; ++c) {
+          if (phasor && c + 1 < TBN / 32) load_ph(c + 1, ph_nxt);
           float v[32];
           tmem_ld32(tb + c * 32, v);
           if (kSplit) {
@@ -297,18 +312,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           __syncwarp();
           const int n = nt * TBN + c * 32 + sc;
-          if (n >= p.N || m_base >= p.M) continue;
+          if (n >= p.N || m_base >= p.M) {
+            if (phasor) {
+#pragma unroll
+              for (int it = 0; it < 8; ++it) ph_cur[it] = ph_nxt[it];
+            }
+            continue;
+          }
           const bool full4 = vec && n + 4 <= p.N;
           float4 d[8];
 #pragma unroll
           for (int it = 0; it < 8; ++it) d[it] = *reinterpret_cast<const float4*>(stg + (it * 4 + sr) * kStg + sc);
-          if (p.re && !p.im) {  // coef epilogue from the saved unit phasor (re/S, im/S) in FP16 pairs
+          if (phasor) {  // coef epilogue from the saved unit phasor (re/S, im/S) in FP16 pairs
             uint4 ph[8];
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
-              const int m = m_base + it * 4 + sr;
-              if (m < p.M && full4)
-                ph[it] = __ldcs(reinterpret_cast<const uint4*>(p.re + (int64_t)m * p.ldc + n));  // read once
+              ph[it] = ph_cur[it];
+              ph_cur[it] = ph_nxt[it];
             }
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
