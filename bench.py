@@ -395,7 +395,8 @@ def main():
             et = float(t.item())
         e2e = {"value": world * B_CLIPS / (et / 1e3), "unit": "spectrograms/s", "ms_per_step": et,
                "h2d_bytes_per_step": B_CLIPS * L_SAMPLES * 4, "d2h_bytes_per_step": B_CLIPS * 84 * T_FRAMES * 4,
-               "path": f"nnab_{args.workload}_forward_host (C ABI, pinned host buffers, 12 chunks, 3-stream overlap)"}
+               "path": ("nnab_cqt1992v2_hybrid_forward_host" if args.workload == "cqt1992v2" else
+                        "nnab_cqt2010v2_forward_host") + " (C ABI, pinned host buffers, 12 chunks, 3-stream overlap)"}
         del xh, oh
     elif args.workload == "train":
         # pinned host batch -> device, fwd + bwd (+ all-reduce), kernel grads -> host, every step
