@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             rrow[(s_row - r0) & (kRing - 1)] += hi;
             rrow[(s_row - 32 - r0) & (kRing - 1)] += lo;
+            __syncwarp();  // the next window's cells overlap other lanes' cells of this one
           }
         }
         tc_fence_before();
