@@ -128,6 +128,20 @@ int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const floa
                            int32_t mel_ld, const int32_t* mel_band, float* out_host, int64_t chunk_clips,
                            void* device_scratch, size_t scratch_bytes, void* stream);
 
+/* ------------------------------------------------------- signal primitives
+ * The reference's signal.py primitives as standalone device ops (the
+ * transforms fuse them into their own kernels).  Device pointers, stream-ordered. */
+/* pad_signal (signal.py:138-156): x (B, L) -> y (B, L + left + right), mode
+ * NNAB_PAD_REFLECT / NNAB_PAD_ZERO, bit-exact; EINVAL for negative pads or a
+ * reflect pad >= L (the reference's ValueErrors). */
+int nnab_pad_signal(const float* x, int64_t B, int64_t L, int64_t left, int64_t right, int32_t mode, float* y,
+                    void* stream);
+/* downsample2 (signal.py:232-247): reflect pad (n_taps-1)/2, np.convolve-valid
+ * with the (device) taps, keep even samples: y (B, ceil(L/2)); EINVAL for an
+ * even n_taps or L < n_taps. */
+int nnab_downsample2(const float* x, int64_t B, int64_t L, const float* taps, int32_t n_taps, float* y,
+                     void* stream);
+
 /* ------------------------------------------------------- trainable layers
  * TrainableLayer / spectrogram_vjp (gradients.py:28-149) on the device.
  * Frame slots: clip b, frame t -> slot b*R + t (R = rows per clip from

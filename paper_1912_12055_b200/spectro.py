@@ -76,6 +76,99 @@ class Spectrogram:
         return int(self.data.shape[1])
 
 
+# ------------------------------------------------------------- signal primitives
+# signal.py's building blocks on the device (the transforms below fuse them
+# into their own kernels; these serve direct callers and the primitives' KATs).
+
+PAD_MODES = {"reflect": 0, "constant_zero": 1}
+
+
+@dataclass(frozen=True)
+class FrameMatrix:
+    """signal.py:91-103 -- kernel responses per frame: values (n_kernels, n_frames)."""
+
+    values: torch.Tensor
+    hop: int = 1
+
+    @property
+    def n_frames(self):
+        return int(self.values.shape[1])
+
+
+@dataclass(frozen=True)
+class FirFilter:
+    """signal.py:76-88 -- FIR taps (float64, host) and their normalised cutoff."""
+
+    taps: np.ndarray
+    normalized_cutoff: float
+
+
+def make_window(kind: str, n: int, periodic: bool = True) -> np.ndarray:
+    """signal.py:106-135 (host, init-time)."""
+    return banks.make_window(kind, n, periodic)
+
+
+def design_lowpass_fir(num_taps: int, cutoff: float, window_kind: str = "hamming") -> FirFilter:
+    """signal.py:186-211 (host, init-time)."""
+    return FirFilter(banks.lowpass_fir(num_taps, cutoff, window_kind), float(cutoff))
+
+
+def pad_signal(x: Signal, mode: str, left: int, right: int) -> Signal:
+    """signal.py:138-156 on the device (nnab_pad_signal), bit-exact."""
+    from . import _lib as L
+    if left < 0 or right < 0:
+        raise ValueError("pad amounts must be non-negative")
+    if mode not in PAD_MODES:
+        raise ValueError(f"unknown pad mode {mode!r}")
+    n = len(x)
+    if mode == "reflect" and (left >= n or right >= n):
+        raise ValueError(f"reflect padding ({left}, {right}) must be shorter than the signal (len {n})")
+    y = torch.empty(n + left + right, dtype=torch.float32, device=x.samples.device)
+    L.check(L.load().nnab_pad_signal(x.samples.data_ptr(), 1, n, int(left), int(right), PAD_MODES[mode],
+                                     y.data_ptr(), L.stream_handle(y.device)), "pad_signal")
+    return Signal(y, x.sample_rate, device=str(y.device))
+
+
+def conv1d_strided(x: Signal, kernels, stride: int, precision: str = "fp32") -> FrameMatrix:
+    """signal.py:159-183: out[r, t] = sum_m x[t*stride + m] * kernels[r, m] (no
+    padding, cross-correlation), on the tcgen05 GEMM (a real bank as the
+    cosine rows of a DFT-type bank with zero sine rows, complex output).
+    precision "fp32" (3xTF32, default: FP32-accurate) or "tf32"."""
+    k = kernels.detach().cpu().numpy() if torch.is_tensor(kernels) else np.asarray(kernels)
+    k = np.atleast_2d(k)
+    if np.iscomplexobj(k):
+        raise ValueError("kernels must be real; run real and imaginary parts separately")
+    if k.size == 0:
+        raise ValueError("at least one non-empty kernel row is required")
+    m = k.shape[1]
+    if m > len(x):
+        raise ValueError(f"kernel length {m} exceeds signal length {len(x)}; pad the signal first")
+    if stride < 1:
+        raise ValueError(f"stride must be >= 1, got {stride}")
+    k32 = k.astype(np.float32)
+    eng = DftEngine(k32, np.zeros_like(k32), int(stride), center=False, precision=precision,
+                    device=x.samples.device, allow_fold=False)
+    out = eng.forward(x.samples[None], "complex")[0]  # re - i*im with zero sine rows: re
+    return FrameMatrix(out.real.contiguous(), hop=int(stride))
+
+
+def downsample2(x: Signal, f: FirFilter) -> Signal:
+    """signal.py:232-247 on the device (nnab_downsample2): reflect pad, FIR,
+    keep every second sample; FP32 accumulation."""
+    from . import _lib as L
+    taps = np.asarray(f.taps if isinstance(f, FirFilter) else f, dtype=np.float64)
+    if taps.size % 2 == 0:
+        raise ValueError("downsample2 requires an odd-length (center-tap) filter")
+    if len(x) < taps.size:
+        raise ValueError(f"signal (len {len(x)}) shorter than filter (len {taps.size})")
+    dev = x.samples.device
+    t = torch.as_tensor(taps, dtype=torch.float32, device=dev)
+    y = torch.empty((len(x) + 1) // 2, dtype=torch.float32, device=dev)
+    L.check(L.load().nnab_downsample2(x.samples.data_ptr(), 1, len(x), t.data_ptr(), int(taps.size), y.data_ptr(),
+                                      L.stream_handle(dev)), "downsample2")
+    return Signal(y, x.sample_rate / 2.0, device=str(dev))
+
+
 @dataclass(frozen=True)
 class StftParams:
     """transforms.py:50-65."""
