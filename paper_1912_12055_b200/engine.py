@@ -141,10 +141,12 @@ class DftEngine:
         pad = self.n_fft // 2 if self.center else 0
         return geometry(length, self.n_fft, self.hop, pad, self.pad_mode)[0]
 
-    def forward(self, x: torch.Tensor, kind: str = "magnitude", eps: float = 1e-12,
+    def forward(self, x: torch.Tensor, kind: str = "magnitude", eps: float | None = None,
                 out: torch.Tensor | None = None) -> torch.Tensor:
         """x (B, L) float32 on the engine's device -> (B, F, T) [complex64 for 'complex',
-        (B, n_mels, T) for 'mel']."""
+        (B, n_mels, T) for 'mel'].  eps only enters 'smooth' (sqrt(|X|^2 + eps),
+        default 1e-12, gradients.py:61-67) and 'mel' (default 0: MelSpec is
+        W @ |X|**power with the plain magnitude, transforms.py:164-172)."""
         B, length = self.stage(x)
         return self.run_staged(B, length, kind, eps, out)
 
@@ -172,10 +174,12 @@ class DftEngine:
                                       L.stream_handle(self.device)), "stage_frames")
         return B, length
 
-    def run_staged(self, B: int, length: int, kind: str = "magnitude", eps: float = 1e-12,
+    def run_staged(self, B: int, length: int, kind: str = "magnitude", eps: float | None = None,
                    out: torch.Tensor | None = None) -> torch.Tensor:
         """The tcgen05 GEMM + fused epilogue on the frames staged by stage()."""
         lib = L.load()
+        if eps is None:
+            eps = 1e-12 if kind == "smooth" else 0.0
         T = self.n_frames(length)
         if kind not in self._KINDS:
             raise ValueError(f"output must be one of {sorted(self._KINDS)}, got {kind!r}")
@@ -216,7 +220,7 @@ class DftEngine:
         mel = k == L.OUT_MEL
         L.check(lib.nnab_stft_forward_host(
             C.byref(f), x_host.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins, self.fold,
-            self.precision, k, float(getattr(self, "power", 1.0)), 1e-12,
+            self.precision, k, float(getattr(self, "power", 1.0)), 0.0,
             self.mel_w.data_ptr() if mel else None, self.n_mels if mel else 0, self.mel_ld if mel else 0,
             L.ptr(self.mel_band) if mel else None, out_host.data_ptr(), int(chunk_clips), ws.data_ptr(),
             ws.numel(), L.stream_handle(self.device)), "stft_forward_host")
