@@ -9,6 +9,7 @@ Citations are relative to /root/reference/pkg/src/spectro/.
 from __future__ import annotations
 
 import math
+import warnings
 
 import numpy as np
 
@@ -107,6 +108,9 @@ def mel_filter_bank(sr: float, n_fft: int, n_mels: int, fmin: float = 0.0, fmax:
     left, centre, right = hz[:-2, None], hz[1:-1, None], hz[2:, None]
     tri = np.maximum(0.0, np.minimum((fb - left) / (centre - left), (right - fb) / (right - centre)))
     peak = tri.max(axis=1, keepdims=True)
+    if (peak[:, 0] == 0).any():  # kernels.py: an n_fft too small for n_mels leaves empty rows
+        warnings.warn(f"{int((peak[:, 0] == 0).sum())} of {n_mels} mel filters are empty; "
+                      "increase n_fft or reduce n_mels", UserWarning, stacklevel=2)
     if norm == "none":
         w = np.where(peak > 0, tri / np.where(peak > 0, peak, 1.0), tri)
     else:
