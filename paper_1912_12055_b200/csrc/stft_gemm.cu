@@ -379,7 +379,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int ch = bin0 >> 5;
             const int lo = p.mel_band ? p.mel_band[2 * ch] : 0;
             const int hi = p.mel_band ? p.mel_band[2 * ch + 1] : p.n_mels;
-            for (int m = lo; m < hi; ++m) {
+            // two mel rows per step: independent FMA chains and all 16 weight
+            // loads of both rows in flight before the first use
+            int m = lo;
+            for (; m + 1 < hi; m += 2) {
+              const float4* w0 = reinterpret_cast<const float4*>(p.mel_w + (int64_t)m * p.mel_ld + bin0);
+              const float4* w1 = reinterpret_cast<const float4*>(p.mel_w + (int64_t)(m + 1) * p.mel_ld + bin0);
+              float4 wa[8], wb[8];
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                wa[j4] = __ldg(w0 + j4);
+                wb[j4] = __ldg(w1 + j4);
+              }
+              float a = mel_acc[m * kBM + row], a2 = mel_acc[(m + 1) * kBM + row];
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                a = fmaf(wa[j4].x, m32[4 * j4 + 0], a);
+                a2 = fmaf(wb[j4].x, m32[4 * j4 + 0], a2);
+                a = fmaf(wa[j4].y, m32[4 * j4 + 1], a);
+                a2 = fmaf(wb[j4].y, m32[4 * j4 + 1], a2);
+                a = fmaf(wa[j4].z, m32[4 * j4 + 2], a);
+                a2 = fmaf(wb[j4].z, m32[4 * j4 + 2], a2);
+                a = fmaf(wa[j4].w, m32[4 * j4 + 3], a);
+                a2 = fmaf(wb[j4].w, m32[4 * j4 + 3], a2);
+              }
+              mel_acc[m * kBM + row] = a;
+              mel_acc[(m + 1) * kBM + row] = a2;
+            }
+            if (m < hi) {
               const float4* w = reinterpret_cast<const float4*>(p.mel_w + (int64_t)m * p.mel_ld + bin0);
               float a = mel_acc[m * kBM + row];
 #pragma unroll
