@@ -256,13 +256,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (meta == kUnused) break;
             const int r0 = (int)(meta & 0xFF);
             float* rrow = myring + (meta >> 8) * kRing;
-            float hi = 0.f, lo = 0.f;
+            float h4[4] = {0.f, 0.f, 0.f, 0.f}, l4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 chains: ILP over the adds
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
               const float x = __shfl_sync(0xffffffffu, v[16 * w16 + k], (lane + k) & 31);
-              if (lane + k < 32) hi += x;
-              else lo += x;
+              if (lane + k < 32) h4[k & 3] += x;
+              else l4[k & 3] += x;
             }
+            const float hi = (h4[0] + h4[1]) + (h4[2] + h4[3]), lo = (l4[0] + l4[1]) + (l4[2] + l4[3]);
             rrow[(s_row - r0) & (kRing - 1)] += hi;
             rrow[(s_row - 32 - r0) & (kRing - 1)] += lo;
             __syncwarp();  // the next window's cells overlap other lanes' cells of this one
