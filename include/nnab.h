@@ -163,6 +163,9 @@ int nnab_stft_forward_train_staged(const nnab_frames* f, const float* packed_hi,
 /* (B, rows, T) -> slot-major [rows][ld], zero on non-frame slots */
 int nnab_grad_to_slots(const float* g_brt, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld, float* out,
                        void* stream);
+/* the same, fused with the GEMM-operand split: hi = TF32(g) (+ lo = TF32(g - hi) in 3xTF32) */
+int nnab_grad_to_slots_split(const float* g_brt, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld,
+                             int32_t precision, float* hi, float* lo, void* stream);
 /* slot-major [rows][ld] -> (B, rows, T) */
 int nnab_from_slots(const float* src, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld, float* out_brt,
                     void* stream);
@@ -171,6 +174,13 @@ int nnab_from_slots(const float* src, int64_t B, int32_t rows, int32_t T, int32_
 int nnab_dft_coef(const float* ds_slots, const float* g_bft, const float* re_s, const float* im_s, int32_t F,
                   int64_t B, int32_t T, int32_t R, int64_t ld, float eps, int32_t precision, float* coef_hi,
                   float* coef_lo, void* stream);
+/* Mel layer forward of the trainable layer (gradients.py:69-80): W @ S on the
+ * slot-major smoothed magnitude S [F][ld] (save_mag of the training forward),
+ * written as (B, n_mels, T).  w = W zero-padded to [n_mels][kp], kp = F
+ * rounded up to 32 (<= 2048 in TF32, <= 1024 in 3xTF32, else NNAB_ENOTSUP); R % 4 == 0. */
+int nnab_mel_forward_slots(int32_t n_mels, int64_t ld, int32_t kp, const float* w_hi, const float* w_lo,
+                           const float* s_hi, const float* s_lo, int32_t F, int64_t B, int32_t R, int32_t T,
+                           int32_t precision, float* out, void* stream);
 /* Joint mel + trainable STFT backward: dS = W^T g computed on the tensor cores
  * with the coef step (gradients.py:125-128) in the GEMM epilogue, so dS never
  * reaches HBM.  wt = W^T zero-padded to [F][kp] (kp = n_mels rounded up to 32,

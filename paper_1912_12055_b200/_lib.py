@@ -58,8 +58,10 @@ SIGNATURES = {
     "nnab_stft_forward_train_staged": (C.c_int, [_FR, _fp, _fp, _i32, _i32, _i32, _i32, _f32, _f32, _fp, _i32, _i32,
                                                  _ip, _fp, _fp, _fp, _fp, _i64, _vp, _sz, _vp]),
     "nnab_grad_to_slots": (C.c_int, [_fp, _i64, _i32, _i32, _i32, _i64, _fp, _vp]),
+    "nnab_grad_to_slots_split": (C.c_int, [_fp, _i64, _i32, _i32, _i32, _i64, _i32, _fp, _fp, _vp]),
     "nnab_from_slots": (C.c_int, [_fp, _i64, _i32, _i32, _i32, _i64, _fp, _vp]),
     "nnab_dft_coef": (C.c_int, [_fp, _fp, _fp, _fp, _i32, _i64, _i32, _i32, _i64, _f32, _i32, _fp, _fp, _vp]),
+    "nnab_mel_forward_slots": (C.c_int, [_i32, _i64, _i32, _fp, _fp, _fp, _fp, _i32, _i64, _i32, _i32, _i32, _fp, _vp]),
     "nnab_mel_dft_coef": (C.c_int, [_i32, _i64, _i32, _fp, _fp, _fp, _fp, _i32, _fp, _fp, _f32, _i32, _fp, _fp, _vp]),
     "nnab_transpose_pad": (C.c_int, [_fp, _i32, _i32, _i32, _i32, _fp, _fp, _vp]),
     "nnab_tf32_split": (C.c_int, [_fp, _i64, _i32, _fp, _fp, _vp]),

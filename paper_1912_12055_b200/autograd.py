@@ -88,10 +88,16 @@ class DftLayerOp:
             wp[:, :F] = mel_w.detach().to(self.device, torch.float32)
             magp = self._split(mag_s) if self.split else (mag_s, None)
             saved["magp"] = magp
-            mel_s = _f32(nm, ld, self.device)
-            self._rgemm(nm, ld, kp, self._split(wp), kp, magp, ld, 1, ld, F, mel_s, ld)
             out = torch.empty(B, nm, T, device=self.device)
-            L.check(lib.nnab_from_slots(mel_s.data_ptr(), B, nm, T, R, ld, out.data_ptr(), stream), "from_slots")
+            wsp = self._split(wp)
+            if R % 4 == 0 and kp <= (1024 if self.split else 2048):  # W @ S straight into (B, n_mels, T)
+                L.check(lib.nnab_mel_forward_slots(nm, ld, kp, wsp[0].data_ptr(), L.ptr(wsp[1]), magp[0].data_ptr(),
+                                                   L.ptr(magp[1]), F, B, R, T, self.prec, out.data_ptr(), stream),
+                        "mel_forward_slots")
+            else:
+                mel_s = _f32(nm, ld, self.device)
+                self._rgemm(nm, ld, kp, wsp, kp, magp, ld, 1, ld, F, mel_s, ld)
+                L.check(lib.nnab_from_slots(mel_s.data_ptr(), B, nm, T, R, ld, out.data_ptr(), stream), "from_slots")
         return out, saved
 
     def _rows_per_clip(self, length):
@@ -131,9 +137,9 @@ class DftLayerOp:
         ds = None
         if mel_w is not None:
             nm = int(mel_w.shape[0])
-            gs = _f32(nm, ld, self.device)
-            L.check(lib.nnab_grad_to_slots(g.data_ptr(), B, nm, T, R, ld, gs.data_ptr(), stream), "grad_to_slots")
-            gsp = self._split(gs)
+            gsp = (_f32(nm, ld, self.device), _f32(nm, ld, self.device) if self.split else None)
+            L.check(lib.nnab_grad_to_slots_split(g.data_ptr(), B, nm, T, R, ld, self.prec, gsp[0].data_ptr(),
+                                                 L.ptr(gsp[1]), stream), "grad_to_slots_split")
             if need_mel:  # dW[m][f] = sum_slot g[m][slot] S[f][slot]
                 magp = saved["magp"]
                 dW = torch.empty(nm, F, device=self.device)

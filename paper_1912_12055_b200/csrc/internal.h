@@ -93,6 +93,10 @@ struct RGemmArgs {
   const float *coef_re = nullptr, *coef_im = nullptr;
   float* coef_lo = nullptr;
   float coef_eps = 0.f;
+  // frames output (mel forward of the training layer): column n = slot b*R + t is
+  // written to c[(b*M + m)*T + t] for t < T (the (B, M, T) layout), nothing else
+  int64_t frames_B = 0;
+  int32_t frames_R = 0, frames_T = 0;
 };
 size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits);
 // fused tensor-core CQT2010v2 (cqt2010_tc.cu); NNAB_ENOTSUP outside its envelope

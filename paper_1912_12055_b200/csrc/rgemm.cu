@@ -51,6 +51,8 @@ struct RParams {
   const float *re, *im;  // coef epilogue (RGemmArgs::coef_re): C is coef_hi; im null: re holds FP16 phasor pairs
   float* c_lo;
   float eps;
+  int64_t fB;  // frames output (RGemmArgs::frames_R > 0)
+  int32_t fR, fT;
 };
 
 NNAB_DEV float4 tf32_hi4(float4 a) { return make_float4(tf32_rne(a.x), tf32_rne(a.y), tf32_rne(a.z), tf32_rne(a.w)); }
@@ -398,6 +400,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             }
+          } else if (p.fR) {  // one chunk, no split: the slot tile lands in (B, M, T) directly
+            const int64_t b = n / p.fR;  // R % 4 == 0: the lane's 4 slots share a clip
+            const int t0 = (int)(n - b * p.fR);
+            if (b < p.fB) {
+#pragma unroll
+              for (int it = 0; it < 8; ++it) {
+                const int m = m_base + it * 4 + sr;
+                if (m >= p.M) continue;
+                float* orow = p.C + (b * p.M + m) * (int64_t)p.fT;
+                const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  if (t0 + j < p.fT && n + j < p.N) orow[t0 + j] = dv[j];
+              }
+            }
           } else {
             // the running sum lives in C (L2): all loads are in flight before any add
             float4 cur[8];
@@ -485,7 +502,7 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.n_tiles = (g.N + TBN - 1) / TBN;
   const int tiles = p.m_tiles * p.n_tiles;
   const int units = (kPair ? (p.m_tiles + 1) / 2 * 2 : p.m_tiles) * p.n_tiles;  // CTAs per split
-  int splits = g.coef_re ? 1 : g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, units));
+  int splits = (g.coef_re || g.frames_R) ? 1 : g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, units));
   const int64_t kb = g.K / C::BK;
   splits = (int)std::min<int64_t>(splits, kb);
   p.k_per_split = (kb + splits - 1) / splits * C::BK;
@@ -498,6 +515,10 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.im = g.coef_im;
   p.c_lo = g.coef_lo;
   p.eps = g.coef_eps;
+  p.fB = g.frames_B;
+  p.fR = g.frames_R;
+  p.fT = g.frames_T;
+  if (p.fR && (p.fR % 4 || p.splits != 1 || kb > p.k_chunk / C::BK || g.alpha != 1.f || p.re)) return NNAB_EINVAL;
   if (p.re && (p.splits != 1 || kb > p.k_chunk / C::BK || g.alpha != 1.f)) return NNAB_EINVAL;  // one TMEM chain
   const bool direct = p.splits == 1 && g.alpha == 1.f;
   p.C = direct ? g.c : g.partial;

@@ -23,7 +23,7 @@ namespace {
 // out[r][b*R + t] = g[b][r][t] for t < T, 0 for the staging-only slots and the
 // tail up to ld.
 __global__ void to_slots_kernel(const float* __restrict__ g, int64_t B, int32_t rows, int32_t T, int32_t R,
-                                int64_t ld, float* __restrict__ out) {
+                                int64_t ld, float* __restrict__ out, int round, float* __restrict__ lo) {
   const int64_t total = (int64_t)rows * ld;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / ld, slot = e - r * ld;
@@ -31,7 +31,13 @@ __global__ void to_slots_kernel(const float* __restrict__ g, int64_t B, int32_t 
     const int t = (int)(slot - b * R);
     float v = 0.f;
     if (b < B && t < T) v = g[(b * rows + r) * (int64_t)T + t];
-    out[e] = v;
+    if (round) {
+      const float h = tf32_rne(v);
+      out[e] = h;
+      if (lo) lo[e] = tf32_rne(v - h);
+    } else {
+      out[e] = v;
+    }
   }
 }
 
@@ -198,12 +204,26 @@ extern "C" int nnab_stft_forward_train_staged(const nnab_frames* f, const float*
   return launch_stft_gemm(g, a, precision, (cudaStream_t)stream);
 }
 
+// as nnab_grad_to_slots, fused with the GEMM-operand split: hi = TF32(v) and, in
+// 3xTF32, lo = TF32(v - hi) -- the layout nnab_rgemm / nnab_mel_dft_coef read
+extern "C" int nnab_grad_to_slots_split(const float* g_brt, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld,
+                                        int32_t precision, float* hi, float* lo, void* stream) {
+  if (!g_brt || !hi || rows < 1 || T < 1 || R < T || ld < B * R) return NNAB_EINVAL;
+  if (precision == NNAB_PREC_3XTF32 && !lo) return NNAB_EINVAL;
+  const int64_t total = (int64_t)rows * ld;
+  if (total == 0) return NNAB_OK;
+  to_slots_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(g_brt, B, rows, T, R, ld, hi, 1,
+                                                                     precision == NNAB_PREC_3XTF32 ? lo : nullptr);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
 extern "C" int nnab_grad_to_slots(const float* g_brt, int64_t B, int32_t rows, int32_t T, int32_t R, int64_t ld,
                                   float* out, void* stream) {
   if (!g_brt || !out || rows < 1 || T < 1 || R < T || ld < B * R) return NNAB_EINVAL;
   const int64_t total = (int64_t)rows * ld;
   if (total == 0) return NNAB_OK;
-  to_slots_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(g_brt, B, rows, T, R, ld, out);
+  to_slots_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(g_brt, B, rows, T, R, ld, out, 0, nullptr);
   NNAB_LAUNCHED();
   return NNAB_OK;
 }
@@ -316,6 +336,41 @@ extern "C" int nnab_mel_dft_coef(int32_t F, int64_t ld, int32_t kp, const float*
   g.coef_im = im_s;
   g.coef_lo = coef_lo;
   g.coef_eps = eps;
+  return launch_rgemm(g, precision, (cudaStream_t)stream);
+}
+
+// Mel layer forward of the trainable layer (gradients.py:69-80): mel = W @ S
+// with S the slot-major smoothed magnitude [F][ld] of the training forward, on
+// the tcgen05 reduction GEMM, written straight to (B, n_mels, T) from the
+// epilogue (no slot-major intermediate).  w: W zero-padded to [n_mels][kp]
+// (kp = F rounded up to 32), TF32 hi (+ lo).
+extern "C" int nnab_mel_forward_slots(int32_t n_mels, int64_t ld, int32_t kp, const float* w_hi, const float* w_lo,
+                                      const float* s_hi, const float* s_lo, int32_t F, int64_t B, int32_t R, int32_t T,
+                                      int32_t precision, float* out, void* stream) {
+  if (n_mels < 1 || ld < 1 || kp < F || F < 1 || !w_hi || !s_hi || !out || B < 0 || R < T || T < 1)
+    return NNAB_EINVAL;
+  if (precision == NNAB_PREC_3XTF32 && (!w_lo || !s_lo)) return NNAB_EINVAL;
+  if (ld > INT32_MAX || ld < B * R || R % 4) return NNAB_EINVAL;
+  if (kp > (precision == NNAB_PREC_3XTF32 ? 1024 : 2048)) return NNAB_ENOTSUP;  // one TMEM chain per tile
+  if (B == 0) return NNAB_OK;
+  RGemmArgs g;
+  g.M = n_mels;
+  g.N = (int32_t)ld;
+  g.K = kp;
+  g.a_hi = w_hi;
+  g.a_lo = w_lo;
+  g.lda = kp;
+  g.b_hi = s_hi;
+  g.b_lo = s_lo;
+  g.b_mn = 1;
+  g.b_row_len = (int32_t)ld;
+  g.b_rows = F;
+  g.c = out;
+  g.ldc = ld;
+  g.splits = 1;
+  g.frames_B = B;
+  g.frames_R = R;
+  g.frames_T = T;
   return launch_rgemm(g, precision, (cudaStream_t)stream);
 }
 
