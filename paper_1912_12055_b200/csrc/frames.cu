@@ -86,6 +86,23 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
         const int m = (int)(ga & 3);
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = m == 0 ? e[u] : m == 1 ? e[u + 1] : m == 2 ? e[u + 2] : e[u + 3];
+      } else if (x_aligned && mode == NNAB_PAD_REFLECT && i0 + 3 < padded_len &&
+                 ((j0 + 3 < 0 && -j0 < L) || (j0 >= L && 2 * (L - 1) - j0 - 3 >= 0))) {
+        // a reflected group (np.pad "reflect": one mirror image, left or right):
+        // its 4 sources are one descending run -- the same funnel, reversed
+        const int64_t a_lo = j0 < 0 ? -j0 - 3 : 2 * (L - 1) - j0 - 3;
+        const int64_t gl = b * L + a_lo;
+        if (a_lo - (gl & 3) + 7 < L) {
+          const float4* a4 = reinterpret_cast<const float4*>(x + (gl & ~int64_t(3)));
+          const float4 w0 = __ldg(a4), w1 = __ldg(a4 + 1);
+          const float e[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+          const int m = (int)(gl & 3);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[3 - u] = m == 0 ? e[u] : m == 1 ? e[u + 1] : m == 2 ? e[u + 2] : e[u + 3];
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[3 - u] = __ldg(xb + a_lo + u);
+        }
       } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
