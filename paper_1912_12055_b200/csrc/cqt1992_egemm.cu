@@ -62,7 +62,6 @@ struct EParams {
   int32_t n_groups, ctas_per_group, r_max;
   float eps;
   const uint16_t* col_table;  // [n_groups][256]: row_local << 8 | r
-  const uint32_t* run_table;  // [n_groups][kChunks][kRunSlots]: count, runs (see nnab_cqt_egemm_plan)
   const int32_t* group_rows;  // [n_groups][64]: bank row 2*bin + im, -1 unused
   float* out;
 };
