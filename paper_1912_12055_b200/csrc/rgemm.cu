@@ -96,8 +96,10 @@ NNAB_DEV uint64_t mndesc(const void* p, int /*swz*/, uint32_t lbo) {
 // reduction dK = coef @ frames is L2-bandwidth bound at 128 x 256 per CTA).
 // kWide (with kPair): 256 x 512 tiles -- two N=256 MMAs per K step into all
 // 512 TMEM columns (one accumulator), a quarter less L2 traffic per MAC again.
-template <bool kSplit, bool kPair, bool kWide>
-__global__ void __launch_bounds__(kThreads, 1)
+// kE8: the phasor coef epilogue (nnab_mel_dft_coef, TF32) on 8 epilogue warps
+// (384 threads, 3 stages): its HBM-latency-bound loads get twice the warps in flight.
+template <bool kSplit, bool kPair, bool kWide, bool kE8 = false>
+__global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
     rgemm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                  const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                  const RParams p) {
@@ -107,24 +109,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NACC = kWide ? 1 : C::NUM_ACC;   // TMEM accumulators
   constexpr int kBNc = kPair ? kBN / 2 : kBN;  // B columns this CTA stages per MMA
   constexpr int kHalves = kWide ? 2 : 1;       // N=256 MMAs per K step
+  constexpr int NST = kE8 ? 3 : kStages;        // pipeline stages
+  constexpr int kEW = kE8 ? 8 : 4;              // epilogue warps
+  static_assert(!kE8 || (!kSplit && !kWide), "8-warp epilogue: TF32 coef GEMM only");
   const uint32_t rank = kPair ? cluster_ctarank() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * C::STAGE);
   uint64_t* full = bars;
-  uint64_t* empty = bars + kStages;
-  uint64_t* tfull = bars + 2 * kStages;
-  uint64_t* tempty = bars + 2 * kStages + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* empty = bars + NST;
+  uint64_t* tfull = bars + 2 * NST;
+  uint64_t* tempty = bars + 2 * NST + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 4);
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kPair ? 2 * kBM : kBM);  // pair: the leader's counts both CTAs' threads
+      mbar_init(&tempty[i], (kPair ? 2 : 1) * kEW * 32);  // pair: the leader's counts both CTAs' threads
     }
     fence_barrier_init();
   }
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             }
-            if (++s == kStages) { s = 0; ph ^= 1; }
+            if (++s == NST) { s = 0; ph ^= 1; }
             continue;
           }
           mbar_expect_tx(&full[s], C::STAGE);
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES + j * C::BK * 128, &tb_lo, &full[s], col, row);
             }
           }
-          if (++s == kStages) { s = 0; ph ^= 1; }
+          if (++s == NST) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (kPair) mma_commit_pair(&empty[s], 0x3);
             else mma_commit(&empty[s]);
-            if (++s == kStages) { s = 0; ph ^= 1; }
+            if (++s == NST) { s = 0; ph ^= 1; }
           }
           if (kPair) mma_commit_pair(&tfull[acc], 0x3);
           else mma_commit(&tfull[acc]);
@@ -260,8 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // per-warp shared-memory transpose (32 rows x 36-float stride, conflict-free
     // for float4) and leaves as float4 runs of 8 lanes per row: every global
     // access is a full 128-byte line instead of 32 rows x 16 B.
-    const uint32_t q = warp - 4;
-    float* stg = reinterpret_cast<float*>(smem + kStages * C::STAGE + 128) + q * 32 * kStg;
+    const uint32_t ew = warp - 4, q = ew & 3;  // TMEM lane quarter
+    const int hsel = kE8 ? (int)(ew >> 2) : 0;  // kE8: warps 4-7 even chunks, 8-11 odd ones
+    constexpr int CSTEP = kE8 ? 2 : 1;
+    float* stg = reinterpret_cast<float*>(smem + NST * C::STAGE + 128) + ew * 32 * kStg;
     const int sr = (int)(lane >> 3), sc = (int)(lane & 7) * 4;  // this lane's (row in 4, float4 column)
     int acc = 0;
     uint32_t aph = 0;
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tb = tbase + ((q * 32) << 16) + (NACC > 1 ? acc * C::ACC_STRIDE : 0);
         // phasor coef epilogue: chunk c + 1's phasor loads are in flight while chunk c
         // is drained (the epilogue is HBM-latency bound with 4 warps per SM)
-        const bool phasor = p.re && !p.im;
+        const bool phasor = kE8 || (p.re && !p.im);
         uint4 ph_cur[8], ph_nxt[8];
         auto load_ph = [&](int c, uint4* dst) {
           const int n = nt * TBN + c * 32 + sc;
@@ -292,10 +299,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (m < p.M && full4) dst[it] = __ldcs(reinterpret_cast<const uint4*>(p.re + (int64_t)m * p.ldc + n));
           }
         };
-        if (phasor) load_ph(0, ph_cur);
+        if (phasor) load_ph(hsel, ph_cur);
 #pragma unroll 1
-        for (int c = 0; c < TBN / 32; ++c) {
-          if (phasor && c + 1 < TBN / 32) load_ph(c + 1, ph_nxt);
+        for (int c = hsel; c < TBN / 32; c += CSTEP) {
+          if (phasor && c + CSTEP < TBN / 32) load_ph(c + CSTEP, ph_nxt);
           float v[32];
           tmem_ld32(tb + c * 32, v);
           if (kSplit) {
@@ -356,7 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             }
-          } else if (p.re) {  // coef epilogue: the dS tile never leaves the SM
+          } else if constexpr (!kE8) {
+          if (p.re) {  // coef epilogue: the dS tile never leaves the SM
             float4 rr[8], ii[8];
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
@@ -441,6 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          }  // !kE8
         }
         tc_fence_before();
         if (kPair) mbar_arrive_cluster(tempty0 + 8 * acc);
@@ -471,7 +480,7 @@ __global__ void sum_splits_kernel(const float* __restrict__ parts, int32_t split
   }
 }
 
-template <bool kSplit, bool kPair, bool kWide = false>
+template <bool kSplit, bool kPair, bool kWide = false, bool kE8 = false>
 int launch(const RGemmArgs& g, cudaStream_t st) {
   using C = RCfg<kSplit>;
   constexpr int kBNc = kPair ? kBN / 2 : kBN;
@@ -525,17 +534,18 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.ldc = direct ? g.ldc : (int64_t)p.n_tiles * TBN;
   p.split_stride = (int64_t)p.m_tiles * kBM * p.ldc;
   if (!direct && !g.partial) return NNAB_EINVAL;
-  const size_t smem = 1024 + kStages * C::STAGE + 128 + 4 * 32 * kStg * 4;
-  auto k = rgemm_kernel<kSplit, kPair, kWide>;
+  const size_t smem = 1024 + (kE8 ? 3 : kStages) * C::STAGE + 128 + (kE8 ? 8 : 4) * 32 * kStg * 4;
+  constexpr int threads = kE8 ? 384 : kThreads;
+  auto k = rgemm_kernel<kSplit, kPair, kWide, kE8>;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   (void)tiles;
   if (!kPair) {
     const int grid = std::min(units * p.splits, num_sms());
-    k<<<grid, kThreads, smem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+    k<<<grid, threads, smem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(std::min(units * p.splits, num_sms() / 2 * 2));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -583,6 +593,11 @@ int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s) {
     const bool pair = pair_ok && (pair_env >= 2 || g.M > kBM);  // one m tile: the peer would idle
     const bool wide = pair && !g.coef_re && (pair_env == 3 || (pair_env == 1 && g.N > kBN && g.K >= 65536));
     if (wide) return launch<false, true, true>(g, s);
+    static const bool e8_ok = [] {
+      const char* e = getenv("NNAB_COEF_E8");
+      return !(e && e[0] == '0');
+    }();
+    if (pair && e8_ok && g.coef_re && !g.coef_im) return launch<false, true, false, true>(g, s);
     return pair ? launch<false, true>(g, s) : launch<false, false>(g, s);
   }
   return NNAB_EINVAL;
