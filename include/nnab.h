@@ -128,6 +128,20 @@ int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const floa
                            int32_t mel_ld, const int32_t* mel_band, float* out_host, int64_t chunk_clips,
                            void* device_scratch, size_t scratch_bytes, void* stream);
 
+/* spectrogram_vjp (gradients.py:103-149) in one call, recomputing the forward
+ * like the reference: convolution layer (n_mels = 0; d_h = [dh_re; dh_im]
+ * (2 n_bins, n_fft), optional d_x (B, L)) or Mel layer over a fixed DFT stage
+ * (n_mels > 0; d_w (n_mels, n_bins); d_h / d_x must be NULL, the reference
+ * raises NotImplementedError for the Mel input gradient).  packed_*: the bank
+ * from nnab_pack_dft_bank (fold 0); h_re / h_im: the same bank unpacked (needed
+ * for d_x); upstream (B, rows, T).  Kernel gradients are summed over the batch. */
+size_t nnab_layer_vjp_workspace_bytes(const nnab_frames* f, int32_t n_bins, int32_t n_mels, int32_t precision,
+                                      int32_t need_x);
+int nnab_layer_vjp(const nnab_frames* f, const float* x, const float* packed_hi, const float* packed_lo,
+                   int32_t n_bins, const float* h_re, const float* h_im, const float* mel_w, int32_t n_mels,
+                   const float* upstream, float eps, int32_t precision, float* d_h, float* d_w, float* d_x,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------- signal primitives
  * The reference's signal.py primitives as standalone device ops (the
  * transforms fuse them into their own kernels).  Device pointers, stream-ordered. */

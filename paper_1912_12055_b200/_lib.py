@@ -91,6 +91,9 @@ SIGNATURES = {
     "nnab_cqt1992v2_host_scratch_bytes": (_sz, [_FR, _i32, _i32, _i32, _i64]),
     "nnab_cqt1992v2_forward_host": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _ip, _i32, _i32, _i32, _f32, _fp, _i64,
                                               _vp, _sz, _vp]),
+    "nnab_layer_vjp_workspace_bytes": (_sz, [_FR, _i32, _i32, _i32, _i32]),
+    "nnab_layer_vjp": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _fp, _fp, _fp, _i32, _fp, _f32, _i32, _fp, _fp, _fp, _vp,
+                                 _sz, _vp]),
     "nnab_pad_signal": (C.c_int, [_fp, _i64, _i64, _i64, _i64, _i32, _fp, _vp]),
     "nnab_downsample2": (C.c_int, [_fp, _i64, _i64, _fp, _i32, _fp, _vp]),
     "nnab_decode_wav": (C.c_int, [_vp, _i64, _i32, _i32, _fp, _vp]),

@@ -207,3 +207,58 @@ def test_layer_spectrogram_matches_transform(cuda_dev):  # test_gradients.py:166
     s_layer = layer.spectrogram(x).cpu().numpy()
     s_ref = S.Stft(S.StftParams(n_fft=64, hop_length=32, output="magnitude"), 8000.0, precision="fp32")(x).data
     assert np.max(np.abs(s_layer - s_ref.cpu().numpy())) < 1e-5 * np.max(np.abs(s_layer))
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("mel", [False, True])
+def test_c_abi_layer_vjp_matches_python_path(cuda_dev, precision, mel):
+    """nnab_layer_vjp (one C-ABI call for spectrogram_vjp, csrc/vjp.cu) against
+    the oracle VJP on the same inputs -- the boundary an FFI caller binds."""
+    import ctypes as C
+    from paper_1912_12055_b200 import _lib as L
+    from paper_1912_12055_b200.engine import DftEngine
+    lib = L.load()
+    h_re, h_im = O.stft_bank(64, 8000.0)
+    eng = DftEngine(h_re, h_im, 16, precision=precision, device="cuda", allow_fold=False)
+    rng = np.random.default_rng(21)
+    xs = (rng.standard_normal((3, 700)) * 0.5).astype(np.float32)
+    x = torch.from_numpy(xs).to(cuda_dev)
+    B, Ln = xs.shape
+    T = eng.n_frames(Ln)
+    f = eng.frames(B, Ln)
+    F = h_re.shape[0]
+    W = O.mel_bank(8000.0, 64, 6, formula="htk") if mel else None
+    rows = 6 if mel else F
+    up = rng.standard_normal((B, rows, T))
+    upd = torch.from_numpy(up.astype(np.float32)).to(cuda_dev)
+    hre = torch.from_numpy(h_re.astype(np.float32)).to(cuda_dev)
+    him = torch.from_numpy(h_im.astype(np.float32)).to(cuda_dev)
+    prec = L.PRECISIONS[precision]
+    need_x = 0 if mel else 1
+    ws = torch.empty(lib.nnab_layer_vjp_workspace_bytes(C.byref(f), F, 6 if mel else 0, prec, need_x),
+                     dtype=torch.uint8, device=cuda_dev)
+    d_h = None if mel else torch.empty(2 * F, 64, device=cuda_dev)
+    d_w = torch.empty(6, F, device=cuda_dev) if mel else None
+    d_x = None if mel else torch.empty(B, Ln, device=cuda_dev)
+    wd = torch.from_numpy(W.astype(np.float32)).to(cuda_dev) if mel else None
+    L.check(lib.nnab_layer_vjp(C.byref(f), x.data_ptr(), eng.packed_hi.data_ptr(), L.ptr(eng.packed_lo), F,
+                               hre.data_ptr(), him.data_ptr(), L.ptr(wd), 6 if mel else 0, upd.data_ptr(), 1e-12,
+                               prec, L.ptr(d_h), L.ptr(d_w), L.ptr(d_x), ws.data_ptr(), ws.numel(),
+                               L.stream_handle(cuda_dev)), "layer_vjp")
+    torch.cuda.synchronize()
+    if mel:
+        ref = sum(O.mel_layer_vjp(c.astype(np.float64), W, h_re, h_im, 16, g)["weights"] for c, g in zip(xs, up))
+        assert O.peak_err(d_w.cpu().numpy(), ref) <= TOL_GRAD[precision]
+        # the reference's mel layer has no input gradient
+        with pytest.raises(ValueError):
+            L.check(lib.nnab_layer_vjp(C.byref(f), x.data_ptr(), eng.packed_hi.data_ptr(), L.ptr(eng.packed_lo), F,
+                                       hre.data_ptr(), him.data_ptr(), wd.data_ptr(), 6, upd.data_ptr(), 1e-12, prec,
+                                       None, d_w.data_ptr(), x.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       L.stream_handle(cuda_dev)), "layer_vjp")
+        return
+    ref_h = np.zeros((2 * F, 64))
+    for i, (c, g) in enumerate(zip(xs, up)):
+        gr, gx = O.conv_layer_vjp(c.astype(np.float64), h_re, h_im, 16, g, with_input_grad=True)
+        ref_h += np.concatenate([gr["h_re"], gr["h_im"]])
+        assert O.peak_err(d_x[i].cpu().numpy(), gx) <= TOL_GRAD[precision]
+    assert O.peak_err(d_h.cpu().numpy(), ref_h) <= TOL_GRAD[precision]
