@@ -320,9 +320,33 @@ NNAB_DEV void build_frames(Ctx& c, const __half* sig, int h, int t0, int ntile) 
     dst = c.base + p.off_col + 128 * KC * 2 + (t - 128) * 16;
     cstride = (uint32_t)p.rows2 * 16u;
   }
+  const int tt = t0 + t;
+  if (h < 8 && (h & 1) == 0 && tt < p.T) {
+    // short hops (the top octaves): the frame's 96 taps start 2*sh halves past an
+    // 8-aligned position -- 13 aligned 16-byte loads, each chunk four 32-bit words
+    // of two neighbours picked by two select levels, instead of 8 (h = 2) or 2
+    // (h = 4) narrow swizzled loads per chunk
+    const int s_base = ML + tt * h - p.pad_al;
+    const int a0 = s_base & ~7, sh = (s_base & 7) >> 1;
+    uint4 q0 = ld8(sig, a0);
+#pragma unroll
+    for (int cc = 0; cc < KC / 8; ++cc) {
+      const uint4 q1 = ld8(sig, a0 + 8 * (cc + 1));
+      const uint32_t e[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      uint32_t f[5];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) f[j] = (sh & 2) ? e[j + 2] : e[j];
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = (sh & 1) ? f[j + 1] : f[j];
+      *reinterpret_cast<uint4*>(dst + cc * cstride) = make_uint4(o[0], o[1], o[2], o[3]);
+      q0 = q1;
+    }
+    return;
+  }
   uint4 v[KC / 8];
 #pragma unroll
-  for (int cc = 0; cc < KC / 8; ++cc) v[cc] = frame_chunk(p, sig, h, t0 + t, cc);
+  for (int cc = 0; cc < KC / 8; ++cc) v[cc] = frame_chunk(p, sig, h, tt, cc);
 #pragma unroll
   for (int cc = 0; cc < KC / 8; ++cc) *reinterpret_cast<uint4*>(dst + cc * cstride) = v[cc];
 }
