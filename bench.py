@@ -135,9 +135,25 @@ class Clocks:
                     if v.lower().startswith("active"):
                         reasons.add(n)
         os.unlink(self.path)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        note = None
+        if not sm:  # timed region shorter than nvidia-smi's first sample: one query right after it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=10).stdout
+                parts = [p.strip() for p in out.strip().split(",")]
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                for n, v in zip(names, parts[2:]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+                note = "timed region shorter than the 100 ms sampler: one sample right after it"
+            except Exception:
+                return None
+        d = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if note:
+            d["note"] = note
+        return d
 
 
 # ------------------------------------------------------------------ workloads
