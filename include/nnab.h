@@ -48,6 +48,12 @@ extern "C" {
 #define NNAB_OUT_COMPLEX 2   /* re - i*im (interleaved complex64)            */
 #define NNAB_OUT_MEL 3       /* W @ |X|^power            transforms.py:164-172 */
 #define NNAB_OUT_SMOOTH_MAG 4 /* sqrt(re^2+im^2+eps)      gradients.py:61-67 */
+/* flag, OR-ed into NNAB_OUT_MAGNITUDE / NNAB_OUT_POWER / NNAB_OUT_MEL of the
+ * STFT entry points: the fused epilogue writes log(value + eps) (log
+ * compression, north_star item 3; the reference has no log op, so parity is
+ * log of the parity-checked value).  With it, eps is the log offset only (the
+ * Mel magnitude is the plain sqrt(re^2 + im^2)). */
+#define NNAB_OUT_LOG 0x100
 
 #define NNAB_PREC_TF32 0  /* one TF32 tcgen05 pass (peak-normalised error <= 1e-3) */
 #define NNAB_PREC_3XTF32 1 /* hi/lo split, 3 passes (<= 1e-5, FP32-equivalent) */

@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("NNAB_LIB") or os.path.join(_HERE, "libnnab.so")  # NN
 OK, EINVAL, ECUDA, ENOTSUP, ENODEV = 0, 1, 2, 3, 4
 PAD_REFLECT, PAD_ZERO = 0, 1
 OUT_MAGNITUDE, OUT_POWER, OUT_COMPLEX, OUT_MEL, OUT_SMOOTH_MAG = 0, 1, 2, 3, 4
+OUT_LOG = 0x100  # flag: log(value + eps) in the fused epilogue (STFT / Mel)
 PREC_TF32, PREC_3XTF32 = 0, 1
 PAD_MODES = {"reflect": PAD_REFLECT, "constant_zero": PAD_ZERO, "constant": PAD_ZERO}
 PRECISIONS = {"tf32": PREC_TF32, "fp32": PREC_3XTF32, "3xtf32": PREC_3XTF32}

@@ -120,6 +120,10 @@ extern "C" size_t nnab_stft_workspace_bytes(const nnab_frames* f, int32_t precis
 
 static int validate_kind(int32_t out_kind, int32_t n_bins, const float* mel_w, int32_t n_mels, int32_t mel_ld,
                          int32_t n_tiles) {
+  if (out_kind & NNAB_OUT_LOG) {
+    out_kind &= ~NNAB_OUT_LOG;
+    if (out_kind != NNAB_OUT_MAGNITUDE && out_kind != NNAB_OUT_POWER && out_kind != NNAB_OUT_MEL) return NNAB_EINVAL;
+  }
   if (out_kind < NNAB_OUT_MAGNITUDE || out_kind > NNAB_OUT_SMOOTH_MAG) return NNAB_EINVAL;
   if (out_kind == NNAB_OUT_MEL) {
     if (!mel_w || n_mels < 1) return NNAB_EINVAL;
@@ -210,6 +214,7 @@ static size_t pipeline_bytes(int64_t chunk, int64_t L, int64_t out_per_clip) {
 }
 
 static int64_t out_elems_per_clip(int32_t out_kind, int32_t n_bins, int32_t n_mels, int32_t T) {
+  out_kind &= ~NNAB_OUT_LOG;
   if (out_kind == NNAB_OUT_MEL) return (int64_t)n_mels * T;
   if (out_kind == NNAB_OUT_COMPLEX) return 2ll * n_bins * T;
   return (int64_t)n_bins * T;

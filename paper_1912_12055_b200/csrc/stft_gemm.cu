@@ -66,6 +66,7 @@ struct Params {
   // longest-first so the first MMA (N = max) initialises every used column.
   const uint32_t* kb_tab;
   int32_t n_tab, b_box, pairs, out_bins;
+  float log_eps;  // >= 0: outputs are log(value + log_eps) (NNAB_OUT_LOG)
   int32_t stages;  // smem pipeline depth (4, or 3 when the Mel accumulator takes 64 KB)
   // training forward: re, im and smoothed magnitude per (bin, slot) saved in
   // slot-major layout [bin][ld_slots] for the backward GEMMs (may be null)
@@ -83,6 +84,9 @@ NNAB_DEV uint64_t make_sdesc(const void* p, int swz_bytes) {
   d |= (uint64_t)(swz_bytes == 128 ? 2 : 4) << 61;
   return d;
 }
+
+// log compression of an output value (NNAB_OUT_LOG); log_eps < 0: off
+NNAB_DEV float log_out(float v, float log_eps) { return log_eps >= 0.f ? logf(v + log_eps) : v; }
 
 NNAB_DEV float finish(float re, float im, int kind, float power, float eps) {
   const float p = fmaf(re, re, im * im);
@@ -431,8 +435,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (bin0 + j < F - p.fold) p.out[(ob + bin0 + j) * p.T + t] = finish(re[j], im[j], kind, p.power, p.eps);
-              if (p.fold && n == 0 && c == 0) p.out[(ob + F - 1) * p.T + t] = finish(nyq_re, 0.f, kind, p.power, p.eps);
+                if (bin0 + j < F - p.fold)
+                  p.out[(ob + bin0 + j) * p.T + t] = log_out(finish(re[j], im[j], kind, p.power, p.eps), p.log_eps);
+              if (p.fold && n == 0 && c == 0)
+                p.out[(ob + F - 1) * p.T + t] = log_out(finish(nyq_re, 0.f, kind, p.power, p.eps), p.log_eps);
             }
           }
         }
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mel_acc[m * kBM + row] = fmaf(__ldg(p.mel_w + (int64_t)m * p.mel_ld + F - 1), nyq_val, mel_acc[m * kBM + row]);
         }
         for (int m = 0; m < p.n_mels; ++m) {
-          if (valid) p.out[(b * p.n_mels + m) * (int64_t)p.T + t] = mel_acc[m * kBM + row];
+          if (valid) p.out[(b * p.n_mels + m) * (int64_t)p.T + t] = log_out(mel_acc[m * kBM + row], p.log_eps);
           mel_acc[m * kBM + row] = 0.f;
         }
       }
@@ -468,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <bool kSplit, bool kPair>
 int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   using C = Cfg<kSplit, kPair>;
-  const bool mel = a.out_kind == NNAB_OUT_MEL;
+  const bool mel = (a.out_kind & ~NNAB_OUT_LOG) == NNAB_OUT_MEL;
   if (mel && (a.n_mels < 1 || a.n_mels > kMelRows || !a.mel_w || a.mel_ld % 4 != 0)) return NNAB_ENOTSUP;
   if (g.row_len % C::BK != 0) return NNAB_ENOTSUP;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
@@ -496,9 +502,10 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.n_tiles = a.n_tiles;
   p.n_bins = a.n_bins;
   p.fold = a.fold;
-  p.out_kind = a.out_kind;
+  p.out_kind = a.out_kind & ~NNAB_OUT_LOG;
+  p.log_eps = (a.out_kind & NNAB_OUT_LOG) ? a.eps : -1.f;
   p.power = a.power;
-  p.eps = a.eps;
+  p.eps = (a.out_kind & NNAB_OUT_LOG) ? 0.f : a.eps;
   p.mel_w = a.mel_w;
   p.n_mels = a.n_mels;
   p.mel_ld = a.mel_ld;

@@ -142,13 +142,14 @@ class DftEngine:
         return geometry(length, self.n_fft, self.hop, pad, self.pad_mode)[0]
 
     def forward(self, x: torch.Tensor, kind: str = "magnitude", eps: float | None = None,
-                out: torch.Tensor | None = None) -> torch.Tensor:
+                out: torch.Tensor | None = None, log_eps: float | None = None) -> torch.Tensor:
         """x (B, L) float32 on the engine's device -> (B, F, T) [complex64 for 'complex',
         (B, n_mels, T) for 'mel'].  eps only enters 'smooth' (sqrt(|X|^2 + eps),
         default 1e-12, gradients.py:61-67) and 'mel' (default 0: MelSpec is
-        W @ |X|**power with the plain magnitude, transforms.py:164-172)."""
+        W @ |X|**power with the plain magnitude, transforms.py:164-172).  log_eps
+        (magnitude / power / mel): the epilogue writes log(value + log_eps)."""
         B, length = self.stage(x)
-        return self.run_staged(B, length, kind, eps, out)
+        return self.run_staged(B, length, kind, eps, out, log_eps)
 
     _KINDS = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "complex": L.OUT_COMPLEX,
               "mel": L.OUT_MEL, "smooth": L.OUT_SMOOTH_MAG}
@@ -175,11 +176,18 @@ class DftEngine:
         return B, length
 
     def run_staged(self, B: int, length: int, kind: str = "magnitude", eps: float | None = None,
-                   out: torch.Tensor | None = None) -> torch.Tensor:
+                   out: torch.Tensor | None = None, log_eps: float | None = None) -> torch.Tensor:
         """The tcgen05 GEMM + fused epilogue on the frames staged by stage()."""
         lib = L.load()
         if eps is None:
             eps = 1e-12 if kind == "smooth" else 0.0
+        log_flag = 0
+        if log_eps is not None:
+            if kind not in ("magnitude", "power", "mel"):
+                raise ValueError("log compression applies to magnitude, power and mel outputs")
+            if not log_eps >= 0.0:
+                raise ValueError(f"log_eps must be >= 0, got {log_eps}")
+            log_flag, eps = L.OUT_LOG, float(log_eps)
         T = self.n_frames(length)
         if kind not in self._KINDS:
             raise ValueError(f"output must be one of {sorted(self._KINDS)}, got {kind!r}")
@@ -197,14 +205,14 @@ class DftEngine:
         mel = k == L.OUT_MEL
         L.check(lib.nnab_stft_forward_staged(
             C.byref(f), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins, self.fold,
-            self.precision, k, float(getattr(self, "power", 1.0)), float(eps),
+            self.precision, k | log_flag, float(getattr(self, "power", 1.0)), float(eps),
             self.mel_w.data_ptr() if mel else None, self.n_mels if mel else 0, self.mel_ld if mel else 0,
             L.ptr(self.mel_band) if mel else None, out.data_ptr(), ws.data_ptr(), ws.numel(),
             L.stream_handle(self.device)), "stft_forward_staged")
         return out
 
     def forward_host(self, x_host: torch.Tensor, kind: str = "magnitude", chunk_clips: int = 128,
-                     out_host: torch.Tensor | None = None) -> torch.Tensor:
+                     out_host: torch.Tensor | None = None, log_eps: float | None = None) -> torch.Tensor:
         """Pinned host (B, L) -> pinned host result, streamed through the GPU
         in chunks with copy/compute overlap (nnab_stft_forward_host)."""
         lib = L.load()
@@ -220,7 +228,8 @@ class DftEngine:
         mel = k == L.OUT_MEL
         L.check(lib.nnab_stft_forward_host(
             C.byref(f), x_host.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins, self.fold,
-            self.precision, k, float(getattr(self, "power", 1.0)), 0.0,
+            self.precision, k | (L.OUT_LOG if log_eps is not None else 0), float(getattr(self, "power", 1.0)),
+            float(log_eps) if log_eps is not None else 0.0,
             self.mel_w.data_ptr() if mel else None, self.n_mels if mel else 0, self.mel_ld if mel else 0,
             L.ptr(self.mel_band) if mel else None, out_host.data_ptr(), int(chunk_clips), ws.data_ptr(),
             ws.numel(), L.stream_handle(self.device)), "stft_forward_host")

@@ -57,10 +57,13 @@ def _as_batch(x: torch.Tensor) -> torch.Tensor:
 class STFT(nn.Module):
     def __init__(self, n_fft=2048, freq_bins=None, hop_length=512, window="hann", freq_scale="no", center=True,
                  pad_mode="reflect", fmin=50, fmax=6000, sr=22050, trainable=False, output_format="Magnitude",
-                 precision="tf32", device="cuda"):
+                 precision="tf32", device="cuda", log_eps=None):
         super().__init__()
         self.device = _require_cuda(device)
         self.output_format = _fmt(output_format)
+        # log_eps: log(|X| + log_eps) (or of the power) fused into the epilogue (extension,
+        # north_star item 3); the trainable path composes torch.log on the kernel output
+        self.log_eps = log_eps
         self.trainable = bool(trainable)
         nf, self.bin_freqs_hz = banks.frequency_scale(freq_scale, n_fft, sr, fmin, fmax, freq_bins)
         h_re, h_im = banks.dft_kernels(nf, banks.make_window(window, n_fft, True))
@@ -73,16 +76,21 @@ class STFT(nn.Module):
     def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
         x = _as_batch(x)
         if self.trainable or x.requires_grad:
-            return DftLayerFunction.apply(x, self.h_re, self.h_im, None, self._op, _bank_key(self.h_re, self.h_im))
-        return self._infer.forward(x, _fmt(output_format or self.output_format))
+            y = DftLayerFunction.apply(x, self.h_re, self.h_im, None, self._op, _bank_key(self.h_re, self.h_im))
+            return y if self.log_eps is None else torch.log(y + self.log_eps)
+        fmt = _fmt(output_format or self.output_format)
+        if self.log_eps is not None and fmt != "complex":
+            return self._infer.forward(x, fmt, log_eps=self.log_eps)
+        return self._infer.forward(x, fmt)
 
 
 class MelSpectrogram(nn.Module):
     def __init__(self, sr=22050, n_fft=2048, n_mels=128, hop_length=512, window="hann", center=True,
                  pad_mode="reflect", htk=False, fmin=0.0, fmax=None, norm=None, power=1.0, trainable_mel=False,
-                 trainable_STFT=False, precision="tf32", device="cuda"):
+                 trainable_STFT=False, precision="tf32", device="cuda", log_eps=None):
         super().__init__()
         self.device = _require_cuda(device)
+        self.log_eps = log_eps  # log(mel + log_eps) fused into the epilogue (extension, north_star item 3)
         nf, _ = banks.frequency_scale("no", n_fft, sr, 50.0, 6000.0, None)
         h_re, h_im = banks.dft_kernels(nf, banks.make_window(window, n_fft, True))
         mel_norm = {None: "none", "none": "none", 1: "area", "slaney": "area", "area": "area"}[norm]
@@ -107,14 +115,15 @@ class MelSpectrogram(nn.Module):
         if self.trainable_mel or self.trainable_STFT or x.requires_grad:
             if self.power != 1.0:
                 raise NotImplementedError("trainable Mel layers use power=1 (gradients.py:69-80)")
-            return DftLayerFunction.apply(x, self.h_re, self.h_im, self.mel_basis, self._op,
-                                          _bank_key(self.h_re, self.h_im))
+            y = DftLayerFunction.apply(x, self.h_re, self.h_im, self.mel_basis, self._op,
+                                       _bank_key(self.h_re, self.h_im))
+            return y if self.log_eps is None else torch.log(y + self.log_eps)
         key = _bank_key(self.h_re, self.h_im, self.mel_basis)
         if key != self._infer_key:  # parameters edited in place since construction
             self._infer.set_bank(self.h_re.detach(), self.h_im.detach())
             self._infer.set_mel(self.mel_basis.detach(), power=self.power)
             self._infer_key = key
-        return self._infer.forward(x, "mel")
+        return self._infer.forward(x, "mel", log_eps=self.log_eps)
 
 
 class CQT1992v2(nn.Module):

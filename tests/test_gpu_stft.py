@@ -114,3 +114,32 @@ def test_zero_signal_and_bin_exact_tone(cuda_dev):
     assert np.max(np.delete(got, 8, axis=0)) <= 1e-4
     z = eng.forward(torch.zeros(2, 4000, device=cuda_dev), "magnitude")
     assert not z.any()
+
+
+@pytest.mark.parametrize("kind,power", [("magnitude", 1.0), ("power", 1.0), ("mel", 1.0), ("mel", 2.0)])
+def test_fused_log_compression(cuda_dev, kind, power):
+    """NNAB_OUT_LOG: log(value + eps) in the fused epilogue equals log of the
+    parity-checked output (the reference has no log op, so log is
+    pinned by composition) -- device path, host path and the nnAudio module."""
+    from paper_1912_12055_b200.layers import MelSpectrogram
+    h_re, h_im = O.stft_bank(512, 16000.0)
+    eng = engine(h_re, h_im, 128, "tf32")
+    if kind == "mel":
+        eng.set_mel(O.mel_bank(16000.0, 512, 40, formula="slaney"), power=power)
+    x = torch.from_numpy((np.random.default_rng(4).standard_normal((3, 9000)) * 0.5).astype(np.float32)).to(cuda_dev)
+    x[1].zero_()  # silent clip: log(0 + eps) exactly
+    plain = eng.forward(x, kind)
+    logged = eng.forward(x, kind, log_eps=1e-6)
+    ref = torch.log(plain.double() + 1e-6)
+    assert torch.allclose(logged.double(), ref, rtol=0, atol=2e-6), (logged.double() - ref).abs().max()
+    assert torch.all(logged[1] == torch.log(torch.tensor(1e-6, dtype=torch.float32)).to(cuda_dev))
+    if kind != "mel" or power == 1.0:
+        host = eng.forward_host(x.cpu().pin_memory(), kind, chunk_clips=2, log_eps=1e-6)
+        torch.cuda.synchronize()
+        assert torch.allclose(host.double(), ref.cpu(), rtol=0, atol=2e-6)
+    with pytest.raises(ValueError):
+        eng.forward(x, "complex", log_eps=1e-6)
+    if kind == "mel" and power == 1.0:
+        m = MelSpectrogram(sr=16000, n_fft=512, n_mels=40, hop_length=128, log_eps=1e-6)
+        mref = torch.log(MelSpectrogram(sr=16000, n_fft=512, n_mels=40, hop_length=128)(x).double() + 1e-6)
+        assert torch.allclose(m(x).double(), mref, rtol=0, atol=2e-6)
