@@ -121,7 +121,9 @@ extern "C" int nnab_layer_vjp(const nnab_frames* f, const float* x, const float*
   float* part = take(Lo.part);
   float* ht = take(Lo.ht);
   float* fgt = take(Lo.fgt);
-  auto lo_of = [&](float* a, size_t bytes) { return split ? reinterpret_cast<float*>(reinterpret_cast<char*>(a) + bytes / 2) : nullptr; };
+  auto lo_of = [&](float* a, size_t bytes) {  // the lo half of a hi/lo allocation (3xTF32)
+    return split ? reinterpret_cast<float*>(reinterpret_cast<char*>(a) + bytes / 2) : nullptr;
+  };
 
   // forward with the saved operands (gradients.py:61-80)
   if ((rc = nnab_stage_frames(f, x, precision, ws, Lo.stft, stream))) return rc;
