@@ -498,7 +498,9 @@ def main():
             "metric": f"{args.workload} spectrograms/s on the 1,770-clip batch (+ roofline fraction)",
             "value": value, "unit": "spectrograms/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "tf32" if args.precision == "tf32" else "3xtf32",
+            "dtype": (("f16 operands (exact per-clip power-of-two scale), f32 accumulate" if args.precision == "tf32"
+                       else "f32 (CUDA cores)") if args.workload == "cqt2010v2"
+                      else "tf32" if args.precision == "tf32" else "3xtf32"),
             "data": "synthetic: N(0, 0.5^2) float32 clips generated on device (cli.py:98-99 distribution)",
             "config": {"workload": WORKLOADS[args.workload], "clips_per_gpu": B_CLIPS, "global_clips": B_CLIPS * world,
                        "samples": L_SAMPLES, "sr": SR, "precision": args.precision,

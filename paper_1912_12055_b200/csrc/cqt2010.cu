@@ -69,6 +69,57 @@ __global__ void __launch_bounds__(256) halve_kernel(const float* __restrict__ x,
   }
 }
 
+// downsample2 for a half-band filter (pairs at every odd offset 1, 3, ..,
+// 2P-1, as the reference's 255-tap design): y[i] = c x[2i] + sum_k g_k
+// (x[2i - 2k - 1] + x[2i + 2k + 1]) only touches the even sample of the centre
+// and odd samples otherwise, so the CTA stages the odd phase xo and the even
+// phase xe of its span contiguously (reflect-padded) and each thread keeps 4
+// consecutive outputs: per 4 taps one aligned 16-byte load per side feeds 16
+// FMAs, conflict-free (lanes 16 bytes apart).  Same FMA order as halve_kernel.
+constexpr int kHbOut = 1024;  // outputs per CTA (256 threads x 4)
+
+__global__ void __launch_bounds__(256) halfband_kernel(const float* __restrict__ x, int64_t L, float* __restrict__ y,
+                                                       int64_t Lout, const __grid_constant__ FirPairs fir) {
+  extern __shared__ __align__(16) float hb[];
+  const int P = fir.n_pairs;
+  float* xo = hb;                // [kHbOut + 2P]: xo[u] = x[2 (i0 + u) - 2P + 1]
+  float* xe = hb + kHbOut + 2 * P + 4;  // [kHbOut]:   xe[u] = x[2 (i0 + u)]
+  const int64_t b = blockIdx.y;
+  const int64_t i0 = (int64_t)blockIdx.x * kHbOut;
+  const int n_out = (int)min((int64_t)kHbOut, Lout - i0);
+  if (n_out <= 0) return;
+  const float* xb = x + b * L;
+  for (int u = threadIdx.x; u < n_out + 2 * P; u += blockDim.x) xo[u] = __ldg(xb + reflect_idx(2 * (i0 + u) - 2 * P + 1, L));
+  for (int u = threadIdx.x; u < n_out; u += blockDim.x) xe[u] = __ldg(xb + reflect_idx(2 * (i0 + u), L));
+  __syncthreads();
+  const int ii = 4 * threadIdx.x;
+  if (ii >= n_out) return;
+  float acc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = fir.centre * xe[ii + j];
+  // right taps: xo[ii + P + k + j]; left taps: xo[ii + P - 1 - k + j]  (P % 4 == 0)
+  const float4* r4 = reinterpret_cast<const float4*>(xo + ii + P);
+  const float4* l4 = reinterpret_cast<const float4*>(xo + ii + P - 4);
+  float4 ra = r4[0], lhi = l4[1];
+#pragma unroll 1
+  for (int k0 = 0; k0 < P; k0 += 4) {
+    const float4 rb = r4[k0 / 4 + 1], llo = l4[-(k0 / 4)];
+    const float r[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};          // xo[ii + P + k0 + 0..7]
+    const float l[8] = {llo.x, llo.y, llo.z, llo.w, lhi.x, lhi.y, lhi.z, lhi.w};  // xo[ii + P - 4 - k0 + 0..7]
+#pragma unroll
+    for (int dk = 0; dk < 4; ++dk) {
+      const float g = fir.h[k0 + dk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = fmaf(g, l[3 - dk + j] + r[dk + j], acc[j]);
+    }
+    ra = rb;
+    lhi = llo;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (ii + j < n_out) y[b * Lout + i0 + ii + j] = acc[j];
+}
+
 // One octave: frames t < T_out of the centred complex conv at `hop`, written
 // to rows row0 + j (j >= skip) of out (B, n_bins, T_out).
 __global__ void octave_conv_kernel(const float* __restrict__ x, int64_t L, const float* __restrict__ k_re,
@@ -107,6 +158,84 @@ __global__ void octave_conv_kernel(const float* __restrict__ x, int64_t L, const
       o[0] = fmaf(re, re, im * im);
     } else {
       o[0] = sqrtf(fmaf(re, re, im * im));
+    }
+  }
+}
+
+// The same octave conv, one CTA per (128 frames, clip): the frames' signal span
+// (reflect / zero padded) and the bank sit in shared memory, thread = frame with
+// all 2 x n_filt accumulators in registers.  The span is stored skewed -- one pad
+// word per hop-length row -- so the lanes (frames hop samples apart) hit
+// distinct banks for every hop.  Same per-output FMA order as octave_conv_kernel.
+constexpr int kConvFrames = 128;
+
+template <int kMaxFilt>  // filters per octave, rounded up to 4 (12 for 12 bins per octave)
+__global__ void __launch_bounds__(kConvFrames) octave_conv_smem_kernel(
+    const float* __restrict__ x, int64_t L, const float* __restrict__ k_re, const float* __restrict__ k_im,
+    int32_t n_filt, int32_t width, int32_t hop, int32_t pad_mode, int32_t skip, int32_t row0, int32_t n_bins,
+    int32_t T_out, int32_t out_kind, float* __restrict__ out) {
+  extern __shared__ float sm[];
+  float* kr = sm;                          // [width][kMaxFilt]: tap-major, one row per tap
+  float* ki = kr + width * kMaxFilt;
+  float* sx = ki + width * kMaxFilt;       // skewed span
+  const int64_t b = blockIdx.y;
+  const int t0 = blockIdx.x * kConvFrames;
+  const int nf = min(kConvFrames, T_out - t0);
+  const int pad = width / 2;
+  const int span = (nf - 1) * hop + width;
+  const float* xb = x + b * L;
+  for (int e = threadIdx.x; e < width * kMaxFilt; e += blockDim.x) {
+    const int m = e / kMaxFilt, j = e - m * kMaxFilt;
+    kr[e] = j < n_filt ? __ldg(k_re + (int64_t)j * width + m) : 0.f;
+    ki[e] = j < n_filt ? __ldg(k_im + (int64_t)j * width + m) : 0.f;
+  }
+  const int64_t q0 = (int64_t)t0 * hop - pad;
+  for (int i = threadIdx.x; i < span; i += blockDim.x) {
+    const int64_t q = q0 + i;
+    float v;
+    if (pad_mode == NNAB_PAD_REFLECT) {
+      v = __ldg(xb + reflect_idx(q, L));
+    } else {
+      v = (q >= 0 && q < L) ? __ldg(xb + q) : 0.f;
+    }
+    sx[i + i / hop] = v;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t >= nf) return;
+  float re[kMaxFilt], im[kMaxFilt];
+#pragma unroll
+  for (int j = 0; j < kMaxFilt; ++j) re[j] = im[j] = 0.f;
+  for (int m = 0; m < width; ++m) {
+    const int r = t + m / hop, c = m - (m / hop) * hop;
+    const float v = sx[r * (hop + 1) + c];
+    const float4* kr4 = reinterpret_cast<const float4*>(kr + m * kMaxFilt);
+    const float4* ki4 = reinterpret_cast<const float4*>(ki + m * kMaxFilt);
+#pragma unroll
+    for (int j4 = 0; j4 < kMaxFilt / 4; ++j4) {
+      const float4 a = kr4[j4], bq = ki4[j4];
+      re[4 * j4] = fmaf(v, a.x, re[4 * j4]);
+      re[4 * j4 + 1] = fmaf(v, a.y, re[4 * j4 + 1]);
+      re[4 * j4 + 2] = fmaf(v, a.z, re[4 * j4 + 2]);
+      re[4 * j4 + 3] = fmaf(v, a.w, re[4 * j4 + 3]);
+      im[4 * j4] = fmaf(v, bq.x, im[4 * j4]);
+      im[4 * j4 + 1] = fmaf(v, bq.y, im[4 * j4 + 1]);
+      im[4 * j4 + 2] = fmaf(v, bq.z, im[4 * j4 + 2]);
+      im[4 * j4 + 3] = fmaf(v, bq.w, im[4 * j4 + 3]);
+    }
+  }
+  const int tt = t0 + t;
+#pragma unroll
+  for (int j = 0; j < kMaxFilt; ++j) {
+    if (j < skip || j >= n_filt) continue;
+    float* o = out + ((b * n_bins + row0 + j) * (int64_t)T_out + tt) * (out_kind == NNAB_OUT_COMPLEX ? 2 : 1);
+    if (out_kind == NNAB_OUT_COMPLEX) {
+      o[0] = re[j];
+      o[1] = im[j];
+    } else if (out_kind == NNAB_OUT_POWER) {
+      o[0] = fmaf(re[j], re[j], im[j] * im[j]);
+    } else {
+      o[0] = sqrtf(fmaf(re[j], re[j], im[j] * im[j]));
     }
   }
 }
@@ -188,11 +317,20 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
   const float* cur = x;
   int64_t cur_len = L;
   int pp = 0;
+  // half-band (pairs exactly at offsets 1, 3, .., 2P-1 with P % 4 == 0): the polyphase kernel
+  bool halfband = fp.n_pairs > 0 && fp.n_pairs % 4 == 0;
+  for (int k = 0; halfband && k < fp.n_pairs; ++k) halfband = fp.d[k] == 2 * k + 1;
   auto halve = [&]() -> int {
     const int64_t lo = halved(cur_len);
-    dim3 grid((unsigned)((lo + kSegOut - 1) / kSegOut), (unsigned)B);
-    const size_t smem = (size_t)(2 * (kSegOut - 1) + 2 * fp.half + 1) * sizeof(float);
-    halve_kernel<<<grid, 256, smem, s>>>(cur, cur_len, buf[pp], lo, fp);
+    if (halfband && cur_len > 2 * fp.n_pairs) {
+      const dim3 grid((unsigned)((lo + kHbOut - 1) / kHbOut), (unsigned)B);
+      const size_t smem = (size_t)(2 * kHbOut + 2 * fp.n_pairs + 4) * sizeof(float);
+      halfband_kernel<<<grid, 256, smem, s>>>(cur, cur_len, buf[pp], lo, fp);
+    } else {
+      dim3 grid((unsigned)((lo + kSegOut - 1) / kSegOut), (unsigned)B);
+      const size_t smem = (size_t)(2 * (kSegOut - 1) + 2 * fp.half + 1) * sizeof(float);
+      halve_kernel<<<grid, 256, smem, s>>>(cur, cur_len, buf[pp], lo, fp);
+    }
     NNAB_LAUNCHED();
     cur = buf[pp];
     cur_len = lo;
@@ -207,10 +345,22 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
     const int skip = std::max(0, a * bins_per_octave - first_bin);
     if (skip >= n_filters) continue;
     const int row0 = first_bin - a * bins_per_octave;
-    const int64_t total = B * (int64_t)(n_filters - skip) * T;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 32);
-    octave_conv_kernel<<<blocks, 256, 0, s>>>(cur, cur_len, k_re, k_im, n_filters, width, kernel_hop >> a, pad_mode,
-                                             skip, row0, n_bins, T, out_kind, out, B);
+    const int hop = kernel_hop >> a;
+    const int mf = n_filters <= 12 ? 12 : 16;
+    const size_t smem = (size_t)(2 * width * mf + ((kConvFrames - 1) * (int64_t)hop + width) * (hop + 1) / hop + 8) *
+                        sizeof(float);
+    if (n_filters <= 16 && smem <= 200 * 1024) {
+      auto kern = mf == 12 ? octave_conv_smem_kernel<12> : octave_conv_smem_kernel<16>;
+      NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const dim3 grid((unsigned)((T + kConvFrames - 1) / kConvFrames), (unsigned)B);
+      kern<<<grid, kConvFrames, smem, s>>>(cur, cur_len, k_re, k_im, n_filters, width, hop, pad_mode, skip, row0,
+                                           n_bins, T, out_kind, out);
+    } else {
+      const int64_t total = B * (int64_t)(n_filters - skip) * T;
+      const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 32);
+      octave_conv_kernel<<<blocks, 256, 0, s>>>(cur, cur_len, k_re, k_im, n_filters, width, hop, pad_mode, skip,
+                                               row0, n_bins, T, out_kind, out, B);
+    }
     NNAB_LAUNCHED();
   }
   return NNAB_OK;
