@@ -163,19 +163,24 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
           uint8_t* st = smem + s * C::STAGE;
           if (kPair) {  // both CTAs' bytes complete on the leader's barrier
             const uint32_t fb = mapa(&full[s], 0);
-            if (rank == 0) mbar_expect_tx(&full[s], 2 * (C::A_BYTES + kHalves * C::B_BYTES / 2));
+            if (rank == 0)
+              mbar_expect_tx(&full[s], 2 * (C::A_BYTES + kHalves * C::B_BYTES / 2) * (kSplit ? 2 : 1));
             tma_load_2d_pair(st, &ta_hi, fb, (int)k, mt * kBM, pol);
+            if (kSplit) tma_load_2d_pair(st + C::A_BYTES + C::B_BYTES, &ta_lo, fb, (int)k, mt * kBM, pol);
 #pragma unroll
             for (int h = 0; h < kHalves; ++h) {  // this CTA's half of each MMA's 256 columns
               const int nb = nt * TBN + h * kBN + (int)rank * kBNc;
               uint8_t* sb = st + C::A_BYTES + h * (C::B_BYTES / 2);
+              uint8_t* sb_lo = st + 2 * C::A_BYTES + C::B_BYTES;  // 3xTF32 (never wide)
               if (!p.b_mn) {
                 tma_load_2d_pair(sb, &tb_hi, fb, (int)k, nb, pol);
+                if (kSplit) tma_load_2d_pair(sb_lo, &tb_lo, fb, (int)k, nb, pol);
               } else {
                 int col = nb % p.b_row_len, row = (int)(k + nb / p.b_row_len);
 #pragma unroll 1
                 for (int j = 0; j < kBNc / 32; ++j) {
                   tma_load_2d_pair(sb + j * C::BK * 128, &tb_hi, fb, col, row, pol);
+                  if (kSplit) tma_load_2d_pair(sb_lo + j * C::BK * 128, &tb_lo, fb, col, row, pol);
                   if ((col += 32) == p.b_row_len) col = 0, ++row;  // b_row_len % 32 == 0
                 }
               }
@@ -240,12 +245,16 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
                 mma_tf32_pair(d, a + ao, b + bo, idesc, first ? 0u : 1u);
                 if (kWide)  // second 256 columns: B half staged B_BYTES/2 further on
                   mma_tf32_pair(d + kBN, a + ao, b + bo + (uint64_t)((C::B_BYTES / 2) >> 4), idesc, first ? 0u : 1u);
+                if (kSplit) {
+                  mma_tf32_pair(d + kBN, a + ao, b_lo + bo, idesc, first ? 0u : 1u);
+                  mma_tf32_pair(d + kBN, a_lo + ao, b + bo, idesc, 1u);
+                }
               } else {
                 mma_tf32(d, a + ao, b + bo, idesc, first ? 0u : 1u);
-              }
-              if (kSplit) {
-                mma_tf32(d + kBN, a + ao, b_lo + bo, idesc, first ? 0u : 1u);
-                mma_tf32(d + kBN, a_lo + ao, b + bo, idesc, 1u);
+                if (kSplit) {
+                  mma_tf32(d + kBN, a + ao, b_lo + bo, idesc, first ? 0u : 1u);
+                  mma_tf32(d + kBN, a_lo + ao, b + bo, idesc, 1u);
+                }
               }
               first = false;
             }
@@ -491,7 +500,7 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, g.a_lo, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
   if (!g.b_mn) {
     if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBNc, C::SWZ);
-    if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, g.b_lo, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBN, C::SWZ);
+    if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, g.b_lo, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBNc, C::SWZ);
   } else {
     // rows of b_row_len floats; b_rows rows in total; boxes of 32 columns x BK rows, 128-byte swizzle
     if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 4, 32, C::BK, -128);
@@ -588,7 +597,10 @@ int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s) {
     return e ? e[0] - '0' : 1;
   }();
   const bool pair_ok = pair_env != 0;
-  if (precision == NNAB_PREC_3XTF32) return launch<true, false>(g, s);
+  if (precision == NNAB_PREC_3XTF32) {  // CTA pairs too (the long reductions are L2-bound)
+    const bool pair = pair_ok && (pair_env >= 2 || g.M > kBM);
+    return pair ? launch<true, true>(g, s) : launch<true, false>(g, s);
+  }
   if (precision == NNAB_PREC_TF32) {
     const bool pair = pair_ok && (pair_env >= 2 || g.M > kBM);  // one m tile: the peer would idle
     const bool wide = pair && !g.coef_re && (pair_env == 3 || (pair_env == 1 && g.N > kBN && g.K >= 65536));
