@@ -273,28 +273,32 @@ int nnab_cqt1992v2_egemm_staged(const nnab_frames* f, const float* packed_hi, co
                                 int32_t r_max, int32_t n_bins,
                                 int32_t out_kind, float eps, float* out, const void* workspace,
                                 size_t workspace_bytes, void* stream);
-/* CQT1992v2 hybrid (TF32): bins [0, n_long) on the E-GEMM (eg_bank/col_table/
+/* CQT1992v2 hybrid: bins [0, n_long) on the E-GEMM (eg_bank/col_table/
  * group_rows/n_groups/r_max from nnab_cqt_egemm_plan + nnab_pack_cqt_egemm over
  * those bins), bins [n_long, n_bins) on the per-K-block schedule (sched_bank and
  * schedule of those rows at the same width), both from one staging of the
- * frames; out (B, n_bins, T).  Replaces the reference's single DGEMM
- * (transforms.py:175-208). */
-int nnab_cqt1992v2_hybrid_staged(const nnab_frames* f, const float* eg_bank, const uint16_t* col_table,
-                                 const int32_t* group_rows, int32_t n_groups, int32_t r_max, const float* sched_bank,
+ * frames; out (B, n_bins, T).  TF32, or 3xTF32 with the *_lo banks (the
+ * E-GEMM then runs as CTA pairs with main + correction accumulators).
+ * Replaces the reference's single DGEMM (transforms.py:175-208). */
+int nnab_cqt1992v2_hybrid_staged(const nnab_frames* f, const float* eg_bank, const float* eg_bank_lo,
+                                 const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups,
+                                 int32_t r_max, const float* sched_bank, const float* sched_bank_lo,
                                  const uint32_t* schedule, int32_t n_entries, int32_t n_long, int32_t n_bins,
-                                 int32_t out_kind, float eps, float* out, const void* workspace,
+                                 int32_t precision, int32_t out_kind, float eps, float* out, const void* workspace,
                                  size_t workspace_bytes, void* stream);
 int nnab_cqt1992v2_hybrid_forward(const nnab_frames* f, const float* x, const float* eg_bank,
-                                  const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups,
-                                  int32_t r_max, const float* sched_bank, const uint32_t* schedule, int32_t n_entries,
-                                  int32_t n_long, int32_t n_bins, int32_t out_kind, float eps, float* out,
-                                  void* workspace, size_t workspace_bytes, void* stream);
-/* pinned host (B, L) -> pinned host (B, n_bins, T); scratch: nnab_cqt1992v2_host_scratch_bytes(TF32) */
+                                  const float* eg_bank_lo, const uint16_t* col_table, const int32_t* group_rows,
+                                  int32_t n_groups, int32_t r_max, const float* sched_bank,
+                                  const float* sched_bank_lo, const uint32_t* schedule, int32_t n_entries,
+                                  int32_t n_long, int32_t n_bins, int32_t precision, int32_t out_kind, float eps,
+                                  float* out, void* workspace, size_t workspace_bytes, void* stream);
+/* pinned host (B, L) -> pinned host (B, n_bins, T); scratch: nnab_cqt1992v2_host_scratch_bytes(precision) */
 int nnab_cqt1992v2_hybrid_forward_host(const nnab_frames* f, const float* x_host, const float* eg_bank,
-                                       const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups,
-                                       int32_t r_max, const float* sched_bank, const uint32_t* schedule,
-                                       int32_t n_entries, int32_t n_long, int32_t n_bins, int32_t out_kind, float eps,
-                                       float* out_host, int64_t chunk_clips, void* device_scratch,
+                                       const float* eg_bank_lo, const uint16_t* col_table, const int32_t* group_rows,
+                                       int32_t n_groups, int32_t r_max, const float* sched_bank,
+                                       const float* sched_bank_lo, const uint32_t* schedule, int32_t n_entries,
+                                       int32_t n_long, int32_t n_bins, int32_t precision, int32_t out_kind,
+                                       float eps, float* out_host, int64_t chunk_clips, void* device_scratch,
                                        size_t scratch_bytes, void* stream);
 
 /* Host-buffer end-to-end variant of nnab_cqt1992v2_forward (pinned x_host ->

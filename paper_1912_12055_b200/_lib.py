@@ -83,12 +83,12 @@ SIGNATURES = {
     "nnab_pack_cqt_egemm": (C.c_int, [_fp, _fp, _i32, _i32, _vp, _ip, _i32, _i32, _fp, _fp, _vp]),
     "nnab_cqt1992v2_egemm_staged": (C.c_int, [_FR, _fp, _vp, _ip, _vp, _i32, _i32, _i32, _i32, _f32, _fp, _vp,
                                               _sz, _vp]),
-    "nnab_cqt1992v2_hybrid_staged": (C.c_int, [_FR, _fp, _vp, _ip, _i32, _i32, _fp, _ip, _i32, _i32, _i32, _i32,
-                                               _f32, _fp, _vp, _sz, _vp]),
-    "nnab_cqt1992v2_hybrid_forward": (C.c_int, [_FR, _fp, _fp, _vp, _ip, _i32, _i32, _fp, _ip, _i32, _i32, _i32,
-                                                _i32, _f32, _fp, _vp, _sz, _vp]),
-    "nnab_cqt1992v2_hybrid_forward_host": (C.c_int, [_FR, _fp, _fp, _vp, _ip, _i32, _i32, _fp, _ip, _i32, _i32,
-                                                     _i32, _i32, _f32, _fp, _i64, _vp, _sz, _vp]),
+    "nnab_cqt1992v2_hybrid_staged": (C.c_int, [_FR, _fp, _fp, _vp, _ip, _i32, _i32, _fp, _fp, _ip, _i32, _i32, _i32,
+                                               _i32, _i32, _f32, _fp, _vp, _sz, _vp]),
+    "nnab_cqt1992v2_hybrid_forward": (C.c_int, [_FR, _fp, _fp, _fp, _vp, _ip, _i32, _i32, _fp, _fp, _ip, _i32,
+                                                _i32, _i32, _i32, _i32, _f32, _fp, _vp, _sz, _vp]),
+    "nnab_cqt1992v2_hybrid_forward_host": (C.c_int, [_FR, _fp, _fp, _fp, _vp, _ip, _i32, _i32, _fp, _fp, _ip,
+                                                     _i32, _i32, _i32, _i32, _i32, _f32, _fp, _i64, _vp, _sz, _vp]),
     "nnab_cqt1992v2_host_scratch_bytes": (_sz, [_FR, _i32, _i32, _i32, _i64]),
     "nnab_cqt1992v2_forward_host": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _ip, _i32, _i32, _i32, _f32, _fp, _i64,
                                               _vp, _sz, _vp]),

@@ -354,14 +354,15 @@ extern "C" int nnab_cqt1992v2_forward_host(const nnab_frames* f, const float* x_
 }
 
 // Hybrid CQT1992v2 (nnab_cqt1992v2_hybrid_staged) streamed from pinned host
-// memory; scratch as nnab_cqt1992v2_host_scratch_bytes(f, TF32, n_bins, ...).
+// memory; scratch as nnab_cqt1992v2_host_scratch_bytes(f, precision, n_bins, ...).
 extern "C" int nnab_cqt1992v2_hybrid_forward_host(const nnab_frames* f, const float* x_host, const float* eg_bank,
-                                                  const uint16_t* col_table, const int32_t* group_rows,
-                                                  int32_t n_groups, int32_t r_max, const float* sched_bank,
+                                                  const float* eg_bank_lo, const uint16_t* col_table,
+                                                  const int32_t* group_rows, int32_t n_groups, int32_t r_max,
+                                                  const float* sched_bank, const float* sched_bank_lo,
                                                   const uint32_t* schedule, int32_t n_entries, int32_t n_long,
-                                                  int32_t n_bins, int32_t out_kind, float eps, float* out_host,
-                                                  int64_t chunk_clips, void* device_scratch, size_t scratch_bytes,
-                                                  void* stream) {
+                                                  int32_t n_bins, int32_t precision, int32_t out_kind, float eps,
+                                                  float* out_host, int64_t chunk_clips, void* device_scratch,
+                                                  size_t scratch_bytes, void* stream) {
   int rc = check_device();
   if (rc) return rc;
   FrameGeom g;
@@ -369,21 +370,21 @@ extern "C" int nnab_cqt1992v2_hybrid_forward_host(const nnab_frames* f, const fl
   if (!x_host || !out_host || chunk_clips < 1) return NNAB_EINVAL;
   if (g.B == 0) return NNAB_OK;
   const int64_t chunk = std::min<int64_t>(chunk_clips, g.B);
-  if (!device_scratch ||
-      scratch_bytes < nnab_cqt1992v2_host_scratch_bytes(f, NNAB_PREC_TF32, n_bins, out_kind, chunk))
+  if (!device_scratch || scratch_bytes < nnab_cqt1992v2_host_scratch_bytes(f, precision, n_bins, out_kind, chunk))
     return NNAB_EINVAL;
   const int64_t per = (out_kind == NNAB_OUT_COMPLEX ? 2ll : 1ll) * n_bins * g.T;
   nnab_frames fc = *f;
   fc.batch = chunk;
   char* base = reinterpret_cast<char*>(device_scratch);
   void* ws = base + pipeline_bytes(chunk, g.L, per);
-  const size_t ws_bytes = nnab_stft_workspace_bytes(&fc, NNAB_PREC_TF32);
+  const size_t ws_bytes = nnab_stft_workspace_bytes(&fc, precision);
   return host_pipeline(g.B, g.L, per, chunk, x_host, out_host, base, (cudaStream_t)stream,
                        [&](const float* xd, int64_t nb, float* od) {
                          fc.batch = nb;
-                         return nnab_cqt1992v2_hybrid_forward(&fc, xd, eg_bank, col_table, group_rows, n_groups,
-                                                              r_max, sched_bank, schedule, n_entries, n_long, n_bins,
-                                                              out_kind, eps, od, ws, ws_bytes, stream);
+                         return nnab_cqt1992v2_hybrid_forward(&fc, xd, eg_bank, eg_bank_lo, col_table, group_rows,
+                                                              n_groups, r_max, sched_bank, sched_bank_lo, schedule,
+                                                              n_entries, n_long, n_bins, precision, out_kind, eps, od,
+                                                              ws, ws_bytes, stream);
                        });
 }
 

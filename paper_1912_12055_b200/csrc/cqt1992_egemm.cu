@@ -78,28 +78,36 @@ NNAB_DEV uint64_t sdesc(const void* p) {  // K-major, 128-byte swizzle, 8-row at
 NNAB_DEV void ep_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // epilogue warps 4-7
 
 // Pipeline geometry: single CTAs stage A (16 KB) + all of B (32 KB) x 3; a CTA
-// pair (kPair) stages A + half of B (16 + 16 KB) x 4.
-template <bool kPair>
+// pair (kPair) stages A + half of B (16 + 16 KB) x 4; 3xTF32 (kSplit, pairs)
+// stages hi and lo of both (64 KB) x 2.
+template <bool kPair, bool kSplit = false>
 struct ECfg {
-  static constexpr int STAGES = kPair ? 4 : 3;
+  static constexpr int STAGES = kSplit ? 2 : kPair ? 4 : 3;
   static constexpr int B_ROWS = kPair ? kBN / 2 : kBN;
-  static constexpr int STAGE = kA + B_ROWS * kBK * 4;
+  static constexpr int HALF = kA + B_ROWS * kBK * 4;  // the hi (or lo) operands
+  static constexpr int STAGE = HALF * (kSplit ? 2 : 1);
+  static constexpr int NACC = kSplit ? 1 : 2;  // 3xTF32: main + correction fill TMEM
 };
-template <bool kPair>
+template <bool kPair, bool kSplit = false>
 constexpr size_t egemm_smem() {
-  return 1024 + (size_t)ECfg<kPair>::STAGES * ECfg<kPair>::STAGE + (size_t)4 * kRows * kRing * 4 + kBN * 2 +
-         kRows * 4 + 16 * 8;
+  return 1024 + (size_t)ECfg<kPair, kSplit>::STAGES * ECfg<kPair, kSplit>::STAGE + (size_t)4 * kRows * kRing * 4 +
+         kBN * 2 + kRows * 4 + 16 * 8;
 }
 
 // kPair: a cluster of two CTAs of the same group runs two independent tile runs
 // in lockstep with cta_group::2 MMAs (M = 256: each CTA's A tile, the group's
 // B columns split between them), ~25 % more MMA throughput per SM; each CTA's
 // epilogue and D rings stay its own.
-template <bool kPair>
+// kSplit (3xTF32, FP32-accurate): E = A_hi B_hi (main accumulator) +
+// (A_hi B_lo + A_lo B_hi) (correction accumulator), summed in the epilogue.
+template <bool kPair, bool kSplit = false>
 __global__ void __launch_bounds__(kThreads, 1)
     cqt1992_egemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                         const __grid_constant__ CUtensorMap tm_a_lo, const __grid_constant__ CUtensorMap tm_b_lo,
                          const EParams p) {
-  using EC = ECfg<kPair>;
+  using EC = ECfg<kPair, kSplit>;
+  static_assert(!kSplit || kPair, "3xTF32 E-GEMM runs as CTA pairs");
+  constexpr int NACC = EC::NACC;
   constexpr int kStages = EC::STAGES, kStage = EC::STAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -167,6 +175,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (rank == 0) mbar_expect_tx(&full[s], 2 * kStage);
               tma_load_2d_pair(st, &tm_a, fb, kb * kBK, m * kBM, keep);
               tma_load_2d_pair(st + kA, &tm_b, fb, kb * kBK, g * kBN + (int)rank * EC::B_ROWS, keep);
+              if (kSplit) {
+                tma_load_2d_pair(st + EC::HALF, &tm_a_lo, fb, kb * kBK, m * kBM, keep);
+                tma_load_2d_pair(st + EC::HALF + kA, &tm_b_lo, fb, kb * kBK, g * kBN + (int)rank * EC::B_ROWS,
+                                 keep);
+              }
             } else {
               mbar_expect_tx(&full[s], kStage);
               tma_load_2d_hint(st, &tm_a, &full[s], kb * kBK, m * kBM, keep);
@@ -194,10 +207,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             uint8_t* st = smem + s * kStage;
             const uint64_t a = sdesc(st), b = sdesc(st + kA);
+            const uint64_t a_lo = sdesc(st + EC::HALF), b_lo = sdesc(st + EC::HALF + kA);
 #pragma unroll
             for (int k = 0; k < kBK / 8; ++k) {
               if (kPair) mma_tf32_pair(d, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
               else mma_tf32(d, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
+              if (kSplit) {
+                mma_tf32_pair(d + kBN, a + 2 * k, b_lo + 2 * k, idesc, (kb | k) != 0);
+                mma_tf32_pair(d + kBN, a_lo + 2 * k, b + 2 * k, idesc, 1u);
+              }
             }
             if (kPair) mma_commit_pair(&empty[s], 0x3);
             else mma_commit(&empty[s]);
@@ -208,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (kPair) mma_commit_pair(&tfull[acc], 0x3);
           else mma_commit(&tfull[acc]);
-          if (++acc == 2) {
+          if (++acc == NACC) {
             acc = 0;
             aph ^= 1;
           }
@@ -242,7 +260,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c0 = 0; c0 < n_cols; c0 += 32) {
           float v[32];
           tmem_ld32(ta + c0, v);
-          tmem_ld_wait();
+          if (kSplit) {
+            float u[32];
+            tmem_ld32(ta + kBN + c0, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += u[j];
+          } else {
+            tmem_ld_wait();
+          }
           // The plan lays each bank row's columns out as whole windows of 16
           // consecutive r (zero-weight padding past the support).  Column k of a
           // window (row, r0 + k): lane l gathers E[s_l + k][k] from lane (l + k) mod
@@ -274,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (kPair) mbar_arrive_cluster(mapa(&tempty[acc], 0));
           else mbar_arrive(&tempty[acc]);
         }
-        if (++acc == 2) {
+        if (++acc == NACC) {
           acc = 0;
           aph ^= 1;
         }
@@ -454,35 +480,49 @@ int cqt_schedule_staged(const nnab_frames* f, const float* packed_hi, const floa
 
 // E-GEMM on staged frames (TF32): the group tables' bins are written into an
 // output of out_bins bins per clip (group_rows hold global bank rows).
-static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const uint16_t* col_table,
-                            const int32_t* group_rows, int32_t n_groups, int32_t r_max, int32_t out_bins,
-                            int32_t out_kind, float eps, float* out, const void* workspace, size_t workspace_bytes,
-                            cudaStream_t stream) {
+static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
+                            const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups, int32_t r_max,
+                            int32_t out_bins, int32_t out_kind, float eps, float* out, const void* workspace,
+                            size_t workspace_bytes, int32_t precision, cudaStream_t stream) {
   FrameGeom g;
   int rc = frame_geometry(f, &g);
   if (rc) return rc;
-  if (!packed_hi || !col_table || !group_rows || !out || n_groups < 1 || out_bins < 1) return NNAB_EINVAL;
+  const bool split = precision == NNAB_PREC_3XTF32;
+  if (precision != NNAB_PREC_TF32 && !split) return NNAB_EINVAL;
+  if (!packed_hi || (split && !packed_lo) || !col_table || !group_rows || !out || n_groups < 1 || out_bins < 1)
+    return NNAB_EINVAL;
   if (r_max < 0 || r_max + kBM > kRing) return NNAB_EINVAL;
   if (g.row_len != g.hop || g.hop % kBK != 0 || g.hop / kBK != 16) return NNAB_ENOTSUP;  // K = hop = 512
   if (out_kind != NNAB_OUT_MAGNITUDE && out_kind != NNAB_OUT_POWER && out_kind != NNAB_OUT_COMPLEX &&
       out_kind != NNAB_OUT_SMOOTH_MAG)
     return NNAB_EINVAL;
   if (g.B == 0) return NNAB_OK;
-  if (!workspace || workspace_bytes < nnab_stft_workspace_bytes(f, NNAB_PREC_TF32)) return NNAB_EINVAL;
+  const size_t need = nnab_stft_workspace_bytes(f, precision);
+  if (!workspace || workspace_bytes < need) return NNAB_EINVAL;
   const int nsm = num_sms();
   if (n_groups > nsm) return NNAB_ENOTSUP;
   static const bool pair_ok = [] {
     const char* e = getenv("NNAB_EGEMM_PAIR");
     return !(e && e[0] == '0');
   }();
-  const bool pair = pair_ok && nsm / n_groups >= 2;
-  CUtensorMap ta, tb;
+  const bool pair = (pair_ok || split) && nsm / n_groups >= 2;
+  if (split && !pair) return NNAB_ENOTSUP;  // 3xTF32 runs as CTA pairs only
+  CUtensorMap ta, tb, ta_lo, tb_lo;
   const uint64_t rows_total = (uint64_t)g.B * g.R;
+  const int b_box = pair ? kBN / 2 : kBN;
   rc = make_tmap_2d(&ta, workspace, g.row_len, rows_total, (uint64_t)g.row_len * 4, kBK, kBM, 128);
-  if (!rc)
-    rc = make_tmap_2d(&tb, packed_hi, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * 4, kBK, pair ? kBN / 2 : kBN,
-                      128);
+  if (!rc) rc = make_tmap_2d(&tb, packed_hi, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * 4, kBK, b_box, 128);
+  if (!rc && split) {  // staged rows: hi then lo halves of the workspace (as cqt1992.cu)
+    const void* rows_lo = reinterpret_cast<const char*>(workspace) + need / 2;
+    rc = make_tmap_2d(&ta_lo, rows_lo, g.row_len, rows_total, (uint64_t)g.row_len * 4, kBK, kBM, 128);
+    if (!rc)
+      rc = make_tmap_2d(&tb_lo, packed_lo, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * 4, kBK, b_box, 128);
+  }
   if (rc) return rc;
+  if (!split) {
+    ta_lo = ta;
+    tb_lo = tb;
+  }
   EParams p{};
   p.B = g.B;
   p.R = g.R;
@@ -502,11 +542,11 @@ static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const 
     const size_t smem = egemm_smem<false>();
     NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt1992_egemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    cqt1992_egemm_kernel<false><<<grid, kThreads, smem, stream>>>(ta, tb, p);
+    cqt1992_egemm_kernel<false><<<grid, kThreads, smem, stream>>>(ta, tb, ta_lo, tb_lo, p);
   } else {
-    const size_t smem = egemm_smem<true>();
-    NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt1992_egemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+    auto kern = split ? cqt1992_egemm_kernel<true, true> : cqt1992_egemm_kernel<true, false>;
+    const size_t smem = split ? egemm_smem<true, true>() : egemm_smem<true, false>();
+    NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -519,7 +559,7 @@ static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    NNAB_CUDA_TRY(cudaLaunchKernelEx(&cfg, cqt1992_egemm_kernel<true>, ta, tb, p));
+    NNAB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, ta_lo, tb_lo, p));
   }
   NNAB_LAUNCHED();
   return NNAB_OK;
@@ -535,47 +575,49 @@ extern "C" int nnab_cqt1992v2_egemm_staged(const nnab_frames* f, const float* pa
                                            const void* workspace, size_t workspace_bytes, void* stream) {
   (void)run_table;
   if (n_bins < 1) return NNAB_EINVAL;
-  return cqt_egemm_staged(f, packed_hi, col_table, group_rows, n_groups, r_max, n_bins, out_kind, eps, out,
-                          workspace, workspace_bytes, (cudaStream_t)stream);
+  return cqt_egemm_staged(f, packed_hi, nullptr, col_table, group_rows, n_groups, r_max, n_bins, out_kind, eps, out,
+                          workspace, workspace_bytes, NNAB_PREC_TF32, (cudaStream_t)stream);
 }
 
 // CQT1992v2 hybrid on staged frames (TF32): bins [0, n_long) -- the long,
 // low-frequency kernels -- on the E-GEMM (tables from nnab_cqt_egemm_plan over
 // those bins), bins [n_long, n_bins) on the per-K-block schedule (bank and
 // schedule of those rows at the full width, so both share the staged frames).
-extern "C" int nnab_cqt1992v2_hybrid_staged(const nnab_frames* f, const float* eg_bank, const uint16_t* col_table,
-                                            const int32_t* group_rows, int32_t n_groups, int32_t r_max,
-                                            const float* sched_bank, const uint32_t* schedule, int32_t n_entries,
-                                            int32_t n_long, int32_t n_bins, int32_t out_kind, float eps, float* out,
-                                            const void* workspace, size_t workspace_bytes, void* stream) {
+extern "C" int nnab_cqt1992v2_hybrid_staged(const nnab_frames* f, const float* eg_bank, const float* eg_bank_lo,
+                                            const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups,
+                                            int32_t r_max, const float* sched_bank, const float* sched_bank_lo,
+                                            const uint32_t* schedule, int32_t n_entries, int32_t n_long,
+                                            int32_t n_bins, int32_t precision, int32_t out_kind, float eps,
+                                            float* out, const void* workspace, size_t workspace_bytes, void* stream) {
   if (n_long < 0 || n_long > n_bins || n_bins < 1 || !out) return NNAB_EINVAL;
   FrameGeom g;
   int rc = frame_geometry(f, &g);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (n_long > 0) {
-    rc = cqt_egemm_staged(f, eg_bank, col_table, group_rows, n_groups, r_max, n_bins, out_kind, eps, out, workspace,
-                          workspace_bytes, s);
+    rc = cqt_egemm_staged(f, eg_bank, eg_bank_lo, col_table, group_rows, n_groups, r_max, n_bins, out_kind, eps, out,
+                          workspace, workspace_bytes, precision, s);
     if (rc) return rc;
   }
   if (n_long < n_bins) {
     float* o = out + (int64_t)n_long * g.T * (out_kind == NNAB_OUT_COMPLEX ? 2 : 1);
-    rc = cqt_schedule_staged(f, sched_bank, nullptr, n_bins - n_long, schedule, n_entries, NNAB_PREC_TF32, out_kind,
+    rc = cqt_schedule_staged(f, sched_bank, sched_bank_lo, n_bins - n_long, schedule, n_entries, precision, out_kind,
                              eps, o, n_bins, workspace, workspace_bytes, s);
   }
   return rc;
 }
 
 extern "C" int nnab_cqt1992v2_hybrid_forward(const nnab_frames* f, const float* x, const float* eg_bank,
-                                             const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups,
-                                             int32_t r_max, const float* sched_bank, const uint32_t* schedule,
-                                             int32_t n_entries, int32_t n_long, int32_t n_bins, int32_t out_kind,
-                                             float eps, float* out, void* workspace, size_t workspace_bytes,
-                                             void* stream) {
+                                             const float* eg_bank_lo, const uint16_t* col_table,
+                                             const int32_t* group_rows, int32_t n_groups, int32_t r_max,
+                                             const float* sched_bank, const float* sched_bank_lo,
+                                             const uint32_t* schedule, int32_t n_entries, int32_t n_long,
+                                             int32_t n_bins, int32_t precision, int32_t out_kind, float eps,
+                                             float* out, void* workspace, size_t workspace_bytes, void* stream) {
   if (!x) return NNAB_EINVAL;
-  int rc = nnab_stage_frames(f, x, NNAB_PREC_TF32, workspace, workspace_bytes, stream);
+  int rc = nnab_stage_frames(f, x, precision, workspace, workspace_bytes, stream);
   if (rc) return rc;
-  return nnab_cqt1992v2_hybrid_staged(f, eg_bank, col_table, group_rows, n_groups, r_max, sched_bank, schedule,
-                                      n_entries, n_long, n_bins, out_kind, eps, out, workspace, workspace_bytes,
-                                      stream);
+  return nnab_cqt1992v2_hybrid_staged(f, eg_bank, eg_bank_lo, col_table, group_rows, n_groups, r_max, sched_bank,
+                                      sched_bank_lo, schedule, n_entries, n_long, n_bins, precision, out_kind, eps,
+                                      out, workspace, workspace_bytes, stream);
 }

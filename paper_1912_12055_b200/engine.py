@@ -305,19 +305,18 @@ class CqtLongEngine:
         di = torch.as_tensor(k_im).to(self.device, torch.float32).contiguous()
         self.schedule, self.n_entries, self.packed_hi, self.packed_lo = self._schedule(sup, dr, di)
         self.egemm = self.hybrid = None
-        eg_ok = self.precision == L.PREC_TF32 and self.hop == 512 and kr is not None and not dense
-        if self.method == "hybrid" and eg_ok:
+        eg_ok = self.hop == 512 and kr is not None and not dense
+        if self.method == "hybrid" and eg_ok:  # TF32 or 3xTF32
             span = sup[:, 1] - sup[:, 0]
             n_long = 0
             while n_long < self.n_bins and span[n_long] >= self.LONG_HOPS * self.hop:
                 n_long += 1
             eg = self._egemm_tables(sup[:n_long], dr[:n_long], di[:n_long]) if n_long else None
-            if n_long == self.n_bins:
-                self.egemm = eg
-            elif eg is not None:
-                sch, n_ent, hi, _ = self._schedule(sup[n_long:], dr[n_long:].contiguous(), di[n_long:].contiguous())
-                self.hybrid = (eg, sch, n_ent, hi, n_long)
-        elif self.method == "egemm" and eg_ok:
+            if eg is not None:
+                sch, n_ent, hi, lo = (self._schedule(sup[n_long:], dr[n_long:].contiguous(), di[n_long:].contiguous())
+                                      if n_long < self.n_bins else (None, 0, None, None))
+                self.hybrid = (eg, sch, n_ent, hi, lo, n_long)
+        elif self.method == "egemm" and eg_ok and self.precision == L.PREC_TF32:
             self.egemm = self._egemm_tables(sup, dr, di)
 
     def _egemm_tables(self, sup, dr, di):
@@ -337,12 +336,14 @@ class CqtLongEngine:
             col_t = torch.from_numpy(ct[: n * 256].view(np.int16).copy()).to(self.device)
             rows_t = torch.from_numpy(gr[: n * 64].copy()).to(self.device)
             runs_t = torch.from_numpy(rt[: n * 4 * 65].view(np.int32).copy()).to(self.device)
-            bank = torch.empty(lib.nnab_cqt_egemm_bank_bytes(n, self.hop) // 4, dtype=torch.float32,
-                               device=self.device)
+            nb = lib.nnab_cqt_egemm_bank_bytes(n, self.hop) // 4
+            bank = torch.empty(nb, dtype=torch.float32, device=self.device)
+            bank_lo = (torch.empty(nb, dtype=torch.float32, device=self.device)
+                       if self.precision == L.PREC_3XTF32 else None)
             L.check(lib.nnab_pack_cqt_egemm(dr.data_ptr(), di.data_ptr(), self.width, self.hop, col_t.data_ptr(),
-                                            rows_t.data_ptr(), n, self.precision, bank.data_ptr(), None,
+                                            rows_t.data_ptr(), n, self.precision, bank.data_ptr(), L.ptr(bank_lo),
                                             L.stream_handle(self.device)), "pack_cqt_egemm")
-            return (bank, col_t, rows_t, runs_t, n, rm.value)
+            return (bank, col_t, rows_t, runs_t, n, rm.value, bank_lo)
         return None
 
     def frames(self, B: int, length: int) -> L.nnab_frames:
@@ -385,15 +386,16 @@ class CqtLongEngine:
         f = self.frames(B, length)
         ws = self._ws.buf
         if self.hybrid is not None:
-            (bank, col_t, rows_t, _, n, rmax), sch, n_ent, s_hi, n_long = self.hybrid
-            L.check(lib.nnab_cqt1992v2_hybrid_staged(C.byref(f), bank.data_ptr(), col_t.data_ptr(), rows_t.data_ptr(),
-                                                     n, rmax, s_hi.data_ptr(), sch.data_ptr(), n_ent, n_long,
-                                                     self.n_bins, kinds[kind], float(eps), out.data_ptr(),
-                                                     ws.data_ptr(), ws.numel(), L.stream_handle(self.device)),
+            (bank, col_t, rows_t, _, n, rmax, bank_lo), sch, n_ent, s_hi, s_lo, n_long = self.hybrid
+            L.check(lib.nnab_cqt1992v2_hybrid_staged(C.byref(f), bank.data_ptr(), L.ptr(bank_lo), col_t.data_ptr(),
+                                                     rows_t.data_ptr(), n, rmax, L.ptr(s_hi), L.ptr(s_lo),
+                                                     L.ptr(sch), n_ent, n_long, self.n_bins, self.precision,
+                                                     kinds[kind], float(eps), out.data_ptr(), ws.data_ptr(),
+                                                     ws.numel(), L.stream_handle(self.device)),
                     "cqt1992v2_hybrid_staged")
             return out
         if self.egemm is not None:
-            bank, col_t, rows_t, runs_t, n, rmax = self.egemm
+            bank, col_t, rows_t, runs_t, n, rmax, _ = self.egemm
             rc = lib.nnab_cqt1992v2_egemm_staged(C.byref(f), bank.data_ptr(), col_t.data_ptr(), rows_t.data_ptr(),
                                                  runs_t.data_ptr(), n, rmax, self.n_bins, kinds[kind], float(eps),
                                                  out.data_ptr(),
@@ -423,12 +425,12 @@ class CqtLongEngine:
         ws = self._ws.get(lib.nnab_cqt1992v2_host_scratch_bytes(C.byref(f), self.precision, self.n_bins, k,
                                                                  chunk_clips), self.device)
         if self.hybrid is not None:
-            (bank, col_t, rows_t, _, n, rmax), sch, n_ent, s_hi, n_long = self.hybrid
+            (bank, col_t, rows_t, _, n, rmax, bank_lo), sch, n_ent, s_hi, s_lo, n_long = self.hybrid
             L.check(lib.nnab_cqt1992v2_hybrid_forward_host(
-                C.byref(f), x_host.data_ptr(), bank.data_ptr(), col_t.data_ptr(), rows_t.data_ptr(), n, rmax,
-                s_hi.data_ptr(), sch.data_ptr(), n_ent, n_long, self.n_bins, k, float(eps), out_host.data_ptr(),
-                int(chunk_clips), ws.data_ptr(), ws.numel(), L.stream_handle(self.device)),
-                "cqt1992v2_hybrid_forward_host")
+                C.byref(f), x_host.data_ptr(), bank.data_ptr(), L.ptr(bank_lo), col_t.data_ptr(), rows_t.data_ptr(),
+                n, rmax, L.ptr(s_hi), L.ptr(s_lo), L.ptr(sch), n_ent, n_long, self.n_bins, self.precision, k,
+                float(eps), out_host.data_ptr(), int(chunk_clips), ws.data_ptr(), ws.numel(),
+                L.stream_handle(self.device)), "cqt1992v2_hybrid_forward_host")
             return out_host
         L.check(lib.nnab_cqt1992v2_forward_host(
             C.byref(f), x_host.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins,

@@ -181,7 +181,20 @@ def test_cqt1992v2_default_is_hybrid(cuda_dev):
     cfg = O.CqtCfg(sr=SR)
     e = long_engine(cfg, "tf32")
     assert e.hybrid is not None
-    assert long_engine(cfg, "3xtf32").hybrid is None  # FP32-accurate mode: schedule only
+    assert long_engine(cfg, "3xtf32").hybrid is not None  # FP32-accurate mode: 3xTF32 E-GEMM + schedule
+
+
+def test_cqt1992v2_hybrid_3xtf32_matches_oracle(golden, cuda_dev):
+    """The 3xTF32 hybrid (E-GEMM with main + correction accumulators) at the FP32
+    tolerance, against the schedule in the same precision and the golden output."""
+    cfg = O.CqtCfg(sr=SR)
+    x = torch.from_numpy(golden["clips"]).to(cuda_dev)
+    a = long_engine(cfg, "3xtf32")
+    b = long_engine(cfg, "3xtf32", method="schedule")
+    for kind in ("magnitude", "complex"):
+        ga, gb = a.forward(x, kind).cpu().numpy(), b.forward(x, kind).cpu().numpy()
+        assert O.peak_err(ga, gb) < 1e-5, (kind, O.peak_err(ga, gb))
+    assert O.peak_err(a.forward(x).cpu().numpy(), golden["cqt1992v2_full"]) <= 1e-5
 
 
 def test_frequency_domain_variants_golden(golden, cuda_dev):
