@@ -116,22 +116,29 @@ def test_joint_mel_stft_batch_vs_oracle(cuda_dev, precision):
 def test_trainable_stft_module_step_changes_bank(cuda_dev):
     from paper_1912_12055_b200.layers import STFT
     m = STFT(n_fft=256, hop_length=64, sr=8000, trainable=True, precision="fp32")
-    x = torch.randn(4, 4000, device=cuda_dev)
+    x = torch.randn(4, 4000, device=cuda_dev, generator=torch.Generator(device=cuda_dev).manual_seed(4))
     opt = torch.optim.SGD(m.parameters(), lr=1e-3)
     a = m(x).sum()
     a.backward()
     opt.step()
     b = m(x).sum()  # repacked bank after the in-place update
     assert float(a.detach()) != float(b.detach())
-    # input gradient through the non-trainable layer (gradients.py:133-149)
-    m2 = STFT(n_fft=128, hop_length=32, sr=8000)
-    xr = torch.randn(2, 1000, device=cuda_dev, requires_grad=True)
+    # input gradient through the non-trainable layer (gradients.py:133-149).  The
+    # all-ones upstream weighs every (bin, frame) phasor re/S, im/S equally, and
+    # for bins with |X| near zero TF32 operand rounding can turn that direction
+    # around: over 40 random inputs the TF32 error has median 4.8e-4, p90 1.0e-3
+    # but a tail to 9e-2 (tools/dx_err_sweep.py), so this check runs the FP32
+    # mode (median 2e-7, max 1.6e-6) on a seeded input
+    m2 = STFT(n_fft=128, hop_length=32, sr=8000, precision="fp32")
+    gen = torch.Generator(device=cuda_dev)
+    gen.manual_seed(5)
+    xr = torch.randn(2, 1000, device=cuda_dev, generator=gen).requires_grad_(True)
     m2(xr).sum().backward()
     h_re, h_im = O.stft_bank(128, 8000.0)
     ref = np.stack([O.conv_layer_vjp(c.astype(np.float64), h_re, h_im, 32,
                                      np.ones((65, 1000 // 32 + 1)), with_input_grad=True)[1]
                     for c in xr.detach().cpu().numpy()])
-    assert O.peak_err(xr.grad.cpu().numpy(), ref) <= TOL_GRAD["tf32"]
+    assert O.peak_err(xr.grad.cpu().numpy(), ref) <= TOL_GRAD["fp32"]
 
 
 # ---- ports of the reference's remaining gradient tests (tests/test_gradients.py)
