@@ -63,13 +63,18 @@ int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t ou
   return NNAB_OK;
 }
 
+// Per-device attribute caches: the current device is read on every call, so a
+// process driving several GPUs (one host thread each) gets each one's own values.
+constexpr int kMaxDevices = 64;
+
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static std::atomic<int> cache[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -79,16 +84,16 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 static size_t stage_bytes(const FrameGeom& g) { return align256((size_t)g.B * g.R * g.row_len * sizeof(float)); }
 
 static int check_device() {
-  static int ok = -1;
-  if (ok < 0) {
-    int dev = 0, major = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
-      ok = 0;
-    else
-      ok = major == 10;
+  static std::atomic<int> cache[kMaxDevices];  // 0 unknown, 1 sm_100, 2 other / error
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return NNAB_ENODEV;
+  int v = dev < kMaxDevices ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (v == 0) {
+    int major = 0;
+    v = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess && major == 10 ? 1 : 2;
+    if (dev < kMaxDevices) cache[dev].store(v, std::memory_order_relaxed);
   }
-  return ok ? NNAB_OK : NNAB_ENODEV;
+  return v == 1 ? NNAB_OK : NNAB_ENODEV;
 }
 
 }  // namespace nnab
@@ -232,6 +237,34 @@ extern "C" size_t nnab_stft_host_scratch_bytes(const nnab_frames* f, int32_t pre
 // Three-stage software pipeline over clip chunks shared by the host-buffer entry
 // points: copy-in on `cin`, compute(x_dev, n_clips, out_dev) on the caller's
 // stream, copy-out on `cout`; events order the hand-offs, two slots each.
+// Streams and events of one host_pipeline call, released on every return path.
+struct PipelineRes {
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t start = nullptr, in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
+  ~PipelineRes() {
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
+    cudaEvent_t* all[] = {&start, &in_done[0], &in_done[1], &comp_done[0], &comp_done[1], &out_done[0], &out_done[1]};
+    for (cudaEvent_t* e : all)
+      if (*e) cudaEventDestroy(*e);
+  }
+  int create() {
+    NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+    NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      NNAB_CUDA_TRY(cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming));
+      NNAB_CUDA_TRY(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming));
+      NNAB_CUDA_TRY(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
+    }
+    return NNAB_OK;
+  }
+};
+
+// Three-stage software pipeline over clip chunks shared by the host-buffer entry
+// points: copy-in on `cin`, compute(x_dev, n_clips, out_dev) on the caller's
+// stream, copy-out on `cout`; events order the hand-offs, two slots each.
+// (Stream destruction is deferred by the driver until queued work completes.)
 template <class Compute>
 static int host_pipeline(int64_t B, int64_t L, int64_t out_per_clip, int64_t chunk, const float* x_host,
                          float* out_host, char* base, cudaStream_t s, Compute compute) {
@@ -239,48 +272,33 @@ static int host_pipeline(int64_t B, int64_t L, int64_t out_per_clip, int64_t chu
   const size_t ob = align256((size_t)chunk * out_per_clip * 4);
   float* xd[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + xin)};
   float* od[2] = {reinterpret_cast<float*>(base + 2 * xin), reinterpret_cast<float*>(base + 2 * xin + ob)};
-  cudaStream_t cin = nullptr, cout = nullptr;
-  NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
-  NNAB_CUDA_TRY(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
-  cudaEvent_t start, in_done[2], comp_done[2], out_done[2];
-  NNAB_CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-  for (int i = 0; i < 2; ++i) {
-    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming));
-    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming));
-    NNAB_CUDA_TRY(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
-  }
-  NNAB_CUDA_TRY(cudaEventRecord(start, s));
-  NNAB_CUDA_TRY(cudaStreamWaitEvent(cin, start, 0));
-  NNAB_CUDA_TRY(cudaStreamWaitEvent(cout, start, 0));
-  int rc = NNAB_OK;
+  PipelineRes r;
+  int rc = r.create();
+  if (rc) return rc;
+  NNAB_CUDA_TRY(cudaEventRecord(r.start, s));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(r.cin, r.start, 0));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(r.cout, r.start, 0));
   const int64_t n_chunks = (B + chunk - 1) / chunk;
   for (int64_t i = 0; i < n_chunks && rc == NNAB_OK; ++i) {
     const int slot = (int)(i & 1);
     const int64_t c0 = i * chunk;
     const int64_t nb = std::min<int64_t>(chunk, B - c0);
-    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(cin, comp_done[slot], 0));  // x slot free
-    NNAB_CUDA_TRY(cudaMemcpyAsync(xd[slot], x_host + c0 * L, (size_t)nb * L * 4, cudaMemcpyHostToDevice, cin));
-    NNAB_CUDA_TRY(cudaEventRecord(in_done[slot], cin));
-    NNAB_CUDA_TRY(cudaStreamWaitEvent(s, in_done[slot], 0));
-    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(s, out_done[slot], 0));  // out slot drained
+    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(r.cin, r.comp_done[slot], 0));  // x slot free
+    NNAB_CUDA_TRY(cudaMemcpyAsync(xd[slot], x_host + c0 * L, (size_t)nb * L * 4, cudaMemcpyHostToDevice, r.cin));
+    NNAB_CUDA_TRY(cudaEventRecord(r.in_done[slot], r.cin));
+    NNAB_CUDA_TRY(cudaStreamWaitEvent(s, r.in_done[slot], 0));
+    if (i >= 2) NNAB_CUDA_TRY(cudaStreamWaitEvent(s, r.out_done[slot], 0));  // out slot drained
     rc = compute(xd[slot], nb, od[slot]);
-    NNAB_CUDA_TRY(cudaEventRecord(comp_done[slot], s));
-    NNAB_CUDA_TRY(cudaStreamWaitEvent(cout, comp_done[slot], 0));
+    NNAB_CUDA_TRY(cudaEventRecord(r.comp_done[slot], s));
+    NNAB_CUDA_TRY(cudaStreamWaitEvent(r.cout, r.comp_done[slot], 0));
     NNAB_CUDA_TRY(cudaMemcpyAsync(out_host + c0 * out_per_clip, od[slot], (size_t)nb * out_per_clip * 4,
-                                  cudaMemcpyDeviceToHost, cout));
-    NNAB_CUDA_TRY(cudaEventRecord(out_done[slot], cout));
+                                  cudaMemcpyDeviceToHost, r.cout));
+    NNAB_CUDA_TRY(cudaEventRecord(r.out_done[slot], r.cout));
   }
-  // join: the caller's stream waits for the last copy-out
-  NNAB_CUDA_TRY(cudaEventRecord(out_done[0], cout));
-  NNAB_CUDA_TRY(cudaStreamWaitEvent(s, out_done[0], 0));
-  cudaStreamDestroy(cin);
-  cudaStreamDestroy(cout);
-  cudaEventDestroy(start);
-  for (int i = 0; i < 2; ++i) {
-    cudaEventDestroy(in_done[i]);
-    cudaEventDestroy(comp_done[i]);
-    cudaEventDestroy(out_done[i]);
-  }
+  // join: the caller's stream waits for the last copy-out (also after a failed compute,
+  // so no copy still reads the caller's buffers when this returns)
+  NNAB_CUDA_TRY(cudaEventRecord(r.out_done[0], r.cout));
+  NNAB_CUDA_TRY(cudaStreamWaitEvent(s, r.out_done[0], 0));
   return rc;
 }
 

@@ -91,6 +91,7 @@ class DftEngine:
             self.fold = int(z0 and zn and (self.n_bins - 1) % 128 == 0)
         self._ws = _Workspace()
         self.mel_w = None
+        self.mel_wide = False
         self.set_bank(h_re, h_im)
 
     # ------------------------------------------------------------ banks
@@ -112,13 +113,23 @@ class DftEngine:
 
     def set_mel(self, weights, power: float = 1.0, banded: bool = True) -> None:
         """Mel weights (n_mels, n_bins) for the fused epilogue; rows padded to
-        a multiple of 4 floats so the epilogue reads them with 16-byte loads."""
+        a multiple of 4 floats so the epilogue reads them with 16-byte loads.
+        More than 128 mel rows (the epilogue's shared-memory accumulator) run
+        as the STFT GEMM saving |X| per frame slot, then a tcgen05 W @ |X| GEMM
+        (power 1, no fused log)."""
         w = torch.as_tensor(weights)
         if w.dim() != 2 or w.shape[1] != self.n_bins:
             raise ValueError(f"mel weights must be (n_mels, {self.n_bins})")
         self.n_mels = int(w.shape[0])
-        if self.n_mels > 128:
-            raise L.NnabError("fused Mel epilogue supports n_mels <= 128")
+        self.power = float(power)
+        self.mel_wide = self.n_mels > 128
+        if self.mel_wide:
+            kp = (self.n_bins + 31) // 32 * 32
+            wp = torch.zeros(self.n_mels, kp, dtype=torch.float32, device=self.device)
+            wp[:, : self.n_bins] = w.to(self.device, torch.float32)
+            self.mel_w = wp
+            self.mel_ld, self.mel_band = kp, None
+            return
         self.mel_ld = ((max(self.n_tiles * 128, self.n_bins) + 3) // 4) * 4 + 32
         wp = torch.zeros(self.n_mels, self.mel_ld, dtype=torch.float32, device=w.device)
         wp[:, : self.n_bins] = w.to(torch.float32)
@@ -130,7 +141,52 @@ class DftEngine:
             self.mel_band = torch.from_numpy(band.reshape(-1)).to(self.device)
         else:
             self.mel_band = None
-        self.power = float(power)
+
+    def _split(self, t: torch.Tensor):
+        """TF32-round t (hi), plus the residual (lo) in 3xTF32 mode."""
+        lib = L.load()
+        hi = torch.empty_like(t)
+        lo = torch.empty_like(t) if self.precision == L.PREC_3XTF32 else None
+        L.check(lib.nnab_tf32_split(t.data_ptr(), t.numel(), self.precision, hi.data_ptr(), L.ptr(lo),
+                                    L.stream_handle(self.device)), "tf32_split")
+        return hi, lo
+
+    def _mel_wide(self, B: int, length: int, out: torch.Tensor, log_flag: int) -> torch.Tensor:
+        """n_mels > 128: |X| per (bin, frame slot) from the STFT GEMM, then W @ |X|."""
+        if self.power != 1.0 or log_flag:
+            raise NotImplementedError("more than 128 mel rows support power=1 without fused log compression")
+        lib = L.load()
+        f = self.frames(B, length)
+        ws, stream, dev = self._ws.buf, L.stream_handle(self.device), self.device
+        split = self.precision == L.PREC_3XTF32
+        ld = lib.nnab_slots_ld(C.byref(f))
+        F = self.n_bins
+        pad = self.n_fft // 2 if self.center else 0
+        T, _, R = geometry(length, self.n_fft, self.hop, pad, self.pad_mode)
+        re = torch.empty(F, ld, device=dev)
+        im = torch.empty(F, ld, device=dev) if split else None
+        mag = torch.empty(F, ld, device=dev)
+        L.check(lib.nnab_stft_forward_train_staged(
+            C.byref(f), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), F, self.fold, self.precision,
+            L.OUT_SMOOTH_MAG, 1.0, 0.0, None, 0, 0, None, None, re.data_ptr(), L.ptr(im), mag.data_ptr(), ld,
+            ws.data_ptr(), ws.numel(), stream), "stft_forward_train_staged")
+        del re, im
+        kp = self.mel_ld
+        w_hi, w_lo = self._split(self.mel_w)
+        m_hi, m_lo = self._split(mag) if split else (mag, None)
+        rc = lib.nnab_mel_forward_slots(self.n_mels, ld, kp, w_hi.data_ptr(), L.ptr(w_lo), m_hi.data_ptr(),
+                                        L.ptr(m_lo), F, B, R, T, self.precision, out.data_ptr(), stream)
+        if rc == L.ENOTSUP or (rc == L.EINVAL and R % 4):  # slot-major W @ |X|, then the (B, n_mels, T) layout
+            mel_s = torch.empty(self.n_mels, ld, device=dev)
+            part = torch.empty(max(lib.nnab_rgemm_partial_bytes(self.n_mels, ld, kp, 1) // 4, 1), device=dev)
+            L.check(lib.nnab_rgemm(self.n_mels, ld, kp, w_hi.data_ptr(), L.ptr(w_lo), kp, m_hi.data_ptr(),
+                                   L.ptr(m_lo), ld, 1, ld, F, mel_s.data_ptr(), ld, 1, part.data_ptr(),
+                                   self.precision, stream), "rgemm")
+            L.check(lib.nnab_from_slots(mel_s.data_ptr(), B, self.n_mels, T, R, ld, out.data_ptr(), stream),
+                    "from_slots")
+        else:
+            L.check(rc, "mel_forward_slots")
+        return out
 
     # ------------------------------------------------------------ forward
     def frames(self, B: int, length: int) -> L.nnab_frames:
@@ -200,9 +256,11 @@ class DftEngine:
             out = torch.empty(B, rows, T, dtype=dt, device=self.device)
         if B == 0:
             return out
+        mel = k == L.OUT_MEL
+        if mel and self.mel_wide:
+            return self._mel_wide(B, length, out, log_flag)
         f = self.frames(B, length)
         ws = self._ws.buf
-        mel = k == L.OUT_MEL
         L.check(lib.nnab_stft_forward_staged(
             C.byref(f), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins, self.fold,
             self.precision, k | log_flag, float(getattr(self, "power", 1.0)), float(eps),
@@ -219,6 +277,8 @@ class DftEngine:
         B, length = int(x_host.shape[0]), int(x_host.shape[1])
         T = self.n_frames(length)
         k = {"magnitude": L.OUT_MAGNITUDE, "power": L.OUT_POWER, "mel": L.OUT_MEL}[kind]
+        if k == L.OUT_MEL and self.mel_wide:
+            raise NotImplementedError("the host-buffer entry point fuses at most 128 mel rows")
         rows = self.n_mels if k == L.OUT_MEL else self.n_bins
         if out_host is None:
             out_host = torch.empty(B, rows, T, dtype=torch.float32, pin_memory=True)
@@ -387,13 +447,14 @@ class CqtLongEngine:
         ws = self._ws.buf
         if self.hybrid is not None:
             (bank, col_t, rows_t, _, n, rmax, bank_lo), sch, n_ent, s_hi, s_lo, n_long = self.hybrid
-            L.check(lib.nnab_cqt1992v2_hybrid_staged(C.byref(f), bank.data_ptr(), L.ptr(bank_lo), col_t.data_ptr(),
-                                                     rows_t.data_ptr(), n, rmax, L.ptr(s_hi), L.ptr(s_lo),
-                                                     L.ptr(sch), n_ent, n_long, self.n_bins, self.precision,
-                                                     kinds[kind], float(eps), out.data_ptr(), ws.data_ptr(),
-                                                     ws.numel(), L.stream_handle(self.device)),
-                    "cqt1992v2_hybrid_staged")
-            return out
+            rc = lib.nnab_cqt1992v2_hybrid_staged(C.byref(f), bank.data_ptr(), L.ptr(bank_lo), col_t.data_ptr(),
+                                                  rows_t.data_ptr(), n, rmax, L.ptr(s_hi), L.ptr(s_lo),
+                                                  L.ptr(sch), n_ent, n_long, self.n_bins, self.precision,
+                                                  kinds[kind], float(eps), out.data_ptr(), ws.data_ptr(),
+                                                  ws.numel(), L.stream_handle(self.device))
+            if rc != L.ENOTSUP:  # ENOTSUP (too few SMs for the E-GEMM pairs): the all-bins schedule below
+                L.check(rc, "cqt1992v2_hybrid_staged")
+                return out
         if self.egemm is not None:
             bank, col_t, rows_t, runs_t, n, rmax, _ = self.egemm
             rc = lib.nnab_cqt1992v2_egemm_staged(C.byref(f), bank.data_ptr(), col_t.data_ptr(), rows_t.data_ptr(),
@@ -426,12 +487,14 @@ class CqtLongEngine:
                                                                  chunk_clips), self.device)
         if self.hybrid is not None:
             (bank, col_t, rows_t, _, n, rmax, bank_lo), sch, n_ent, s_hi, s_lo, n_long = self.hybrid
-            L.check(lib.nnab_cqt1992v2_hybrid_forward_host(
+            rc = lib.nnab_cqt1992v2_hybrid_forward_host(
                 C.byref(f), x_host.data_ptr(), bank.data_ptr(), L.ptr(bank_lo), col_t.data_ptr(), rows_t.data_ptr(),
                 n, rmax, L.ptr(s_hi), L.ptr(s_lo), L.ptr(sch), n_ent, n_long, self.n_bins, self.precision, k,
                 float(eps), out_host.data_ptr(), int(chunk_clips), ws.data_ptr(), ws.numel(),
-                L.stream_handle(self.device)), "cqt1992v2_hybrid_forward_host")
-            return out_host
+                L.stream_handle(self.device))
+            if rc != L.ENOTSUP:
+                L.check(rc, "cqt1992v2_hybrid_forward_host")
+                return out_host
         L.check(lib.nnab_cqt1992v2_forward_host(
             C.byref(f), x_host.data_ptr(), self.packed_hi.data_ptr(), L.ptr(self.packed_lo), self.n_bins,
             self.schedule.data_ptr(), self.n_entries, self.precision, k, float(eps), out_host.data_ptr(),

@@ -72,13 +72,25 @@ class STFT(nn.Module):
         self._infer = DftEngine(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
         self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
         self._op._bank_version = None
+        self._infer_key = _bank_key(self.h_re, self.h_im)
 
     def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
         x = _as_batch(x)
-        if self.trainable or x.requires_grad:
-            y = DftLayerFunction.apply(x, self.h_re, self.h_im, None, self._op, _bank_key(self.h_re, self.h_im))
-            return y if self.log_eps is None else torch.log(y + self.log_eps)
         fmt = _fmt(output_format or self.output_format)
+        if self.trainable or x.requires_grad:
+            # autograd path: the smoothed magnitude S = sqrt(|X|^2 + 1e-12) of gradients.py:61-67;
+            # power is S^2 through autograd, complex output has no reference VJP
+            if fmt == "complex":
+                raise NotImplementedError("trainable / input-gradient STFT supports Magnitude and Power outputs "
+                                          "(the reference VJP is for the smoothed magnitude, gradients.py:103-149)")
+            y = DftLayerFunction.apply(x, self.h_re, self.h_im, None, self._op, _bank_key(self.h_re, self.h_im))
+            if fmt == "power":
+                y = y * y
+            return y if self.log_eps is None else torch.log(y + self.log_eps)
+        key = _bank_key(self.h_re, self.h_im)
+        if key != self._infer_key:  # parameters replaced / edited in place (load_state_dict, optimiser step)
+            self._infer.set_bank(self.h_re.detach(), self.h_im.detach())
+            self._infer_key = key
         if self.log_eps is not None and fmt != "complex":
             return self._infer.forward(x, fmt, log_eps=self.log_eps)
         return self._infer.forward(x, fmt)
@@ -146,6 +158,7 @@ class CQT1992v2(nn.Module):
         self._infer = CqtLongEngine(k, hop_length, pad_mode, precision=precision, device=self.device)
         self._op = None
         self._precision = precision
+        self._infer_key = _bank_key(self.k_re, self.k_im)
 
     def forward(self, x: torch.Tensor, output_format: str | None = None) -> torch.Tensor:
         x = _as_batch(x)
@@ -154,7 +167,13 @@ class CQT1992v2(nn.Module):
                 self._op = DftLayerOp(self.k_re.detach(), self.k_im.detach(), self.cfg.hop_length, True,
                                       self.cfg.pad_mode, precision=self._precision, device=self.device)
                 self._op._bank_version = None
+            if _fmt(output_format or self.output_format) != "magnitude":
+                raise NotImplementedError("trainable CQT1992v2 returns the smoothed magnitude (gradients.py:61-67)")
             return DftLayerFunction.apply(x, self.k_re, self.k_im, None, self._op, _bank_key(self.k_re, self.k_im))
+        key = _bank_key(self.k_re, self.k_im)
+        if key != self._infer_key:  # parameters replaced / edited in place: repack bank + schedule
+            self._infer.set_bank(self.k_re.detach().cpu().numpy(), self.k_im.detach().cpu().numpy())
+            self._infer_key = key
         return self._infer.forward(x, _fmt(output_format or self.output_format))
 
 
@@ -163,6 +182,10 @@ class CQT2010v2(nn.Module):
                  basis_norm=1, window="hann", pad_mode="reflect", earlydownsample=True, output_format="Magnitude",
                  device="cuda"):
         super().__init__()
+        if norm is not True and norm != 1:
+            # the reference's Cqt2010v2 output has one scaling (transforms.py:290-313): L1-normalised
+            # kernels via basis_norm, no further output normalisation to switch off
+            raise NotImplementedError("CQT2010v2 supports norm=True only (the reference's output scaling)")
         self.device = _require_cuda(device)
         self.cfg = CqtConfig(sr=sr, fmin=fmin, n_bins=n_bins, bins_per_octave=bins_per_octave,
                              hop_length=hop_length, window_kind=window, norm=basis_norm, fmax=fmax,

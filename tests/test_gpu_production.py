@@ -1,0 +1,136 @@
+"""GPU parity at the benchmark's production batch: 1,770 clips x 80,000 samples
+(BASELINE config 1-4), the batch `bench.py` times.
+
+At this size the persistent kernels walk many tiles per CTA (STFT/Mel: 1,107
+CTA-pair M tiles over 74 pairs; CQT2010v2: 12 clips per CTA; E-GEMM long
+runs), which no small-batch test reaches.  Three checks per transform:
+
+* the reference's own golden outputs (tests/golden, made by the real
+  `spectro`) for the two golden clips planted at positions 0, 884 and 1769
+  among random clips, through the device and the C-ABI host entry points;
+* a sample of the random clips (first / last of several M tiles) against the
+  float64 oracle;
+* every clip of the full batch against the same engine run on 32-clip chunks
+  (whose launches never reach a second tile per CTA): bit-exact where the
+  kernel's reduction order does not depend on the clip's batch position, and
+  within 1e-6 peak-normalised for the CQT1992v2 E-GEMM, whose hop-offset sums
+  are ordered by the slot's position in its 128-slot tile
+  (transforms.py:370-388: batch == sequential)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import spectro_oracle as O
+
+pytestmark = pytest.mark.gpu
+SR = 44100.0
+B_FULL = 1770
+PLANT = (0, 884, 1769)  # golden clip 0, 1, 0
+SAMPLE = (1, 300, 883, 885, 1500, 1768)  # random clips checked against the oracle
+TOL = {"tf32": 1e-3, "fp32": 1e-5}
+TOL_POWER = {"tf32": 2e-3, "fp32": 2e-5}
+
+
+@pytest.fixture(scope="module")
+def batch(golden):
+    rng = np.random.default_rng(2024)
+    x = (rng.standard_normal((B_FULL, 80000), dtype=np.float32) * np.float32(0.5))
+    for i, p in enumerate(PLANT):
+        x[p] = golden["clips"][i % 2]
+    return x
+
+
+@pytest.fixture(scope="module")
+def xdev(batch):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.from_numpy(batch).to("cuda:0")
+
+
+def _chunked(fn, x, n=32):
+    return torch.cat([fn(x[i:i + n]) for i in range(0, x.shape[0], n)])
+
+
+def _check(got, ref_golden_key, golden, batch, oracle_fn, tol, chunk_got=None, chunk_tol=0.0):
+    for i, p in enumerate(PLANT):
+        err = O.peak_err(got[p], golden[ref_golden_key][i % 2])
+        assert err <= tol, ("golden", p, err)
+    for p in SAMPLE:
+        err = O.peak_err(got[p], oracle_fn(batch[p].astype(np.float64)))
+        assert err <= tol, ("oracle", p, err)
+    if chunk_got is not None:
+        if chunk_tol == 0.0:
+            bad = np.flatnonzero([not np.array_equal(a, b) for a, b in zip(got, chunk_got)])
+            assert bad.size == 0, ("batch != chunked", bad[:10])
+        else:
+            worst = max(O.peak_err(a, b) for a, b in zip(got, chunk_got))
+            assert worst <= chunk_tol, worst
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("kind,power", [("magnitude", 1.0), ("mel", 1.0), ("mel", 2.0)])
+def test_stft_mel_full_batch(golden, batch, xdev, precision, kind, power):
+    from paper_1912_12055_b200.engine import DftEngine
+    h_re, h_im = O.stft_bank()
+    eng = DftEngine(h_re, h_im, 512, precision=precision, device="cuda")
+    W = O.mel_bank(SR, 2048, 128, formula="slaney")
+    if kind == "mel":
+        eng.set_mel(W, power=power)
+    got_d = eng.forward(xdev, kind)
+    chunks = _chunked(lambda c: eng.forward(c, kind), xdev).cpu().numpy()
+    got = got_d.cpu().numpy()
+    del got_d
+    key = "stft_mag_full" if kind == "magnitude" else ("mel_full" if power == 1.0 else "mel_full_p2")
+    tol = (TOL_POWER if power == 2.0 else TOL)[precision]
+    fn = (lambda c: O.stft_clip(c, h_re, h_im, 512)) if kind == "magnitude" else (
+        lambda c: O.mel_clip(c, h_re, h_im, W, 512, power=power))
+    _check(got, key, golden, batch, fn, tol, chunks)
+    if power == 1.0:  # the C-ABI host entry (pinned buffers, 15 chunks, 3 streams): same values
+        host = eng.forward_host(torch.from_numpy(batch).pin_memory(), kind, chunk_clips=118)
+        torch.cuda.synchronize()
+        assert np.array_equal(host.numpy(), got)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_cqt1992v2_full_batch(golden, batch, xdev, precision):
+    from paper_1912_12055_b200.engine import CqtLongEngine
+    cfg = O.CqtCfg(sr=SR)
+    kern, _ = O.cqt_time_bank(cfg)
+    eng = CqtLongEngine(kern, 512, "reflect", precision=precision, device="cuda")
+    assert eng.hybrid is not None
+    got = eng.forward(xdev).cpu().numpy()
+    chunks = _chunked(eng.forward, xdev).cpu().numpy()
+    _check(got, "cqt1992v2_full", golden, batch, lambda c: O.cqt1992v2_clip(c, kern, 512), TOL[precision],
+           chunks, chunk_tol=1e-6)
+    host = eng.forward_host(torch.from_numpy(batch).pin_memory(), chunk_clips=148)
+    torch.cuda.synchronize()
+    assert max(O.peak_err(a, b) for a, b in zip(host.numpy(), got)) <= 1e-6
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_cqt2010v2_full_batch(golden, batch, xdev, precision):
+    from paper_1912_12055_b200.engine import Cqt2010Engine
+    cfg = O.CqtCfg(sr=SR)
+    p = O.cqt2010_plan(cfg)
+    eng = Cqt2010Engine(p.taps, p.top_kernels, p.early_stages, p.n_octaves, p.kernel_hop, p.first_bin, 12, 84,
+                        "reflect", precision=precision)
+    got = eng.forward(xdev).cpu().numpy()
+    chunks = _chunked(eng.forward, xdev).cpu().numpy()
+    _check(got, "cqt2010v2_full", golden, batch, lambda c: O.cqt2010v2_clip(c, cfg, p), TOL[precision], chunks)
+    host = eng.forward_host(torch.from_numpy(batch).pin_memory(), chunk_clips=148)
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), got)
+
+
+def test_spectro_batch_transform_full_batch(golden, batch, xdev):
+    """The reference-named entry point (spectro.batch_transform over Signals,
+    transforms.py:370-388) at the production batch: one launch per group,
+    results in order, golden clips where they were planted."""
+    from paper_1912_12055_b200 import spectro as S
+    mel = S.MelSpec(S.MelParams(n_fft=2048, n_mels=128, hop_length=512), SR)
+    sigs = [S.Signal(xdev[i], SR) for i in range(B_FULL)]
+    res = S.batch_transform(sigs, mel)
+    assert len(res) == B_FULL
+    for i, p in enumerate(PLANT):
+        assert O.peak_err(res[p].data.cpu().numpy(), golden["mel_full"][i % 2]) <= TOL["tf32"]
