@@ -42,6 +42,7 @@ class DftLayerOp:
         self.device = self.engine.device
         self.prec = self.engine.precision
         self.split = self.prec == L.PREC_3XTF32
+        self.reducer = None  # dist.GradReducer while armed: gradient blocks are all-reduced as they finish
 
     @property
     def n_bins(self):
@@ -145,6 +146,8 @@ class DftLayerOp:
                 dW = torch.empty(nm, F, device=self.device)
                 self._rgemm(nm, F, ld, gsp, ld, magp, ld, 0, 0, 0, dW, F)
                 grads["weights"] = dW
+                if self.reducer is not None:  # overlaps the coef and dK GEMMs below
+                    self.reducer.launch(dW)
             if need_bank or need_x:  # dS[f][slot] = sum_m W[m][f] g[m][slot]
                 kp = (nm + 31) // 32 * 32
                 wt_hi = _f32(F, kp, self.device)
@@ -160,6 +163,8 @@ class DftLayerOp:
                         "mel_dft_coef")
                 ds = True
         if not (need_bank or need_x):
+            if self.reducer is not None:
+                self.reducer.wait()
             return grads
         if ds is None:
             coef_hi = _f32(2 * F, ld, self.device)
@@ -170,10 +175,18 @@ class DftLayerOp:
         ws = saved["ws"]
         if need_bank:
             dk = _f32(2 * F, n_fft, self.device)
-            part = torch.empty(max(lib.nnab_rgemm_partial_bytes(2 * F, n_fft, ld, 0) // 4, 1), device=self.device)
-            L.check(lib.nnab_kernel_grad(C.byref(f), coef_hi.data_ptr(), L.ptr(coef_lo), 2 * F, ld, self.prec,
-                                         dk.data_ptr(), n_fft, ws.data_ptr(), ws.numel(), part.data_ptr(), 0, stream),
-                    "kernel_grad")
+            # with a reducer: rows [0, 1024) first (whole 256-row tiles), all-reduced while
+            # the remaining rows' GEMM runs; without: one launch over all 2F rows
+            blocks = [(0, 2 * F)] if self.reducer is None or 2 * F <= 1280 else [(0, 1024), (1024, 2 * F)]
+            for r0, r1 in blocks:
+                part = torch.empty(max(lib.nnab_rgemm_partial_bytes(r1 - r0, n_fft, ld, 0) // 4, 1),
+                                   device=self.device)
+                L.check(lib.nnab_kernel_grad(C.byref(f), coef_hi.data_ptr() + 4 * r0 * ld,
+                                             None if coef_lo is None else coef_lo.data_ptr() + 4 * r0 * ld,
+                                             r1 - r0, ld, self.prec, dk.data_ptr() + 4 * r0 * n_fft, n_fft,
+                                             ws.data_ptr(), ws.numel(), part.data_ptr(), 0, stream), "kernel_grad")
+                if self.reducer is not None:
+                    self.reducer.launch(dk[r0:r1])
             grads["h_re"], grads["h_im"] = dk[:F], dk[F:]
         if need_x:  # frame grads^T [tap][slot] = h^T @ coef, then overlap-add + pad fold
             h = torch.cat([torch.as_tensor(h_re), torch.as_tensor(h_im)]).to(self.device, torch.float32).contiguous()
@@ -187,6 +200,8 @@ class DftLayerOp:
             gx = torch.empty(B, length, device=self.device)
             L.check(lib.nnab_input_grad(C.byref(f), fgt.data_ptr(), ld, gx.data_ptr(), stream), "input_grad")
             grads["x"] = gx
+        if self.reducer is not None:  # order the compute stream after every reduction
+            self.reducer.wait()
         return grads
 
 

@@ -3,9 +3,12 @@
 The forward path shards clips across ranks with no collective (outputs stay
 sharded).  Trainable layers need exactly one exchange per step: the sum of
 the kernel / mel-weight gradients over ranks (NCCL all-reduce over NVLink on
-B200; gloo in the CPU tests).  Gradients are flattened into one bucket so the
-step issues a single collective, and the summation order is fixed by NCCL's
-ring/tree for a given world size, so runs are reproducible.
+B200; gloo in the CPU tests).  `GradReducer` buckets it by readiness inside
+the backward pass -- the mel-weight gradient as soon as its GEMM finishes
+(overlapping the coef and dK GEMMs), the first 1,024 DFT-bank rows while the
+rest of dK runs, the remainder last -- and `allreduce_grads` is the one-bucket
+form.  The summation order is fixed by NCCL's ring/tree for a given world
+size, so runs are reproducible.
 """
 
 from __future__ import annotations
@@ -69,3 +72,47 @@ def gather_shards(y: torch.Tensor, n_items: int, group=None) -> torch.Tensor:
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
     return torch.cat([p[: hi - lo] for p, (lo, hi) in zip(parts, sizes)])
+
+
+class GradReducer:
+    """Bucketed all-reduce (sum) of the gradients a trainable layer's backward
+    produces, each bucket launched asynchronously the moment its GEMM has been
+    issued (NCCL's stream waits for the compute stream at launch, so the
+    reduction of bucket i overlaps the GEMMs that produce bucket i+1).
+
+    Protocol with `autograd.DftLayerOp.backward`: while armed, the op calls
+    `launch(t)` for every finished gradient block and `wait()` before it
+    returns, so the compute stream is ordered after every reduction before
+    autograd accumulates the gradients (no stream race on .grad)."""
+
+    def __init__(self, module_or_ops, group=None):
+        from .autograd import DftLayerOp
+        if isinstance(module_or_ops, torch.nn.Module):
+            ops = []
+            for m in module_or_ops.modules():
+                op = getattr(m, "_op", None)
+                if isinstance(op, DftLayerOp) and op not in ops:
+                    ops.append(op)
+        else:
+            ops = list(module_or_ops)
+        self.ops, self.group, self.works, self.buckets = ops, group, [], 0
+
+    def arm(self):
+        for op in self.ops:
+            op.reducer = self
+        self.works, self.buckets = [], 0
+
+    def launch(self, t: torch.Tensor):
+        if dist.is_available() and dist.is_initialized():
+            self.works.append(dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+        self.buckets += 1
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        self.works = []
+
+    def finish(self):
+        self.wait()
+        for op in self.ops:
+            op.reducer = None
