@@ -110,7 +110,7 @@ class Clocks:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", "25"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -162,8 +162,36 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ workloads
-def build_workload(name: str, device, precision: str, nb: int = B_CLIPS):
-    """Returns (step_fn, gemm_fn or None, launches_per_step, roofline dict builder, e2e fn)."""
+# Operand modes per workload: the engine precision a bench mode maps to, the dtype
+# label, and the tensor peak it is measured against ("f16": dense FP16 = measured bf16;
+# "tf32": half of it).  "f16" is each transform's fastest <= 1e-3 mode (FP16 operands
+# under exact power-of-two scales where the transform has it, else TF32); "fp32" its
+# <= 1e-5 mode.
+MODES = {
+    ("stft", "f16"): ("f16", "f16 operands (exact per-clip / per-bank power-of-two scales), f32 accumulate", "f16"),
+    ("stft", "tf32"): ("tf32", "tf32", "tf32"),
+    ("stft", "fp32"): ("fp32", "3xf16 (FP16 hi/lo split, exact power-of-two scales, f32 accumulate)", "f16"),
+    ("stft", "3xtf32"): ("3xtf32", "3xtf32", "tf32"),
+    ("cqt1992v2", "f16"): ("tf32", "tf32", "tf32"),
+    ("cqt1992v2", "tf32"): ("tf32", "tf32", "tf32"),
+    ("cqt1992v2", "fp32"): ("fp32", "3xtf32", "tf32"),
+    ("cqt2010v2", "f16"): ("f16", "f16 operands (exact per-clip power-of-two scale), f32 accumulate", None),
+    ("cqt2010v2", "tf32"): ("f16", "f16 operands (exact per-clip power-of-two scale), f32 accumulate", None),
+    ("cqt2010v2", "fp32"): ("fp32", "f32 (CUDA cores)", None),
+    ("train", "f16"): ("tf32", "tf32", "tf32"),
+    ("train", "tf32"): ("tf32", "tf32", "tf32"),
+    ("train", "fp32"): ("fp32", "3xtf32", "tf32"),
+}
+for _m in ("f16", "tf32", "fp32", "3xtf32"):
+    if ("stft", _m) in MODES:
+        MODES[("mel", _m)] = MODES[("melpow2", _m)] = MODES[("stft", _m)]
+BREAKDOWN_MODES = {"stft": ["f16", "tf32", "fp32"], "mel": ["f16", "tf32", "fp32"], "melpow2": ["f16", "tf32", "fp32"],
+                   "cqt1992v2": ["tf32", "fp32"], "cqt2010v2": ["f16", "fp32"], "train": ["tf32", "fp32"]}
+
+
+def build_workload(name: str, device, mode: str, nb: int = B_CLIPS):
+    """Returns (engine, output kind, roofline work dict, launches per step)."""
+    precision = MODES[(name, mode)][0]
     from paper_1912_12055_b200 import banks
     from paper_1912_12055_b200.engine import CqtLongEngine, Cqt2010Engine, DftEngine
     from paper_1912_12055_b200.spectro import CqtConfig, cqt2010_plan
@@ -385,7 +413,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="mel", choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--precision", default="f16", choices=["f16", "tf32", "fp32", "3xtf32"],
+                    help="operand mode (bench.MODES): f16 = the fastest <= 1e-3 mode, fp32 = the <= 1e-5 mode")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=150.0,
@@ -432,17 +461,18 @@ def main():
     x = x_full[lo:hi].contiguous()
     del x_full
 
-    def roofline(work, kernel_ms, clips=B_CLIPS):
+    def roofline(work, kernel_ms, clips=B_CLIPS, mma="tf32"):
         t = kernel_ms / 1e3
         per = work["per_batch"] * clips / B_CLIPS
         if work["bound"] == "tensor":
-            ach, peak = per / t / 1e12, tf32_peak
+            ach, peak = per / t / 1e12, (bf16_peak if mma == "f16" else tf32_peak)
         else:
             ach, peak = per / t / 1e9, hbm_peak
         return {"bound": work["bound"], "achieved": ach, "peak": peak, "unit": work["unit"], "frac": ach / peak,
                 "traffic": traffic.get(work["kernel"] + ":" + args.workload) if work["kernel"] else None,
                 "kernel": work["kernel"], "kernel_ms": kernel_ms,
-                "peak_source": (f"TF32 = measured dense bf16 {bf16_peak:.1f} TF/s / 2 ({peak_src}, burst)"
+                "peak_source": ((f"FP16 dense = measured bf16 {bf16_peak:.1f} TF/s ({peak_src}, burst)" if mma == "f16"
+                                 else f"TF32 = measured dense bf16 {bf16_peak:.1f} TF/s / 2 ({peak_src}, burst)")
                                 if work["bound"] == "tensor" else f"HBM copy {hbm_peak:.1f} GB/s ({peak_src})"),
                 "work_per_step": per}
 
@@ -468,7 +498,10 @@ def main():
         ms = float(t.item())
         dist.barrier()
     value = B_CLIPS / (ms / 1e3)  # whole-job clips / max-over-ranks step time
-    rf = roofline(work, gemm_ms if staged else ms, nb)
+    mode = MODES[(args.workload, args.precision)] if (args.workload, args.precision) in MODES else None
+    if mode is None:
+        raise SystemExit(f"workload {args.workload} has no {args.precision} mode")
+    rf = roofline(work, gemm_ms if staged else ms, nb, mode[2])
 
     # end to end through the C ABI host path: pinned input -> pinned output,
     # H2D + compute + D2H inside the timed region, chunked with copy/compute overlap
@@ -564,16 +597,17 @@ def main():
     breakdown = {}
     if rank == 0 and world == 1 and not args.no_breakdown:
         for name in ["stft", "mel", "melpow2", "cqt1992v2", "cqt2010v2", "train"]:
-            for prec in ["tf32", "fp32"]:
+            for prec in BREAKDOWN_MODES[name]:
                 if name == args.workload and prec == args.precision:
                     continue
                 e, k, w, _ = build_workload(name, device, prec, nb)
                 st = name not in ("cqt2010v2", "train")
                 m, gm = run_timed(e, k, x, 20 if name != "train" else 5, 3, torch, stream, time_gemm=st)
-                r = roofline(w, gm if st else m, nb)
+                r = roofline(w, gm if st else m, nb, MODES[(name, prec)][2])
                 breakdown[f"{name}_{prec}"] = {"ms_per_step": m, "value": nb / (m / 1e3),
                                                "roofline_frac": r["frac"], "achieved": r["achieved"],
-                                               "unit": r["unit"], "kernel_ms": r["kernel_ms"]}
+                                               "unit": r["unit"], "kernel_ms": r["kernel_ms"],
+                                               "dtype": MODES[(name, prec)][1]}
                 del e
         breakdown[f"{args.workload}_{args.precision}"] = {"ms_per_step": ms, "value": value,
                                                           "roofline_frac": rf["frac"], "achieved": rf["achieved"],
@@ -592,9 +626,7 @@ def main():
             "metric": metric,
             "value": value, "unit": "spectrograms/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": (("f16 operands (exact per-clip power-of-two scale), f32 accumulate" if args.precision == "tf32"
-                       else "f32 (CUDA cores)") if args.workload == "cqt2010v2"
-                      else "tf32" if args.precision == "tf32" else "3xtf32"),
+            "dtype": mode[1],
             "data": "synthetic: N(0, 0.5^2) float32 clips generated on device (cli.py:98-99 distribution)",
             "config": {"workload": WORKLOADS[args.workload], "global_clips": B_CLIPS, "clips_per_rank": nb,
                        "samples": L_SAMPLES, "sr": SR, "precision": args.precision,

@@ -57,6 +57,12 @@ extern "C" {
 
 #define NNAB_PREC_TF32 0  /* one TF32 tcgen05 pass (peak-normalised error <= 1e-3) */
 #define NNAB_PREC_3XTF32 1 /* hi/lo split, 3 passes (<= 1e-5, FP32-equivalent) */
+/* FP16 operands under exact power-of-two scales (per clip for the signal, per
+ * bank for the kernels) so every operand sits in FP16's normal range: the same
+ * 11-bit significand as TF32 at twice the tcgen05 rate (kind::f16, FP32
+ * accumulate); the scales are undone exactly in the epilogue.  STFT / Mel only. */
+#define NNAB_PREC_F16 2   /* one FP16 pass (<= 1e-3) */
+#define NNAB_PREC_3XF16 3 /* FP16 hi/lo split, 3 passes (<= 1e-5) */
 
 /* A strided-correlation ("conv1d with a kernel bank") problem:
  * out[r, t] = sum_m padded[t*hop + m] * bank[r, m]   (signal.py:159-183)  */
@@ -90,6 +96,10 @@ int nnab_frames_geometry(const nnab_frames* f, int32_t* n_frames, int32_t* row_l
  * and the bank tiles exactly (1025 bins -> 8 tiles).                    */
 int nnab_dft_bank_tiles(int32_t n_bins, int32_t fold_nyquist);
 size_t nnab_dft_bank_bytes(int32_t n_bins, int32_t n_fft, int32_t fold_nyquist);
+/* bytes of each packed array (hi, and lo for the split modes) for `precision`:
+ * the FP16 modes store halves (K padded to 64) plus a 256-byte trailer in the
+ * hi array holding the bank's scale exponent; = nnab_dft_bank_bytes for TF32. */
+size_t nnab_dft_bank_bytes_prec(int32_t n_bins, int32_t n_fft, int32_t fold_nyquist, int32_t precision);
 int nnab_pack_dft_bank(const float* h_re, const float* h_im, int32_t n_bins, int32_t n_fft,
                        int32_t fold_nyquist, int32_t precision, float* packed_hi, float* packed_lo,
                        void* stream);

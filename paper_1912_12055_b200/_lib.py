@@ -17,9 +17,13 @@ OK, EINVAL, ECUDA, ENOTSUP, ENODEV = 0, 1, 2, 3, 4
 PAD_REFLECT, PAD_ZERO = 0, 1
 OUT_MAGNITUDE, OUT_POWER, OUT_COMPLEX, OUT_MEL, OUT_SMOOTH_MAG = 0, 1, 2, 3, 4
 OUT_LOG = 0x100  # flag: log(value + eps) in the fused epilogue (STFT / Mel)
-PREC_TF32, PREC_3XTF32 = 0, 1
+PREC_TF32, PREC_3XTF32, PREC_F16, PREC_3XF16 = 0, 1, 2, 3
 PAD_MODES = {"reflect": PAD_REFLECT, "constant_zero": PAD_ZERO, "constant": PAD_ZERO}
-PRECISIONS = {"tf32": PREC_TF32, "fp32": PREC_3XTF32, "3xtf32": PREC_3XTF32}
+# precision names -> operand modes.  "tf32" / "f16": one pass, peak-normalised error
+# <= 1e-3 (FP16 operands under exact power-of-two scales: TF32's 11-bit significand at
+# twice the tensor rate).  "fp32": <= 1e-5 (3xTF32; the STFT / Mel engine runs it as
+# 3xF16, the same accuracy at half the tensor-core time).
+PRECISIONS = {"tf32": PREC_TF32, "fp32": PREC_3XTF32, "3xtf32": PREC_3XTF32, "f16": PREC_F16, "3xf16": PREC_3XF16}
 
 
 class NnabError(RuntimeError):
@@ -43,6 +47,7 @@ SIGNATURES = {
     "nnab_frames_geometry": (C.c_int, [_FR, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "nnab_dft_bank_tiles": (C.c_int, [_i32, _i32]),
     "nnab_dft_bank_bytes": (_sz, [_i32, _i32, _i32]),
+    "nnab_dft_bank_bytes_prec": (_sz, [_i32, _i32, _i32, _i32]),
     "nnab_pack_dft_bank": (C.c_int, [_fp, _fp, _i32, _i32, _i32, _i32, _fp, _fp, _vp]),
     "nnab_stft_workspace_bytes": (_sz, [_FR, _i32]),
     "nnab_stft_forward": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _i32, _i32, _i32, _f32, _f32, _fp, _i32, _i32, _ip,

@@ -37,7 +37,7 @@ class DftLayerOp:
                  precision: str = "tf32", device="cuda"):
         # trainable sine rows may leave zero -> never fold the Nyquist bin
         self.engine = DftEngine(h_re, h_im, hop, center, pad_mode, precision=precision, device=device,
-                                allow_fold=False)
+                                allow_fold=False, f16_ok=False)
         self.eps = float(eps)
         self.device = self.engine.device
         self.prec = self.engine.precision

@@ -36,7 +36,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                 uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+                 uint32_t box_inner, uint32_t box_outer, int swizzle_bytes, int elem_bytes) {
   auto enc = get_encode();
   if (!enc) {
     std::snprintf(g_last_error, sizeof(g_last_error), "cuTensorMapEncodeTiled unavailable");
@@ -53,7 +53,7 @@ int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t ou
                           : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                           : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                 : CU_TENSOR_MAP_SWIZZLE_NONE;
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = enc(map, elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -82,6 +82,24 @@ int num_sms() {
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static size_t stage_bytes(const FrameGeom& g) { return align256((size_t)g.B * g.R * g.row_len * sizeof(float)); }
+
+// Staged-frames workspace: [hi rows][lo rows (split modes)][per-clip scale exponents (FP16 modes)];
+// rows are fp32 (TF32 modes) or FP16, laid out with the precision's K alignment.
+struct StageLayout {
+  FrameGeom g;
+  size_t half_bytes = 0, lo_off = 0, exp_off = 0, total = 0;
+};
+static int stage_layout(const nnab_frames* f, int32_t precision, StageLayout* s) {
+  if (!prec_valid(precision)) return NNAB_EINVAL;
+  int rc = frame_geometry(f, &s->g, prec_kalign(precision));
+  if (rc) return rc;
+  const size_t elem = prec_is_f16(precision) ? 2 : 4;
+  s->half_bytes = align256((size_t)s->g.B * s->g.R * s->g.row_len * elem);
+  s->lo_off = s->half_bytes;
+  s->exp_off = s->half_bytes * (prec_is_split(precision) ? 2 : 1);
+  s->total = s->exp_off + (prec_is_f16(precision) ? align256((size_t)s->g.B * 4) : 0);
+  return NNAB_OK;
+}
 
 static int check_device() {
   static std::atomic<int> cache[kMaxDevices];  // 0 unknown, 1 sm_100, 2 other / error
@@ -118,9 +136,9 @@ extern "C" const char* nnab_last_error(void) { return g_last_error; }
 extern "C" uint64_t nnab_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" size_t nnab_stft_workspace_bytes(const nnab_frames* f, int32_t precision) {
-  FrameGeom g;
-  if (frame_geometry(f, &g)) return 0;
-  return stage_bytes(g) * (precision == NNAB_PREC_3XTF32 ? 2 : 1);
+  StageLayout sl;
+  if (stage_layout(f, precision, &sl)) return 0;
+  return sl.total;
 }
 
 static int validate_kind(int32_t out_kind, int32_t n_bins, const float* mel_w, int32_t n_mels, int32_t mel_ld,
@@ -146,8 +164,8 @@ extern "C" int nnab_stft_forward(const nnab_frames* f, const float* x, const flo
   if (rc) return rc;
   FrameGeom g;
   if ((rc = frame_geometry(f, &g))) return rc;
-  if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
-  const int split = precision == NNAB_PREC_3XTF32;
+  if (!prec_valid(precision)) return NNAB_EINVAL;
+  const int split = prec_is_split(precision);
   if (!x || !packed_hi || (split && !packed_lo) || !out || n_bins < 1) return NNAB_EINVAL;
   if (fold_nyquist && n_bins < 2) return NNAB_EINVAL;
   const int32_t tiles = nnab_dft_bank_tiles(n_bins, fold_nyquist);
@@ -162,15 +180,18 @@ extern "C" int nnab_stage_frames(const nnab_frames* f, const float* x, int32_t p
                                  size_t workspace_bytes, void* stream) {
   int rc = check_device();
   if (rc) return rc;
-  FrameGeom g;
-  if ((rc = frame_geometry(f, &g))) return rc;
-  if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
+  StageLayout sl;
+  if ((rc = stage_layout(f, precision, &sl))) return rc;
+  const FrameGeom& g = sl.g;
   if (g.B == 0) return NNAB_OK;
-  if (!x || !workspace || workspace_bytes < nnab_stft_workspace_bytes(f, precision)) return NNAB_EINVAL;
-  const int split = precision == NNAB_PREC_3XTF32;
-  float* rows_hi = reinterpret_cast<float*>(workspace);
-  float* rows_lo = split ? reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + stage_bytes(g)) : nullptr;
-  return stage_frames(g, x, rows_hi, rows_lo, split, (cudaStream_t)stream);
+  if (!x || !workspace || workspace_bytes < sl.total) return NNAB_EINVAL;
+  const int split = prec_is_split(precision);
+  char* w = reinterpret_cast<char*>(workspace);
+  if (prec_is_f16(precision))
+    return stage_frames_f16(g, x, w, split ? w + sl.lo_off : nullptr, reinterpret_cast<int32_t*>(w + sl.exp_off),
+                            split, (cudaStream_t)stream);
+  return stage_frames(g, x, reinterpret_cast<float*>(w), split ? reinterpret_cast<float*>(w + sl.lo_off) : nullptr,
+                      split, (cudaStream_t)stream);
 }
 
 extern "C" int nnab_stft_forward_staged(const nnab_frames* f, const float* packed_hi, const float* packed_lo,
@@ -180,23 +201,27 @@ extern "C" int nnab_stft_forward_staged(const nnab_frames* f, const float* packe
                                         size_t workspace_bytes, void* stream) {
   int rc = check_device();
   if (rc) return rc;
-  FrameGeom g;
-  if ((rc = frame_geometry(f, &g))) return rc;
-  if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
-  const int split = precision == NNAB_PREC_3XTF32;
+  StageLayout sl;
+  if ((rc = stage_layout(f, precision, &sl))) return rc;
+  const FrameGeom& g = sl.g;
+  const int split = prec_is_split(precision);
   if (!packed_hi || (split && !packed_lo) || !out || n_bins < 1) return NNAB_EINVAL;
   if (fold_nyquist && n_bins < 2) return NNAB_EINVAL;
   const int32_t tiles = nnab_dft_bank_tiles(n_bins, fold_nyquist);
   if ((rc = validate_kind(out_kind, n_bins, mel_w, n_mels, mel_ld, tiles))) return rc;
   if (g.B == 0) return NNAB_OK;
-  if (!workspace || workspace_bytes < nnab_stft_workspace_bytes(f, precision)) return NNAB_EINVAL;
+  if (!workspace || workspace_bytes < sl.total) return NNAB_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  const float* rows_hi = reinterpret_cast<const float*>(workspace);
-  const float* rows_lo =
-      split ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + stage_bytes(g)) : nullptr;
+  const char* w = reinterpret_cast<const char*>(workspace);
   StftGemmArgs a{};
-  a.a_hi = rows_hi;
-  a.a_lo = rows_lo;
+  a.a_hi = reinterpret_cast<const float*>(w);
+  a.a_lo = split ? reinterpret_cast<const float*>(w + sl.lo_off) : nullptr;
+  if (prec_is_f16(precision)) {
+    a.a_exp = reinterpret_cast<const int32_t*>(w + sl.exp_off);
+    a.b_exp = reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(packed_hi) +
+                                               nnab_dft_bank_bytes_prec(n_bins, g.width, fold_nyquist, precision) -
+                                               256) + 1;
+  }
   a.b_hi = packed_hi;
   a.b_lo = packed_lo;
   a.n_tiles = tiles;

@@ -10,6 +10,8 @@
 // materialised, and the reflect/zero padding is resolved here with the exact
 // np.pad index map (gradients.py:18-25).  When hop does not divide into 32-sample
 // K blocks (or hop > width) the rows are whole frames (row_len = width rounded up).
+#include <cuda_fp16.h>
+
 #include <algorithm>
 
 #include "internal.h"
@@ -17,7 +19,7 @@
 
 namespace nnab {
 
-int frame_geometry(const nnab_frames* f, FrameGeom* g) {
+int frame_geometry(const nnab_frames* f, FrameGeom* g, int kalign) {
   if (!f || !g) return NNAB_EINVAL;
   if (f->batch < 0 || f->length < 1 || f->width < 1 || f->hop < 1 || f->pad < 0) return NNAB_EINVAL;
   if (f->pad_mode != NNAB_PAD_REFLECT && f->pad_mode != NNAB_PAD_ZERO) return NNAB_EINVAL;
@@ -33,8 +35,8 @@ int frame_geometry(const nnab_frames* f, FrameGeom* g) {
   int64_t T = (g->padded_len - f->width) / f->hop + 1;
   if (T > (1ll << 30)) return NNAB_ENOTSUP;
   g->T = (int32_t)T;
-  g->k_pad = (f->width + 31) / 32 * 32;
-  if (f->hop % 32 == 0 && f->hop <= g->k_pad) {
+  g->k_pad = (f->width + kalign - 1) / kalign * kalign;
+  if (f->hop % kalign == 0 && f->hop <= g->k_pad) {
     g->row_len = f->hop;
     g->R = g->T + (g->k_pad + f->hop - 1) / f->hop - 1;
   } else {
@@ -44,10 +46,70 @@ int frame_geometry(const nnab_frames* f, FrameGeom* g) {
   return NNAB_OK;
 }
 
+// The 4 padded samples i0 .. i0+3 of clip b (np.pad index map, signal.py:151;
+// 0 beyond the padded clip): interior groups of 4 samples are one aligned
+// 16-byte load (or two aligned loads and a funnel when clip starts are off
+// 16-byte boundaries), reflected groups a reversed funnel, the rest scalar.
+NNAB_DEV void gather4(const float* __restrict__ x, int64_t b, int64_t L, int32_t pad, int32_t mode,
+                      int64_t padded_len, bool aligned_clips, bool x_aligned, int64_t i0, float* v) {
+  const float* xb = x + b * L;
+  const int64_t j0 = i0 - pad;    // source sample
+  const int64_t ga = b * L + j0;  // absolute source index
+  if (aligned_clips && j0 >= 0 && j0 + 3 < L && i0 + 3 < padded_len) {
+    const float4 w = __ldg(reinterpret_cast<const float4*>(xb + j0));
+    v[0] = w.x;
+    v[1] = w.y;
+    v[2] = w.z;
+    v[3] = w.w;
+  } else if (x_aligned && j0 >= 0 && j0 - (ga & 3) + 7 < L && i0 + 3 < padded_len) {
+    // interior of a clip whose rows start off a 16-byte boundary (e.g. the CQT
+    // pad of 11,341): two aligned loads and a funnel by the misalignment
+    const float4* a4 = reinterpret_cast<const float4*>(x + (ga & ~int64_t(3)));
+    const float4 w0 = __ldg(a4), w1 = __ldg(a4 + 1);
+    const float e[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const int m = (int)(ga & 3);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = m == 0 ? e[u] : m == 1 ? e[u + 1] : m == 2 ? e[u + 2] : e[u + 3];
+  } else if (x_aligned && mode == NNAB_PAD_REFLECT && i0 + 3 < padded_len &&
+             ((j0 + 3 < 0 && -j0 < L) || (j0 >= L && 2 * (L - 1) - j0 - 3 >= 0))) {
+    // a reflected group (np.pad "reflect": one mirror image, left or right):
+    // its 4 sources are one descending run -- the same funnel, reversed
+    const int64_t a_lo = j0 < 0 ? -j0 - 3 : 2 * (L - 1) - j0 - 3;
+    const int64_t gl = b * L + a_lo;
+    if (a_lo - (gl & 3) + 7 < L) {
+      const float4* a4 = reinterpret_cast<const float4*>(x + (gl & ~int64_t(3)));
+      const float4 w0 = __ldg(a4), w1 = __ldg(a4 + 1);
+      const float e[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      const int m = (int)(gl & 3);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[3 - u] = m == 0 ? e[u] : m == 1 ? e[u + 1] : m == 2 ? e[u + 2] : e[u + 3];
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[3 - u] = __ldg(xb + a_lo + u);
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u;
+      float sv = 0.f;
+      if (i < padded_len) {
+        int64_t j = i - pad;
+        if (mode == NNAB_PAD_REFLECT) {
+          if (j < 0) j = -j;
+          if (j >= L) j = 2 * (L - 1) - j;
+          sv = __ldg(xb + j);
+        } else if (j >= 0 && j < L) {
+          sv = __ldg(xb + j);
+        }
+      }
+      v[u] = sv;
+    }
+  }
+}
+
 // rows[(b*R + r)*row_len + c] = padded_b[r*hop + c]  (0 beyond the padded clip),
 // TF32-rounded (split=0) or split into tf32 hi + tf32 lo residual (split=1).
-// One CTA walks whole rows (no 64-bit divisions per element); interior groups of
-// 4 samples are one aligned 16-byte load, the reflect/zero edges go element-wise.
+// One CTA walks whole rows (no 64-bit divisions per element).
 __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict__ x, int64_t B, int64_t L,
                                                          int32_t pad, int32_t mode, int32_t hop, int32_t row_len,
                                                          int32_t R, int64_t padded_len, int split,
@@ -63,64 +125,11 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
   for (int64_t grow = (int64_t)blockIdx.x * rpb + sub; grow < rows; grow += (int64_t)gridDim.x * rpb) {
     const int64_t b = grow / R;
     const int64_t r = grow - b * R;
-    const float* xb = x + b * L;
     float4* hrow = reinterpret_cast<float4*>(hi) + grow * q_per_row;
     float4* lrow = reinterpret_cast<float4*>(lo) + grow * q_per_row;
     for (int32_t q = lane; q < q_per_row; q += per) {
-      const int64_t i0 = r * hop + 4 * q;  // padded position of the first sample
-      const int64_t j0 = i0 - pad;         // source sample
       float v[4];
-      const int64_t ga = b * L + j0;  // absolute source index
-      if (aligned_clips && j0 >= 0 && j0 + 3 < L && i0 + 3 < padded_len) {
-        const float4 w = __ldg(reinterpret_cast<const float4*>(xb + j0));
-        v[0] = w.x;
-        v[1] = w.y;
-        v[2] = w.z;
-        v[3] = w.w;
-      } else if (x_aligned && j0 >= 0 && j0 - (ga & 3) + 7 < L && i0 + 3 < padded_len) {
-        // interior of a clip whose rows start off a 16-byte boundary (e.g. the CQT
-        // pad of 11,341): two aligned loads and a funnel by the misalignment
-        const float4* a4 = reinterpret_cast<const float4*>(x + (ga & ~int64_t(3)));
-        const float4 w0 = __ldg(a4), w1 = __ldg(a4 + 1);
-        const float e[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        const int m = (int)(ga & 3);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = m == 0 ? e[u] : m == 1 ? e[u + 1] : m == 2 ? e[u + 2] : e[u + 3];
-      } else if (x_aligned && mode == NNAB_PAD_REFLECT && i0 + 3 < padded_len &&
-                 ((j0 + 3 < 0 && -j0 < L) || (j0 >= L && 2 * (L - 1) - j0 - 3 >= 0))) {
-        // a reflected group (np.pad "reflect": one mirror image, left or right):
-        // its 4 sources are one descending run -- the same funnel, reversed
-        const int64_t a_lo = j0 < 0 ? -j0 - 3 : 2 * (L - 1) - j0 - 3;
-        const int64_t gl = b * L + a_lo;
-        if (a_lo - (gl & 3) + 7 < L) {
-          const float4* a4 = reinterpret_cast<const float4*>(x + (gl & ~int64_t(3)));
-          const float4 w0 = __ldg(a4), w1 = __ldg(a4 + 1);
-          const float e[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-          const int m = (int)(gl & 3);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) v[3 - u] = m == 0 ? e[u] : m == 1 ? e[u + 1] : m == 2 ? e[u + 2] : e[u + 3];
-        } else {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) v[3 - u] = __ldg(xb + a_lo + u);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t i = i0 + u;
-          float sv = 0.f;
-          if (i < padded_len) {
-            int64_t j = i - pad;
-            if (mode == NNAB_PAD_REFLECT) {
-              if (j < 0) j = -j;
-              if (j >= L) j = 2 * (L - 1) - j;
-              sv = __ldg(xb + j);
-            } else if (j >= 0 && j < L) {
-              sv = __ldg(xb + j);
-            }
-          }
-          v[u] = sv;
-        }
-      }
+      gather4(x, b, L, pad, mode, padded_len, aligned_clips, x_aligned, r * hop + 4 * q, v);
       float4 h, l;
       h.x = tf32_rne(v[0]);
       h.y = tf32_rne(v[1]);
@@ -138,12 +147,111 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
   }
 }
 
+// FP16 operands: 2^scale_exp(peak) so the clip's peak lands in [2^14, 2^15)
+// (FP16's 11-bit significand = TF32's, with the 5-bit exponent kept in range by
+// the exact power-of-two scale).  0 for a silent clip; clamped so 2^e is finite.
+NNAB_DEV int f16_scale_exp(float peak) {
+  int ex = 0;
+  if (peak > 0.f && peak < INFINITY) frexpf(peak, &ex);  // peak = m 2^ex, m in [0.5, 1)
+  return peak > 0.f ? max(-100, min(100, 15 - ex)) : 0;
+}
+
+// One CTA per clip (persistent over clips): pass 1 finds the clip's peak, pass 2
+// (the clip now in L2) writes its hop rows scaled by 2^e as FP16 (split: hi =
+// RN(v), lo = RN(v - hi), 22 significant bits), and exps[b] = e.
+__global__ void __launch_bounds__(1024) stage_rows_f16_kernel(const float* __restrict__ x, int64_t B, int64_t L,
+                                                              int32_t pad, int32_t mode, int32_t hop, int32_t row_len,
+                                                              int32_t R, int64_t padded_len, int split,
+                                                              __half* __restrict__ hi, __half* __restrict__ lo,
+                                                              int32_t* __restrict__ exps) {
+  __shared__ float red[32];
+  const bool aligned_clips = (L % 4) == 0 && (pad % 4) == 0 && (hop % 4) == 0;
+  const bool x_aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const int32_t q_per_row = row_len / 4;
+  const int64_t groups = (int64_t)R * q_per_row;
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    const float* xb = x + b * L;
+    float mx = 0.f;
+    if (x_aligned && ((b * L) & 3) == 0) {
+      const int64_t n4 = L / 4;
+      const float4* x4 = reinterpret_cast<const float4*>(xb);
+      const int64_t step = blockDim.x;
+      int64_t i = threadIdx.x;
+      for (; i + 3 * step < n4; i += 4 * step) {  // 4 loads in flight per thread (64 KB per SM)
+        float4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = __ldg(x4 + i + u * step);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(w[u].x), fabsf(w[u].y)), fmaxf(fabsf(w[u].z), fabsf(w[u].w))));
+      }
+      for (; i < n4; i += step) {
+        const float4 w = __ldg(x4 + i);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(w.x), fabsf(w.y)), fmaxf(fabsf(w.z), fabsf(w.w))));
+      }
+      for (int64_t i = 4 * n4 + threadIdx.x; i < L; i += blockDim.x) mx = fmaxf(mx, fabsf(__ldg(xb + i)));
+    } else {
+      for (int64_t i = threadIdx.x; i < L; i += blockDim.x) mx = fmaxf(mx, fabsf(__ldg(xb + i)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (threadIdx.x == 0) red[0] = m;
+    }
+    __syncthreads();
+    const int e = f16_scale_exp(red[0]);
+    __syncthreads();  // red[] reused by the next clip
+    if (threadIdx.x == 0) exps[b] = e;
+    const float sc = ldexpf(1.f, e);
+    uint2* hrow = reinterpret_cast<uint2*>(hi) + b * groups;
+    uint2* lrow = reinterpret_cast<uint2*>(lo) + b * groups;
+    for (int64_t gq = threadIdx.x; gq < groups; gq += blockDim.x) {
+      const int64_t r = gq / q_per_row;
+      const int32_t q = (int32_t)(gq - r * q_per_row);
+      float v[4];
+      gather4(x, b, L, pad, mode, padded_len, aligned_clips, x_aligned, r * hop + 4 * q, v);
+      __half2 h01 = __floats2half2_rn(v[0] * sc, v[1] * sc), h23 = __floats2half2_rn(v[2] * sc, v[3] * sc);
+      uint2 hv;
+      hv.x = *reinterpret_cast<uint32_t*>(&h01);
+      hv.y = *reinterpret_cast<uint32_t*>(&h23);
+      hrow[gq] = hv;
+      if (split) {
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        __half2 l01 = __floats2half2_rn(v[0] * sc - f01.x, v[1] * sc - f01.y);
+        __half2 l23 = __floats2half2_rn(v[2] * sc - f23.x, v[3] * sc - f23.y);
+        uint2 lv;
+        lv.x = *reinterpret_cast<uint32_t*>(&l01);
+        lv.y = *reinterpret_cast<uint32_t*>(&l23);
+        lrow[gq] = lv;
+      }
+    }
+  }
+}
+
 int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows_lo, int split, cudaStream_t s) {
   const int64_t rows = g.B * (int64_t)g.R;
   if (rows == 0) return NNAB_OK;
   const int blocks = (int)std::min<int64_t>(rows, (int64_t)num_sms() * 16);
   stage_rows_kernel<<<blocks, 256, 0, s>>>(x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.row_len, g.R, g.padded_len,
                                           split, rows_hi, rows_lo);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
+int stage_frames_f16(const FrameGeom& g, const float* x, void* rows_hi, void* rows_lo, int32_t* exps, int split,
+                     cudaStream_t s) {
+  if (g.B == 0) return NNAB_OK;
+  // one clip per CTA at a time, one CTA per SM: 148 clips (47 MB) in flight, so
+  // pass 2 re-reads each clip from L2
+  const int blocks = (int)std::min<int64_t>(g.B, (int64_t)num_sms());
+  stage_rows_f16_kernel<<<blocks, 1024, 0, s>>>(x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.row_len, g.R, g.padded_len,
+                                               split, reinterpret_cast<__half*>(rows_hi),
+                                               reinterpret_cast<__half*>(rows_lo), exps);
   NNAB_LAUNCHED();
   return NNAB_OK;
 }
@@ -175,6 +283,45 @@ __global__ void pack_dft_bank_kernel(const float* __restrict__ h_re, const float
   }
 }
 
+// FP16 bank: |h| peak over both banks (as ordered bits of a non-negative float)
+__global__ void bank_absmax_kernel(const float* __restrict__ a, const float* __restrict__ b, int64_t n,
+                                   unsigned int* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fmaxf(fabsf(__ldg(a + i)), fabsf(__ldg(b + i))));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
+// The same tile layout as pack_dft_bank_kernel in FP16, scaled by 2^e_h (peak in
+// [2^14, 2^15)); trailer[1] = e_h for the GEMM epilogue.
+__global__ void pack_dft_bank_f16_kernel(const float* __restrict__ h_re, const float* __restrict__ h_im,
+                                         int32_t n_bins, int32_t n_fft, int32_t k_pad, int32_t n_tiles, int32_t fold,
+                                         int32_t split, __half* __restrict__ hi, __half* __restrict__ lo,
+                                         int32_t* __restrict__ trailer) {
+  const int e = f16_scale_exp(__uint_as_float(static_cast<unsigned int>(trailer[0])));
+  const float sc = ldexpf(1.f, e);
+  if (blockIdx.x == 0 && threadIdx.x == 0) trailer[1] = e;
+  const int64_t total = (int64_t)n_tiles * 256 * k_pad;
+  const int32_t n_body = fold ? n_bins - 1 : n_bins;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / k_pad;
+    const int32_t k = (int32_t)(i - row * k_pad);
+    const int32_t tile = (int32_t)(row / 256), col = (int32_t)(row % 256);
+    const int32_t bin = tile * 128 + (col & 127);
+    float v = 0.f;
+    if (k < n_fft) {
+      if (fold && tile == 0 && col == 128) v = h_re[(int64_t)(n_bins - 1) * n_fft + k];
+      else if (bin < n_body) v = (col >= 128 ? h_im : h_re)[(int64_t)bin * n_fft + k];
+    }
+    v *= sc;
+    const __half h = __float2half_rn(v);
+    hi[i] = h;
+    if (split) lo[i] = __float2half_rn(v - __half2float(h));
+  }
+}
+
 }  // namespace nnab
 
 using namespace nnab;
@@ -190,19 +337,45 @@ extern "C" size_t nnab_dft_bank_bytes(int32_t n_bins, int32_t n_fft, int32_t fol
   return (size_t)nnab_dft_bank_tiles(n_bins, fold_nyquist) * 256 * k_pad * sizeof(float);
 }
 
+extern "C" size_t nnab_dft_bank_bytes_prec(int32_t n_bins, int32_t n_fft, int32_t fold_nyquist, int32_t precision) {
+  if (!prec_is_f16(precision)) return nnab_dft_bank_bytes(n_bins, n_fft, fold_nyquist);
+  const int64_t k_pad = (n_fft + 63) / 64 * 64;
+  const size_t data = (size_t)nnab_dft_bank_tiles(n_bins, fold_nyquist) * 256 * k_pad * 2;
+  return ((data + 255) & ~size_t(255)) + 256;  // + trailer: [0] peak bits, [1] scale exponent
+}
+
 extern "C" int nnab_pack_dft_bank(const float* h_re, const float* h_im, int32_t n_bins, int32_t n_fft,
                                   int32_t fold_nyquist, int32_t precision, float* packed_hi, float* packed_lo,
                                   void* stream) {
   if (!h_re || !h_im || !packed_hi || n_bins < 1 || n_fft < 1) return NNAB_EINVAL;
   if (fold_nyquist && n_bins < 2) return NNAB_EINVAL;
-  const int split = precision == NNAB_PREC_3XTF32;
+  if (precision < NNAB_PREC_TF32 || precision > NNAB_PREC_3XF16) return NNAB_EINVAL;
+  const int split = prec_is_split(precision);
   if (split && !packed_lo) return NNAB_EINVAL;
-  const int32_t k_pad = (n_fft + 31) / 32 * 32;
   const int32_t tiles = nnab_dft_bank_tiles(n_bins, fold_nyquist);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (prec_is_f16(precision)) {
+    const int32_t k_pad = (n_fft + 63) / 64 * 64;
+    const int64_t total = (int64_t)tiles * 256 * k_pad;
+    int32_t* trailer = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(packed_hi) +
+                                                  nnab_dft_bank_bytes_prec(n_bins, n_fft, fold_nyquist, precision) -
+                                                  256);
+    NNAB_CUDA_TRY(cudaMemsetAsync(trailer, 0, 8, s));
+    const int64_t n = (int64_t)n_bins * n_fft;
+    bank_absmax_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(
+        h_re, h_im, n, reinterpret_cast<unsigned int*>(trailer));
+    NNAB_LAUNCHED();
+    pack_dft_bank_f16_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, s>>>(
+        h_re, h_im, n_bins, n_fft, k_pad, tiles, fold_nyquist, split, reinterpret_cast<__half*>(packed_hi),
+        reinterpret_cast<__half*>(packed_lo), trailer);
+    NNAB_LAUNCHED();
+    return NNAB_OK;
+  }
+  const int32_t k_pad = (n_fft + 31) / 32 * 32;
   const int64_t total = (int64_t)tiles * 256 * k_pad;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
-  pack_dft_bank_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(h_re, h_im, n_bins, n_fft, k_pad, tiles,
-                                                                 fold_nyquist, split, packed_hi, packed_lo);
+  pack_dft_bank_kernel<<<blocks, 256, 0, s>>>(h_re, h_im, n_bins, n_fft, k_pad, tiles, fold_nyquist, split,
+                                              packed_hi, packed_lo);
   NNAB_LAUNCHED();
   return NNAB_OK;
 }

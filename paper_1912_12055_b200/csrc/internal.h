@@ -27,7 +27,7 @@ void note_launch();
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                 uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+                 uint32_t box_inner, uint32_t box_outer, int swizzle_bytes, int elem_bytes = 4);
 
 int num_sms();
 
@@ -41,16 +41,28 @@ struct FrameGeom {
   int32_t R;         // staged rows per clip
   int64_t padded_len;
 };
-int frame_geometry(const nnab_frames* f, FrameGeom* g);
+// kalign: K-block alignment of the staged rows in elements (32 for the fp32 /
+// TF32 operand modes, 64 for FP16: one 128-byte swizzle row)
+int frame_geometry(const nnab_frames* f, FrameGeom* g, int kalign = 32);
+
+inline bool prec_is_f16(int p) { return p == NNAB_PREC_F16 || p == NNAB_PREC_3XF16; }
+inline bool prec_is_split(int p) { return p == NNAB_PREC_3XTF32 || p == NNAB_PREC_3XF16; }
+inline int prec_kalign(int p) { return prec_is_f16(p) ? 64 : 32; }
+inline bool prec_valid(int p) { return p >= NNAB_PREC_TF32 && p <= NNAB_PREC_3XF16; }
 
 int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows_lo, int split,
                  cudaStream_t s);
+// FP16 hop rows scaled per clip by 2^exps[b] (frames.cu)
+int stage_frames_f16(const FrameGeom& g, const float* x, void* rows_hi, void* rows_lo, int32_t* exps, int split,
+                     cudaStream_t s);
 
 struct StftGemmArgs {
-  const float* a_hi;  // staged rows (B*R, row_len)
+  const float* a_hi;  // staged rows (B*R, row_len) -- fp32, or FP16 in the F16 modes
   const float* a_lo;
   const float* b_hi;  // packed bank (n_tiles*256, k_pad)
   const float* b_lo;
+  const int32_t* a_exp = nullptr;  // F16 modes: per-clip scale exponent of the staged rows
+  const int32_t* b_exp = nullptr;  // F16 modes: the bank's scale exponent (pack trailer)
   int32_t n_tiles;
   int32_t n_bins;
   int32_t fold;

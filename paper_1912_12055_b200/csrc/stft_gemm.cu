@@ -37,22 +37,38 @@ constexpr int kBN = 256;  // 128 bins x {cos, sin}
 constexpr int kThreads = 256;
 constexpr int kMelRows = 128;  // mel accumulator rows resident in smem
 
-template <bool kSplit, bool kPair>
+// kP: NNAB_PREC_* (TF32, 3xTF32, F16, 3xF16)
+template <int kP, bool kPair>
 struct Cfg {
-  static constexpr int BK = kSplit ? 16 : 32;            // fp32 elements per K block
-  static constexpr int SWZ = BK * 4;                     // swizzle span in bytes (64 or 128)
-  static constexpr int A_BYTES = kBM * BK * 4;           // 16 KB | 8 KB
+  static constexpr bool kSplit = kP == NNAB_PREC_3XTF32 || kP == NNAB_PREC_3XF16;
+  static constexpr bool kHalf = kP == NNAB_PREC_F16 || kP == NNAB_PREC_3XF16;
+  static constexpr int ELEM = kHalf ? 2 : 4;              // operand bytes
+  static constexpr int SWZ = kSplit ? 64 : 128;           // swizzle span = bytes of one K block row
+  static constexpr int BK = SWZ / ELEM;                   // elements per K block (TF32 32|16, FP16 64|32)
+  static constexpr int KSTEPS = SWZ / 32;                 // MMAs per K block (32 bytes of K each)
+  static constexpr int A_BYTES = kBM * SWZ;               // 16 KB | 8 KB
   // a CTA pair splits the N = 256 bank rows: each CTA stages 128 of them
-  static constexpr int B_BYTES = (kPair ? kBN / 2 : kBN) * BK * 4;
+  static constexpr int B_BYTES = (kPair ? kBN / 2 : kBN) * SWZ;
   static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);  // 48 KB | 32 KB (pair)
-  // TF32: two 256-column accumulators (double buffer).  3xTF32: one buffer of
+  // unsplit: two 256-column accumulators (double buffer).  Split: one buffer of
   // main (hi*hi) + correction (hi*lo + lo*hi) accumulators.  Keeping the large
   // hi*hi chain apart from the small cross terms cuts the number of
   // accumulate steps the big partial sums go through by 3x, which is what
-  // bounds 3xTF32 accuracy (the tensor-core FP32 accumulate is not RNE).
+  // bounds the split modes' accuracy (the tensor-core FP32 accumulate is not RNE).
   static constexpr int NUM_ACC = kSplit ? 1 : 2;
   static constexpr int ACC_STRIDE = kSplit ? 512 : 256;
+  static constexpr uint32_t idesc(uint32_t M, uint32_t N) { return kHalf ? idesc_f16(M, N) : idesc_tf32(M, N); }
 };
+
+NNAB_DEV void mma_any(bool half, bool pair, uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (half) {
+    if (pair) mma_f16_pair(d, a, b, idesc, acc);
+    else mma_f16(d, a, b, idesc, acc);
+  } else {
+    if (pair) mma_tf32_pair(d, a, b, idesc, acc);
+    else mma_tf32(d, a, b, idesc, acc);
+  }
+}
 
 struct Params {
   int64_t B;
@@ -68,6 +84,9 @@ struct Params {
   int32_t n_tab, b_box, pairs, out_bins;
   float log_eps;  // >= 0: outputs are log(value + log_eps) (NNAB_OUT_LOG)
   int32_t stages;  // smem pipeline depth (4, or 3 when the Mel accumulator takes 64 KB)
+  // FP16 modes: epilogue scale 2^-(a_exp[clip] + *b_exp) undoes the operand scales (null: 1)
+  const int32_t* a_exp;
+  const int32_t* b_exp;
   // training forward: re, im and smoothed magnitude per (bin, slot) saved in
   // slot-major layout [bin][ld_slots] for the backward GEMMs (may be null)
   float *save_re, *save_im, *save_mag;
@@ -100,12 +119,13 @@ NNAB_DEV float finish(float re, float im, int kind, float power, float eps) {
   return fast_sqrt(p);
 }
 
-template <bool kSplit, bool kPair>
+template <int kP, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     stft_gemm_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                      const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
                      const Params p) {
-  using C = Cfg<kSplit, kPair>;
+  using C = Cfg<kP, kPair>;
+  constexpr bool kSplit = C::kSplit;
   const bool mel = p.out_kind == NNAB_OUT_MEL;
   const int stages = p.stages;
   const uint32_t rank = kPair ? cluster_ctarank() : 0;  // 0 = leader (issues the pair's MMAs)
@@ -160,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nt = p.n_tiles;
   const int n_iter = p.kb_tab ? p.n_tab : p.kblocks;
   const int b_rows = kPair ? p.b_box / 2 : p.b_box;  // bank rows this CTA stages per K block
-  const uint32_t stage_tx = (uint32_t)(C::A_BYTES + b_rows * C::BK * 4) * (kSplit ? 2 : 1) * (kPair ? 2 : 1);
+  const uint32_t stage_tx = (uint32_t)(C::A_BYTES + b_rows * C::SWZ) * (kSplit ? 2 : 1) * (kPair ? 2 : 1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -209,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (rank == 0 && elect_one()) {
       constexpr uint32_t kM = kPair ? 2 * kBM : kBM;
-      constexpr uint32_t idesc_full = idesc_tf32(kM, kBN);
+      constexpr uint32_t idesc_full = C::idesc(kM, kBN);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -221,29 +241,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d = tmem_base + acc * C::ACC_STRIDE;
           for (int kb = 0; kb < n_iter; ++kb) {
             uint32_t idesc = idesc_full;
-            if (p.kb_tab) idesc = idesc_tf32(kM, __ldg(p.kb_tab + n * p.n_tab + kb) & 0xffffu);
+            if (p.kb_tab) idesc = C::idesc(kM, __ldg(p.kb_tab + n * p.n_tab + kb) & 0xffffu);
             mbar_wait(&full[s], ph);
             tc_fence_after();
             uint8_t* st = smem + s * C::STAGE_BYTES;
             const uint64_t a_hi = make_sdesc(st, C::SWZ);
             const uint64_t b_hi = make_sdesc(st + C::A_BYTES, C::SWZ);
 #pragma unroll
-            for (int k = 0; k < C::BK / 8; ++k) {
-              const uint64_t off = (uint64_t)((k * 32) >> 4);  // 8 tf32 = 32 bytes along K
+            for (int k = 0; k < C::KSTEPS; ++k) {
+              const uint64_t off = (uint64_t)((k * 32) >> 4);  // 32 bytes along K per MMA
               const uint64_t a_lo = make_sdesc(st + C::A_BYTES + C::B_BYTES, C::SWZ);
               const uint64_t b_lo = make_sdesc(st + 2 * C::A_BYTES + C::B_BYTES, C::SWZ);
-              if (kPair) {
-                mma_tf32_pair(d, a_hi + off, b_hi + off, idesc, (kb | k) != 0);
-                if (kSplit) {
-                  mma_tf32_pair(d + kBN, a_hi + off, b_lo + off, idesc, (kb | k) != 0);
-                  mma_tf32_pair(d + kBN, a_lo + off, b_hi + off, idesc, 1);
-                }
-              } else {
-                mma_tf32(d, a_hi + off, b_hi + off, idesc, (kb | k) != 0);
-                if (kSplit) {
-                  mma_tf32(d + kBN, a_hi + off, b_lo + off, idesc, (kb | k) != 0);
-                  mma_tf32(d + kBN, a_lo + off, b_hi + off, idesc, 1);
-                }
+              mma_any(C::kHalf, kPair, d, a_hi + off, b_hi + off, idesc, (kb | k) != 0);
+              if (kSplit) {
+                mma_any(C::kHalf, kPair, d + kBN, a_hi + off, b_lo + off, idesc, (kb | k) != 0);
+                mma_any(C::kHalf, kPair, d + kBN, a_lo + off, b_hi + off, idesc, 1);
               }
             }
             if (kPair) mma_commit_pair(&empty[s], 0x3);
@@ -278,6 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t = (int)(g - b * p.R);
       const bool valid = b < p.B && t < p.T;
       float nyq_val = 0.f;
+      // FP16 modes: undo the operand scales (exact powers of two)
+      const float osc = (C::kHalf && p.a_exp) ? ldexpf(1.f, -(__ldg(p.a_exp + min(b, p.B - 1)) + __ldg(p.b_exp))) : 1.f;
       for (int n = 0; n < nt; ++n) {
         mbar_wait(&tmem_full[acc], aph);
         tc_fence_after();
@@ -298,6 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 32; ++j) v[j] += cv[j];
             } else {
               tmem_ld_wait();
+            }
+            if (C::kHalf) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] *= osc;
             }
             if (valid) {
               const int bin0 = n * 128 + c * 16;
@@ -335,6 +353,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
             tmem_ld_wait();
+          }
+          if (C::kHalf) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              re[j] *= osc;
+              im[j] *= osc;
+            }
           }
           const int bin0 = n * 128 + c * 32;
           float nyq_re = 0.f;
@@ -471,22 +496,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <bool kSplit, bool kPair>
+template <int kP, bool kPair>
 int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
-  using C = Cfg<kSplit, kPair>;
+  using C = Cfg<kP, kPair>;
+  constexpr bool kSplit = C::kSplit;
   const bool mel = (a.out_kind & ~NNAB_OUT_LOG) == NNAB_OUT_MEL;
   if (mel && (a.n_mels < 1 || a.n_mels > kMelRows || !a.mel_w || a.mel_ld % 4 != 0)) return NNAB_ENOTSUP;
-  if (g.row_len % C::BK != 0) return NNAB_ENOTSUP;
+  if (g.row_len % C::BK != 0 || g.k_pad % C::BK != 0) return NNAB_ENOTSUP;
+  if (C::kHalf && (!a.a_exp || !a.b_exp)) return NNAB_EINVAL;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   const uint64_t rows_total = (uint64_t)g.B * g.R;
   const uint64_t bank_rows = (uint64_t)a.n_tiles * kBN;
   const int b_box = a.b_box > 0 ? a.b_box : kBN;
   if (b_box % 16 != 0 || b_box > kBN) return NNAB_EINVAL;
   const int b_rows = kPair ? b_box / 2 : b_box;  // each CTA of a pair stages half the bank rows
-  int rc = make_tmap_2d(&ta_hi, a.a_hi, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
-  if (!rc) rc = make_tmap_2d(&tb_hi, a.b_hi, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, b_rows, C::SWZ);
-  if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, a.a_lo, g.row_len, rows_total, (uint64_t)g.row_len * 4, C::BK, kBM, C::SWZ);
-  if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, a.b_lo, g.k_pad, bank_rows, (uint64_t)g.k_pad * 4, C::BK, b_rows, C::SWZ);
+  constexpr int E = C::ELEM;
+  int rc = make_tmap_2d(&ta_hi, a.a_hi, g.row_len, rows_total, (uint64_t)g.row_len * E, C::BK, kBM, C::SWZ, E);
+  if (!rc) rc = make_tmap_2d(&tb_hi, a.b_hi, g.k_pad, bank_rows, (uint64_t)g.k_pad * E, C::BK, b_rows, C::SWZ, E);
+  if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, a.a_lo, g.row_len, rows_total, (uint64_t)g.row_len * E, C::BK, kBM, C::SWZ, E);
+  if (!rc && kSplit) rc = make_tmap_2d(&tb_lo, a.b_lo, g.k_pad, bank_rows, (uint64_t)g.k_pad * E, C::BK, b_rows, C::SWZ, E);
   if (rc) return rc;
   if (!kSplit) {
     ta_lo = ta_hi;
@@ -516,6 +544,8 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.save_im = a.save_im;
   p.save_mag = a.save_mag;
   p.ld_slots = a.ld_slots;
+  p.a_exp = a.a_exp;
+  p.b_exp = a.b_exp;
   if (a.save_re && a.pairs) return NNAB_EINVAL;
   if (a.save_re && !a.save_im && kSplit) return NNAB_EINVAL;  // phasor saves: TF32 only
   p.n_tab = a.n_tab;
@@ -531,7 +561,7 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   if (const char* e = getenv("NNAB_DEBUG_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));
   p.stages = stages;
   const size_t smem = 1024 + (size_t)stages * C::STAGE_BYTES + mel_bytes + 256;
-  auto kern = stft_gemm_kernel<kSplit, kPair>;
+  auto kern = stft_gemm_kernel<kP, kPair>;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (!kPair) {
     const int grid = std::min(p.n_mtiles, num_sms());
@@ -565,9 +595,13 @@ int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, c
     const char* e = getenv("NNAB_CTA_PAIR");
     return !(e && e[0] == '0');
   }();
-  if (precision == NNAB_PREC_3XTF32) return pair ? launch_impl<true, true>(g, a, s) : launch_impl<true, false>(g, a, s);
-  if (precision == NNAB_PREC_TF32) return pair ? launch_impl<false, true>(g, a, s) : launch_impl<false, false>(g, a, s);
-  return NNAB_EINVAL;
+  switch (precision) {
+    case NNAB_PREC_TF32: return pair ? launch_impl<NNAB_PREC_TF32, true>(g, a, s) : launch_impl<NNAB_PREC_TF32, false>(g, a, s);
+    case NNAB_PREC_3XTF32: return pair ? launch_impl<NNAB_PREC_3XTF32, true>(g, a, s) : launch_impl<NNAB_PREC_3XTF32, false>(g, a, s);
+    case NNAB_PREC_F16: return pair ? launch_impl<NNAB_PREC_F16, true>(g, a, s) : launch_impl<NNAB_PREC_F16, false>(g, a, s);
+    case NNAB_PREC_3XF16: return pair ? launch_impl<NNAB_PREC_3XF16, true>(g, a, s) : launch_impl<NNAB_PREC_3XF16, false>(g, a, s);
+    default: return NNAB_EINVAL;
+  }
 }
 
 }  // namespace nnab

@@ -69,12 +69,19 @@ class DftEngine:
     because their sine rows may become non-zero.
     """
 
+    # "fp32" on this engine: the FP16 hi/lo split (same <= 1e-5 accuracy as 3xTF32, 2x the MMA rate)
+    FP32_MODE = L.PREC_3XF16
+
     def __init__(self, h_re, h_im, hop: int, center: bool = True, pad_mode: str = "reflect",
-                 precision: str = "tf32", device="cuda", allow_fold: bool = True):
+                 precision: str = "tf32", device="cuda", allow_fold: bool = True, f16_ok: bool = True):
         self.device = _require_cuda(device)
         if precision not in L.PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
         self.precision = L.PRECISIONS[precision]
+        if precision == "fp32" and f16_ok:
+            self.precision = self.FP32_MODE
+        if not f16_ok and self.precision in (L.PREC_F16, L.PREC_3XF16):
+            raise ValueError("this layer supports precision 'tf32' or 'fp32' (3xTF32)")
         h_re = torch.as_tensor(h_re)
         h_im = torch.as_tensor(h_im)
         if h_re.shape != h_im.shape or h_re.dim() != 2:
@@ -100,12 +107,13 @@ class DftEngine:
         lib = L.load()
         h_re = torch.as_tensor(h_re).to(self.device, torch.float32).contiguous()
         h_im = torch.as_tensor(h_im).to(self.device, torch.float32).contiguous()
-        nbytes = lib.nnab_dft_bank_bytes(self.n_bins, self.n_fft, self.fold)
+        self._bank = (h_re, h_im)
+        nbytes = lib.nnab_dft_bank_bytes_prec(self.n_bins, self.n_fft, self.fold, self.precision)
         n = nbytes // 4
         if getattr(self, "packed_hi", None) is None or self.packed_hi.numel() != n:
             self.packed_hi = torch.empty(n, dtype=torch.float32, device=self.device)
             self.packed_lo = (torch.empty(n, dtype=torch.float32, device=self.device)
-                              if self.precision == L.PREC_3XTF32 else None)
+                              if self.precision in (L.PREC_3XTF32, L.PREC_3XF16) else None)
         L.check(lib.nnab_pack_dft_bank(h_re.data_ptr(), h_im.data_ptr(), self.n_bins, self.n_fft, self.fold,
                                        self.precision, self.packed_hi.data_ptr(), L.ptr(self.packed_lo),
                                        L.stream_handle(self.device)), "pack_dft_bank")
@@ -124,6 +132,9 @@ class DftEngine:
         self.power = float(power)
         self.mel_wide = self.n_mels > 128
         if self.mel_wide:
+            if self.precision in (L.PREC_F16, L.PREC_3XF16):  # the slot GEMMs take TF32 operands
+                self.precision = L.PREC_TF32 if self.precision == L.PREC_F16 else L.PREC_3XTF32
+                self.set_bank(*self._bank)
             kp = (self.n_bins + 31) // 32 * 32
             wp = torch.zeros(self.n_mels, kp, dtype=torch.float32, device=self.device)
             wp[:, : self.n_bins] = w.to(self.device, torch.float32)
@@ -321,8 +332,8 @@ class CqtLongEngine:
     def __init__(self, kernels, hop: int, pad_mode: str = "reflect", precision: str = "tf32", device="cuda",
                  dense: bool = False, method: str = "hybrid"):
         self.device = _require_cuda(device)
-        if precision not in L.PRECISIONS:
-            raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
+        if precision not in ("tf32", "fp32", "3xtf32"):
+            raise ValueError("CQT1992v2 precision must be 'tf32' or 'fp32' (3xTF32)")
         self.precision = L.PRECISIONS[precision]
         k = np.asarray(kernels)
         self.n_bins, self.width = int(k.shape[0]), int(k.shape[1])
@@ -510,9 +521,13 @@ class Cqt2010Engine:
                  kernel_hop: int, first_bin: int, bins_per_octave: int, n_bins: int, pad_mode: str = "reflect",
                  device="cuda", precision: str = "tf32"):
         self.device = _require_cuda(device)
-        if precision not in L.PRECISIONS:
-            raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
-        self.precision = L.PRECISIONS[precision]
+        # the <= 1e-3 mode is the fused tensor-core chain with FP16 operands under an exact
+        # per-clip power-of-two scale ("f16"; "tf32" names the same mode for API symmetry
+        # with the other transforms); "fp32" is the FP32 CUDA-core chain (<= 1e-5)
+        modes = {"f16": L.PREC_TF32, "tf32": L.PREC_TF32, "fp32": L.PREC_3XTF32, "3xtf32": L.PREC_3XTF32}
+        if precision not in modes:
+            raise ValueError(f"CQT2010v2 precision must be one of {sorted(modes)}")
+        self.precision = modes[precision]
         self.taps = np.ascontiguousarray(np.asarray(taps, dtype=np.float32))
         k = np.asarray(top_kernels)
         self.k_re = torch.from_numpy(np.ascontiguousarray(k.real, dtype=np.float32)).to(self.device)

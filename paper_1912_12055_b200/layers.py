@@ -40,6 +40,12 @@ def _fmt(output_format: str) -> str:
     return _FORMATS[k]
 
 
+def _train_prec(precision: str) -> str:
+    """The autograd path's GEMMs take TF32 operands: FP16 inference modes train in
+    the TF32 mode of the same accuracy."""
+    return {"f16": "tf32", "3xf16": "fp32"}.get(precision, precision)
+
+
 def _bank_key(*ps):
     return tuple((p.data_ptr(), p._version) for p in ps)
 
@@ -70,7 +76,8 @@ class STFT(nn.Module):
         self.h_re = nn.Parameter(torch.tensor(h_re, dtype=torch.float32, device=self.device), requires_grad=trainable)
         self.h_im = nn.Parameter(torch.tensor(h_im, dtype=torch.float32, device=self.device), requires_grad=trainable)
         self._infer = DftEngine(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
-        self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
+        self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=_train_prec(precision),
+                              device=self.device)
         self._op._bank_version = None
         self._infer_key = _bank_key(self.h_re, self.h_im)
 
@@ -118,7 +125,8 @@ class MelSpectrogram(nn.Module):
                                  requires_grad=trainable_STFT)
         self._infer = DftEngine(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
         self._infer.set_mel(w, power=self.power)
-        self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
+        self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=_train_prec(precision),
+                              device=self.device)
         self._op._bank_version = None
         self._infer_key = _bank_key(self.h_re, self.h_im, self.mel_basis)
 
@@ -165,7 +173,7 @@ class CQT1992v2(nn.Module):
         if self.trainable or x.requires_grad:
             if self._op is None:  # dense DFT-layout op over the CQT rows (trainable rows lose their support)
                 self._op = DftLayerOp(self.k_re.detach(), self.k_im.detach(), self.cfg.hop_length, True,
-                                      self.cfg.pad_mode, precision=self._precision, device=self.device)
+                                      self.cfg.pad_mode, precision=_train_prec(self._precision), device=self.device)
                 self._op._bank_version = None
             if _fmt(output_format or self.output_format) != "magnitude":
                 raise NotImplementedError("trainable CQT1992v2 returns the smoothed magnitude (gradients.py:61-67)")

@@ -28,8 +28,8 @@ SR = 44100.0
 B_FULL = 1770
 PLANT = (0, 884, 1769)  # golden clip 0, 1, 0
 SAMPLE = (1, 300, 883, 885, 1500, 1768)  # random clips checked against the oracle
-TOL = {"tf32": 1e-3, "fp32": 1e-5}
-TOL_POWER = {"tf32": 2e-3, "fp32": 2e-5}
+TOL = {"tf32": 1e-3, "f16": 1e-3, "fp32": 1e-5, "3xtf32": 1e-5}
+TOL_POWER = {k: 2 * v for k, v in TOL.items()}
 
 
 @pytest.fixture(scope="module")
@@ -68,7 +68,7 @@ def _check(got, ref_golden_key, golden, batch, oracle_fn, tol, chunk_got=None, c
             assert worst <= chunk_tol, worst
 
 
-@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("precision", ["tf32", "f16", "fp32", "3xtf32"])
 @pytest.mark.parametrize("kind,power", [("magnitude", 1.0), ("mel", 1.0), ("mel", 2.0)])
 def test_stft_mel_full_batch(golden, batch, xdev, precision, kind, power):
     from paper_1912_12055_b200.engine import DftEngine

@@ -226,7 +226,7 @@ def test_c_abi_layer_vjp_matches_python_path(cuda_dev, precision, mel):
     from paper_1912_12055_b200.engine import DftEngine
     lib = L.load()
     h_re, h_im = O.stft_bank(64, 8000.0)
-    eng = DftEngine(h_re, h_im, 16, precision=precision, device="cuda", allow_fold=False)
+    eng = DftEngine(h_re, h_im, 16, precision=precision, device="cuda", allow_fold=False, f16_ok=False)
     rng = np.random.default_rng(21)
     xs = (rng.standard_normal((3, 700)) * 0.5).astype(np.float32)
     x = torch.from_numpy(xs).to(cuda_dev)
