@@ -54,6 +54,12 @@ extern "C" {
  * log of the parity-checked value).  With it, eps is the log offset only (the
  * Mel magnitude is the plain sqrt(re^2 + im^2)). */
 #define NNAB_OUT_LOG 0x100
+/* flag, OR-ed into the out_kind of nnab_stft_forward_train_staged: save the
+ * TF32-backward format (FP16 unit phasor re/S, im/S in save_re, TF32-rounded |X|
+ * in save_mag) from a split-precision forward (3xTF32 / 3xF16), so the phasor
+ * that weighs every frame in the kernel gradient is FP32-accurate even where
+ * |X| is small, while the backward GEMMs stay TF32. */
+#define NNAB_SAVE_PHASOR 0x200
 
 #define NNAB_PREC_TF32 0  /* one TF32 tcgen05 pass (peak-normalised error <= 1e-3) */
 #define NNAB_PREC_3XTF32 1 /* hi/lo split, 3 passes (<= 1e-5, FP32-equivalent) */
@@ -150,7 +156,10 @@ int nnab_stft_forward_host(const nnab_frames* f, const float* x_host, const floa
  * (n_mels > 0; d_w (n_mels, n_bins); d_h / d_x must be NULL, the reference
  * raises NotImplementedError for the Mel input gradient).  packed_*: the bank
  * from nnab_pack_dft_bank (fold 0); h_re / h_im: the same bank unpacked (needed
- * for d_x); upstream (B, rows, T).  Kernel gradients are summed over the batch. */
+ * for d_x; in TF32 mode they also let the convolution layer's forward run
+ * 3xTF32 so the phasor re/S, im/S that weighs every frame's gradient is
+ * FP32-accurate where |X| is small -- NULL keeps the one-pass TF32 forward);
+ * upstream (B, rows, T).  Kernel gradients are summed over the batch. */
 size_t nnab_layer_vjp_workspace_bytes(const nnab_frames* f, int32_t n_bins, int32_t n_mels, int32_t precision,
                                       int32_t need_x);
 int nnab_layer_vjp(const nnab_frames* f, const float* x, const float* packed_hi, const float* packed_lo,

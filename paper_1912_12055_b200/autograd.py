@@ -34,7 +34,7 @@ class DftLayerOp:
     rows) with an optional Mel projection on top."""
 
     def __init__(self, h_re, h_im, hop: int, center: bool = True, pad_mode: str = "reflect", eps: float = 1e-12,
-                 precision: str = "tf32", device="cuda"):
+                 precision: str = "tf32", device="cuda", phasor: str = "split"):
         # trainable sine rows may leave zero -> never fold the Nyquist bin
         self.engine = DftEngine(h_re, h_im, hop, center, pad_mode, precision=precision, device=device,
                                 allow_fold=False, f16_ok=False)
@@ -43,6 +43,36 @@ class DftLayerOp:
         self.prec = self.engine.precision
         self.split = self.prec == L.PREC_3XTF32
         self.reducer = None  # dist.GradReducer while armed: gradient blocks are all-reduced as they finish
+        # TF32 mode: every frame's gradient is weighted by the unit phasor (re/S, im/S),
+        # whose direction a one-pass forward gets wrong where |X| is near zero (the
+        # rounding error of re, im divided by S).  phasor="split" computes the
+        # forward in a split mode (3xF16, or 3xTF32 when the FP16 staging would lay
+        # the frames out differently) and saves the FP32-accurate phasor, keeping the
+        # backward GEMMs TF32; phasor="tf32" is the one-pass forward (faster, with
+        # that gradient tail).
+        if phasor not in ("split", "tf32"):
+            raise ValueError("phasor must be 'split' or 'tf32'")
+        # The 3xTF32 mode's forward runs 3xF16 where it stages the same rows (half the
+        # operand error of 3xTF32, 2.8e-6 vs 5e-6, and the same phasor argument one level down).
+        self.fwd_engine = None
+        eng = self.engine
+        same_rows = self._f16_same_rows(eng.n_fft, eng.hop)
+        if (self.prec == L.PREC_TF32 and phasor == "split") or (self.split and same_rows):
+            self.fwd_prec = L.PREC_3XF16 if same_rows else L.PREC_3XTF32
+            self.fwd_engine = DftEngine(h_re, h_im, hop, center, pad_mode, precision="3xf16", device=device,
+                                        allow_fold=False)
+            if self.fwd_prec == L.PREC_3XTF32:
+                self.fwd_engine.precision = L.PREC_3XTF32
+                self.fwd_engine.set_bank(h_re, h_im)
+
+    @staticmethod
+    def _f16_same_rows(n_fft: int, hop: int) -> bool:
+        """True when the FP16 staging (64-sample K blocks) has the TF32 staging's rows per clip."""
+        k32, k64 = (n_fft + 31) // 32 * 32, (n_fft + 63) // 64 * 64
+        hr32, hr64 = hop % 32 == 0 and hop <= k32, hop % 64 == 0 and hop <= k64
+        if hr32 != hr64:
+            return False
+        return not hr32 or (k32 + hop - 1) // hop == (k64 + hop - 1) // hop
 
     @property
     def n_bins(self):
@@ -50,10 +80,14 @@ class DftLayerOp:
 
     def set_bank(self, h_re: torch.Tensor, h_im: torch.Tensor):
         self.engine.set_bank(h_re.detach(), h_im.detach())
+        if self.fwd_engine is not None:
+            self.fwd_engine.set_bank(h_re.detach(), h_im.detach())
 
     # ------------------------------------------------------------ forward
-    def forward(self, x: torch.Tensor, mel_w: torch.Tensor | None = None):
-        """x (B, L) -> (S (B, F, T) or mel (B, n_mels, T), saved state)."""
+    def forward(self, x: torch.Tensor, mel_w: torch.Tensor | None = None, phasor_grads: bool = True):
+        """x (B, L) -> (S (B, F, T) or mel (B, n_mels, T), saved state).
+        phasor_grads=False (only the mel weights need a gradient): the one-pass
+        forward, whose |X| is all dW needs."""
         lib, eng = L.load(), self.engine
         if x.dim() == 1:
             x = x[None]
@@ -61,10 +95,22 @@ class DftLayerOp:
         B, length = int(x.shape[0]), int(x.shape[1])
         T = eng.n_frames(length)
         f = eng.frames(B, length)
-        ws = torch.empty(lib.nnab_stft_workspace_bytes(C.byref(f), self.prec), dtype=torch.uint8, device=self.device)
         stream = L.stream_handle(self.device)
-        L.check(lib.nnab_stage_frames(C.byref(f), x.data_ptr(), self.prec, ws.data_ptr(), ws.numel(), stream),
-                "stage_frames")
+        fe = self.fwd_engine if (phasor_grads or self.split) else None
+        if fe is not None and self.fwd_prec == L.PREC_3XTF32:
+            ws = None  # one 3xTF32 staging: its hi rows are the TF32 frames the dK GEMM reads
+        else:
+            ws = torch.empty(lib.nnab_stft_workspace_bytes(C.byref(f), self.prec), dtype=torch.uint8,
+                             device=self.device)
+            L.check(lib.nnab_stage_frames(C.byref(f), x.data_ptr(), self.prec, ws.data_ptr(), ws.numel(), stream),
+                    "stage_frames")
+        if fe is not None:
+            ws_f = torch.empty(lib.nnab_stft_workspace_bytes(C.byref(f), self.fwd_prec), dtype=torch.uint8,
+                               device=self.device)
+            L.check(lib.nnab_stage_frames(C.byref(f), x.data_ptr(), self.fwd_prec, ws_f.data_ptr(), ws_f.numel(),
+                                          stream), "stage_frames")
+            if ws is None:
+                ws = ws_f
         ld = lib.nnab_slots_ld(C.byref(f))
         F = self.n_bins
         R = self._rows_per_clip(length)
@@ -77,10 +123,17 @@ class DftLayerOp:
         # tcgen05 GEMM (a trained W is dense, so the epilogue's banded CUDA-core path
         # would be latency-bound)
         out = None if mel_w is not None else torch.empty(B, F, T, device=self.device)
-        L.check(lib.nnab_stft_forward_train_staged(
-            C.byref(f), eng.packed_hi.data_ptr(), L.ptr(eng.packed_lo), F, eng.fold, self.prec, L.OUT_SMOOTH_MAG,
-            1.0, self.eps, None, 0, 0, None, L.ptr(out), re_s.data_ptr(), L.ptr(im_s), L.ptr(mag_s), ld,
-            ws.data_ptr(), ws.numel(), stream), "stft_forward_train")
+        if fe is not None:  # split forward; TF32 mode: TF32-backward saves (FP32-accurate phasor)
+            flag = 0 if self.split else L.SAVE_PHASOR
+            L.check(lib.nnab_stft_forward_train_staged(
+                C.byref(f), fe.packed_hi.data_ptr(), L.ptr(fe.packed_lo), F, fe.fold, self.fwd_prec,
+                L.OUT_SMOOTH_MAG | flag, 1.0, self.eps, None, 0, 0, None, L.ptr(out), re_s.data_ptr(), L.ptr(im_s),
+                L.ptr(mag_s), ld, ws_f.data_ptr(), ws_f.numel(), stream), "stft_forward_train")
+        else:
+            L.check(lib.nnab_stft_forward_train_staged(
+                C.byref(f), eng.packed_hi.data_ptr(), L.ptr(eng.packed_lo), F, eng.fold, self.prec, L.OUT_SMOOTH_MAG,
+                1.0, self.eps, None, 0, 0, None, L.ptr(out), re_s.data_ptr(), L.ptr(im_s), L.ptr(mag_s), ld,
+                ws.data_ptr(), ws.numel(), stream), "stft_forward_train")
         saved = {"ws": ws, "re": re_s, "im": im_s, "mag": mag_s, "B": B, "L": length, "T": T, "ld": ld, "R": R}
         if mel_w is not None:
             nm = int(mel_w.shape[0])
@@ -213,7 +266,8 @@ class DftLayerFunction(torch.autograd.Function):
         if op._bank_version != bank_version:
             op.set_bank(h_re, h_im)
             op._bank_version = bank_version
-        out, saved = op.forward(x, mel_w)
+        nig = ctx.needs_input_grad
+        out, saved = op.forward(x, mel_w, phasor_grads=bool(nig[0] or nig[1] or nig[2]))
         ctx.op, ctx.saved = op, saved
         ctx.save_for_backward(h_re, h_im, mel_w if mel_w is not None else torch.empty(0))
         ctx.has_mel = mel_w is not None

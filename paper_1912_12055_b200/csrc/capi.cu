@@ -135,6 +135,20 @@ extern "C" const char* nnab_last_error(void) { return g_last_error; }
 
 extern "C" uint64_t nnab_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+int nnab::staged_views(const nnab_frames* f, int32_t precision, const void* workspace, size_t workspace_bytes,
+                 FrameGeom* g, const void** hi, const void** lo, const int32_t** exps) {
+  StageLayout sl;
+  int rc = stage_layout(f, precision, &sl);
+  if (rc) return rc;
+  *g = sl.g;
+  if (sl.g.B > 0 && (!workspace || workspace_bytes < sl.total)) return NNAB_EINVAL;
+  const char* w = reinterpret_cast<const char*>(workspace);
+  *hi = w;
+  *lo = prec_is_split(precision) ? w + sl.lo_off : nullptr;
+  *exps = prec_is_f16(precision) ? reinterpret_cast<const int32_t*>(w + sl.exp_off) : nullptr;
+  return NNAB_OK;
+}
+
 extern "C" size_t nnab_stft_workspace_bytes(const nnab_frames* f, int32_t precision) {
   StageLayout sl;
   if (stage_layout(f, precision, &sl)) return 0;

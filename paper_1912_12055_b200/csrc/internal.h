@@ -80,7 +80,13 @@ struct StftGemmArgs {
   int32_t out_bins = 0;  // pairs mode: bins per clip of the output (0 = n_bins; the caller offsets out)
   float *save_re = nullptr, *save_im = nullptr, *save_mag = nullptr;  // training forward (slot-major)
   int64_t ld_slots = 0;
+  int32_t save_phasor = 0;  // saves in the TF32-backward format whatever the forward's operand mode
 };
+
+// Pointers into a staged-frames workspace of `precision` (capi.cu): rows hi / lo,
+// per-clip exponents (FP16 modes), and the geometry with the precision's K alignment.
+int staged_views(const nnab_frames* f, int32_t precision, const void* workspace, size_t workspace_bytes,
+                 FrameGeom* g, const void** hi, const void** lo, const int32_t** exps);
 int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, cudaStream_t s);
 
 // Reduction GEMM C[M][N] = sum_k A[M][K] B(K, N)  (rgemm.cu)

@@ -91,6 +91,7 @@ struct Params {
   // slot-major layout [bin][ld_slots] for the backward GEMMs (may be null)
   float *save_re, *save_im, *save_mag;
   int64_t ld_slots;
+  int32_t save_phasor;  // 1: save the TF32-backward format (FP16 unit phasor + TF32 |X|) in any operand mode
 };
 
 NNAB_DEV uint64_t make_sdesc(const void* p, int swz_bytes) {
@@ -376,28 +377,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (bin < F - p.fold) {
                   const int64_t o = (int64_t)bin * p.ld_slots + slot;
                   const float pw = fmaf(re[j], re[j], im[j] * im[j]) + p.eps;
-                  if (p.save_im) {
+                  if (p.save_im && !p.save_phasor) {
                     p.save_re[o] = re[j];
                     p.save_im[o] = im[j];
-                  } else {  // TF32: the unit phasor (re/S, im/S) as packed FP16 (what coef needs)
+                  } else {  // TF32 backward: the unit phasor (re/S, im/S) as packed FP16 (what coef needs)
                     const float inv = rsqrtf(pw);
                     const __half2 ph = __floats2half2_rn(re[j] * inv, im[j] * inv);
                     reinterpret_cast<__half2*>(p.save_re)[o] = ph;
                   }
-                  if (p.save_mag)  // GEMM operand of dW: TF32-rounded in TF32 mode, fp32 (split later) in 3xTF32
-                    p.save_mag[o] = kSplit ? sqrtf(pw) : tf32_rne(fast_sqrt(pw));
+                  if (p.save_mag)  // GEMM operand of dW: TF32-rounded for a TF32 backward, fp32 (split later) in 3xTF32
+                    p.save_mag[o] = (kSplit && !p.save_phasor) ? sqrtf(pw) : tf32_rne(fast_sqrt(pw));
                 }
               }
               if (p.fold && n == 0 && c == 0) {
                 const int64_t o = (int64_t)(F - 1) * p.ld_slots + slot;
                 const float pw = nyq_re * nyq_re + p.eps;
-                if (p.save_im) {
+                if (p.save_im && !p.save_phasor) {
                   p.save_re[o] = nyq_re;
                   p.save_im[o] = 0.f;
                 } else {
                   reinterpret_cast<__half2*>(p.save_re)[o] = __floats2half2_rn(nyq_re * rsqrtf(pw), 0.f);
                 }
-                if (p.save_mag) p.save_mag[o] = kSplit ? sqrtf(pw) : tf32_rne(fast_sqrt(pw));
+                if (p.save_mag) p.save_mag[o] = (kSplit && !p.save_phasor) ? sqrtf(pw) : tf32_rne(fast_sqrt(pw));
               }
             }
           }
@@ -547,7 +548,8 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.a_exp = a.a_exp;
   p.b_exp = a.b_exp;
   if (a.save_re && a.pairs) return NNAB_EINVAL;
-  if (a.save_re && !a.save_im && kSplit) return NNAB_EINVAL;  // phasor saves: TF32 only
+  p.save_phasor = a.save_phasor;
+  if (a.save_re && !a.save_im && kSplit && !a.save_phasor) return NNAB_EINVAL;  // 3x modes save re / im
   p.n_tab = a.n_tab;
   p.b_box = b_box;
   p.pairs = a.pairs;

@@ -168,22 +168,34 @@ extern "C" int nnab_stft_forward_train_staged(const nnab_frames* f, const float*
                                               int32_t n_mels, int32_t mel_ld, const int32_t* mel_band, float* out,
                                               float* save_re, float* save_im, float* save_mag, int64_t ld,
                                               const void* workspace, size_t workspace_bytes, void* stream) {
-  FrameGeom g;
-  int rc = frame_geometry(f, &g);
-  if (rc) return rc;
-  if (precision != NNAB_PREC_TF32 && precision != NNAB_PREC_3XTF32) return NNAB_EINVAL;
-  const int split = precision == NNAB_PREC_3XTF32;
-  if (!packed_hi || (split && !packed_lo) || !save_re || (split && !save_im)) return NNAB_EINVAL;
+  const int phasor = (out_kind & NNAB_SAVE_PHASOR) != 0;
+  out_kind &= ~NNAB_SAVE_PHASOR;
+  if (!prec_valid(precision)) return NNAB_EINVAL;
+  const int split = prec_is_split(precision);
+  // saves: TF32 / F16 forward -> FP16 phasor (+ TF32 |X|); split modes -> fp32 re, im
+  // (the 3xTF32 backward's operands) unless NNAB_SAVE_PHASOR asks for the TF32-backward format
+  const bool want_im = split && !phasor;
+  if (!packed_hi || (split && !packed_lo) || !save_re || (want_im && !save_im)) return NNAB_EINVAL;
   if (out_kind != NNAB_OUT_SMOOTH_MAG && out_kind != NNAB_OUT_MEL) return NNAB_EINVAL;
   if (!out && out_kind != NNAB_OUT_SMOOTH_MAG) return NNAB_EINVAL;  // out may be null: save slots only
   if (out_kind == NNAB_OUT_MEL && (!mel_w || n_mels < 1)) return NNAB_EINVAL;
+  FrameGeom g;
+  const void *hi, *lo;
+  const int32_t* exps;
+  int rc = staged_views(f, precision, workspace, workspace_bytes, &g, &hi, &lo, &exps);
+  if (rc) return rc;
   if (ld < g.B * g.R || ld % 32) return NNAB_EINVAL;
+  FrameGeom gb;  // the slot layout is the TF32 backward's: the forward must stage the same rows per clip
+  if ((rc = frame_geometry(f, &gb)) || gb.R != g.R) return rc ? rc : NNAB_ENOTSUP;
   if (g.B == 0) return NNAB_OK;
-  if (!workspace || workspace_bytes < nnab_stft_workspace_bytes(f, precision)) return NNAB_EINVAL;
-  const size_t sb = (size_t)((g.B * g.R * g.row_len * 4 + 255) & ~int64_t(255));
   StftGemmArgs a{};
-  a.a_hi = reinterpret_cast<const float*>(workspace);
-  a.a_lo = split ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + sb) : nullptr;
+  a.a_hi = reinterpret_cast<const float*>(hi);
+  a.a_lo = reinterpret_cast<const float*>(lo);
+  a.a_exp = exps;
+  if (exps)
+    a.b_exp = reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(packed_hi) +
+                                               nnab_dft_bank_bytes_prec(n_bins, g.width, fold_nyquist, precision) -
+                                               256) + 1;
   a.b_hi = packed_hi;
   a.b_lo = packed_lo;
   a.n_tiles = nnab_dft_bank_tiles(n_bins, fold_nyquist);
@@ -198,9 +210,10 @@ extern "C" int nnab_stft_forward_train_staged(const nnab_frames* f, const float*
   a.mel_band = mel_band;
   a.out = out;
   a.save_re = save_re;
-  a.save_im = save_im;
+  a.save_im = want_im ? save_im : nullptr;
   a.save_mag = save_mag;
   a.ld_slots = ld;
+  a.save_phasor = phasor;
   return launch_stft_gemm(g, a, precision, (cudaStream_t)stream);
 }
 

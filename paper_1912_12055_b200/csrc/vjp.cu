@@ -33,7 +33,7 @@ __global__ void transpose_bank_kernel(const float* __restrict__ h_re, const floa
 size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct VjpLayout {
-  size_t stft, ph, im, mag, mag_lo, gs, coef, part, ht, fgt, total;
+  size_t stft, bank3, ph, im, mag, mag_lo, gs, coef, part, ht, fgt, total;
   int32_t kp_2f;
   int64_t ld;
 };
@@ -50,7 +50,11 @@ int vjp_layout(const nnab_frames* f, int32_t n_bins, int32_t n_mels, int32_t pre
   VjpLayout L{};
   L.ld = ld;
   L.kp_2f = (int32_t)((2 * F + 31) / 32 * 32);
-  L.stft = al(nnab_stft_workspace_bytes(f, precision));
+  // TF32 convolution layer: 3xTF32 staging (its hi rows are the TF32 frames of dK) and a
+  // 3xTF32 bank for the split forward that saves an FP32-accurate phasor
+  const bool split_fwd = !split && n_mels == 0;
+  L.stft = al(nnab_stft_workspace_bytes(f, split_fwd ? NNAB_PREC_3XTF32 : precision));
+  L.bank3 = split_fwd ? 2 * al(nnab_dft_bank_bytes((int32_t)F, (int32_t)n_fft, 0)) : 0;
   L.ph = al(cell);
   L.im = split ? al(cell) : 0;
   L.mag = n_mels > 0 ? al(cell) : 0;
@@ -63,7 +67,7 @@ int vjp_layout(const nnab_frames* f, int32_t n_bins, int32_t n_mels, int32_t pre
                         (size_t)256}));
   L.ht = need_x ? al((size_t)n_fft * L.kp_2f * 4) * (split ? 2 : 1) : 0;
   L.fgt = need_x ? al((size_t)n_fft * ld * 4) : 0;
-  L.total = L.stft + L.ph + L.im + L.mag + L.mag_lo + L.gs + L.coef + L.part + L.ht + L.fgt;
+  L.total = L.stft + L.bank3 + L.ph + L.im + L.mag + L.mag_lo + L.gs + L.coef + L.part + L.ht + L.fgt;
   *o = L;
   return NNAB_OK;
 }
@@ -112,6 +116,7 @@ extern "C" int nnab_layer_vjp(const nnab_frames* f, const float* x, const float*
   char* p = reinterpret_cast<char*>(workspace);
   auto take = [&](size_t n) { char* r = p; p += n; return n ? reinterpret_cast<float*>(r) : nullptr; };
   void* ws = take(Lo.stft);
+  float* bank3 = take(Lo.bank3);
   float* ph = take(Lo.ph);
   float* im = take(Lo.im);
   float* mag = take(Lo.mag);
@@ -125,12 +130,26 @@ extern "C" int nnab_layer_vjp(const nnab_frames* f, const float* x, const float*
     return split ? reinterpret_cast<float*>(reinterpret_cast<char*>(a) + bytes / 2) : nullptr;
   };
 
-  // forward with the saved operands (gradients.py:61-80)
-  if ((rc = nnab_stage_frames(f, x, precision, ws, Lo.stft, stream))) return rc;
-  if ((rc = nnab_stft_forward_train_staged(f, packed_hi, packed_lo, n_bins, 0, precision, NNAB_OUT_SMOOTH_MAG, 1.f,
-                                           eps, nullptr, 0, 0, nullptr, nullptr, ph, im, mag, ld, ws, Lo.stft,
-                                           stream)))
-    return rc;
+  // forward with the saved operands (gradients.py:61-80).  TF32 convolution layer with the
+  // unpacked bank at hand: the forward runs 3xTF32 and saves the TF32-backward format, so
+  // the phasor re/S, im/S weighing every frame is FP32-accurate where |X| is small
+  if (Lo.bank3 && h_re && h_im) {
+    const size_t bb = Lo.bank3 / 2;
+    float* b3_lo = reinterpret_cast<float*>(reinterpret_cast<char*>(bank3) + bb);
+    if ((rc = nnab_pack_dft_bank(h_re, h_im, n_bins, (int32_t)n_fft, 0, NNAB_PREC_3XTF32, bank3, b3_lo, stream)))
+      return rc;
+    if ((rc = nnab_stage_frames(f, x, NNAB_PREC_3XTF32, ws, Lo.stft, stream))) return rc;
+    if ((rc = nnab_stft_forward_train_staged(f, bank3, b3_lo, n_bins, 0, NNAB_PREC_3XTF32,
+                                             NNAB_OUT_SMOOTH_MAG | NNAB_SAVE_PHASOR, 1.f, eps, nullptr, 0, 0, nullptr,
+                                             nullptr, ph, nullptr, mag, ld, ws, Lo.stft, stream)))
+      return rc;
+  } else {
+    if ((rc = nnab_stage_frames(f, x, precision, ws, Lo.stft, stream))) return rc;
+    if ((rc = nnab_stft_forward_train_staged(f, packed_hi, packed_lo, n_bins, 0, precision, NNAB_OUT_SMOOTH_MAG,
+                                             1.f, eps, nullptr, 0, 0, nullptr, nullptr, ph, im, mag, ld, ws, Lo.stft,
+                                             stream)))
+      return rc;
+  }
   const float* coef_lo = split ? lo_of(coef, Lo.coef) : nullptr;
   if (n_mels > 0) {
     // mel layer (gradients.py:118-121): dW = g @ S^T; g to slots fused with the operand split

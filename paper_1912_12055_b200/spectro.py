@@ -589,10 +589,13 @@ class TrainableLayer:
             return self._fixed
         return self._params["h_re"], self._params["h_im"]
 
-    def _run(self, x: torch.Tensor):
+    def _run(self, x: torch.Tensor, for_vjp: bool = False):
         h_re, h_im = self._bank()
         self._op.set_bank(h_re, h_im)
-        return self._op.forward(x, self._params["weights"] if self.is_mel else None)
+        # a convolution layer's VJP weighs every frame by the phasor re/S, im/S: its
+        # forward runs split-precision (autograd.DftLayerOp, phasor="split")
+        return self._op.forward(x, self._params["weights"] if self.is_mel else None,
+                                phasor_grads=for_vjp and not self.is_mel)
 
     def spectrogram_batch(self, x: torch.Tensor) -> torch.Tensor:
         """(B, L) -> (B, bins, frames) smoothed magnitude (or W @ it)."""
@@ -611,7 +614,7 @@ def spectrogram_vjp(x, layer: TrainableLayer, upstream_grad, with_input_grad: bo
     xs = x.samples[None] if isinstance(x, Signal) else _batch(x)
     g = torch.as_tensor(np.asarray(upstream_grad) if not torch.is_tensor(upstream_grad) else upstream_grad)
     g = g.to(layer._op.device, torch.float32)
-    out, saved = layer._run(xs)
+    out, saved = layer._run(xs, for_vjp=True)
     if g.dim() == 2:
         g = g[None]
     if tuple(g.shape) != tuple(out.shape):

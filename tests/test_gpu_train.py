@@ -1,7 +1,10 @@
 """GPU parity of the trainable layers (gradients.py:28-149): smoothed-magnitude
 forward, kernel / mel-weight / input gradients vs the reference's golden
-vectors and the float64 oracle.  Gradients are reductions over frames, so the
-same peak-normalised tolerances apply: <= 1e-3 in TF32, <= 1e-5 in 3xTF32."""
+vectors and the float64 oracle, peak-normalised.  Forward gates: <= 1e-3 in
+TF32, <= 1e-5 in 3xTF32.  Gradient gates: <= 2e-3 in TF32 (the backward GEMMs
+round coef and the frames to TF32; the forward that saves the phasor re/S, im/S
+runs split-precision, autograd.DftLayerOp phasor="split") and <= 1e-5 in
+3xTF32."""
 
 import numpy as np
 import pytest
@@ -11,10 +14,15 @@ from oracle import spectro_oracle as O
 
 pytestmark = pytest.mark.gpu
 TOL = {"tf32": 1e-3, "fp32": 1e-5}
-# Kernel gradients go through coef = g*re/S: where |X| is small the direction
-# re/S inherits the forward error divided by S, so gradient tolerances are
-# looser than the forward ones.
-TOL_GRAD = {"tf32": 3e-2, "fp32": 5e-4}
+TOL_GRAD = {"tf32": 2e-3, "fp32": 1e-5}
+# Config 5 at production-like sizes: each bank row's gradient sums g * (re/S, im/S) over
+# every frame of the batch, and the direction re/S of a near-zero |X| is ill-conditioned:
+# an operand rounding of 2^-22 (the split modes' hi + lo) moves it by 2^-22 |X|_rms / S.
+# Over 72 x 157 frames x 1,025 bins a few |X| < 1e-3 |X|_rms occur, and the worst bank row
+# lands at 6e-5 in FP32 mode (tools/dbg_grad_fp32.py: 1.1e-4 with a 3xTF32 forward, 6.3e-5
+# with the 3xF16 one the layer uses); the TF32 mode's split-precision phasor keeps it
+# under its 2e-3 gate.
+TOL_GRAD_JOINT = {"tf32": 2e-3, "fp32": 1e-4}
 
 
 def layer_for(bank, hop, precision, **kw):
@@ -80,12 +88,15 @@ def test_zero_upstream_and_shape_mismatch(cuda_dev):
 
 
 @pytest.mark.parametrize("precision", ["tf32", "fp32"])
-def test_joint_mel_stft_batch_vs_oracle(cuda_dev, precision):
-    """Config 5 (trainable STFT + Mel) on 6 full-length clips: dW, dh_re, dh_im
-    summed over the batch vs the float64 composition of the reference pieces."""
+@pytest.mark.parametrize("B", [6, 72])
+def test_joint_mel_stft_batch_vs_oracle(cuda_dev, precision, B):
+    """Config 5 (trainable STFT + Mel) on full-length clips: dW, dh_re, dh_im
+    summed over the batch vs the float64 composition of the reference pieces.
+    B = 72 makes the frame-slot reduction K = 72 x 160 = 11,520 -- past the
+    8,192-slot TMEM drain chunk of the wide-pair dK GEMM and the 2,048 / 1,024
+    chunks of the other reductions, so the multi-chunk drains run."""
     from paper_1912_12055_b200.layers import MelSpectrogram
     rng = np.random.default_rng(5)
-    B = 6
     x = (rng.standard_normal((B, 80000)) * 0.5).astype(np.float32)
     m = MelSpectrogram(sr=44100, trainable_mel=True, trainable_STFT=True, precision=precision)
     xt = torch.from_numpy(x).to(cuda_dev)
@@ -107,7 +118,7 @@ def test_joint_mel_stft_batch_vs_oracle(cuda_dev, precision):
         dh_re += (dS * re / S) @ fr
         dh_im += (dS * im / S) @ fr
     assert O.peak_err(out.detach().cpu().numpy(), np.stack(fwd)) <= TOL[precision]
-    tol = TOL_GRAD[precision]
+    tol = TOL_GRAD_JOINT[precision]
     assert O.peak_err(m.mel_basis.grad.cpu().numpy(), dW) <= tol
     assert O.peak_err(m.h_re.grad.cpu().numpy(), dh_re) <= tol
     assert O.peak_err(m.h_im.grad.cpu().numpy(), dh_im) <= tol
@@ -123,22 +134,31 @@ def test_trainable_stft_module_step_changes_bank(cuda_dev):
     opt.step()
     b = m(x).sum()  # repacked bank after the in-place update
     assert float(a.detach()) != float(b.detach())
-    # input gradient through the non-trainable layer (gradients.py:133-149).  The
-    # all-ones upstream weighs every (bin, frame) phasor re/S, im/S equally, and
-    # for bins with |X| near zero TF32 operand rounding can turn that direction
-    # around: over 40 random inputs the TF32 error has median 4.8e-4, p90 1.0e-3
-    # but a tail to 9e-2 (tools/dx_err_sweep.py), so this check runs the FP32
-    # mode (median 2e-7, max 1.6e-6) on a seeded input
-    m2 = STFT(n_fft=128, hop_length=32, sr=8000, precision="fp32")
-    gen = torch.Generator(device=cuda_dev)
-    gen.manual_seed(5)
-    xr = torch.randn(2, 1000, device=cuda_dev, generator=gen).requires_grad_(True)
-    m2(xr).sum().backward()
+
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_module_input_gradient_seed_sweep(cuda_dev, precision):
+    """Input gradient through the STFT module (gradients.py:133-149) under an
+    all-ones upstream, over 24 random inputs.  That upstream weighs every
+    (bin, frame) phasor re/S, im/S equally, so a bin with |X| near zero whose
+    direction a one-pass TF32 forward turns around would show up here (the
+    one-pass tail reached 9e-2, tools/dx_err_sweep.py); the split-precision
+    phasor forward keeps every seed under the gate."""
+    from paper_1912_12055_b200.layers import STFT
+    m2 = STFT(n_fft=128, hop_length=32, sr=8000, precision=precision)
     h_re, h_im = O.stft_bank(128, 8000.0)
-    ref = np.stack([O.conv_layer_vjp(c.astype(np.float64), h_re, h_im, 32,
-                                     np.ones((65, 1000 // 32 + 1)), with_input_grad=True)[1]
-                    for c in xr.detach().cpu().numpy()])
-    assert O.peak_err(xr.grad.cpu().numpy(), ref) <= TOL_GRAD["fp32"]
+    errs = []
+    for seed in range(24):
+        gen = torch.Generator(device=cuda_dev)
+        gen.manual_seed(seed)
+        xr = torch.randn(2, 1000, device=cuda_dev, generator=gen).requires_grad_(True)
+        m2(xr).sum().backward()
+        ref = np.stack([O.conv_layer_vjp(c.astype(np.float64), h_re, h_im, 32,
+                                         np.ones((65, 1000 // 32 + 1)), with_input_grad=True)[1]
+                        for c in xr.detach().cpu().numpy()])
+        errs.append(max(O.peak_err(g, r) for g, r in zip(xr.grad.cpu().numpy(), ref)))
+    assert max(errs) <= TOL_GRAD[precision], (precision, sorted(errs)[-3:])
 
 
 # ---- ports of the reference's remaining gradient tests (tests/test_gradients.py)
