@@ -55,12 +55,12 @@ class TrainStep:
     Mel layer, backward for the mel weights and both DFT banks, and (N > 1)
     the gradient all-reduce (bucketed, overlapped with the backward GEMMs)."""
 
-    def __init__(self, device, precision, world, nb=B_CLIPS):
+    def __init__(self, device, precision, world, nb=B_CLIPS, phasor="split"):
         import torch
         from paper_1912_12055_b200.dist import GradReducer
         from paper_1912_12055_b200.layers import MelSpectrogram
         self.m = MelSpectrogram(sr=SR, n_fft=2048, n_mels=128, hop_length=512, trainable_mel=True,
-                                trainable_STFT=True, precision=precision, device=device)
+                                trainable_STFT=True, precision=precision, device=device, grad_phasor=phasor)
         self.world = world
         self.reducer = GradReducer(list(self.m.parameters())) if world > 1 else None
         gen = torch.Generator(device=device)
@@ -181,12 +181,15 @@ MODES = {
     ("train", "f16"): ("tf32", "tf32", "tf32"),
     ("train", "tf32"): ("tf32", "tf32", "tf32"),
     ("train", "fp32"): ("fp32", "3xtf32", "tf32"),
+    # TF32 training with the one-pass forward phasor (faster; gradient tail)
+    ("train", "tf32-onepass"): ("tf32", "tf32 (one-pass phasor)", "tf32"),
 }
 for _m in ("f16", "tf32", "fp32", "3xtf32"):
     if ("stft", _m) in MODES:
         MODES[("mel", _m)] = MODES[("melpow2", _m)] = MODES[("stft", _m)]
 BREAKDOWN_MODES = {"stft": ["f16", "tf32", "fp32"], "mel": ["f16", "tf32", "fp32"], "melpow2": ["f16", "tf32", "fp32"],
-                   "cqt1992v2": ["tf32", "fp32"], "cqt2010v2": ["f16", "fp32"], "train": ["tf32", "fp32"]}
+                   "cqt1992v2": ["tf32", "fp32"], "cqt2010v2": ["f16", "fp32"],
+                   "train": ["tf32", "tf32-onepass", "fp32"]}
 
 
 def build_workload(name: str, device, mode: str, nb: int = B_CLIPS):
@@ -220,7 +223,7 @@ def build_workload(name: str, device, mode: str, nb: int = B_CLIPS):
         world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
         work = {"bound": "tensor", "per_batch": FLOP_TRAIN, "unit": "TFLOP/s",
                 "kernel": "train step (stft_gemm fwd + rgemm dW/dS/dK + glue)"}
-        return TrainStep(device, precision, world, nb), None, work, 0
+        return TrainStep(device, precision, world, nb, "tf32" if mode.endswith("onepass") else "split"), None, work, 0
     if name == "cqt2010v2":
         cfg = CqtConfig(sr=SR)
         p = cqt2010_plan(cfg)
@@ -413,7 +416,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="mel", choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default="f16", choices=["f16", "tf32", "fp32", "3xtf32"],
+    ap.add_argument("--precision", default="f16", choices=["f16", "tf32", "fp32", "3xtf32", "tf32-onepass"],
                     help="operand mode (bench.MODES): f16 = the fastest <= 1e-3 mode, fp32 = the <= 1e-5 mode")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

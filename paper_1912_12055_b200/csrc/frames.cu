@@ -159,7 +159,7 @@ NNAB_DEV int f16_scale_exp(float peak) {
 // One CTA per clip (persistent over clips): pass 1 finds the clip's peak, pass 2
 // (the clip now in L2) writes its hop rows scaled by 2^e as FP16 (split: hi =
 // RN(v), lo = RN(v - hi), 22 significant bits), and exps[b] = e.
-__global__ void __launch_bounds__(1024) stage_rows_f16_kernel(const float* __restrict__ x, int64_t B, int64_t L,
+__global__ void __launch_bounds__(512, 2) stage_rows_f16_kernel(const float* __restrict__ x, int64_t B, int64_t L,
                                                               int32_t pad, int32_t mode, int32_t hop, int32_t row_len,
                                                               int32_t R, int64_t padded_len, int split,
                                                               __half* __restrict__ hi, __half* __restrict__ lo,
@@ -210,24 +210,37 @@ __global__ void __launch_bounds__(1024) stage_rows_f16_kernel(const float* __res
     const float sc = ldexpf(1.f, e);
     uint2* hrow = reinterpret_cast<uint2*>(hi) + b * groups;
     uint2* lrow = reinterpret_cast<uint2*>(lo) + b * groups;
-    for (int64_t gq = threadIdx.x; gq < groups; gq += blockDim.x) {
-      const int64_t r = gq / q_per_row;
-      const int32_t q = (int32_t)(gq - r * q_per_row);
-      float v[4];
-      gather4(x, b, L, pad, mode, padded_len, aligned_clips, x_aligned, r * hop + 4 * q, v);
-      __half2 h01 = __floats2half2_rn(v[0] * sc, v[1] * sc), h23 = __floats2half2_rn(v[2] * sc, v[3] * sc);
-      uint2 hv;
-      hv.x = *reinterpret_cast<uint32_t*>(&h01);
-      hv.y = *reinterpret_cast<uint32_t*>(&h23);
-      hrow[gq] = hv;
-      if (split) {
-        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-        __half2 l01 = __floats2half2_rn(v[0] * sc - f01.x, v[1] * sc - f01.y);
-        __half2 l23 = __floats2half2_rn(v[2] * sc - f23.x, v[3] * sc - f23.y);
-        uint2 lv;
-        lv.x = *reinterpret_cast<uint32_t*>(&l01);
-        lv.y = *reinterpret_cast<uint32_t*>(&l23);
-        lrow[gq] = lv;
+    // pass 2 from L2: kU independent groups per thread in flight before any store
+    constexpr int kU = 4;
+    for (int64_t g0 = threadIdx.x; g0 < groups; g0 += (int64_t)kU * blockDim.x) {
+      float v[kU][4];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t gq = g0 + (int64_t)u * blockDim.x;
+        if (gq < groups) {
+          const int64_t r = gq / q_per_row;
+          const int32_t q = (int32_t)(gq - r * q_per_row);
+          gather4(x, b, L, pad, mode, padded_len, aligned_clips, x_aligned, r * hop + 4 * q, v[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t gq = g0 + (int64_t)u * blockDim.x;
+        if (gq >= groups) break;
+        __half2 h01 = __floats2half2_rn(v[u][0] * sc, v[u][1] * sc), h23 = __floats2half2_rn(v[u][2] * sc, v[u][3] * sc);
+        uint2 hv;
+        hv.x = *reinterpret_cast<uint32_t*>(&h01);
+        hv.y = *reinterpret_cast<uint32_t*>(&h23);
+        hrow[gq] = hv;
+        if (split) {
+          const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+          __half2 l01 = __floats2half2_rn(v[u][0] * sc - f01.x, v[u][1] * sc - f01.y);
+          __half2 l23 = __floats2half2_rn(v[u][2] * sc - f23.x, v[u][3] * sc - f23.y);
+          uint2 lv;
+          lv.x = *reinterpret_cast<uint32_t*>(&l01);
+          lv.y = *reinterpret_cast<uint32_t*>(&l23);
+          lrow[gq] = lv;
+        }
       }
     }
   }
@@ -246,10 +259,10 @@ int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows
 int stage_frames_f16(const FrameGeom& g, const float* x, void* rows_hi, void* rows_lo, int32_t* exps, int split,
                      cudaStream_t s) {
   if (g.B == 0) return NNAB_OK;
-  // one clip per CTA at a time, one CTA per SM: 148 clips (47 MB) in flight, so
-  // pass 2 re-reads each clip from L2
-  const int blocks = (int)std::min<int64_t>(g.B, (int64_t)num_sms());
-  stage_rows_f16_kernel<<<blocks, 1024, 0, s>>>(x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.row_len, g.R, g.padded_len,
+  // one clip per CTA at a time, two CTAs per SM (one's peak pass overlaps the
+  // other's conversion): 296 clips (95 MB) in flight, so pass 2 re-reads each clip from L2
+  const int blocks = (int)std::min<int64_t>(g.B, 2 * (int64_t)num_sms());
+  stage_rows_f16_kernel<<<blocks, 512, 0, s>>>(x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.row_len, g.R, g.padded_len,
                                                split, reinterpret_cast<__half*>(rows_hi),
                                                reinterpret_cast<__half*>(rows_lo), exps);
   NNAB_LAUNCHED();

@@ -13,6 +13,12 @@
          computed by their time-domain equivalents (spectro.Cqt1992 / Cqt2010)
 
 Input (batch, samples) or (samples,) float32 CUDA tensor; output (batch, freq, time).
+precision: "tf32" (default) / "f16" (FP16 operands under exact power-of-two scales,
+the same <= 1e-3 accuracy at twice the tensor rate; STFT / Mel inference) / "fp32"
+(<= 1e-5).  grad_phasor (trainable STFT / Mel): "split" (default) computes the
+forward that saves the phasor re/S, im/S split-precision so TF32 kernel / input
+gradients meet 2e-3; "tf32" keeps the one-pass forward (faster, gradient tail
+up to ~1e-1 where |X| is near zero).
 Numerics follow the `spectro` reference this repo is parity-checked against:
 Mel `norm=None` is its peak normalisation (spectro MelParams norm="none"); nnAudio's
 `norm=1` selects the area ("slaney") normalisation.  Trainable layers return the
@@ -63,7 +69,7 @@ def _as_batch(x: torch.Tensor) -> torch.Tensor:
 class STFT(nn.Module):
     def __init__(self, n_fft=2048, freq_bins=None, hop_length=512, window="hann", freq_scale="no", center=True,
                  pad_mode="reflect", fmin=50, fmax=6000, sr=22050, trainable=False, output_format="Magnitude",
-                 precision="tf32", device="cuda", log_eps=None):
+                 precision="tf32", device="cuda", log_eps=None, grad_phasor="split"):
         super().__init__()
         self.device = _require_cuda(device)
         self.output_format = _fmt(output_format)
@@ -77,7 +83,7 @@ class STFT(nn.Module):
         self.h_im = nn.Parameter(torch.tensor(h_im, dtype=torch.float32, device=self.device), requires_grad=trainable)
         self._infer = DftEngine(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
         self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=_train_prec(precision),
-                              device=self.device)
+                              device=self.device, phasor=grad_phasor)
         self._op._bank_version = None
         self._infer_key = _bank_key(self.h_re, self.h_im)
 
@@ -106,7 +112,7 @@ class STFT(nn.Module):
 class MelSpectrogram(nn.Module):
     def __init__(self, sr=22050, n_fft=2048, n_mels=128, hop_length=512, window="hann", center=True,
                  pad_mode="reflect", htk=False, fmin=0.0, fmax=None, norm=None, power=1.0, trainable_mel=False,
-                 trainable_STFT=False, precision="tf32", device="cuda", log_eps=None):
+                 trainable_STFT=False, precision="tf32", device="cuda", log_eps=None, grad_phasor="split"):
         super().__init__()
         self.device = _require_cuda(device)
         self.log_eps = log_eps  # log(mel + log_eps) fused into the epilogue (extension, north_star item 3)
@@ -126,7 +132,7 @@ class MelSpectrogram(nn.Module):
         self._infer = DftEngine(h_re, h_im, hop_length, center, pad_mode, precision=precision, device=self.device)
         self._infer.set_mel(w, power=self.power)
         self._op = DftLayerOp(h_re, h_im, hop_length, center, pad_mode, precision=_train_prec(precision),
-                              device=self.device)
+                              device=self.device, phasor=grad_phasor)
         self._op._bank_version = None
         self._infer_key = _bank_key(self.h_re, self.h_im, self.mel_basis)
 
