@@ -159,7 +159,7 @@ NNAB_DEV int f16_scale_exp(float peak) {
 // One CTA per clip (persistent over clips): pass 1 finds the clip's peak, pass 2
 // (the clip now in L2) writes its hop rows scaled by 2^e as FP16 (split: hi =
 // RN(v), lo = RN(v - hi), 22 significant bits), and exps[b] = e.
-__global__ void __launch_bounds__(512, 2) stage_rows_f16_kernel(const float* __restrict__ x, int64_t B, int64_t L,
+__global__ void __launch_bounds__(1024, 1) stage_rows_f16_kernel(const float* __restrict__ x, int64_t B, int64_t L,
                                                               int32_t pad, int32_t mode, int32_t hop, int32_t row_len,
                                                               int32_t R, int64_t padded_len, int split,
                                                               __half* __restrict__ hi, __half* __restrict__ lo,
@@ -259,10 +259,10 @@ int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows
 int stage_frames_f16(const FrameGeom& g, const float* x, void* rows_hi, void* rows_lo, int32_t* exps, int split,
                      cudaStream_t s) {
   if (g.B == 0) return NNAB_OK;
-  // one clip per CTA at a time, two CTAs per SM (one's peak pass overlaps the
-  // other's conversion): 296 clips (95 MB) in flight, so pass 2 re-reads each clip from L2
-  const int blocks = (int)std::min<int64_t>(g.B, 2 * (int64_t)num_sms());
-  stage_rows_f16_kernel<<<blocks, 512, 0, s>>>(x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.row_len, g.R, g.padded_len,
+  // one clip per CTA at a time, one CTA per SM: 148 clips (47 MB) in flight, so pass 2
+  // re-reads each clip from L2 (two CTAs per SM thrashed L2: 960 MB of DRAM reads, ncu)
+  const int blocks = (int)std::min<int64_t>(g.B, (int64_t)num_sms());
+  stage_rows_f16_kernel<<<blocks, 1024, 0, s>>>(x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.row_len, g.R, g.padded_len,
                                                split, reinterpret_cast<__half*>(rows_hi),
                                                reinterpret_cast<__half*>(rows_lo), exps);
   NNAB_LAUNCHED();
