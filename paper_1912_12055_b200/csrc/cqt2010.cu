@@ -17,6 +17,7 @@
 // produces consecutive outputs from registers.  The per-octave conv writes its
 // 12 complex rows straight into the final (B, n_bins, T) output.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -287,9 +288,24 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
   if (n_frames_out) *n_frames_out = T;
   if (B == 0) return NNAB_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (precision == NNAB_PREC_TF32) {  // fused tensor-core chain when the clip fits in shared memory
-    const int rc = launch_cqt2010_tc(x, B, L, taps, n_taps, k_re, k_im, n_filters, width, early_stages, n_octaves,
-                                     kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind, T, out, s);
+  if (precision == NNAB_PREC_TF32) {  // tensor-core chain (FP16 operands) when the clip fits in shared memory
+    // default: the single fused kernel (each clip's whole chain on one SM).  NNAB_CQT2010_LEVELS=1
+    // selects the batched path (per-clip front for stages 1-2, then level-synchronous HALVE
+    // launches and one CONV launch over all octaves and clips, through workspace level buffers):
+    // equal speed today (0.73 ms) -- its front is the fused kernel's stage 1-2, and its per-tile
+    // build / MMA / epilogue chain is still latency-bound
+    static const bool levels = [] {
+      const char* e = getenv("NNAB_CQT2010_LEVELS");
+      return e && e[0] == '1';
+    }();
+    int rc = NNAB_ENOTSUP;
+    if (levels && workspace)
+      rc = launch_cqt2010_levels(x, B, L, taps, n_taps, k_re, k_im, n_filters, width, early_stages, n_octaves,
+                                 kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind, T, out, workspace,
+                                 workspace_bytes, s);
+    if (rc == NNAB_ENOTSUP)
+      rc = launch_cqt2010_tc(x, B, L, taps, n_taps, k_re, k_im, n_filters, width, early_stages, n_octaves,
+                             kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind, T, out, s);
     if (rc != NNAB_ENOTSUP) return rc;
   }
   if (!workspace || workspace_bytes < nnab_cqt2010v2_workspace_bytes(B, L, early_stages)) return NNAB_EINVAL;

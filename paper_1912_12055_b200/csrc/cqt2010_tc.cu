@@ -73,6 +73,12 @@ struct TcParams {
   const float* k_re;                   // top-octave bank (n_filt, width), device
   const float* k_im;
   float* out;
+  // front-only mode (lv0 != null): after stage 2 the octave-0 signal (scaled FP16 with its
+  // ML-sample reflect margins) goes to lv0[b * lv0_stride ..] and the clip's scale
+  // exponent to lv_exp[b]; the octave levels then run as batched kernels
+  __half* lv0;
+  int32_t* lv_exp;
+  int32_t lv0_stride;
   // shared-memory carve-up (bytes from the 1 KB-aligned base)
   int32_t off_toep, off_filt, off_ring, off_x, off_xe, off_y, off_ye, off_col, off_stage, off_bars;
   int32_t pl_x, pl_y, y_rows;          // plane strides (bytes); stage-2 plane rows
@@ -515,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
         issue_fir(c, yp_s, p.pl_y, 0, 0);
         if (p.oct_blocks[0] > 128) issue_fir(c, yp_s, p.pl_y, p.oct_blocks[0] - 128, 128);
         mma_commit(&bars[0]);
+        if (p.lv0) continue;  // front-only: the octave levels run as batched kernels
         for (int a = 0; a < p.n_oct; ++a) {
           if (a + 1 < p.n_oct) {
             wait_fir();
@@ -646,6 +653,26 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
         csync();
         c.pf.mark(p, 5);
       }
+      if (p.lv0) {
+        // front-only: octave 0 with its reflect margins (positions [0, n0 + 2 ML)) to the
+        // level buffer, zero past them; the next clip's stage 1 reuses this region
+        const int n_valid = p.oct_len[0] + 2 * ML;
+        __half* dst = p.lv0 + b * (int64_t)p.lv0_stride;
+        const __half* src = sig(0);
+        for (int k8 = tid; k8 < p.lv0_stride / 8; k8 += kCompute) {
+          uint4 v = ld8(src, 8 * k8);
+          if (8 * k8 + 8 > n_valid) {
+            __half* hv = reinterpret_cast<__half*>(&v);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (8 * k8 + e >= n_valid) hv[e] = __float2half(0.f);
+          }
+          *reinterpret_cast<uint4*>(dst + 8 * k8) = v;
+        }
+        if (tid == 0) p.lv_exp[b] = ex;
+        csync();
+        continue;
+      }
 
       // -------------------------------------------- octaves, software-pipelined: the halving
       // alpha+1 MMA runs under the im2col of alpha, the conv alpha MMA under the
@@ -722,6 +749,348 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
   if (warp == 0) tmem_dealloc<512>(*tslot);
   if (p.prof && tid == 0)
     for (int i = 0; i < 16; ++i) atomicAdd(p.prof + i, prof_acc[i]);
+}
+
+// ------------------------------------------------------------------ batched octave levels
+// After the front (the fused kernel in front-only mode: stages 1-2 per clip, octave 0
+// to the level buffer), every octave level runs as two launches over ALL clips:
+// CONV (the 12-bin complex conv of octave alpha, frames as M) and HALVE (octave alpha ->
+// alpha + 1, blocks of 128 outputs as M, the same Toeplitz band as the fused kernel).
+// Tiles span clips, so no CTA walks one clip's serial chain: small shared memory, several
+// CTAs per SM, and the latency of one tile's build / MMA / epilogue hides behind the others'.
+// Level buffers: [B][stride] FP16 in the clip's power-of-two scale, sample i at ML + i,
+// np.pad "reflect" images of ML samples on both sides (written by the producer).
+struct LvParams {
+  int64_t B;
+  const __half* src;
+  int32_t src_stride, n_src;  // halves per clip row; signal length
+  __half* dst;
+  int32_t dst_stride, n_dst;
+  int32_t nb;                 // HALVE: blocks of 128 outputs per clip
+  float h0;
+  float g[128];
+  const int32_t* exps;        // per-clip scale exponent (values are s * 2^-e)
+  int32_t h, T, pad, pad_al, skip, row0, n_filt, n_bins, out_kind, width;
+  const float* k_re;
+  const float* k_im;
+  float* out;
+  const uint4* toep_img;  // the diagonal Toeplitz chunks (TOEP_CHUNKS x 16 B), built once per call
+  const uint4* filt_img;  // the conv bank operand (KC / 8 x 512 B), built once per call
+  unsigned long long* prof;  // debug: per-phase globaltimer ns sums (block 0's thread 0), or null
+  // CONV over all octaves in one launch: level a's buffer, row stride, length
+  const __half* lv[kMaxOct];
+  int32_t lv_stride[kMaxOct], lv_n[kMaxOct];
+  int32_t n_lv, kernel_hop, first_bin, bpo;
+};
+
+NNAB_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int kLvThreads = 256;
+constexpr int kHalveA = 32 * 128 * 16;   // A tile: 32 K-chunks x 128 rows x 16 B = 64 KB
+constexpr int kConvA = (KC / 8) * 128 * 16;  // im2col: 12 chunks x 128 frames x 16 B = 24 KB
+
+// 8 FP16 samples at (possibly unaligned) position i of a level row, 0 outside [0, lim).
+// The slow path is out of line: inlined, the compiler predicated it into every call.
+__device__ __noinline__ uint4 lv_load8_slow(const __half* row, int i, int lim);
+NNAB_DEV uint4 lv_load8(const __half* row, int i, int lim) {
+  if (i >= 0 && i + 8 <= lim && (i & 7) == 0) return __ldg(reinterpret_cast<const uint4*>(row + i));
+  return lv_load8_slow(row, i, lim);
+}
+__device__ __noinline__ uint4 lv_load8_slow(const __half* row, int i, int lim) {
+  __align__(16) __half v[8];
+  const unsigned short* r16 = reinterpret_cast<const unsigned short*>(row);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int k = i + e;
+    unsigned short u = (k >= 0 && k < lim) ? __ldg(r16 + k) : (unsigned short)0;
+    v[e] = __ushort_as_half(u);
+  }
+  return *reinterpret_cast<uint4*>(v);
+}
+
+// The shared-memory operand images every level CTA copies in: Toeplitz diagonal chunks
+// (chunk j = g[j - 127 + e]) and the conv bank (row 2j = Re bin j, 2j+1 = Im, scaled 2^6,
+// column m = tap m - (pad_al - pad)).  One CTA, once per call.
+__global__ void cqt2010_prep_kernel(const __grid_constant__ LvParams p, uint4* toep_img, uint4* filt_img) {
+  for (int j = threadIdx.x; j < TOEP_CHUNKS; j += blockDim.x) {
+    __align__(16) __half v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int gi = j - 127 + e;
+      v[e] = h16((gi >= 0 && gi < 128) ? p.g[gi] : 0.f);
+    }
+    toep_img[j] = *reinterpret_cast<uint4*>(v);
+  }
+  const int shift = p.pad_al - p.pad;
+  __half* f = reinterpret_cast<__half*>(filt_img);
+  for (int e = threadIdx.x; e < NCONV * KC; e += blockDim.x) {
+    const int n = e / KC, m = e % KC, j = n >> 1, tap = m - shift;
+    float v = 0.f;
+    if (j < p.n_filt && tap >= 0 && tap < p.width)
+      v = ldexpf(((n & 1) ? p.k_im : p.k_re)[(int64_t)j * p.width + tap], kFiltLog2);
+    f[(m >> 3) * 256 + n * 8 + (m & 7)] = h16(v);
+  }
+}
+
+// HALVE: octave alpha -> alpha + 1 for all clips.  Rows: clip b owns nb + 1 rows of 128
+// odd-phase samples (row r = src_ext[2 (128 r + u) - 127], u < 128); block (b, blk) = 128
+// outputs whose Toeplitz window is rows blk, blk + 1, so an M = 128 tile of rows reads 129
+// plane rows (the existing FIR's "planes": 16-byte chunk q of every row in plane q) and a
+// clip's extra row only feeds a discarded D row.  The build reads each row's 256 source
+// samples with coalesced 16-byte loads (16 threads per row) and keeps both phases: odd ->
+// planes, even -> the centre-tap rows (16-byte units XOR-swizzled by row).
+constexpr int kHPl = 131 * 16;  // plane stride: 129 rows + pad, an odd number of 16-byte units
+
+__global__ void __launch_bounds__(kLvThreads) cqt2010_halve_kernel(const __grid_constant__ LvParams p) {
+  const unsigned long long t_start = gtime();
+  unsigned long long t_mark = t_start;
+  auto mark = [&](int i) {
+    if (p.prof && threadIdx.x == 0) {
+      const unsigned long long n = gtime();
+      atomicAdd(p.prof + i, n - t_mark);
+      t_mark = n;
+    }
+  };
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* planes = base;                     // 16 planes x kHPl
+  uint8_t* even = base + 16 * kHPl;           // 129 rows x 256 B (centre taps)
+  uint8_t* toep = even + 129 * 256;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(toep + ((TOEP_CHUNKS * 16 + 127) & ~127));
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<128>(tslot);
+  for (int j = tid; j < TOEP_CHUNKS; j += kLvThreads) reinterpret_cast<uint4*>(toep)[j] = __ldg(p.toep_img + j);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  mark(0);
+  const int R = p.nb + 1;  // rows per clip
+  const int64_t n_rows = p.B * R;
+  const int64_t n_tiles = (n_rows + 127) / 128;
+  const int src_lim = p.n_src + 2 * ML;
+  uint32_t phase = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    // build 129 rows x 16 chunks; thread -> (row, chunk q), 16 threads per row; all of a
+    // thread's loads (9 jobs x 32 B) are in flight before the first store
+    constexpr int kJobs = (129 * 16 + kLvThreads - 1) / kLvThreads;
+    uint4 wa[kJobs], wb[kJobs];
+#pragma unroll
+    for (int jj = 0; jj < kJobs; ++jj) {
+      const int job = tid + jj * kLvThreads;
+      const int rr = job >> 4, qq = job & 15;
+      const int64_t g = tile * 128 + rr;
+      wa[jj] = wb[jj] = make_uint4(0, 0, 0, 0);
+      if (job < 129 * 16 && g < n_rows) {
+        const int64_t b = g / R;
+        const int r = (int)(g - b * R);
+        const __half* row = p.src + b * p.src_stride;
+        const int i0 = ML - 128 + 256 * r + 16 * qq;  // samples i0 .. i0 + 15: odd-phase u = 8 qq + e at i0 + 1 + 2e
+        wa[jj] = lv_load8(row, i0, src_lim);
+        wb[jj] = lv_load8(row, i0 + 8, src_lim);
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < kJobs; ++jj) {
+      const int job = tid + jj * kLvThreads;
+      if (job >= 129 * 16) break;
+      const int rr = job >> 4, qq = job & 15;
+      const uint4 w0 = wa[jj], w1 = wb[jj];
+      uint4 o, e;
+      o.x = __byte_perm(w0.x, w0.y, 0x7632);
+      o.y = __byte_perm(w0.z, w0.w, 0x7632);
+      o.z = __byte_perm(w1.x, w1.y, 0x7632);
+      o.w = __byte_perm(w1.z, w1.w, 0x7632);
+      e.x = __byte_perm(w0.x, w0.y, 0x5410);
+      e.y = __byte_perm(w0.z, w0.w, 0x5410);
+      e.z = __byte_perm(w1.x, w1.y, 0x5410);
+      e.w = __byte_perm(w1.z, w1.w, 0x5410);
+      *reinterpret_cast<uint4*>(planes + qq * kHPl + rr * 16) = o;
+      // even samples of row rr: src[ML - 128 + 256 rr' + 2 (8 qq + e)] = src[2 i] for i = 128 r - 64 + 8 qq + e
+      *reinterpret_cast<uint4*>(even + rr * 256 + ((qq ^ (rr & 15)) << 4)) = e;
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    mark(1);
+    if (tid == 0) {
+      tc_fence_after();
+      constexpr uint32_t idesc = idesc_f16(128, 128);
+      const uint32_t a0 = smem_u32(planes), t0 = smem_u32(toep);
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        mma_f16(tmem, nsw_desc(a0 + (uint32_t)(2 * (k & 7)) * kHPl + (uint32_t)(k >> 3) * 16u, kHPl, 128),
+                nsw_desc(t0 + 256u * k, 128, 128), idesc, k > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    mark(2);
+    // epilogue: TMEM lane = tile row m = block (b, blk), column r' = 127 - r; warp w reads lane
+    // quarter w & 3 and column half w >> 2 in 4 chunks of 16 columns = 16 consecutive outputs
+    const int q = warp & 3, half = warp >> 2;
+    const int m = q * 32 + lane;
+    const int64_t g = tile * 128 + m;
+    const int64_t b = g < n_rows ? g / R : 0;
+    const int blk = g < n_rows ? (int)(g - b * R) : 0;
+    const bool live = g < n_rows && blk < p.nb;  // the clip's extra row is not a block
+    __half* drow = p.dst + b * p.dst_stride;
+    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + half * 64;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int rbase = 112 - 64 * half - 16 * k;
+      const int i0 = blk * 128 + rbase;
+      float v[16];
+      tmem_ld16(ta + 16 * k, v);
+      tmem_ld_wait();
+      if (!live || i0 >= p.n_dst) continue;
+      // centre taps src[2 i], i = i0 .. i0 + 15: the even samples 128 blk - 64 + ... of rows m
+      // (i < 128 blk + 64) and m + 1 (the rest)
+      float y[16];
+      {
+        const int u = rbase + 64;  // even index within rows m, m + 1 (128 per row)
+        const int rr = m + (u >> 7), uu = u & 127;
+        const uint8_t* er = even + rr * 256;
+        const uint4 a = *reinterpret_cast<const uint4*>(er + ((((uu >> 3)) ^ (rr & 15)) << 4));
+        const uint4 c = *reinterpret_cast<const uint4*>(er + ((((uu >> 3) + 1) ^ (rr & 15)) << 4));
+        float t[8];
+        unpack8(a, t);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[e] = t[e];
+        unpack8(c, t);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[8 + e] = t[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) y[e] = fmaf(p.h0, y[e], v[15 - e]);
+      if (i0 + 16 <= p.n_dst) {
+        __align__(16) __half2 al[8];
+        pack_all(y, al);
+        *reinterpret_cast<uint4*>(drow + ML + i0) = reinterpret_cast<const uint4*>(al)[0];
+        *reinterpret_cast<uint4*>(drow + ML + i0 + 8) = reinterpret_cast<const uint4*>(al)[1];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (i0 + e < p.n_dst) drow[ML + i0 + e] = h16(y[e]);
+      }
+      // np.pad "reflect" images of the new level (signal.py:151): left -i, right 2(n-1) - i
+      if (i0 <= ML || i0 + 16 >= p.n_dst - 1 - ML) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int i = i0 + e;
+          if (i >= p.n_dst) break;
+          if (i >= 1 && i <= ML) drow[ML - i] = h16(y[e]);
+          if (i >= p.n_dst - 1 - ML && i <= p.n_dst - 2) drow[ML + 2 * (p.n_dst - 1) - i] = h16(y[e]);
+        }
+      }
+      if (i0 < p.n_dst && i0 + 16 >= p.n_dst) {  // the row's tail past the right image: finite zeros
+        for (int j = p.n_dst + 2 * ML; j < p.dst_stride; ++j) drow[j] = __float2half(0.f);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    mark(3);
+  }
+  if (warp == 0) tmem_dealloc<128>(tmem);
+  mark(4);
+  if (p.prof && threadIdx.x == 0) atomicAdd(p.prof + 5, 1ull);
+}
+
+__global__ void __launch_bounds__(kLvThreads) cqt2010_conv_kernel(const __grid_constant__ LvParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* A = base;
+  uint8_t* filt = base + kConvA;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(filt + KC / 8 * 512);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<32>(tslot);
+  for (int j = tid; j < KC / 8 * 32; j += kLvThreads) reinterpret_cast<uint4*>(filt)[j] = __ldg(p.filt_img + j);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int64_t n_frames = p.B * p.T;
+  const int64_t lv_tiles = (n_frames + 127) / 128;  // tiles per octave level
+  const int64_t n_tiles = lv_tiles * p.n_lv;
+  uint32_t phase = 0;
+  for (int64_t tile_all = blockIdx.x; tile_all < n_tiles; tile_all += gridDim.x) {
+    const int lvl = (int)(tile_all / lv_tiles);
+    const int64_t tile = tile_all - lvl * lv_tiles;
+    const __half* lsrc = p.lv[lvl];
+    const int lstride = p.lv_stride[lvl], src_lim = p.lv_n[lvl] + 2 * ML, lh = p.kernel_hop >> lvl;
+    const int lskip = max(0, lvl * p.bpo - p.first_bin), lrow0 = p.first_bin - lvl * p.bpo;
+    // im2col: frame (b, t) tap column kk holds src[b][ML - pad_al + t h + kk]; thread = frame
+    // row m, 6 chunks per thread with all loads in flight before the stores
+    {
+      const int m = tid & 127, c0 = (tid >> 7) * (KC / 16);
+      const int64_t gf = tile * 128 + m;
+      const bool ok = gf < n_frames;
+      const int64_t b = ok ? gf / p.T : 0;
+      const int t = ok ? (int)(gf - b * p.T) : 0;
+      const __half* row = lsrc + b * lstride;
+      uint4 w[KC / 16];
+#pragma unroll
+      for (int u = 0; u < KC / 16; ++u)
+        w[u] = ok ? lv_load8(row, ML - p.pad_al + t * lh + 8 * (c0 + u), src_lim) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < KC / 16; ++u) *reinterpret_cast<uint4*>(A + (c0 + u) * 2048 + m * 16) = w[u];
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      constexpr uint32_t idesc = idesc_f16(128, NCONV);
+      const uint32_t a0 = smem_u32(A), b0 = smem_u32(filt);
+#pragma unroll
+      for (int k = 0; k < KC / 16; ++k)
+        mma_f16(tmem, nsw_desc(a0 + (uint32_t)k * 4096u, 2048, 128), nsw_desc(b0 + (uint32_t)k * 1024u, 512, 128),
+                idesc, k > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // epilogue: thread = frame (lane quarter q), column half -> bins 8 * half .. + 7
+    const int q = warp & 3, half = warp >> 2;
+    const int64_t gf = tile * 128 + q * 32 + lane;
+    float v[16];
+    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + 16 * half, v);
+    tmem_ld_wait();
+    if (gf < n_frames) {
+      const int64_t b = gf / p.T;
+      const int t = (int)(gf - b * p.T);
+      const float os = ldexpf(1.f, __ldg(p.exps + b) - kFiltLog2);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * half + jj;
+        if (j < lskip || j >= p.n_filt) continue;
+        const float re = v[2 * jj] * os, im = v[2 * jj + 1] * os;
+        const int64_t o = (b * p.n_bins + lrow0 + j) * (int64_t)p.T + t;
+        if (p.out_kind == NNAB_OUT_COMPLEX) reinterpret_cast<float2*>(p.out)[o] = make_float2(re, im);
+        else if (p.out_kind == NNAB_OUT_POWER) p.out[o] = fmaf(re, re, im * im);
+        else p.out[o] = fast_sqrt(fmaf(re, re, im * im));
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+  }
+  if (warp == 0) tmem_dealloc<32>(tmem);
 }
 
 __device__ unsigned long long g_cqt_prof[16];
@@ -828,7 +1197,130 @@ int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, i
   return NNAB_OK;
 }
 
+// Level buffer geometry of the batched path: one [B][stride] FP16 row set per octave.
+struct LvPlan {
+  int32_t n[kMaxOct], stride[kMaxOct];
+  size_t off[kMaxOct], exp_off, toep_off, filt_off, total;
+};
+void lv_plan(const TcParams& tp, int64_t B, LvPlan* lp) {
+  size_t off = ((size_t)B * 4 + 255) & ~size_t(255);  // exps first, then the operand images
+  lp->exp_off = 0;
+  lp->toep_off = off;
+  off += (TOEP_CHUNKS * 16 + 255) & ~255;
+  lp->filt_off = off;
+  off += (KC / 8 * 512 + 255) & ~255;
+  for (int a = 0; a < tp.n_oct; ++a) {
+    lp->n[a] = tp.oct_len[a];
+    lp->stride[a] = rnd((int64_t)tp.oct_len[a] + 2 * ML, 8);
+    lp->off[a] = off;
+    off += ((size_t)B * lp->stride[a] * 2 + 4096 + 255) & ~size_t(255);  // + slack read as 0-weight operands
+  }
+  lp->total = off;
+}
+
 }  // namespace
+
+// Workspace the batched CQT2010v2 path needs (0 outside the fused kernel's envelope).
+size_t cqt2010_levels_bytes(int64_t B, int64_t L, const float* taps, int n_taps, int n_filt, int width,
+                            int early_stages, int n_oct, int kernel_hop, int T, int pad_mode) {
+  Plan pl;
+  if (make_plan(L, n_taps, taps, n_filt, width, early_stages, n_oct, kernel_hop, T, pad_mode, &pl)) return 0;
+  LvPlan lp;
+  lv_plan(pl.p, B, &lp);
+  return lp.total;
+}
+
+// The batched path: the fused kernel in front-only mode (stages 1-2 per clip, octave 0
+// to the level buffer), then per octave one CONV launch and one HALVE launch over all clips.
+int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, const float* k_re,
+                          const float* k_im, int n_filt, int width, int early_stages, int n_oct, int kernel_hop,
+                          int first_bin, int bpo, int n_bins, int pad_mode, int out_kind, int T, float* out,
+                          void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  Plan pl;
+  int rc = make_plan(L, n_taps, taps, n_filt, width, early_stages, n_oct, kernel_hop, T, pad_mode, &pl);
+  if (rc) return rc;
+  if (n_filt > 16) return NNAB_ENOTSUP;
+  LvPlan lp;
+  lv_plan(pl.p, B, &lp);
+  if (!workspace || workspace_bytes < lp.total) return NNAB_ENOTSUP;
+  char* ws = reinterpret_cast<char*>(workspace);
+  int32_t* exps = reinterpret_cast<int32_t*>(ws + lp.exp_off);
+  TcParams& p = pl.p;
+  p.x = x;
+  p.B = B;
+  p.first_bin = first_bin;
+  p.bpo = bpo;
+  p.n_bins = n_bins;
+  p.n_filt = n_filt;
+  p.width = width;
+  p.out_kind = out_kind;
+  p.h0 = taps[127];
+  for (int j = 0; j < 128; ++j) p.g[j] = taps[2 * j];
+  p.k_re = k_re;
+  p.k_im = k_im;
+  p.out = out;
+  p.prof = nullptr;
+  p.lv0 = reinterpret_cast<__half*>(ws + lp.off[0]);
+  p.lv_exp = exps;
+  p.lv0_stride = lp.stride[0];
+  NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  cqt2010_tc_kernel<<<(int)std::min<int64_t>(B, (int64_t)num_sms()), kThreads, pl.smem, st>>>(p);
+  NNAB_LAUNCHED();
+
+  LvParams q{};
+  q.B = B;
+  q.h0 = taps[127];
+  for (int j = 0; j < 128; ++j) q.g[j] = taps[2 * j];
+  q.exps = exps;
+  q.T = T;
+  q.pad = p.pad;
+  q.pad_al = p.pad_al;
+  q.n_filt = n_filt;
+  q.n_bins = n_bins;
+  q.out_kind = out_kind;
+  q.width = width;
+  q.k_re = k_re;
+  q.k_im = k_im;
+  q.out = out;
+  q.prof = cqt2010_prof_ptr();
+  q.toep_img = reinterpret_cast<const uint4*>(ws + lp.toep_off);
+  q.filt_img = reinterpret_cast<const uint4*>(ws + lp.filt_off);
+  cqt2010_prep_kernel<<<1, 256, 0, st>>>(q, reinterpret_cast<uint4*>(ws + lp.toep_off),
+                                          reinterpret_cast<uint4*>(ws + lp.filt_off));
+  NNAB_LAUNCHED();
+  const size_t smem_conv = 1024 + kConvA + KC / 8 * 512 + 64;
+  const size_t smem_halve = 1024 + 16 * kHPl + 129 * 256 + ((TOEP_CHUNKS * 16 + 127) & ~127) + 64;
+  NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_conv));
+  NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_halve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_halve));
+  q.n_lv = n_oct;
+  q.kernel_hop = kernel_hop;
+  q.first_bin = first_bin;
+  q.bpo = bpo;
+  for (int a = 0; a < n_oct; ++a) {
+    q.lv[a] = reinterpret_cast<const __half*>(ws + lp.off[a]);
+    q.lv_stride[a] = lp.stride[a];
+    q.lv_n[a] = lp.n[a];
+  }
+  // the halvings octave by octave, then every octave's conv in one launch
+  for (int a = 0; a < n_oct; ++a) {
+    q.src = reinterpret_cast<const __half*>(ws + lp.off[a]);
+    q.src_stride = lp.stride[a];
+    q.n_src = lp.n[a];
+    if (a + 1 < n_oct) {
+      q.dst = reinterpret_cast<__half*>(ws + lp.off[a + 1]);
+      q.dst_stride = lp.stride[a + 1];
+      q.n_dst = lp.n[a + 1];
+      q.nb = (q.n_dst + 127) / 128;
+      const int64_t tiles = (B * (int64_t)(q.nb + 1) + 127) / 128;
+      cqt2010_halve_kernel<<<(int)std::min<int64_t>(tiles, 2 * (int64_t)num_sms()), kLvThreads, smem_halve, st>>>(q);
+      NNAB_LAUNCHED();
+    }
+  }
+  const int64_t conv_tiles = n_oct * ((B * (int64_t)T + 127) / 128);
+  cqt2010_conv_kernel<<<(int)std::min<int64_t>(conv_tiles, 4 * (int64_t)num_sms()), kLvThreads, smem_conv, st>>>(q);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
 
 // Debug: enable per-phase cycle counters of the fused kernel (on != 0), or read
 // and clear them into out[16] (on == 0).  Phases: 12 wait for the scale,

@@ -123,5 +123,14 @@ int launch_cqt2010_tc(const float* x, int64_t B, int64_t L, const float* taps, i
                       int first_bin, int bpo, int n_bins, int pad_mode, int out_kind, int T, float* out,
                       cudaStream_t st);
 int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s);
+// CQT2010v2 batched path (cqt2010_tc.cu): the fused kernel as a per-clip front (stages
+// 1-2), then per octave a CONV and a HALVE launch over all clips through level buffers
+// in `workspace` (cqt2010_levels_bytes); NNAB_ENOTSUP outside the envelope / without room
+size_t cqt2010_levels_bytes(int64_t B, int64_t L, const float* taps, int n_taps, int n_filt, int width,
+                            int early_stages, int n_oct, int kernel_hop, int T, int pad_mode);
+int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, const float* k_re,
+                          const float* k_im, int n_filt, int width, int early_stages, int n_oct, int kernel_hop,
+                          int first_bin, int bpo, int n_bins, int pad_mode, int out_kind, int T, float* out,
+                          void* workspace, size_t workspace_bytes, cudaStream_t st);
 
 }  // namespace nnab

@@ -250,3 +250,34 @@ def test_cqt1992v2_batch_vs_sequential(golden, cuda_dev):
             assert O.peak_err(one, whole) < 1e-6
         # and run to run, the same launch is bit-reproducible
         assert np.array_equal(e.forward(x).cpu().numpy(), whole)
+
+
+def test_cqt2010v2_levels_path_matches_oracle(tmp_path):
+    """The batched CQT2010v2 path (NNAB_CQT2010_LEVELS=1: fused front for stages 1-2,
+    level-synchronous HALVE launches, one CONV launch over all octaves) against the
+    oracle and the default fused kernel, in a subprocess (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys; sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from oracle import spectro_oracle as O
+from paper_1912_12055_b200.engine import Cqt2010Engine
+cfg = O.CqtCfg(sr=44100.0); p = O.cqt2010_plan(cfg)
+eng = Cqt2010Engine(p.taps, p.top_kernels, p.early_stages, p.n_octaves, p.kernel_hop, p.first_bin, 12, 84,
+                    "reflect", precision="f16")
+rng = np.random.default_rng(13)
+x = (rng.standard_normal((300, 80000)) * 0.5).astype(np.float32)
+x[7] *= 1e-4
+got = eng.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+errs = [O.peak_err(got[i], O.cqt2010v2_clip(x[i].astype(np.float64), cfg, p)) for i in (0, 7, 150, 299)]
+np.save(sys.argv[2], got[:4])
+print(max(errs))
+'''
+    out = str(tmp_path / "lv.npy")
+    env = dict(os.environ, NNAB_CQT2010_LEVELS="1")
+    r = subprocess.run([sys.executable, "-c", code, root, out], env=env, capture_output=True, text=True, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= 1e-3
