@@ -172,9 +172,10 @@ MODES = {
     ("stft", "tf32"): ("tf32", "tf32", "tf32"),
     ("stft", "fp32"): ("fp32", "3xf16 (FP16 hi/lo split, exact power-of-two scales, f32 accumulate)", "f16"),
     ("stft", "3xtf32"): ("3xtf32", "3xtf32", "tf32"),
-    ("cqt1992v2", "f16"): ("tf32", "tf32", "tf32"),
+    ("cqt1992v2", "f16"): ("f16", "f16 operands (exact per-clip / per-bank power-of-two scales), f32 accumulate", "f16"),
     ("cqt1992v2", "tf32"): ("tf32", "tf32", "tf32"),
-    ("cqt1992v2", "fp32"): ("fp32", "3xtf32", "tf32"),
+    ("cqt1992v2", "fp32"): ("fp32", "3xf16 (FP16 hi/lo split, exact power-of-two scales, f32 accumulate)", "f16"),
+    ("cqt1992v2", "3xtf32"): ("3xtf32", "3xtf32", "tf32"),
     ("cqt2010v2", "f16"): ("f16", "f16 operands (exact per-clip power-of-two scale), f32 accumulate", None),
     ("cqt2010v2", "tf32"): ("f16", "f16 operands (exact per-clip power-of-two scale), f32 accumulate", None),
     ("cqt2010v2", "fp32"): ("fp32", "f32 (CUDA cores)", None),
@@ -188,7 +189,7 @@ for _m in ("f16", "tf32", "fp32", "3xtf32"):
     if ("stft", _m) in MODES:
         MODES[("mel", _m)] = MODES[("melpow2", _m)] = MODES[("stft", _m)]
 BREAKDOWN_MODES = {"stft": ["f16", "tf32", "fp32"], "mel": ["f16", "tf32", "fp32"], "melpow2": ["f16", "tf32", "fp32"],
-                   "cqt1992v2": ["tf32", "fp32"], "cqt2010v2": ["f16", "fp32"],
+                   "cqt1992v2": ["f16", "tf32", "fp32"], "cqt2010v2": ["f16", "fp32"],
                    "train": ["tf32", "tf32-onepass", "fp32"]}
 
 

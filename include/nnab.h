@@ -66,7 +66,8 @@ extern "C" {
 /* FP16 operands under exact power-of-two scales (per clip for the signal, per
  * bank for the kernels) so every operand sits in FP16's normal range: the same
  * 11-bit significand as TF32 at twice the tcgen05 rate (kind::f16, FP32
- * accumulate); the scales are undone exactly in the epilogue.  STFT / Mel only. */
+ * accumulate); the scales are undone exactly in the epilogue.  STFT / Mel and
+ * CQT1992v2 (hybrid E-GEMM + schedule). */
 #define NNAB_PREC_F16 2   /* one FP16 pass (<= 1e-3) */
 #define NNAB_PREC_3XF16 3 /* FP16 hi/lo split, 3 passes (<= 1e-5) */
 
@@ -257,6 +258,9 @@ int nnab_input_grad(const nnab_frames* f, const float* frame_grads_t, int64_t ld
  * out: (B, n_bins, T) float32, or complex64 re + i*im for NNAB_OUT_COMPLEX. */
 int nnab_cqt_bank_tiles(int32_t n_bins);
 size_t nnab_cqt_bank_bytes(int32_t n_bins, int32_t width);
+/* bytes of each packed schedule-bank array for `precision` (FP16 modes: halves, K
+ * padded to 64, plus a 256-byte scale trailer in the hi array) */
+size_t nnab_cqt_bank_bytes_prec(int32_t n_bins, int32_t width, int32_t precision);
 int nnab_pack_cqt_bank(const float* k_re, const float* k_im, int32_t n_bins, int32_t width, int32_t precision,
                        float* packed_hi, float* packed_lo, void* stream);
 /* host-only: support[2*bin], support[2*bin+1] = non-zero column range [begin, end)
@@ -284,6 +288,8 @@ int nnab_cqt_egemm_plan(const int32_t* support, int32_t n_bins, int32_t width, i
                         uint16_t* col_table, int32_t* group_rows, uint32_t* run_table /* [max_groups*4*65] */,
                         int32_t* n_groups, int32_t* r_max);
 size_t nnab_cqt_egemm_bank_bytes(int32_t n_groups, int32_t hop);
+/* the same for `precision` (FP16 modes: halves plus a 256-byte scale trailer) */
+size_t nnab_cqt_egemm_bank_bytes_prec(int32_t n_groups, int32_t hop, int32_t precision);
 int nnab_pack_cqt_egemm(const float* k_re, const float* k_im, int32_t width, int32_t hop, const uint16_t* col_table,
                         const int32_t* group_rows, int32_t n_groups, int32_t precision, float* packed_hi,
                         float* packed_lo, void* stream);

@@ -79,6 +79,8 @@ SIGNATURES = {
     "nnab_input_grad": (C.c_int, [_FR, _fp, _i64, _fp, _vp]),
     "nnab_cqt_bank_tiles": (C.c_int, [_i32]),
     "nnab_cqt_bank_bytes": (_sz, [_i32, _i32]),
+    "nnab_cqt_bank_bytes_prec": (_sz, [_i32, _i32, _i32]),
+    "nnab_cqt_egemm_bank_bytes_prec": (_sz, [_i32, _i32, _i32]),
     "nnab_pack_cqt_bank": (C.c_int, [_fp, _fp, _i32, _i32, _i32, _fp, _fp, _vp]),
     "nnab_cqt_schedule": (C.c_int, [_ip, _i32, _i32, _i32, _ip, C.POINTER(_i32)]),
     "nnab_cqt1992v2_forward": (C.c_int, [_FR, _fp, _fp, _fp, _i32, _ip, _i32, _i32, _i32, _f32, _fp, _vp, _sz,

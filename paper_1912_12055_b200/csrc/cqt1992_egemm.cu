@@ -33,6 +33,8 @@
 // output, coalesced along T.  Each CTA also computes the first tile past its
 // run (a 1-in-~150 overlap) so its last D rows are complete; D rows before its
 // run belong to the previous CTA.
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -64,6 +66,8 @@ struct EParams {
   const uint16_t* col_table;  // [n_groups][256]: row_local << 8 | r
   const int32_t* group_rows;  // [n_groups][64]: bank row 2*bin + im, -1 unused
   float* out;
+  const int32_t* a_exp;  // FP16: per-clip scale exponent of the staged rows
+  const int32_t* b_exp;  // FP16: the bank's scale exponent
 };
 
 NNAB_DEV uint64_t sdesc(const void* p) {  // K-major, 128-byte swizzle, 8-row atoms
@@ -80,18 +84,23 @@ NNAB_DEV void ep_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // e
 // Pipeline geometry: single CTAs stage A (16 KB) + all of B (32 KB) x 3; a CTA
 // pair (kPair) stages A + half of B (16 + 16 KB) x 4; 3xTF32 (kSplit, pairs)
 // stages hi and lo of both (64 KB) x 2.
-template <bool kPair, bool kSplit = false>
+// kHalf: FP16 operands (staged rows and bank under exact power-of-two scales, kind::f16):
+// the same 128-byte K-block rows hold 64 samples instead of 32, so K = hop = 512 is 8
+// K blocks; the scales are undone when the D rows are emitted.
+template <bool kPair, bool kSplit = false, bool kHalf = false>
 struct ECfg {
   static constexpr int STAGES = kSplit ? 2 : kPair ? 4 : 3;
   static constexpr int B_ROWS = kPair ? kBN / 2 : kBN;
-  static constexpr int HALF = kA + B_ROWS * kBK * 4;  // the hi (or lo) operands
+  static constexpr int HALF = kA + B_ROWS * 128;  // the hi (or lo) operands: 128-byte rows
   static constexpr int STAGE = HALF * (kSplit ? 2 : 1);
-  static constexpr int NACC = kSplit ? 1 : 2;  // 3xTF32: main + correction fill TMEM
+  static constexpr int NACC = kSplit ? 1 : 2;  // split: main + correction fill TMEM
+  static constexpr int BK = kHalf ? 64 : 32;   // elements per K block
+  static constexpr int NKB = 512 / BK;         // K blocks per hop
 };
-template <bool kPair, bool kSplit = false>
+template <bool kPair, bool kSplit = false, bool kHalf = false>
 constexpr size_t egemm_smem() {
-  return 1024 + (size_t)ECfg<kPair, kSplit>::STAGES * ECfg<kPair, kSplit>::STAGE + (size_t)4 * kRows * kRing * 4 +
-         kBN * 2 + kRows * 4 + 16 * 8;
+  using EC = ECfg<kPair, kSplit, kHalf>;
+  return 1024 + (size_t)EC::STAGES * EC::STAGE + (size_t)4 * kRows * kRing * 4 + kBN * 2 + kRows * 4 + 16 * 8;
 }
 
 // kPair: a cluster of two CTAs of the same group runs two independent tile runs
@@ -100,12 +109,13 @@ constexpr size_t egemm_smem() {
 // epilogue and D rings stay its own.
 // kSplit (3xTF32, FP32-accurate): E = A_hi B_hi (main accumulator) +
 // (A_hi B_lo + A_lo B_hi) (correction accumulator), summed in the epilogue.
-template <bool kPair, bool kSplit = false>
+template <bool kPair, bool kSplit = false, bool kHalf = false>
 __global__ void __launch_bounds__(kThreads, 1)
     cqt1992_egemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                          const __grid_constant__ CUtensorMap tm_a_lo, const __grid_constant__ CUtensorMap tm_b_lo,
                          const EParams p) {
-  using EC = ECfg<kPair, kSplit>;
+  using EC = ECfg<kPair, kSplit, kHalf>;
+  constexpr int kBK = EC::BK;
   static_assert(!kSplit || kPair, "3xTF32 E-GEMM runs as CTA pairs");
   constexpr int NACC = EC::NACC;
   constexpr int kStages = EC::STAGES, kStage = EC::STAGE;
@@ -167,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int s = 0;
         uint32_t ph = 0;
         for (int m = m_a; m < m_end; ++m)
-          for (int kb = 0; kb < 16; ++kb) {
+          for (int kb = 0; kb < EC::NKB; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             uint8_t* st = smem + s * kStage;
             if (kPair) {  // both CTAs' bytes complete on the leader's barrier
@@ -195,26 +205,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
       // -------------------------------------------------------------- MMA issuer
       if (rank == 0 && elect_one()) {
-        constexpr uint32_t idesc = idesc_tf32(kPair ? 2 * kBM : kBM, kBN);
+        constexpr uint32_t idesc = kHalf ? idesc_f16(kPair ? 2 * kBM : kBM, kBN) : idesc_tf32(kPair ? 2 * kBM : kBM, kBN);
         int s = 0, acc = 0;
         uint32_t ph = 0, aph = 0;
         for (int m = m_a; m < m_end; ++m) {
           mbar_wait(&tempty[acc], aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + acc * kBN;
-          for (int kb = 0; kb < 16; ++kb) {
+          for (int kb = 0; kb < EC::NKB; ++kb) {
             mbar_wait(&full[s], ph);
             tc_fence_after();
             uint8_t* st = smem + s * kStage;
             const uint64_t a = sdesc(st), b = sdesc(st + kA);
             const uint64_t a_lo = sdesc(st + EC::HALF), b_lo = sdesc(st + EC::HALF + kA);
+            auto mma = [&](uint32_t dd, uint64_t aa, uint64_t bb, uint32_t acc_) {
+              if (kHalf) {
+                if (kPair) mma_f16_pair(dd, aa, bb, idesc, acc_);
+                else mma_f16(dd, aa, bb, idesc, acc_);
+              } else {
+                if (kPair) mma_tf32_pair(dd, aa, bb, idesc, acc_);
+                else mma_tf32(dd, aa, bb, idesc, acc_);
+              }
+            };
 #pragma unroll
-            for (int k = 0; k < kBK / 8; ++k) {
-              if (kPair) mma_tf32_pair(d, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
-              else mma_tf32(d, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) {  // 4 MMAs of 32 bytes of K per 128-byte K block
+              mma(d, a + 2 * k, b + 2 * k, (kb | k) != 0);
               if (kSplit) {
-                mma_tf32_pair(d + kBN, a + 2 * k, b_lo + 2 * k, idesc, (kb | k) != 0);
-                mma_tf32_pair(d + kBN, a_lo + 2 * k, b + 2 * k, idesc, 1u);
+                mma(d + kBN, a + 2 * k, b_lo + 2 * k, (kb | k) != 0);
+                mma(d + kBN, a_lo + 2 * k, b + 2 * k, 1u);
               }
             }
             if (kPair) mma_commit_pair(&empty[s], 0x3);
@@ -313,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int b = (int)(d / p.R), t = (int)(d - (int64_t)b * p.R);
           const bool emit = d >= own && b < p.B && t < p.T;  // else: partial sums of another CTA's rows
           const int slot = (int)(d & (kRing - 1));
+          const float osc = (kHalf && emit) ? ldexpf(1.f, -(__ldg(p.a_exp + b) + __ldg(p.b_exp))) : 1.f;
           for (int bl = 0; bl < n_gbins; ++bl) {
             float re = 0.f, im = 0.f;
 #pragma unroll
@@ -324,6 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               pre[kRing] = 0.f;
             }
             if (!emit) continue;
+            re *= osc;
+            im *= osc;
             const int64_t o = ((int64_t)b * p.n_bins + (rows[2 * bl] >> 1)) * (int64_t)p.T + t;
             if (p.out_kind == NNAB_OUT_COMPLEX) {
               reinterpret_cast<float2*>(p.out)[o] = make_float2(re, im);
@@ -372,7 +393,59 @@ __global__ void pack_egemm_kernel(const float* __restrict__ k_re, const float* _
   }
 }
 
+// Peak |value| over the E-GEMM bank's columns (ordered bits of a non-negative float)
+__global__ void egemm_absmax_kernel(const float* __restrict__ k_re, const float* __restrict__ k_im, int32_t width,
+                                    int32_t hop, const uint16_t* __restrict__ col_table,
+                                    const int32_t* __restrict__ group_rows, int32_t n_groups,
+                                    unsigned int* __restrict__ out) {
+  const int64_t total = (int64_t)n_groups * kBN * hop;
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = i / hop;
+    const int c = (int)(i - col * hop);
+    const uint16_t meta = col_table[col];
+    if (meta == kUnused) continue;
+    const int row = group_rows[(int)(col / kBN) * kRows + (meta >> 8)];
+    const int64_t k = (int64_t)(meta & 0xFF) * hop + c;
+    if (row >= 0 && k < width) m = fmaxf(m, fabsf(((row & 1) ? k_im : k_re)[(int64_t)(row >> 1) * width + k]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
+// FP16 E-GEMM bank: the same columns scaled by 2^e_h (trailer[1], from the bank peak in trailer[0])
+__global__ void pack_egemm_f16_kernel(const float* __restrict__ k_re, const float* __restrict__ k_im, int32_t width,
+                                      int32_t hop, const uint16_t* __restrict__ col_table,
+                                      const int32_t* __restrict__ group_rows, int32_t n_groups, int32_t split,
+                                      __half* __restrict__ hi, __half* __restrict__ lo, int32_t* __restrict__ trailer) {
+  const float pk = __uint_as_float(static_cast<unsigned int>(trailer[0]));
+  int ex = 0;
+  if (pk > 0.f && pk < INFINITY) frexpf(pk, &ex);
+  const int e = pk > 0.f ? max(-100, min(100, 15 - ex)) : 0;
+  const float sc = ldexpf(1.f, e);
+  if (blockIdx.x == 0 && threadIdx.x == 0) trailer[1] = e;
+  const int64_t total = (int64_t)n_groups * kBN * hop;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = i / hop;
+    const int c = (int)(i - col * hop);
+    const int g = (int)(col / kBN);
+    const uint16_t meta = col_table[col];
+    float v = 0.f;
+    if (meta != kUnused) {
+      const int row = group_rows[g * kRows + (meta >> 8)];
+      const int64_t k = (int64_t)(meta & 0xFF) * hop + c;
+      if (row >= 0 && k < width) v = ((row & 1) ? k_im : k_re)[(int64_t)(row >> 1) * width + k];
+    }
+    v *= sc;
+    const __half h = __float2half_rn(v);
+    hi[i] = h;
+    if (split) lo[i] = __float2half_rn(v - __half2float(h));
+  }
+}
+
 }  // namespace
+
 }  // namespace nnab
 
 using namespace nnab;
@@ -456,18 +529,39 @@ extern "C" size_t nnab_cqt_egemm_bank_bytes(int32_t n_groups, int32_t hop) {
   return (size_t)std::max(0, n_groups) * kBN * std::max(0, hop) * sizeof(float);
 }
 
+extern "C" size_t nnab_cqt_egemm_bank_bytes_prec(int32_t n_groups, int32_t hop, int32_t precision) {
+  if (!prec_is_f16(precision)) return nnab_cqt_egemm_bank_bytes(n_groups, hop);
+  const size_t data = (size_t)std::max(0, n_groups) * kBN * std::max(0, hop) * 2;
+  return ((data + 255) & ~size_t(255)) + 256;  // + trailer: [0] peak bits, [1] scale exponent
+}
+
 // Device tables (col_table, group_rows as produced by nnab_cqt_egemm_plan).
 extern "C" int nnab_pack_cqt_egemm(const float* k_re, const float* k_im, int32_t width, int32_t hop,
                                    const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups,
                                    int32_t precision, float* packed_hi, float* packed_lo, void* stream) {
   if (!k_re || !k_im || !col_table || !group_rows || !packed_hi || n_groups < 1 || width < 1 || hop < 1)
     return NNAB_EINVAL;
-  const int split = precision == NNAB_PREC_3XTF32;
+  if (!prec_valid(precision)) return NNAB_EINVAL;
+  const int split = prec_is_split(precision);
   if (split && !packed_lo) return NNAB_EINVAL;
   const int64_t total = (int64_t)n_groups * kBN * hop;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8192);
-  pack_egemm_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(k_re, k_im, width, hop, col_table, group_rows,
-                                                              n_groups, split, packed_hi, packed_lo);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (prec_is_f16(precision)) {
+    int32_t* trailer = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(packed_hi) +
+                                                  nnab_cqt_egemm_bank_bytes_prec(n_groups, hop, precision) - 256);
+    NNAB_CUDA_TRY(cudaMemsetAsync(trailer, 0, 8, s));
+    egemm_absmax_kernel<<<blocks, 256, 0, s>>>(k_re, k_im, width, hop, col_table, group_rows, n_groups,
+                                               reinterpret_cast<unsigned int*>(trailer));
+    NNAB_LAUNCHED();
+    pack_egemm_f16_kernel<<<blocks, 256, 0, s>>>(k_re, k_im, width, hop, col_table, group_rows, n_groups, split,
+                                                 reinterpret_cast<__half*>(packed_hi),
+                                                 reinterpret_cast<__half*>(packed_lo), trailer);
+    NNAB_LAUNCHED();
+    return NNAB_OK;
+  }
+  pack_egemm_kernel<<<blocks, 256, 0, s>>>(k_re, k_im, width, hop, col_table, group_rows, n_groups, split,
+                                           packed_hi, packed_lo);
   NNAB_LAUNCHED();
   return NNAB_OK;
 }
@@ -484,39 +578,40 @@ static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const 
                             const uint16_t* col_table, const int32_t* group_rows, int32_t n_groups, int32_t r_max,
                             int32_t out_bins, int32_t out_kind, float eps, float* out, const void* workspace,
                             size_t workspace_bytes, int32_t precision, cudaStream_t stream) {
+  if (!prec_valid(precision)) return NNAB_EINVAL;
+  const bool split = prec_is_split(precision), half = prec_is_f16(precision);
   FrameGeom g;
-  int rc = frame_geometry(f, &g);
+  const void *rows_hi, *rows_lo;
+  const int32_t* exps;
+  int rc = staged_views(f, precision, workspace, workspace_bytes, &g, &rows_hi, &rows_lo, &exps);
   if (rc) return rc;
-  const bool split = precision == NNAB_PREC_3XTF32;
-  if (precision != NNAB_PREC_TF32 && !split) return NNAB_EINVAL;
   if (!packed_hi || (split && !packed_lo) || !col_table || !group_rows || !out || n_groups < 1 || out_bins < 1)
     return NNAB_EINVAL;
   if (r_max < 0 || r_max + kBM > kRing) return NNAB_EINVAL;
-  if (g.row_len != g.hop || g.hop % kBK != 0 || g.hop / kBK != 16) return NNAB_ENOTSUP;  // K = hop = 512
+  const int bk = half ? 64 : 32;  // elements per 128-byte K block
+  if (g.row_len != g.hop || g.hop != 512) return NNAB_ENOTSUP;  // K = hop = 512
   if (out_kind != NNAB_OUT_MAGNITUDE && out_kind != NNAB_OUT_POWER && out_kind != NNAB_OUT_COMPLEX &&
       out_kind != NNAB_OUT_SMOOTH_MAG)
     return NNAB_EINVAL;
   if (g.B == 0) return NNAB_OK;
-  const size_t need = nnab_stft_workspace_bytes(f, precision);
-  if (!workspace || workspace_bytes < need) return NNAB_EINVAL;
   const int nsm = num_sms();
   if (n_groups > nsm) return NNAB_ENOTSUP;
   static const bool pair_ok = [] {
     const char* e = getenv("NNAB_EGEMM_PAIR");
     return !(e && e[0] == '0');
   }();
-  const bool pair = (pair_ok || split) && nsm / n_groups >= 2;
-  if (split && !pair) return NNAB_ENOTSUP;  // 3xTF32 runs as CTA pairs only
+  const bool pair = (pair_ok || split || half) && nsm / n_groups >= 2;
+  if ((split || half) && !pair) return NNAB_ENOTSUP;  // split and FP16 modes run as CTA pairs only
   CUtensorMap ta, tb, ta_lo, tb_lo;
   const uint64_t rows_total = (uint64_t)g.B * g.R;
   const int b_box = pair ? kBN / 2 : kBN;
-  rc = make_tmap_2d(&ta, workspace, g.row_len, rows_total, (uint64_t)g.row_len * 4, kBK, kBM, 128);
-  if (!rc) rc = make_tmap_2d(&tb, packed_hi, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * 4, kBK, b_box, 128);
-  if (!rc && split) {  // staged rows: hi then lo halves of the workspace (as cqt1992.cu)
-    const void* rows_lo = reinterpret_cast<const char*>(workspace) + need / 2;
-    rc = make_tmap_2d(&ta_lo, rows_lo, g.row_len, rows_total, (uint64_t)g.row_len * 4, kBK, kBM, 128);
+  const int E = half ? 2 : 4;
+  rc = make_tmap_2d(&ta, rows_hi, g.row_len, rows_total, (uint64_t)g.row_len * E, bk, kBM, 128, E);
+  if (!rc) rc = make_tmap_2d(&tb, packed_hi, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * E, bk, b_box, 128, E);
+  if (!rc && split) {
+    rc = make_tmap_2d(&ta_lo, rows_lo, g.row_len, rows_total, (uint64_t)g.row_len * E, bk, kBM, 128, E);
     if (!rc)
-      rc = make_tmap_2d(&tb_lo, packed_lo, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * 4, kBK, b_box, 128);
+      rc = make_tmap_2d(&tb_lo, packed_lo, g.hop, (uint64_t)n_groups * kBN, (uint64_t)g.hop * E, bk, b_box, 128, E);
   }
   if (rc) return rc;
   if (!split) {
@@ -537,6 +632,10 @@ static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const 
   p.col_table = col_table;
   p.group_rows = group_rows;
   p.out = out;
+  p.a_exp = exps;
+  if (half)
+    p.b_exp = reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(packed_hi) +
+                                               nnab_cqt_egemm_bank_bytes_prec(n_groups, g.hop, precision) - 256) + 1;
   const int grid = p.ctas_per_group * n_groups;
   if (!pair) {
     const size_t smem = egemm_smem<false>();
@@ -544,8 +643,10 @@ static int cqt_egemm_staged(const nnab_frames* f, const float* packed_hi, const 
                                        (int)smem));
     cqt1992_egemm_kernel<false><<<grid, kThreads, smem, stream>>>(ta, tb, ta_lo, tb_lo, p);
   } else {
-    auto kern = split ? cqt1992_egemm_kernel<true, true> : cqt1992_egemm_kernel<true, false>;
-    const size_t smem = split ? egemm_smem<true, true>() : egemm_smem<true, false>();
+    auto kern = half ? (split ? cqt1992_egemm_kernel<true, true, true> : cqt1992_egemm_kernel<true, false, true>)
+                     : (split ? cqt1992_egemm_kernel<true, true> : cqt1992_egemm_kernel<true, false>);
+    const size_t smem = half ? (split ? egemm_smem<true, true, true>() : egemm_smem<true, false, true>())
+                             : (split ? egemm_smem<true, true>() : egemm_smem<true, false>());
     NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);

@@ -335,6 +335,13 @@ __global__ void pack_dft_bank_f16_kernel(const float* __restrict__ h_re, const f
   }
 }
 
+int launch_bank_absmax(const float* a, const float* b, int64_t n, unsigned int* out, cudaStream_t s) {
+  if (n <= 0) return NNAB_OK;
+  bank_absmax_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(a, b, n, out);
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
 }  // namespace nnab
 
 using namespace nnab;

@@ -52,6 +52,9 @@ inline bool prec_valid(int p) { return p >= NNAB_PREC_TF32 && p <= NNAB_PREC_3XF
 
 int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows_lo, int split,
                  cudaStream_t s);
+// atomicMax of |a|, |b| over n elements into *out as ordered float bits (the FP16 bank
+// packers' peak; *out zeroed by the caller) (frames.cu)
+int launch_bank_absmax(const float* a, const float* b, int64_t n, unsigned int* out, cudaStream_t s);
 // FP16 hop rows scaled per clip by 2^exps[b] (frames.cu)
 int stage_frames_f16(const FrameGeom& g, const float* x, void* rows_hi, void* rows_lo, int32_t* exps, int split,
                      cudaStream_t s);

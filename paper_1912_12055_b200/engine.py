@@ -332,9 +332,14 @@ class CqtLongEngine:
     def __init__(self, kernels, hop: int, pad_mode: str = "reflect", precision: str = "tf32", device="cuda",
                  dense: bool = False, method: str = "hybrid"):
         self.device = _require_cuda(device)
-        if precision not in ("tf32", "fp32", "3xtf32"):
-            raise ValueError("CQT1992v2 precision must be 'tf32' or 'fp32' (3xTF32)")
+        if precision not in L.PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(L.PRECISIONS)}")
+        # "fp32": 3xF16 on the hybrid (E-GEMM + schedule), 3xTF32 for the other methods
         self.precision = L.PRECISIONS[precision]
+        if precision == "fp32" and method == "hybrid" and not dense and int(hop) == 512:
+            self.precision = L.PREC_3XF16
+        if self.precision in (L.PREC_F16, L.PREC_3XF16) and (method != "hybrid" or dense or int(hop) != 512):
+            raise ValueError("FP16 operand modes run the hybrid CQT1992v2 (hop 512)")
         k = np.asarray(kernels)
         self.n_bins, self.width = int(k.shape[0]), int(k.shape[1])
         self.hop, self.pad_mode = int(hop), pad_mode
@@ -350,16 +355,17 @@ class CqtLongEngine:
         """Per-K-block schedule + packed bank of the rows in dr/di (device) with supports sup."""
         lib = L.load()
         nb = int(sup.shape[0])
-        cap = lib.nnab_cqt_bank_tiles(nb) * (((self.width + 31) // 32 * 32) // 16) + 16
+        cap = lib.nnab_cqt_bank_tiles(nb) * (((self.width + 63) // 64 * 64) // 16) + 16
         tab = np.zeros(cap, dtype=np.uint32)
         n_ent = C.c_int32()
         L.check(lib.nnab_cqt_schedule(np.ascontiguousarray(sup).ctypes.data, nb, self.width, self.precision,
                                       tab.ctypes.data, C.byref(n_ent)), "cqt_schedule")
         tiles = lib.nnab_cqt_bank_tiles(nb)
         schedule = torch.from_numpy(tab[: tiles * n_ent.value].astype(np.int32)).to(self.device)
-        n = lib.nnab_cqt_bank_bytes(nb, self.width) // 4
+        n = lib.nnab_cqt_bank_bytes_prec(nb, self.width, self.precision) // 4
         hi = torch.empty(n, dtype=torch.float32, device=self.device)
-        lo = torch.empty(n, dtype=torch.float32, device=self.device) if self.precision == L.PREC_3XTF32 else None
+        lo = (torch.empty(n, dtype=torch.float32, device=self.device)
+              if self.precision in (L.PREC_3XTF32, L.PREC_3XF16) else None)
         L.check(lib.nnab_pack_cqt_bank(dr.data_ptr(), di.data_ptr(), nb, self.width, self.precision, hi.data_ptr(),
                                        L.ptr(lo), L.stream_handle(self.device)), "pack_cqt_bank")
         return schedule, n_ent.value, hi, lo
@@ -407,10 +413,10 @@ class CqtLongEngine:
             col_t = torch.from_numpy(ct[: n * 256].view(np.int16).copy()).to(self.device)
             rows_t = torch.from_numpy(gr[: n * 64].copy()).to(self.device)
             runs_t = torch.from_numpy(rt[: n * 4 * 65].view(np.int32).copy()).to(self.device)
-            nb = lib.nnab_cqt_egemm_bank_bytes(n, self.hop) // 4
+            nb = lib.nnab_cqt_egemm_bank_bytes_prec(n, self.hop, self.precision) // 4
             bank = torch.empty(nb, dtype=torch.float32, device=self.device)
             bank_lo = (torch.empty(nb, dtype=torch.float32, device=self.device)
-                       if self.precision == L.PREC_3XTF32 else None)
+                       if self.precision in (L.PREC_3XTF32, L.PREC_3XF16) else None)
             L.check(lib.nnab_pack_cqt_egemm(dr.data_ptr(), di.data_ptr(), self.width, self.hop, col_t.data_ptr(),
                                             rows_t.data_ptr(), n, self.precision, bank.data_ptr(), L.ptr(bank_lo),
                                             L.stream_handle(self.device)), "pack_cqt_egemm")

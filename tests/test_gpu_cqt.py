@@ -9,7 +9,7 @@ from oracle import spectro_oracle as O
 
 pytestmark = pytest.mark.gpu
 SR = 44100.0
-TOL = {"tf32": 1e-3, "fp32": 1e-5}
+TOL = {"tf32": 1e-3, "f16": 1e-3, "fp32": 1e-5, "3xtf32": 1e-5}
 
 
 def long_engine(cfg, precision, **kw):
@@ -25,7 +25,7 @@ def rec_engine(cfg, precision="fp32"):
                          cfg.bins_per_octave, cfg.n_bins, cfg.pad_mode, precision=precision)
 
 
-@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("precision", ["tf32", "f16", "fp32", "3xtf32"])
 def test_cqt1992v2_full_config_golden(golden, cuda_dev, precision):
     eng = long_engine(O.CqtCfg(sr=SR), precision)
     x = torch.from_numpy(golden["clips"]).to(cuda_dev)
@@ -281,3 +281,22 @@ print(max(errs))
     r = subprocess.run([sys.executable, "-c", code, root, out], env=env, capture_output=True, text=True, cwd=root)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= 1e-3
+
+
+@pytest.mark.parametrize("precision", ["f16", "fp32"])
+def test_cqt1992v2_f16_modes_small_and_ragged(golden, cuda_dev, precision):
+    """FP16-operand hybrid (f16, and fp32 = 3xF16): other banks, ragged lengths, a batch
+    mixing amplitudes 1e-6 .. 1e4 (per-clip scales) against the oracle."""
+    from paper_1912_12055_b200.engine import CqtLongEngine
+    for cfg, n in [(O.CqtCfg(sr=22050.0, fmin=55.0, n_bins=48, hop_length=512), 22050),
+                   (O.CqtCfg(sr=44100.0, fmin=65.4, n_bins=60, hop_length=512), 50001)]:
+        kern, _ = O.cqt_time_bank(cfg)
+        eng = CqtLongEngine(kern, 512, "reflect", precision=precision)
+        assert eng.hybrid is not None
+        rng = np.random.default_rng(21)
+        amps = [1e-6, 1.0, 1e4]
+        x = np.stack([rng.standard_normal(n) * a for a in amps]).astype(np.float32)
+        got = eng.forward(torch.from_numpy(x).to(cuda_dev)).cpu().numpy()
+        for i in range(len(amps)):
+            ref = O.cqt1992v2_clip(x[i].astype(np.float64), kern, 512)
+            assert O.peak_err(got[i], ref) <= TOL[precision], (cfg.n_bins, i, O.peak_err(got[i], ref))

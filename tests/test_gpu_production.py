@@ -92,7 +92,7 @@ def test_stft_mel_full_batch(golden, batch, xdev, precision, kind, power):
         assert np.array_equal(host.numpy(), got)
 
 
-@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("precision", ["tf32", "f16", "fp32", "3xtf32"])
 def test_cqt1992v2_full_batch(golden, batch, xdev, precision):
     from paper_1912_12055_b200.engine import CqtLongEngine
     cfg = O.CqtCfg(sr=SR)
