@@ -46,7 +46,7 @@
 namespace nnab {
 namespace {
 
-constexpr int kBM = 128, kBN = 256, kBK = 32, kThreads = 256;
+constexpr int kBM = 128, kBN = 256, kBK = 32, kThreads = 384;
 constexpr int kA = kBM * kBK * 4;  // 16 KB A tile per stage
 constexpr int kRows = 16;   // D rows (bank rows: 2 per bin) per group
 constexpr int kRing = 256;  // D ring length (slots, power of two); >= 128 + max r
@@ -56,7 +56,7 @@ constexpr int kWin = 16;  // a row's columns come in windows of 16 consecutive r
 constexpr int kChunk = 64;  // run-table granularity (host plan only)
 constexpr int kChunks = kBN / kChunk;
 constexpr int kRunSlots = kChunk + 1;  // per chunk: count, then up to 64 runs
-constexpr int kEpi = 128;  // warps 4-7: TMEM readers and reducers
+constexpr int kEpi = 256;  // warps 4-11: TMEM readers and reducers (two per TMEM lane quarter)
 
 struct EParams {
   int64_t B;
@@ -79,7 +79,7 @@ NNAB_DEV uint64_t sdesc(const void* p) {  // K-major, 128-byte swizzle, 8-row at
   return d;
 }
 
-NNAB_DEV void ep_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // epilogue warps 4-7
+NNAB_DEV void ep_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // epilogue warps 4-11
 
 // Pipeline geometry: single CTAs stage A (16 KB) + all of B (32 KB) x 3; a CTA
 // pair (kPair) stages A + half of B (16 + 16 KB) x 4; 3xTF32 (kSplit, pairs)
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kPair ? 8 : 4);  // pair: the leader's counts both CTAs' epilogue warps
+      mbar_init(&tempty[i], kPair ? 16 : 8);  // one per epilogue warp (pair: of both CTAs)
     }
     fence_barrier_init();
   }
@@ -259,7 +259,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // consecutive D rows, so every add is a conflict-free shared-memory RMW
       // and no two threads ever touch the same element (no atomics).  Rows that
       // can receive nothing more are summed over the four rings and emitted.
-      const int q = warp - 4, et = threadIdx.x - 128;  // et: 0 .. 127
+      // Two warps per TMEM lane quarter: part 0 takes the windows of even bank rows (Re),
+      // part 1 those of odd rows (Im), so no two warps ever update the same ring row.
+      const int q = (warp - 4) & 3, part = (warp - 4) >> 2, et = threadIdx.x - 128;  // et: 0 .. 255
       float* myring = ring + q * (kRows * kRing);
       int acc = 0;
       uint32_t aph = 0;
@@ -274,43 +276,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * kBN;
         const int s_row = m * kBM + q * 32 + lane;  // this thread's E row (global slot)
+        // The plan lays each bank row's columns out as whole windows of 16
+        // consecutive r (zero-weight padding past the support).  Column k of a
+        // window (row, r0 + k): lane l gathers E[s_l + k][k] from lane (l + k) mod
+        // 32 -- pairs whose source lane did not wrap all belong to D row s_l - r0,
+        // the wrapped ones to s_l - 32 - r0 -- so a window costs 16 shuffles and
+        // two read-modify-writes per lane, cells distinct across lanes.
 #pragma unroll 1
-        for (int c0 = 0; c0 < n_cols; c0 += 32) {
-          float v[32];
-          tmem_ld32(ta + c0, v);
+        for (int c0 = 0; c0 < n_cols; c0 += 16) {
+          const uint32_t meta = cols[c0];  // warp-uniform
+          if (((meta >> 8) & 1) != (uint32_t)part) continue;
+          float v[16];
+          tmem_ld16(ta + c0, v);
           if (kSplit) {
-            float u[32];
-            tmem_ld32(ta + kBN + c0, u);
+            float u[16];
+            tmem_ld16(ta + kBN + c0, u);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += u[j];
+            for (int j = 0; j < 16; ++j) v[j] += u[j];
           } else {
             tmem_ld_wait();
           }
-          // The plan lays each bank row's columns out as whole windows of 16
-          // consecutive r (zero-weight padding past the support).  Column k of a
-          // window (row, r0 + k): lane l gathers E[s_l + k][k] from lane (l + k) mod
-          // 32 -- pairs whose source lane did not wrap all belong to D row s_l - r0,
-          // the wrapped ones to s_l - 32 - r0 -- so a window costs 16 shuffles and
-          // two read-modify-writes per lane, cells distinct across lanes.
+          const int r0 = (int)(meta & 0xFF);
+          float* rrow = myring + (meta >> 8) * kRing;
+          float h4[4] = {0.f, 0.f, 0.f, 0.f}, l4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 chains: ILP over the adds
 #pragma unroll
-          for (int w16 = 0; w16 < 2; ++w16) {
-            const uint32_t meta = cols[c0 + 16 * w16];  // warp-uniform
-            if (meta == kUnused) break;
-            const int r0 = (int)(meta & 0xFF);
-            float* rrow = myring + (meta >> 8) * kRing;
-            float h4[4] = {0.f, 0.f, 0.f, 0.f}, l4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 chains: ILP over the adds
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float x = __shfl_sync(0xffffffffu, v[16 * w16 + k], (lane + k) & 31);
-              if (lane + k < 32) h4[k & 3] += x;
-              else l4[k & 3] += x;
-            }
-            const float hi = (h4[0] + h4[1]) + (h4[2] + h4[3]), lo = (l4[0] + l4[1]) + (l4[2] + l4[3]);
-            rrow[(s_row - r0) & (kRing - 1)] += hi;
-            rrow[(s_row - 32 - r0) & (kRing - 1)] += lo;
-            __syncwarp();  // the next window's cells overlap other lanes' cells of this one
+          for (int k = 0; k < 16; ++k) {
+            const float x = __shfl_sync(0xffffffffu, v[k], (lane + k) & 31);
+            if (lane + k < 32) h4[k & 3] += x;
+            else l4[k & 3] += x;
           }
+          const float hi = (h4[0] + h4[1]) + (h4[2] + h4[3]), lo = (l4[0] + l4[1]) + (l4[2] + l4[3]);
+          rrow[(s_row - r0) & (kRing - 1)] += hi;
+          rrow[(s_row - 32 - r0) & (kRing - 1)] += lo;
+          __syncwarp();  // the next window's cells overlap other lanes' cells of this one
         }
         tc_fence_before();
         __syncwarp();
