@@ -246,6 +246,139 @@ __global__ void __launch_bounds__(1024, 1) stage_rows_f16_kernel(const float* __
   }
 }
 
+// FP16 staging that reads each clip from HBM once: a cluster of two CTAs (two SMs) per
+// clip, each holding half of it in shared memory (bulk copies); the clip's peak is the max
+// of the two halves' (exchanged through distributed shared memory); each CTA then writes
+// half of the clip's hop rows, reading its sources from its own half or, near the split
+// and for reflected samples, from the peer's (ld.shared::cluster).  Hop-row layouts with
+// halves up to kPairHalf samples; else the two-pass kernel above.
+constexpr int kPairHalf = 54 * 1024;  // floats per CTA (216 KB)
+
+NNAB_DEV float ld_cluster_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(1024, 1) stage_rows_f16_pair_kernel(
+    const float* __restrict__ x, int64_t B, int64_t L, int32_t pad, int32_t mode, int32_t hop, int32_t R,
+    int64_t padded_len, int split, __half* __restrict__ hi, __half* __restrict__ lo, int32_t* __restrict__ exps) {
+  extern __shared__ __align__(128) float sx[];  // this CTA's half of the clip
+  __shared__ float red[32];
+  __shared__ float half_max[2];                  // [clip parity]: this CTA's peak, read by the peer
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
+  const int64_t L2 = (L / 2) & ~int64_t(3);
+  const int64_t h0 = rank ? L2 : 0, h1 = rank ? L : L2, hn = h1 - h0;
+  const uint32_t peer_sx = mapa(sx, peer);
+  const bool bulk = (L % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t q_total = (int64_t)R * hop;                 // staged elements per clip (row_len = hop)
+  const int64_t qh = ((q_total / 2) & ~int64_t(3));          // CTA 0 writes [0, qh), CTA 1 [qh, q_total)
+  const int64_t q0 = rank ? qh : 0, q1 = rank ? q_total : qh;
+  uint32_t phase = 0;
+  int it = 0;
+  for (int64_t b = cluster_id_x(); b < B; b += nclusters_x(), ++it) {
+    const float* xb = x + b * L;
+    // ---- load this CTA's half
+    if (bulk) {
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar, (uint32_t)(hn * 4));
+        for (int64_t o = 0; o < hn * 4; o += 32768) {
+          const uint32_t n = (uint32_t)(hn * 4 - o < 32768 ? hn * 4 - o : 32768);
+          bulk_load(reinterpret_cast<char*>(sx) + o, reinterpret_cast<const char*>(xb + h0) + o, n, &bar);
+        }
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+    } else {
+      for (int64_t i = threadIdx.x; i < hn; i += blockDim.x) sx[i] = __ldg(xb + h0 + i);
+      __syncthreads();
+    }
+    // ---- the clip's peak: this half's, then the max with the peer's
+    float mx = 0.f;
+    for (int64_t i = threadIdx.x; i < hn; i += blockDim.x) mx = fmaxf(mx, fabsf(sx[i]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (threadIdx.x == 0) half_max[it & 1] = m;
+    }
+    cluster_sync();  // both halves loaded and both peaks published
+    const float pk = fmaxf(half_max[it & 1], ld_cluster_f32(mapa(&half_max[it & 1], peer)));
+    const int e = f16_scale_exp(pk);
+    if (rank == 0 && threadIdx.x == 0) exps[b] = e;
+    const float sc = ldexpf(1.f, e);
+    // ---- write staged elements [q0, q1): padded position q -> source sample j
+    auto src = [&](int64_t j) -> float {
+      if (j >= h0 && j < h1) return sx[j - h0];
+      return ld_cluster_f32(peer_sx + (uint32_t)((j - (rank ? 0 : L2)) * 4));
+    };
+    uint2* hrow = reinterpret_cast<uint2*>(hi + b * q_total);
+    uint2* lrow = reinterpret_cast<uint2*>(lo + b * q_total);
+    const int li0 = (int)h0, li1 = (int)h1, lpad = pad, lL = (int)L, lpl = (int)padded_len;
+    for (int g4 = (int)(q0 / 4) + threadIdx.x; g4 < (int)(q1 / 4); g4 += blockDim.x) {
+      float v[4];
+      const int j0 = 4 * g4 - lpad;  // source of the group's first element (interior)
+      if (j0 >= li0 && j0 + 3 < li1 && 4 * g4 + 3 < lpl) {  // interior of this half: smem only
+        const int a = j0 - li0;
+        if ((a & 3) == 0) {
+          const float4 w = *reinterpret_cast<const float4*>(sx + a);
+          v[0] = w.x;
+          v[1] = w.y;
+          v[2] = w.z;
+          v[3] = w.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = sx[a + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] *= sc;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = 4 * g4 + u;
+          float sv = 0.f;
+          if (q < lpl) {
+            int j = q - lpad;
+            if (mode == NNAB_PAD_REFLECT) {
+              if (j < 0) j = -j;
+              if (j >= lL) j = 2 * (lL - 1) - j;
+              sv = src(j);
+            } else if (j >= 0 && j < lL) {
+              sv = src(j);
+            }
+          }
+          v[u] = sv * sc;
+        }
+      }
+      __half2 h01 = __floats2half2_rn(v[0], v[1]), h23 = __floats2half2_rn(v[2], v[3]);
+      uint2 hv;
+      hv.x = *reinterpret_cast<uint32_t*>(&h01);
+      hv.y = *reinterpret_cast<uint32_t*>(&h23);
+      hrow[g4] = hv;
+      if (split) {
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        __half2 l01 = __floats2half2_rn(v[0] - f01.x, v[1] - f01.y);
+        __half2 l23 = __floats2half2_rn(v[2] - f23.x, v[3] - f23.y);
+        uint2 lv;
+        lv.x = *reinterpret_cast<uint32_t*>(&l01);
+        lv.y = *reinterpret_cast<uint32_t*>(&l23);
+        lrow[g4] = lv;
+      }
+    }
+    cluster_sync();  // the peer is done reading this half before the next clip overwrites it
+  }
+}
+
 int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows_lo, int split, cudaStream_t s) {
   const int64_t rows = g.B * (int64_t)g.R;
   if (rows == 0) return NNAB_OK;
@@ -259,6 +392,30 @@ int stage_frames(const FrameGeom& g, const float* x, float* rows_hi, float* rows
 int stage_frames_f16(const FrameGeom& g, const float* x, void* rows_hi, void* rows_lo, int32_t* exps, int split,
                      cudaStream_t s) {
   if (g.B == 0) return NNAB_OK;
+  if (g.row_len == g.hop && (g.L - ((g.L / 2) & ~int64_t(3))) <= kPairHalf && num_sms() >= 2 &&
+      (int64_t)g.R * g.hop % 8 == 0) {
+    // read once: clip halves in the shared memory of a two-CTA cluster
+    const int64_t half = g.L - ((g.L / 2) & ~int64_t(3));
+    const size_t smem = (size_t)half * 4;
+    auto kern = stage_rows_f16_pair_kernel;
+    NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(g.B, num_sms() / 2)));
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    NNAB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, x, g.B, g.L, g.pad, g.pad_mode, g.hop, g.R, g.padded_len, split,
+                                     reinterpret_cast<__half*>(rows_hi), reinterpret_cast<__half*>(rows_lo), exps));
+    NNAB_LAUNCHED();
+    return NNAB_OK;
+  }
   // one clip per CTA at a time, one CTA per SM: 148 clips (47 MB) in flight, so pass 2
   // re-reads each clip from L2 (two CTAs per SM thrashed L2: 960 MB of DRAM reads, ncu)
   const int blocks = (int)std::min<int64_t>(g.B, (int64_t)num_sms());
