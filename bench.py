@@ -98,15 +98,46 @@ def load_traffic():
 
 # ------------------------------------------------------------------ clocks
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+    """SM clocks and throttle reasons sampled DURING the timed region (B200_PROFILING.md
+    recipe): an NVML thread polling every 2 ms (the timed regions are tens of ms, shorter
+    than nvidia-smi's first sample), falling back to `nvidia-smi -lms 25`."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
-        self.index, self.proc, self.path = index, None, f"/tmp/nnab_clocks_{os.getpid()}.csv"
+        self.index, self.proc, self.path, self.thread = index, None, f"/tmp/nnab_clocks_{os.getpid()}.csv", None
+        self.samples, self.reasons, self.max_mhz = [], set(), 0.0
 
     def start(self):
+        try:
+            import threading
+
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            self.stop_flag = False
+
+            def run():
+                while not self.stop_flag:
+                    self.samples.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for n, bit in bits.items():
+                        if r & bit:
+                            self.reasons.add(n)
+                    time.sleep(0.002)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -116,6 +147,13 @@ class Clocks:
             self.proc = None
 
     def stop(self):
+        if self.thread is not None:
+            self.stop_flag = True
+            self.thread.join(timeout=2)
+            if not self.samples:
+                return None
+            return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                    "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "NVML, 2 ms"}
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -125,7 +163,6 @@ class Clocks:
             self.proc.kill()
         self.f.close()
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:
             for line in f:
                 parts = [p.strip() for p in line.split(",")]
@@ -136,29 +173,14 @@ class Clocks:
                     mx = max(mx, float(parts[1]))
                 except ValueError:
                     continue
-                for n, v in zip(names, parts[2:]):
+                for n, v in zip(self.NAMES, parts[2:]):
                     if v.lower().startswith("active"):
                         reasons.add(n)
         os.unlink(self.path)
-        note = None
-        if not sm:  # timed region shorter than nvidia-smi's first sample: one query right after it
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=10).stdout
-                parts = [p.strip() for p in out.strip().split(",")]
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-                for n, v in zip(names, parts[2:]):
-                    if v.lower().startswith("active"):
-                        reasons.add(n)
-                note = "timed region shorter than the 100 ms sampler: one sample right after it"
-            except Exception:
-                return None
-        d = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
-        if note:
-            d["note"] = note
-        return d
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi -lms 25"}
 
 
 # ------------------------------------------------------------------ workloads
@@ -239,7 +261,7 @@ L2_BYTES = 126 * 1024 * 1024
 _flush_buf = None
 
 
-def run_timed(eng, kind, x, steps, warmup, torch, stream, time_gemm=True, barrier=None):
+def run_timed(eng, kind, x, steps, warmup, torch, stream, time_gemm=True, barrier=None, on_start=None):
     """W untimed steps then exactly K timed steps; events around each step and
     around the GEMM launch inside it (for the roofline).  When the input is
     smaller than 2x L2 (a rank's shard at N >= 4) a 256 MB buffer is written
@@ -255,6 +277,8 @@ def run_timed(eng, kind, x, steps, warmup, torch, stream, time_gemm=True, barrie
     if barrier is not None:
         barrier()
     torch.cuda.synchronize()
+    if on_start is not None:  # e.g. the clock sampler: the timed region starts here
+        on_start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     g_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for i in range(steps):
@@ -488,11 +512,10 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    if rank == 0:
-        clocks.start()
     n0 = _lib.load().nnab_launch_count()
     ms, gemm_ms = run_timed(eng, kind, x, args.steps, args.warmup, torch, stream, time_gemm=staged,
-                            barrier=(dist.barrier if world > 1 else None))
+                            barrier=(dist.barrier if world > 1 else None),
+                            on_start=(clocks.start if rank == 0 else None))
     launches_total = _lib.load().nnab_launch_count() - n0  # includes the W warm-up steps
     launches = launches_total * args.steps // (args.steps + args.warmup)
     ck = clocks.stop() if rank == 0 else None
