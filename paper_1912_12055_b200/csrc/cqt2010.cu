@@ -294,15 +294,15 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
     // launches and one CONV launch over all octaves and clips, through workspace level buffers):
     // equal speed today (0.73 ms) -- its front is the fused kernel's stage 1-2, and its per-tile
     // build / MMA / epilogue chain is still latency-bound
-    static const bool levels = [] {
+    static const int levels = [] {
       const char* e = getenv("NNAB_CQT2010_LEVELS");
-      return e && e[0] == '1';
+      return e && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
     }();
     int rc = NNAB_ENOTSUP;
     if (levels && workspace)
       rc = launch_cqt2010_levels(x, B, L, taps, n_taps, k_re, k_im, n_filters, width, early_stages, n_octaves,
                                  kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind, T, out, workspace,
-                                 workspace_bytes, s);
+                                 workspace_bytes, s, levels);
     if (rc == NNAB_ENOTSUP)
       rc = launch_cqt2010_tc(x, B, L, taps, n_taps, k_re, k_im, n_filters, width, early_stages, n_octaves,
                              kernel_hop, first_bin, bins_per_octave, n_bins, pad_mode, out_kind, T, out, s);

@@ -79,6 +79,11 @@ struct TcParams {
   __half* lv0;
   int32_t* lv_exp;
   int32_t lv0_stride;
+  // lv_mode 2 ("no-conv"): the kernel also runs the halvings and writes every octave to
+  // lv[a] (stride lv_stride[a]); the convs of all octaves then run as one batched launch
+  int32_t lv_mode;
+  __half* lv[kMaxOct];
+  int32_t lv_stride[kMaxOct];
   // shared-memory carve-up (bytes from the 1 KB-aligned base)
   int32_t off_toep, off_filt, off_ring, off_x, off_xe, off_y, off_ye, off_col, off_stage, off_bars;
   int32_t pl_x, pl_y, y_rows;          // plane strides (bytes); stage-2 plane rows
@@ -521,7 +526,15 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
         issue_fir(c, yp_s, p.pl_y, 0, 0);
         if (p.oct_blocks[0] > 128) issue_fir(c, yp_s, p.pl_y, p.oct_blocks[0] - 128, 128);
         mma_commit(&bars[0]);
-        if (p.lv0) continue;  // front-only: the octave levels run as batched kernels
+        if (p.lv0) {  // the octave levels (mode 1) or just the convs (mode 2) run as batched kernels
+          if (p.lv_mode == 2)
+            for (int a = 0; a + 1 < p.n_oct; ++a) {
+              wait_fir();
+              issue_fir(c, smem_u32(base + p.o_off[a]), (uint32_t)p.plane_rows[a] * 16u, 0, 0);
+              mma_commit(&bars[0]);
+            }
+          continue;
+        }
         for (int a = 0; a < p.n_oct; ++a) {
           if (a + 1 < p.n_oct) {
             wait_fir();
@@ -670,6 +683,48 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_tc_kernel(const __grid_co
           *reinterpret_cast<uint4*>(dst + 8 * k8) = v;
         }
         if (tid == 0) p.lv_exp[b] = ex;
+        csync();
+        if (p.lv_mode != 2) continue;
+        // no-conv mode: the halvings, each octave to its level buffer
+        for (int a = 0; a + 1 < p.n_oct; ++a) {
+          if (tid == 0) mbar_arrive(&bars[6]);  // octave a's planes are ready: the issue warp runs the FIR
+          c.wait_mma();
+          const __half* sp = sig(a);
+          __half* sd = sig(a + 1);
+          uint8_t* po = planes_of(a + 1);
+          const uint32_t pl_out = (uint32_t)p.plane_rows[a + 1] * 16u;
+          const int n_out = p.oct_len[a + 1];
+          fir_epilogue(
+              c, 0, 0, n_out, 0, p.h0,
+              [&](int i0, float* cv) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint4 w = ld8(sp, ML + 2 * i0 + 8 * kk);
+                  const __half2* h2 = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) cv[4 * kk + u] = __low2float(h2[u]);
+                }
+              },
+              [&](int i) { return __half2float(sp[sw(ML + 2 * i)]); }, out16_of(sd, po, pl_out, p.plane_rows[a + 1]),
+              out1_of(sd, po, pl_out, p.plane_rows[a + 1]));
+          tc_fence_before();
+          csync();
+          edge_pass(sd, po, pl_out, p.plane_rows[a + 1], n_out);
+          fence_proxy_async_smem();
+          csync();
+          const int nv = n_out + 2 * ML;
+          __half* dst = p.lv[a + 1] + b * (int64_t)p.lv_stride[a + 1];
+          for (int k8 = tid; k8 < p.lv_stride[a + 1] / 8; k8 += kCompute) {
+            uint4 v = ld8(sd, 8 * k8);
+            if (8 * k8 + 8 > nv) {
+              __half* hv = reinterpret_cast<__half*>(&v);
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (8 * k8 + e >= nv) hv[e] = __float2half(0.f);
+            }
+            *reinterpret_cast<uint4*>(dst + 8 * k8) = v;
+          }
+        }
         csync();
         continue;
       }
@@ -1235,7 +1290,7 @@ size_t cqt2010_levels_bytes(int64_t B, int64_t L, const float* taps, int n_taps,
 int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, const float* k_re,
                           const float* k_im, int n_filt, int width, int early_stages, int n_oct, int kernel_hop,
                           int first_bin, int bpo, int n_bins, int pad_mode, int out_kind, int T, float* out,
-                          void* workspace, size_t workspace_bytes, cudaStream_t st) {
+                          void* workspace, size_t workspace_bytes, cudaStream_t st, int mode) {
   Plan pl;
   int rc = make_plan(L, n_taps, taps, n_filt, width, early_stages, n_oct, kernel_hop, T, pad_mode, &pl);
   if (rc) return rc;
@@ -1263,6 +1318,11 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
   p.lv0 = reinterpret_cast<__half*>(ws + lp.off[0]);
   p.lv_exp = exps;
   p.lv0_stride = lp.stride[0];
+  p.lv_mode = mode;
+  for (int a = 0; a < n_oct; ++a) {
+    p.lv[a] = reinterpret_cast<__half*>(ws + lp.off[a]);
+    p.lv_stride[a] = lp.stride[a];
+  }
   NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   cqt2010_tc_kernel<<<(int)std::min<int64_t>(B, (int64_t)num_sms()), kThreads, pl.smem, st>>>(p);
   NNAB_LAUNCHED();
@@ -1301,8 +1361,9 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
     q.lv_stride[a] = lp.stride[a];
     q.lv_n[a] = lp.n[a];
   }
-  // the halvings octave by octave, then every octave's conv in one launch
-  for (int a = 0; a < n_oct; ++a) {
+  // the halvings octave by octave (mode 1; mode 2 ran them in the fused kernel), then every
+  // octave's conv in one launch
+  for (int a = 0; a < n_oct && mode == 1; ++a) {
     q.src = reinterpret_cast<const __half*>(ws + lp.off[a]);
     q.src_stride = lp.stride[a];
     q.n_src = lp.n[a];

@@ -134,6 +134,6 @@ size_t cqt2010_levels_bytes(int64_t B, int64_t L, const float* taps, int n_taps,
 int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, const float* k_re,
                           const float* k_im, int n_filt, int width, int early_stages, int n_oct, int kernel_hop,
                           int first_bin, int bpo, int n_bins, int pad_mode, int out_kind, int T, float* out,
-                          void* workspace, size_t workspace_bytes, cudaStream_t st);
+                          void* workspace, size_t workspace_bytes, cudaStream_t st, int mode);
 
 }  // namespace nnab
