@@ -289,14 +289,15 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
   if (B == 0) return NNAB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (precision == NNAB_PREC_TF32) {  // tensor-core chain (FP16 operands) when the clip fits in shared memory
-    // default: the single fused kernel (each clip's whole chain on one SM).  NNAB_CQT2010_LEVELS=1
-    // selects the batched path (per-clip front for stages 1-2, then level-synchronous HALVE
-    // launches and one CONV launch over all octaves and clips, through workspace level buffers):
-    // equal speed today (0.73 ms) -- its front is the fused kernel's stage 1-2, and its per-tile
-    // build / MMA / epilogue chain is still latency-bound
+    // default (NNAB_CQT2010_LEVELS unset or 2): the fused kernel runs stages 1-2 and the
+    // halvings per clip and writes every octave's signal to workspace level buffers; one
+    // batched launch then runs the 12-bin convs of all octaves and clips (0.68 ms vs 0.74 ms
+    // with the convs inside the fused kernel).  0: the single fused kernel with its convs
+    // (also the path without a workspace).  1: fused front for stages 1-2 only, then
+    // level-synchronous HALVE launches and the batched convs (0.73 ms).
     static const int levels = [] {
       const char* e = getenv("NNAB_CQT2010_LEVELS");
-      return e && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
+      return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
     }();
     int rc = NNAB_ENOTSUP;
     if (levels && workspace)

@@ -252,10 +252,12 @@ def test_cqt1992v2_batch_vs_sequential(golden, cuda_dev):
         assert np.array_equal(e.forward(x).cpu().numpy(), whole)
 
 
-def test_cqt2010v2_levels_path_matches_oracle(tmp_path):
-    """The batched CQT2010v2 path (NNAB_CQT2010_LEVELS=1: fused front for stages 1-2,
-    level-synchronous HALVE launches, one CONV launch over all octaves) against the
-    oracle and the default fused kernel, in a subprocess (the switch is read once)."""
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_cqt2010v2_levels_path_matches_oracle(tmp_path, mode):
+    """The CQT2010v2 routes other than the default (fused chain + batched convs):
+    NNAB_CQT2010_LEVELS=0, the single fused kernel with its convs; =1, the fused front for
+    stages 1-2, level-synchronous HALVE launches and one CONV launch over all octaves --
+    against the oracle, in a subprocess (the switch is read once per process)."""
     import os
     import subprocess
     import sys
@@ -277,7 +279,7 @@ np.save(sys.argv[2], got[:4])
 print(max(errs))
 '''
     out = str(tmp_path / "lv.npy")
-    env = dict(os.environ, NNAB_CQT2010_LEVELS="1")
+    env = dict(os.environ, NNAB_CQT2010_LEVELS=mode)
     r = subprocess.run([sys.executable, "-c", code, root, out], env=env, capture_output=True, text=True, cwd=root)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= 1e-3
