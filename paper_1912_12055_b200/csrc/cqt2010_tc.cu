@@ -855,6 +855,20 @@ NNAB_DEV uint4 lv_load8(const __half* row, int i, int lim) {
   if (i >= 0 && i + 8 <= lim && (i & 7) == 0) return __ldg(reinterpret_cast<const uint4*>(row + i));
   return lv_load8_slow(row, i, lim);
 }
+// 8 samples at an EVEN misalignment (the deep octaves' frames at hop 2 / 4): two aligned
+// loads and a word select (explicit selects: no local-memory array)
+NNAB_DEV uint4 lv_load8_even(const __half* row, int i, int lim) {
+  const int a = i & ~7;
+  if ((i & 1) || a < 0 || a + 16 > lim) return lv_load8(row, i, lim);
+  const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(row + a)), w1 = __ldg(reinterpret_cast<const uint4*>(row + a + 8));
+  const int sh = (i & 7) >> 1;
+  uint4 o;
+  o.x = sh == 0 ? w0.x : sh == 1 ? w0.y : sh == 2 ? w0.z : w0.w;
+  o.y = sh == 0 ? w0.y : sh == 1 ? w0.z : sh == 2 ? w0.w : w1.x;
+  o.z = sh == 0 ? w0.z : sh == 1 ? w0.w : sh == 2 ? w1.x : w1.y;
+  o.w = sh == 0 ? w0.w : sh == 1 ? w1.x : sh == 2 ? w1.y : w1.z;
+  return o;
+}
 __device__ __noinline__ uint4 lv_load8_slow(const __half* row, int i, int lim) {
   __align__(16) __half v[8];
   const unsigned short* r16 = reinterpret_cast<const unsigned short*>(row);
@@ -1096,13 +1110,19 @@ __global__ void __launch_bounds__(kLvThreads) cqt2010_conv_kernel(const __grid_c
       const int m = tid & 127, c0 = (tid >> 7) * (KC / 16);
       const int64_t gf = tile * 128 + m;
       const bool ok = gf < n_frames;
-      const int64_t b = ok ? gf / p.T : 0;
-      const int t = ok ? (int)(gf - b * p.T) : 0;
-      const __half* row = lsrc + b * lstride;
+      const int b = ok ? (int)(gf / p.T) : 0;
+      const int t = ok ? (int)(gf - (int64_t)b * p.T) : 0;
+      const __half* row = lsrc + (int64_t)b * lstride;
+      const int i0 = ML - p.pad_al + t * lh + 8 * c0;
       uint4 w[KC / 16];
+      if (ok && (lh & 7) == 0 && i0 >= 0 && i0 + 8 * (KC / 16) <= src_lim) {  // interior, aligned (hop >= 8)
 #pragma unroll
-      for (int u = 0; u < KC / 16; ++u)
-        w[u] = ok ? lv_load8(row, ML - p.pad_al + t * lh + 8 * (c0 + u), src_lim) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < KC / 16; ++u) w[u] = __ldg(reinterpret_cast<const uint4*>(row + i0 + 8 * u));
+      } else {
+#pragma unroll
+        for (int u = 0; u < KC / 16; ++u)
+          w[u] = ok ? lv_load8_even(row, i0 + 8 * u, src_lim) : make_uint4(0, 0, 0, 0);
+      }
 #pragma unroll
       for (int u = 0; u < KC / 16; ++u) *reinterpret_cast<uint4*>(A + (c0 + u) * 2048 + m * 16) = w[u];
     }
@@ -1128,18 +1148,24 @@ __global__ void __launch_bounds__(kLvThreads) cqt2010_conv_kernel(const __grid_c
     tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + 16 * half, v);
     tmem_ld_wait();
     if (gf < n_frames) {
-      const int64_t b = gf / p.T;
-      const int t = (int)(gf - b * p.T);
+      const int b = (int)(gf / p.T);
+      const int t = (int)(gf - (int64_t)b * p.T);
       const float os = ldexpf(1.f, __ldg(p.exps + b) - kFiltLog2);
+      const int64_t obase = ((int64_t)b * p.n_bins + lrow0) * p.T + t;
+      const int j_lo = max(lskip, 8 * half), j_hi = min(p.n_filt, 8 * half + 8);
+      if (p.out_kind == NNAB_OUT_COMPLEX) {
+        for (int j = j_lo; j < j_hi; ++j)
+          reinterpret_cast<float2*>(p.out)[obase + (int64_t)j * p.T] =
+              make_float2(v[2 * (j - 8 * half)] * os, v[2 * (j - 8 * half) + 1] * os);
+      } else {
+        const bool pw = p.out_kind == NNAB_OUT_POWER;
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const int j = 8 * half + jj;
-        if (j < lskip || j >= p.n_filt) continue;
-        const float re = v[2 * jj] * os, im = v[2 * jj + 1] * os;
-        const int64_t o = (b * p.n_bins + lrow0 + j) * (int64_t)p.T + t;
-        if (p.out_kind == NNAB_OUT_COMPLEX) reinterpret_cast<float2*>(p.out)[o] = make_float2(re, im);
-        else if (p.out_kind == NNAB_OUT_POWER) p.out[o] = fmaf(re, re, im * im);
-        else p.out[o] = fast_sqrt(fmaf(re, re, im * im));
+        for (int jj = 0; jj < 8; ++jj) {
+          const int j = 8 * half + jj;
+          if (j < j_lo || j >= j_hi) continue;
+          const float re = v[2 * jj] * os, im = v[2 * jj + 1] * os, q2 = fmaf(re, re, im * im);
+          p.out[obase + (int64_t)j * p.T] = pw ? q2 : fast_sqrt(q2);
+        }
       }
     }
     tc_fence_before();
