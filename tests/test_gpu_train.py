@@ -289,3 +289,30 @@ def test_c_abi_layer_vjp_matches_python_path(cuda_dev, precision, mel):
         ref_h += np.concatenate([gr["h_re"], gr["h_im"]])
         assert O.peak_err(d_x[i].cpu().numpy(), gx) <= TOL_GRAD[precision]
     assert O.peak_err(d_h.cpu().numpy(), ref_h) <= TOL_GRAD[precision]
+
+
+def test_grad_reducer_bucketed_backward_matches(cuda_dev):
+    """The multi-GPU backward path on one GPU: with a dist.GradReducer armed (no process
+    group: its launches are no-ops) the trainable layer's dK GEMM runs as two launches
+    (rows [0, 1024) then the rest) and hands three buckets to the reducer -- the
+    gradients equal the single-launch backward's, and the reducer saw the blocks."""
+    from paper_1912_12055_b200.dist import GradReducer
+    from paper_1912_12055_b200.layers import MelSpectrogram
+    x = torch.randn(3, 20000, device=cuda_dev, generator=torch.Generator(device=cuda_dev).manual_seed(3)) * 0.5
+
+    def grads(armed):
+        m = MelSpectrogram(sr=44100, trainable_mel=True, trainable_STFT=True)
+        red = GradReducer(m)
+        assert len(red.ops) == 1
+        out = m(x)
+        if armed:
+            red.arm()
+        out.backward(torch.ones_like(out) * 1e-3)
+        if armed:
+            red.finish()
+            assert red.buckets == 3  # mel weights, dK rows [0, 1024), dK rows [1024, 2050)
+        return [p.grad.clone() for p in (m.mel_basis, m.h_re, m.h_im)]
+
+    a, b = grads(False), grads(True)
+    for u, v in zip(a, b):
+        assert torch.allclose(u, v, rtol=0, atol=1e-6 * float(u.abs().max())), float((u - v).abs().max())
