@@ -1075,103 +1075,241 @@ __global__ void __launch_bounds__(kLvThreads) cqt2010_halve_kernel(const __grid_
   if (p.prof && threadIdx.x == 0) atomicAdd(p.prof + 5, 1ull);
 }
 
-__global__ void __launch_bounds__(kLvThreads) cqt2010_conv_kernel(const __grid_constant__ LvParams p) {
+// CONV: the complex conv of every octave and clip in one persistent launch, frames as M,
+// the top-octave bank as N = 32 (re/im rows of <= 16 bins), K = 96 taps.  Level a's
+// buffer is laid out as rows of rs = max(h, 8) samples (clip stride U rows, so the rows
+// of all clips form one uniform array): frame (b, u) starts at row g = b U + u and its
+// K window is (row g + k / rs, col k mod rs).  The im2col tile is therefore a handful of
+// bulk copies, no thread touches it:
+//   rs >= 64: taps 0-63 one TMA box (64 cols x 128 rows, 128-byte swizzle), taps 64-95
+//             one box (32 cols, 64-byte swizzle) at row + 64 / rs
+//   rs = 32:  three boxes of 32 cols (64-byte swizzle) at rows g, g + 1, g + 2
+//   rs = 16:  six boxes of 16 cols (32-byte swizzle)
+//   rs = 8:   the rows are the contiguous signal: one 1-D bulk copy of 139 rows, read by
+//             a no-swizzle descriptor with LBO 16 B / SBO 128 B (frame g + 1 = 16 B on)
+// Hops below 8 (the deepest octaves) read C = 8 / h copies of the level shifted by v h
+// samples, frame t = C u + v.  Rows past a clip's T frames are computed and discarded.
+// Warp roles (persistent, one CTA per SM, ring of kConvStages tiles / accumulators):
+//   warp 0    producer (one elected thread)
+//   warp 1    MMA issue (one elected thread) + TMEM allocation
+//   warps 4-19 epilogue, four warpgroups taking tiles in turn: thread = frame (TMEM lane
+//             quarter), magnitude / power / complex of the bins, stores coalesced along T
+constexpr int kConvStages = 8;
+constexpr int kConvEpi = 4;  // epilogue warpgroups
+constexpr int kConvThreads = (4 + 4 * kConvEpi) * 32;
+constexpr int kConvMaps = 16;
+constexpr uint32_t kRows8 = 128 + KC / 8 - 1;  // rs = 8: rows a 128-frame tile reads
+
+struct ConvParams {
+  CUtensorMap map[kConvMaps];       // per (octave, copy): [wide box, narrow box] (rs >= 64) or one
+  int64_t B;
+  int32_t n_oct, T, n_bins, first_bin, bpo, n_filt, out_kind;
+  int32_t copies[kMaxOct], U[kMaxOct], map0[kMaxOct], rs[kMaxOct];
+  int64_t tiles_per_copy[kMaxOct], tile0[kMaxOct + 1];
+  const __half* rows[kMaxOct];      // rs = 8: level base (+ the frame offset), copy stride below
+  int64_t copy_stride[kMaxOct];
+  const int32_t* exps;
+  const uint4* filt_img;
+  float* out;
+};
+
+NNAB_DEV uint64_t swz_desc(uint32_t addr, uint32_t row_bytes) {  // K-major, 32/64/128-byte swizzle
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(((8 * row_bytes) >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(row_bytes == 128 ? 2 : row_bytes == 64 ? 4 : 6) << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __grid_constant__ ConvParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* A = base;
-  uint8_t* filt = base + kConvA;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(filt + KC / 8 * 512);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint8_t* A = base;                                   // kConvStages x kConvA
+  uint8_t* filt = base + kConvStages * kConvA;
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(filt + KC / 8 * 512);  // [S] operands landed (TMA tx)
+  uint64_t* bar_mma = bar_full + kConvStages;                             // [S] MMAs done (commit)
+  uint64_t* bar_tfree = bar_mma + kConvStages;                            // [S] accumulator read (4 warps)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar_tfree + kConvStages);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    mbar_init(bar, 1);
+    for (int s = 0; s < kConvStages; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_mma[s], 1);
+      mbar_init(&bar_tfree[s], 4);
+    }
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc<32>(tslot);
-  for (int j = tid; j < KC / 8 * 32; j += kLvThreads) reinterpret_cast<uint4*>(filt)[j] = __ldg(p.filt_img + j);
+  if (warp == 1) tmem_alloc<32 * kConvStages>(tslot);
+  for (int j = tid; j < KC / 8 * 32; j += kConvThreads) reinterpret_cast<uint4*>(filt)[j] = __ldg(p.filt_img + j);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const int64_t n_frames = p.B * p.T;
-  const int64_t lv_tiles = (n_frames + 127) / 128;  // tiles per octave level
-  const int64_t n_tiles = lv_tiles * p.n_lv;
-  uint32_t phase = 0;
-  for (int64_t tile_all = blockIdx.x; tile_all < n_tiles; tile_all += gridDim.x) {
-    const int lvl = (int)(tile_all / lv_tiles);
-    const int64_t tile = tile_all - lvl * lv_tiles;
-    const __half* lsrc = p.lv[lvl];
-    const int lstride = p.lv_stride[lvl], src_lim = p.lv_n[lvl] + 2 * ML, lh = p.kernel_hop >> lvl;
-    const int lskip = max(0, lvl * p.bpo - p.first_bin), lrow0 = p.first_bin - lvl * p.bpo;
-    // im2col: frame (b, t) tap column kk holds src[b][ML - pad_al + t h + kk]; thread = frame
-    // row m, 6 chunks per thread with all loads in flight before the stores
-    {
-      const int m = tid & 127, c0 = (tid >> 7) * (KC / 16);
-      const int64_t gf = tile * 128 + m;
-      const bool ok = gf < n_frames;
-      const int b = ok ? (int)(gf / p.T) : 0;
-      const int t = ok ? (int)(gf - (int64_t)b * p.T) : 0;
-      const __half* row = lsrc + (int64_t)b * lstride;
-      const int i0 = ML - p.pad_al + t * lh + 8 * c0;
-      uint4 w[KC / 16];
-      if (ok && (lh & 7) == 0 && i0 >= 0 && i0 + 8 * (KC / 16) <= src_lim) {  // interior, aligned (hop >= 8)
-#pragma unroll
-        for (int u = 0; u < KC / 16; ++u) w[u] = __ldg(reinterpret_cast<const uint4*>(row + i0 + 8 * u));
-      } else {
-#pragma unroll
-        for (int u = 0; u < KC / 16; ++u)
-          w[u] = ok ? lv_load8_even(row, i0 + 8 * u, src_lim) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < KC / 16; ++u) *reinterpret_cast<uint4*>(A + (c0 + u) * 2048 + m * 16) = w[u];
+  const int64_t n_tiles = p.tile0[p.n_oct];
+  const int64_t n_local = n_tiles > blockIdx.x ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // tile -> (octave, copy, first row); i only grows, so the octave is tracked incrementally
+  struct Loc {
+    int a = 0;
+    NNAB_DEV void at(const ConvParams& p, int64_t i, int& v, int& row0) {
+      const int k = (int)(blockIdx.x + i * gridDim.x);
+      while (a + 1 < p.n_oct && k >= (int)p.tile0[a + 1]) ++a;
+      const int kl = k - (int)p.tile0[a], tpc = (int)p.tiles_per_copy[a];
+      v = kl / tpc;
+      row0 = (kl - v * tpc) * 128;
     }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      constexpr uint32_t idesc = idesc_f16(128, NCONV);
-      const uint32_t a0 = smem_u32(A), b0 = smem_u32(filt);
-#pragma unroll
-      for (int k = 0; k < KC / 16; ++k)
-        mma_f16(tmem, nsw_desc(a0 + (uint32_t)k * 4096u, 2048, 128), nsw_desc(b0 + (uint32_t)k * 1024u, 512, 128),
-                idesc, k > 0);
-      mma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    // epilogue: thread = frame (lane quarter q), column half -> bins 8 * half .. + 7
-    const int q = warp & 3, half = warp >> 2;
-    const int64_t gf = tile * 128 + q * 32 + lane;
-    float v[16];
-    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + 16 * half, v);
-    tmem_ld_wait();
-    if (gf < n_frames) {
-      const int b = (int)(gf / p.T);
-      const int t = (int)(gf - (int64_t)b * p.T);
-      const float os = ldexpf(1.f, __ldg(p.exps + b) - kFiltLog2);
-      const int64_t obase = ((int64_t)b * p.n_bins + lrow0) * p.T + t;
-      const int j_lo = max(lskip, 8 * half), j_hi = min(p.n_filt, 8 * half + 8);
-      if (p.out_kind == NNAB_OUT_COMPLEX) {
-        for (int j = j_lo; j < j_hi; ++j)
-          reinterpret_cast<float2*>(p.out)[obase + (int64_t)j * p.T] =
-              make_float2(v[2 * (j - 8 * half)] * os, v[2 * (j - 8 * half) + 1] * os);
-      } else {
-        const bool pw = p.out_kind == NNAB_OUT_POWER;
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int j = 8 * half + jj;
-          if (j < j_lo || j >= j_hi) continue;
-          const float re = v[2 * jj] * os, im = v[2 * jj + 1] * os, q2 = fmaf(re, re, im * im);
-          p.out[obase + (int64_t)j * p.T] = pw ? q2 : fast_sqrt(q2);
+  };
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer
+    if (elect_one()) {
+      Loc loc;
+      for (int m = 0; m < kConvMaps; ++m)
+        if (m < p.map0[p.n_oct - 1] + 2) tma_prefetch(&p.map[m]);
+      for (int64_t i = 0; i < n_local; ++i) {
+        const int s = (int)(i % kConvStages);
+        const uint32_t r = (uint32_t)(i / kConvStages);
+        int v, row0;
+        loc.at(p, i, v, row0);
+        const int a = loc.a, rs = p.rs[a];
+        if (r > 0) mbar_wait(&bar_mma[s], (r - 1) & 1);  // the stage's previous MMAs have read it
+        uint8_t* As = A + s * kConvA;
+        const int y = (int)row0;
+        if (rs == 8) {
+          mbar_expect_tx(&bar_full[s], kRows8 * 16);
+          bulk_load(As, p.rows[a] + v * p.copy_stride[a] + (int64_t)8 * row0, kRows8 * 16, &bar_full[s]);
+        } else {
+          mbar_expect_tx(&bar_full[s], (uint32_t)kConvA);
+          const CUtensorMap* map = &p.map[p.map0[a] + v * (rs >= 64 ? 2 : 1)];
+          if (rs >= 64) {
+            tma_load_2d(As, map, &bar_full[s], 0, y);
+            tma_load_2d(As + 16384, map + 1, &bar_full[s], 64 % rs, y + 64 / rs);
+          } else if (rs == 32) {
+            for (int j = 0; j < 3; ++j) tma_load_2d(As + 8192 * j, map, &bar_full[s], 0, y + j);
+          } else {
+            for (int j = 0; j < 6; ++j) tma_load_2d(As + 4096 * j, map, &bar_full[s], 0, y + j);
+          }
         }
       }
     }
-    tc_fence_before();
-    __syncthreads();
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issue
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_f16(128, NCONV);
+      const uint32_t b0 = smem_u32(filt);
+      Loc loc;
+      for (int64_t i = 0; i < n_local; ++i) {
+        const int s = (int)(i % kConvStages);
+        const uint32_t r = (uint32_t)(i / kConvStages);
+        int v, row0;
+        loc.at(p, i, v, row0);
+        const int rs = p.rs[loc.a];
+        mbar_wait(&bar_full[s], r & 1);
+        if (r > 0) mbar_wait(&bar_tfree[s], (r - 1) & 1);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(A + s * kConvA);
+#pragma unroll
+        for (int k = 0; k < KC / 16; ++k) {
+          uint64_t ad;
+          if (rs >= 64) ad = k < 4 ? swz_desc(a0 + 32u * k, 128) : swz_desc(a0 + 16384u + 32u * (k - 4), 64);
+          else if (rs == 32) ad = swz_desc(a0 + 8192u * (k >> 1) + 32u * (k & 1), 64);
+          else if (rs == 16) ad = swz_desc(a0 + 4096u * k, 32);
+          else ad = nsw_desc(a0 + 32u * k, 16, 128);
+          mma_f16(tmem + 32 * s, ad, nsw_desc(b0 + (uint32_t)k * 1024u, 512, 128), idesc, k > 0);
+        }
+        mma_commit(&bar_mma[s]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue: kConvEpi warpgroups
+    // taking tiles in turn; the clip's scale exponent is fetched before the accumulator wait
+    const int q = warp & 3, eg = (warp - 4) >> 2;
+    const int j_hi = min(p.n_filt, NCONV / 2);
+    Loc loc;
+    for (int64_t i = eg; i < n_local; i += kConvEpi) {
+      const int s = (int)(i % kConvStages);
+      const uint32_t r = (uint32_t)(i / kConvStages);
+      int v, row0;
+      loc.at(p, i, v, row0);
+      const int a = loc.a;
+      const int g = row0 + q * 32 + lane;
+      const int b = g / p.U[a];
+      const int t = p.copies[a] * (g - b * p.U[a]) + v;
+      const bool live = b < p.B && t < p.T;
+      const int ex = live ? __ldg(p.exps + b) : 0;
+      mbar_wait(&bar_mma[s], r & 1);
+      tc_fence_after();
+      float acc[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 32 * s, acc);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_tfree[s]);
+      if (!live) continue;
+      const int lskip = max(0, a * p.bpo - p.first_bin), lrow0 = p.first_bin - a * p.bpo;
+      const int eo = ex - kFiltLog2;  // 2^eo without ldexpf's call in the common range
+      const float os = (eo > -126 && eo < 128) ? __int_as_float((eo + 127) << 23) : ldexpf(1.f, eo);
+      const int64_t obase = ((int64_t)b * p.n_bins + lrow0) * p.T + t;
+      if (p.out_kind == NNAB_OUT_COMPLEX) {
+        float2* o2 = reinterpret_cast<float2*>(p.out) + obase;
+#pragma unroll
+        for (int j = 0; j < NCONV / 2; ++j)
+          if (j >= lskip && j < j_hi) o2[j * p.T] = make_float2(acc[2 * j] * os, acc[2 * j + 1] * os);
+      } else {
+        float* o = p.out + obase;
+        const bool pw = p.out_kind == NNAB_OUT_POWER;
+#pragma unroll
+        for (int j = 0; j < NCONV / 2; ++j) {
+          if (j < lskip || j >= j_hi) continue;
+          const float re = acc[2 * j] * os, im = acc[2 * j + 1] * os, q2 = fmaf(re, re, im * im);
+          o[j * p.T] = pw ? q2 : fast_sqrt(q2);
+        }
+      }
+    }
   }
-  if (warp == 0) tmem_dealloc<32>(tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<32 * kConvStages>(tmem);
+}
+
+// The shifted copies of the levels whose hop is below 8 (the conv reads 16-byte rows):
+// copy v of level a, row b = copy 0's row b shifted left by v h samples (zero past it).
+// Thread = 8 output samples: two aligned loads and a word select (v h is even).
+struct CopyParams {
+  const __half* src[kMaxOct];
+  int32_t stride[kMaxOct], h[kMaxOct], copies[kMaxOct];
+  int64_t copy_stride[kMaxOct];
+  int32_t B, n_oct;
+};
+__global__ void cqt2010_copies_kernel(const __grid_constant__ CopyParams p) {
+  for (int a = 0; a < p.n_oct; ++a) {
+    if (p.copies[a] < 2) continue;
+    const int n8 = p.stride[a] >> 3;               // 8-sample units per row
+    const int per = (p.copies[a] - 1) * n8;        // units per clip
+    const int n = p.B * per;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+      const int b = e / per;
+      const int rem = e - b * per;
+      const int v = 1 + rem / n8;
+      const int k8 = rem - (v - 1) * n8;
+      const int sh = v * p.h[a];                   // even
+      const __half* row = p.src[a] + (int64_t)b * p.stride[a];
+      const int i0 = 8 * k8 + sh, al = i0 & ~7;
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      const uint4 w0 = al < p.stride[a] ? __ldg(reinterpret_cast<const uint4*>(row + al)) : z;
+      const uint4 w1 = al + 8 < p.stride[a] ? __ldg(reinterpret_cast<const uint4*>(row + al + 8)) : z;
+      const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      const int q = (i0 & 7) >> 1;
+      uint4 o;
+      o.x = q == 0 ? wd[0] : q == 1 ? wd[1] : q == 2 ? wd[2] : wd[3];
+      o.y = q == 0 ? wd[1] : q == 1 ? wd[2] : q == 2 ? wd[3] : wd[4];
+      o.z = q == 0 ? wd[2] : q == 1 ? wd[3] : q == 2 ? wd[4] : wd[5];
+      o.w = q == 0 ? wd[3] : q == 1 ? wd[4] : q == 2 ? wd[5] : wd[6];
+      *reinterpret_cast<uint4*>(const_cast<__half*>(p.src[a]) + v * p.copy_stride[a] + (int64_t)b * p.stride[a] +
+                                8 * k8) = o;
+    }
+  }
 }
 
 __device__ unsigned long long g_cqt_prof[16];
@@ -1278,12 +1416,14 @@ int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, i
   return NNAB_OK;
 }
 
-// Level buffer geometry of the batched path: one [B][stride] FP16 row set per octave.
+// Level buffer geometry of the batched path: one [B][stride] FP16 row set per octave,
+// stride = U rows of rs = max(h, 8) samples (the conv's TMA rows), plus copies - 1
+// shifted copies when h < 8.
 struct LvPlan {
-  int32_t n[kMaxOct], stride[kMaxOct];
+  int32_t n[kMaxOct], stride[kMaxOct], rs[kMaxOct], U[kMaxOct], copies[kMaxOct], h[kMaxOct];
   size_t off[kMaxOct], exp_off, toep_off, filt_off, total;
 };
-void lv_plan(const TcParams& tp, int64_t B, LvPlan* lp) {
+int lv_plan(const TcParams& tp, int64_t B, LvPlan* lp) {
   size_t off = ((size_t)B * 4 + 255) & ~size_t(255);  // exps first, then the operand images
   lp->exp_off = 0;
   lp->toep_off = off;
@@ -1291,12 +1431,21 @@ void lv_plan(const TcParams& tp, int64_t B, LvPlan* lp) {
   lp->filt_off = off;
   off += (KC / 8 * 512 + 255) & ~255;
   for (int a = 0; a < tp.n_oct; ++a) {
+    const int h = tp.kernel_hop >> a;
+    if (h < 1) return NNAB_ENOTSUP;
+    lp->h[a] = h;
     lp->n[a] = tp.oct_len[a];
-    lp->stride[a] = rnd((int64_t)tp.oct_len[a] + 2 * ML, 8);
+    lp->rs[a] = std::max(h, 8);
+    lp->copies[a] = std::max(1, 8 / h);
+    lp->U[a] = (tp.oct_len[a] + 2 * ML + lp->rs[a] - 1) / lp->rs[a];
+    lp->stride[a] = lp->U[a] * lp->rs[a];
+    if ((int64_t)lp->copies[a] * lp->U[a] < tp.T) return NNAB_ENOTSUP;
     lp->off[a] = off;
-    off += ((size_t)B * lp->stride[a] * 2 + 4096 + 255) & ~size_t(255);  // + slack read as 0-weight operands
+    // + slack read as 0-weight operands (HALVE windows, the conv rows' base offset)
+    off += ((size_t)lp->copies[a] * B * lp->stride[a] * 2 + 4096 + 255) & ~size_t(255);
   }
   lp->total = off;
+  return NNAB_OK;
 }
 
 }  // namespace
@@ -1307,8 +1456,82 @@ size_t cqt2010_levels_bytes(int64_t B, int64_t L, const float* taps, int n_taps,
   Plan pl;
   if (make_plan(L, n_taps, taps, n_filt, width, early_stages, n_oct, kernel_hop, T, pad_mode, &pl)) return 0;
   LvPlan lp;
-  lv_plan(pl.p, B, &lp);
+  if (lv_plan(pl.p, B, &lp)) return 0;
   return lp.total;
+}
+
+// The shifted level copies (hops below 8) and the batched conv of every octave.
+int launch_cqt2010_conv(const LvPlan& lp, char* ws, int64_t B, int T, int n_oct, int n_bins, int first_bin, int bpo,
+                        int n_filt, int pad_al, int out_kind, const int32_t* exps, const uint4* filt_img, float* out,
+                        cudaStream_t st) {
+  CopyParams cp{};
+  bool any_copy = false;
+  if (B * (int64_t)lp.stride[0] * 8 > INT32_MAX) return NNAB_ENOTSUP;
+  cp.B = (int32_t)B;
+  cp.n_oct = n_oct;
+  for (int a = 0; a < n_oct; ++a) {
+    cp.src[a] = reinterpret_cast<const __half*>(ws + lp.off[a]);
+    cp.stride[a] = lp.stride[a];
+    cp.h[a] = lp.h[a];
+    cp.copies[a] = lp.copies[a];
+    cp.copy_stride[a] = B * (int64_t)lp.stride[a];
+    any_copy |= lp.copies[a] > 1;
+  }
+  if (any_copy) {
+    cqt2010_copies_kernel<<<2 * num_sms(), 256, 0, st>>>(cp);
+    NNAB_LAUNCHED();
+  }
+  ConvParams* cv = new ConvParams{};  // > 2 KB of tensor maps: off the host stack
+  ConvParams& c = *cv;
+  c.B = B;
+  c.n_oct = n_oct;
+  c.T = T;
+  c.n_bins = n_bins;
+  c.first_bin = first_bin;
+  c.bpo = bpo;
+  c.n_filt = n_filt;
+  c.out_kind = out_kind;
+  c.exps = exps;
+  c.filt_img = filt_img;
+  c.out = out;
+  int nm = 0;
+  c.tile0[0] = 0;
+  for (int a = 0; a < n_oct; ++a) {
+    const int rs = lp.rs[a];
+    if (rs != 8 && rs != 16 && rs != 32 && rs < 64) return NNAB_ENOTSUP;
+    c.copies[a] = lp.copies[a];
+    c.U[a] = lp.U[a];
+    c.rs[a] = rs;
+    c.map0[a] = nm;
+    c.tiles_per_copy[a] = (B * (int64_t)lp.U[a] + 127) / 128;
+    if (c.tiles_per_copy[a] * 128 >= INT32_MAX) { delete cv; return NNAB_ENOTSUP; }
+    c.tile0[a + 1] = c.tile0[a] + c.tiles_per_copy[a] * lp.copies[a];
+    c.copy_stride[a] = B * (int64_t)lp.stride[a];
+    const __half* lbase = reinterpret_cast<const __half*>(ws + lp.off[a]) + (ML - pad_al);
+    c.rows[a] = lbase;
+    if (rs == 8) continue;  // 1-D bulk copies
+    for (int v = 0; v < lp.copies[a]; ++v) {
+      const __half* base = lbase + (int64_t)v * c.copy_stride[a];
+      const int nbox = rs >= 64 ? 2 : 1;
+      if (nm + nbox > kConvMaps) { delete cv; return NNAB_ENOTSUP; }
+      const uint32_t w0 = rs >= 64 ? 64 : (uint32_t)rs;
+      int rc = make_tmap_2d(&c.map[nm++], base, (uint64_t)rs, (uint64_t)(B * lp.U[a]), (uint64_t)rs * 2, w0, 128,
+                            (int)w0 * 2, 2);
+      if (!rc && nbox == 2)
+        rc = make_tmap_2d(&c.map[nm++], base, (uint64_t)rs, (uint64_t)(B * lp.U[a]), (uint64_t)rs * 2, 32, 128, 64, 2);
+      if (rc) { delete cv; return rc; }
+    }
+  }
+  const size_t smem_conv = 1024 + kConvStages * kConvA + KC / 8 * 512 + 3 * kConvStages * 8 + 16;
+  cudaError_t e = cudaFuncSetAttribute(cqt2010_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_conv);
+  if (e == cudaSuccess) {
+    cqt2010_conv_kernel<<<(int)std::min<int64_t>(c.tile0[n_oct], (int64_t)num_sms()), kConvThreads, smem_conv, st>>>(c);
+    e = cudaGetLastError();
+  }
+  delete cv;
+  NNAB_CUDA_TRY(e);
+  note_launch();
+  return NNAB_OK;
 }
 
 // The batched path: the fused kernel in front-only mode (stages 1-2 per clip, octave 0
@@ -1322,7 +1545,7 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
   if (rc) return rc;
   if (n_filt > 16) return NNAB_ENOTSUP;
   LvPlan lp;
-  lv_plan(pl.p, B, &lp);
+  if (lv_plan(pl.p, B, &lp)) return NNAB_ENOTSUP;
   if (!workspace || workspace_bytes < lp.total) return NNAB_ENOTSUP;
   char* ws = reinterpret_cast<char*>(workspace);
   int32_t* exps = reinterpret_cast<int32_t*>(ws + lp.exp_off);
@@ -1374,9 +1597,7 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
   cqt2010_prep_kernel<<<1, 256, 0, st>>>(q, reinterpret_cast<uint4*>(ws + lp.toep_off),
                                           reinterpret_cast<uint4*>(ws + lp.filt_off));
   NNAB_LAUNCHED();
-  const size_t smem_conv = 1024 + kConvA + KC / 8 * 512 + 64;
   const size_t smem_halve = 1024 + 16 * kHPl + 129 * 256 + ((TOEP_CHUNKS * 16 + 127) & ~127) + 64;
-  NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_conv));
   NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_halve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_halve));
   q.n_lv = n_oct;
   q.kernel_hop = kernel_hop;
@@ -1403,9 +1624,8 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
       NNAB_LAUNCHED();
     }
   }
-  const int64_t conv_tiles = n_oct * ((B * (int64_t)T + 127) / 128);
-  cqt2010_conv_kernel<<<(int)std::min<int64_t>(conv_tiles, 4 * (int64_t)num_sms()), kLvThreads, smem_conv, st>>>(q);
-  NNAB_LAUNCHED();
+  return launch_cqt2010_conv(lp, ws, B, T, n_oct, n_bins, first_bin, bpo, n_filt, p.pad_al, out_kind, exps,
+                             reinterpret_cast<const uint4*>(ws + lp.filt_off), out, st);
   return NNAB_OK;
 }
 
