@@ -289,15 +289,15 @@ extern "C" int nnab_cqt2010v2_forward(const float* x, int64_t B, int64_t L, cons
   if (B == 0) return NNAB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (precision == NNAB_PREC_TF32) {  // tensor-core chain (FP16 operands) when the clip fits in shared memory
-    // default (NNAB_CQT2010_LEVELS unset or 2): the fused kernel runs stages 1-2 and the
-    // halvings per clip and writes every octave's signal to workspace level buffers; one
-    // batched launch then runs the 12-bin convs of all octaves and clips (0.68 ms vs 0.74 ms
-    // with the convs inside the fused kernel).  0: the single fused kernel with its convs
-    // (also the path without a workspace).  1: fused front for stages 1-2 only, then
-    // level-synchronous HALVE launches and the batched convs (0.73 ms).
+    // default (NNAB_CQT2010_LEVELS unset or 3): the warp-specialised front kernel runs stages
+    // 1-2 of every clip (cqt2010_front.cu), one chain launch the octave halvings of clip
+    // groups (cqt2010_chain.cu), one batched launch the 12-bin convs of all octaves and clips.
+    // 2: the fused kernel runs stages 1-2 and the halvings per clip, then the batched convs.
+    // 1: fused front for stages 1-2 only, level-synchronous HALVE launches, batched convs.
+    // 0: the single fused kernel with its convs (also the path without a workspace).
     static const int levels = [] {
       const char* e = getenv("NNAB_CQT2010_LEVELS");
-      return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
+      return e && e[0] >= '0' && e[0] <= '3' ? e[0] - '0' : 3;
     }();
     int rc = NNAB_ENOTSUP;
     if (levels && workspace)

@@ -1437,8 +1437,13 @@ int lv_plan(const TcParams& tp, int64_t B, LvPlan* lp) {
     lp->n[a] = tp.oct_len[a];
     lp->rs[a] = std::max(h, 8);
     lp->copies[a] = std::max(1, 8 / h);
-    lp->U[a] = (tp.oct_len[a] + 2 * ML + lp->rs[a] - 1) / lp->rs[a];
-    lp->stride[a] = lp->U[a] * lp->rs[a];
+    // rows of 256 samples (the chain's TMA view; a multiple of every conv row length rs):
+    // the signal with its margins, and for a halving input the rows its last block's
+    // window reads (block n reads rows n, n + 1)
+    int rows = (tp.oct_len[a] + 2 * ML + 255) / 256;
+    if (a + 1 < tp.n_oct) rows = std::max(rows, (tp.oct_len[a + 1] + 127) / 128 + 1);
+    lp->stride[a] = 256 * rows;
+    lp->U[a] = lp->stride[a] / lp->rs[a];
     if ((int64_t)lp->copies[a] * lp->U[a] < tp.T) return NNAB_ENOTSUP;
     lp->off[a] = off;
     // + slack read as 0-weight operands (HALVE windows, the conv rows' base offset)
@@ -1463,7 +1468,7 @@ size_t cqt2010_levels_bytes(int64_t B, int64_t L, const float* taps, int n_taps,
 // The shifted level copies (hops below 8) and the batched conv of every octave.
 int launch_cqt2010_conv(const LvPlan& lp, char* ws, int64_t B, int T, int n_oct, int n_bins, int first_bin, int bpo,
                         int n_filt, int pad_al, int out_kind, const int32_t* exps, const uint4* filt_img, float* out,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool copies_written = false) {
   CopyParams cp{};
   bool any_copy = false;
   if (B * (int64_t)lp.stride[0] * 8 > INT32_MAX) return NNAB_ENOTSUP;
@@ -1477,7 +1482,7 @@ int launch_cqt2010_conv(const LvPlan& lp, char* ws, int64_t B, int T, int n_oct,
     cp.copy_stride[a] = B * (int64_t)lp.stride[a];
     any_copy |= lp.copies[a] > 1;
   }
-  if (any_copy) {
+  if (any_copy && !copies_written) {
     cqt2010_copies_kernel<<<2 * num_sms(), 256, 0, st>>>(cp);
     NNAB_LAUNCHED();
   }
@@ -1572,9 +1577,30 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
     p.lv[a] = reinterpret_cast<__half*>(ws + lp.off[a]);
     p.lv_stride[a] = lp.stride[a];
   }
-  NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-  cqt2010_tc_kernel<<<(int)std::min<int64_t>(B, (int64_t)num_sms()), kThreads, pl.smem, st>>>(p);
-  NNAB_LAUNCHED();
+  // mode 3: the warp-specialised front (cqt2010_front.cu) for stages 1-2, then as mode 1
+  rc = mode == 3 ? launch_cqt2010_front(x, B, L, taps, n_taps, p.lv0, p.lv0_stride, exps, st) : NNAB_ENOTSUP;
+  if (rc == NNAB_ENOTSUP) {
+    if (mode == 3) p.lv_mode = 1;
+    NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    cqt2010_tc_kernel<<<(int)std::min<int64_t>(B, (int64_t)num_sms()), kThreads, pl.smem, st>>>(p);
+    NNAB_LAUNCHED();
+  } else if (rc) {
+    return rc;
+  }
+  bool chained = false;
+  if (mode == 3) {  // the octave chain in one launch (cqt2010_chain.cu), else the HALVE launches
+    __half* lvp[kMaxOct];
+    int32_t hh[kMaxOct], cc[kMaxOct];
+    for (int a = 0; a < n_oct; ++a) {
+      lvp[a] = reinterpret_cast<__half*>(ws + lp.off[a]);
+      hh[a] = lp.h[a];
+      cc[a] = lp.copies[a];
+    }
+    rc = launch_cqt2010_chain(B, n_oct, lvp, lp.stride, lp.n, hh, cc, taps, n_taps, st);
+    if (rc && rc != NNAB_ENOTSUP) return rc;
+    chained = rc == NNAB_OK;
+    mode = chained ? 3 : 1;
+  }
 
   LvParams q{};
   q.B = B;
@@ -1625,7 +1651,7 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
     }
   }
   return launch_cqt2010_conv(lp, ws, B, T, n_oct, n_bins, first_bin, bpo, n_filt, p.pad_al, out_kind, exps,
-                             reinterpret_cast<const uint4*>(ws + lp.filt_off), out, st);
+                             reinterpret_cast<const uint4*>(ws + lp.filt_off), out, st, chained);
   return NNAB_OK;
 }
 

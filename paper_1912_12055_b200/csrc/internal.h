@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 #include <cstdint>
 
@@ -135,5 +136,13 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
                           const float* k_im, int n_filt, int width, int early_stages, int n_oct, int kernel_hop,
                           int first_bin, int bpo, int n_bins, int pad_mode, int out_kind, int T, float* out,
                           void* workspace, size_t workspace_bytes, cudaStream_t st, int mode);
+// CQT2010v2 front (cqt2010_front.cu): stages 1-2 of every clip -> the octave-0 level buffer
+// (FP16 in the clip's scale 2^-exps[b], reflect margins); NNAB_ENOTSUP outside its envelope
+int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, __half* lv0,
+                         int32_t lv0_stride, int32_t* exps, cudaStream_t st);
+// CQT2010v2 octave chain (cqt2010_chain.cu): halvings of levels 0 -> n_oct - 1 for all clips
+// (level 0 written), with margins and the conv's shifted copies; NNAB_ENOTSUP outside it
+int launch_cqt2010_chain(int64_t B, int n_oct, __half* const* lv, const int32_t* stride, const int32_t* n,
+                         const int32_t* h, const int32_t* copies, const float* taps, int n_taps, cudaStream_t st);
 
 }  // namespace nnab

@@ -224,6 +224,17 @@ NNAB_DEV uint64_t sdesc_kmajor_sw128(const void* smem) {
   d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
+// Same, from a shared-memory byte address (K advances inside the 128-byte row add 32 B
+// per K = 16 FP16 step).
+NNAB_DEV uint64_t sdesc_kmajor_sw128_addr(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
 // UMMA shared-memory descriptor, K-major, no swizzle ("interleaved" core
 // matrices of 8 rows x 16 B): LBO = byte step between the two 16-byte K
 // halves of one MMA, SBO = byte step between 8-row groups.
