@@ -14,7 +14,7 @@
 // uniform row array (clip stride R_a rows), rows that are not a block of the group are
 // computed and dropped.
 //
-// Per level: warp 0 issues the TMA loads (2-stage ring), warp 1 the MMAs (2 TMEM
+// Per level: warp 0 issues the TMA loads (K-block ring), warp 1 the MMAs (2 TMEM
 // accumulators), warps 4-7 the epilogue (thread = block: 128 outputs -> level a + 1 in
 // FP16, 16-byte stores).  At the level's end the epilogue warps write the new level's
 // reflect margins, zero tail and (hop < 8) the conv's shifted copies, then the CTA syncs
@@ -34,7 +34,7 @@ constexpr int kML = 128;
 constexpr int kMaxLv = 12;
 constexpr int kThreads = 8 * 32;
 constexpr int kERows = 352;                 // E rows r = -224 .. 127
-constexpr int kStages = 8;                  // K-block ring (16 KB stages: 128 rows x 64 samples)
+constexpr int kStages = 4;                  // K-block ring (16 KB stages: 128 rows x 64 samples); 2 CTAs / SM
 constexpr uint32_t kKB = 16384;
 
 struct ChainParams {
@@ -46,7 +46,7 @@ struct ChainParams {
   float taps[255];
 };
 
-__global__ void __launch_bounds__(kThreads, 1) cqt2010_chain_kernel(const __grid_constant__ ChainParams p) {
+__global__ void __launch_bounds__(kThreads, 2) cqt2010_chain_kernel(const __grid_constant__ ChainParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* A = base;                       // [kStages] x kKB
@@ -72,10 +72,18 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_chain_kernel(const __grid
   if (warp == 1) tmem_alloc<256>(tslot);
   // E[r][k'] = h[k' - 2 r - 1] (r = row - 224), FP16, K-major with the 128-byte swizzle
   // (16-byte chunk c of row w at chunk c ^ (w & 7))
-  for (int i = tid; i < kERows * 64; i += kThreads) {
-    const int w = i >> 6, kk = i & 63, r = w - 224, j = kk - 2 * r - 1;
-    const float v = (j >= 0 && j < 255) ? p.taps[j] : 0.f;
-    reinterpret_cast<__half*>(E + w * 128 + ((((kk >> 3) ^ (w & 7)) << 4)))[kk & 7] = __float2half_rn(v);
+  __shared__ float taps_s[256];
+  for (int j = tid; j < 256; j += kThreads) taps_s[j] = j < 255 ? p.taps[j] : 0.f;
+  __syncthreads();
+  for (int i = tid; i < kERows * 8; i += kThreads) {  // one 16-byte chunk per step
+    const int w = i >> 3, c = i & 7, r = w - 224;
+    __align__(16) __half v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int j = 8 * c + e - 2 * r - 1;
+      v[e] = __float2half_rn((j >= 0 && j < 255) ? taps_s[j] : 0.f);
+    }
+    *reinterpret_cast<uint4*>(E + w * 128 + ((c ^ (w & 7)) << 4)) = *reinterpret_cast<const uint4*>(v);
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -99,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_chain_kernel(const __grid
             const int row0 = b0 * R + 128 * t;
             for (int kb = 0; kb < 8; ++kb) {
               const uint32_t kq = 8 * (seq + t) + kb, s = kq % kStages, r = kq / kStages;
-              if (r > 0) mbar_wait(&a_empty[s], (r - 1) & 1);
+              if (r > 0) mbar_wait_sleep(&a_empty[s], (r - 1) & 1);
               mbar_expect_tx(&a_full[s], kKB);
               tma_load_2d(A + s * kKB, map, &a_full[s], 64 * (kb & 3), row0 + (kb >> 2));
             }
@@ -112,10 +120,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_chain_kernel(const __grid
           const uint32_t e0 = smem_u32(E);
           for (int t = 0; t < n_tiles; ++t) {
             const uint32_t sq = seq + t, d = sq & 1;
-            if (sq >= 2) mbar_wait(&d_empty[d], ((sq >> 1) - 1) & 1);
+            if (sq >= 2) mbar_wait_sleep(&d_empty[d], ((sq >> 1) - 1) & 1);
             for (int kb = 0; kb < 8; ++kb) {
               const uint32_t kq = 8 * sq + kb, s = kq % kStages, r = kq / kStages;
-              mbar_wait(&a_full[s], r & 1);
+              mbar_wait_sleep(&a_full[s], r & 1);
               tc_fence_after();
               const uint32_t a0 = smem_u32(A + s * kKB);
 #pragma unroll
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_chain_kernel(const __grid
           const int g = 128 * t + q * 32 + lane;  // row within the group
           const int bl = g / R, n = g - bl * R;
           const bool live = bl < gc && n < nb;
-          mbar_wait(&d_full[s], (sq >> 1) & 1);
+          mbar_wait_sleep(&d_full[s], (sq >> 1) & 1);
           tc_fence_after();
           __half* drow = dst + (int64_t)(b0 + bl) * dstride + kML + 128 * n;
 #pragma unroll 1
@@ -254,7 +262,7 @@ int launch_cqt2010_chain(int64_t B, int n_oct, __half* const* lv, const int32_t*
   ChainParams& p = *cp;
   p.n_oct = n_oct;
   p.B = (int32_t)B;
-  p.G = (int32_t)((B + num_sms() - 1) / num_sms());
+  p.G = (int32_t)((B + 2 * num_sms() - 1) / (2 * num_sms()));  // two CTAs per SM
   for (int j = 0; j < 255; ++j) p.taps[j] = taps[j];
   int rc = NNAB_OK;
   for (int a = 0; a < n_oct && !rc; ++a) {
@@ -276,7 +284,7 @@ int launch_cqt2010_chain(int64_t B, int n_oct, __half* const* lv, const int32_t*
     cudaError_t e = cudaFuncSetAttribute(cqt2010_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) {
       const int groups = (int)((B + p.G - 1) / p.G);
-      cqt2010_chain_kernel<<<std::min(groups, num_sms()), kThreads, smem, st>>>(p);
+      cqt2010_chain_kernel<<<std::min(groups, 2 * num_sms()), kThreads, smem, st>>>(p);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) rc = cuda_fail(e, "cqt2010_chain_kernel");

@@ -885,7 +885,8 @@ __device__ __noinline__ uint4 lv_load8_slow(const __half* row, int i, int lim) {
 // (chunk j = g[j - 127 + e]) and the conv bank (row 2j = Re bin j, 2j+1 = Im, scaled 2^6,
 // column m = tap m - (pad_al - pad)).  One CTA, once per call.
 __global__ void cqt2010_prep_kernel(const __grid_constant__ LvParams p, uint4* toep_img, uint4* filt_img) {
-  for (int j = threadIdx.x; j < TOEP_CHUNKS; j += blockDim.x) {
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int j = t0; j < TOEP_CHUNKS; j += nt) {
     __align__(16) __half v[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -896,7 +897,7 @@ __global__ void cqt2010_prep_kernel(const __grid_constant__ LvParams p, uint4* t
   }
   const int shift = p.pad_al - p.pad;
   __half* f = reinterpret_cast<__half*>(filt_img);
-  for (int e = threadIdx.x; e < NCONV * KC; e += blockDim.x) {
+  for (int e = t0; e < NCONV * KC; e += nt) {
     const int n = e / KC, m = e % KC, j = n >> 1, tap = m - shift;
     float v = 0.f;
     if (j < p.n_filt && tap >= 0 && tap < p.width)
@@ -1172,7 +1173,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
         int v, row0;
         loc.at(p, i, v, row0);
         const int a = loc.a, rs = p.rs[a];
-        if (r > 0) mbar_wait(&bar_mma[s], (r - 1) & 1);  // the stage's previous MMAs have read it
+        if (r > 0) mbar_wait_sleep(&bar_mma[s], (r - 1) & 1);  // the stage's previous MMAs have read it
         uint8_t* As = A + s * kConvA;
         const int y = (int)row0;
         if (rs == 8) {
@@ -1204,8 +1205,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
         int v, row0;
         loc.at(p, i, v, row0);
         const int rs = p.rs[loc.a];
-        mbar_wait(&bar_full[s], r & 1);
-        if (r > 0) mbar_wait(&bar_tfree[s], (r - 1) & 1);
+        mbar_wait_sleep(&bar_full[s], r & 1);
+        if (r > 0) mbar_wait_sleep(&bar_tfree[s], (r - 1) & 1);
         tc_fence_after();
         const uint32_t a0 = smem_u32(A + s * kConvA);
 #pragma unroll
@@ -1237,7 +1238,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
       const int t = p.copies[a] * (g - b * p.U[a]) + v;
       const bool live = b < p.B && t < p.T;
       const int ex = live ? __ldg(p.exps + b) : 0;
-      mbar_wait(&bar_mma[s], r & 1);
+      mbar_wait_sleep(&bar_mma[s], r & 1);
       tc_fence_after();
       float acc[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 32 * s, acc);
@@ -1620,7 +1621,7 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
   q.prof = cqt2010_prof_ptr();
   q.toep_img = reinterpret_cast<const uint4*>(ws + lp.toep_off);
   q.filt_img = reinterpret_cast<const uint4*>(ws + lp.filt_off);
-  cqt2010_prep_kernel<<<1, 256, 0, st>>>(q, reinterpret_cast<uint4*>(ws + lp.toep_off),
+  cqt2010_prep_kernel<<<8, 256, 0, st>>>(q, reinterpret_cast<uint4*>(ws + lp.toep_off),
                                           reinterpret_cast<uint4*>(ws + lp.filt_off));
   NNAB_LAUNCHED();
   const size_t smem_halve = 1024 + 16 * kHPl + 129 * 256 + ((TOEP_CHUNKS * 16 + 127) & ~127) + 64;

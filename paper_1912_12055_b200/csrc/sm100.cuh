@@ -49,6 +49,20 @@ NNAB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
+// Wait with the thread suspended in the hardware (try_wait's suspend-time hint) instead of
+// spinning: for pipelines whose idle roles would otherwise take issue slots.  Bounded.
+NNAB_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  for (uint32_t it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(20000u) : "memory");
+    if (ok) return;
+    if (it > (1u << 22)) __trap();
+  }
+}
 // Bounded wait: a pipeline bug traps (error 719) instead of hanging the GPU.
 NNAB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
