@@ -1112,6 +1112,7 @@ struct ConvParams {
   const int32_t* exps;
   const uint4* filt_img;
   float* out;
+  unsigned long long* prof;  // debug: [0] producer wait, [1] MMA full wait, [2] MMA tfree wait, [3] epilogue wait, [4] elapsed
 };
 
 NNAB_DEV uint64_t swz_desc(uint32_t addr, uint32_t row_bytes) {  // K-major, 32/64/128-byte swizzle
@@ -1132,6 +1133,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
   uint64_t* bar_mma = bar_full + kConvStages;                             // [S] MMAs done (commit)
   uint64_t* bar_tfree = bar_mma + kConvStages;                            // [S] accumulator read (4 warps)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar_tfree + kConvStages);
+  int32_t* exps_s = reinterpret_cast<int32_t*>(tslot + 4);  // the clips' scale exponents (B ints)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kConvStages; ++s) {
@@ -1143,11 +1145,19 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
   }
   if (warp == 1) tmem_alloc<32 * kConvStages>(tslot);
   for (int j = tid; j < KC / 8 * 32; j += kConvThreads) reinterpret_cast<uint4*>(filt)[j] = __ldg(p.filt_img + j);
+  for (int j = tid; j < p.B; j += kConvThreads) exps_s[j] = __ldg(p.exps + j);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  unsigned long long pw = 0, pw2 = 0;
+  const long long tb = clock64();
+  auto tw = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
+    const long long t0 = clock64();
+    mbar_wait_sleep(bar, par);
+    acc += (unsigned long long)(clock64() - t0);
+  };
   const int64_t n_tiles = p.tile0[p.n_oct];
   const int64_t n_local = n_tiles > blockIdx.x ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   // tile -> (octave, copy, first row); i only grows, so the octave is tracked incrementally
@@ -1173,7 +1183,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
         int v, row0;
         loc.at(p, i, v, row0);
         const int a = loc.a, rs = p.rs[a];
-        if (r > 0) mbar_wait_sleep(&bar_mma[s], (r - 1) & 1);  // the stage's previous MMAs have read it
+        if (r > 0) tw(&bar_mma[s], (r - 1) & 1, pw);  // the stage's previous MMAs have read it
         uint8_t* As = A + s * kConvA;
         const int y = (int)row0;
         if (rs == 8) {
@@ -1205,8 +1215,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
         int v, row0;
         loc.at(p, i, v, row0);
         const int rs = p.rs[loc.a];
-        mbar_wait_sleep(&bar_full[s], r & 1);
-        if (r > 0) mbar_wait_sleep(&bar_tfree[s], (r - 1) & 1);
+        {
+          const long long t0 = clock64();
+          mbar_wait_sleep(&bar_full[s], r & 1);
+          const unsigned long long dt = (unsigned long long)(clock64() - t0);
+          pw += dt;
+          if (p.prof) atomicAdd(p.prof + 5 + loc.a, dt);
+        }
+        if (r > 0) tw(&bar_tfree[s], (r - 1) & 1, pw2);
         tc_fence_after();
         const uint32_t a0 = smem_u32(A + s * kConvA);
 #pragma unroll
@@ -1237,8 +1253,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
       const int b = g / p.U[a];
       const int t = p.copies[a] * (g - b * p.U[a]) + v;
       const bool live = b < p.B && t < p.T;
-      const int ex = live ? __ldg(p.exps + b) : 0;
-      mbar_wait_sleep(&bar_mma[s], r & 1);
+      const int ex = live ? exps_s[b] : 0;
+      tw(&bar_mma[s], r & 1, pw);
       tc_fence_after();
       float acc[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 32 * s, acc);
@@ -1247,6 +1263,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_tfree[s]);
       if (!live) continue;
+#ifdef NNAB_DBG_CONV_NOSTORE
+      if (acc[0] != 12345.f) continue;
+#endif
       const int lskip = max(0, a * p.bpo - p.first_bin), lrow0 = p.first_bin - a * p.bpo;
       const int eo = ex - kFiltLog2;  // 2^eo without ldexpf's call in the common range
       const float os = (eo > -126 && eo < 128) ? __int_as_float((eo + 127) << 23) : ldexpf(1.f, eo);
@@ -1267,6 +1286,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
         }
       }
     }
+  }
+  if (p.prof) {
+    if (warp == 0 && pw) atomicAdd(p.prof + 0, pw);
+    if (warp == 1 && (pw | pw2)) { atomicAdd(p.prof + 1, pw); atomicAdd(p.prof + 2, pw2); }
+    if (tid == 128) atomicAdd(p.prof + 3, pw);
+    if (tid == 128) atomicAdd(p.prof + 4, (unsigned long long)(clock64() - tb));
   }
   tc_fence_before();
   __syncthreads();
@@ -1499,6 +1524,7 @@ int launch_cqt2010_conv(const LvPlan& lp, char* ws, int64_t B, int T, int n_oct,
   c.out_kind = out_kind;
   c.exps = exps;
   c.filt_img = filt_img;
+  c.prof = cqt2010_prof_ptr();
   c.out = out;
   int nm = 0;
   c.tile0[0] = 0;
@@ -1528,7 +1554,8 @@ int launch_cqt2010_conv(const LvPlan& lp, char* ws, int64_t B, int T, int n_oct,
       if (rc) { delete cv; return rc; }
     }
   }
-  const size_t smem_conv = 1024 + kConvStages * kConvA + KC / 8 * 512 + 3 * kConvStages * 8 + 16;
+  const size_t smem_conv = 1024 + kConvStages * kConvA + KC / 8 * 512 + 3 * kConvStages * 8 + 16 + 4 * (size_t)B;
+  if (smem_conv > 227 * 1024) { delete cv; return NNAB_ENOTSUP; }
   cudaError_t e = cudaFuncSetAttribute(cqt2010_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_conv);
   if (e == cudaSuccess) {
     cqt2010_conv_kernel<<<(int)std::min<int64_t>(c.tile0[n_oct], (int64_t)num_sms()), kConvThreads, smem_conv, st>>>(c);
