@@ -2,14 +2,15 @@
 """Benchmark: spectrograms/s on the 1,770-clip x 80,000-sample batch (44.1 kHz)
 plus the roofline fraction of the dominant kernel.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload mel|stft|cqt1992v2|cqt2010v2|train]
-    python bench.py --impl reference ...     # the reference's CPU path (oracle port) on the host cores
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload mel|melpow2|stft|cqt1992v2|cqt2010v2|train]
+    python bench.py --impl reference ...     # the reference spectro (baseline/_ref) on the host cores
 
 A step is one pass of the workload over one full batch already resident in
 HBM (566 MB of input > 126 MB L2, so no L2 flush is needed between steps).
-Multi-GPU: one process per GPU (torchrun); every rank processes its own full
-batch (weak scaling, clips shard with no collective on the forward path);
-`value` = all ranks' clips / max-over-ranks time.  Rank 0 prints ONE JSON line.
+Multi-GPU: one process per GPU (torchrun); the 1,770 clips are sharded over the
+ranks (strong scaling, dist.shard_range; no collective on the forward path,
+one bucketed gradient all-reduce in the train workload); `value` = 1,770 clips /
+max-over-ranks step time.  Rank 0 prints ONE JSON line.
 """
 
 from __future__ import annotations
@@ -252,7 +253,8 @@ def build_workload(name: str, device, mode: str, nb: int = B_CLIPS):
         p = cqt2010_plan(cfg)
         eng = Cqt2010Engine(p["taps"], p["top_kernels"], p["early_stages"], p["n_octaves"], p["kernel_hop"],
                             p["first_bin"], 12, 84, "reflect", device=device, precision=precision)
-        work = {"bound": "hbm", "per_batch": float(BYTES_CQT2010), "unit": "GB/s", "kernel": "cqt2010v2 chain"}
+        work = {"bound": "hbm", "per_batch": float(BYTES_CQT2010), "unit": "GB/s",
+                "kernel": "cqt2010v2 route (front + chain + conv)"}
         return eng, "magnitude", work, 2 + (p["early_stages"] - 2) + 6 + 7
     raise ValueError(name)
 

@@ -316,3 +316,33 @@ def test_grad_reducer_bucketed_backward_matches(cuda_dev):
     a, b = grads(False), grads(True)
     for u, v in zip(a, b):
         assert torch.allclose(u, v, rtol=0, atol=1e-6 * float(u.abs().max())), float((u - v).abs().max())
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_trainable_cqt1992v2_full_config(cuda_dev, precision):
+    """Trainable CQT1992v2 at the benchmark configuration (BASELINE config 3: 44.1 kHz, 84 bins,
+    12 / octave, fmin 32.70 Hz, hop 512, 22,682-tap longest kernel) on full-length clips:
+    the smoothed-magnitude forward (gradients.py:61-67) and the kernel gradients of both
+    banks summed over the batch (gradients.py:103-149) against the float64 oracle."""
+    from paper_1912_12055_b200.layers import CQT1992v2
+    rng = np.random.default_rng(11)
+    B = 3
+    x = (rng.standard_normal((B, 80000)) * 0.5).astype(np.float32)
+    m = CQT1992v2(sr=44100, hop_length=512, fmin=32.70, n_bins=84, bins_per_octave=12, trainable=True,
+                  precision=precision)
+    out = m(torch.from_numpy(x).to(cuda_dev))
+    assert out.shape == (B, 84, 157)
+    g = rng.standard_normal(out.shape).astype(np.float32)
+    out.backward(torch.from_numpy(g).to(cuda_dev))
+    k, _ = O.cqt_time_bank(O.CqtCfg(sr=44100.0, fmin=32.70, n_bins=84, hop_length=512))
+    h_re, h_im = k.real, k.imag
+    dre, dim, fwd = np.zeros_like(h_re), np.zeros_like(h_im), []
+    for b in range(B):
+        fr, re, im, S = O.smooth_mag_forward(x[b].astype(np.float64), h_re, h_im, 512)
+        fwd.append(S)
+        gb = g[b].astype(np.float64)
+        dre += (gb * re / S) @ fr
+        dim += (gb * im / S) @ fr
+    assert O.peak_err(out.detach().cpu().numpy(), np.stack(fwd)) <= TOL[precision]
+    assert O.peak_err(m.k_re.grad.cpu().numpy(), dre) <= TOL_GRAD[precision]
+    assert O.peak_err(m.k_im.grad.cpu().numpy(), dim) <= TOL_GRAD[precision]
