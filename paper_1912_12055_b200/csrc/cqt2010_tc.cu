@@ -1106,7 +1106,8 @@ struct ConvParams {
   int64_t B;
   int32_t n_oct, T, n_bins, first_bin, bpo, n_filt, out_kind;
   int32_t copies[kMaxOct], U[kMaxOct], map0[kMaxOct], rs[kMaxOct];
-  int64_t tiles_per_copy[kMaxOct], tile0[kMaxOct + 1];
+  int64_t tiles_per_copy[kMaxOct], tile0[kMaxOct + 1];  // tile0[i]: first tile of the i-th octave in walk order
+  int32_t ord[kMaxOct];  // walk order: deepest octave first (the chain wrote those last: still in L2)
   const __half* rows[kMaxOct];      // rs = 8: level base (+ the frame offset), copy stride below
   int64_t copy_stride[kMaxOct];
   const int32_t* exps;
@@ -1162,11 +1163,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
   const int64_t n_local = n_tiles > blockIdx.x ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   // tile -> (octave, copy, first row); i only grows, so the octave is tracked incrementally
   struct Loc {
-    int a = 0;
+    int a = 0, ia = 0;
     NNAB_DEV void at(const ConvParams& p, int64_t i, int& v, int& row0) {
       const int k = (int)(blockIdx.x + i * gridDim.x);
-      while (a + 1 < p.n_oct && k >= (int)p.tile0[a + 1]) ++a;
-      const int kl = k - (int)p.tile0[a], tpc = (int)p.tiles_per_copy[a];
+      while (ia + 1 < p.n_oct && k >= (int)p.tile0[ia + 1]) ++ia;
+      a = p.ord[ia];
+      const int kl = k - (int)p.tile0[ia], tpc = (int)p.tiles_per_copy[a];
       v = kl / tpc;
       row0 = (kl - v * tpc) * 128;
     }
@@ -1203,13 +1205,15 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
         }
       }
     }
-  } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issue
+  } else if (warp == 1 || warp == 2) {
+    // ---------------------------------------------------------------- MMA issue: two issuing
+    // threads on alternate tiles (the per-thread tcgen05 issue latency, not the tensor pipe,
+    // bounds these narrow MMAs)
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_f16(128, NCONV);
       const uint32_t b0 = smem_u32(filt);
       Loc loc;
-      for (int64_t i = 0; i < n_local; ++i) {
+      for (int64_t i = warp - 1; i < n_local; i += 2) {
         const int s = (int)(i % kConvStages);
         const uint32_t r = (uint32_t)(i / kConvStages);
         int v, row0;
@@ -1289,7 +1293,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) cqt2010_conv_kernel(const __g
   }
   if (p.prof) {
     if (warp == 0 && pw) atomicAdd(p.prof + 0, pw);
-    if (warp == 1 && (pw | pw2)) { atomicAdd(p.prof + 1, pw); atomicAdd(p.prof + 2, pw2); }
+    if ((warp == 1 || warp == 2) && (pw | pw2)) { atomicAdd(p.prof + 1, pw); atomicAdd(p.prof + 2, pw2); }
     if (tid == 128) atomicAdd(p.prof + 3, pw);
     if (tid == 128) atomicAdd(p.prof + 4, (unsigned long long)(clock64() - tb));
   }
@@ -1528,6 +1532,7 @@ int launch_cqt2010_conv(const LvPlan& lp, char* ws, int64_t B, int T, int n_oct,
   c.out = out;
   int nm = 0;
   c.tile0[0] = 0;
+  for (int i = 0; i < n_oct; ++i) c.ord[i] = n_oct - 1 - i;
   for (int a = 0; a < n_oct; ++a) {
     const int rs = lp.rs[a];
     if (rs != 8 && rs != 16 && rs != 32 && rs < 64) return NNAB_ENOTSUP;
@@ -1537,7 +1542,7 @@ int launch_cqt2010_conv(const LvPlan& lp, char* ws, int64_t B, int T, int n_oct,
     c.map0[a] = nm;
     c.tiles_per_copy[a] = (B * (int64_t)lp.U[a] + 127) / 128;
     if (c.tiles_per_copy[a] * 128 >= INT32_MAX) { delete cv; return NNAB_ENOTSUP; }
-    c.tile0[a + 1] = c.tile0[a] + c.tiles_per_copy[a] * lp.copies[a];
+
     c.copy_stride[a] = B * (int64_t)lp.stride[a];
     const __half* lbase = reinterpret_cast<const __half*>(ws + lp.off[a]) + (ML - pad_al);
     c.rows[a] = lbase;
@@ -1554,6 +1559,7 @@ int launch_cqt2010_conv(const LvPlan& lp, char* ws, int64_t B, int T, int n_oct,
       if (rc) { delete cv; return rc; }
     }
   }
+  for (int i = 0; i < n_oct; ++i) c.tile0[i + 1] = c.tile0[i] + c.tiles_per_copy[c.ord[i]] * lp.copies[c.ord[i]];
   const size_t smem_conv = 1024 + kConvStages * kConvA + KC / 8 * 512 + 3 * kConvStages * 8 + 16 + 4 * (size_t)B;
   if (smem_conv > 227 * 1024) { delete cv; return NNAB_ENOTSUP; }
   cudaError_t e = cudaFuncSetAttribute(cqt2010_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_conv);
