@@ -5,14 +5,14 @@
 // warp set so the HBM stream, the operand conversion, the tensor-core FIRs and the
 // epilogues of consecutive tiles and clips overlap:
 //
-//   warps 0-2    scan: the peak of the NEXT clip (an L2 bulk prefetch of the whole clip,
+//   warp 5       scan: the peak of the NEXT clip (an L2 bulk prefetch of the whole clip,
 //                then 16 float4 loads in flight per thread, L2 evict-last so the clip is
 //                still in L2 for the converters) -> the clip's power-of-two scale exponent
-//   warps 4-7    epilogue: stage-1 D -> y1 (odd phase -> stage-2 planes, even ->
+//   warps 0-3    epilogue: stage-1 D -> y1 (odd phase -> stage-2 planes, even ->
 //                stage-2 centre planes), y1's reflect images, stage-2 D -> octave 0 (+
 //                its reflect margins) in the level buffer
-//   warp 3       MMA issue (one thread) + TMEM allocation (512 columns)
-//   warps 8-15   converters: the tile's clip segment from L2 (16 float4 loads in flight
+//   warp 4       MMA issue (one thread) + TMEM allocation (512 columns)
+//   warps 6-17   converters: the tile's clip segment from L2 (16 float4 loads in flight
 //                per thread) -> scaled FP16, odd phase -> stage-1 "planes", even phase ->
 //                centre-tap planes, into one of two stage-1 operand buffers
 //
@@ -36,11 +36,14 @@ namespace {
 constexpr int kML = 128;                 // level-buffer reflect margins (cqt2010_tc.cu ML)
 constexpr int kToepChunks = 8 * 31 + 128;  // Toeplitz diagonal chunks (cqt2010_tc.cu TOEP_CHUNKS)
 constexpr int kCenChunks = 256;
-constexpr int kScanWarps = 3;
+constexpr int kScanWarps = 1;
 constexpr int kScanBatch = 24;           // float4 loads in flight per scan thread
-constexpr int kMmaWarp = 3, kEpiWarp0 = 4, kConvWarp0 = 8, kConvWarps = 8;  // 16 warps: 128 registers
-constexpr int kConvBatch = 16;           // float4 loads in flight per converter thread
+constexpr int kEpiWarp0 = 0, kMmaWarp = 4, kScanWarp0 = 5, kConvWarp0 = 6, kConvWarps = 12;  // 18 warps
+constexpr int kCT = 32 * kConvWarps;     // converter threads
+constexpr int kRowU = kCT / 64;          // plane rows one float4 step of every converter thread covers
+constexpr int kConvBatch = 10;           // float4 loads in flight per converter thread
 constexpr int kThreads = (kConvWarp0 + kConvWarps) * 32;
+static_assert(kScanWarps == 1, "the scan role is one warp");
 
 struct FrontParams {
   const float* x;
@@ -56,7 +59,17 @@ struct FrontParams {
   int32_t lv0_stride;
   int32_t* exps;
   unsigned long long* prof;  // debug: per-role wait cycles (nnab_debug_cqt2010_front_profile), or null
+  // scale: exact = 0 (fast): the scale comes from the clip's first kPeek samples with kHead
+  // bits of headroom, and a clip whose peak would leave that headroom (or whose first
+  // kPeek samples are all zero) is flagged in flags[b]; exact = 1: the exact peak of the
+  // whole clip (a full scan), over the clips listed in list[0 .. *list_n) (the flagged ones)
+  int32_t exact;
+  int32_t* flags;
+  const int32_t* list;
+  const int32_t* list_n;
 };
+constexpr int kPeek = 2048;  // samples the fast scale looks at
+constexpr int kHead = 8;     // headroom bits of the fast scale: the rest of the clip may be 2^(kHead + 13) louder
 
 NNAB_DEV uint64_t nsw(uint32_t addr, uint32_t lbo, uint32_t sbo) {  // no-swizzle K-major descriptor
   uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
@@ -155,8 +168,9 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
   uint64_t* s2_done = s2_ready + 1;                 // commit
   uint64_t* s2_free = s2_done + 1;                  // 4 epilogue warps
   uint32_t* tslot = reinterpret_cast<uint32_t*>(s2_free + 1);
-  int* ex_slot = reinterpret_cast<int*>(tslot + 1);     // [2]
-  float* scan_part = reinterpret_cast<float*>(ex_slot + 2);  // [2][kScanWarps]
+  int* ex_slot = reinterpret_cast<int*>(tslot + 1);     // [2] scale exponent, [2] peek-was-zero
+  float* scan_part = reinterpret_cast<float*>(ex_slot + 4);  // [2][kScanWarps]
+  unsigned* conv_max = reinterpret_cast<unsigned*>(scan_part + 2 * kScanWarps);  // [2] converter peak bits
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (tid == 0) {
@@ -164,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
     mbar_init(&ex_ready[1], 1);
     mbar_init(conv_start, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&a_full[i], 32 * kConvWarps);
+      mbar_init(&a_full[i], kConvWarps);
       mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -177,6 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tslot);
+  if (tid < 2) conv_max[tid] = 0u;
   // operand regions start zeroed: the stage-2 windows of real blocks read plane rows past
   // the signal at zero Toeplitz weight (0 * NaN would poison them); everything written
   // later is finite
@@ -204,31 +219,37 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
   const uint32_t tmem = *tslot;
   unsigned long long pf[4] = {0, 0, 0, 0};
   const long long t_begin = clock64();
-  const int n_clips = p.B > blockIdx.x ? (int)((p.B - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
-  auto clip_of = [&](int k) { return (int64_t)blockIdx.x + (int64_t)k * gridDim.x; };
+  const int64_t n_all = p.list ? (int64_t)*p.list_n : p.B;  // clips this launch walks
+  const int n_clips = n_all > blockIdx.x ? (int)((n_all - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+  auto clip_of = [&](int k) {
+    const int64_t i = (int64_t)blockIdx.x + (int64_t)k * gridDim.x;
+    return p.list ? (int64_t)p.list[i] : i;
+  };
 
-  if (warp < kScanWarps) {
+  if (warp == kScanWarp0) {
+    const int st = tid - kScanWarp0 * 32;
     // ------------------------------------------------------------ scan: exponent of each clip
     const uint64_t keep = policy_evict_last();
     const int n4 = p.L / 4;
     for (int k = 0; k < n_clips; ++k) {
       if (k > 0) wait_p(conv_start, (k - 1) & 1, pf[0]);  // the converter is on clip k - 1
-      if (tid == 0) tl_mark(p, k, 0, t_begin);
+      if (st == 0) tl_mark(p, k, 0, t_begin);
       const float* xb = p.x + clip_of(k) * p.L;
       // the whole clip is requested from HBM at once (L2 prefetch: no registers, no shared
       // memory in flight); the scan's loads then meet lines already arriving
-      if (tid < 32) {
+      {
         const uint32_t bytes = (uint32_t)p.L * 4u, piece = ((bytes + 31) / 32 + 15) & ~15u;
-        const uint32_t o = (uint32_t)tid * piece;
+        const uint32_t o = (uint32_t)st * piece;
         if (o < bytes) prefetch_l2(reinterpret_cast<const char*>(xb) + o, min(piece, bytes - o));
       }
       float mx = 0.f;
-      for (int f0 = tid; f0 < n4; f0 += kScanBatch * kScanWarps * 32) {
+      const int n4s = p.exact ? n4 : min(n4, kPeek / 4);  // fast: the first kPeek samples
+      for (int f0 = st; f0 < n4s; f0 += kScanBatch * 32) {
         float4 v[kScanBatch];
 #pragma unroll
         for (int u = 0; u < kScanBatch; ++u) {
-          const int f = f0 + u * kScanWarps * 32;
-          v[u] = f < n4 ? ldg_keep(xb + 4 * f, keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const int f = f0 + u * 32;
+          v[u] = f < n4s ? ldg_keep(xb + 4 * f, keep) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < kScanBatch; ++u)
@@ -236,14 +257,12 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) scan_part[(k & 1) * kScanWarps + warp] = mx;
-      named_sync(1, kScanWarps * 32);
-      if (tid == 0) {
-        float m = 0.f;
-        for (int w = 0; w < kScanWarps; ++w) m = fmaxf(m, scan_part[(k & 1) * kScanWarps + w]);
+      if (st == 0) {
+        const float m = mx;
         int ex = 0;
         if (m > 0.f && m < INFINITY) frexpf(m, &ex);
-        ex_slot[k & 1] = ex;
+        ex_slot[k & 1] = p.exact ? ex : ex + kHead;
+        ex_slot[2 + (k & 1)] = !p.exact && !(m > 0.f && m < INFINITY);  // fast scale undefined: flag
         mbar_arrive(&ex_ready[k & 1]);
         tl_mark(p, k, 1, t_begin);
       }
@@ -281,11 +300,11 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
     }
   } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kConvWarps) {
     // ------------------------------------------------------------ converters
-    // the tile's ext segment [e0, e1) as float4 f = ct + 256 u: its samples d = 4 f are
+    // the tile's ext segment [e0, e1) as float4 f = ct + kCT u: its samples d = 4 f are
     //   odd  d + 1, d + 3 -> odd row f / 64 = ct / 64 + 4 u, odd index 2 (ct % 64) (+1)
     //   even d, d + 2     -> even row (f - 32) / 64 = (ct - 32) / 64 + 4 u, index 2 ((ct - 32) % 64)
     // so both store addresses are per-thread constants plus 64 B per u
-    const int ct = tid - kConvWarp0 * 32;  // 0..255
+    const int ct = tid - kConvWarp0 * 32;  // 0 .. kCT - 1
     const int uo = 2 * (ct & 63), ue = 2 * ((ct - 32) & 63);
     const int ro = ct >> 6, re = ((ct - 32 + 64) >> 6) - 1;
     const uint32_t oo = (uint32_t)((uo >> 3) * p.pl1 + (uo & 7) * 2 + ro * 16);
@@ -302,7 +321,9 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
         p.exps[b] = ex;
         tl_mark(p, k, 2, t_begin);
       }
+      const bool zero_peek = ex_slot[2 + (k & 1)] != 0;
       const float scale = ldexpf(1.f, -ex);
+      float cmax = 0.f;  // the clip's peak as converted (fast-scale overflow check)
       for (int t = 0; t < p.n1; ++t, ++g1) {
         const int slot = (int)(g1 & 1);
         const int n0 = 128 * t, nb = min(128, p.nb1 - n0);
@@ -311,43 +332,54 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
         if (g1 >= 2) wait_p(&a_empty[slot], ((g1 >> 1) - 1) & 1, pf[1]);  // this buffer's last MMAs are done
         const uint32_t a1 = smem_u32(base + p.off_a1[slot]);
         const float* pb = xb + e0 + 4 * ct;  // float4 u of this thread: pb + 1024 u
-        for (int u0 = 0; 256 * u0 < n4; u0 += kConvBatch) {
-          const uint32_t so = a1 + oo + 64u * u0, se = a1 + oe + 64u * u0;
-          const int rl0 = re + 4 * u0;  // even row of v[0]
-          // batch fully inside the clip and the tile, every even row a block of the tile:
-          // unconditional loads (immediate offsets) and stores
-          const bool fast = e0 + 1024 * u0 >= 0 && e0 + 1024 * (u0 + kConvBatch) <= min(e1, p.L) && rl0 >= 0 &&
-                            rl0 + 4 * (kConvBatch - 1) < nb;
+        for (int u0 = 0; kCT * u0 < n4; u0 += kConvBatch) {
+          const uint32_t so = a1 + oo + 16u * kRowU * u0, se = a1 + oe + 16u * kRowU * u0;
+          const int rl0 = re + kRowU * u0;  // even row of v[0]
+          const float* q = pb + 4 * kCT * u0;  // float4 u at q + 4 kCT u (immediate offsets)
+          const int fr = n4 - (ct + kCT * u0);  // float4 u of this thread is live iff kCT u < fr
+          // every load of the batch inside the clip (no reflect image): predicated loads only
+          const bool inside = e0 + 4 * kCT * u0 >= 0 && e0 + 4 * kCT * (u0 + kConvBatch) <= p.L;
           float4 v[kConvBatch];
-          if (fast) {
+          if (inside) {
 #pragma unroll
-            for (int u = 0; u < kConvBatch; ++u) v[u] = ldg_keep(pb + 1024 * (u0 + u), last);
-#pragma unroll
-            for (int u = 0; u < kConvBatch; ++u) {
-              sts32(so + 64u * u, pack2(v[u].y * scale, v[u].w * scale));
-              sts32(se + 64u * u, pack2(v[u].x * scale, v[u].z * scale));
-            }
+#ifdef NNAB_DBG_FRONT_NOLOAD
+            for (int u = 0; u < kConvBatch; ++u) v[u] = make_float4((float)u0, (float)u, 0.5f, 0.25f);
+#else
+            for (int u = 0; u < kConvBatch; ++u)
+              v[u] = kCT * u < fr ? ldg_keep(q + 4 * kCT * u, last) : make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
           } else {
 #pragma unroll
             for (int u = 0; u < kConvBatch; ++u) {
-              const int f = ct + 256 * (u0 + u), e = e0 + 4 * f;
-              if (f < n4 && e >= 0 && e + 4 <= p.L) v[u] = ldg_keep(pb + 1024 * (u0 + u), last);
-              else v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+              const int e = e0 + 4 * (ct + kCT * (u0 + u));
+              v[u] = kCT * u >= fr ? make_float4(0.f, 0.f, 0.f, 0.f)
+                             : (e >= 0 && e + 4 <= p.L) ? ldg_keep(q + 4 * kCT * u, last) : edge_float4(e, e1, p.L, xb);
             }
+          }
 #pragma unroll
-            for (int u = 0; u < kConvBatch; ++u) {
-              const int f = ct + 256 * (u0 + u), e = e0 + 4 * f;
-              if (f >= n4) continue;
-              if (e < 0 || e + 4 > p.L) v[u] = edge_float4(e, e1, p.L, xb);
-              sts32(so + 64u * u, pack2(v[u].y * scale, v[u].w * scale));
-              if (rl0 + 4 * u >= 0 && rl0 + 4 * u < nb) sts32(se + 64u * u, pack2(v[u].x * scale, v[u].z * scale));
-            }
+          for (int u = 0; u < kConvBatch; ++u) {
+            if (kCT * u >= fr) break;
+            cmax = fmaxf(cmax, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+            sts32(so + 16u * kRowU * u, pack2(v[u].y * scale, v[u].w * scale));
+            if ((unsigned)(rl0 + kRowU * u) < (unsigned)nb) sts32(se + 16u * kRowU * u, pack2(v[u].x * scale, v[u].z * scale));
           }
         }
         fence_proxy_async_smem();
-        mbar_arrive(&a_full[slot]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[slot]);
       }
       if (ct == 0) tl_mark(p, k, 3, t_begin);
+      if (!p.exact) {  // flag the clip when the fast scale left less than 2 bits below FP16's range
+#pragma unroll
+        for (int o = 16; o; o >>= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+        if (lane == 0) atomicMax(&conv_max[k & 1], __float_as_uint(cmax));
+        named_sync(4, 32 * kConvWarps);
+        if (ct == 0) {
+          const float m = __uint_as_float(conv_max[k & 1]);
+          if (zero_peek || !(m * scale < 16384.f)) p.flags[b] = 1;
+          conv_max[k & 1] = 0u;  // reused by clip k + 2, after clip k + 1's barrier
+        }
+      }
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
     // ------------------------------------------------------------ epilogue
@@ -501,8 +533,8 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
     if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the last row is written
   }
   if (p.prof) {  // role leaders: [4 role slots] x 5 roles + total
-    const int role = warp < kScanWarps ? 0 : warp == kMmaWarp ? 2 : warp >= kConvWarp0 ? 3 : 4;
-    const bool lead = tid == 0 || tid == kMmaWarp * 32 || tid == kConvWarp0 * 32 || tid == kEpiWarp0 * 32;
+    const int role = warp == kScanWarp0 ? 0 : warp == kMmaWarp ? 2 : warp >= kConvWarp0 ? 3 : 4;
+    const bool lead = tid == kScanWarp0 * 32 || tid == kMmaWarp * 32 || tid == kConvWarp0 * 32 || tid == kEpiWarp0 * 32;
     if ((lead || role == 2) && (pf[0] | pf[1] | pf[2] | pf[3]))
       for (int i = 0; i < 4; ++i) atomicAdd(p.prof + 4 * role + i, pf[i]);
     if (tid == 0) atomicAdd(p.prof + 20, (unsigned long long)(clock64() - t_begin));
@@ -516,13 +548,28 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
 __device__ unsigned long long g_front_prof[24];
 bool g_front_prof_on = false;
 
+// the flagged clips' indices (order irrelevant: clips are independent) and their count
+__global__ void cqt2010_flag_list_kernel(const int32_t* flags, int64_t B, int32_t* list, int32_t* list_n) {
+  __shared__ int32_t cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int64_t b = threadIdx.x; b < B; b += blockDim.x)
+    if (flags[b]) list[atomicAdd(&cnt, 1)] = (int32_t)b;
+  __syncthreads();
+  if (threadIdx.x == 0) *list_n = cnt;
+}
+
 }  // namespace
 
-// Shared-memory plan + launch; NNAB_ENOTSUP outside the kernel's envelope (the caller
-// then runs the fused kernel's front-only mode).
+// Shared-memory plan + launches; NNAB_ENOTSUP outside the kernel's envelope (the caller
+// then runs the fused kernel's front-only mode).  Fast launch (scale from the first kPeek
+// samples) over every clip, then the flagged clips (zero / too quiet start, a later peak
+// beyond the headroom) again with the exact whole-clip scale.  flags / list: B ints each,
+// list_n: one int, in the caller's workspace.
 int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, __half* lv0,
-                         int32_t lv0_stride, int32_t* exps, cudaStream_t st) {
-  if (n_taps != 255 || L % 4 != 0 || L < 1024 || L > (1 << 24)) return NNAB_ENOTSUP;
+                         int32_t lv0_stride, int32_t* exps, int32_t* flags, int32_t* list, int32_t* list_n,
+                         cudaStream_t st) {
+  if (n_taps != 255 || L % 4 != 0 || L < 1024 || L > (1 << 24) || !flags || !list || !list_n) return NNAB_ENOTSUP;
   FrontParams p{};
   p.x = x;
   p.B = B;
@@ -567,7 +614,19 @@ int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps
     p.prof = reinterpret_cast<unsigned long long*>(ptr);
   }
   NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  cqt2010_front_kernel<<<(int)std::min<int64_t>(B, (int64_t)num_sms()), kThreads, smem, st>>>(p);
+  const int grid = (int)std::min<int64_t>(B, (int64_t)num_sms());
+  NNAB_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)B * 4, st));
+  p.exact = 0;
+  p.flags = flags;
+  cqt2010_front_kernel<<<grid, kThreads, smem, st>>>(p);
+  NNAB_LAUNCHED();
+  cqt2010_flag_list_kernel<<<1, 1024, 0, st>>>(flags, B, list, list_n);
+  NNAB_LAUNCHED();
+  p.exact = 1;
+  p.list = list;
+  p.list_n = list_n;
+  p.prof = nullptr;
+  cqt2010_front_kernel<<<grid, kThreads, smem, st>>>(p);
   NNAB_LAUNCHED();
   return NNAB_OK;
 }

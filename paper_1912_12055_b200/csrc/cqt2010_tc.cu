@@ -1451,7 +1451,7 @@ int make_plan(int64_t L, int n_taps, const float* taps, int n_filt, int width, i
 // shifted copies when h < 8.
 struct LvPlan {
   int32_t n[kMaxOct], stride[kMaxOct], rs[kMaxOct], U[kMaxOct], copies[kMaxOct], h[kMaxOct];
-  size_t off[kMaxOct], exp_off, toep_off, filt_off, total;
+  size_t off[kMaxOct], exp_off, toep_off, filt_off, flag_off, list_off, total;
 };
 int lv_plan(const TcParams& tp, int64_t B, LvPlan* lp) {
   size_t off = ((size_t)B * 4 + 255) & ~size_t(255);  // exps first, then the operand images
@@ -1460,6 +1460,10 @@ int lv_plan(const TcParams& tp, int64_t B, LvPlan* lp) {
   off += (TOEP_CHUNKS * 16 + 255) & ~255;
   lp->filt_off = off;
   off += (KC / 8 * 512 + 255) & ~255;
+  lp->flag_off = off;  // the front's fast-scale flags, then the flagged-clip list and its count
+  off += ((size_t)B * 4 + 255) & ~size_t(255);
+  lp->list_off = off;
+  off += ((size_t)B * 4 + 4 + 255) & ~size_t(255);
   for (int a = 0; a < tp.n_oct; ++a) {
     const int h = tp.kernel_hop >> a;
     if (h < 1) return NNAB_ENOTSUP;
@@ -1612,7 +1616,11 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
     p.lv_stride[a] = lp.stride[a];
   }
   // mode 3: the warp-specialised front (cqt2010_front.cu) for stages 1-2, then as mode 1
-  rc = mode == 3 ? launch_cqt2010_front(x, B, L, taps, n_taps, p.lv0, p.lv0_stride, exps, st) : NNAB_ENOTSUP;
+  rc = mode == 3 ? launch_cqt2010_front(x, B, L, taps, n_taps, p.lv0, p.lv0_stride, exps,
+                                        reinterpret_cast<int32_t*>(ws + lp.flag_off),
+                                        reinterpret_cast<int32_t*>(ws + lp.list_off),
+                                        reinterpret_cast<int32_t*>(ws + lp.list_off) + B, st)
+                  : NNAB_ENOTSUP;
   if (rc == NNAB_ENOTSUP) {
     if (mode == 3) p.lv_mode = 1;
     NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));

@@ -139,7 +139,8 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
 // CQT2010v2 front (cqt2010_front.cu): stages 1-2 of every clip -> the octave-0 level buffer
 // (FP16 in the clip's scale 2^-exps[b], reflect margins); NNAB_ENOTSUP outside its envelope
 int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, __half* lv0,
-                         int32_t lv0_stride, int32_t* exps, cudaStream_t st);
+                         int32_t lv0_stride, int32_t* exps, int32_t* flags, int32_t* list, int32_t* list_n,
+                         cudaStream_t st);
 // CQT2010v2 octave chain (cqt2010_chain.cu): halvings of levels 0 -> n_oct - 1 for all clips
 // (level 0 written), with margins and the conv's shifted copies; NNAB_ENOTSUP outside it
 int launch_cqt2010_chain(int64_t B, int n_oct, __half* const* lv, const int32_t* stride, const int32_t* n,
