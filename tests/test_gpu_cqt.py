@@ -252,12 +252,13 @@ def test_cqt1992v2_batch_vs_sequential(golden, cuda_dev):
         assert np.array_equal(e.forward(x).cpu().numpy(), whole)
 
 
-@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
 def test_cqt2010v2_levels_path_matches_oracle(tmp_path, mode):
-    """The CQT2010v2 routes other than the default (fused chain + batched convs):
-    NNAB_CQT2010_LEVELS=0, the single fused kernel with its convs; =1, the fused front for
-    stages 1-2, level-synchronous HALVE launches and one CONV launch over all octaves --
-    against the oracle, in a subprocess (the switch is read once per process)."""
+    """The CQT2010v2 routes other than the default (front kernel + octave chain + batched
+    convs): NNAB_CQT2010_LEVELS=0, the single fused kernel with its convs; =1, the fused
+    kernel's front for stages 1-2, level-synchronous HALVE launches and one CONV launch over
+    all octaves; =2, the fused kernel through the halvings + the batched convs -- against
+    the oracle, in a subprocess (the switch is read once per process)."""
     import os
     import subprocess
     import sys
@@ -302,3 +303,26 @@ def test_cqt1992v2_f16_modes_small_and_ragged(golden, cuda_dev, precision):
         for i in range(len(amps)):
             ref = O.cqt1992v2_clip(x[i].astype(np.float64), kern, 512)
             assert O.peak_err(got[i], ref) <= TOL[precision], (cfg.n_bins, i, O.peak_err(got[i], ref))
+
+
+def test_cqt2010v2_mixed_batch_fast_and_exact_scales(cuda_dev):
+    """The front kernel's fast scale (from each clip's first 2,048 samples) and its exact
+    relaunch for the clips it flags (a silent start, a later peak beyond the headroom), in
+    one batch: every clip against the oracle, the silent one exactly zero."""
+    cfg = O.CqtCfg(sr=SR)
+    plan = O.cqt2010_plan(cfg)
+    rng = np.random.default_rng(17)
+    n = 80000
+    xs = [rng.standard_normal(n) * 0.5,                                           # fast scale
+          np.concatenate([np.zeros(5000), rng.standard_normal(n - 5000)]),        # zero start: flagged
+          np.concatenate([rng.standard_normal(3000) * 1e-7, rng.standard_normal(n - 3000) * 3.0]),  # flagged
+          rng.standard_normal(n) * 1e-6,                                          # fast, quiet
+          np.zeros(n),                                                            # all zero: flagged
+          rng.standard_normal(n) * 2e4]                                           # fast, loud
+    x = np.stack(xs).astype(np.float32)
+    got = rec_engine(cfg, "tf32").forward(torch.from_numpy(x).to(cuda_dev)).cpu().numpy()
+    assert np.isfinite(got).all()
+    assert not got[4].any()
+    for i in (0, 1, 2, 3, 5):
+        ref = O.cqt2010v2_clip(x[i].astype(np.float64), cfg, plan)
+        assert O.peak_err(got[i], ref) <= TOL["tf32"], (i, O.peak_err(got[i], ref))
