@@ -44,6 +44,7 @@ struct ChainParams {
   int64_t copy_stride[kMaxLv];
   __half* lv[kMaxLv];
   float taps[255];
+  unsigned long long* prof;  // debug: per level [3a]: tiles done (epilogue), [3a+1]: margins done, [3a+2]: level end
 };
 
 __global__ void __launch_bounds__(kThreads, 2) cqt2010_chain_kernel(const __grid_constant__ ChainParams p) {
@@ -92,6 +93,7 @@ __global__ void __launch_bounds__(kThreads, 2) cqt2010_chain_kernel(const __grid
   const uint32_t tmem = *tslot;
   const int n_groups = (p.B + p.G - 1) / p.G;
   uint32_t seq = 0;  // tile sequence over groups and levels (ring / accumulator phases)
+  long long tl = clock64();
 
   for (int grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
     const int b0 = grp * p.G, gc = min(p.G, p.B - b0);
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 2) cqt2010_chain_kernel(const __grid
         // conv's shifted copies (hop < 8); items over all the group's clips, loads batched
         // ahead of the stores (plain loads: this CTA's own stores)
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (p.prof && et == 0) { const long long n = clock64(); atomicAdd(p.prof + 3 * a, (unsigned long long)(n - tl)); tl = n; }
         {
           const int n_items = gc * 2 * kML;
           for (int j0 = et; j0 < n_items; j0 += 8 * 128) {
@@ -240,9 +243,11 @@ __global__ void __launch_bounds__(kThreads, 2) cqt2010_chain_kernel(const __grid
           }
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");  // the next level's TMA reads these stores
+        if (p.prof && et == 0) { const long long n = clock64(); atomicAdd(p.prof + 3 * a + 1, (unsigned long long)(n - tl)); tl = n; }
       }
       seq += (uint32_t)n_tiles;
       __syncthreads();
+      if (p.prof && tid == 128) { const long long n = clock64(); atomicAdd(p.prof + 3 * a + 2, (unsigned long long)(n - tl)); tl = n; }
     }
   }
   tc_fence_before();
@@ -251,7 +256,30 @@ __global__ void __launch_bounds__(kThreads, 2) cqt2010_chain_kernel(const __grid
   if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
+__device__ unsigned long long g_chain_prof[40];
+bool g_chain_prof_on = false;
+unsigned long long* cqt2010_chain_prof() {
+  if (!g_chain_prof_on) return nullptr;
+  void* ptr = nullptr;
+  cudaGetSymbolAddress(&ptr, g_chain_prof);
+  return reinterpret_cast<unsigned long long*>(ptr);
+}
+
 }  // namespace
+
+// Debug: per-level phase cycles of the octave chain (on != 0 clears and enables; on == 0
+// copies [40] out): level a at 3 a: tiles, 3 a + 1: margins / copies, 3 a + 2: barrier.
+extern "C" int nnab_debug_cqt2010_chain_profile(int on, unsigned long long* out) {
+  if (on) {
+    g_chain_prof_on = true;
+    unsigned long long z[40] = {};
+    NNAB_CUDA_TRY(cudaMemcpyToSymbol(g_chain_prof, z, sizeof(z)));
+    return NNAB_OK;
+  }
+  g_chain_prof_on = false;
+  if (out) NNAB_CUDA_TRY(cudaMemcpyFromSymbol(out, g_chain_prof, 40 * sizeof(unsigned long long)));
+  return NNAB_OK;
+}
 
 // levels: base pointers, strides (multiples of 256), lengths, hops and conv copies of every
 // octave; level 0 (with its margins) is already written.  NNAB_ENOTSUP outside the envelope.
@@ -264,6 +292,7 @@ int launch_cqt2010_chain(int64_t B, int n_oct, __half* const* lv, const int32_t*
   p.B = (int32_t)B;
   p.G = (int32_t)((B + 2 * num_sms() - 1) / (2 * num_sms()));  // two CTAs per SM
   for (int j = 0; j < 255; ++j) p.taps[j] = taps[j];
+  p.prof = cqt2010_chain_prof();
   int rc = NNAB_OK;
   for (int a = 0; a < n_oct && !rc; ++a) {
     p.lv[a] = lv[a];

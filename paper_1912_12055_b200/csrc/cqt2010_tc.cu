@@ -1629,21 +1629,9 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
   } else if (rc) {
     return rc;
   }
+  const bool mode3 = mode == 3;
+  if (mode == 3) mode = 1;  // the halving launches below run only if the mode-3 back end is out of reach
   bool chained = false;
-  if (mode == 3) {  // the octave chain in one launch (cqt2010_chain.cu), else the HALVE launches
-    __half* lvp[kMaxOct];
-    int32_t hh[kMaxOct], cc[kMaxOct];
-    for (int a = 0; a < n_oct; ++a) {
-      lvp[a] = reinterpret_cast<__half*>(ws + lp.off[a]);
-      hh[a] = lp.h[a];
-      cc[a] = lp.copies[a];
-    }
-    rc = launch_cqt2010_chain(B, n_oct, lvp, lp.stride, lp.n, hh, cc, taps, n_taps, st);
-    if (rc && rc != NNAB_ENOTSUP) return rc;
-    chained = rc == NNAB_OK;
-    mode = chained ? 3 : 1;
-  }
-
   LvParams q{};
   q.B = B;
   q.h0 = taps[127];
@@ -1665,6 +1653,48 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
   cqt2010_prep_kernel<<<8, 256, 0, st>>>(q, reinterpret_cast<uint4*>(ws + lp.toep_off),
                                           reinterpret_cast<uint4*>(ws + lp.filt_off));
   NNAB_LAUNCHED();
+  if (mode3) {
+    // mode 3: the octave chain and every octave's conv in one launch (cqt2010_back.cu); else the
+    // chain launch (cqt2010_chain.cu) + the batched conv; else the HALVE launches + batched conv
+    CqtBackArgs bg{};
+    bg.n_oct = n_oct;
+    bg.B = B;
+    bg.taps = taps;
+    bg.n_taps = n_taps;
+    for (int a = 0; a < n_oct; ++a) {
+      bg.lv[a] = reinterpret_cast<__half*>(ws + lp.off[a]);
+      bg.n[a] = lp.n[a];
+      bg.stride[a] = lp.stride[a];
+      bg.h[a] = lp.h[a];
+      bg.copies[a] = lp.copies[a];
+      bg.U[a] = lp.U[a];
+      bg.rs[a] = lp.rs[a];
+    }
+    bg.pad_al = p.pad_al;
+    bg.T = T;
+    bg.n_bins = n_bins;
+    bg.first_bin = first_bin;
+    bg.bpo = bpo;
+    bg.n_filt = n_filt;
+    bg.out_kind = out_kind;
+    bg.exps = exps;
+    bg.filt_img = reinterpret_cast<const uint4*>(ws + lp.filt_off);
+    bg.out = out;
+    static const bool no_back = [] { const char* e = getenv("NNAB_CQT2010_NOBACK"); return e && e[0] == '1'; }();
+    rc = no_back ? NNAB_ENOTSUP : launch_cqt2010_back(bg, st);
+    if (rc != NNAB_ENOTSUP) return rc;
+    __half* lvp[kMaxOct];
+    int32_t hh[kMaxOct], cc[kMaxOct];
+    for (int a = 0; a < n_oct; ++a) {
+      lvp[a] = reinterpret_cast<__half*>(ws + lp.off[a]);
+      hh[a] = lp.h[a];
+      cc[a] = lp.copies[a];
+    }
+    rc = launch_cqt2010_chain(B, n_oct, lvp, lp.stride, lp.n, hh, cc, taps, n_taps, st);
+    if (rc && rc != NNAB_ENOTSUP) return rc;
+    chained = rc == NNAB_OK;
+    if (chained) mode = 3;
+  }
   const size_t smem_halve = 1024 + 16 * kHPl + 129 * 256 + ((TOEP_CHUNKS * 16 + 127) & ~127) + 64;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_halve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_halve));
   q.n_lv = n_oct;

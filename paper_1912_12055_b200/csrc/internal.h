@@ -141,6 +141,21 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
 int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, __half* lv0,
                          int32_t lv0_stride, int32_t* exps, int32_t* flags, int32_t* list, int32_t* list_n,
                          cudaStream_t st);
+// CQT2010v2 back end (cqt2010_back.cu): the octave chain and every octave's conv of clip
+// groups in one launch (level 0 written by the front, the conv bank image by the prep kernel)
+struct CqtBackArgs {
+  int n_oct;
+  int64_t B;
+  const float* taps;
+  int n_taps;
+  __half* lv[12];
+  int32_t n[12], stride[12], h[12], copies[12], U[12], rs[12];
+  int pad_al, T, n_bins, first_bin, bpo, n_filt, out_kind;
+  const int32_t* exps;
+  const uint4* filt_img;
+  float* out;
+};
+int launch_cqt2010_back(const CqtBackArgs& g, cudaStream_t st);
 // CQT2010v2 octave chain (cqt2010_chain.cu): halvings of levels 0 -> n_oct - 1 for all clips
 // (level 0 written), with margins and the conv's shifted copies; NNAB_ENOTSUP outside it
 int launch_cqt2010_chain(int64_t B, int n_oct, __half* const* lv, const int32_t* stride, const int32_t* n,

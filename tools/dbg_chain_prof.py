@@ -1,0 +1,24 @@
+"""Per-level phase cycles of the CQT2010v2 octave-chain kernel (averaged over CTAs)."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from oracle import spectro_oracle as O
+from paper_1912_12055_b200 import _lib as L
+from paper_1912_12055_b200.engine import Cqt2010Engine
+lib = L.load()
+fn = lib.nnab_debug_cqt2010_chain_profile
+fn.restype = C.c_int; fn.argtypes = [C.c_int, C.c_void_p]
+cfg = O.CqtCfg(sr=44100.0)
+p = O.cqt2010_plan(cfg)
+eng = Cqt2010Engine(p.taps, p.top_kernels, p.early_stages, p.n_octaves, p.kernel_hop, p.first_bin, 12, 84, "reflect",
+                    precision="f16")
+x = torch.randn(1770, 80000, device="cuda") * 0.5
+eng.forward(x); torch.cuda.synchronize()
+fn(1, None)
+eng.forward(x); torch.cuda.synchronize()
+out = (C.c_ulonglong * 40)()
+fn(0, out)
+n = 296
+for a in range(6):
+    print(f"level {a}->{a + 1}: tiles {out[3 * a] / n / 1e3:6.1f}k  margins {out[3 * a + 1] / n / 1e3:6.1f}k  "
+          f"barrier {out[3 * a + 2] / n / 1e3:6.1f}k cycles per CTA")
