@@ -252,13 +252,15 @@ def test_cqt1992v2_batch_vs_sequential(golden, cuda_dev):
         assert np.array_equal(e.forward(x).cpu().numpy(), whole)
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3-noback"])
 def test_cqt2010v2_levels_path_matches_oracle(tmp_path, mode):
     """The CQT2010v2 routes other than the default (front kernel + octave chain + batched
     convs): NNAB_CQT2010_LEVELS=0, the single fused kernel with its convs; =1, the fused
     kernel's front for stages 1-2, level-synchronous HALVE launches and one CONV launch over
     all octaves; =2, the fused kernel through the halvings + the batched convs -- against
-    the oracle, in a subprocess (the switch is read once per process)."""
+    the oracle; 3-noback: the default front with the separate octave-chain and conv launches
+    (NNAB_CQT2010_NOBACK=1, the route when the merged back-end kernel is out of reach) -- in a
+    subprocess (the switches are read once per process)."""
     import os
     import subprocess
     import sys
@@ -280,7 +282,9 @@ np.save(sys.argv[2], got[:4])
 print(max(errs))
 '''
     out = str(tmp_path / "lv.npy")
-    env = dict(os.environ, NNAB_CQT2010_LEVELS=mode)
+    env = dict(os.environ, NNAB_CQT2010_LEVELS=mode[0])
+    if mode == "3-noback":
+        env["NNAB_CQT2010_NOBACK"] = "1"
     r = subprocess.run([sys.executable, "-c", code, root, out], env=env, capture_output=True, text=True, cwd=root)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= 1e-3
