@@ -40,6 +40,9 @@ constexpr uint32_t kCA = 12 * 2048;
 constexpr int KC = 96, NCONV = 32, kFiltLog2 = 6;
 constexpr int kCMaps = 8;
 constexpr uint32_t kRows8 = 128 + KC / 8 - 1;
+constexpr int kMaxG = 8;     // clips per group (the margin buffers)
+constexpr int kMLeft = 160;  // margin sources kept in shared memory: outputs [0, 160) ...
+constexpr int kMRight = 192; // ... and [rb, rb + 192), rb = (n - 160) rounded down to 32
 
 struct BackParams {
   CUtensorMap hmap[kMaxLv];        // halving input: level a as rows of 256 samples
@@ -92,6 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
   uint64_t* cgrp_done = lvl_ready + 2 * kMaxLv;   // conv producer finished a group pair
   uint32_t* tslot = reinterpret_cast<uint32_t*>(cgrp_done + 1);
   int32_t* exps_s = reinterpret_cast<int32_t*>(tslot + 4);  // B ints
+  __half* mbuf = reinterpret_cast<__half*>((reinterpret_cast<uintptr_t>(exps_s + p.B) + 15) & ~uintptr_t(15));  // [kMaxG][kMLeft + kMRight]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < kHStages; ++i) {
@@ -311,34 +315,33 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
               for (int e = 0; e < 32; ++e)
                 if (i0 + e < n_out) drow[32 * c + e] = __float2half_rn(v[e]);
             }
+            // the outputs the reflect margins mirror, kept in shared memory for the margin pass
+            const int rb = (n_out - kMLeft) & ~31;
+            if (i0 < kMLeft || i0 >= rb) {
+              __half* mb = mbuf + bl * (kMLeft + kMRight) + (i0 < kMLeft ? i0 : kMLeft + i0 - rb);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                __align__(16) __half2 w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) w[e] = __floats2half2_rn(v[8 * u + 2 * e], v[8 * u + 2 * e + 1]);
+                *reinterpret_cast<uint4*>(mb + 8 * u) = *reinterpret_cast<const uint4*>(w);
+              }
+            }
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&hd_empty[d]);
         }
-        // level a + 1: reflect margins (np.pad "reflect", signal.py:245), zero tail, the conv's
-        // shifted copies (hop < 8); loads batched ahead of the stores (this CTA's own stores)
+        // level a + 1: reflect margins (np.pad "reflect", signal.py:245) from the shared-memory copy
+        // of the outputs they mirror, zero tail; then the conv's shifted copies (hop < 8)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         {
-          const int n_items = gc * 2 * kML;
-          for (int j0 = et; j0 < n_items; j0 += 8 * 128) {
-            __half v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = j0 + 128 * u;
-              if (j >= n_items) break;
-              const int bl = j / (2 * kML), r = j - bl * 2 * kML;
-              const int i = r < kML ? r + 1 : n_out - 1 - kML + (r - kML);
-              v[u] = dst[(int64_t)(b0 + bl) * dstride + kML + i];
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = j0 + 128 * u;
-              if (j >= n_items) break;
-              const int bl = j / (2 * kML), r = j - bl * 2 * kML;
-              const int i = r < kML ? r + 1 : n_out - 1 - kML + (r - kML);
-              dst[(int64_t)(b0 + bl) * dstride + (r < kML ? kML - i : kML + 2 * (n_out - 1) - i)] = v[u];
-            }
+          const int rb = (n_out - kMLeft) & ~31;
+          for (int j = et; j < gc * 2 * kML; j += 128) {
+            const int bl = j / (2 * kML), r = j - bl * 2 * kML;
+            const int i = r < kML ? r + 1 : n_out - 1 - kML + (r - kML);
+            const __half val = mbuf[bl * (kMLeft + kMRight) + (r < kML ? i : kMLeft + i - rb)];
+            dst[(int64_t)(b0 + bl) * dstride + (r < kML ? kML - i : kML + 2 * (n_out - 1) - i)] = val;
           }
           const int z0 = n_out + 2 * kML, nz = dstride - z0;
           for (int j = et; j < gc * nz; j += 128) {
@@ -517,7 +520,9 @@ int launch_cqt2010_back(const CqtBackArgs& g, cudaStream_t st) {
     }
   }
   const size_t smem = 1024 + kHStages * kKB + kERows * 128 + kCStages * kCA + KC / 8 * 512 +
-                      (2 * kHStages + 4 + 3 * kCStages + 2 * kMaxLv + 1) * 8 + 16 + 4 * (size_t)B;
+                      (2 * kHStages + 4 + 3 * kCStages + 2 * kMaxLv + 1) * 8 + 16 + 4 * (size_t)((B + 7) & ~7) +
+                      2 * kMaxG * (kMLeft + kMRight) + 16;
+  if (p.G > kMaxG) rc = NNAB_ENOTSUP;
   if (!rc && smem > 227 * 1024) rc = NNAB_ENOTSUP;
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(cqt2010_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -20,7 +20,7 @@ out = (C.c_ulonglong * 32)()
 fn(0, out)
 n = 148
 names = [("h-producer", ["cgrp_done", "lvl_ready", "h_empty"]), ("h-MMA", ["hd_empty", "h_full"]),
-         ("c-producer", ["lvl_ready", "c_mma"]), ("c-MMA", ["c_full", "c_tfree"]), ("h-epilogue", ["hd_full"]),
+         ("c-producer", ["lvl_ready", "c_mma"]), ("c-MMA", ["c_full", "c_tfree"]), ("h-epilogue", ["hd_full", "tiles(incl wait)", "margins+copies"]),
          ("c-epilogue", ["c_mma"])]
 print(f"elapsed {out[24] / n / 1e3:.1f}k cycles per CTA")
 for r, (nm, ws) in enumerate(names):
