@@ -254,7 +254,7 @@ def build_workload(name: str, device, mode: str, nb: int = B_CLIPS):
         eng = Cqt2010Engine(p["taps"], p["top_kernels"], p["early_stages"], p["n_octaves"], p["kernel_hop"],
                             p["first_bin"], 12, 84, "reflect", device=device, precision=precision)
         work = {"bound": "hbm", "per_batch": float(BYTES_CQT2010), "unit": "GB/s",
-                "kernel": "cqt2010v2 route (front + chain + conv)"}
+                "kernel": "cqt2010v2 route (front + back end)"}
         return eng, "magnitude", work, 2 + (p["early_stages"] - 2) + 6 + 7
     raise ValueError(name)
 
