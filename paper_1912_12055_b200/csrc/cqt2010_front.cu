@@ -99,11 +99,19 @@ NNAB_DEV bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity) {
       : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(20000u) : "memory");
   return ok != 0;
 }
+// per-role wait cycles only in a profiling build (-DNNAB_FRONT_PROF): the accumulators would
+// otherwise sit in local memory on every wait of the production kernel
 NNAB_DEV void wait_p(uint64_t* bar, uint32_t parity, unsigned long long& acc) {
+#ifdef NNAB_FRONT_PROF
   const long long t0 = clock64();
+#endif
   for (uint32_t it = 0; !mbar_try_wait_hint(bar, parity); ++it)
     if (it > (1u << 22)) __trap();  // a pipeline bug traps instead of hanging the GPU
+#ifdef NNAB_FRONT_PROF
   acc += (unsigned long long)(clock64() - t0);
+#else
+  (void)acc;
+#endif
 }
 
 __device__ long long g_front_tl[16 * 12];
