@@ -17,6 +17,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "internal.h"
@@ -24,6 +25,22 @@
 
 namespace nnab {
 namespace {
+
+// Split-K count for a reduction with `units` CTAs per split: the smallest count whose work
+// units fill whole waves of the persistent grid to >= 90 % (a TF32 CQT kernel gradient has 90
+// CTAs per split: 3 splits -> 1.82 of 2 waves instead of 0.61 of 1; its 3xTF32 form 178: 3 ->
+// 3.6 of 4 instead of 1.2 of 2).
+int auto_splits(int64_t units, int64_t kb) {
+  const int n = num_sms();
+  int best = 1;
+  double best_e = 0.;
+  for (int s = 1; s <= 16 && s <= kb; ++s) {
+    const double w = (double)units * s / n, e = w / std::ceil(w);
+    if (w >= 0.9 && e >= 0.9) return s;
+    if (w >= 0.9 && e > best_e) { best_e = e; best = s; }
+  }
+  return best_e > 0. ? best : std::max(1, (int)std::min<int64_t>(kb, n / std::max<int64_t>(1, units)));
+}
 
 constexpr int kBM = 128, kBN = 256, kThreads = 256, kStages = 4;
 constexpr int kStg = 36;  // epilogue transpose row stride (floats)
@@ -520,8 +537,8 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.n_tiles = (g.N + TBN - 1) / TBN;
   const int tiles = p.m_tiles * p.n_tiles;
   const int units = (kPair ? (p.m_tiles + 1) / 2 * 2 : p.m_tiles) * p.n_tiles;  // CTAs per split
-  int splits = (g.coef_re || g.frames_R) ? 1 : g.splits > 0 ? g.splits : std::max(1, num_sms() / std::max(1, units));
   const int64_t kb = g.K / C::BK;
+  int splits = (g.coef_re || g.frames_R) ? 1 : g.splits > 0 ? g.splits : auto_splits(units, kb);
   splits = (int)std::min<int64_t>(splits, kb);
   p.k_per_split = (kb + splits - 1) / splits * C::BK;
   p.splits = (int)((g.K + p.k_per_split - 1) / p.k_per_split);
@@ -582,9 +599,12 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
 size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits) {
   const int64_t mt = (M + kBM - 1) / kBM;
   const int64_t nt = (N + 2 * kBN - 1) / (2 * kBN) * 2;  // 256-column tiles, even: covers the wide layout
-  // auto split count: the largest any mode picks (fewest CTAs per split: wide pairs)
-  const int64_t units = std::min<int64_t>(mt * ((N + kBN - 1) / kBN), (mt + 1) / 2 * 2 * (nt / 2));
-  if (splits <= 0) splits = std::max(1, num_sms() / (int)std::max<int64_t>(1, units));
+  if (splits <= 0) {  // auto split count: the largest any tile form picks
+    const int64_t kb = std::max<int64_t>(1, K / 16);
+    const int64_t u_single = mt * ((N + kBN - 1) / kBN), u_pair = (mt + 1) / 2 * 2 * ((N + kBN - 1) / kBN),
+                  u_wide = (mt + 1) / 2 * 2 * (nt / 2);
+    splits = std::max(auto_splits(u_single, kb), std::max(auto_splits(u_pair, kb), auto_splits(u_wide, kb)));
+  }
   return (size_t)splits * mt * kBM * nt * kBN * sizeof(float);
 }
 
