@@ -18,6 +18,7 @@ caller's choice of upstream scaling).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -64,6 +65,11 @@ class DftLayerOp:
             if self.fwd_prec == L.PREC_3XTF32:
                 self.fwd_engine.precision = L.PREC_3XTF32
                 self.fwd_engine.set_bank(h_re, h_im)
+        # FP32 mode: the kernel gradient runs 3xF16 on the forward's FP16 staging
+        # (nnab_kernel_grad_f16) where that staging holds hop rows of 64-sample multiples
+        hop, k64 = eng.hop, (eng.n_fft + 63) // 64 * 64
+        self.f16_dk = (self.split and self.fwd_engine is not None and self.fwd_prec == L.PREC_3XF16
+                       and hop % 64 == 0 and hop <= k64 and os.environ.get("NNAB_F16_DK", "1") != "0")
 
     @staticmethod
     def _f16_same_rows(n_fft: int, hop: int) -> bool:
@@ -97,8 +103,8 @@ class DftLayerOp:
         f = eng.frames(B, length)
         stream = L.stream_handle(self.device)
         fe = self.fwd_engine if (phasor_grads or self.split) else None
-        if fe is not None and self.fwd_prec == L.PREC_3XTF32:
-            ws = None  # one 3xTF32 staging: its hi rows are the TF32 frames the dK GEMM reads
+        if fe is not None and (self.fwd_prec == L.PREC_3XTF32 or self.f16_dk):
+            ws = None  # one staging: the forward's rows are the frames the dK GEMM reads
         else:
             ws = torch.empty(lib.nnab_stft_workspace_bytes(C.byref(f), self.prec), dtype=torch.uint8,
                              device=self.device)
@@ -176,6 +182,11 @@ class DftLayerOp:
                                b_row_len, b_rows, c.data_ptr(), ldc, splits, part.data_ptr(), self.prec,
                                L.stream_handle(self.device)), "rgemm")
 
+    def _f16_operands(self, F, ld):
+        """FP16 hi/lo coef [2F][ld] and the int32 row exponents [2F + 1] of the 3xF16 dK"""
+        c16 = tuple(torch.empty(2 * F, ld, dtype=torch.float16, device=self.device) for _ in range(2))
+        return c16, torch.empty(2 * F + 1, dtype=torch.int32, device=self.device)
+
     # ------------------------------------------------------------ backward
     def backward(self, saved: dict, g: torch.Tensor, h_re=None, h_im=None, mel_w: torch.Tensor | None = None,
                  need_bank: bool = True, need_mel: bool = False, need_x: bool = False):
@@ -189,6 +200,7 @@ class DftLayerOp:
         f = eng.frames(B, length)
         grads = {}
         ds = None
+        use16 = self.f16_dk and need_bank
         if mel_w is not None:
             nm = int(mel_w.shape[0])
             gsp = (_f32(nm, ld, self.device), _f32(nm, ld, self.device) if self.split else None)
@@ -208,25 +220,52 @@ class DftLayerOp:
                 L.check(lib.nnab_transpose_pad(mel_w.detach().float().contiguous().data_ptr(), nm, F, kp, self.prec,
                                                wt_hi.data_ptr(), L.ptr(wt_lo), stream), "transpose_pad")
                 # coef = (dS*re/S, dS*im/S) straight from the dS GEMM's epilogue
-                coef_hi = _f32(2 * F, ld, self.device)
-                coef_lo = _f32(2 * F, ld, self.device) if self.split else None
-                L.check(lib.nnab_mel_dft_coef(F, ld, kp, wt_hi.data_ptr(), L.ptr(wt_lo), gsp[0].data_ptr(),
-                                              L.ptr(gsp[1]), nm, saved["re"].data_ptr(), L.ptr(saved["im"]),
-                                              self.eps, self.prec, coef_hi.data_ptr(), L.ptr(coef_lo), stream),
-                        "mel_dft_coef")
+                if use16:  # the 3xF16 dK operand
+                    c16, rexp = self._f16_operands(F, ld)
+                    L.check(lib.nnab_mel_dft_coef_f16(
+                        C.byref(f), saved["ws"].data_ptr(), saved["ws"].numel(), F, ld, kp, wt_hi.data_ptr(),
+                        wt_lo.data_ptr(), gsp[0].data_ptr(), gsp[1].data_ptr(), nm, saved["re"].data_ptr(),
+                        saved["im"].data_ptr(), self.eps, c16[0].data_ptr(), c16[1].data_ptr(), rexp.data_ptr(),
+                        stream), "mel_dft_coef_f16")
+                if need_x or not use16:
+                    coef_hi = _f32(2 * F, ld, self.device)
+                    coef_lo = _f32(2 * F, ld, self.device) if self.split else None
+                    L.check(lib.nnab_mel_dft_coef(F, ld, kp, wt_hi.data_ptr(), L.ptr(wt_lo), gsp[0].data_ptr(),
+                                                  L.ptr(gsp[1]), nm, saved["re"].data_ptr(), L.ptr(saved["im"]),
+                                                  self.eps, self.prec, coef_hi.data_ptr(), L.ptr(coef_lo), stream),
+                            "mel_dft_coef")
                 ds = True
         if not (need_bank or need_x):
             if self.reducer is not None:
                 self.reducer.wait()
             return grads
-        if ds is None:
+        if ds is None and (need_x or not use16):
             coef_hi = _f32(2 * F, ld, self.device)
             coef_lo = _f32(2 * F, ld, self.device) if self.split else None
             L.check(lib.nnab_dft_coef(None, g.data_ptr(), saved["re"].data_ptr(), L.ptr(saved["im"]), F, B, T,
                                       R, ld, self.eps, self.prec, coef_hi.data_ptr(), L.ptr(coef_lo), stream),
                     "dft_coef")
         ws = saved["ws"]
-        if need_bank:
+        if use16 and ds is None:  # conv layer: coef from g directly
+            c16, rexp = self._f16_operands(F, ld)
+            L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), g.data_ptr(), saved["re"].data_ptr(),
+                                          saved["im"].data_ptr(), F, T, ld, self.eps, c16[0].data_ptr(),
+                                          c16[1].data_ptr(), rexp.data_ptr(), stream), "dft_coef_f16")
+        if need_bank and use16:
+            dk = _f32(2 * F, n_fft, self.device)
+            blocks = [(0, 2 * F)] if self.reducer is None or 2 * F <= 1280 else [(0, 1024), (1024, 2 * F)]
+            for r0, r1 in blocks:
+                part = torch.empty(max(lib.nnab_rgemm_partial_bytes(r1 - r0, n_fft, ld, 0) // 4, 1),
+                                   device=self.device)
+                L.check(lib.nnab_kernel_grad_f16(C.byref(f), c16[0].data_ptr() + 2 * r0 * ld,
+                                                 c16[1].data_ptr() + 2 * r0 * ld, r1 - r0, ld,
+                                                 rexp.data_ptr() + 4 * r0, dk.data_ptr() + 4 * r0 * n_fft, n_fft,
+                                                 ws.data_ptr(), ws.numel(), part.data_ptr(), 0, stream),
+                        "kernel_grad_f16")
+                if self.reducer is not None:
+                    self.reducer.launch(dk[r0:r1])
+            grads["h_re"], grads["h_im"] = dk[:F], dk[F:]
+        elif need_bank:
             dk = _f32(2 * F, n_fft, self.device)
             # with a reducer: rows [0, 1024) first (whole 256-row tiles), all-reduced while
             # the remaining rows' GEMM runs; without: one launch over all 2F rows

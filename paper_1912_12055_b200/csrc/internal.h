@@ -119,6 +119,14 @@ struct RGemmArgs {
   // written to c[(b*M + m)*T + t] for t < T (the (B, M, T) layout), nothing else
   int64_t frames_B = 0;
   int32_t frames_R = 0, frames_T = 0;
+  // 3xF16 kernel gradient (precision NNAB_PREC_3XF16): a_hi/a_lo and b_hi/b_lo are FP16
+  // (lda in halves, B the MN-major staged hop rows); C rows are scaled by 2^-row_exp[m]
+  const int32_t* row_exp = nullptr;
+  // coef epilogue in FP16 (3xTF32 coef GEMM, coef_f16 = 1): c / coef_lo are FP16 hi/lo of
+  // coef * 2^(row_exp[row] - clip_exp[slot / clip_R]) (0 past n_clips); ldc in halves
+  const int32_t* clip_exp = nullptr;
+  int64_t n_clips = 0;
+  int32_t clip_R = 0, coef_f16 = 0;
 };
 size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits);
 // fused tensor-core CQT2010v2 (cqt2010_tc.cu); NNAB_ENOTSUP outside its envelope

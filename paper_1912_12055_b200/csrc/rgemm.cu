@@ -43,15 +43,31 @@ int auto_splits(int64_t units, int64_t kb) {
 }
 
 constexpr int kBM = 128, kBN = 256, kThreads = 256, kStages = 4;
-constexpr int kStg = 36;  // epilogue transpose row stride (floats)
 
-template <bool kSplit>
+// 3xF16 TMEM accumulation chunk (K per chain before the FP32 drain into C); NNAB_RGEMM_F16_CHUNK
+int f16_chunk() {
+  static const int c = [] {
+    const char* e = getenv("NNAB_RGEMM_F16_CHUNK");
+    const int v = e ? atoi(e) : 2048;
+    return v >= 64 && v % 64 == 0 ? v : 2048;
+  }();
+  return c;
+}
+constexpr int kStg = 36;  // epilogue transpose row stride (floats)
+// 3xF16 epilogue: per warp two 32 x 32 fp32 staging tiles (128-byte swizzle) that TMA
+// stores / reduce-adds into C
+constexpr int kF16Stg = 4 * 2 * 4096;
+
+// kF16 (3xF16, CTA pairs only): FP16 hi/lo operands, 64 K per stage, a stage holds
+// A hi | A lo | this CTA's half of B hi | of B lo.
+template <bool kSplit, bool kF16 = false>
 struct RCfg {
-  static constexpr int BK = kSplit ? 16 : 32;
-  static constexpr int SWZ = BK * 4;
-  static constexpr int A_BYTES = kBM * BK * 4;
-  static constexpr int B_BYTES = kBN * BK * 4;
-  static constexpr int STAGE = (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);
+  static constexpr int BK = kF16 ? 64 : kSplit ? 16 : 32;
+  static constexpr int EB = kF16 ? 2 : 4;  // element bytes
+  static constexpr int SWZ = BK * EB;
+  static constexpr int A_BYTES = kBM * BK * EB;
+  static constexpr int B_BYTES = kBN * BK * EB;
+  static constexpr int STAGE = kF16 ? 2 * (A_BYTES + B_BYTES / 2) : (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);
   static constexpr int NUM_ACC = kSplit ? 1 : 2;
   static constexpr int ACC_STRIDE = kSplit ? 512 : 256;
 };
@@ -70,6 +86,11 @@ struct RParams {
   float eps;
   int64_t fB;  // frames output (RGemmArgs::frames_R > 0)
   int32_t fR, fT;
+  const int32_t* row_exp;   // RGemmArgs::row_exp
+  const int32_t* clip_exp;  // RGemmArgs::clip_exp (coef_f16)
+  int64_t n_clips;
+  int32_t clip_R, coef_f16;
+  int32_t c_split_rows;  // kF16: rows of C (its tensor map) per split (0: C is the output)
 };
 
 NNAB_DEV float4 tf32_hi4(float4 a) { return make_float4(tf32_rne(a.x), tf32_rne(a.y), tf32_rne(a.z), tf32_rne(a.w)); }
@@ -95,6 +116,16 @@ NNAB_DEV uint64_t kdesc(const void* p, int swz) {
   d |= (uint64_t)(swz == 128 ? 2 : 4) << 61;
   return d;
 }
+// MN-major FP16, 128-byte swizzle: K-rows of 128 B (64 MN elements), 8-row atoms
+// SBO = 1024 B apart along K, 64-element MN atoms LBO apart.
+NNAB_DEV uint64_t mndesc_f16(uint32_t addr, uint32_t lbo) {
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
 // MN-major TF32 uses the "128B_BASE32B" layout (32-byte units swizzled in a
 // 128-byte row, 4 K-rows per atom; TMA SWIZZLE_128B_ATOM_32B): K-rows of 128 B
 // (32 MN elements), SBO = 4 rows = 512 B between K groups, MN atoms LBO apart.
@@ -115,24 +146,28 @@ NNAB_DEV uint64_t mndesc(const void* p, int /*swz*/, uint32_t lbo) {
 // 512 TMEM columns (one accumulator), a quarter less L2 traffic per MAC again.
 // kE8: the phasor coef epilogue (nnab_mel_dft_coef, TF32) on 8 epilogue warps
 // (384 threads, 3 stages): its HBM-latency-bound loads get twice the warps in flight.
-template <bool kSplit, bool kPair, bool kWide, bool kE8 = false>
+// kF16: the 3xF16 kernel gradient (nnab_kernel_grad_f16) -- A = coef rows scaled by
+// 2^(row_exp - clip_exp) as FP16 hi/lo, B = the 3xF16 forward's staged frames (MN-major
+// hop rows, x 2^clip_exp); the epilogue undoes 2^row_exp.
+template <bool kSplit, bool kPair, bool kWide, bool kE8 = false, bool kF16 = false>
 __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
     rgemm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                  const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-                 const RParams p) {
-  using C = RCfg<kSplit>;
+                 const __grid_constant__ CUtensorMap tc, const RParams p) {
+  using C = RCfg<kSplit, kF16>;
+  static_assert(!kF16 || (kSplit && kPair && !kWide && !kE8), "3xF16: split CTA-pair tiles");
   static_assert(!kWide || (kPair && !kSplit), "wide tiles are a TF32 pair mode");
   constexpr int TBN = kWide ? 2 * kBN : kBN;     // tile columns
   constexpr int NACC = kWide ? 1 : C::NUM_ACC;   // TMEM accumulators
   constexpr int kBNc = kPair ? kBN / 2 : kBN;  // B columns this CTA stages per MMA
   constexpr int kHalves = kWide ? 2 : 1;       // N=256 MMAs per K step
-  constexpr int NST = kE8 ? 3 : kStages;        // pipeline stages
+  constexpr int NST = (kE8 || kF16) ? 3 : kStages;  // pipeline stages
   constexpr int kEW = kE8 ? 8 : 4;              // epilogue warps
   static_assert(!kE8 || (!kSplit && !kWide), "8-warp epilogue: TF32 coef GEMM only");
   const uint32_t rank = kPair ? cluster_ctarank() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * C::STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * C::STAGE + (kF16 ? kF16Stg : 0));
   uint64_t* full = bars;
   uint64_t* empty = bars + NST;
   uint64_t* tfull = bars + 2 * NST;
@@ -178,7 +213,22 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
         for (int64_t k = k_lo; k < k_hi; k += C::BK) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * C::STAGE;
-          if (kPair) {  // both CTAs' bytes complete on the leader's barrier
+          if constexpr (kF16) {
+            const uint32_t fb = mapa(&full[s], 0);
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * C::STAGE);
+            tma_load_2d_pair(st, &ta_hi, fb, (int)k, mt * kBM, pol);
+            tma_load_2d_pair(st + C::A_BYTES, &ta_lo, fb, (int)k, mt * kBM, pol);
+            const int nb = nt * kBN + (int)rank * kBNc;
+            int col = nb % p.b_row_len, row = (int)(k + nb / p.b_row_len);
+#pragma unroll
+            for (int j = 0; j < kBNc / 64; ++j) {  // boxes of {64 n, 64 k}: 8 KB, one MN atom column
+              tma_load_2d_pair(st + 2 * C::A_BYTES + j * 8192, &tb_hi, fb, col, row, pol);
+              tma_load_2d_pair(st + 2 * C::A_BYTES + C::B_BYTES / 2 + j * 8192, &tb_lo, fb, col, row, pol);
+              if ((col += 64) == p.b_row_len) col = 0, ++row;  // b_row_len % 64 == 0
+            }
+            if (++s == NST) { s = 0; ph ^= 1; }
+            continue;
+          } else if (kPair) {  // both CTAs' bytes complete on the leader's barrier
             const uint32_t fb = mapa(&full[s], 0);
             if (rank == 0)
               mbar_expect_tx(&full[s], 2 * (C::A_BYTES + kHalves * C::B_BYTES / 2) * (kSplit ? 2 : 1));
@@ -248,6 +298,24 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
             mbar_wait(&full[s], ph);
             tc_fence_after();
             uint8_t* st = smem + s * C::STAGE;
+            if constexpr (kF16) {
+              constexpr uint32_t idf = idesc_f16(2 * kBM, kBN) | (1u << 16);  // B MN-major
+              const uint32_t sa = smem_u32(st), sb = sa + 2 * C::A_BYTES;
+#pragma unroll
+              for (int kk = 0; kk < C::BK / 16; ++kk) {
+                const uint64_t a = sdesc_kmajor_sw128_addr(sa + kk * 32);
+                const uint64_t a_lo = sdesc_kmajor_sw128_addr(sa + C::A_BYTES + kk * 32);
+                const uint64_t b = mndesc_f16(sb + kk * 2048, 8192);  // 16 K rows = two 8-row atoms
+                const uint64_t b_lo = mndesc_f16(sb + C::B_BYTES / 2 + kk * 2048, 8192);
+                mma_f16_pair(d, a, b, idf, first ? 0u : 1u);
+                mma_f16_pair(d + kBN, a, b_lo, idf, first ? 0u : 1u);
+                mma_f16_pair(d + kBN, a_lo, b, idf, 1u);
+                first = false;
+              }
+              mma_commit_pair(&empty[s], 0x3);
+              if (++s == NST) { s = 0; ph ^= 1; }
+              continue;
+            }
             const uint64_t a = kdesc(st, C::SWZ);
             const uint64_t a_lo = kdesc(st + C::A_BYTES + C::B_BYTES, C::SWZ);
             // MN-major B: the kBN/32 boxes are C::BK*128 bytes apart (LBO)
@@ -292,6 +360,67 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
     // for float4) and leaves as float4 runs of 8 lanes per row: every global
     // access is a full 128-byte line instead of 32 rows x 16 B.
     const uint32_t ew = warp - 4, q = ew & 3;  // TMEM lane quarter
+    if constexpr (kF16) {
+      // Drain per TMEM chunk: main + correction accumulators -> registers (thread = row),
+      // x 2^-row_exp, into a swizzled staging tile, then TMA: the split's first chunk
+      // stores, later ones reduce-add in L2 (no read-modify-write round trip through the
+      // SM).  TMEM is released right after the last tcgen05.ld, so the MMAs of the next
+      // chunk overlap the stores.  Chunk d's reduce-adds are issued only after chunk
+      // d - 1's completed: a fixed summation order (deterministic).
+      uint8_t* stg16 = smem + NST * C::STAGE + ew * 8192;
+      const uint32_t tempty0 = mapa(&tempty[0], 0);
+      uint32_t aph = 0;
+      for (int w = w_start; w < n_work; w += w_step) {
+        const int sp = w % p.splits, tile = w / p.splits;
+        const int mt = (tile / p.n_tiles) * 2 + (int)rank, nt = tile % p.n_tiles;
+        const int64_t k_lo = sp * p.k_per_split;
+        const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
+        const int m_base = mt * kBM + (int)q * 32;
+        const int crow = sp * p.c_split_rows + m_base;
+        const int m = m_base + (int)lane;
+        const float rs = m < p.M ? __int_as_float((127 - p.row_exp[m]) << 23) : 0.f;
+        for (int64_t kc = k_lo; kc < k_hi; kc += p.k_chunk) {
+          const bool first_chunk = kc == k_lo;
+          mbar_wait(&tfull[0], aph);
+          tc_fence_after();
+          const uint32_t tb = tbase + ((q * 32) << 16);
+          if (lane == 0) bulk_wait_all();  // the previous chunk's stores / adds have landed
+          __syncwarp();
+#pragma unroll 1
+          for (int c = 0; c < kBN / 32; ++c) {
+            float v[32], u[32];
+            tmem_ld32(tb + c * 32, v);
+            tmem_ld32(tb + kBN + c * 32, u);
+            tmem_ld_wait();
+            if (c == kBN / 32 - 1) {  // accumulators read: the next chunk's MMAs may start
+              tc_fence_before();
+              mbar_arrive_cluster(tempty0);
+            }
+            uint8_t* buf = stg16 + (c & 1) * 4096;
+            if (c >= 2) {
+              if (lane == 0) bulk_wait_read_n<1>();  // chunk c - 2's copy has read this buffer
+              __syncwarp();
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                  make_float4((v[4 * j] + u[4 * j]) * rs, (v[4 * j + 1] + u[4 * j + 1]) * rs,
+                              (v[4 * j + 2] + u[4 * j + 2]) * rs, (v[4 * j + 3] + u[4 * j + 3]) * rs);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && m_base < p.M) {  // a pair's rows past M: nothing (they would reach the next split)
+              const int col = nt * kBN + c * 32;
+              if (first_chunk) tma_store_2d(&tc, buf, col, crow);
+              else tma_reduce_add_2d(&tc, buf, col, crow);
+              bulk_commit();
+            }
+          }
+          aph ^= 1;
+        }
+      }
+      if (lane == 0) bulk_wait_all();
+      __syncwarp();
+    } else {
     const int hsel = kE8 ? (int)(ew >> 2) : 0;  // kE8: warps 4-7 even chunks, 8-11 odd ones
     constexpr int CSTEP = kE8 ? 2 : 1;
     float* stg = reinterpret_cast<float*>(smem + NST * C::STAGE + 128) + ew * 32 * kStg;
@@ -401,6 +530,56 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
                 ii[it] = __ldcs(reinterpret_cast<const float4*>(p.im + o));
               }
             }
+            if (p.coef_f16) {  // FP16 hi/lo of coef * 2^(row_exp[m] - clip_exp[slot]) (3xF16 dK operand)
+              float es[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int64_t b = (int64_t)(n + j) / p.clip_R;
+                es[j] = b < p.n_clips ? __int_as_float((127 - p.clip_exp[b]) << 23) : 0.f;  // |e| <= 100
+              }
+              __half* ch = reinterpret_cast<__half*>(p.C);
+              __half* cl = reinterpret_cast<__half*>(p.c_lo);
+#pragma unroll
+              for (int it = 0; it < 8; ++it) {
+                const int m = m_base + it * 4 + sr;
+                if (m >= p.M) continue;
+                const float rs = __int_as_float((127 + p.row_exp[m]) << 23);  // |row_exp| <= 125
+                const int64_t o = (int64_t)m * p.ldc + n, o2 = o + (int64_t)p.M * p.ldc;
+                const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
+                float rr_[4] = {rr[it].x, rr[it].y, rr[it].z, rr[it].w}, ii_[4] = {ii[it].x, ii[it].y, ii[it].z, ii[it].w};
+                __half hr[4], lr[4], hi4[4], li4[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  if (!full4) {
+                    if (n + j >= p.N) { rr_[j] = 0.f; ii_[j] = 0.f; }
+                    else { rr_[j] = p.re[o + j]; ii_[j] = p.im[o + j]; }
+                  }
+                  float cr, ci;
+                  coef_store(dv[j], rr_[j], ii_[j], p.eps, cr, ci);
+                  cr = cr * es[j] * rs;
+                  ci = ci * es[j] * rs;
+                  hr[j] = __float2half_rn(cr);
+                  lr[j] = __float2half_rn(cr - __half2float(hr[j]));
+                  hi4[j] = __float2half_rn(ci);
+                  li4[j] = __float2half_rn(ci - __half2float(hi4[j]));
+                }
+                if (full4) {
+                  __stcs(reinterpret_cast<uint2*>(ch + o), *reinterpret_cast<const uint2*>(hr));
+                  __stcs(reinterpret_cast<uint2*>(cl + o), *reinterpret_cast<const uint2*>(lr));
+                  __stcs(reinterpret_cast<uint2*>(ch + o2), *reinterpret_cast<const uint2*>(hi4));
+                  __stcs(reinterpret_cast<uint2*>(cl + o2), *reinterpret_cast<const uint2*>(li4));
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    if (n + j >= p.N) continue;
+                    ch[o + j] = hr[j];
+                    cl[o + j] = lr[j];
+                    ch[o2 + j] = hi4[j];
+                    cl[o2 + j] = li4[j];
+                  }
+                }
+              }
+            } else {
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
               const int m = m_base + it * 4 + sr;
@@ -434,6 +613,7 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
                 }
               }
             }
+            }  // !coef_f16
           } else if (p.fR) {  // one chunk, no split: the slot tile lands in (B, M, T) directly
             const int64_t b = n / p.fR;  // R % 4 == 0: the lane's 4 slots share a clip
             const int t0 = (int)(n - b * p.fR);
@@ -459,6 +639,15 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
               if (!first_chunk && m < p.M && full4)
                 cur[it] = *reinterpret_cast<const float4*>(cbase + (int64_t)m * p.ldc + n);
             }
+            if (p.row_exp) {  // undo the operand's per-row 2^row_exp (exact)
+#pragma unroll
+              for (int it = 0; it < 8; ++it) {
+                const int m = m_base + it * 4 + sr;
+                if (m >= p.M) continue;
+                const float rs = __int_as_float((127 - p.row_exp[m]) << 23);
+                d[it] = make_float4(d[it].x * rs, d[it].y * rs, d[it].z * rs, d[it].w * rs);
+              }
+            }
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
               const int m = m_base + it * 4 + sr;
@@ -483,6 +672,7 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
         if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
     }
+    }  // !kF16
   }
   tc_fence_before();
   __syncthreads();
@@ -506,14 +696,23 @@ __global__ void sum_splits_kernel(const float* __restrict__ parts, int32_t split
   }
 }
 
-template <bool kSplit, bool kPair, bool kWide = false, bool kE8 = false>
+template <bool kSplit, bool kPair, bool kWide = false, bool kE8 = false, bool kF16 = false>
 int launch(const RGemmArgs& g, cudaStream_t st) {
-  using C = RCfg<kSplit>;
+  using C = RCfg<kSplit, kF16>;
   constexpr int kBNc = kPair ? kBN / 2 : kBN;
   constexpr int TBN = kWide ? 2 * kBN : kBN;
-  if (g.K % C::BK || g.lda % 4 || (g.b_mn && g.b_row_len % 32) || (!g.b_mn && g.ldb % 4)) return NNAB_EINVAL;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
-  int rc = make_tmap_2d(&ta_hi, g.a_hi, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
+  int rc = NNAB_OK;
+  if (kF16) {  // K need not be a multiple of BK: the tail boxes are zero-filled past K and b_rows
+    if (g.lda % 8 || !g.b_mn || g.b_row_len % 64 || !g.a_lo || !g.b_lo || !g.row_exp) return NNAB_EINVAL;
+    rc = make_tmap_2d(&ta_hi, g.a_hi, g.K, g.M, (uint64_t)g.lda * 2, 64, kBM, 128, 2);
+    if (!rc) rc = make_tmap_2d(&ta_lo, g.a_lo, g.K, g.M, (uint64_t)g.lda * 2, 64, kBM, 128, 2);
+    if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 2, 64, 64, 128, 2);
+    if (!rc) rc = make_tmap_2d(&tb_lo, g.b_lo, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 2, 64, 64, 128, 2);
+  } else if (g.K % C::BK || g.lda % 4 || (g.b_mn && g.b_row_len % 32) || (!g.b_mn && g.ldb % 4)) {
+    return NNAB_EINVAL;
+  } else {
+  rc = make_tmap_2d(&ta_hi, g.a_hi, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
   if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, g.a_lo, g.K, g.M, (uint64_t)g.lda * 4, C::BK, kBM, C::SWZ);
   if (!g.b_mn) {
     if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.K, g.N, (uint64_t)g.ldb * 4, C::BK, kBNc, C::SWZ);
@@ -523,6 +722,7 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
     if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 4, 32, C::BK, -128);
     if (!rc && kSplit)
       rc = make_tmap_2d(&tb_lo, g.b_lo, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 4, 32, C::BK, -128);
+  }
   }
   if (rc) return rc;
   if (!kSplit) {
@@ -537,13 +737,13 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.n_tiles = (g.N + TBN - 1) / TBN;
   const int tiles = p.m_tiles * p.n_tiles;
   const int units = (kPair ? (p.m_tiles + 1) / 2 * 2 : p.m_tiles) * p.n_tiles;  // CTAs per split
-  const int64_t kb = g.K / C::BK;
+  const int64_t kb = (g.K + C::BK - 1) / C::BK;
   int splits = (g.coef_re || g.frames_R) ? 1 : g.splits > 0 ? g.splits : auto_splits(units, kb);
   splits = (int)std::min<int64_t>(splits, kb);
   p.k_per_split = (kb + splits - 1) / splits * C::BK;
   p.splits = (int)((g.K + p.k_per_split - 1) / p.k_per_split);
-  p.k_chunk = (kSplit ? 1024 : kWide ? 8192 : 2048);  // accumulate steps per TMEM chain (wide: no
-                                                       // second accumulator, so drain less often)
+  p.k_chunk = (kF16 ? f16_chunk() : kSplit ? 1024 : kWide ? 8192 : 2048);  // accumulate steps per TMEM
+                                                    // chain (wide: no second accumulator, so drain less often)
   p.b_mn = g.b_mn;
   p.b_row_len = g.b_mn ? g.b_row_len : 1 << 30;
   p.re = g.coef_re;
@@ -553,21 +753,39 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.fB = g.frames_B;
   p.fR = g.frames_R;
   p.fT = g.frames_T;
+  p.row_exp = g.row_exp;
+  p.clip_exp = g.clip_exp;
+  p.n_clips = g.n_clips;
+  p.clip_R = g.clip_R;
+  p.coef_f16 = g.coef_f16;
+  if (p.coef_f16 && (!kSplit || kF16 || !p.re || !p.im || !p.row_exp || !p.clip_exp || p.clip_R < 1 || g.ldc % 4))
+    return NNAB_EINVAL;
   if (p.fR && (p.fR % 4 || p.splits != 1 || kb > p.k_chunk / C::BK || g.alpha != 1.f || p.re)) return NNAB_EINVAL;
   if (p.re && (p.splits != 1 || kb > p.k_chunk / C::BK || g.alpha != 1.f)) return NNAB_EINVAL;  // one TMEM chain
-  const bool direct = p.splits == 1 && g.alpha == 1.f;
+  const bool direct = p.splits == 1 && g.alpha == 1.f && (!kF16 || g.ldc % 4 == 0);  // kF16: TMA row stride
   p.C = direct ? g.c : g.partial;
   p.ldc = direct ? g.ldc : (int64_t)p.n_tiles * TBN;
   p.split_stride = (int64_t)p.m_tiles * kBM * p.ldc;
   if (!direct && !g.partial) return NNAB_EINVAL;
-  const size_t smem = 1024 + (kE8 ? 3 : kStages) * C::STAGE + 128 + (kE8 ? 8 : 4) * 32 * kStg * 4;
+  CUtensorMap tc = ta_hi;
+  p.c_split_rows = 0;
+  if (kF16) {  // C (or the split partials) as a 2-D fp32 tensor, 32 x 32 boxes, 128-byte swizzle
+    if (direct) rc = make_tmap_2d(&tc, p.C, g.N, g.M, (uint64_t)p.ldc * 4, 32, 32, 128, 4);
+    else {
+      p.c_split_rows = p.m_tiles * kBM;
+      rc = make_tmap_2d(&tc, p.C, p.ldc, (uint64_t)p.splits * p.c_split_rows, (uint64_t)p.ldc * 4, 32, 32, 128, 4);
+    }
+    if (rc) return rc;
+  }
+  const size_t smem = 1024 + ((kE8 || kF16) ? 3 : kStages) * C::STAGE + 128 +
+                      (kF16 ? kF16Stg : (kE8 ? 8 : 4) * 32 * kStg * 4);
   constexpr int threads = kE8 ? 384 : kThreads;
-  auto k = rgemm_kernel<kSplit, kPair, kWide, kE8>;
+  auto k = rgemm_kernel<kSplit, kPair, kWide, kE8, kF16>;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   (void)tiles;
   if (!kPair) {
     const int grid = std::min(units * p.splits, num_sms());
-    k<<<grid, threads, smem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+    k<<<grid, threads, smem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, tc, p);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(std::min(units * p.splits, num_sms() / 2 * 2));
@@ -581,7 +799,7 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    NNAB_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, ta_hi, ta_lo, tb_hi, tb_lo, p));
+    NNAB_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, ta_hi, ta_lo, tb_hi, tb_lo, tc, p));
   }
   NNAB_LAUNCHED();
   if (!direct) {
@@ -600,10 +818,11 @@ size_t rgemm_partial_bytes(int32_t M, int32_t N, int64_t K, int32_t splits) {
   const int64_t mt = (M + kBM - 1) / kBM;
   const int64_t nt = (N + 2 * kBN - 1) / (2 * kBN) * 2;  // 256-column tiles, even: covers the wide layout
   if (splits <= 0) {  // auto split count: the largest any tile form picks
-    const int64_t kb = std::max<int64_t>(1, K / 16);
+    const int64_t kb = std::max<int64_t>(1, K / 16), kb64 = std::max<int64_t>(1, (K + 63) / 64);
     const int64_t u_single = mt * ((N + kBN - 1) / kBN), u_pair = (mt + 1) / 2 * 2 * ((N + kBN - 1) / kBN),
                   u_wide = (mt + 1) / 2 * 2 * (nt / 2);
     splits = std::max(auto_splits(u_single, kb), std::max(auto_splits(u_pair, kb), auto_splits(u_wide, kb)));
+    splits = std::max(splits, auto_splits(u_pair, kb64));  // 3xF16 (64 K per block)
   }
   return (size_t)splits * mt * kBM * nt * kBN * sizeof(float);
 }
@@ -621,6 +840,7 @@ int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s) {
     const bool pair = pair_ok && (pair_env >= 2 || g.M > kBM);
     return pair ? launch<true, true>(g, s) : launch<true, false>(g, s);
   }
+  if (precision == NNAB_PREC_3XF16) return launch<true, true, false, false, true>(g, s);
   if (precision == NNAB_PREC_TF32) {
     const bool pair = pair_ok && (pair_env >= 2 || g.M > kBM);  // one m tile: the peer would idle
     const bool wide = pair && !g.coef_re && (pair_env == 3 || (pair_env == 1 && g.N > kBN && g.K >= 65536));

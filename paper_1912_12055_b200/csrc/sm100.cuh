@@ -188,6 +188,23 @@ NNAB_DEV void bulk_store(void* gdst, const void* src, uint32_t bytes) {
 // Wait until the bulk stores committed so far have read their shared-memory source.
 NNAB_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
+// 2-D tensor store / reduce-add shared -> global (bulk group; commit with bulk_commit).
+NNAB_DEV void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tmap), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+NNAB_DEV void tma_reduce_add_2d(const void* tmap, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tmap),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+NNAB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N committed groups still reading shared memory / still in flight at all
+template <int N>
+NNAB_DEV void bulk_wait_read_n() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+NNAB_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Arrive on an mbarrier once all prior tcgen05 ops of this thread completed.
 NNAB_DEV void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -151,6 +151,84 @@ __global__ void input_grad_kernel(const float* __restrict__ fg, int64_t ld_fg, i
 
 int grid_for(int64_t total) { return (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 32); }
 
+// ---- 3xF16 kernel gradient operands -------------------------------------------------
+// The staged frames of clip b are x * 2^e_b (FP16 hi/lo, stage_rows_f16*).  The coef row
+// m enters the dK GEMM as FP16 hi/lo of coef * 2^(r_m - e_b): 2^-e_b makes the product
+// with the staged frames exact, 2^r_m keeps the row's largest magnitude below 2^14
+// (FP16 holds 2^16; no overflow is possible) and the epilogue multiplies by 2^-r_m.
+// r_m comes from a bound, not a max pass over coef: |coef| <= |dS| (|re|, |im| <= S)
+// and |dS[f]| <= sum_m |W[m][f]| * G with G = max |g * 2^-e_b|.  A loose bound only
+// moves small values toward FP16's subnormal range, whose spacing (2^-24 against the
+// row's 2^14 ceiling) is far below the 2^-22 split error.
+
+// gmax = max over e of |v[e]| * 2^-e_clip(e) (+ |lo[e]|), as float bits (non-negative
+// floats order as unsigned); slots layout: clip = (e % ld) / R, else clip = e / per_clip
+__global__ void clip_absmax_kernel(const float* __restrict__ v, const float* __restrict__ lo, int64_t n, int64_t ld,
+                                   int32_t R, int64_t per_clip, int64_t B, const int32_t* __restrict__ exps,
+                                   unsigned* __restrict__ gmax) {
+  float mx = 0.f;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = ld > 0 ? (e % ld) / R : e / per_clip;
+    if (b >= B) continue;
+    float a = fabsf(v[e]);
+    if (lo) a += fabsf(lo[e]);
+    mx = fmaxf(mx, a * __int_as_float((127 - exps[b]) << 23));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(gmax, __float_as_uint(mx));
+}
+
+// row_exp[f] = row_exp[F + f] = 14 - ceil(log2(bound_f)), bound_f = colsum_f * G with
+// colsum_f = sum_m |wt[f][m]| (wt null: 1); 0 where the bound is 0 or not finite
+__global__ void row_exp_kernel(const float* __restrict__ wt_hi, const float* __restrict__ wt_lo, int32_t F,
+                               int32_t kp, int32_t n_mels, const unsigned* __restrict__ gmax,
+                               int32_t* __restrict__ row_exp) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  float c = 1.f;
+  if (wt_hi) {
+    c = 0.f;
+    for (int m = 0; m < n_mels; ++m) c += fabsf(wt_hi[(int64_t)f * kp + m]) + (wt_lo ? fabsf(wt_lo[(int64_t)f * kp + m]) : 0.f);
+  }
+  const float b = c * __uint_as_float(*gmax) * 1.001f;  // margin for the rounding of the sums
+  int e = 0;
+  if (b > 0.f && b < INFINITY) {
+    int ex;
+    frexpf(b, &ex);  // b < 2^ex
+    e = max(-125, min(125, 14 - ex));
+  }
+  row_exp[f] = e;
+  row_exp[F + f] = e;
+}
+
+// coef_kernel's conv-layer form (g straight from (B, F, T)) writing the 3xF16 dK operand
+__global__ void coef_f16_kernel(const float* __restrict__ g_bft, const float* __restrict__ re,
+                                const float* __restrict__ im, int32_t F, int64_t B, int32_t T, int32_t R, int64_t ld,
+                                float eps, const int32_t* __restrict__ exps, const int32_t* __restrict__ row_exp,
+                                __half* __restrict__ hi, __half* __restrict__ lo) {
+  const int64_t total = (int64_t)F * ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = e / ld, slot = e - f * ld;
+    const int64_t b = slot / R;
+    const int t = (int)(slot - b * R);
+    float cr = 0.f, ci = 0.f;
+    if (b < B && t < T) {
+      const float d = g_bft[(b * F + f) * (int64_t)T + t];
+      const float r = re[e], i = im[e];
+      const float di = d * rsqrtf(fmaf(r, r, i * i) + eps);
+      const float sc = __int_as_float((127 - exps[b]) << 23) * __int_as_float((127 + row_exp[f]) << 23);
+      cr = di * r * sc;
+      ci = di * i * sc;
+    }
+    const __half hr = __float2half_rn(cr), hi_ = __float2half_rn(ci);
+    hi[e] = hr;
+    hi[e + (int64_t)F * ld] = hi_;
+    lo[e] = __float2half_rn(cr - __half2float(hr));
+    lo[e + (int64_t)F * ld] = __float2half_rn(ci - __half2float(hi_));
+  }
+}
+
 }  // namespace
 }  // namespace nnab
 
@@ -415,4 +493,125 @@ extern "C" int nnab_input_grad(const nnab_frames* f, const float* frame_grads, i
                                                                        g.pad, g.pad_mode, g.T, g.R, gx);
   NNAB_LAUNCHED();
   return NNAB_OK;
+}
+
+// ---- 3xF16 kernel gradient (FP32 mode) ----------------------------
+
+static int f16_views(const nnab_frames* f, const void* ws16, size_t ws16_bytes, FrameGeom* g, const void** hi,
+                     const void** lo, const int32_t** exps) {
+  int rc = staged_views(f, NNAB_PREC_3XF16, ws16, ws16_bytes, g, hi, lo, exps);
+  if (rc) return rc;
+  if (g->B > 0 && (!*exps || !*lo)) return NNAB_EINVAL;
+  return NNAB_OK;
+}
+
+extern "C" int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t F, int64_t ld,
+                                     int32_t kp, const float* wt_hi, const float* wt_lo, const float* gs_hi,
+                                     const float* gs_lo, int32_t n_mels, const float* re_s, const float* im_s,
+                                     float eps, void* coef_hi, void* coef_lo, int32_t* row_exps, void* stream) {
+  FrameGeom g;
+  const void *hi, *lo;
+  const int32_t* exps;
+  int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
+  if (rc) return rc;
+  if (F < 1 || ld < g.B * g.R || ld % 8 || kp < n_mels || n_mels < 1 || !wt_hi || !wt_lo || !gs_hi || !gs_lo ||
+      !re_s || !im_s || !coef_hi || !coef_lo || !row_exps)
+    return NNAB_EINVAL;
+  if (ld > INT32_MAX) return NNAB_EINVAL;
+  if (kp > 1024) return NNAB_ENOTSUP;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned* gmax = reinterpret_cast<unsigned*>(row_exps + 2 * F);
+  NNAB_CUDA_TRY(cudaMemsetAsync(gmax, 0, 4, s));
+  if (g.B > 0) {
+    clip_absmax_kernel<<<grid_for((int64_t)n_mels * ld), 256, 0, s>>>(gs_hi, gs_lo, (int64_t)n_mels * ld, ld, g.R, 0,
+                                                                       g.B, exps, gmax);
+    NNAB_LAUNCHED();
+  }
+  row_exp_kernel<<<(F + 127) / 128, 128, 0, s>>>(wt_hi, wt_lo, F, kp, n_mels, gmax, row_exps);
+  NNAB_LAUNCHED();
+  RGemmArgs a;
+  a.M = F;
+  a.N = (int32_t)ld;
+  a.K = kp;
+  a.a_hi = wt_hi;
+  a.a_lo = wt_lo;
+  a.lda = kp;
+  a.b_hi = gs_hi;
+  a.b_lo = gs_lo;
+  a.b_mn = 1;
+  a.b_row_len = (int32_t)ld;
+  a.b_rows = n_mels;
+  a.c = reinterpret_cast<float*>(coef_hi);
+  a.ldc = ld;
+  a.splits = 1;
+  a.coef_re = re_s;
+  a.coef_im = im_s;
+  a.coef_lo = reinterpret_cast<float*>(coef_lo);
+  a.coef_eps = eps;
+  a.coef_f16 = 1;
+  a.row_exp = row_exps;
+  a.clip_exp = exps;
+  a.n_clips = g.B;
+  a.clip_R = g.R;
+  return launch_rgemm(a, NNAB_PREC_3XTF32, s);
+}
+
+extern "C" int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, const float* g_bft,
+                                 const float* re_s, const float* im_s, int32_t F, int32_t T, int64_t ld, float eps,
+                                 void* coef_hi, void* coef_lo, int32_t* row_exps, void* stream) {
+  FrameGeom g;
+  const void *hi, *lo;
+  const int32_t* exps;
+  int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
+  if (rc) return rc;
+  if (!g_bft || !re_s || !im_s || !coef_hi || !coef_lo || !row_exps || F < 1 || T < 1 || T > g.R ||
+      ld < g.B * g.R || ld % 8)
+    return NNAB_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned* gmax = reinterpret_cast<unsigned*>(row_exps + 2 * F);
+  NNAB_CUDA_TRY(cudaMemsetAsync(gmax, 0, 4, s));
+  const int64_t n = g.B * (int64_t)F * T;
+  if (n > 0) {
+    clip_absmax_kernel<<<grid_for(n), 256, 0, s>>>(g_bft, nullptr, n, 0, 1, (int64_t)F * T, g.B, exps, gmax);
+    NNAB_LAUNCHED();
+  }
+  row_exp_kernel<<<(F + 127) / 128, 128, 0, s>>>(nullptr, nullptr, F, 0, 0, gmax, row_exps);
+  NNAB_LAUNCHED();
+  const int64_t total = (int64_t)F * ld;
+  coef_f16_kernel<<<grid_for(total), 256, 0, s>>>(g_bft, re_s, im_s, F, g.B, T, g.R, ld, eps, exps, row_exps,
+                                                   reinterpret_cast<__half*>(coef_hi),
+                                                   reinterpret_cast<__half*>(coef_lo));
+  NNAB_LAUNCHED();
+  return NNAB_OK;
+}
+
+extern "C" int nnab_kernel_grad_f16(const nnab_frames* f, const void* coef_hi, const void* coef_lo, int32_t rows,
+                                    int64_t ld, const int32_t* row_exps, float* dk, int64_t ldk, const void* ws16,
+                                    size_t ws16_bytes, float* partial, int32_t splits, void* stream) {
+  FrameGeom g;
+  const void *hi, *lo;
+  const int32_t* exps;
+  int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
+  if (rc) return rc;
+  if (!coef_hi || !coef_lo || !row_exps || !dk || rows < 1 || ld < g.B * g.R || ld % 8) return NNAB_EINVAL;
+  if (g.row_len != g.hop || g.hop % 64) return NNAB_ENOTSUP;  // MN-major 64-column boxes of hop rows
+  if (g.B == 0) return NNAB_OK;
+  RGemmArgs a;
+  a.M = rows;
+  a.N = g.width;
+  a.K = ld;
+  a.a_hi = reinterpret_cast<const float*>(coef_hi);
+  a.a_lo = reinterpret_cast<const float*>(coef_lo);
+  a.lda = ld;
+  a.b_hi = reinterpret_cast<const float*>(hi);
+  a.b_lo = reinterpret_cast<const float*>(lo);
+  a.b_mn = 1;
+  a.b_row_len = g.row_len;
+  a.b_rows = g.B * g.R;
+  a.c = dk;
+  a.ldc = ldk;
+  a.splits = splits;
+  a.partial = partial;
+  a.row_exp = row_exps;
+  return launch_rgemm(a, NNAB_PREC_3XF16, (cudaStream_t)stream);
 }

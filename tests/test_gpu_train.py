@@ -348,3 +348,60 @@ def test_trainable_cqt1992v2_full_config(cuda_dev, precision):
     # (FP32 mode measured 7.0e-5 on this seed), hence the joint gates
     assert O.peak_err(m.k_re.grad.cpu().numpy(), dre) <= TOL_GRAD_JOINT[precision]
     assert O.peak_err(m.k_im.grad.cpu().numpy(), dim) <= TOL_GRAD_JOINT[precision]
+
+
+@pytest.mark.parametrize("n_fft,hop,F,B,spread", [
+    (2048, 512, 1025, 72, True),   # config 5 shape: 144 pair tiles, one split, C written directly
+    (1024, 256, 84, 40, False),    # 168 rows: 1 pair row x 4 column tiles -> split-K partials + fixed-order sum
+    (1000, 256, 33, 24, True),     # N = 1000: TMA clips the last column tile
+    (1002, 256, 40, 24, False),    # ldk = 1002 (row stride not 16-byte aligned): the partial-buffer path
+])
+def test_kernel_grad_f16_vs_float64(cuda_dev, n_fft, hop, F, B, spread):
+    """FP32 mode's 3xF16 kernel gradient (nnab_dft_coef_f16 + nnab_kernel_grad_f16, gradients.py:125-129)
+    against float64: dK = (g re/S, g im/S) @ frames summed over the batch, with per-clip loudness spread
+    over 1e-3..1e3 and upstream grads of 1e-9 (the power-of-two clip / row scales), K = B x T frame slots
+    over several TMEM drain chunks (the first stores, later ones TMA reduce-add).  Gate 1e-5."""
+    import ctypes as C
+    import torch.nn.functional as Fn
+    from paper_1912_12055_b200 import _lib as L
+    from paper_1912_12055_b200.engine import DftEngine
+    lib = L.load()
+    gen = torch.Generator(device=cuda_dev)
+    gen.manual_seed(n_fft + F)
+    Lx = 80000
+    x = torch.randn(B, Lx, device=cuda_dev, generator=gen) * 0.5
+    gscale = 1.0
+    if spread:
+        x *= torch.logspace(-3, 3, B, device=cuda_dev)[:, None]
+        gscale = 1e-9
+    h = torch.zeros(F, n_fft)
+    eng = DftEngine(h, h, hop, True, "reflect", precision="3xf16", device=cuda_dev, allow_fold=False)
+    f = eng.frames(B, Lx)
+    ld, T = lib.nnab_slots_ld(C.byref(f)), eng.n_frames(Lx)
+    st = L.stream_handle(cuda_dev)
+    ws = torch.empty(lib.nnab_stft_workspace_bytes(C.byref(f), L.PREC_3XF16), dtype=torch.uint8, device=cuda_dev)
+    L.check(lib.nnab_stage_frames(C.byref(f), x.data_ptr(), L.PREC_3XF16, ws.data_ptr(), ws.numel(), st), "stage")
+    g = torch.randn(B, F, T, device=cuda_dev, generator=gen) * gscale
+    re = torch.randn(F, ld, device=cuda_dev, generator=gen)
+    im = torch.randn(F, ld, device=cuda_dev, generator=gen)
+    c16 = [torch.empty(2 * F, ld, dtype=torch.float16, device=cuda_dev) for _ in range(2)]
+    rexp = torch.empty(2 * F + 1, dtype=torch.int32, device=cuda_dev)
+    L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), g.data_ptr(), re.data_ptr(), im.data_ptr(),
+                                  F, T, ld, 0.0, c16[0].data_ptr(), c16[1].data_ptr(), rexp.data_ptr(), st), "coef")
+    dk = torch.full((2 * F, n_fft), float("nan"), device=cuda_dev)
+    part = torch.empty(max(lib.nnab_rgemm_partial_bytes(2 * F, n_fft, ld, 0) // 4, 1), device=cuda_dev)
+    L.check(lib.nnab_kernel_grad_f16(C.byref(f), c16[0].data_ptr(), c16[1].data_ptr(), 2 * F, ld, rexp.data_ptr(),
+                                     dk.data_ptr(), n_fft, ws.data_ptr(), ws.numel(), part.data_ptr(), 0, st), "dk")
+    torch.cuda.synchronize()
+    from paper_1912_12055_b200.engine import geometry
+    R = geometry(Lx, n_fft, hop, n_fft // 2, "reflect")[2]  # slot layout: clip b, frame t -> slot b * R + t
+    slots = (torch.arange(B, device=cuda_dev)[:, None] * R + torch.arange(T, device=cuda_dev)[None]).reshape(-1)
+    re64, im64 = re.double()[:, slots], im.double()[:, slots]
+    S = torch.sqrt(re64 ** 2 + im64 ** 2)
+    g64 = g.double().permute(1, 0, 2).reshape(F, B * T)
+    xp = Fn.pad(x.double()[:, None], (n_fft // 2, n_fft // 2), mode="reflect")[:, 0]
+    fr = xp.unfold(1, n_fft, hop)[:, :T].reshape(B * T, n_fft)
+    ref = torch.cat([(g64 * re64 / S) @ fr, (g64 * im64 / S) @ fr])
+    assert torch.isfinite(dk).all()
+    err = float((dk.double() - ref).abs().max() / ref.abs().max())
+    assert err <= 1e-5, err
