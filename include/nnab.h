@@ -60,6 +60,10 @@ extern "C" {
  * that weighs every frame in the kernel gradient is FP32-accurate even where
  * |X| is small, while the backward GEMMs stay TF32. */
 #define NNAB_SAVE_PHASOR 0x200
+/* flag (split modes without NNAB_SAVE_PHASOR): save_mag is [2][n_bins][ld], the
+ * TF32 hi of |X| then its TF32 residual -- the 3xTF32 operand pair of the Mel
+ * layer's forward W @ S and dW = g S^T, with no separate split pass. */
+#define NNAB_SAVE_MAG_SPLIT 0x400
 
 #define NNAB_PREC_TF32 0  /* one TF32 tcgen05 pass (peak-normalised error <= 1e-3) */
 #define NNAB_PREC_3XTF32 1 /* hi/lo split, 3 passes (<= 1e-5, FP32-equivalent) */
@@ -217,7 +221,7 @@ int nnab_dft_coef(const float* ds_slots, const float* g_bft, const float* re_s, 
 /* Mel layer forward of the trainable layer (gradients.py:69-80): W @ S on the
  * slot-major smoothed magnitude S [F][ld] (save_mag of the training forward),
  * written as (B, n_mels, T).  w = W zero-padded to [n_mels][kp], kp = F
- * rounded up to 32 (<= 2048 in TF32, <= 1024 in 3xTF32, else NNAB_ENOTSUP); R % 4 == 0. */
+ * rounded up to 32 (<= 2048, else NNAB_ENOTSUP); R % 4 == 0. */
 int nnab_mel_forward_slots(int32_t n_mels, int64_t ld, int32_t kp, const float* w_hi, const float* w_lo,
                            const float* s_hi, const float* s_lo, int32_t F, int64_t B, int32_t R, int32_t T,
                            int32_t precision, float* out, void* stream);

@@ -17,6 +17,7 @@ OK, EINVAL, ECUDA, ENOTSUP, ENODEV = 0, 1, 2, 3, 4
 PAD_REFLECT, PAD_ZERO = 0, 1
 OUT_MAGNITUDE, OUT_POWER, OUT_COMPLEX, OUT_MEL, OUT_SMOOTH_MAG = 0, 1, 2, 3, 4
 OUT_LOG = 0x100  # flag: log(value + eps) in the fused epilogue (STFT / Mel)
+SAVE_MAG_SPLIT = 0x400  # flag (training forward, split modes): |X| saved as the 3xTF32 hi / lo pair
 SAVE_PHASOR = 0x200  # flag (training forward): TF32-backward saves from a split-precision forward
 PREC_TF32, PREC_3XTF32, PREC_F16, PREC_3XF16 = 0, 1, 2, 3
 PAD_MODES = {"reflect": PAD_REFLECT, "constant_zero": PAD_ZERO, "constant": PAD_ZERO}

@@ -124,13 +124,15 @@ class DftLayerOp:
         # pairs in one 32-bit word per (bin, slot); 3xTF32 keeps re and im in FP32
         re_s = _f32(F, ld, self.device)
         im_s = _f32(F, ld, self.device) if self.split else None
-        mag_s = _f32(F, ld, self.device) if mel_w is not None else None
+        # split modes: |X| saved as its 3xTF32 (hi, lo) pair [2][F][ld] straight from the epilogue
+        mag_split = mel_w is not None and fe is not None and self.split
+        mag_s = _f32((2 if mag_split else 1) * F, ld, self.device) if mel_w is not None else None
         # mel layer: the STFT GEMM only saves re/im/S per slot; W @ S then runs as a
         # tcgen05 GEMM (a trained W is dense, so the epilogue's banded CUDA-core path
         # would be latency-bound)
         out = None if mel_w is not None else torch.empty(B, F, T, device=self.device)
         if fe is not None:  # split forward; TF32 mode: TF32-backward saves (FP32-accurate phasor)
-            flag = 0 if self.split else L.SAVE_PHASOR
+            flag = (L.SAVE_MAG_SPLIT if mag_split else 0) if self.split else L.SAVE_PHASOR
             L.check(lib.nnab_stft_forward_train_staged(
                 C.byref(f), fe.packed_hi.data_ptr(), L.ptr(fe.packed_lo), F, fe.fold, self.fwd_prec,
                 L.OUT_SMOOTH_MAG | flag, 1.0, self.eps, None, 0, 0, None, L.ptr(out), re_s.data_ptr(), L.ptr(im_s),
@@ -146,11 +148,14 @@ class DftLayerOp:
             kp = (F + 31) // 32 * 32
             wp = torch.zeros(nm, kp, device=self.device)
             wp[:, :F] = mel_w.detach().to(self.device, torch.float32)
-            magp = self._split(mag_s) if self.split else (mag_s, None)
+            if mag_split:
+                magp = (mag_s[:F], mag_s[F:])
+            else:
+                magp = self._split(mag_s) if self.split else (mag_s, None)
             saved["magp"] = magp
             out = torch.empty(B, nm, T, device=self.device)
             wsp = self._split(wp)
-            if R % 4 == 0 and kp <= (1024 if self.split else 2048):  # W @ S straight into (B, n_mels, T)
+            if R % 4 == 0 and kp <= 2048:  # W @ S straight into (B, n_mels, T)
                 L.check(lib.nnab_mel_forward_slots(nm, ld, kp, wsp[0].data_ptr(), L.ptr(wsp[1]), magp[0].data_ptr(),
                                                    L.ptr(magp[1]), F, B, R, T, self.prec, out.data_ptr(), stream),
                         "mel_forward_slots")

@@ -83,6 +83,7 @@ struct StftGemmArgs {
   int32_t pairs = 0;
   int32_t out_bins = 0;  // pairs mode: bins per clip of the output (0 = n_bins; the caller offsets out)
   float *save_re = nullptr, *save_im = nullptr, *save_mag = nullptr;  // training forward (slot-major)
+  float* save_mag_lo = nullptr;  // NNAB_SAVE_MAG_SPLIT: save_mag TF32 hi, this the lo residual
   int64_t ld_slots = 0;
   int32_t save_phasor = 0;  // saves in the TF32-backward format whatever the forward's operand mode
 };

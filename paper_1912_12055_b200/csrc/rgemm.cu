@@ -108,6 +108,15 @@ NNAB_DEV void coef_store(float d, float r, float i, float eps, float& cr, float&
   ci = di * i;
 }
 
+// FP16 hi = RN(v), lo = RN(v - hi) of four values, packed in pairs
+NNAB_DEV void split_f16x4(float a, float b, float c, float d, uint2& hi, uint2& lo) {
+  const __half2 h0 = __floats2half2_rn(a, b), h1 = __floats2half2_rn(c, d);
+  const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+  const __half2 l0 = __floats2half2_rn(a - f0.x, b - f0.y), l1 = __floats2half2_rn(c - f1.x, d - f1.y);
+  hi = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+  lo = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
+}
+
 NNAB_DEV uint64_t kdesc(const void* p, int swz) {
   uint64_t d = (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
@@ -144,7 +153,7 @@ NNAB_DEV uint64_t mndesc(const void* p, int /*swz*/, uint32_t lbo) {
 // reduction dK = coef @ frames is L2-bandwidth bound at 128 x 256 per CTA).
 // kWide (with kPair): 256 x 512 tiles -- two N=256 MMAs per K step into all
 // 512 TMEM columns (one accumulator), a quarter less L2 traffic per MAC again.
-// kE8: the phasor coef epilogue (nnab_mel_dft_coef, TF32) on 8 epilogue warps
+// kE8: the coef epilogues (nnab_mel_dft_coef: TF32 phasor; 3xTF32 with FP16 output) on 8 epilogue warps
 // (384 threads, 3 stages): its HBM-latency-bound loads get twice the warps in flight.
 // kF16: the 3xF16 kernel gradient (nnab_kernel_grad_f16) -- A = coef rows scaled by
 // 2^(row_exp - clip_exp) as FP16 hi/lo, B = the 3xF16 forward's staged frames (MN-major
@@ -163,7 +172,7 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
   constexpr int kHalves = kWide ? 2 : 1;       // N=256 MMAs per K step
   constexpr int NST = (kE8 || kF16) ? 3 : kStages;  // pipeline stages
   constexpr int kEW = kE8 ? 8 : 4;              // epilogue warps
-  static_assert(!kE8 || (!kSplit && !kWide), "8-warp epilogue: TF32 coef GEMM only");
+  static_assert(!kE8 || !kWide, "8-warp epilogue: coef GEMMs only");
   const uint32_t rank = kPair ? cluster_ctarank() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
         const uint32_t tb = tbase + ((q * 32) << 16) + (NACC > 1 ? acc * C::ACC_STRIDE : 0);
         // phasor coef epilogue: chunk c + 1's phasor loads are in flight while chunk c
         // is drained (the epilogue is HBM-latency bound with 4 warps per SM)
-        const bool phasor = kE8 || (p.re && !p.im);
+        const bool phasor = !kSplit && (kE8 || (p.re && !p.im));  // split modes save re and im
         uint4 ph_cur[8], ph_nxt[8];
         auto load_ph = [&](int c, uint4* dst) {
           const int n = nt * TBN + c * 32 + sc;
@@ -518,7 +527,7 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
                 }
               }
             }
-          } else if constexpr (!kE8) {
+          } else if constexpr (!kE8 || kSplit) {
           if (p.re) {  // coef epilogue: the dS tile never leaves the SM
             float4 rr[8], ii[8];
 #pragma unroll
@@ -546,37 +555,38 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
                 const float rs = __int_as_float((127 + p.row_exp[m]) << 23);  // |row_exp| <= 125
                 const int64_t o = (int64_t)m * p.ldc + n, o2 = o + (int64_t)p.M * p.ldc;
                 const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
-                float rr_[4] = {rr[it].x, rr[it].y, rr[it].z, rr[it].w}, ii_[4] = {ii[it].x, ii[it].y, ii[it].z, ii[it].w};
-                __half hr[4], lr[4], hi4[4], li4[4];
+                float cr[4], ci[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  if (!full4) {
-                    if (n + j >= p.N) { rr_[j] = 0.f; ii_[j] = 0.f; }
-                    else { rr_[j] = p.re[o + j]; ii_[j] = p.im[o + j]; }
+                  float r_, i_;
+                  if (full4) {
+                    r_ = j == 0 ? rr[it].x : j == 1 ? rr[it].y : j == 2 ? rr[it].z : rr[it].w;
+                    i_ = j == 0 ? ii[it].x : j == 1 ? ii[it].y : j == 2 ? ii[it].z : ii[it].w;
+                  } else {
+                    r_ = n + j < p.N ? p.re[o + j] : 0.f;
+                    i_ = n + j < p.N ? p.im[o + j] : 0.f;
                   }
-                  float cr, ci;
-                  coef_store(dv[j], rr_[j], ii_[j], p.eps, cr, ci);
-                  cr = cr * es[j] * rs;
-                  ci = ci * es[j] * rs;
-                  hr[j] = __float2half_rn(cr);
-                  lr[j] = __float2half_rn(cr - __half2float(hr[j]));
-                  hi4[j] = __float2half_rn(ci);
-                  li4[j] = __float2half_rn(ci - __half2float(hi4[j]));
+                  coef_store(dv[j], r_, i_, p.eps, cr[j], ci[j]);
+                  cr[j] *= es[j] * rs;
+                  ci[j] *= es[j] * rs;
                 }
+                uint2 hr, lr, hi4, li4;
+                split_f16x4(cr[0], cr[1], cr[2], cr[3], hr, lr);
+                split_f16x4(ci[0], ci[1], ci[2], ci[3], hi4, li4);
                 if (full4) {
-                  __stcs(reinterpret_cast<uint2*>(ch + o), *reinterpret_cast<const uint2*>(hr));
-                  __stcs(reinterpret_cast<uint2*>(cl + o), *reinterpret_cast<const uint2*>(lr));
-                  __stcs(reinterpret_cast<uint2*>(ch + o2), *reinterpret_cast<const uint2*>(hi4));
-                  __stcs(reinterpret_cast<uint2*>(cl + o2), *reinterpret_cast<const uint2*>(li4));
+                  __stcs(reinterpret_cast<uint2*>(ch + o), hr);
+                  __stcs(reinterpret_cast<uint2*>(cl + o), lr);
+                  __stcs(reinterpret_cast<uint2*>(ch + o2), hi4);
+                  __stcs(reinterpret_cast<uint2*>(cl + o2), li4);
                 } else {
+                  const uint32_t w4[4][2] = {{hr.x, hr.y}, {lr.x, lr.y}, {hi4.x, hi4.y}, {li4.x, li4.y}};
+                  __half* dst[4] = {ch + o, cl + o, ch + o2, cl + o2};
 #pragma unroll
-                  for (int j = 0; j < 4; ++j) {
-                    if (n + j >= p.N) continue;
-                    ch[o + j] = hr[j];
-                    cl[o + j] = lr[j];
-                    ch[o2 + j] = hi4[j];
-                    cl[o2 + j] = li4[j];
-                  }
+                  for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                      if (n + j < p.N)
+                        dst[a][j] = __ushort_as_half((unsigned short)(w4[a][j >> 1] >> (16 * (j & 1))));
                 }
               }
             } else {
@@ -744,6 +754,9 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.splits = (int)((g.K + p.k_per_split - 1) / p.k_per_split);
   p.k_chunk = (kF16 ? f16_chunk() : kSplit ? 1024 : kWide ? 8192 : 2048);  // accumulate steps per TMEM
                                                     // chain (wide: no second accumulator, so drain less often)
+  // the epilogues that write final values (frames output, coef) need one TMEM chain per tile:
+  // up to 2,048 K in every mode (a 3xTF32 Mel forward over 1,025 bins has K = 1,056)
+  if ((g.frames_R || g.coef_re) && kb * C::BK <= 2048) p.k_chunk = std::max<int64_t>(p.k_chunk, kb * C::BK);
   p.b_mn = g.b_mn;
   p.b_row_len = g.b_mn ? g.b_row_len : 1 << 30;
   p.re = g.coef_re;
@@ -838,6 +851,12 @@ int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s) {
   const bool pair_ok = pair_env != 0;
   if (precision == NNAB_PREC_3XTF32) {  // CTA pairs too (the long reductions are L2-bound)
     const bool pair = pair_ok && (pair_env >= 2 || g.M > kBM);
+    static const bool e8_split = [] {
+      const char* e = getenv("NNAB_COEF_E8");
+      return !(e && e[0] == '0');
+    }();
+    // the FP16-output coef epilogue is ALU-latency bound on 4 warps: twice the warps
+    if (pair && e8_split && g.coef_f16) return launch<true, true, false, true>(g, s);
     return pair ? launch<true, true>(g, s) : launch<true, false>(g, s);
   }
   if (precision == NNAB_PREC_3XF16) return launch<true, true, false, false, true>(g, s);

@@ -89,9 +89,10 @@ struct Params {
   const int32_t* b_exp;
   // training forward: re, im and smoothed magnitude per (bin, slot) saved in
   // slot-major layout [bin][ld_slots] for the backward GEMMs (may be null)
-  float *save_re, *save_im, *save_mag;
+  float *save_re, *save_im, *save_mag, *save_mag_lo;
   int64_t ld_slots;
   int32_t save_phasor;  // 1: save the TF32-backward format (FP16 unit phasor + TF32 |X|) in any operand mode
+  int32_t stage_acc;    // kE8: stage the accumulators in shared memory and release TMEM before the processing
 };
 
 NNAB_DEV uint64_t make_sdesc(const void* p, int swz_bytes) {
@@ -120,8 +121,12 @@ NNAB_DEV float finish(float re, float im, int kind, float power, float eps) {
   return fast_sqrt(p);
 }
 
-template <int kP, bool kPair>
-__global__ void __launch_bounds__(kThreads, 1)
+// kE8 (split modes, non-Mel outputs): 8 epilogue warps, two per TMEM lane quarter on
+// alternate 32-column chunks.  The split modes have one accumulator buffer, so the
+// MMAs of tile n + 1 wait for tile n's epilogue; halving its time raises the tensor
+// pipe's active share.
+template <int kP, bool kPair, bool kE8 = false>
+__global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
     stft_gemm_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                      const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
                      const Params p) {
@@ -134,7 +139,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* mel_acc = reinterpret_cast<float*>(smem + stages * C::STAGE_BYTES);  // [kMelRows][kBM]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * C::STAGE_BYTES + (mel ? kMelRows * kBM * 4 : 0));
+  // kE8 + stage_acc: the fp32 (re | im) staging tile [kBM][256] (16-byte chunks XOR-swizzled by row) in its place
+  float* stage_acc = mel_acc;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * C::STAGE_BYTES +
+                                               (mel ? kMelRows * kBM * 4 : (kE8 && p.stage_acc) ? kBM * kBN * 4 : 0));
   uint64_t* full = bars;            // [stages]  (pair: only the leader's are used)
   uint64_t* empty = bars + 8;       // [stages]
   uint64_t* tmem_full = bars + 16;  // [2]
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], kPair ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
+      mbar_init(&tmem_empty[i], (kPair ? 2 : 1) * (kE8 ? 8 : 4));  // one arrive per epilogue warp (of both CTAs)
     }
     fence_barrier_init();
   }
@@ -167,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     else tmem_alloc<512>(tmem_slot);
   }
   if (mel) {
-    for (int i = threadIdx.x; i < kMelRows * kBM; i += kThreads) mel_acc[i] = 0.f;
+    for (int i = threadIdx.x; i < kMelRows * kBM; i += blockDim.x) mel_acc[i] = 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -272,13 +280,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const uint32_t q = warp - 4;  // TMEM lane quarter
+    const uint32_t q = (warp - 4) & 3;  // TMEM lane quarter
+    const int hsel = kE8 ? (int)((warp - 4) >> 2) : 0;  // kE8: chunks hsel, hsel + 2
+    constexpr int CSTEP = kE8 ? 2 : 1;
     const uint32_t row = q * 32 + lane;
     const int kind = p.out_kind;
     const int F = p.n_bins;
     int acc = 0;
     uint32_t aph = 0;
     const uint32_t empty_addr0 = kPair ? mapa(&tmem_empty[0], 0) : smem_u32(&tmem_empty[0]);
+    // |X| for the backward GEMMs: TF32 for a TF32 backward; fp32 in the split modes, or
+    // (save_mag_lo) already split into the 3xTF32 operand pair
+    auto save_mag = [&](int64_t o, float pw) {
+      if (!kSplit || p.save_phasor) {
+        p.save_mag[o] = tf32_rne(fast_sqrt(pw));
+      } else {
+        const float m = sqrtf(pw);
+        if (p.save_mag_lo) {
+          const float h = tf32_rne(m);
+          p.save_mag[o] = h;
+          p.save_mag_lo[o] = tf32_rne(m - h);
+        } else {
+          p.save_mag[o] = m;
+        }
+      }
+    };
     auto release_acc = [&](int a) {  // one arrive per warp on the (leader's) tmem_empty
       tc_fence_before();
       __syncwarp();
@@ -337,9 +363,43 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
           continue;
         }
+        // kE8 + stage_acc: copy this warp's chunks (main + correction, scaled) to its rows of
+        // the staging tile and release TMEM at once, so the next tile's MMAs overlap the
+        // processing below (the split modes have one accumulator buffer)
+        float4* srow = reinterpret_cast<float4*>(stage_acc) + row * 64;
+        const int sw = (int)(row & 7);
+        if (kE8 && p.stage_acc) {
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+          for (int c = hsel; c < 4; c += CSTEP) {
+            float re[32], im[32], cre[32], cim[32];
+            tmem_ld32(tb + c * 32, re);
+            tmem_ld32(tb + 128 + c * 32, im);
+            tmem_ld32(tb + kBN + c * 32, cre);
+            tmem_ld32(tb + kBN + 128 + c * 32, cim);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              srow[(c * 8 + j) ^ sw] = make_float4((re[4 * j] + cre[4 * j]) * osc, (re[4 * j + 1] + cre[4 * j + 1]) * osc,
+                                                   (re[4 * j + 2] + cre[4 * j + 2]) * osc,
+                                                   (re[4 * j + 3] + cre[4 * j + 3]) * osc);
+              srow[(32 + c * 8 + j) ^ sw] =
+                  make_float4((im[4 * j] + cim[4 * j]) * osc, (im[4 * j + 1] + cim[4 * j + 1]) * osc,
+                              (im[4 * j + 2] + cim[4 * j + 2]) * osc, (im[4 * j + 3] + cim[4 * j + 3]) * osc);
+            }
+          }
+          release_acc(acc);
+        }
+#pragma unroll 1
+        for (int c = hsel; c < 4; c += CSTEP) {
           float re[32], im[32];
+          if (kE8 && p.stage_acc) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 a = srow[(c * 8 + j) ^ sw], b = srow[(32 + c * 8 + j) ^ sw];
+              re[4 * j] = a.x, re[4 * j + 1] = a.y, re[4 * j + 2] = a.z, re[4 * j + 3] = a.w;
+              im[4 * j] = b.x, im[4 * j + 1] = b.y, im[4 * j + 2] = b.z, im[4 * j + 3] = b.w;
+            }
+          } else {
           tmem_ld32(tb + c * 32, re);
           tmem_ld32(tb + 128 + c * 32, im);
           if (kSplit) {
@@ -362,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               im[j] *= osc;
             }
           }
+          }  // TMEM read
           const int bin0 = n * 128 + c * 32;
           float nyq_re = 0.f;
           if (p.fold && n == 0 && c == 0) {
@@ -386,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     reinterpret_cast<__half2*>(p.save_re)[o] = ph;
                   }
                   if (p.save_mag)  // GEMM operand of dW: TF32-rounded for a TF32 backward, fp32 (split later) in 3xTF32
-                    p.save_mag[o] = (kSplit && !p.save_phasor) ? sqrtf(pw) : tf32_rne(fast_sqrt(pw));
+                    save_mag(o, pw);
                 }
               }
               if (p.fold && n == 0 && c == 0) {
@@ -398,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                   reinterpret_cast<__half2*>(p.save_re)[o] = __floats2half2_rn(nyq_re * rsqrtf(pw), 0.f);
                 }
-                if (p.save_mag) p.save_mag[o] = (kSplit && !p.save_phasor) ? sqrtf(pw) : tf32_rne(fast_sqrt(pw));
+                if (p.save_mag) save_mag(o, pw);
               }
             }
           }
@@ -468,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        release_acc(acc);
+        if (!(kE8 && p.stage_acc)) release_acc(acc);
         if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
       }
       if (kind == NNAB_OUT_MEL) {
@@ -497,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int kP, bool kPair>
+template <int kP, bool kPair, bool kE8 = false>
 int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   using C = Cfg<kP, kPair>;
   constexpr bool kSplit = C::kSplit;
@@ -544,6 +605,7 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.save_re = a.save_re;
   p.save_im = a.save_im;
   p.save_mag = a.save_mag;
+  p.save_mag_lo = a.save_mag_lo;
   p.ld_slots = a.ld_slots;
   p.a_exp = a.a_exp;
   p.b_exp = a.b_exp;
@@ -555,25 +617,32 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.pairs = a.pairs;
   p.out_bins = a.out_bins > 0 ? a.out_bins : a.n_bins;
   if (a.kb_tab && (a.n_tab < 1 || mel)) return NNAB_EINVAL;
+  if (kE8 && (mel || a.pairs)) return NNAB_EINVAL;  // per-row Mel accumulation / the pairs loop: 4 warps
   if (p.n_mtiles == 0) return NNAB_OK;
   // as many pipeline stages as fit next to the Mel accumulator (<= 8)
-  const size_t mel_bytes = mel ? (size_t)kMelRows * kBM * 4 : 0;
+  static const bool stage_env = [] {
+    const char* e = getenv("NNAB_STFT_STAGE_ACC");
+    return !(e && e[0] == '0');
+  }();
+  p.stage_acc = kE8 && stage_env;
+  const size_t mel_bytes = mel ? (size_t)kMelRows * kBM * 4 : p.stage_acc ? (size_t)kBM * kBN * 4 : 0;
   constexpr size_t kBudget = 227 * 1024 - 1024 - 256;  // max dynamic smem - alignment slack - barriers
   int stages = (int)std::min<size_t>(8, (kBudget - mel_bytes) / C::STAGE_BYTES);
   if (const char* e = getenv("NNAB_DEBUG_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));
   p.stages = stages;
   const size_t smem = 1024 + (size_t)stages * C::STAGE_BYTES + mel_bytes + 256;
-  auto kern = stft_gemm_kernel<kP, kPair>;
+  auto kern = stft_gemm_kernel<kP, kPair, kE8>;
+  constexpr int threads = kE8 ? kThreads + 128 : kThreads;
   NNAB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (!kPair) {
     const int grid = std::min(p.n_mtiles, num_sms());
-    kern<<<grid, kThreads, smem, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
+    kern<<<grid, threads, smem, s>>>(ta_hi, ta_lo, tb_hi, tb_lo, p);
   } else {
     const int pairs = (p.n_mtiles + 1) / 2;
     const int grid = 2 * std::min(pairs, num_sms() / 2);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -597,11 +666,18 @@ int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, c
     const char* e = getenv("NNAB_CTA_PAIR");
     return !(e && e[0] == '0');
   }();
+  static const bool e8 = [] {  // NNAB_STFT_E8=0: 4 epilogue warps in the split modes too
+    const char* e = getenv("NNAB_STFT_E8");
+    return !(e && e[0] == '0');
+  }();
   switch (precision) {
     case NNAB_PREC_TF32: return pair ? launch_impl<NNAB_PREC_TF32, true>(g, a, s) : launch_impl<NNAB_PREC_TF32, false>(g, a, s);
     case NNAB_PREC_3XTF32: return pair ? launch_impl<NNAB_PREC_3XTF32, true>(g, a, s) : launch_impl<NNAB_PREC_3XTF32, false>(g, a, s);
     case NNAB_PREC_F16: return pair ? launch_impl<NNAB_PREC_F16, true>(g, a, s) : launch_impl<NNAB_PREC_F16, false>(g, a, s);
-    case NNAB_PREC_3XF16: return pair ? launch_impl<NNAB_PREC_3XF16, true>(g, a, s) : launch_impl<NNAB_PREC_3XF16, false>(g, a, s);
+    case NNAB_PREC_3XF16:
+      if (pair && e8 && (a.out_kind & ~NNAB_OUT_LOG) != NNAB_OUT_MEL && !a.pairs)
+        return launch_impl<NNAB_PREC_3XF16, true, true>(g, a, s);
+      return pair ? launch_impl<NNAB_PREC_3XF16, true>(g, a, s) : launch_impl<NNAB_PREC_3XF16, false>(g, a, s);
     default: return NNAB_EINVAL;
   }
 }

@@ -21,22 +21,27 @@ namespace nnab {
 namespace {
 
 // out[r][b*R + t] = g[b][r][t] for t < T, 0 for the staging-only slots and the
-// tail up to ld.
+// tail up to ld.  Block b < B: clip b, one warp per row at a time, lanes over its R
+// slots (coalesced on both sides, no per-element index division); block B: the tail.
 __global__ void to_slots_kernel(const float* __restrict__ g, int64_t B, int32_t rows, int32_t T, int32_t R,
                                 int64_t ld, float* __restrict__ out, int round, float* __restrict__ lo) {
-  const int64_t total = (int64_t)rows * ld;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / ld, slot = e - r * ld;
-    const int64_t b = slot / R;
-    const int t = (int)(slot - b * R);
-    float v = 0.f;
-    if (b < B && t < T) v = g[(b * rows + r) * (int64_t)T + t];
-    if (round) {
-      const float h = tf32_rne(v);
-      out[e] = h;
-      if (lo) lo[e] = tf32_rne(v - h);
-    } else {
-      out[e] = v;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int64_t b = blockIdx.x; b <= B; b += gridDim.x) {
+    const int64_t s0 = b * R, n = b < B ? R : ld - B * R;
+    for (int r = w; r < rows; r += nw) {
+      const float* src = g + (b * rows + r) * (int64_t)T;
+      float* dst = out + (int64_t)r * ld + s0;
+      float* dlo = lo ? lo + (int64_t)r * ld + s0 : nullptr;
+      for (int64_t t = lane; t < n; t += 32) {
+        const float v = (b < B && t < T) ? src[t] : 0.f;
+        if (round) {
+          const float h = tf32_rne(v);
+          dst[t] = h;
+          if (dlo) dlo[t] = tf32_rne(v - h);
+        } else {
+          dst[t] = v;
+        }
+      }
     }
   }
 }
@@ -161,22 +166,29 @@ int grid_for(int64_t total) { return (int)std::min<int64_t>((total + 255) / 256,
 // moves small values toward FP16's subnormal range, whose spacing (2^-24 against the
 // row's 2^14 ceiling) is far below the 2^-22 split error.
 
-// gmax = max over e of |v[e]| * 2^-e_clip(e) (+ |lo[e]|), as float bits (non-negative
-// floats order as unsigned); slots layout: clip = (e % ld) / R, else clip = e / per_clip
-__global__ void clip_absmax_kernel(const float* __restrict__ v, const float* __restrict__ lo, int64_t n, int64_t ld,
-                                   int32_t R, int64_t per_clip, int64_t B, const int32_t* __restrict__ exps,
-                                   unsigned* __restrict__ gmax) {
-  float mx = 0.f;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = ld > 0 ? (e % ld) / R : e / per_clip;
-    if (b >= B) continue;
-    float a = fabsf(v[e]);
-    if (lo) a += fabsf(lo[e]);
-    mx = fmaxf(mx, a * __int_as_float((127 - exps[b]) << 23));
-  }
+// gmax = max over clips b of 2^-e_b * max |v| over clip b's elements (+ |lo|), as float
+// bits (non-negative floats order as unsigned): element (r, t) of clip b at
+// v[b * clip_stride + r * row_stride + t], r < rows, t < T.  One block per clip, one
+// warp per row at a time (no per-element index division).
+__global__ void clip_absmax_kernel(const float* __restrict__ v, const float* __restrict__ lo, int64_t B, int32_t rows,
+                                   int64_t row_stride, int64_t clip_stride, int32_t T,
+                                   const int32_t* __restrict__ exps, unsigned* __restrict__ gmax) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    const float* vb = v + b * clip_stride;
+    const float* lb = lo ? lo + b * clip_stride : nullptr;
+    float mx = 0.f;
+    for (int r = w; r < rows; r += nw) {
+      for (int t = lane; t < T; t += 32) {
+        const int64_t o = r * row_stride + t;
+        mx = fmaxf(mx, fabsf(vb[o]) + (lb ? fabsf(lb[o]) : 0.f));
+      }
+    }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(gmax, __float_as_uint(mx));
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mx *= __int_as_float((127 - exps[b]) << 23);
+    if (lane == 0 && mx > 0.f) atomicMax(gmax, __float_as_uint(mx));
+  }
 }
 
 // row_exp[f] = row_exp[F + f] = 14 - ceil(log2(bound_f)), bound_f = colsum_f * G with
@@ -247,7 +259,8 @@ extern "C" int nnab_stft_forward_train_staged(const nnab_frames* f, const float*
                                               float* save_re, float* save_im, float* save_mag, int64_t ld,
                                               const void* workspace, size_t workspace_bytes, void* stream) {
   const int phasor = (out_kind & NNAB_SAVE_PHASOR) != 0;
-  out_kind &= ~NNAB_SAVE_PHASOR;
+  const int mag_split = (out_kind & NNAB_SAVE_MAG_SPLIT) != 0;
+  out_kind &= ~(NNAB_SAVE_PHASOR | NNAB_SAVE_MAG_SPLIT);
   if (!prec_valid(precision)) return NNAB_EINVAL;
   const int split = prec_is_split(precision);
   // saves: TF32 / F16 forward -> FP16 phasor (+ TF32 |X|); split modes -> fp32 re, im
@@ -290,6 +303,10 @@ extern "C" int nnab_stft_forward_train_staged(const nnab_frames* f, const float*
   a.save_re = save_re;
   a.save_im = want_im ? save_im : nullptr;
   a.save_mag = save_mag;
+  if (mag_split) {  // [2][n_bins][ld]: the 3xTF32 pair of |X| (split modes' fp32 saves only)
+    if (!split || phasor || !save_mag) return NNAB_EINVAL;
+    a.save_mag_lo = save_mag + (int64_t)n_bins * ld;
+  }
   a.ld_slots = ld;
   a.save_phasor = phasor;
   return launch_stft_gemm(g, a, precision, (cudaStream_t)stream);
@@ -303,8 +320,8 @@ extern "C" int nnab_grad_to_slots_split(const float* g_brt, int64_t B, int32_t r
   if (precision == NNAB_PREC_3XTF32 && !lo) return NNAB_EINVAL;
   const int64_t total = (int64_t)rows * ld;
   if (total == 0) return NNAB_OK;
-  to_slots_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(g_brt, B, rows, T, R, ld, hi, 1,
-                                                                     precision == NNAB_PREC_3XTF32 ? lo : nullptr);
+  to_slots_kernel<<<(int)std::min<int64_t>(B + 1, 65535), 256, 0, (cudaStream_t)stream>>>(
+      g_brt, B, rows, T, R, ld, hi, 1, precision == NNAB_PREC_3XTF32 ? lo : nullptr);
   NNAB_LAUNCHED();
   return NNAB_OK;
 }
@@ -314,7 +331,8 @@ extern "C" int nnab_grad_to_slots(const float* g_brt, int64_t B, int32_t rows, i
   if (!g_brt || !out || rows < 1 || T < 1 || R < T || ld < B * R) return NNAB_EINVAL;
   const int64_t total = (int64_t)rows * ld;
   if (total == 0) return NNAB_OK;
-  to_slots_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(g_brt, B, rows, T, R, ld, out, 0, nullptr);
+  to_slots_kernel<<<(int)std::min<int64_t>(B + 1, 65535), 256, 0, (cudaStream_t)stream>>>(g_brt, B, rows, T, R, ld,
+                                                                                           out, 0, nullptr);
   NNAB_LAUNCHED();
   return NNAB_OK;
 }
@@ -442,7 +460,7 @@ extern "C" int nnab_mel_forward_slots(int32_t n_mels, int64_t ld, int32_t kp, co
     return NNAB_EINVAL;
   if (precision == NNAB_PREC_3XTF32 && (!w_lo || !s_lo)) return NNAB_EINVAL;
   if (ld > INT32_MAX || ld < B * R || R % 4) return NNAB_EINVAL;
-  if (kp > (precision == NNAB_PREC_3XTF32 ? 1024 : 2048)) return NNAB_ENOTSUP;  // one TMEM chain per tile
+  if (kp > 2048) return NNAB_ENOTSUP;  // one TMEM chain per tile
   if (B == 0) return NNAB_OK;
   RGemmArgs g;
   g.M = n_mels;
@@ -523,8 +541,9 @@ extern "C" int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, siz
   unsigned* gmax = reinterpret_cast<unsigned*>(row_exps + 2 * F);
   NNAB_CUDA_TRY(cudaMemsetAsync(gmax, 0, 4, s));
   if (g.B > 0) {
-    clip_absmax_kernel<<<grid_for((int64_t)n_mels * ld), 256, 0, s>>>(gs_hi, gs_lo, (int64_t)n_mels * ld, ld, g.R, 0,
-                                                                       g.B, exps, gmax);
+    const int T = (int)std::min<int64_t>(g.R, g.T);
+    clip_absmax_kernel<<<(int)std::min<int64_t>(g.B, 65535), 256, 0, s>>>(gs_hi, gs_lo, g.B, n_mels, ld, g.R, T,
+                                                                          exps, gmax);
     NNAB_LAUNCHED();
   }
   row_exp_kernel<<<(F + 127) / 128, 128, 0, s>>>(wt_hi, wt_lo, F, kp, n_mels, gmax, row_exps);
@@ -572,7 +591,8 @@ extern "C" int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t 
   NNAB_CUDA_TRY(cudaMemsetAsync(gmax, 0, 4, s));
   const int64_t n = g.B * (int64_t)F * T;
   if (n > 0) {
-    clip_absmax_kernel<<<grid_for(n), 256, 0, s>>>(g_bft, nullptr, n, 0, 1, (int64_t)F * T, g.B, exps, gmax);
+    clip_absmax_kernel<<<(int)std::min<int64_t>(g.B, 65535), 256, 0, s>>>(g_bft, nullptr, g.B, F, T,
+                                                                          (int64_t)F * T, T, exps, gmax);
     NNAB_LAUNCHED();
   }
   row_exp_kernel<<<(F + 127) / 128, 128, 0, s>>>(nullptr, nullptr, F, 0, 0, gmax, row_exps);
