@@ -141,8 +141,13 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
   float* mel_acc = reinterpret_cast<float*>(smem + stages * C::STAGE_BYTES);  // [kMelRows][kBM]
   // kE8 + stage_acc: the fp32 (re | im) staging tile [kBM][256] (16-byte chunks XOR-swizzled by row) in its place
   float* stage_acc = mel_acc;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * C::STAGE_BYTES +
-                                               (mel ? kMelRows * kBM * 4 : (kE8 && p.stage_acc) ? kBM * kBN * 4 : 0));
+  // kE8 + Mel + stage_acc: |X| staging [kBM][128] after the Mel accumulator, then the
+  // folded Nyquist |X| per row
+  float* mag_stage = mel_acc + kMelRows * kBM;
+  float* nyq_stage = mag_stage + kBM * 128;
+  const size_t extra = mel ? kMelRows * kBM * 4 + ((kE8 && p.stage_acc) ? kBM * 128 * 4 + kBM * 4 : 0)
+                           : (kE8 && p.stage_acc) ? kBM * kBN * 4 : 0;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * C::STAGE_BYTES + extra);
   uint64_t* full = bars;            // [stages]  (pair: only the leader's are used)
   uint64_t* empty = bars + 8;       // [stages]
   uint64_t* tmem_full = bars + 16;  // [2]
@@ -281,8 +286,12 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t q = (warp - 4) & 3;  // TMEM lane quarter
-    const int hsel = kE8 ? (int)((warp - 4) >> 2) : 0;  // kE8: chunks hsel, hsel + 2
-    constexpr int CSTEP = kE8 ? 2 : 1;
+    const int hsel = kE8 ? (int)((warp - 4) >> 2) : 0;
+    // kE8: chunks hsel, hsel + 2; with a Mel output both warps of a lane quarter read every
+    // chunk and each accumulates half of every chunk's Mel band rows (each (row, mel) sum
+    // keeps the 4-warp order: deterministic, and no second accumulator)
+    const int CSTEP = (kE8 && !mel) ? 2 : 1;
+    const int c_first = (kE8 && !mel) ? hsel : 0;
     const uint32_t row = q * 32 + lane;
     const int kind = p.out_kind;
     const int F = p.n_bins;
@@ -323,6 +332,94 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
         mbar_wait(&tmem_full[acc], aph);
         tc_fence_after();
         const uint32_t tb = tmem_base + ((q * 32) << 16) + acc * C::ACC_STRIDE;
+        if (kE8 && mel && p.stage_acc) {
+          // Mel with the magnitudes staged: the warp pair of a lane quarter turns its two
+          // chunks into |X| in shared memory and frees TMEM, then each warp projects every
+          // chunk onto its parity's Mel rows while the next tile's MMAs run
+          float4* mrow = reinterpret_cast<float4*>(mag_stage) + row * 32;
+          const int sw = (int)(row & 7);
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)q) : "memory");  // the pair is done reading the staging
+#pragma unroll 1
+          for (int c = hsel; c < 4; c += 2) {
+            float re[32], im[32], cre[32], cim[32];
+            tmem_ld32(tb + c * 32, re);
+            tmem_ld32(tb + 128 + c * 32, im);
+            tmem_ld32(tb + kBN + c * 32, cre);
+            tmem_ld32(tb + kBN + 128 + c * 32, cim);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              re[j] = (re[j] + cre[j]) * osc;
+              im[j] = (im[j] + cim[j]) * osc;
+            }
+            if (p.fold && n == 0 && c == 0) {
+              nyq_stage[row] = finish(im[0], 0.f, kind, p.power, p.eps);  // cosine row of bin F-1 in bin 0's sine slot
+              im[0] = 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              mrow[(c * 8 + j) ^ sw] = make_float4(
+                  finish(re[4 * j], im[4 * j], kind, p.power, p.eps), finish(re[4 * j + 1], im[4 * j + 1], kind, p.power, p.eps),
+                  finish(re[4 * j + 2], im[4 * j + 2], kind, p.power, p.eps),
+                  finish(re[4 * j + 3], im[4 * j + 3], kind, p.power, p.eps));
+          }
+          release_acc(acc);
+          if (++acc == C::NUM_ACC) { acc = 0; aph ^= 1; }
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)q) : "memory");  // both halves staged
+          if (p.fold && n == 0) nyq_val = nyq_stage[row];
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            float m32[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v4 = mrow[(c * 8 + j) ^ sw];
+              m32[4 * j] = v4.x, m32[4 * j + 1] = v4.y, m32[4 * j + 2] = v4.z, m32[4 * j + 3] = v4.w;
+            }
+            const int bin0 = n * 128 + c * 32;
+            const int ch = bin0 >> 5;
+            const int lo = p.mel_band ? p.mel_band[2 * ch] : 0;
+            const int hi = p.mel_band ? p.mel_band[2 * ch + 1] : p.n_mels;
+            int m = lo + ((lo ^ hsel) & 1);
+            for (; m + 2 < hi; m += 4) {
+              const float4* w0 = reinterpret_cast<const float4*>(p.mel_w + (int64_t)m * p.mel_ld + bin0);
+              const float4* w1 = reinterpret_cast<const float4*>(p.mel_w + (int64_t)(m + 2) * p.mel_ld + bin0);
+              float4 wa[8], wb[8];
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                wa[j4] = __ldg(w0 + j4);
+                wb[j4] = __ldg(w1 + j4);
+              }
+              float a = mel_acc[m * kBM + row], a2 = mel_acc[(m + 2) * kBM + row];
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                a = fmaf(wa[j4].x, m32[4 * j4 + 0], a);
+                a2 = fmaf(wb[j4].x, m32[4 * j4 + 0], a2);
+                a = fmaf(wa[j4].y, m32[4 * j4 + 1], a);
+                a2 = fmaf(wb[j4].y, m32[4 * j4 + 1], a2);
+                a = fmaf(wa[j4].z, m32[4 * j4 + 2], a);
+                a2 = fmaf(wb[j4].z, m32[4 * j4 + 2], a2);
+                a = fmaf(wa[j4].w, m32[4 * j4 + 3], a);
+                a2 = fmaf(wb[j4].w, m32[4 * j4 + 3], a2);
+              }
+              mel_acc[m * kBM + row] = a;
+              mel_acc[(m + 2) * kBM + row] = a2;
+            }
+            if (m < hi) {
+              const float4* w = reinterpret_cast<const float4*>(p.mel_w + (int64_t)m * p.mel_ld + bin0);
+              float a = mel_acc[m * kBM + row];
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 wv = __ldg(w + j4);
+                a = fmaf(wv.x, m32[4 * j4 + 0], a);
+                a = fmaf(wv.y, m32[4 * j4 + 1], a);
+                a = fmaf(wv.z, m32[4 * j4 + 2], a);
+                a = fmaf(wv.w, m32[4 * j4 + 3], a);
+              }
+              mel_acc[m * kBM + row] = a;
+            }
+          }
+          continue;
+        }
         if (p.pairs) {
           // columns (2j, 2j+1) = (re, im) of bin 128n + j; complex value re + i*im
           const int bins_here = min(128, F - n * 128);
@@ -370,7 +467,7 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
         const int sw = (int)(row & 7);
         if (kE8 && p.stage_acc) {
 #pragma unroll 1
-          for (int c = hsel; c < 4; c += CSTEP) {
+          for (int c = c_first; c < 4; c += CSTEP) {
             float re[32], im[32], cre[32], cim[32];
             tmem_ld32(tb + c * 32, re);
             tmem_ld32(tb + 128 + c * 32, im);
@@ -390,7 +487,7 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
           release_acc(acc);
         }
 #pragma unroll 1
-        for (int c = hsel; c < 4; c += CSTEP) {
+        for (int c = c_first; c < 4; c += CSTEP) {
           float re[32], im[32];
           if (kE8 && p.stage_acc) {
 #pragma unroll
@@ -429,7 +526,7 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
             nyq_re = im[0];  // cosine row of bin F-1 sits in bin 0's sine slot
             im[0] = 0.f;
           }
-          if (p.save_re) {  // slot-major copies for the backward pass (coalesced across lanes)
+          if (p.save_re && (!kE8 || !mel || hsel == 0)) {  // slot-major copies for the backward (coalesced)
             const int64_t slot = (int64_t)mt * kBM + row;
             if (slot < p.ld_slots) {
 #pragma unroll
@@ -470,19 +567,22 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
             const int ch = bin0 >> 5;
             const int lo = p.mel_band ? p.mel_band[2 * ch] : 0;
             const int hi = p.mel_band ? p.mel_band[2 * ch + 1] : p.n_mels;
+            // kE8: this warp owns the Mel rows of parity hsel (fixed per row, so every
+            // (row, mel) sum is updated by one thread in chunk order)
+            const int mst = kE8 ? 2 : 1;
             // two mel rows per step: independent FMA chains and all 16 weight
             // loads of both rows in flight before the first use
-            int m = lo;
-            for (; m + 1 < hi; m += 2) {
+            int m = kE8 ? lo + ((lo ^ hsel) & 1) : lo;
+            for (; m + mst < hi; m += 2 * mst) {
               const float4* w0 = reinterpret_cast<const float4*>(p.mel_w + (int64_t)m * p.mel_ld + bin0);
-              const float4* w1 = reinterpret_cast<const float4*>(p.mel_w + (int64_t)(m + 1) * p.mel_ld + bin0);
+              const float4* w1 = reinterpret_cast<const float4*>(p.mel_w + (int64_t)(m + mst) * p.mel_ld + bin0);
               float4 wa[8], wb[8];
 #pragma unroll
               for (int j4 = 0; j4 < 8; ++j4) {
                 wa[j4] = __ldg(w0 + j4);
                 wb[j4] = __ldg(w1 + j4);
               }
-              float a = mel_acc[m * kBM + row], a2 = mel_acc[(m + 1) * kBM + row];
+              float a = mel_acc[m * kBM + row], a2 = mel_acc[(m + mst) * kBM + row];
 #pragma unroll
               for (int j4 = 0; j4 < 8; ++j4) {
                 a = fmaf(wa[j4].x, m32[4 * j4 + 0], a);
@@ -495,7 +595,7 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
                 a2 = fmaf(wb[j4].w, m32[4 * j4 + 3], a2);
               }
               mel_acc[m * kBM + row] = a;
-              mel_acc[(m + 1) * kBM + row] = a2;
+              mel_acc[(m + mst) * kBM + row] = a2;
             }
             if (m < hi) {
               const float4* w = reinterpret_cast<const float4*>(p.mel_w + (int64_t)m * p.mel_ld + bin0);
@@ -537,13 +637,17 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
           const int ch = (F - 1) >> 5;
           const int lo = p.mel_band ? p.mel_band[2 * ch] : 0;
           const int hi = p.mel_band ? p.mel_band[2 * ch + 1] : p.n_mels;
-          for (int m = lo; m < hi; ++m)
+          for (int m = kE8 ? lo + ((lo ^ hsel) & 1) : lo; m < hi; m += kE8 ? 2 : 1)
             mel_acc[m * kBM + row] = fmaf(__ldg(p.mel_w + (int64_t)m * p.mel_ld + F - 1), nyq_val, mel_acc[m * kBM + row]);
         }
-        for (int m = 0; m < p.n_mels; ++m) {
+        if (kE8) {  // both halves of the band rows are in: the warp pair syncs on a named barrier
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)q) : "memory");
+        }
+        for (int m = kE8 ? hsel : 0; m < p.n_mels; m += kE8 ? 2 : 1) {
           if (valid) p.out[(b * p.n_mels + m) * (int64_t)p.T + t] = log_out(mel_acc[m * kBM + row], p.log_eps);
           mel_acc[m * kBM + row] = 0.f;
         }
+        if (kE8) asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)q) : "memory");  // zeroed before the next tile's adds
       }
     }
   }
@@ -617,15 +721,17 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   p.pairs = a.pairs;
   p.out_bins = a.out_bins > 0 ? a.out_bins : a.n_bins;
   if (a.kb_tab && (a.n_tab < 1 || mel)) return NNAB_EINVAL;
-  if (kE8 && (mel || a.pairs)) return NNAB_EINVAL;  // per-row Mel accumulation / the pairs loop: 4 warps
+  if (kE8 && a.pairs) return NNAB_EINVAL;  // the pairs loop: 4 warps
   if (p.n_mtiles == 0) return NNAB_OK;
   // as many pipeline stages as fit next to the Mel accumulator (<= 8)
   static const bool stage_env = [] {
     const char* e = getenv("NNAB_STFT_STAGE_ACC");
     return !(e && e[0] == '0');
   }();
-  p.stage_acc = kE8 && stage_env;
-  const size_t mel_bytes = mel ? (size_t)kMelRows * kBM * 4 : p.stage_acc ? (size_t)kBM * kBN * 4 : 0;
+  // staging: the re | im tile, or (Mel, no slot saves) the |X| tile next to the Mel accumulator
+  p.stage_acc = kE8 && stage_env && !(mel && a.save_re);
+  const size_t mel_bytes = mel ? (size_t)kMelRows * kBM * 4 + (p.stage_acc ? (size_t)kBM * 128 * 4 + kBM * 4 : 0)
+                               : p.stage_acc ? (size_t)kBM * kBN * 4 : 0;
   constexpr size_t kBudget = 227 * 1024 - 1024 - 256;  // max dynamic smem - alignment slack - barriers
   int stages = (int)std::min<size_t>(8, (kBudget - mel_bytes) / C::STAGE_BYTES);
   if (const char* e = getenv("NNAB_DEBUG_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));
@@ -675,7 +781,7 @@ int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, c
     case NNAB_PREC_3XTF32: return pair ? launch_impl<NNAB_PREC_3XTF32, true>(g, a, s) : launch_impl<NNAB_PREC_3XTF32, false>(g, a, s);
     case NNAB_PREC_F16: return pair ? launch_impl<NNAB_PREC_F16, true>(g, a, s) : launch_impl<NNAB_PREC_F16, false>(g, a, s);
     case NNAB_PREC_3XF16:
-      if (pair && e8 && (a.out_kind & ~NNAB_OUT_LOG) != NNAB_OUT_MEL && !a.pairs)
+      if (pair && e8 && !a.pairs)
         return launch_impl<NNAB_PREC_3XF16, true, true>(g, a, s);
       return pair ? launch_impl<NNAB_PREC_3XF16, true>(g, a, s) : launch_impl<NNAB_PREC_3XF16, false>(g, a, s);
     default: return NNAB_EINVAL;
