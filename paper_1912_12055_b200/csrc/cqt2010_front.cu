@@ -5,9 +5,8 @@
 // warp set so the HBM stream, the operand conversion, the tensor-core FIRs and the
 // epilogues of consecutive tiles and clips overlap:
 //
-//   warp 5       scan: the peak of the NEXT clip (an L2 bulk prefetch of the whole clip,
-//                then 16 float4 loads in flight per thread, L2 evict-last so the clip is
-//                still in L2 for the converters) -> the clip's power-of-two scale exponent
+//   warp 5       scan: the peak of the NEXT clip's first kPeek samples (the whole clip in
+//                the exact relaunch) -> the clip's power-of-two scale exponent
 //   warps 0-3    epilogue: stage-1 D -> y1 (odd phase -> stage-2 planes, even ->
 //                stage-2 centre planes), y1's reflect images, stage-2 D -> octave 0 (+
 //                its reflect margins) in the level buffer
@@ -24,6 +23,7 @@
 // too, so the epilogue reads nothing but TMEM.  24 MMAs (M = N = 128, K = 16) per tile.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include <cuda_fp16.h>
 
@@ -243,13 +243,9 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
       if (k > 0) wait_p(conv_start, (k - 1) & 1, pf[0]);  // the converter is on clip k - 1
       if (st == 0) tl_mark(p, k, 0, t_begin);
       const float* xb = p.x + clip_of(k) * p.L;
-      // the whole clip is requested from HBM at once (L2 prefetch: no registers, no shared
-      // memory in flight); the scan's loads then meet lines already arriving
-      {
-        const uint32_t bytes = (uint32_t)p.L * 4u, piece = ((bytes + 31) / 32 + 15) & ~15u;
-        const uint32_t o = (uint32_t)st * piece;
-        if (o < bytes) prefetch_l2(reinterpret_cast<const char*>(xb) + o, min(piece, bytes - o));
-      }
+      // (no L2 bulk prefetch of the clip: prefetching the next one ahead of the converters
+      // made the route 0.325 -> 0.357 ms, two or three clips ahead 0.38 ms -- the prefetches
+      // compete with the converters' demand loads)
       float mx = 0.f;
       const int n4s = p.exact ? n4 : min(n4, kPeek / 4);  // fast: the first kPeek samples
       for (int f0 = st; f0 < n4s; f0 += kScanBatch * 32) {
@@ -317,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
     const int ro = ct >> 6, re = ((ct - 32 + 64) >> 6) - 1;
     const uint32_t oo = (uint32_t)((uo >> 3) * p.pl1 + (uo & 7) * 2 + ro * 16);
     const uint32_t oe = (uint32_t)(16 * p.pl1 + (ue >> 3) * p.pe1 + (ue & 7) * 2 + 16 * re);  // row re at u = 0
-    const uint64_t last = policy_evict_first();
+    const uint64_t last = policy_evict_first();  // (evict_unchanged / evict_last: no faster)
     uint32_t g1 = 0;
     for (int k = 0; k < n_clips; ++k) {
       const int64_t b = clip_of(k);
@@ -579,6 +575,7 @@ int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps
                          cudaStream_t st) {
   if (n_taps != 255 || L % 4 != 0 || L < 1024 || L > (1 << 24) || !flags || !list || !list_n) return NNAB_ENOTSUP;
   FrontParams p{};
+
   p.x = x;
   p.B = B;
   p.L = (int32_t)L;
