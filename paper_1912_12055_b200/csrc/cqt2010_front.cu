@@ -61,10 +61,11 @@ struct FrontParams {
   unsigned long long* prof;  // debug: per-role wait cycles (nnab_debug_cqt2010_front_profile), or null
   // scale: exact = 0 (fast): the scale comes from the clip's first kPeek samples with kHead
   // bits of headroom, and a clip whose peak would leave that headroom (or whose first
-  // kPeek samples are all zero) is flagged in flags[b]; exact = 1: the exact peak of the
+  // kPeek samples are all zero) is appended to out_list; exact = 1: the exact peak of the
   // whole clip (a full scan), over the clips listed in list[0 .. *list_n) (the flagged ones)
   int32_t exact;
-  int32_t* flags;
+  int32_t* out_list;      // fast launch: flagged clips appended here ...
+  int32_t* out_list_n;    // ... (count, zeroed before the launch)
   const int32_t* list;
   const int32_t* list_n;
 };
@@ -163,6 +164,9 @@ NNAB_DEV void issue_tile(uint32_t d_tmem, uint32_t odd, uint32_t pl, uint32_t ev
 }
 
 __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid_constant__ FrontParams p) {
+  // the exact relaunch over the flagged clips: CTAs without a listed clip leave at once
+  // (usually all of them: no TMEM allocation, no shared-memory setup)
+  if (p.list && (int64_t)*p.list_n <= (int64_t)blockIdx.x) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + p.off_bars);
@@ -380,7 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
         named_sync(4, 32 * kConvWarps);
         if (ct == 0) {
           const float m = __uint_as_float(conv_max[k & 1]);
-          if (zero_peek || !(m * scale < 16384.f)) p.flags[b] = 1;
+          // flagged: appended to the exact relaunch's list (any order: each listed clip is
+          // redone on its own, so the output does not depend on it)
+          if (zero_peek || !(m * scale < 16384.f)) p.out_list[atomicAdd(p.out_list_n, 1)] = (int32_t)b;
           conv_max[k & 1] = 0u;  // reused by clip k + 2, after clip k + 1's barrier
         }
       }
@@ -553,16 +559,6 @@ __device__ unsigned long long g_front_prof[24];
 bool g_front_prof_on = false;
 
 // the flagged clips' indices (order irrelevant: clips are independent) and their count
-__global__ void cqt2010_flag_list_kernel(const int32_t* flags, int64_t B, int32_t* list, int32_t* list_n) {
-  __shared__ int32_t cnt;
-  if (threadIdx.x == 0) cnt = 0;
-  __syncthreads();
-  for (int64_t b = threadIdx.x; b < B; b += blockDim.x)
-    if (flags[b]) list[atomicAdd(&cnt, 1)] = (int32_t)b;
-  __syncthreads();
-  if (threadIdx.x == 0) *list_n = cnt;
-}
-
 }  // namespace
 
 // Shared-memory plan + launches; NNAB_ENOTSUP outside the kernel's envelope (the caller
@@ -620,14 +616,16 @@ int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps
   }
   NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (int)std::min<int64_t>(B, (int64_t)num_sms());
-  NNAB_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)B * 4, st));
+  (void)flags;
+  NNAB_CUDA_TRY(cudaMemsetAsync(list_n, 0, 4, st));
   p.exact = 0;
-  p.flags = flags;
+  p.out_list = list;
+  p.out_list_n = list_n;
   cqt2010_front_kernel<<<grid, kThreads, smem, st>>>(p);
   NNAB_LAUNCHED();
-  cqt2010_flag_list_kernel<<<1, 1024, 0, st>>>(flags, B, list, list_n);
-  NNAB_LAUNCHED();
   p.exact = 1;
+  p.out_list = nullptr;
+  p.out_list_n = nullptr;
   p.list = list;
   p.list_n = list_n;
   p.prof = nullptr;
