@@ -64,6 +64,7 @@ struct FrontParams {
   // kPeek samples are all zero) is appended to out_list; exact = 1: the exact peak of the
   // whole clip (a full scan), over the clips listed in list[0 .. *list_n) (the flagged ones)
   int32_t exact;
+  CqtPrepArgs prep;       // fast launch: the back end's bank images (toep_img null: none)
   int32_t* out_list;      // fast launch: flagged clips appended here ...
   int32_t* out_list_n;    // ... (count, zeroed before the launch)
   const int32_t* list;
@@ -167,6 +168,26 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_front_kernel(const __grid
   // the exact relaunch over the flagged clips: CTAs without a listed clip leave at once
   // (usually all of them: no TMEM allocation, no shared-memory setup)
   if (p.list && (int64_t)*p.list_n <= (int64_t)blockIdx.x) return;
+  if (p.prep.toep_img) {  // the back end's bank images (cqt2010_prep_kernel's formulas), spread over the grid
+    const int gt = blockIdx.x * kThreads + threadIdx.x, gn = gridDim.x * kThreads;
+    for (int j = gt; j < kToepChunks; j += gn) {  // chunk j = g[j - 127 + e]
+      __align__(16) __half v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int gi = j - 127 + e;
+        v[e] = __float2half_rn((gi >= 0 && gi < 128) ? p.g[gi] : 0.f);
+      }
+      p.prep.toep_img[j] = *reinterpret_cast<uint4*>(v);
+    }
+    __half* f = reinterpret_cast<__half*>(p.prep.filt_img);
+    for (int e = gt; e < p.prep.nconv * p.prep.kc; e += gn) {
+      const int n = e / p.prep.kc, m = e % p.prep.kc, j = n >> 1, tap = m - p.prep.shift;
+      float v = 0.f;
+      if (j < p.prep.n_filt && tap >= 0 && tap < p.prep.width)
+        v = ldexpf(((n & 1) ? p.prep.k_im : p.prep.k_re)[(int64_t)j * p.prep.width + tap], p.prep.filt_log2);
+      f[(m >> 3) * (8 * p.prep.nconv) + n * 8 + (m & 7)] = __float2half_rn(v);
+    }
+  }
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + p.off_bars);
@@ -568,7 +589,7 @@ bool g_front_prof_on = false;
 // list_n: one int, in the caller's workspace.
 int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, __half* lv0,
                          int32_t lv0_stride, int32_t* exps, int32_t* flags, int32_t* list, int32_t* list_n,
-                         cudaStream_t st) {
+                         cudaStream_t st, const CqtPrepArgs* prep) {
   if (n_taps != 255 || L % 4 != 0 || L < 1024 || L > (1 << 24) || !flags || !list || !list_n) return NNAB_ENOTSUP;
   FrontParams p{};
 
@@ -619,11 +640,13 @@ int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps
   (void)flags;
   NNAB_CUDA_TRY(cudaMemsetAsync(list_n, 0, 4, st));
   p.exact = 0;
+  if (prep) p.prep = *prep;
   p.out_list = list;
   p.out_list_n = list_n;
   cqt2010_front_kernel<<<grid, kThreads, smem, st>>>(p);
   NNAB_LAUNCHED();
   p.exact = 1;
+  p.prep = CqtPrepArgs{};
   p.out_list = nullptr;
   p.out_list_n = nullptr;
   p.list = list;

@@ -1615,12 +1615,25 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
     p.lv[a] = reinterpret_cast<__half*>(ws + lp.off[a]);
     p.lv_stride[a] = lp.stride[a];
   }
-  // mode 3: the warp-specialised front (cqt2010_front.cu) for stages 1-2, then as mode 1
+  // mode 3: the warp-specialised front (cqt2010_front.cu) for stages 1-2, then as mode 1;
+  // it also writes the bank images cqt2010_prep_kernel would
+  CqtPrepArgs pa;
+  pa.toep_img = reinterpret_cast<uint4*>(ws + lp.toep_off);
+  pa.filt_img = reinterpret_cast<uint4*>(ws + lp.filt_off);
+  pa.k_re = k_re;
+  pa.k_im = k_im;
+  pa.n_filt = n_filt;
+  pa.width = width;
+  pa.shift = p.pad_al - p.pad;
+  pa.nconv = NCONV;
+  pa.kc = KC;
+  pa.filt_log2 = kFiltLog2;
   rc = mode == 3 ? launch_cqt2010_front(x, B, L, taps, n_taps, p.lv0, p.lv0_stride, exps,
                                         reinterpret_cast<int32_t*>(ws + lp.flag_off),
                                         reinterpret_cast<int32_t*>(ws + lp.list_off),
-                                        reinterpret_cast<int32_t*>(ws + lp.list_off) + B, st)
+                                        reinterpret_cast<int32_t*>(ws + lp.list_off) + B, st, &pa)
                   : NNAB_ENOTSUP;
+  const bool prepped = mode == 3 && rc == NNAB_OK;
   if (rc == NNAB_ENOTSUP) {
     if (mode == 3) p.lv_mode = 1;
     NNAB_CUDA_TRY(cudaFuncSetAttribute(cqt2010_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
@@ -1650,9 +1663,11 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
   q.prof = cqt2010_prof_ptr();
   q.toep_img = reinterpret_cast<const uint4*>(ws + lp.toep_off);
   q.filt_img = reinterpret_cast<const uint4*>(ws + lp.filt_off);
-  cqt2010_prep_kernel<<<8, 256, 0, st>>>(q, reinterpret_cast<uint4*>(ws + lp.toep_off),
-                                          reinterpret_cast<uint4*>(ws + lp.filt_off));
-  NNAB_LAUNCHED();
+  if (!prepped) {
+    cqt2010_prep_kernel<<<8, 256, 0, st>>>(q, reinterpret_cast<uint4*>(ws + lp.toep_off),
+                                            reinterpret_cast<uint4*>(ws + lp.filt_off));
+    NNAB_LAUNCHED();
+  }
   if (mode3) {
     // mode 3: the octave chain and every octave's conv in one launch (cqt2010_back.cu); else the
     // chain launch (cqt2010_chain.cu) + the batched conv; else the HALVE launches + batched conv

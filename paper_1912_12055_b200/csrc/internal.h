@@ -147,9 +147,16 @@ int launch_cqt2010_levels(const float* x, int64_t B, int64_t L, const float* tap
                           void* workspace, size_t workspace_bytes, cudaStream_t st, int mode);
 // CQT2010v2 front (cqt2010_front.cu): stages 1-2 of every clip -> the octave-0 level buffer
 // (FP16 in the clip's scale 2^-exps[b], reflect margins); NNAB_ENOTSUP outside its envelope
+// the conv-bank images the back end reads (cqt2010_prep_kernel's work), written by the front
+// launch instead of a launch of their own
+struct CqtPrepArgs {
+  uint4 *toep_img = nullptr, *filt_img = nullptr;
+  const float *k_re = nullptr, *k_im = nullptr;
+  int n_filt = 0, width = 0, shift = 0, nconv = 0, kc = 0, filt_log2 = 0;
+};
 int launch_cqt2010_front(const float* x, int64_t B, int64_t L, const float* taps, int n_taps, __half* lv0,
                          int32_t lv0_stride, int32_t* exps, int32_t* flags, int32_t* list, int32_t* list_n,
-                         cudaStream_t st);
+                         cudaStream_t st, const CqtPrepArgs* prep = nullptr);
 // CQT2010v2 back end (cqt2010_back.cu): the octave chain and every octave's conv of clip
 // groups in one launch (level 0 written by the front, the conv bank image by the prep kernel)
 struct CqtBackArgs {
