@@ -11,7 +11,7 @@
 //                stage-2 centre planes), y1's reflect images, stage-2 D -> octave 0 (+
 //                its reflect margins) in the level buffer
 //   warp 4       MMA issue (one thread) + TMEM allocation (512 columns)
-//   warps 6-17   converters: the tile's clip segment from L2 (16 float4 loads in flight
+//   warps 6-19   converters: the tile's clip segment from HBM (10 float4 loads in flight
 //                per thread) -> scaled FP16, odd phase -> stage-1 "planes", even phase ->
 //                centre-tap planes, into one of two stage-1 operand buffers
 //
@@ -38,7 +38,7 @@ constexpr int kToepChunks = 8 * 31 + 128;  // Toeplitz diagonal chunks (cqt2010_
 constexpr int kCenChunks = 256;
 constexpr int kScanWarps = 1;
 constexpr int kScanBatch = 24;           // float4 loads in flight per scan thread
-constexpr int kEpiWarp0 = 0, kMmaWarp = 4, kScanWarp0 = 5, kConvWarp0 = 6, kConvWarps = 12;  // 18 warps
+constexpr int kEpiWarp0 = 0, kMmaWarp = 4, kScanWarp0 = 5, kConvWarp0 = 6, kConvWarps = 14;  // 20 warps (12: 0.322 ms, 16 / 18: 0.318 / 0.320)
 constexpr int kCT = 32 * kConvWarps;     // converter threads
 constexpr int kRowU = kCT / 64;          // plane rows one float4 step of every converter thread covers
 constexpr int kConvBatch = 10;           // float4 loads in flight per converter thread
