@@ -38,7 +38,8 @@ constexpr int kToepChunks = 8 * 31 + 128;  // Toeplitz diagonal chunks (cqt2010_
 constexpr int kCenChunks = 256;
 constexpr int kScanWarps = 1;
 constexpr int kScanBatch = 24;           // float4 loads in flight per scan thread
-constexpr int kEpiWarp0 = 0, kMmaWarp = 4, kScanWarp0 = 5, kConvWarp0 = 6, kConvWarps = 14;  // 20 warps (12: 0.322 ms, 16 / 18: 0.318 / 0.320)
+constexpr int kEpiWarp0 = 0, kMmaWarp = 4, kScanWarp0 = 5, kConvWarp0 = 6, kConvWarps = 14;  // 20 warps (12: 0.322 ms, 16 / 18: 0.318 / 0.320;
+                                                                                             // 8 epilogue warps: 0.323-0.33)
 constexpr int kCT = 32 * kConvWarps;     // converter threads
 constexpr int kRowU = kCT / 64;          // plane rows one float4 step of every converter thread covers
 constexpr int kConvBatch = 10;           // float4 loads in flight per converter thread
