@@ -499,7 +499,10 @@ def main():
         else:
             ach, peak = per / t / 1e9, hbm_peak
         return {"bound": work["bound"], "achieved": ach, "peak": peak, "unit": work["unit"], "frac": ach / peak,
-                "traffic": traffic.get(work["kernel"] + ":" + args.workload) if work["kernel"] else None,
+                # measured per precision where a capture exists (kernel:workload:precision), else the
+                # default mode's capture (kernel:workload)
+                "traffic": (traffic.get(f'{work["kernel"]}:{args.workload}:{args.precision}',
+                                        traffic.get(work["kernel"] + ":" + args.workload)) if work["kernel"] else None),
                 "kernel": work["kernel"], "kernel_ms": kernel_ms,
                 "peak_source": ((f"FP16 dense = measured bf16 {bf16_peak:.1f} TF/s ({peak_src}, burst)" if mma == "f16"
                                  else f"TF32 = measured dense bf16 {bf16_peak:.1f} TF/s / 2 ({peak_src}, burst)")
