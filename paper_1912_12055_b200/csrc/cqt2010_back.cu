@@ -12,11 +12,11 @@
 //              the conv's shifted copies; arrives lvl_ready[a + 1]
 //   warps 8-15 conv epilogue: two warpgroups on alternate tiles
 //
-// Each CTA walks PAIRS of clip groups with their levels interleaved (group A level a,
-// group B level a, group A level a + 1, ...), so one group's level transition (drain,
-// margins, barrier) hides behind the other's tiles.  Level a's conv and halving both need
+// Each CTA walks SETS of kNG clip groups with their levels interleaved (group A level a,
+// group B level a, group C level a, group A level a + 1, ...), so one group's level
+// transition (drain, margins, barrier) hides behind the others' tiles.  Level a's conv and halving both need
 // level a of that group complete (lvl_ready[group][a]; level 0 comes from the front
-// kernel); the halving producer waits for the conv producer to finish the previous pair,
+// kernel); the halving producer waits for the conv producer to finish the previous set,
 // so no level barrier runs two phases ahead of a waiter.
 #include <algorithm>
 #include <cmath>
@@ -48,6 +48,10 @@ constexpr int KC = 96, NCONV = 32, kFiltLog2 = 6;
 constexpr int kCMaps = 8;
 constexpr uint32_t kRows8 = 128 + KC / 8 - 1;
 constexpr int kMaxG = 8;     // clips per group (the margin buffers)
+#ifndef NNAB_BACK_NG
+#define NNAB_BACK_NG 3  // 2: 0.316-0.317 ms, 3: 0.314-0.315, 4: 0.326, 6: 0.364
+#endif
+constexpr int kNG = NNAB_BACK_NG;  // clip groups per CTA, levels interleaved between them
 constexpr int kMLeft = 160;  // margin sources kept in shared memory: outputs [0, 160) ...
 constexpr int kMRight = 192; // ... and [rb, rb + 192), rb = (n - 160) rounded down to 32
 
@@ -98,8 +102,8 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
   uint64_t* c_full = hd_empty + 2;                // [kCStages] tx
   uint64_t* c_mma = c_full + kCStages;            // [kCStages] commit
   uint64_t* c_tfree = c_mma + kCStages;           // [kCStages] 4 warps
-  uint64_t* lvl_ready = c_tfree + kCStages;       // [2][kMaxLv] per group of the pair, 128 halving-epilogue threads
-  uint64_t* cgrp_done = lvl_ready + 2 * kMaxLv;   // conv producer finished a group pair
+  uint64_t* lvl_ready = c_tfree + kCStages;       // [kNG][kMaxLv] per group of the set, 128 halving-epilogue threads
+  uint64_t* cgrp_done = lvl_ready + kNG * kMaxLv; // conv producer finished a group set
   uint32_t* tslot = reinterpret_cast<uint32_t*>(cgrp_done + 1);
   int32_t* exps_s = reinterpret_cast<int32_t*>(tslot + 4);  // B ints
   __half* mbuf = reinterpret_cast<__half*>((reinterpret_cast<uintptr_t>(exps_s + p.B) + 15) & ~uintptr_t(15));  // [kMaxG][kMLeft + kMRight]
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
       mbar_init(&c_mma[i], 1);
       mbar_init(&c_tfree[i], 4);
     }
-    for (int i = 0; i < 2 * kMaxLv; ++i) mbar_init(&lvl_ready[i], 128);
+    for (int i = 0; i < kNG * kMaxLv; ++i) mbar_init(&lvl_ready[i], 128);
     mbar_init(cgrp_done, 1);
     fence_barrier_init();
   }
@@ -162,11 +166,11 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
     if (elect_one()) {
       uint32_t kq = 0;
       int gi = 0;
-      for (int pr = blockIdx.x; 2 * pr < n_groups; pr += gridDim.x, ++gi) {
+      for (int pr = blockIdx.x; kNG * pr < n_groups; pr += gridDim.x, ++gi) {
         if (gi > 0) W(cgrp_done, (gi - 1) & 1, 0);  // keeps lvl_ready at most one pair ahead
         for (int a = 0; a + 1 < nl; ++a)
-        for (int hm = 0; hm < 2 && 2 * pr + hm < n_groups; ++hm) {
-          const int b0 = (2 * pr + hm) * p.G, gc = min(p.G, p.B - b0);
+        for (int hm = 0; hm < kNG && kNG * pr + hm < n_groups; ++hm) {
+          const int b0 = (kNG * pr + hm) * p.G, gc = min(p.G, p.B - b0);
           if (a > 0) W(&lvl_ready[hm * kMaxLv + a], gi & 1, 1);
           const int R = p.R[a], nt = htiles(a, gc);
           for (int t = 0; t < nt; ++t) {
@@ -187,10 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
       constexpr uint32_t idesc = idesc_f16(128, 128);
       const uint32_t e0 = smem_u32(E);
       uint32_t kq = 0, sq = 0;
-      for (int pr = blockIdx.x; 2 * pr < n_groups; pr += gridDim.x) {
+      for (int pr = blockIdx.x; kNG * pr < n_groups; pr += gridDim.x) {
         for (int a = 0; a + 1 < nl; ++a)
-        for (int hm = 0; hm < 2 && 2 * pr + hm < n_groups; ++hm) {
-          const int gc = min(p.G, p.B - (2 * pr + hm) * p.G);
+        for (int hm = 0; hm < kNG && kNG * pr + hm < n_groups; ++hm) {
+          const int gc = min(p.G, p.B - (kNG * pr + hm) * p.G);
           const int nt = htiles(a, gc);
           for (int t = 0; t < nt; ++t, ++sq) {
             const uint32_t d = sq & 1;
@@ -217,10 +221,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
     if (elect_one()) {
       uint32_t i = 0;
       int gi = 0;
-      for (int pr = blockIdx.x; 2 * pr < n_groups; pr += gridDim.x, ++gi) {
+      for (int pr = blockIdx.x; kNG * pr < n_groups; pr += gridDim.x, ++gi) {
         for (int a = 0; a < nl; ++a)
-        for (int hm = 0; hm < 2 && 2 * pr + hm < n_groups; ++hm) {
-          const int b0 = (2 * pr + hm) * p.G, gc = min(p.G, p.B - b0);
+        for (int hm = 0; hm < kNG && kNG * pr + hm < n_groups; ++hm) {
+          const int b0 = (kNG * pr + hm) * p.G, gc = min(p.G, p.B - b0);
           if (a > 0) W(&lvl_ready[hm * kMaxLv + a], gi & 1, 0);
           const int rs = p.rs[a], U = p.U[a], tpc = (gc * U + 127) / 128;
           for (int v = 0; v < p.copies[a]; ++v) {
@@ -257,10 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
       constexpr uint32_t idesc = idesc_f16(128, NCONV);
       const uint32_t b0s = smem_u32(filt);
       uint32_t i = 0;
-      for (int pr = blockIdx.x; 2 * pr < n_groups; pr += gridDim.x) {
+      for (int pr = blockIdx.x; kNG * pr < n_groups; pr += gridDim.x) {
         for (int a = 0; a < nl; ++a)
-        for (int hm = 0; hm < 2 && 2 * pr + hm < n_groups; ++hm) {
-          const int gc = min(p.G, p.B - (2 * pr + hm) * p.G);
+        for (int hm = 0; hm < kNG && kNG * pr + hm < n_groups; ++hm) {
+          const int gc = min(p.G, p.B - (kNG * pr + hm) * p.G);
           const int rs = p.rs[a], nt = ctiles(a, gc);
           for (int t = 0; t < nt; ++t, ++i) {
             const int s = (int)(i % kCStages);
@@ -287,10 +291,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
     // ------------------------------------------------------------ halving epilogue + level edges
     const int q = warp & 3, et = tid - 128;
     uint32_t sq = 0;
-    for (int pr = blockIdx.x; 2 * pr < n_groups; pr += gridDim.x) {
+    for (int pr = blockIdx.x; kNG * pr < n_groups; pr += gridDim.x) {
       for (int a = 0; a + 1 < nl; ++a)
-      for (int hm = 0; hm < 2 && 2 * pr + hm < n_groups; ++hm) {
-        const int b0 = (2 * pr + hm) * p.G, gc = min(p.G, p.B - b0);
+      for (int hm = 0; hm < kNG && kNG * pr + hm < n_groups; ++hm) {
+        const int b0 = (kNG * pr + hm) * p.G, gc = min(p.G, p.B - b0);
         const int R = p.R[a], nt = htiles(a, gc);
         const int n_out = p.n[a + 1], nb = (n_out + 127) / 128;
         __half* dst = p.lv[a + 1];
@@ -400,10 +404,10 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
     const int q = warp & 3, eg = (warp - 8) >> 2;
     const int j_hi = min(p.n_filt, NCONV / 2);
     uint32_t i = 0;
-    for (int pr = blockIdx.x; 2 * pr < n_groups; pr += gridDim.x) {
+    for (int pr = blockIdx.x; kNG * pr < n_groups; pr += gridDim.x) {
       for (int a = 0; a < nl; ++a)
-      for (int hm = 0; hm < 2 && 2 * pr + hm < n_groups; ++hm) {
-        const int b0 = (2 * pr + hm) * p.G, gc = min(p.G, p.B - b0);
+      for (int hm = 0; hm < kNG && kNG * pr + hm < n_groups; ++hm) {
+        const int b0 = (kNG * pr + hm) * p.G, gc = min(p.G, p.B - b0);
         const int U = p.U[a], C = p.copies[a], tpc = (gc * U + 127) / 128;
         const int lskip = max(0, a * p.bpo - p.first_bin), lrow0 = p.first_bin - a * p.bpo;
         for (int v = 0; v < C; ++v) {
@@ -475,7 +479,7 @@ int launch_cqt2010_back(const CqtBackArgs& g, cudaStream_t st) {
   BackParams& p = *pp;
   p.n_oct = n_oct;
   p.B = (int32_t)B;
-  p.G = (int32_t)((B + 2 * num_sms() - 1) / (2 * num_sms()));  // two groups (a pair) per CTA
+  p.G = (int32_t)((B + kNG * num_sms() - 1) / (kNG * num_sms()));  // kNG groups per CTA
   for (int j = 0; j < 255; ++j) p.taps[j] = g.taps[j];
   p.T = g.T;
   p.n_bins = g.n_bins;
@@ -527,14 +531,14 @@ int launch_cqt2010_back(const CqtBackArgs& g, cudaStream_t st) {
     }
   }
   const size_t smem = 1024 + kHStages * kKB + kERows * 128 + kCStages * kCA + KC / 8 * 512 +
-                      (2 * kHStages + 4 + 3 * kCStages + 2 * kMaxLv + 1) * 8 + 16 + 4 * (size_t)((B + 7) & ~7) +
+                      (2 * kHStages + 4 + 3 * kCStages + kNG * kMaxLv + 1) * 8 + 16 + 4 * (size_t)((B + 7) & ~7) +
                       2 * kMaxG * (kMLeft + kMRight) + 16;
   if (p.G > kMaxG) rc = NNAB_ENOTSUP;
   if (!rc && smem > 227 * 1024) rc = NNAB_ENOTSUP;
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(cqt2010_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) {
-      const int pairs = (int)(((B + p.G - 1) / p.G + 1) / 2);
+      const int pairs = (int)(((B + p.G - 1) / p.G + kNG - 1) / kNG);  // group sets
       cqt2010_back_kernel<<<std::min(pairs, num_sms()), kThreads, smem, st>>>(p);
       e = cudaGetLastError();
     }
