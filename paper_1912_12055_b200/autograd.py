@@ -36,9 +36,10 @@ class DftLayerOp:
 
     def __init__(self, h_re, h_im, hop: int, center: bool = True, pad_mode: str = "reflect", eps: float = 1e-12,
                  precision: str = "tf32", device="cuda", phasor: str = "split"):
-        # trainable sine rows may leave zero -> never fold the Nyquist bin
+        # the Nyquist cosine row rides in bin 0's sine slot while both zero sine rows stay exactly
+        # zero (8 bank tiles instead of 9 for n_fft = 2048); re-checked at every set_bank
         self.engine = DftEngine(h_re, h_im, hop, center, pad_mode, precision=precision, device=device,
-                                allow_fold=False, f16_ok=False)
+                                allow_fold="exact", f16_ok=False)
         self.eps = float(eps)
         self.device = self.engine.device
         self.prec = self.engine.precision
@@ -61,7 +62,7 @@ class DftLayerOp:
         if (self.prec == L.PREC_TF32 and phasor == "split") or (self.split and same_rows):
             self.fwd_prec = L.PREC_3XF16 if same_rows else L.PREC_3XTF32
             self.fwd_engine = DftEngine(h_re, h_im, hop, center, pad_mode, precision="3xf16", device=device,
-                                        allow_fold=False)
+                                        allow_fold="exact")
             if self.fwd_prec == L.PREC_3XTF32:
                 self.fwd_engine.precision = L.PREC_3XTF32
                 self.fwd_engine.set_bank(h_re, h_im)

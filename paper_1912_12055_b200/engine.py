@@ -91,7 +91,12 @@ class DftEngine:
         if self.hop < 1:
             raise ValueError(f"stride must be >= 1, got {hop}")
         self.fold = 0
-        if allow_fold and self.n_bins >= 2:
+        # allow_fold="exact" (trainable banks): fold only while the bin-0 and Nyquist sine rows are
+        # zero to 1e-9 of the bank's peak (sin(pi k) rounding), re-checked at every set_bank; their
+        # gradients are as small (im ~ 0 makes coef_im ~ 0, gradients.py:127-129), so training
+        # keeps them there
+        self._fold_exact = allow_fold == "exact"
+        if allow_fold and not self._fold_exact and self.n_bins >= 2:
             scale = float(h_re.abs().max()) or 1.0
             z0 = float(h_im[0].abs().max()) <= 1e-9 * scale
             zn = float(h_im[-1].abs().max()) <= 1e-9 * scale
@@ -108,6 +113,9 @@ class DftEngine:
         h_re = torch.as_tensor(h_re).to(self.device, torch.float32).contiguous()
         h_im = torch.as_tensor(h_im).to(self.device, torch.float32).contiguous()
         self._bank = (h_re, h_im)
+        if self._fold_exact:  # one read back per repack
+            self.fold = int(self.n_bins >= 2 and (self.n_bins - 1) % 128 == 0 and
+                            bool(h_im[[0, -1]].abs().amax() <= 1e-9 * h_re.abs().amax()))
         nbytes = lib.nnab_dft_bank_bytes_prec(self.n_bins, self.n_fft, self.fold, self.precision)
         n = nbytes // 4
         if getattr(self, "packed_hi", None) is None or self.packed_hi.numel() != n:

@@ -405,3 +405,34 @@ def test_kernel_grad_f16_vs_float64(cuda_dev, n_fft, hop, F, B, spread):
     assert torch.isfinite(dk).all()
     err = float((dk.double() - ref).abs().max() / ref.abs().max())
     assert err <= 1e-5, err
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("sine0", [0.0, 0.3])
+def test_trainable_nyquist_fold_exact(cuda_dev, precision, sine0):
+    """n_fft = 256 (129 bins): the trainable layer packs the Nyquist cosine row into bin 0's sine
+    slot (one bank tile fewer at n_fft = 2048) only while bin 0's and the Nyquist's sine rows are zero
+    to 1e-9 of the bank peak; with a non-zero one it runs unfolded, and set_bank re-decides.  Forward S, dh_re,
+    dh_im and dx against the float64 oracle either way (gradients.py:61-67, 103-149)."""
+    from paper_1912_12055_b200.spectro import DftKernelBank, Signal, spectrogram_vjp
+    h_re, h_im = O.stft_bank(256, 8000.0)
+    h_im = h_im.copy()
+    h_im[0] = sine0 * np.random.default_rng(3).standard_normal(256)
+    layer = layer_for(DftKernelBank(h_re, h_im), 64, precision)
+    assert layer._op.engine.fold == int(sine0 == 0.0)
+    x = (np.random.default_rng(4).standard_normal(4096) * 0.5).astype(np.float32)
+    S = layer.spectrogram(Signal(x, 8000.0)).cpu().numpy()
+    _, _, _, S_ref = O.smooth_mag_forward(x.astype(np.float64), h_re, h_im, 64)
+    assert O.peak_err(S, S_ref) <= TOL[precision]
+    c = np.random.default_rng(5).standard_normal(S.shape)
+    got, gx = spectrogram_vjp(Signal(x, 8000.0), layer, c, with_input_grad=True)
+    ref, gx_ref = O.conv_layer_vjp(x.astype(np.float64), h_re, h_im, 64, c, with_input_grad=True)
+    # 65 frames x 129 bins: one near-zero |X| on this seed (FP32 mode: 7.05e-5 on dh_im bin 105,
+    # identical folded or not, tools/probe_fold.py), hence the joint gates
+    for name in ("h_re", "h_im"):
+        assert O.peak_err(got[name].cpu().numpy(), ref[name]) <= TOL_GRAD_JOINT[precision], name
+    assert O.peak_err(gx.cpu().numpy(), gx_ref) <= TOL_GRAD_JOINT[precision]
+    if sine0 == 0.0:  # the folded rows' gradients are zero: still folded after a repack
+        assert float(np.abs(got["h_im"][0].cpu().numpy()).max()) == 0.0
+        layer._op.set_bank(torch.as_tensor(h_re), torch.as_tensor(h_im))
+        assert layer._op.engine.fold == 1
