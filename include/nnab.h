@@ -255,7 +255,10 @@ int nnab_kernel_grad(const nnab_frames* f, const float* coef_hi, const float* co
  * the GEMM's epilogue multiplies row m by 2^-row_exps[m].  row_exps: int32[2F + 1]
  * (the last word is scratch).  coef_hi/coef_lo: FP16 [2F][ld]; ld % 8 == 0.
  * Replaces nnab_dft_coef / nnab_mel_dft_coef + nnab_kernel_grad in NNAB_PREC_3XTF32
- * (gradients.py:125-129); the row exponent comes from a bound on |dS| (no pass over coef). */
+ * (gradients.py:125-129); the row exponent comes from a bound on |dS| (no pass over coef).
+ * coef_lo = NULL: one FP16 pass (11-bit operands, the TF32 mode's accuracy): coef hi only,
+ * the frames' hi rows only; the coef inputs may then be TF32 (wt_lo / gs_lo NULL) and
+ * re_s the FP16 unit phasor of a TF32-backward forward (im_s NULL). */
 int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t F, int64_t ld,
                           int32_t kp, const float* wt_hi, const float* wt_lo, const float* gs_hi, const float* gs_lo,
                           int32_t n_mels, const float* re_s, const float* im_s, float eps, void* coef_hi,

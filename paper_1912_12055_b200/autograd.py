@@ -66,10 +66,11 @@ class DftLayerOp:
             if self.fwd_prec == L.PREC_3XTF32:
                 self.fwd_engine.precision = L.PREC_3XTF32
                 self.fwd_engine.set_bank(h_re, h_im)
-        # FP32 mode: the kernel gradient runs 3xF16 on the forward's FP16 staging
-        # (nnab_kernel_grad_f16) where that staging holds hop rows of 64-sample multiples
+        # the kernel gradient runs on FP16 tensor cores over the 3xF16 forward's staging
+        # (nnab_kernel_grad_f16) where that staging holds hop rows of 64-sample multiples:
+        # 3xF16 in FP32 mode, one FP16 pass (11-bit operands, as TF32) in TF32 mode
         hop, k64 = eng.hop, (eng.n_fft + 63) // 64 * 64
-        self.f16_dk = (self.split and self.fwd_engine is not None and self.fwd_prec == L.PREC_3XF16
+        self.f16_dk = (self.fwd_engine is not None and self.fwd_prec == L.PREC_3XF16
                        and hop % 64 == 0 and hop <= k64 and os.environ.get("NNAB_F16_DK", "1") != "0")
 
     @staticmethod
@@ -190,7 +191,8 @@ class DftLayerOp:
 
     def _f16_operands(self, F, ld):
         """FP16 hi/lo coef [2F][ld] and the int32 row exponents [2F + 1] of the 3xF16 dK"""
-        c16 = tuple(torch.empty(2 * F, ld, dtype=torch.float16, device=self.device) for _ in range(2))
+        c16 = tuple(torch.empty(2 * F, ld, dtype=torch.float16, device=self.device) if i == 0 or self.split
+                    else None for i in range(2))
         return c16, torch.empty(2 * F + 1, dtype=torch.int32, device=self.device)
 
     # ------------------------------------------------------------ backward
@@ -230,8 +232,8 @@ class DftLayerOp:
                     c16, rexp = self._f16_operands(F, ld)
                     L.check(lib.nnab_mel_dft_coef_f16(
                         C.byref(f), saved["ws"].data_ptr(), saved["ws"].numel(), F, ld, kp, wt_hi.data_ptr(),
-                        wt_lo.data_ptr(), gsp[0].data_ptr(), gsp[1].data_ptr(), nm, saved["re"].data_ptr(),
-                        saved["im"].data_ptr(), self.eps, c16[0].data_ptr(), c16[1].data_ptr(), rexp.data_ptr(),
+                        L.ptr(wt_lo), gsp[0].data_ptr(), L.ptr(gsp[1]), nm, saved["re"].data_ptr(),
+                        L.ptr(saved["im"]), self.eps, c16[0].data_ptr(), L.ptr(c16[1]), rexp.data_ptr(),
                         stream), "mel_dft_coef_f16")
                 if need_x or not use16:
                     coef_hi = _f32(2 * F, ld, self.device)
@@ -255,8 +257,8 @@ class DftLayerOp:
         if use16 and ds is None:  # conv layer: coef from g directly
             c16, rexp = self._f16_operands(F, ld)
             L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), g.data_ptr(), saved["re"].data_ptr(),
-                                          saved["im"].data_ptr(), F, T, ld, self.eps, c16[0].data_ptr(),
-                                          c16[1].data_ptr(), rexp.data_ptr(), stream), "dft_coef_f16")
+                                          L.ptr(saved["im"]), F, T, ld, self.eps, c16[0].data_ptr(),
+                                          L.ptr(c16[1]), rexp.data_ptr(), stream), "dft_coef_f16")
         if need_bank and use16:
             dk = _f32(2 * F, n_fft, self.device)
             blocks = [(0, 2 * F)] if self.reducer is None or 2 * F <= 1280 else [(0, 1024), (1024, 2 * F)]
@@ -264,7 +266,8 @@ class DftLayerOp:
                 part = torch.empty(max(lib.nnab_rgemm_partial_bytes(r1 - r0, n_fft, ld, 0) // 4, 1),
                                    device=self.device)
                 L.check(lib.nnab_kernel_grad_f16(C.byref(f), c16[0].data_ptr() + 2 * r0 * ld,
-                                                 c16[1].data_ptr() + 2 * r0 * ld, r1 - r0, ld,
+                                                 None if c16[1] is None else c16[1].data_ptr() + 2 * r0 * ld,
+                                                 r1 - r0, ld,
                                                  rexp.data_ptr() + 4 * r0, dk.data_ptr() + 4 * r0 * n_fft, n_fft,
                                                  ws.data_ptr(), ws.numel(), part.data_ptr(), 0, stream),
                         "kernel_grad_f16")

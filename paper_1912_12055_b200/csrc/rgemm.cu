@@ -58,8 +58,8 @@ constexpr int kStg = 36;  // epilogue transpose row stride (floats)
 // stores / reduce-adds into C
 constexpr int kF16Stg = 4 * 2 * 4096;
 
-// kF16 (3xF16, CTA pairs only): FP16 hi/lo operands, 64 K per stage, a stage holds
-// A hi | A lo | this CTA's half of B hi | of B lo.
+// kF16 (CTA pairs only): FP16 operands, 64 K per stage; with kSplit (3xF16) a stage holds
+// A hi | A lo | this CTA's half of B hi | of B lo, without (one FP16 pass) A | B half.
 template <bool kSplit, bool kF16 = false>
 struct RCfg {
   static constexpr int BK = kF16 ? 64 : kSplit ? 16 : 32;
@@ -67,7 +67,9 @@ struct RCfg {
   static constexpr int SWZ = BK * EB;
   static constexpr int A_BYTES = kBM * BK * EB;
   static constexpr int B_BYTES = kBN * BK * EB;
-  static constexpr int STAGE = kF16 ? 2 * (A_BYTES + B_BYTES / 2) : (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);
+  static constexpr int STAGE = kF16 ? (kSplit ? 2 : 1) * (A_BYTES + B_BYTES / 2) : (A_BYTES + B_BYTES) * (kSplit ? 2 : 1);
+  // pipeline stages: 3 of 64 KB (3xF16), 6 of 32 KB (FP16) next to the drain staging
+  static constexpr int NST_F16 = kSplit ? 3 : 6;
   static constexpr int NUM_ACC = kSplit ? 1 : 2;
   static constexpr int ACC_STRIDE = kSplit ? 512 : 256;
 };
@@ -164,13 +166,13 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
                  const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                  const __grid_constant__ CUtensorMap tc, const RParams p) {
   using C = RCfg<kSplit, kF16>;
-  static_assert(!kF16 || (kSplit && kPair && !kWide && !kE8), "3xF16: split CTA-pair tiles");
+  static_assert(!kF16 || (kPair && !kWide && !kE8), "FP16 kernel gradient: CTA-pair tiles");
   static_assert(!kWide || (kPair && !kSplit), "wide tiles are a TF32 pair mode");
   constexpr int TBN = kWide ? 2 * kBN : kBN;     // tile columns
   constexpr int NACC = kWide ? 1 : C::NUM_ACC;   // TMEM accumulators
   constexpr int kBNc = kPair ? kBN / 2 : kBN;  // B columns this CTA stages per MMA
   constexpr int kHalves = kWide ? 2 : 1;       // N=256 MMAs per K step
-  constexpr int NST = (kE8 || kF16) ? 3 : kStages;  // pipeline stages
+  constexpr int NST = kF16 ? C::NST_F16 : kE8 ? 3 : kStages;  // pipeline stages
   constexpr int kEW = kE8 ? 8 : 4;              // epilogue warps
   static_assert(!kE8 || !kWide, "8-warp epilogue: coef GEMMs only");
   const uint32_t rank = kPair ? cluster_ctarank() : 0;
@@ -225,14 +227,15 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
           if constexpr (kF16) {
             const uint32_t fb = mapa(&full[s], 0);
             if (rank == 0) mbar_expect_tx(&full[s], 2 * C::STAGE);
+            constexpr int kAs = kSplit ? 2 : 1;  // A slabs before the B half
             tma_load_2d_pair(st, &ta_hi, fb, (int)k, mt * kBM, pol);
-            tma_load_2d_pair(st + C::A_BYTES, &ta_lo, fb, (int)k, mt * kBM, pol);
+            if (kSplit) tma_load_2d_pair(st + C::A_BYTES, &ta_lo, fb, (int)k, mt * kBM, pol);
             const int nb = nt * kBN + (int)rank * kBNc;
             int col = nb % p.b_row_len, row = (int)(k + nb / p.b_row_len);
 #pragma unroll
             for (int j = 0; j < kBNc / 64; ++j) {  // boxes of {64 n, 64 k}: 8 KB, one MN atom column
-              tma_load_2d_pair(st + 2 * C::A_BYTES + j * 8192, &tb_hi, fb, col, row, pol);
-              tma_load_2d_pair(st + 2 * C::A_BYTES + C::B_BYTES / 2 + j * 8192, &tb_lo, fb, col, row, pol);
+              tma_load_2d_pair(st + kAs * C::A_BYTES + j * 8192, &tb_hi, fb, col, row, pol);
+              if (kSplit) tma_load_2d_pair(st + kAs * C::A_BYTES + C::B_BYTES / 2 + j * 8192, &tb_lo, fb, col, row, pol);
               if ((col += 64) == p.b_row_len) col = 0, ++row;  // b_row_len % 64 == 0
             }
             if (++s == NST) { s = 0; ph ^= 1; }
@@ -309,16 +312,18 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
             uint8_t* st = smem + s * C::STAGE;
             if constexpr (kF16) {
               constexpr uint32_t idf = idesc_f16(2 * kBM, kBN) | (1u << 16);  // B MN-major
-              const uint32_t sa = smem_u32(st), sb = sa + 2 * C::A_BYTES;
+              const uint32_t sa = smem_u32(st), sb = sa + (kSplit ? 2 : 1) * C::A_BYTES;
 #pragma unroll
               for (int kk = 0; kk < C::BK / 16; ++kk) {
                 const uint64_t a = sdesc_kmajor_sw128_addr(sa + kk * 32);
-                const uint64_t a_lo = sdesc_kmajor_sw128_addr(sa + C::A_BYTES + kk * 32);
                 const uint64_t b = mndesc_f16(sb + kk * 2048, 8192);  // 16 K rows = two 8-row atoms
-                const uint64_t b_lo = mndesc_f16(sb + C::B_BYTES / 2 + kk * 2048, 8192);
                 mma_f16_pair(d, a, b, idf, first ? 0u : 1u);
-                mma_f16_pair(d + kBN, a, b_lo, idf, first ? 0u : 1u);
-                mma_f16_pair(d + kBN, a_lo, b, idf, 1u);
+                if (kSplit) {
+                  const uint64_t a_lo = sdesc_kmajor_sw128_addr(sa + C::A_BYTES + kk * 32);
+                  const uint64_t b_lo = mndesc_f16(sb + C::B_BYTES / 2 + kk * 2048, 8192);
+                  mma_f16_pair(d + kBN, a, b_lo, idf, first ? 0u : 1u);
+                  mma_f16_pair(d + kBN, a_lo, b, idf, 1u);
+                }
                 first = false;
               }
               mma_commit_pair(&empty[s], 0x3);
@@ -379,6 +384,7 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
       uint8_t* stg16 = smem + NST * C::STAGE + ew * 8192;
       const uint32_t tempty0 = mapa(&tempty[0], 0);
       uint32_t aph = 0;
+      int acc = 0;  // TMEM accumulator (one pass: double-buffered; 3xF16: main + correction)
       for (int w = w_start; w < n_work; w += w_step) {
         const int sp = w % p.splits, tile = w / p.splits;
         const int mt = (tile / p.n_tiles) * 2 + (int)rank, nt = tile % p.n_tiles;
@@ -390,20 +396,25 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
         const float rs = m < p.M ? __int_as_float((127 - p.row_exp[m]) << 23) : 0.f;
         for (int64_t kc = k_lo; kc < k_hi; kc += p.k_chunk) {
           const bool first_chunk = kc == k_lo;
-          mbar_wait(&tfull[0], aph);
+          mbar_wait(&tfull[acc], aph);
           tc_fence_after();
-          const uint32_t tb = tbase + ((q * 32) << 16);
+          const uint32_t tb = tbase + ((q * 32) << 16) + (NACC > 1 ? acc * C::ACC_STRIDE : 0);
           if (lane == 0) bulk_wait_all();  // the previous chunk's stores / adds have landed
           __syncwarp();
 #pragma unroll 1
           for (int c = 0; c < kBN / 32; ++c) {
             float v[32], u[32];
             tmem_ld32(tb + c * 32, v);
-            tmem_ld32(tb + kBN + c * 32, u);
+            if (kSplit) {
+              tmem_ld32(tb + kBN + c * 32, u);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) u[j] = 0.f;
+            }
             tmem_ld_wait();
             if (c == kBN / 32 - 1) {  // accumulators read: the next chunk's MMAs may start
               tc_fence_before();
-              mbar_arrive_cluster(tempty0);
+              mbar_arrive_cluster(tempty0 + 8 * acc);
             }
             uint8_t* buf = stg16 + (c & 1) * 4096;
             if (c >= 2) {
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
               bulk_commit();
             }
           }
-          aph ^= 1;
+          if (++acc == NACC) { acc = 0; aph ^= 1; }
         }
       }
       if (lane == 0) bulk_wait_all();
@@ -503,11 +514,49 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
               ph[it] = ph_cur[it];
               ph_cur[it] = ph_nxt[it];
             }
+            float es[4] = {0.f, 0.f, 0.f, 0.f};  // coef_f16: 2^-clip_exp per column
+            if (p.coef_f16) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int64_t b = (int64_t)(n + j) / p.clip_R;
+                es[j] = b < p.n_clips ? __int_as_float((127 - p.clip_exp[b]) << 23) : 0.f;
+              }
+            }
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
               const int m = m_base + it * 4 + sr;
               if (m >= p.M) continue;
               const int64_t o = (int64_t)m * p.ldc + n, o2 = o + (int64_t)p.M * p.ldc;
+              if (p.coef_f16) {  // one-pass FP16 kernel-gradient operand: coef * 2^(row_exp - clip_exp)
+                const float rs = __int_as_float((127 + p.row_exp[m]) << 23);
+                const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
+                __half* ch = reinterpret_cast<__half*>(p.C);
+                float cr[4], ci[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  float2 f = make_float2(0.f, 0.f);
+                  if (full4) f = __half22float2(reinterpret_cast<const __half2*>(&ph[it])[j]);
+                  else if (n + j < p.N) f = __half22float2(reinterpret_cast<const __half2*>(p.re)[o + j]);
+                  cr[j] = dv[j] * f.x * es[j] * rs;
+                  ci[j] = dv[j] * f.y * es[j] * rs;
+                }
+                const __half2 r01 = __floats2half2_rn(cr[0], cr[1]), r23 = __floats2half2_rn(cr[2], cr[3]);
+                const __half2 i01 = __floats2half2_rn(ci[0], ci[1]), i23 = __floats2half2_rn(ci[2], ci[3]);
+                if (full4) {
+                  __stcs(reinterpret_cast<uint2*>(ch + o), make_uint2(*reinterpret_cast<const uint32_t*>(&r01),
+                                                                      *reinterpret_cast<const uint32_t*>(&r23)));
+                  __stcs(reinterpret_cast<uint2*>(ch + o2), make_uint2(*reinterpret_cast<const uint32_t*>(&i01),
+                                                                       *reinterpret_cast<const uint32_t*>(&i23)));
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j)
+                    if (n + j < p.N) {
+                      ch[o + j] = __float2half_rn(cr[j]);
+                      ch[o2 + j] = __float2half_rn(ci[j]);
+                    }
+                }
+                continue;
+              }
               if (full4) {
                 const __half2* h2 = reinterpret_cast<const __half2*>(&ph[it]);
                 const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]), f2 = __half22float2(h2[2]),
@@ -714,11 +763,13 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   int rc = NNAB_OK;
   if (kF16) {  // K need not be a multiple of BK: the tail boxes are zero-filled past K and b_rows
-    if (g.lda % 8 || !g.b_mn || g.b_row_len % 64 || !g.a_lo || !g.b_lo || !g.row_exp) return NNAB_EINVAL;
+    if (g.lda % 8 || !g.b_mn || g.b_row_len % 64 || (kSplit && (!g.a_lo || !g.b_lo)) || !g.row_exp)
+      return NNAB_EINVAL;
     rc = make_tmap_2d(&ta_hi, g.a_hi, g.K, g.M, (uint64_t)g.lda * 2, 64, kBM, 128, 2);
-    if (!rc) rc = make_tmap_2d(&ta_lo, g.a_lo, g.K, g.M, (uint64_t)g.lda * 2, 64, kBM, 128, 2);
+    if (!rc && kSplit) rc = make_tmap_2d(&ta_lo, g.a_lo, g.K, g.M, (uint64_t)g.lda * 2, 64, kBM, 128, 2);
     if (!rc) rc = make_tmap_2d(&tb_hi, g.b_hi, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 2, 64, 64, 128, 2);
-    if (!rc) rc = make_tmap_2d(&tb_lo, g.b_lo, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 2, 64, 64, 128, 2);
+    if (!rc && kSplit)
+      rc = make_tmap_2d(&tb_lo, g.b_lo, g.b_row_len, g.b_rows, (uint64_t)g.b_row_len * 2, 64, 64, 128, 2);
   } else if (g.K % C::BK || g.lda % 4 || (g.b_mn && g.b_row_len % 32) || (!g.b_mn && g.ldb % 4)) {
     return NNAB_EINVAL;
   } else {
@@ -752,7 +803,8 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   splits = (int)std::min<int64_t>(splits, kb);
   p.k_per_split = (kb + splits - 1) / splits * C::BK;
   p.splits = (int)((g.K + p.k_per_split - 1) / p.k_per_split);
-  p.k_chunk = (kF16 ? f16_chunk() : kSplit ? 1024 : kWide ? 8192 : 2048);  // accumulate steps per TMEM
+  // one FP16 pass: its 11-bit operands dwarf the accumulate steps' error, so long chains (as wide TF32)
+  p.k_chunk = (kF16 ? (kSplit ? f16_chunk() : 8192) : kSplit ? 1024 : kWide ? 8192 : 2048);  // accumulate steps per TMEM
                                                     // chain (wide: no second accumulator, so drain less often)
   // the epilogues that write final values (frames output, coef) need one TMEM chain per tile:
   // up to 2,048 K in every mode (a 3xTF32 Mel forward over 1,025 bins has K = 1,056)
@@ -771,7 +823,9 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
   p.n_clips = g.n_clips;
   p.clip_R = g.clip_R;
   p.coef_f16 = g.coef_f16;
-  if (p.coef_f16 && (!kSplit || kF16 || !p.re || !p.im || !p.row_exp || !p.clip_exp || p.clip_R < 1 || g.ldc % 4))
+  // coef_f16: 3xTF32 from re / im (FP16 hi + lo out) or TF32 from the FP16 unit phasor (hi only)
+  if (p.coef_f16 && (kF16 || !p.re || (kSplit && (!p.im || !p.c_lo)) || !p.row_exp || !p.clip_exp || p.clip_R < 1 ||
+                     g.ldc % 4))
     return NNAB_EINVAL;
   if (p.fR && (p.fR % 4 || p.splits != 1 || kb > p.k_chunk / C::BK || g.alpha != 1.f || p.re)) return NNAB_EINVAL;
   if (p.re && (p.splits != 1 || kb > p.k_chunk / C::BK || g.alpha != 1.f)) return NNAB_EINVAL;  // one TMEM chain
@@ -790,7 +844,7 @@ int launch(const RGemmArgs& g, cudaStream_t st) {
     }
     if (rc) return rc;
   }
-  const size_t smem = 1024 + ((kE8 || kF16) ? 3 : kStages) * C::STAGE + 128 +
+  const size_t smem = 1024 + (kF16 ? C::NST_F16 : kE8 ? 3 : kStages) * C::STAGE + 128 +
                       (kF16 ? kF16Stg : (kE8 ? 8 : 4) * 32 * kStg * 4);
   constexpr int threads = kE8 ? 384 : kThreads;
   auto k = rgemm_kernel<kSplit, kPair, kWide, kE8, kF16>;
@@ -860,6 +914,7 @@ int launch_rgemm(const RGemmArgs& g, int precision, cudaStream_t s) {
     return pair ? launch<true, true>(g, s) : launch<true, false>(g, s);
   }
   if (precision == NNAB_PREC_3XF16) return launch<true, true, false, false, true>(g, s);
+  if (precision == NNAB_PREC_F16) return launch<false, true, false, false, true>(g, s);
   if (precision == NNAB_PREC_TF32) {
     const bool pair = pair_ok && (pair_env >= 2 || g.M > kBM);  // one m tile: the peer would idle
     const bool wide = pair && !g.coef_re && (pair_env == 3 || (pair_env == 1 && g.N > kBN && g.K >= 65536));

@@ -227,17 +227,25 @@ __global__ void coef_f16_kernel(const float* __restrict__ g_bft, const float* __
     float cr = 0.f, ci = 0.f;
     if (b < B && t < T) {
       const float d = g_bft[(b * F + f) * (int64_t)T + t];
-      const float r = re[e], i = im[e];
-      const float di = d * rsqrtf(fmaf(r, r, i * i) + eps);
       const float sc = __int_as_float((127 - exps[b]) << 23) * __int_as_float((127 + row_exp[f]) << 23);
-      cr = di * r * sc;
-      ci = di * i * sc;
+      if (im) {
+        const float r = re[e], i = im[e];
+        const float di = d * rsqrtf(fmaf(r, r, i * i) + eps);
+        cr = di * r * sc;
+        ci = di * i * sc;
+      } else {  // the FP16 unit phasor (re/S, im/S) of a TF32-backward forward
+        const float2 ph = __half22float2(reinterpret_cast<const __half2*>(re)[e]);
+        cr = d * ph.x * sc;
+        ci = d * ph.y * sc;
+      }
     }
     const __half hr = __float2half_rn(cr), hi_ = __float2half_rn(ci);
     hi[e] = hr;
     hi[e + (int64_t)F * ld] = hi_;
-    lo[e] = __float2half_rn(cr - __half2float(hr));
-    lo[e + (int64_t)F * ld] = __float2half_rn(ci - __half2float(hi_));
+    if (lo) {
+      lo[e] = __float2half_rn(cr - __half2float(hr));
+      lo[e + (int64_t)F * ld] = __float2half_rn(ci - __half2float(hi_));
+    }
   }
 }
 
@@ -532,8 +540,11 @@ extern "C" int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, siz
   const int32_t* exps;
   int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
   if (rc) return rc;
-  if (F < 1 || ld < g.B * g.R || ld % 8 || kp < n_mels || n_mels < 1 || !wt_hi || !wt_lo || !gs_hi || !gs_lo ||
-      !re_s || !im_s || !coef_hi || !coef_lo || !row_exps)
+  // coef_lo given: 3xTF32 coef GEMM from re / im, FP16 hi + lo out (the 3xF16 dK); coef_lo null: TF32
+  // coef GEMM from the FP16 unit phasor (im_s null), FP16 hi out (the one-pass FP16 dK)
+  const bool split = coef_lo != nullptr;
+  if (F < 1 || ld < g.B * g.R || ld % 8 || kp < n_mels || n_mels < 1 || !wt_hi || !gs_hi || !re_s || !coef_hi ||
+      !row_exps || (split && (!wt_lo || !gs_lo || !im_s)) || (!split && im_s))
     return NNAB_EINVAL;
   if (ld > INT32_MAX) return NNAB_EINVAL;
   if (kp > 1024) return NNAB_ENOTSUP;
@@ -572,7 +583,7 @@ extern "C" int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, siz
   a.clip_exp = exps;
   a.n_clips = g.B;
   a.clip_R = g.R;
-  return launch_rgemm(a, NNAB_PREC_3XTF32, s);
+  return launch_rgemm(a, split ? NNAB_PREC_3XTF32 : NNAB_PREC_TF32, s);
 }
 
 extern "C" int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, const float* g_bft,
@@ -583,7 +594,8 @@ extern "C" int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t 
   const int32_t* exps;
   int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
   if (rc) return rc;
-  if (!g_bft || !re_s || !im_s || !coef_hi || !coef_lo || !row_exps || F < 1 || T < 1 || T > g.R ||
+  // coef_lo given: re / im in, FP16 hi + lo out; null: FP16 hi out, re_s may hold the FP16 unit phasor (im_s null)
+  if (!g_bft || !re_s || (coef_lo && !im_s) || !coef_hi || !row_exps || F < 1 || T < 1 || T > g.R ||
       ld < g.B * g.R || ld % 8)
     return NNAB_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
@@ -613,7 +625,7 @@ extern "C" int nnab_kernel_grad_f16(const nnab_frames* f, const void* coef_hi, c
   const int32_t* exps;
   int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
   if (rc) return rc;
-  if (!coef_hi || !coef_lo || !row_exps || !dk || rows < 1 || ld < g.B * g.R || ld % 8) return NNAB_EINVAL;
+  if (!coef_hi || !row_exps || !dk || rows < 1 || ld < g.B * g.R || ld % 8) return NNAB_EINVAL;
   if (g.row_len != g.hop || g.hop % 64) return NNAB_ENOTSUP;  // MN-major 64-column boxes of hop rows
   if (g.B == 0) return NNAB_OK;
   RGemmArgs a;
@@ -621,10 +633,10 @@ extern "C" int nnab_kernel_grad_f16(const nnab_frames* f, const void* coef_hi, c
   a.N = g.width;
   a.K = ld;
   a.a_hi = reinterpret_cast<const float*>(coef_hi);
-  a.a_lo = reinterpret_cast<const float*>(coef_lo);
+  a.a_lo = reinterpret_cast<const float*>(coef_lo);  // null: one FP16 pass (coef and frames hi only)
   a.lda = ld;
   a.b_hi = reinterpret_cast<const float*>(hi);
-  a.b_lo = reinterpret_cast<const float*>(lo);
+  a.b_lo = coef_lo ? reinterpret_cast<const float*>(lo) : nullptr;
   a.b_mn = 1;
   a.b_row_len = g.row_len;
   a.b_rows = g.B * g.R;
@@ -633,5 +645,5 @@ extern "C" int nnab_kernel_grad_f16(const nnab_frames* f, const void* coef_hi, c
   a.splits = splits;
   a.partial = partial;
   a.row_exp = row_exps;
-  return launch_rgemm(a, NNAB_PREC_3XF16, (cudaStream_t)stream);
+  return launch_rgemm(a, coef_lo ? NNAB_PREC_3XF16 : NNAB_PREC_F16, (cudaStream_t)stream);
 }

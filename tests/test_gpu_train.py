@@ -350,17 +350,19 @@ def test_trainable_cqt1992v2_full_config(cuda_dev, precision):
     assert O.peak_err(m.k_im.grad.cpu().numpy(), dim) <= TOL_GRAD_JOINT[precision]
 
 
+@pytest.mark.parametrize("split", [True, False])
 @pytest.mark.parametrize("n_fft,hop,F,B,spread", [
     (2048, 512, 1025, 72, True),   # config 5 shape: 144 pair tiles, one split, C written directly
     (1024, 256, 84, 40, False),    # 168 rows: 1 pair row x 4 column tiles -> split-K partials + fixed-order sum
     (1000, 256, 33, 24, True),     # N = 1000: TMA clips the last column tile
     (1002, 256, 40, 24, False),    # ldk = 1002 (row stride not 16-byte aligned): the partial-buffer path
 ])
-def test_kernel_grad_f16_vs_float64(cuda_dev, n_fft, hop, F, B, spread):
-    """FP32 mode's 3xF16 kernel gradient (nnab_dft_coef_f16 + nnab_kernel_grad_f16, gradients.py:125-129)
-    against float64: dK = (g re/S, g im/S) @ frames summed over the batch, with per-clip loudness spread
-    over 1e-3..1e3 and upstream grads of 1e-9 (the power-of-two clip / row scales), K = B x T frame slots
-    over several TMEM drain chunks (the first stores, later ones TMA reduce-add).  Gate 1e-5."""
+def test_kernel_grad_f16_vs_float64(cuda_dev, n_fft, hop, F, B, spread, split):
+    """The FP16 kernel gradient (nnab_dft_coef_f16 + nnab_kernel_grad_f16, gradients.py:125-129) against
+    float64: dK = (g re/S, g im/S) @ frames summed over the batch, with per-clip loudness spread over
+    1e-3..1e3 and upstream grads of 1e-9 (the power-of-two clip / row scales), K = B x T frame slots over
+    several TMEM drain chunks (the first stores, later ones TMA reduce-add).  split: 3xF16 (FP32 mode,
+    gate 1e-5); else one FP16 pass (TF32 mode's 11-bit operands, gate 1e-3)."""
     import ctypes as C
     import torch.nn.functional as Fn
     from paper_1912_12055_b200 import _lib as L
@@ -384,13 +386,13 @@ def test_kernel_grad_f16_vs_float64(cuda_dev, n_fft, hop, F, B, spread):
     g = torch.randn(B, F, T, device=cuda_dev, generator=gen) * gscale
     re = torch.randn(F, ld, device=cuda_dev, generator=gen)
     im = torch.randn(F, ld, device=cuda_dev, generator=gen)
-    c16 = [torch.empty(2 * F, ld, dtype=torch.float16, device=cuda_dev) for _ in range(2)]
+    c16 = [torch.empty(2 * F, ld, dtype=torch.float16, device=cuda_dev) if i == 0 or split else None for i in range(2)]
     rexp = torch.empty(2 * F + 1, dtype=torch.int32, device=cuda_dev)
     L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), g.data_ptr(), re.data_ptr(), im.data_ptr(),
-                                  F, T, ld, 0.0, c16[0].data_ptr(), c16[1].data_ptr(), rexp.data_ptr(), st), "coef")
+                                  F, T, ld, 0.0, c16[0].data_ptr(), L.ptr(c16[1]), rexp.data_ptr(), st), "coef")
     dk = torch.full((2 * F, n_fft), float("nan"), device=cuda_dev)
     part = torch.empty(max(lib.nnab_rgemm_partial_bytes(2 * F, n_fft, ld, 0) // 4, 1), device=cuda_dev)
-    L.check(lib.nnab_kernel_grad_f16(C.byref(f), c16[0].data_ptr(), c16[1].data_ptr(), 2 * F, ld, rexp.data_ptr(),
+    L.check(lib.nnab_kernel_grad_f16(C.byref(f), c16[0].data_ptr(), L.ptr(c16[1]), 2 * F, ld, rexp.data_ptr(),
                                      dk.data_ptr(), n_fft, ws.data_ptr(), ws.numel(), part.data_ptr(), 0, st), "dk")
     torch.cuda.synchronize()
     from paper_1912_12055_b200.engine import geometry
@@ -404,7 +406,7 @@ def test_kernel_grad_f16_vs_float64(cuda_dev, n_fft, hop, F, B, spread):
     ref = torch.cat([(g64 * re64 / S) @ fr, (g64 * im64 / S) @ fr])
     assert torch.isfinite(dk).all()
     err = float((dk.double() - ref).abs().max() / ref.abs().max())
-    assert err <= 1e-5, err
+    assert err <= (1e-5 if split else 1e-3), err
 
 
 @pytest.mark.parametrize("precision", ["tf32", "fp32"])
