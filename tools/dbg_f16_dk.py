@@ -1,5 +1,6 @@
-"""FP32-mode kernel-gradient error: 3xF16 dK (default) vs the 3xTF32 dK (NNAB_F16_DK=0).
-    python tools/dbg_f16_dk.py [B]
+"""Kernel-gradient error: the FP16 dK (default; 3xF16 in FP32 mode, one FP16 pass in TF32 mode) vs
+the 3xTF32 / TF32 dK (NNAB_F16_DK=0).
+    python tools/dbg_f16_dk.py [B] [precision: fp32|tf32]
 Cases: the joint mel + STFT layer on N(0, 0.25) clips; the same with per-clip loudness
 spread over 1e-3..1e3 and upstream grads scaled by 1e-9 (the scale logic's stress case)."""
 import os, sys
@@ -9,6 +10,7 @@ from oracle import spectro_oracle as O
 from paper_1912_12055_b200.layers import MelSpectrogram
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+PREC = sys.argv[2] if len(sys.argv) > 2 else "fp32"
 h_re, h_im = O.stft_bank()
 W = O.mel_bank(44100.0, 2048, 128, formula="slaney")
 for case in ["plain", "stress"]:
@@ -21,7 +23,7 @@ for case in ["plain", "stress"]:
     ref = None
     for f16 in ["1", "0"]:
         os.environ["NNAB_F16_DK"] = f16
-        m = MelSpectrogram(sr=44100, trainable_mel=True, trainable_STFT=True, precision="fp32")
+        m = MelSpectrogram(sr=44100, trainable_mel=True, trainable_STFT=True, precision=PREC)
         assert m._op.f16_dk == (f16 == "1")
         out = m(torch.from_numpy(x).cuda())
         g = (np.random.default_rng(7).standard_normal(out.shape) * gs).astype(np.float32)
@@ -35,4 +37,4 @@ for case in ["plain", "stress"]:
             ref = (dh_re, dh_im)
         e_re = O.peak_err(m.h_re.grad.cpu().numpy(), ref[0])
         e_im = O.peak_err(m.h_im.grad.cpu().numpy(), ref[1])
-        print(f"{case:6s} B={B} f16_dk={f16}: dh_re {e_re:.2e} dh_im {e_im:.2e}", flush=True)
+        print(f"{PREC} {case:6s} B={B} f16_dk={f16}: dh_re {e_re:.2e} dh_im {e_im:.2e}", flush=True)
