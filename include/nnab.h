@@ -251,7 +251,8 @@ int nnab_kernel_grad(const nnab_frames* f, const float* coef_hi, const float* co
 /* FP32-mode (<= 1e-5) kernel gradient on FP16 tensor cores (3xF16): the coef
  * operand is written as FP16 hi/lo of coef * 2^(row_exps[m] - e_b) (e_b: clip b's
  * staging exponent), the frames are the 3xF16 training forward's staged rows
- * (ws16: its nnab_stage_frames workspace, NNAB_PREC_3XF16; hop % 64 == 0), and
+ * (ws16: its nnab_stage_frames workspace, staged in `staging` = NNAB_PREC_3XF16, or
+ * NNAB_PREC_F16 for the one-pass form; hop % 64 == 0), and
  * the GEMM's epilogue multiplies row m by 2^-row_exps[m].  row_exps: int32[2F + 1]
  * (the last word is scratch).  coef_hi/coef_lo: FP16 [2F][ld]; ld % 8 == 0.
  * Replaces nnab_dft_coef / nnab_mel_dft_coef + nnab_kernel_grad in NNAB_PREC_3XTF32
@@ -259,16 +260,16 @@ int nnab_kernel_grad(const nnab_frames* f, const float* coef_hi, const float* co
  * coef_lo = NULL: one FP16 pass (11-bit operands, the TF32 mode's accuracy): coef hi only,
  * the frames' hi rows only; the coef inputs may then be TF32 (wt_lo / gs_lo NULL) and
  * re_s the FP16 unit phasor of a TF32-backward forward (im_s NULL). */
-int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t F, int64_t ld,
+int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t staging, int32_t F, int64_t ld,
                           int32_t kp, const float* wt_hi, const float* wt_lo, const float* gs_hi, const float* gs_lo,
                           int32_t n_mels, const float* re_s, const float* im_s, float eps, void* coef_hi,
                           void* coef_lo, int32_t* row_exps, void* stream);
-int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, const float* g_bft,
+int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t staging, const float* g_bft,
                       const float* re_s, const float* im_s, int32_t F, int32_t T, int64_t ld, float eps,
                       void* coef_hi, void* coef_lo, int32_t* row_exps, void* stream);
 int nnab_kernel_grad_f16(const nnab_frames* f, const void* coef_hi, const void* coef_lo, int32_t rows, int64_t ld,
                          const int32_t* row_exps, float* dk, int64_t ldk, const void* ws16, size_t ws16_bytes,
-                         float* partial, int32_t splits, void* stream);
+                         int32_t staging, float* partial, int32_t splits, void* stream);
 /* dx: overlap-add of frame grads ([tap][ld] = h^T @ coef) folded through the
  * pad index map (gradients.py:133-149); deterministic gather, (B, L) out. */
 int nnab_input_grad(const nnab_frames* f, const float* frame_grads_t, int64_t ld, float* gx, void* stream);

@@ -78,10 +78,10 @@ SIGNATURES = {
                              _fp, _i32, _vp]),
     "nnab_kernel_grad": (C.c_int, [_FR, _fp, _fp, _i32, _i64, _i32, _fp, _i64, _vp, _sz, _fp, _i32, _vp]),
     "nnab_input_grad": (C.c_int, [_FR, _fp, _i64, _fp, _vp]),
-    "nnab_mel_dft_coef_f16": (C.c_int, [_FR, _vp, _sz, _i32, _i64, _i32, _fp, _fp, _fp, _fp, _i32, _fp, _fp, _f32, _vp,
-                                        _vp, _ip, _vp]),
-    "nnab_dft_coef_f16": (C.c_int, [_FR, _vp, _sz, _fp, _fp, _fp, _i32, _i32, _i64, _f32, _vp, _vp, _ip, _vp]),
-    "nnab_kernel_grad_f16": (C.c_int, [_FR, _vp, _vp, _i32, _i64, _ip, _fp, _i64, _vp, _sz, _fp, _i32, _vp]),
+    "nnab_mel_dft_coef_f16": (C.c_int, [_FR, _vp, _sz, _i32, _i32, _i64, _i32, _fp, _fp, _fp, _fp, _i32, _fp, _fp, _f32,
+                                        _vp, _vp, _ip, _vp]),
+    "nnab_dft_coef_f16": (C.c_int, [_FR, _vp, _sz, _i32, _fp, _fp, _fp, _i32, _i32, _i64, _f32, _vp, _vp, _ip, _vp]),
+    "nnab_kernel_grad_f16": (C.c_int, [_FR, _vp, _vp, _i32, _i64, _ip, _fp, _i64, _vp, _sz, _i32, _fp, _i32, _vp]),
     "nnab_cqt_bank_tiles": (C.c_int, [_i32]),
     "nnab_cqt_bank_bytes": (_sz, [_i32, _i32]),
     "nnab_cqt_bank_bytes_prec": (_sz, [_i32, _i32, _i32]),

@@ -66,11 +66,18 @@ class DftLayerOp:
             if self.fwd_prec == L.PREC_3XTF32:
                 self.fwd_engine.precision = L.PREC_3XTF32
                 self.fwd_engine.set_bank(h_re, h_im)
+        elif (self.prec == L.PREC_TF32 and same_rows and eng.hop % 64 == 0
+              and os.environ.get("NNAB_F16_DK", "1") != "0"):
+            # phasor="tf32" (one-pass forward): FP16 operands keep TF32's 11 bits at twice the rate,
+            # and their staging feeds the one-pass FP16 kernel gradient
+            self.fwd_prec = L.PREC_F16
+            self.fwd_engine = DftEngine(h_re, h_im, hop, center, pad_mode, precision="f16", device=device,
+                                        allow_fold="exact")
         # the kernel gradient runs on FP16 tensor cores over the 3xF16 forward's staging
         # (nnab_kernel_grad_f16) where that staging holds hop rows of 64-sample multiples:
         # 3xF16 in FP32 mode, one FP16 pass (11-bit operands, as TF32) in TF32 mode
         hop, k64 = eng.hop, (eng.n_fft + 63) // 64 * 64
-        self.f16_dk = (self.fwd_engine is not None and self.fwd_prec == L.PREC_3XF16
+        self.f16_dk = (self.fwd_engine is not None and self.fwd_prec in (L.PREC_3XF16, L.PREC_F16)
                        and hop % 64 == 0 and hop <= k64 and os.environ.get("NNAB_F16_DK", "1") != "0")
 
     @staticmethod
@@ -231,7 +238,8 @@ class DftLayerOp:
                 if use16:  # the 3xF16 dK operand
                     c16, rexp = self._f16_operands(F, ld)
                     L.check(lib.nnab_mel_dft_coef_f16(
-                        C.byref(f), saved["ws"].data_ptr(), saved["ws"].numel(), F, ld, kp, wt_hi.data_ptr(),
+                        C.byref(f), saved["ws"].data_ptr(), saved["ws"].numel(), self.fwd_prec, F, ld, kp,
+                        wt_hi.data_ptr(),
                         L.ptr(wt_lo), gsp[0].data_ptr(), L.ptr(gsp[1]), nm, saved["re"].data_ptr(),
                         L.ptr(saved["im"]), self.eps, c16[0].data_ptr(), L.ptr(c16[1]), rexp.data_ptr(),
                         stream), "mel_dft_coef_f16")
@@ -256,7 +264,8 @@ class DftLayerOp:
         ws = saved["ws"]
         if use16 and ds is None:  # conv layer: coef from g directly
             c16, rexp = self._f16_operands(F, ld)
-            L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), g.data_ptr(), saved["re"].data_ptr(),
+            L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), self.fwd_prec, g.data_ptr(),
+                                          saved["re"].data_ptr(),
                                           L.ptr(saved["im"]), F, T, ld, self.eps, c16[0].data_ptr(),
                                           L.ptr(c16[1]), rexp.data_ptr(), stream), "dft_coef_f16")
         if need_bank and use16:
@@ -269,7 +278,8 @@ class DftLayerOp:
                                                  None if c16[1] is None else c16[1].data_ptr() + 2 * r0 * ld,
                                                  r1 - r0, ld,
                                                  rexp.data_ptr() + 4 * r0, dk.data_ptr() + 4 * r0 * n_fft, n_fft,
-                                                 ws.data_ptr(), ws.numel(), part.data_ptr(), 0, stream),
+                                                 ws.data_ptr(), ws.numel(), self.fwd_prec, part.data_ptr(), 0,
+                                                 stream),
                         "kernel_grad_f16")
                 if self.reducer is not None:
                     self.reducer.launch(dk[r0:r1])

@@ -523,22 +523,25 @@ extern "C" int nnab_input_grad(const nnab_frames* f, const float* frame_grads, i
 
 // ---- 3xF16 kernel gradient (FP32 mode) ----------------------------
 
-static int f16_views(const nnab_frames* f, const void* ws16, size_t ws16_bytes, FrameGeom* g, const void** hi,
-                     const void** lo, const int32_t** exps) {
-  int rc = staged_views(f, NNAB_PREC_3XF16, ws16, ws16_bytes, g, hi, lo, exps);
+// staging: the precision ws16 was staged in -- NNAB_PREC_3XF16 (hi + lo rows) or NNAB_PREC_F16 (hi)
+static int f16_views(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t staging, FrameGeom* g,
+                     const void** hi, const void** lo, const int32_t** exps) {
+  if (staging != NNAB_PREC_3XF16 && staging != NNAB_PREC_F16) return NNAB_EINVAL;
+  int rc = staged_views(f, staging, ws16, ws16_bytes, g, hi, lo, exps);
   if (rc) return rc;
-  if (g->B > 0 && (!*exps || !*lo)) return NNAB_EINVAL;
+  if (g->B > 0 && (!*exps || (staging == NNAB_PREC_3XF16 && !*lo))) return NNAB_EINVAL;
   return NNAB_OK;
 }
 
-extern "C" int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t F, int64_t ld,
+extern "C" int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t staging,
+                                     int32_t F, int64_t ld,
                                      int32_t kp, const float* wt_hi, const float* wt_lo, const float* gs_hi,
                                      const float* gs_lo, int32_t n_mels, const float* re_s, const float* im_s,
                                      float eps, void* coef_hi, void* coef_lo, int32_t* row_exps, void* stream) {
   FrameGeom g;
   const void *hi, *lo;
   const int32_t* exps;
-  int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
+  int rc = f16_views(f, ws16, ws16_bytes, staging, &g, &hi, &lo, &exps);
   if (rc) return rc;
   // coef_lo given: 3xTF32 coef GEMM from re / im, FP16 hi + lo out (the 3xF16 dK); coef_lo null: TF32
   // coef GEMM from the FP16 unit phasor (im_s null), FP16 hi out (the one-pass FP16 dK)
@@ -586,13 +589,14 @@ extern "C" int nnab_mel_dft_coef_f16(const nnab_frames* f, const void* ws16, siz
   return launch_rgemm(a, split ? NNAB_PREC_3XTF32 : NNAB_PREC_TF32, s);
 }
 
-extern "C" int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, const float* g_bft,
+extern "C" int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t ws16_bytes, int32_t staging,
+                                 const float* g_bft,
                                  const float* re_s, const float* im_s, int32_t F, int32_t T, int64_t ld, float eps,
                                  void* coef_hi, void* coef_lo, int32_t* row_exps, void* stream) {
   FrameGeom g;
   const void *hi, *lo;
   const int32_t* exps;
-  int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
+  int rc = f16_views(f, ws16, ws16_bytes, staging, &g, &hi, &lo, &exps);
   if (rc) return rc;
   // coef_lo given: re / im in, FP16 hi + lo out; null: FP16 hi out, re_s may hold the FP16 unit phasor (im_s null)
   if (!g_bft || !re_s || (coef_lo && !im_s) || !coef_hi || !row_exps || F < 1 || T < 1 || T > g.R ||
@@ -619,13 +623,14 @@ extern "C" int nnab_dft_coef_f16(const nnab_frames* f, const void* ws16, size_t 
 
 extern "C" int nnab_kernel_grad_f16(const nnab_frames* f, const void* coef_hi, const void* coef_lo, int32_t rows,
                                     int64_t ld, const int32_t* row_exps, float* dk, int64_t ldk, const void* ws16,
-                                    size_t ws16_bytes, float* partial, int32_t splits, void* stream) {
+                                    size_t ws16_bytes, int32_t staging, float* partial, int32_t splits, void* stream) {
   FrameGeom g;
   const void *hi, *lo;
   const int32_t* exps;
-  int rc = f16_views(f, ws16, ws16_bytes, &g, &hi, &lo, &exps);
+  int rc = f16_views(f, ws16, ws16_bytes, staging, &g, &hi, &lo, &exps);
   if (rc) return rc;
   if (!coef_hi || !row_exps || !dk || rows < 1 || ld < g.B * g.R || ld % 8) return NNAB_EINVAL;
+  if (coef_lo && staging != NNAB_PREC_3XF16) return NNAB_EINVAL;  // 3xF16 reads the frames' lo rows
   if (g.row_len != g.hop || g.hop % 64) return NNAB_ENOTSUP;  // MN-major 64-column boxes of hop rows
   if (g.B == 0) return NNAB_OK;
   RGemmArgs a;

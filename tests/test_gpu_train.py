@@ -388,12 +388,14 @@ def test_kernel_grad_f16_vs_float64(cuda_dev, n_fft, hop, F, B, spread, split):
     im = torch.randn(F, ld, device=cuda_dev, generator=gen)
     c16 = [torch.empty(2 * F, ld, dtype=torch.float16, device=cuda_dev) if i == 0 or split else None for i in range(2)]
     rexp = torch.empty(2 * F + 1, dtype=torch.int32, device=cuda_dev)
-    L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), g.data_ptr(), re.data_ptr(), im.data_ptr(),
+    L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), L.PREC_3XF16, g.data_ptr(), re.data_ptr(),
+                                  im.data_ptr(),
                                   F, T, ld, 0.0, c16[0].data_ptr(), L.ptr(c16[1]), rexp.data_ptr(), st), "coef")
     dk = torch.full((2 * F, n_fft), float("nan"), device=cuda_dev)
     part = torch.empty(max(lib.nnab_rgemm_partial_bytes(2 * F, n_fft, ld, 0) // 4, 1), device=cuda_dev)
     L.check(lib.nnab_kernel_grad_f16(C.byref(f), c16[0].data_ptr(), L.ptr(c16[1]), 2 * F, ld, rexp.data_ptr(),
-                                     dk.data_ptr(), n_fft, ws.data_ptr(), ws.numel(), part.data_ptr(), 0, st), "dk")
+                                     dk.data_ptr(), n_fft, ws.data_ptr(), ws.numel(), L.PREC_3XF16, part.data_ptr(), 0, st),
+            "dk")
     torch.cuda.synchronize()
     from paper_1912_12055_b200.engine import geometry
     R = geometry(Lx, n_fft, hop, n_fft // 2, "reflect")[2]  # slot layout: clip b, frame t -> slot b * R + t

@@ -28,12 +28,14 @@ re = torch.ones(F, ld, device=dev)
 im = torch.zeros(F, ld, device=dev)
 c16 = [torch.empty(2 * F, ld, dtype=torch.float16, device=dev) for _ in range(2)]
 rexp = torch.empty(2 * F + 1, dtype=torch.int32, device=dev)
-L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), g.data_ptr(), re.data_ptr(), im.data_ptr(), F,
+L.check(lib.nnab_dft_coef_f16(C.byref(f), ws.data_ptr(), ws.numel(), L.PREC_3XF16, g.data_ptr(), re.data_ptr(),
+                              im.data_ptr(), F,
                               T, ld, 0.0, c16[0].data_ptr(), c16[1].data_ptr(), rexp.data_ptr(), st), "coef")
 dk = torch.empty(2 * F, n_fft, device=dev)
 part = torch.empty(max(lib.nnab_rgemm_partial_bytes(2 * F, n_fft, ld, 0) // 4, 1), device=dev)
 L.check(lib.nnab_kernel_grad_f16(C.byref(f), c16[0].data_ptr(), c16[1].data_ptr(), 2 * F, ld, rexp.data_ptr(),
-                                 dk.data_ptr(), n_fft, ws.data_ptr(), ws.numel(), part.data_ptr(), 0, st), "dk")
+                                 dk.data_ptr(), n_fft, ws.data_ptr(), ws.numel(), L.PREC_3XF16, part.data_ptr(), 0, st),
+        "dk")
 torch.cuda.synchronize()
 xp = Fn.pad(x.double()[:, None], (n_fft // 2, n_fft // 2), mode="reflect")[:, 0]
 fr = xp.unfold(1, n_fft, hop)[:, :T]  # (B, T, n_fft)
