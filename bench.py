@@ -202,11 +202,17 @@ MODES = {
     ("cqt2010v2", "f16"): ("f16", "f16 operands (exact per-clip power-of-two scale), f32 accumulate", None),
     ("cqt2010v2", "tf32"): ("f16", "f16 operands (exact per-clip power-of-two scale), f32 accumulate", None),
     ("cqt2010v2", "fp32"): ("fp32", "f32 (CUDA cores)", None),
-    ("train", "f16"): ("tf32", "tf32", "tf32"),
-    ("train", "tf32"): ("tf32", "tf32", "tf32"),
-    ("train", "fp32"): ("fp32", "3xtf32", "tf32"),
+    # training: the dominant GEMMs (forward, kernel gradient) run on FP16 tensor cores, so the
+    # roofline divides by the FP16 (= bf16) peak -- conservative for the TF32 reductions in the step
+    ("train", "f16"): ("tf32", "tf32-accurate: 3xf16 forward (phasor), one-pass fp16 kernel gradient (exact "
+                               "power-of-two scales), tf32 reductions, f32 accumulate", "f16"),
+    ("train", "tf32"): ("tf32", "tf32-accurate: 3xf16 forward (phasor), one-pass fp16 kernel gradient (exact "
+                                "power-of-two scales), tf32 reductions, f32 accumulate", "f16"),
+    ("train", "fp32"): ("fp32", "fp32-accurate: 3xf16 forward and kernel gradient, 3xtf32 reductions, f32 accumulate",
+                        "f16"),
     # TF32 training with the one-pass forward phasor (faster; gradient tail)
-    ("train", "tf32-onepass"): ("tf32", "tf32 (one-pass phasor)", "tf32"),
+    ("train", "tf32-onepass"): ("tf32", "f16 forward (one-pass phasor), one-pass fp16 kernel gradient, tf32 "
+                                        "reductions, f32 accumulate", "f16"),
 }
 for _m in ("f16", "tf32", "fp32", "3xtf32"):
     if ("stft", _m) in MODES:
