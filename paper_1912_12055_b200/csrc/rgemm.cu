@@ -119,6 +119,17 @@ NNAB_DEV void split_f16x4(float a, float b, float c, float d, uint2& hi, uint2& 
   lo = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
 }
 
+// 2^-clip_exp of the clips owning slots n .. n + 3 (0 past the last clip): one division
+// when R >= 4 (the four slots then span at most two clips); |clip_exp| <= 100
+NNAB_DEV void clip_scales(const RParams& p, int n, float* es) {
+  const int b0 = n / p.clip_R, r0 = n - b0 * p.clip_R;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int b = p.clip_R >= 4 ? b0 + (r0 + j >= p.clip_R ? 1 : 0) : (n + j) / p.clip_R;
+    es[j] = b < p.n_clips ? __int_as_float((127 - p.clip_exp[b]) << 23) : 0.f;
+  }
+}
+
 NNAB_DEV uint64_t kdesc(const void* p, int swz) {
   uint64_t d = (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
@@ -455,6 +466,14 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
       const int64_t k_lo = sp * p.k_per_split;
       const int64_t k_hi = (k_lo + p.k_per_split < p.K) ? k_lo + p.k_per_split : p.K;
       const int m_base = mt * kBM + (int)q * 32;
+      float rsv[8];  // coef_f16: this thread's rows' 2^row_exp (rows m_base + 4 it + sr)
+      if (p.coef_f16) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int m = m_base + it * 4 + sr;
+          rsv[it] = m < p.M ? __int_as_float((127 + p.row_exp[m]) << 23) : 0.f;
+        }
+      }
       float* cbase = p.C + sp * p.split_stride;
       for (int64_t kc = k_lo; kc < k_hi; kc += p.k_chunk) {
         const bool first_chunk = kc == k_lo;  // later chunks add into C in fixed order: deterministic
@@ -515,20 +534,14 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
               ph_cur[it] = ph_nxt[it];
             }
             float es[4] = {0.f, 0.f, 0.f, 0.f};  // coef_f16: 2^-clip_exp per column
-            if (p.coef_f16) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int64_t b = (int64_t)(n + j) / p.clip_R;
-                es[j] = b < p.n_clips ? __int_as_float((127 - p.clip_exp[b]) << 23) : 0.f;
-              }
-            }
+            if (p.coef_f16) clip_scales(p, n, es);
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
               const int m = m_base + it * 4 + sr;
               if (m >= p.M) continue;
               const int64_t o = (int64_t)m * p.ldc + n, o2 = o + (int64_t)p.M * p.ldc;
               if (p.coef_f16) {  // one-pass FP16 kernel-gradient operand: coef * 2^(row_exp - clip_exp)
-                const float rs = __int_as_float((127 + p.row_exp[m]) << 23);
+                const float rs = rsv[it];
                 const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
                 __half* ch = reinterpret_cast<__half*>(p.C);
                 float cr[4], ci[4];
@@ -590,18 +603,14 @@ __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
             }
             if (p.coef_f16) {  // FP16 hi/lo of coef * 2^(row_exp[m] - clip_exp[slot]) (3xF16 dK operand)
               float es[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int64_t b = (int64_t)(n + j) / p.clip_R;
-                es[j] = b < p.n_clips ? __int_as_float((127 - p.clip_exp[b]) << 23) : 0.f;  // |e| <= 100
-              }
+              clip_scales(p, n, es);
               __half* ch = reinterpret_cast<__half*>(p.C);
               __half* cl = reinterpret_cast<__half*>(p.c_lo);
 #pragma unroll
               for (int it = 0; it < 8; ++it) {
                 const int m = m_base + it * 4 + sr;
                 if (m >= p.M) continue;
-                const float rs = __int_as_float((127 + p.row_exp[m]) << 23);  // |row_exp| <= 125
+                const float rs = rsv[it];  // |row_exp| <= 125
                 const int64_t o = (int64_t)m * p.ldc + n, o2 = o + (int64_t)p.M * p.ldc;
                 const float dv[4] = {d[it].x, d[it].y, d[it].z, d[it].w};
                 float cr[4], ci[4];
