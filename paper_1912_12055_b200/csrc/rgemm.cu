@@ -166,10 +166,11 @@ NNAB_DEV uint64_t mndesc(const void* p, int /*swz*/, uint32_t lbo) {
 // reduction dK = coef @ frames is L2-bandwidth bound at 128 x 256 per CTA).
 // kWide (with kPair): 256 x 512 tiles -- two N=256 MMAs per K step into all
 // 512 TMEM columns (one accumulator), a quarter less L2 traffic per MAC again.
-// kE8: the coef epilogues (nnab_mel_dft_coef: TF32 phasor; 3xTF32 with FP16 output) on 8 epilogue warps
-// (384 threads, 3 stages): its HBM-latency-bound loads get twice the warps in flight.
-// kF16: the 3xF16 kernel gradient (nnab_kernel_grad_f16) -- A = coef rows scaled by
-// 2^(row_exp - clip_exp) as FP16 hi/lo, B = the 3xF16 forward's staged frames (MN-major
+// kE8: the coef epilogues (nnab_mel_dft_coef: TF32 phasor, also with FP16 output; 3xTF32 with FP16
+// output) on 8 epilogue warps (384 threads, 3 stages): their HBM-latency-bound loads get twice the
+// warps in flight.
+// kF16: the FP16 kernel gradient (nnab_kernel_grad_f16), 3xF16 with kSplit, else one FP16 pass --
+// A = coef rows scaled by 2^(row_exp - clip_exp) as FP16 (hi/lo), B = the FP16 forward's staged frames (MN-major
 // hop rows, x 2^clip_exp); the epilogue undoes 2^row_exp.
 template <bool kSplit, bool kPair, bool kWide, bool kE8 = false, bool kF16 = false>
 __global__ void __launch_bounds__(kE8 ? 384 : kThreads, 1)
