@@ -360,6 +360,9 @@ __global__ void __launch_bounds__(kThreads, 1) cqt2010_back_kernel(const __grid_
             dst[(int64_t)(b0 + bl) * dstride + z0 + (j - bl * nz)] = __float2half_rn(0.f);
           }
         }
+        // the margin pass's mbuf reads finish before any warp writes the next group's tile
+        // outputs into mbuf (the copies pass below has the same barrier)
+        if (p.copies[a + 1] <= 1) asm volatile("bar.sync 1, 128;" ::: "memory");
         if (p.copies[a + 1] > 1) {
           asm volatile("bar.sync 1, 128;" ::: "memory");
           const int h = p.h[a + 1], n8 = dstride / 8, nc = p.copies[a + 1] - 1;
