@@ -162,3 +162,24 @@ def test_wav_header_errors(tmp_path):
     with pytest.raises(fileio.CorruptFileError):
         fileio._parse_wav(str(trunc))
     assert issubclass(fileio.CorruptFileError, ValueError) and issubclass(fileio.UnsupportedFormatError, ValueError)
+
+
+def test_fp16_kernel_gradient_argument_checks():
+    """nnab_*_f16 reject bad arguments before touching a device: an unknown staging precision,
+    a missing workspace, a 3xF16 kernel gradient over a one-pass (F16) staging."""
+    from paper_1912_12055_b200 import _lib as L
+    lib = L.load()
+    f = L.nnab_frames(4, 80000, 2048, 512, 1024, L.PAD_REFLECT)
+    ld = lib.nnab_slots_ld(ctypes.byref(f))
+    fake = 1 << 20  # never dereferenced: every call below fails its checks first
+    assert lib.nnab_kernel_grad_f16(ctypes.byref(f), fake, fake, 2050, ld, fake, fake, 2048, fake, 1 << 40,
+                                    L.PREC_TF32, fake, 0, None) == L.EINVAL  # not an FP16 staging
+    assert lib.nnab_kernel_grad_f16(ctypes.byref(f), fake, fake, 2050, ld, fake, fake, 2048, None, 0,
+                                    L.PREC_3XF16, fake, 0, None) == L.EINVAL  # no workspace
+    f16_bytes = lib.nnab_stft_workspace_bytes(ctypes.byref(f), L.PREC_F16)
+    assert lib.nnab_kernel_grad_f16(ctypes.byref(f), fake, fake, 2050, ld, fake, fake, 2048, fake, f16_bytes,
+                                    L.PREC_F16, fake, 0, None) == L.EINVAL  # lo rows needed, staging has none
+    assert lib.nnab_dft_coef_f16(ctypes.byref(f), fake, 1 << 40, L.PREC_3XF16, None, fake, fake, 1025, 157, ld,
+                                 1e-12, fake, fake, fake, None) == L.EINVAL  # no upstream grad
+    assert lib.nnab_mel_dft_coef_f16(ctypes.byref(f), fake, 1 << 40, L.PREC_3XF16, 1025, ld, 128, fake, None, fake,
+                                     fake, 128, fake, fake, 1e-12, fake, fake, fake, None) == L.EINVAL  # 3xTF32 w/o wt_lo
