@@ -729,7 +729,7 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
     return !(e && e[0] == '0');
   }();
   // staging: the re | im tile, or (Mel, no slot saves) the |X| tile next to the Mel accumulator
-  p.stage_acc = kE8 && stage_env && !(mel && a.save_re);
+  p.stage_acc = kE8 && kSplit && stage_env && !(mel && a.save_re);  // one buffer (split modes) only
   const size_t mel_bytes = mel ? (size_t)kMelRows * kBM * 4 + (p.stage_acc ? (size_t)kBM * 128 * 4 + kBM * 4 : 0)
                                : p.stage_acc ? (size_t)kBM * kBN * 4 : 0;
   constexpr size_t kBudget = 227 * 1024 - 1024 - 256;  // max dynamic smem - alignment slack - barriers
@@ -776,10 +776,20 @@ int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, c
     const char* e = getenv("NNAB_STFT_E8");
     return !(e && e[0] == '0');
   }();
+  static const bool e8_f16 = [] {
+    const char* e = getenv("NNAB_STFT_E8_F16");
+    return e && e[0] == '1';
+  }();
   switch (precision) {
     case NNAB_PREC_TF32: return pair ? launch_impl<NNAB_PREC_TF32, true>(g, a, s) : launch_impl<NNAB_PREC_TF32, false>(g, a, s);
     case NNAB_PREC_3XTF32: return pair ? launch_impl<NNAB_PREC_3XTF32, true>(g, a, s) : launch_impl<NNAB_PREC_3XTF32, false>(g, a, s);
-    case NNAB_PREC_F16: return pair ? launch_impl<NNAB_PREC_F16, true>(g, a, s) : launch_impl<NNAB_PREC_F16, false>(g, a, s);
+    case NNAB_PREC_F16:
+      // the fused Mel projection on 8 epilogue warps: opt-in (NNAB_STFT_E8_F16=1), measured neutral
+      // (Mel 2.04-2.10 vs 2.09 ms, power 2 2.33-2.42 vs 2.40-2.42: the two accumulator buffers already
+      // hide the 4-warp epilogue)
+      if (pair && e8_f16 && (a.out_kind & ~NNAB_OUT_LOG) == NNAB_OUT_MEL && !a.pairs)
+        return launch_impl<NNAB_PREC_F16, true, true>(g, a, s);
+      return pair ? launch_impl<NNAB_PREC_F16, true>(g, a, s) : launch_impl<NNAB_PREC_F16, false>(g, a, s);
     case NNAB_PREC_3XF16:
       if (pair && e8 && !a.pairs)
         return launch_impl<NNAB_PREC_3XF16, true, true>(g, a, s);
