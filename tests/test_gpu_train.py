@@ -440,3 +440,34 @@ def test_trainable_nyquist_fold_exact(cuda_dev, precision, sine0):
         assert float(np.abs(got["h_im"][0].cpu().numpy()).max()) == 0.0
         layer._op.set_bank(torch.as_tensor(h_re), torch.as_tensor(h_im))
         assert layer._op.engine.fold == 1
+
+
+def test_one_pass_phasor_mode_full_length(cuda_dev):
+    """grad_phasor="tf32" (the one-pass forward, now FP16 operands, feeding the one-pass FP16 kernel
+    gradient): config-5 layer on 6 full-length clips against the float64 oracle.  The forward and the
+    mel-weight gradient meet the TF32 gates; the bank gradients carry the one-pass phasor's documented
+    near-zero-|X| tail (1.06e-2 here, the same as the TF32 one-pass), gated at 3e-2."""
+    from paper_1912_12055_b200.layers import MelSpectrogram
+    B = 6
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((B, 80000)) * 0.5).astype(np.float32)
+    m = MelSpectrogram(sr=44100, trainable_mel=True, trainable_STFT=True, precision="tf32", grad_phasor="tf32")
+    assert m._op.fwd_engine is not None and m._op.f16_dk
+    out = m(torch.from_numpy(x).to(cuda_dev))
+    g = np.random.default_rng(7).standard_normal(out.shape).astype(np.float32)
+    out.backward(torch.from_numpy(g).to(cuda_dev))
+    h_re, h_im = O.stft_bank()
+    W = O.mel_bank(44100.0, 2048, 128, formula="slaney")
+    dW, dre, dim, fwd = np.zeros_like(W), np.zeros_like(h_re), np.zeros_like(h_im), []
+    for b in range(B):
+        fr, re, im, S = O.smooth_mag_forward(x[b].astype(np.float64), h_re, h_im, 512)
+        gb = g[b].astype(np.float64)
+        dS = W.T @ gb
+        dW += gb @ S.T
+        dre += (dS * re / S) @ fr
+        dim += (dS * im / S) @ fr
+        fwd.append(W @ S)
+    assert O.peak_err(out.detach().cpu().numpy(), np.stack(fwd)) <= TOL["tf32"]
+    assert O.peak_err(m.mel_basis.grad.cpu().numpy(), dW) <= TOL_GRAD["tf32"]
+    assert O.peak_err(m.h_re.grad.cpu().numpy(), dre) <= 3e-2
+    assert O.peak_err(m.h_im.grad.cpu().numpy(), dim) <= 3e-2
