@@ -13,6 +13,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -426,22 +427,23 @@ int stage_frames_f16(const FrameGeom& g, const float* x, void* rows_hi, void* ro
   return NNAB_OK;
 }
 
-// Bank operand layout: tile n = rows [256n, 256n+256): 128 cosine rows of bins
-// 128n.. then the 128 matching sine rows; K zero-padded to k_pad.
+// Bank operand layout: tile n = rows [2hb n, 2hb (n + 1)): hb cosine rows of bins hb n.. then
+// the hb matching sine rows (hb = dft_half: 128, or the bin count rounded up to 8 for a one-tile
+// bank, whose GEMM then runs N = 2 hb); K zero-padded to k_pad.
 __global__ void pack_dft_bank_kernel(const float* __restrict__ h_re, const float* __restrict__ h_im, int32_t n_bins,
                                      int32_t n_fft, int32_t k_pad, int32_t n_tiles, int32_t fold, int32_t split,
-                                     float* __restrict__ hi, float* __restrict__ lo) {
-  const int64_t total = (int64_t)n_tiles * 256 * k_pad;
+                                     int32_t hb, float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = (int64_t)n_tiles * 2 * hb * k_pad;
   const int32_t n_body = fold ? n_bins - 1 : n_bins;  // bins held in the regular slots
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = e / k_pad;
     const int32_t k = (int32_t)(e - row * k_pad);
-    const int32_t tile = (int32_t)(row / 256), col = (int32_t)(row % 256);
-    const bool is_sin = col >= 128;
-    const int32_t bin = tile * 128 + (col & 127);
+    const int32_t tile = (int32_t)(row / (2 * hb)), col = (int32_t)(row % (2 * hb));
+    const bool is_sin = col >= hb;
+    const int32_t bin = tile * hb + (is_sin ? col - hb : col);
     float v = 0.f;
     if (k < n_fft) {
-      if (fold && tile == 0 && col == 128) {
+      if (fold && tile == 0 && col == hb) {
         v = h_re[(int64_t)(n_bins - 1) * n_fft + k];  // Nyquist cosine in bin 0's (zero) sine slot
       } else if (bin < n_body) {
         v = (is_sin ? h_im : h_re)[(int64_t)bin * n_fft + k];
@@ -468,22 +470,23 @@ __global__ void bank_absmax_kernel(const float* __restrict__ a, const float* __r
 // [2^14, 2^15)); trailer[1] = e_h for the GEMM epilogue.
 __global__ void pack_dft_bank_f16_kernel(const float* __restrict__ h_re, const float* __restrict__ h_im,
                                          int32_t n_bins, int32_t n_fft, int32_t k_pad, int32_t n_tiles, int32_t fold,
-                                         int32_t split, __half* __restrict__ hi, __half* __restrict__ lo,
-                                         int32_t* __restrict__ trailer) {
+                                         int32_t split, int32_t hb, __half* __restrict__ hi,
+                                         __half* __restrict__ lo, int32_t* __restrict__ trailer) {
   const int e = f16_scale_exp(__uint_as_float(static_cast<unsigned int>(trailer[0])));
   const float sc = ldexpf(1.f, e);
   if (blockIdx.x == 0 && threadIdx.x == 0) trailer[1] = e;
-  const int64_t total = (int64_t)n_tiles * 256 * k_pad;
+  const int64_t total = (int64_t)n_tiles * 2 * hb * k_pad;
   const int32_t n_body = fold ? n_bins - 1 : n_bins;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / k_pad;
     const int32_t k = (int32_t)(i - row * k_pad);
-    const int32_t tile = (int32_t)(row / 256), col = (int32_t)(row % 256);
-    const int32_t bin = tile * 128 + (col & 127);
+    const int32_t tile = (int32_t)(row / (2 * hb)), col = (int32_t)(row % (2 * hb));
+    const bool is_sin = col >= hb;
+    const int32_t bin = tile * hb + (is_sin ? col - hb : col);
     float v = 0.f;
     if (k < n_fft) {
-      if (fold && tile == 0 && col == 128) v = h_re[(int64_t)(n_bins - 1) * n_fft + k];
-      else if (bin < n_body) v = (col >= 128 ? h_im : h_re)[(int64_t)bin * n_fft + k];
+      if (fold && tile == 0 && col == hb) v = h_re[(int64_t)(n_bins - 1) * n_fft + k];
+      else if (bin < n_body) v = (is_sin ? h_im : h_re)[(int64_t)bin * n_fft + k];
     }
     v *= sc;
     const __half h = __float2half_rn(v);
@@ -503,6 +506,16 @@ int launch_bank_absmax(const float* a, const float* b, int64_t n, unsigned int* 
 
 using namespace nnab;
 
+// cosine (= sine) rows per DFT-layout tile: 128, or for a one-tile bank of <= 120 bins (not
+// folded) the bin count rounded up to 8 -- its GEMMs then run N = 2 hb instead of 256
+int nnab::dft_half(int32_t n_bins, int32_t fold_nyquist) {
+  static const bool narrow = [] {
+    const char* e = getenv("NNAB_DFT_NARROW");
+    return !(e && e[0] == '0');
+  }();
+  return (narrow && !fold_nyquist && n_bins >= 1 && n_bins <= 120) ? (n_bins + 7) / 8 * 8 : 128;
+}
+
 extern "C" int nnab_dft_bank_tiles(int32_t n_bins, int32_t fold_nyquist) {
   if (n_bins < 1) return 0;
   const int body = fold_nyquist ? n_bins - 1 : n_bins;
@@ -511,13 +524,14 @@ extern "C" int nnab_dft_bank_tiles(int32_t n_bins, int32_t fold_nyquist) {
 
 extern "C" size_t nnab_dft_bank_bytes(int32_t n_bins, int32_t n_fft, int32_t fold_nyquist) {
   const int64_t k_pad = (n_fft + 31) / 32 * 32;
-  return (size_t)nnab_dft_bank_tiles(n_bins, fold_nyquist) * 256 * k_pad * sizeof(float);
+  return (size_t)nnab_dft_bank_tiles(n_bins, fold_nyquist) * 2 * dft_half(n_bins, fold_nyquist) * k_pad *
+         sizeof(float);
 }
 
 extern "C" size_t nnab_dft_bank_bytes_prec(int32_t n_bins, int32_t n_fft, int32_t fold_nyquist, int32_t precision) {
   if (!prec_is_f16(precision)) return nnab_dft_bank_bytes(n_bins, n_fft, fold_nyquist);
   const int64_t k_pad = (n_fft + 63) / 64 * 64;
-  const size_t data = (size_t)nnab_dft_bank_tiles(n_bins, fold_nyquist) * 256 * k_pad * 2;
+  const size_t data = (size_t)nnab_dft_bank_tiles(n_bins, fold_nyquist) * 2 * dft_half(n_bins, fold_nyquist) * k_pad * 2;
   return ((data + 255) & ~size_t(255)) + 256;  // + trailer: [0] peak bits, [1] scale exponent
 }
 
@@ -533,7 +547,8 @@ extern "C" int nnab_pack_dft_bank(const float* h_re, const float* h_im, int32_t 
   cudaStream_t s = (cudaStream_t)stream;
   if (prec_is_f16(precision)) {
     const int32_t k_pad = (n_fft + 63) / 64 * 64;
-    const int64_t total = (int64_t)tiles * 256 * k_pad;
+    const int32_t hb = dft_half(n_bins, fold_nyquist);
+    const int64_t total = (int64_t)tiles * 2 * hb * k_pad;
     int32_t* trailer = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(packed_hi) +
                                                   nnab_dft_bank_bytes_prec(n_bins, n_fft, fold_nyquist, precision) -
                                                   256);
@@ -543,15 +558,16 @@ extern "C" int nnab_pack_dft_bank(const float* h_re, const float* h_im, int32_t 
         h_re, h_im, n, reinterpret_cast<unsigned int*>(trailer));
     NNAB_LAUNCHED();
     pack_dft_bank_f16_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, s>>>(
-        h_re, h_im, n_bins, n_fft, k_pad, tiles, fold_nyquist, split, reinterpret_cast<__half*>(packed_hi),
+        h_re, h_im, n_bins, n_fft, k_pad, tiles, fold_nyquist, split, hb, reinterpret_cast<__half*>(packed_hi),
         reinterpret_cast<__half*>(packed_lo), trailer);
     NNAB_LAUNCHED();
     return NNAB_OK;
   }
   const int32_t k_pad = (n_fft + 31) / 32 * 32;
-  const int64_t total = (int64_t)tiles * 256 * k_pad;
+  const int32_t hb = dft_half(n_bins, fold_nyquist);
+  const int64_t total = (int64_t)tiles * 2 * hb * k_pad;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
-  pack_dft_bank_kernel<<<blocks, 256, 0, s>>>(h_re, h_im, n_bins, n_fft, k_pad, tiles, fold_nyquist, split,
+  pack_dft_bank_kernel<<<blocks, 256, 0, s>>>(h_re, h_im, n_bins, n_fft, k_pad, tiles, fold_nyquist, split, hb,
                                               packed_hi, packed_lo);
   NNAB_LAUNCHED();
   return NNAB_OK;

@@ -93,6 +93,8 @@ struct StftGemmArgs {
 int staged_views(const nnab_frames* f, int32_t precision, const void* workspace, size_t workspace_bytes,
                  FrameGeom* g, const void** hi, const void** lo, const int32_t** exps);
 int launch_stft_gemm(const FrameGeom& g, const StftGemmArgs& a, int precision, cudaStream_t s);
+// cosine (= sine) rows per DFT-layout bank tile (frames.cu): 128, or fewer for a one-tile bank
+int dft_half(int32_t n_bins, int32_t fold_nyquist);
 
 // Reduction GEMM C[M][N] = sum_k A[M][K] B(K, N)  (rgemm.cu)
 struct RGemmArgs {

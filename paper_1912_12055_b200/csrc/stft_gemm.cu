@@ -82,6 +82,7 @@ struct Params {
   // longest-first so the first MMA (N = max) initialises every used column.
   const uint32_t* kb_tab;
   int32_t n_tab, b_box, pairs, out_bins;
+  int32_t half;  // DFT-layout tiles: cosine (= sine) rows per tile (dft_half)
   float log_eps;  // >= 0: outputs are log(value + log_eps) (NNAB_OUT_LOG)
   int32_t stages;  // smem pipeline depth (4, or 3 when the Mel accumulator takes 64 KB)
   // FP16 modes: epilogue scale 2^-(a_exp[clip] + *b_exp) undoes the operand scales (null: 1)
@@ -209,7 +210,9 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
             const uint32_t e = p.kb_tab ? __ldg(p.kb_tab + n * p.n_tab + it) : 0u;
             const int kb = p.kb_tab ? (int)(e >> 16) : it;
             // pair: the peer stages bank rows [N/2, N) of this K block's MMA width N
-            const int b_row = n * kBN + (kPair && rank ? (p.kb_tab ? (int)(e & 0xffffu) / 2 : kBN / 2) : 0);
+            const int tile_rows = (p.pairs || p.kb_tab) ? kBN : 2 * p.half;  // DFT layout: 2 hb rows per tile
+            const int b_row = n * tile_rows +
+                              (kPair && rank ? (p.kb_tab ? (int)(e & 0xffffu) / 2 : tile_rows / 2) : 0);
             mbar_wait(&empty[s], ph ^ 1);
             uint8_t* st = smem + s * C::STAGE_BYTES;
             const int k = kb * C::BK;
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (rank == 0 && elect_one()) {
       constexpr uint32_t kM = kPair ? 2 * kBM : kBM;
-      constexpr uint32_t idesc_full = C::idesc(kM, kBN);
+      const uint32_t idesc_full = C::idesc(kM, (p.pairs || p.kb_tab) ? kBN : 2 * p.half);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -292,6 +295,9 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
     // keeps the 4-warp order: deterministic, and no second accumulator)
     const int CSTEP = (kE8 && !mel) ? 2 : 1;
     const int c_first = (kE8 && !mel) ? hsel : 0;
+    // DFT-layout tiles: hb cosine columns then hb sine columns (hb = 128, or the bin count
+    // rounded up to 8 for a one-tile bank of <= 120 bins), nch 32-column chunks of each
+    const int hb = p.half, nch = (p.half + 31) / 32;
     const uint32_t row = q * 32 + lane;
     const int kind = p.out_kind;
     const int F = p.n_bins;
@@ -340,12 +346,12 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
           const int sw = (int)(row & 7);
           asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)q) : "memory");  // the pair is done reading the staging
 #pragma unroll 1
-          for (int c = hsel; c < 4; c += 2) {
+          for (int c = hsel; c < nch; c += 2) {
             float re[32], im[32], cre[32], cim[32];
             tmem_ld32(tb + c * 32, re);
-            tmem_ld32(tb + 128 + c * 32, im);
+            tmem_ld32(tb + hb + c * 32, im);
             tmem_ld32(tb + kBN + c * 32, cre);
-            tmem_ld32(tb + kBN + 128 + c * 32, cim);
+            tmem_ld32(tb + kBN + hb + c * 32, cim);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -368,14 +374,14 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
           asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)q) : "memory");  // both halves staged
           if (p.fold && n == 0) nyq_val = nyq_stage[row];
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < nch; ++c) {
             float m32[32];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 v4 = mrow[(c * 8 + j) ^ sw];
               m32[4 * j] = v4.x, m32[4 * j + 1] = v4.y, m32[4 * j + 2] = v4.z, m32[4 * j + 3] = v4.w;
             }
-            const int bin0 = n * 128 + c * 32;
+            const int bin0 = n * hb + c * 32;
             const int ch = bin0 >> 5;
             const int lo = p.mel_band ? p.mel_band[2 * ch] : 0;
             const int hi = p.mel_band ? p.mel_band[2 * ch + 1] : p.n_mels;
@@ -467,12 +473,12 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
         const int sw = (int)(row & 7);
         if (kE8 && p.stage_acc) {
 #pragma unroll 1
-          for (int c = c_first; c < 4; c += CSTEP) {
+          for (int c = c_first; c < nch; c += CSTEP) {
             float re[32], im[32], cre[32], cim[32];
             tmem_ld32(tb + c * 32, re);
-            tmem_ld32(tb + 128 + c * 32, im);
+            tmem_ld32(tb + hb + c * 32, im);
             tmem_ld32(tb + kBN + c * 32, cre);
-            tmem_ld32(tb + kBN + 128 + c * 32, cim);
+            tmem_ld32(tb + kBN + hb + c * 32, cim);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
           release_acc(acc);
         }
 #pragma unroll 1
-        for (int c = c_first; c < 4; c += CSTEP) {
+        for (int c = c_first; c < nch; c += CSTEP) {
           float re[32], im[32];
           if (kE8 && p.stage_acc) {
 #pragma unroll
@@ -498,11 +504,11 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
             }
           } else {
           tmem_ld32(tb + c * 32, re);
-          tmem_ld32(tb + 128 + c * 32, im);
+          tmem_ld32(tb + hb + c * 32, im);
           if (kSplit) {
             float cre[32], cim[32];
             tmem_ld32(tb + kBN + c * 32, cre);
-            tmem_ld32(tb + kBN + 128 + c * 32, cim);
+            tmem_ld32(tb + kBN + hb + c * 32, cim);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(kE8 ? kThreads + 128 : kThreads, 1)
             }
           }
           }  // TMEM read
-          const int bin0 = n * 128 + c * 32;
+          const int bin0 = n * hb + c * 32;
           float nyq_re = 0.f;
           if (p.fold && n == 0 && c == 0) {
             nyq_re = im[0];  // cosine row of bin F-1 sits in bin 0's sine slot
@@ -672,8 +678,10 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   if (C::kHalf && (!a.a_exp || !a.b_exp)) return NNAB_EINVAL;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   const uint64_t rows_total = (uint64_t)g.B * g.R;
-  const uint64_t bank_rows = (uint64_t)a.n_tiles * kBN;
-  const int b_box = a.b_box > 0 ? a.b_box : kBN;
+  // DFT-layout banks: tiles of 2 hb rows (hb = dft_half: 128, or fewer for a one-tile bank)
+  const int hb = (a.pairs || a.kb_tab) ? 128 : dft_half(a.n_bins, a.fold);
+  const uint64_t bank_rows = (uint64_t)a.n_tiles * ((a.pairs || a.kb_tab) ? kBN : 2 * hb);
+  const int b_box = a.b_box > 0 ? a.b_box : 2 * hb;
   if (b_box % 16 != 0 || b_box > kBN) return NNAB_EINVAL;
   const int b_rows = kPair ? b_box / 2 : b_box;  // each CTA of a pair stages half the bank rows
   constexpr int E = C::ELEM;
@@ -718,6 +726,7 @@ int launch_impl(const FrameGeom& g, const StftGemmArgs& a, cudaStream_t s) {
   if (a.save_re && !a.save_im && kSplit && !a.save_phasor) return NNAB_EINVAL;  // 3x modes save re / im
   p.n_tab = a.n_tab;
   p.b_box = b_box;
+  p.half = hb;
   p.pairs = a.pairs;
   p.out_bins = a.out_bins > 0 ? a.out_bins : a.n_bins;
   if (a.kb_tab && (a.n_tab < 1 || mel)) return NNAB_EINVAL;
